@@ -1,0 +1,71 @@
+"""Pin the CPU oracle against outputs of the real reference (tests/golden, made by
+oracle/gen_golden.py).  Tree/lists must be bit-exact; operators and solutions match
+to rounding (the restatement reproduces the reference's arithmetic order)."""
+import numpy as np
+import pytest
+
+from conftest import golden_kernel, load_golden
+from oracle import ifmm_oracle as O
+
+CASES = ["c1_invr", "log_2k", "exact_512", "reglog_1k", "d4_invr"]
+
+
+def _setup(name):
+    g = load_golden(name)
+    N, depth = int(g["N"]), int(g["depth"])
+    pts = O.baseline_points(N, seed=0)
+    return g, pts, O.build_tree(pts, depth), golden_kernel(g)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_tree_lists_bit_exact(name):
+    g, pts, T, _ = _setup(name)
+    assert np.array_equal(T.perm, g["perm"])
+    assert np.array_equal(T.leaf_off, g["leaf_off"])
+    for k in range(1, int(g["depth"]) + 1):
+        for i in range(T.n_clusters(k)):
+            nb = g[f"nbr{k}"][i]
+            il = g[f"il{k}"][i]
+            assert T.nbr[k][i] == list(nb[nb >= 0])
+            assert T.ilist[k][i] == list(il[il >= 0])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_init_and_matvec(name):
+    g, pts, T, spec = _setup(name)
+    st = O.init_operators(T, spec, int(g["p"]), float(g["tol"]))
+    for k in range(2, int(g["depth"]) + 1):
+        assert np.array_equal([st.r(k, i) for i in range(T.n_clusters(k))], g[f"rank0_{k}"])
+    mv = O.fmm_matvec(st, g["xm"])
+    assert np.linalg.norm(mv - g["mv"]) <= 1e-13 * np.linalg.norm(g["mv"])
+
+
+@pytest.mark.parametrize("name", ["c1_invr", "log_2k", "exact_512", "reglog_1k"])
+@pytest.mark.parametrize("order", ["morton", "colour9"])
+def test_factor_solve_matches_reference(name, order):
+    g, pts, T, spec = _setup(name)
+    st = O.init_operators(T, spec, int(g["p"]), float(g["tol"]))
+    fac = O.factorize(st, order=order)
+    x = O.solve(fac, g["b"])
+    ref = g[f"x_{order}"]
+    assert np.linalg.norm(x - ref) <= 1e-11 * np.linalg.norm(ref)
+    assert fac.r_m == int(g[f"rm_{order}"])
+    assert int(fac.top_off[-1]) == int(g[f"top_{order}"])
+
+
+def test_exact_mode_matches_dense_lu():
+    g, pts, T, spec = _setup("exact_512")
+    st = O.init_operators(T, spec, int(g["p"]), 0.0)
+    x = O.solve(O.factorize(st, order="colour9"), g["phi"])
+    assert np.linalg.norm(x - g["x_dense"]) <= 1e-11 * np.linalg.norm(g["x_dense"])
+
+
+def test_nrhs_solve_equals_columnwise():
+    g, pts, T, spec = _setup("log_2k")
+    st = O.init_operators(T, spec, int(g["p"]), float(g["tol"]))
+    fac = O.factorize(st, order="colour9")
+    B = np.stack([g["b"], g["xm"]], axis=1)
+    X = O.solve(fac, B)
+    for c, v in enumerate((g["b"], g["xm"])):
+        ref = O.solve(fac, v)
+        assert np.linalg.norm(X[:, c] - ref) <= 1e-13 * np.linalg.norm(ref)
