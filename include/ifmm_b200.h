@@ -1,0 +1,127 @@
+/*
+ * ifmm_b200.h -- C ABI of the B200-native IFMM factorize/solve library
+ * (libifmm_b200.so, sm_100a).  Plain pointers and sizes only.
+ *
+ * The reference (`/root/reference/pkg/src/ifmm`, Python) has no FFI of its own:
+ * its boundary is the Python module API.  Each entry point below replaces one
+ * reference call (file:line cited); the Python mirror `paper_1407_1572_b200`
+ * binds them with ctypes and keeps the reference's names,
+ * argument meaning and exceptions.
+ *
+ * Conventions
+ *   - every function returns an IFMM_* status; on failure ifmm_last_error()
+ *     holds a message (thread-local).  IFMM_SINGULAR_PIVOT additionally sets
+ *     ifmm_last_singular(level, index, cond)   (SingularPivotError,
+ *     ifmm/solver.py:53-60, raised at :214-218).
+ *   - point arrays are (n, dim) row-major doubles; right-hand sides and
+ *     solutions are (n, nrhs) row-major doubles, in ORIGINAL point order.
+ *   - ptr_kind = IFMM_PTR_HOST (pageable/pinned host memory; the library does
+ *     the host<->device copies) or IFMM_PTR_DEVICE (CUDA device pointers).
+ *   - there is no CPU fallback: without a CUDA device every compute entry
+ *     point returns IFMM_NO_DEVICE.
+ */
+#ifndef IFMM_B200_H
+#define IFMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  IFMM_OK = 0,
+  IFMM_INVALID = 1,        /* ValueError */
+  IFMM_SINGULAR_PIVOT = 2, /* SingularPivotError */
+  IFMM_CUDA = 3,           /* RuntimeError */
+  IFMM_OOM = 4,            /* MemoryError */
+  IFMM_NO_DEVICE = 5       /* RuntimeError: no CUDA device, no fallback */
+};
+
+enum { IFMM_PTR_HOST = 0, IFMM_PTR_DEVICE = 1 };
+
+/* kernel ids: the reference registry ifmm/kernels.py:160-170 plus the two
+ * BASELINE kernels inv_r = scale/r and log_r = scale*(ln r + shift) */
+enum {
+  IFMM_K_LOG = 0, IFMM_K_LAPLACE3D = 1, IFMM_K_BIHARMONIC = 2, IFMM_K_BESSEL_Y0 = 3,
+  IFMM_K_INVERSE_QUADRIC = 4, IFMM_K_INVERSE_MULTIQUADRIC = 5, IFMM_K_HELMHOLTZ3D = 6,
+  IFMM_K_GAUSSIAN = 7, IFMM_K_MULTIQUADRIC = 8, IFMM_K_INV_R = 9, IFMM_K_LOG_R = 10
+};
+
+typedef struct ifmm_tree ifmm_tree;
+typedef struct ifmm_store ifmm_store;
+typedef struct ifmm_factor ifmm_factor;
+
+const char* ifmm_last_error(void);
+int ifmm_last_singular(int* level, int* index, double* cond);
+int ifmm_version(void);
+int ifmm_device_count(void);
+
+/* ---- tree: PointSet checks + build_tree + compute_lists
+ *      (ifmm/geometry.py:47-61, :174-226, :229-262) */
+int ifmm_tree_build(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out);
+int ifmm_tree_info(const ifmm_tree* t, int64_t* n, int* dim, int* depth);
+/* permuted position -> original index (ClusterTree.point_permutation) */
+int ifmm_tree_permutation(const ifmm_tree* t, int64_t* perm);
+/* leaf point ranges: 2^(dim*depth)+1 offsets into the permuted points */
+int ifmm_tree_leaf_offsets(const ifmm_tree* t, int64_t* off);
+/* neighbour / interaction lists of `level` as CSR; call with null arrays to
+ * get sizes[0] = #nbr entries, sizes[1] = #il entries */
+int ifmm_tree_lists(const ifmm_tree* t, int level, int32_t* nbr_off, int32_t* nbr, int32_t* il_off, int32_t* il,
+                    int64_t* sizes);
+/* elimination colour of every cluster of `level` (sum_d (g_d mod 3) 3^d) */
+int ifmm_tree_colours(const ifmm_tree* t, int level, int32_t* colours);
+void ifmm_tree_free(ifmm_tree* t);
+
+/* ---- operators: init_operators(tree, kernel, p, tol) (ifmm/operators.py:164-274)
+ * probe_table: (probe_maxm+1) x 10 ACA probe rows (row m = the seeded draw of
+ * ifmm/lowrank.py:196-197 for an m-row fill). */
+int ifmm_store_init(ifmm_tree* t, int kernel_id, double a, double scale, double shift, int p, double tol,
+                    const int32_t* probe_table, int probe_maxm, ifmm_store** out);
+int ifmm_store_max_init_rank(const ifmm_store* s, int* r);
+/* particle dims and initial ranks of every cluster of `level` (>= 2) */
+int ifmm_store_dims(const ifmm_store* s, int level, int32_t* n, int32_t* r);
+/* basis U (n x r, column-major) of cluster `index` (OperatorStore.l2p) */
+int ifmm_store_basis(const ifmm_store* s, int level, int index, double* out);
+/* M2L block (r_i x r_j, column-major) of interaction-list pair (i, j) */
+int ifmm_store_m2l(const ifmm_store* s, int level, int i, int j, double* out);
+/* fmm_matvec (ifmm/operators.py:282-330): y = A~ x, x/y (n, nrhs) */
+int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr_kind);
+void ifmm_store_free(ifmm_store* s);
+
+/* ---- factorize(store, tree, tol) (ifmm/solver.py:106-153); tol < 0 -> store tol.
+ * The store's initial operators are left intact (matvec stays valid). */
+int ifmm_factorize(ifmm_store* s, double tol, int flags, ifmm_factor** out);
+/* r_m, top-level dimension, number of eliminations, factorization wall ms */
+int ifmm_factor_info(const ifmm_factor* f, int* r_m, int* top_dim, int64_t* n_records, double* ms);
+/* LevelStats of `level`: clusters, max_rank, fillins_compressed, fillins_dense_kept */
+int ifmm_factor_level_stats(const ifmm_factor* f, int level, int32_t* out4);
+/* per elimination (in order): level, index, n, r, w */
+int ifmm_factor_records(const ifmm_factor* f, int32_t* out5);
+/* work accounting: out[0] executed FP64 flops (GJ inverses, X = S^-1 C,
+ * symmetric Schur update, top inverse), out[1] of which in the Schur update,
+ * out[2] reference-equivalent flops (sum 2/3 m^3 + 2 m^2 w + 2 h n w
+ * + 2/3 M_top^3), out[3] bytes one solve sweep streams per right-hand side */
+int ifmm_factor_work(const ifmm_factor* f, double* out4);
+/* solve(fact, rhs) (ifmm/solver.py:549-626) for nrhs >= 1 columns */
+int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int ptr_kind);
+void ifmm_factor_free(ifmm_factor* f);
+
+/* ---- test hooks for the batched kernels (host arrays in/out) */
+/* in-place inverse of `count` column-major matrices of sizes m[c], packed */
+int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info);
+/* C = alpha op(A) op(B) + beta C, column-major, one problem */
+int ifmm_test_gemm(int transA, int transB, int M, int N, int K, double alpha, const double* A, int lda,
+                   const double* B, int ldb, double beta, double* C, int ldc, int transC);
+/* one-sided Jacobi: A (m x n) -> orthogonal columns, V (n x n), sig (n) */
+int ifmm_test_jacobi(double* a, int m, int n, double* v, double* sig);
+/* Householder QR: A (m x k) -> Q (m x k), R (k x k) */
+int ifmm_test_qr(const double* a, int m, int k, double* q, double* r);
+/* ACA + recompression of F (m x n): returns rank, left (m x rank), right (n x rank) */
+int ifmm_test_aca(const double* f, int m, int n, double tol, const int32_t* probes, int kmax, double* left,
+                  double* right, int32_t* rank, int32_t* incompressible);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

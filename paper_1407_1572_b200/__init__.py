@@ -1,0 +1,39 @@
+"""B200-native IFMM factorize/solve (drop-in for the reference `ifmm` hot path).
+
+Same public names as the reference package (ifmm/__init__.py:73-104) for the
+factorize/solve path; every numerical step runs in hand-written sm_100a CUDA
+(libifmm_b200.so, include/ifmm_b200.h).  There is no CPU fallback.
+"""
+from ._lib import SingularPivotError
+from .estimator import IfmmSolver, default_depth
+from .geometry import ClusterTree, Cluster, PointSet, build_tree, compute_lists, morton_decode, morton_encode
+from .kernels import KERNEL_NAMES, Kernel, baseline_kernel, kernel_block, make_kernel
+from .operators import OperatorStore, fmm_matvec, init_operators
+from .solver import IfmmFactorization, LevelStats, factorize, solve
+
+__all__ = [
+    "Cluster",
+    "ClusterTree",
+    "IfmmFactorization",
+    "IfmmSolver",
+    "KERNEL_NAMES",
+    "Kernel",
+    "LevelStats",
+    "OperatorStore",
+    "PointSet",
+    "SingularPivotError",
+    "baseline_kernel",
+    "build_tree",
+    "compute_lists",
+    "default_depth",
+    "factorize",
+    "fmm_matvec",
+    "init_operators",
+    "kernel_block",
+    "make_kernel",
+    "morton_decode",
+    "morton_encode",
+    "solve",
+]
+
+__version__ = "0.1.0"

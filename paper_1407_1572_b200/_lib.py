@@ -1,0 +1,155 @@
+"""ctypes binding of libifmm_b200.so (include/ifmm_b200.h).
+
+There is no fallback: if the shared library is missing this module raises at
+import, and compute entry points raise RuntimeError when no CUDA device is
+present.  Status codes map onto the reference's exception types
+(ValueError, SingularPivotError, RuntimeError, MemoryError).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libifmm_b200.so")
+
+OK, INVALID, SINGULAR, CUDA, OOM, NO_DEVICE = range(6)
+PTR_HOST, PTR_DEVICE = 0, 1
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build the CUDA library first "
+        "(python -c 'import __graft_entry__ as g; g.build()' or make -C paper_1407_1572_b200)")
+
+lib = ctypes.CDLL(LIB_PATH)
+
+_c = ctypes
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int
+_d = ctypes.c_double
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+_pd = ctypes.POINTER(ctypes.c_double)
+
+# name -> (restype, argtypes); every symbol declared in include/ifmm_b200.h
+SIGNATURES = {
+    "ifmm_last_error": (ctypes.c_char_p, []),
+    "ifmm_last_singular": (_i32, [_pi32, _pi32, _pd]),
+    "ifmm_version": (_i32, []),
+    "ifmm_device_count": (_i32, []),
+    "ifmm_tree_build": (_i32, [_p, _i64, _i32, _i32, _i32, ctypes.POINTER(_p)]),
+    "ifmm_tree_info": (_i32, [_p, _pi64, _pi32, _pi32]),
+    "ifmm_tree_permutation": (_i32, [_p, _p]),
+    "ifmm_tree_leaf_offsets": (_i32, [_p, _p]),
+    "ifmm_tree_lists": (_i32, [_p, _i32, _p, _p, _p, _p, _p]),
+    "ifmm_tree_colours": (_i32, [_p, _i32, _p]),
+    "ifmm_tree_free": (None, [_p]),
+    "ifmm_store_init": (_i32, [_p, _i32, _d, _d, _d, _i32, _d, _p, _i32, ctypes.POINTER(_p)]),
+    "ifmm_store_max_init_rank": (_i32, [_p, _pi32]),
+    "ifmm_store_dims": (_i32, [_p, _i32, _p, _p]),
+    "ifmm_store_basis": (_i32, [_p, _i32, _i32, _p]),
+    "ifmm_store_m2l": (_i32, [_p, _i32, _i32, _i32, _p]),
+    "ifmm_matvec": (_i32, [_p, _p, _p, _i64, _i32]),
+    "ifmm_store_free": (None, [_p]),
+    "ifmm_factorize": (_i32, [_p, _d, _i32, ctypes.POINTER(_p)]),
+    "ifmm_factor_info": (_i32, [_p, _pi32, _pi32, _pi64, _pd]),
+    "ifmm_factor_level_stats": (_i32, [_p, _i32, _p]),
+    "ifmm_factor_records": (_i32, [_p, _p]),
+    "ifmm_factor_work": (_i32, [_p, _p]),
+    "ifmm_solve": (_i32, [_p, _p, _p, _i64, _i32]),
+    "ifmm_factor_free": (None, [_p]),
+    "ifmm_test_gj_inverse": (_i32, [_p, _p, _i32, _p]),
+    "ifmm_test_gemm": (_i32, [_i32, _i32, _i32, _i32, _i32, _d, _p, _i32, _p, _i32, _d, _p, _i32, _i32]),
+    "ifmm_test_jacobi": (_i32, [_p, _i32, _i32, _p, _p]),
+    "ifmm_test_qr": (_i32, [_p, _i32, _i32, _p, _p]),
+    "ifmm_test_aca": (_i32, [_p, _i32, _i32, _d, _p, _i32, _p, _p, _p, _p]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class SingularPivotError(RuntimeError):
+    """Numerically singular pivot block (ifmm/solver.py:53-60)."""
+
+    def __init__(self, level: int, index: int, cond: float):
+        super().__init__(
+            f"pivot for cluster {index} at level {level} is numerically "
+            f"singular (condition estimate {cond:.2e})")
+        self.level = level
+        self.index = index
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    msg = lib.ifmm_last_error().decode(errors="replace")
+    if status == INVALID:
+        raise ValueError(msg)
+    if status == SINGULAR:
+        lv, ix, cd = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+        lib.ifmm_last_singular(ctypes.byref(lv), ctypes.byref(ix), ctypes.byref(cd))
+        raise SingularPivotError(lv.value, ix.value, cd.value)
+    if status == OOM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def as_input(x, rows: int):
+    """Normalise a (rows,) / (rows, k) numpy array or CUDA torch tensor.
+
+    Returns (pointer, ptr_kind, nrhs, keepalive, is_torch, was_1d)."""
+    if type(x).__module__.startswith("torch"):
+        import torch  # only when the caller already uses torch
+        t = x.detach()
+        if t.dim() not in (1, 2) or t.shape[0] != rows:
+            raise ValueError(f"expected shape ({rows},) or ({rows}, k), got {tuple(t.shape)}")
+        t = t.to(torch.float64).contiguous()
+        nr = 1 if t.dim() == 1 else int(t.shape[1])
+        kind = PTR_DEVICE if t.is_cuda else PTR_HOST
+        if kind == PTR_HOST:
+            a = t.numpy()
+            return ptr(a), PTR_HOST, nr, a, True, t.dim() == 1
+        return ctypes.c_void_p(t.data_ptr()), PTR_DEVICE, nr, t, True, t.dim() == 1
+    a = np.ascontiguousarray(np.asarray(x, dtype=float))
+    if a.ndim not in (1, 2) or a.shape[0] != rows:
+        raise ValueError(f"expected shape ({rows},) or ({rows}, k), got {a.shape}")
+    nr = 1 if a.ndim == 1 else a.shape[1]
+    return ptr(a), PTR_HOST, nr, a, False, a.ndim == 1
+
+
+def alloc_output(like, kind: int, rows: int, nrhs: int, one_d: bool):
+    """Output buffer matching an input normalised by as_input."""
+    if kind == PTR_DEVICE:
+        import torch
+        out = torch.empty((rows, nrhs), dtype=torch.float64, device=like.device)
+        return out, ctypes.c_void_p(out.data_ptr())
+    out = np.empty((rows, nrhs))
+    return out, ptr(out)
+
+
+def aca_probe_table(maxm: int = 4096) -> np.ndarray:
+    """Probe rows of the reference's ACA for every fill height m <= maxm:
+    numpy's default_rng(0).choice(m, size=min(10, m), replace=False), exactly
+    as ifmm/lowrank.py:196-197 draws them."""
+    global _PROBES
+    if _PROBES is not None and _PROBES.shape[0] > maxm:
+        return _PROBES
+    tab = np.zeros((maxm + 1, 10), dtype=np.int32)
+    for m in range(1, maxm + 1):
+        d = np.random.default_rng(0).choice(m, size=min(10, m), replace=False)
+        tab[m, :len(d)] = d
+    _PROBES = tab
+    return tab
+
+
+_PROBES = None

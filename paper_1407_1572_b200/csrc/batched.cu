@@ -1,0 +1,256 @@
+// Batched block copies, grouped DGEMM launch, 1-norms and the blocked
+// Gauss-Jordan inverse (Quintana-Orti et al. GJE formulation: an m x b panel is
+// transformed in shared memory, the rest of the matrix is updated with six
+// rank-b DMMA GEMMs per panel, row swaps are undone as column swaps at the end).
+#include <algorithm>
+
+#include "batched.cuh"
+
+namespace ifmm {
+
+// ------------------------------------------------------------------ copies
+__global__ void __launch_bounds__(256) copy_kernel(const CopyDesc* __restrict__ desc) {
+  __shared__ double tile[32][33];
+  const CopyDesc D = desc[blockIdx.x];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (!D.trans || D.src == nullptr) {
+    for (int j = ty; j < D.cols; j += 8) {
+      double* dcol = D.dst + (size_t)j * D.ldd;
+      const double* scol = D.src ? D.src + (size_t)j * D.lds : nullptr;
+      for (int i = tx; i < D.rows; i += 32) {
+        double v = scol ? D.alpha * scol[i] : 0.0;
+        if (D.accumulate) dcol[i] += v; else dcol[i] = v;
+      }
+    }
+    return;
+  }
+  // transposed: dst(i,j) = src(j,i); go through 32x32 smem tiles
+  for (int j0 = 0; j0 < D.cols; j0 += 32)
+    for (int i0 = 0; i0 < D.rows; i0 += 32) {
+      // src(j,i): column i of src, rows j -> coalesced along j
+      for (int r = ty; r < 32; r += 8) {
+        int i = i0 + r, j = j0 + tx;
+        tile[r][tx] = (i < D.rows && j < D.cols) ? D.src[j + (size_t)i * D.lds] : 0.0;
+      }
+      __syncthreads();
+      for (int r = ty; r < 32; r += 8) {
+        int j = j0 + r, i = i0 + tx;
+        if (i < D.rows && j < D.cols) {
+          double v = D.alpha * tile[tx][r];
+          double* d = D.dst + i + (size_t)j * D.ldd;
+          if (D.accumulate) *d += v; else *d = v;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+void launch_copies(CopyBatch& b, Arena& ws, Staging& st, cudaStream_t s) {
+  if (b.d.empty()) return;
+  const CopyDesc* dd = upload(ws, b.d, s, st);
+  size_t n = b.d.size();
+  for (size_t off = 0; off < n; off += 2147483647u) {
+    unsigned g = unsigned(std::min<size_t>(n - off, 2147483647u));
+    copy_kernel<<<g, 256, 0, s>>>(dd + off);
+    CK_LAUNCH();
+  }
+  b.clear();
+}
+
+// ------------------------------------------------------------------ gemm launch
+void launch_grouped_gemm(GemmBatch& b, bool transA, bool transB, Arena& ws, Staging& st, cudaStream_t s) {
+  if (b.probs.empty()) return;
+  const GemmProb* dp = upload(ws, b.probs, s, st);
+  int np = int(b.probs.size());
+  if (!transA && !transB) grouped_dgemm_kernel<false, false><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+  else if (transA && !transB) grouped_dgemm_kernel<true, false><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+  else if (!transA && transB) grouped_dgemm_kernel<false, true><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+  else grouped_dgemm_kernel<true, true><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+  CK_LAUNCH();
+  b.clear();
+}
+
+// ------------------------------------------------------------------ norms
+__global__ void __launch_bounds__(256) norm1_kernel(const MatDesc* __restrict__ desc, double* out) {
+  __shared__ double red[32];
+  const MatDesc D = desc[blockIdx.x];
+  double best = 0.0;
+  for (int c = threadIdx.x >> 5; c < D.m; c += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int r = threadIdx.x & 31; r < D.m; r += 32) s += fabs(D.A[r + (size_t)c * D.lda]);
+    s = warp_sum(s);
+    best = fmax(best, s);
+  }
+  // block max via the sum helper on a max-reduce: reuse smem manually
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) b = fmax(b, red[w]);
+    // NaN propagates as non-finite norm
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++)
+      if (red[w] != red[w]) b = red[w];
+    out[blockIdx.x] = b;
+  }
+}
+
+void launch_norm1(const MatDesc* d_desc, int n, double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  norm1_kernel<<<n, 256, 0, s>>>(d_desc, out);
+  CK_LAUNCH();
+}
+
+// ------------------------------------------------------------------ Gauss-Jordan
+// Panel transform: columns [j, j+b) of every matrix with m > j.
+__global__ void __launch_bounds__(512) gj_panel_kernel(const MatDesc* __restrict__ desc, int j, int b,
+                                                       int* info) {
+  extern __shared__ double sm[];
+  __shared__ ArgMax red[32];
+  const MatDesc D = desc[blockIdx.x];
+  const int m = D.m;
+  if (m <= j) return;
+  const int bb = min(b, m - j);
+  const int ld = bb + 1;  // odd row stride: conflict-free per-row access
+  double* P = sm;         // P[r*ld + c] = A(r, j+c)
+  for (int c = 0; c < bb; c++)
+    for (int r = threadIdx.x; r < m; r += blockDim.x) P[r * ld + c] = D.A[r + (size_t)(j + c) * D.lda];
+  __syncthreads();
+  __shared__ int s_piv;
+  __shared__ double s_inv;
+  for (int c = 0; c < bb; c++) {
+    const int jc = j + c;
+    ArgMax am{-1.0, -1};
+    for (int r = jc + threadIdx.x; r < m; r += blockDim.x) am = argmax_merge(am, ArgMax{fabs(P[r * ld + c]), r});
+    am = block_argmax(am, red);
+    if (threadIdx.x == 0) {
+      int p = am.i < 0 ? jc : am.i;
+      s_piv = p;
+      D.ipiv[jc] = p;
+      double pv = P[p * ld + c];
+      if (pv == 0.0 || pv != pv) {
+        if (info[blockIdx.x] == 0) info[blockIdx.x] = jc + 1;
+        s_inv = 0.0;
+      } else {
+        s_inv = 1.0 / pv;
+      }
+    }
+    __syncthreads();
+    const int p = s_piv;
+    if (p != jc)
+      for (int cc = threadIdx.x; cc < bb; cc += blockDim.x) {
+        double t = P[p * ld + cc];
+        P[p * ld + cc] = P[jc * ld + cc];
+        P[jc * ld + cc] = t;
+      }
+    __syncthreads();
+    const double inv = s_inv;
+    for (int cc = threadIdx.x; cc < bb; cc += blockDim.x) P[jc * ld + cc] = (cc == c) ? inv : P[jc * ld + cc] * inv;
+    __syncthreads();
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      if (r == jc) continue;
+      double* row = P + r * ld;
+      const double* prow = P + jc * ld;
+      const double f = row[c];
+      if (f != 0.0) {
+        for (int cc = 0; cc < bb; cc++)
+          if (cc != c) row[cc] -= f * prow[cc];
+      }
+      row[c] = -f * inv;
+    }
+    __syncthreads();
+  }
+  for (int c = 0; c < bb; c++)
+    for (int r = threadIdx.x; r < m; r += blockDim.x) D.A[r + (size_t)(j + c) * D.lda] = P[r * ld + c];
+}
+
+// Apply the panel's row interchanges to every column outside the panel.
+__global__ void __launch_bounds__(256) gj_rowswap_kernel(const MatDesc* __restrict__ desc, int j, int b) {
+  const MatDesc D = desc[blockIdx.x];
+  if (D.m <= j) return;
+  const int bb = min(b, D.m - j);
+  for (int col = threadIdx.x + blockIdx.y * blockDim.x; col < D.m; col += blockDim.x * gridDim.y) {
+    if (col >= j && col < j + bb) continue;
+    double* a = D.A + (size_t)col * D.lda;
+    for (int t = 0; t < bb; t++) {
+      int p = D.ipiv[j + t];
+      if (p != j + t) {
+        double x = a[j + t];
+        a[j + t] = a[p];
+        a[p] = x;
+      }
+    }
+  }
+}
+
+// Undo the row pivoting of the factorised matrix: inv(A) = inv(PA) P, i.e.
+// column swaps in reverse order.
+__global__ void __launch_bounds__(256) gj_colswap_kernel(const MatDesc* __restrict__ desc) {
+  const MatDesc D = desc[blockIdx.x];
+  for (int r = threadIdx.x + blockIdx.y * blockDim.x; r < D.m; r += blockDim.x * gridDim.y) {
+    for (int c = D.m - 1; c >= 0; c--) {
+      int p = D.ipiv[c];
+      if (p != c) {
+        double x = D.A[r + (size_t)c * D.lda];
+        D.A[r + (size_t)c * D.lda] = D.A[r + (size_t)p * D.lda];
+        D.A[r + (size_t)p * D.lda] = x;
+      }
+    }
+  }
+}
+
+void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
+                        Staging& st, cudaStream_t s) {
+  const int n = int(h.size());
+  if (n == 0) return;
+  int maxm = 0;
+  for (auto& d : h) maxm = std::max(maxm, d.m);
+  int b = 32;
+  while (b > 4 && size_t(maxm) * (b + 1) * 8 > 200 * 1024) b /= 2;
+  if (size_t(maxm) * (b + 1) * 8 > 220 * 1024) invalid("pivot block too large for the Gauss-Jordan panel");
+  size_t smem = size_t(maxm) * (b + 1) * 8;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  CK(cudaMemsetAsync(d_info, 0, sizeof(int) * n, s));
+  // scratch for the pivot-row block W (b x m per matrix)
+  std::vector<double*> W(n);
+  for (int p = 0; p < n; p++) W[p] = ws.alloc_n<double>(size_t(b) * h[p].m);
+  CopyBatch cb;
+  GemmBatch gb;
+  const int threads = maxm >= 256 ? 512 : 256;
+  for (int j = 0; j < maxm; j += b) {
+    gj_panel_kernel<<<n, threads, smem, s>>>(d_desc, j, b, d_info);
+    CK_LAUNCH();
+    gj_rowswap_kernel<<<dim3(n, std::max(1, std::min(8, maxm / 256 + 1))), 256, 0, s>>>(d_desc, j, b);
+    CK_LAUNCH();
+    for (int p = 0; p < n; p++) {
+      const MatDesc& D = h[p];
+      if (D.m <= j) continue;
+      const int bb = std::min(b, D.m - j), m = D.m, r2 = j + bb, n2 = m - r2;
+      double* A = D.A;
+      const int ld = D.lda;
+      cb.add(A + j, ld, W[p], bb, bb, m);  // W = A[R1, :]
+      const double* pan = A + (size_t)j * ld;  // A[:, J]
+      const double* W0 = W[p];
+      const double* W2 = W[p] + (size_t)r2 * bb;
+      // rows R0
+      gb.add(pan, ld, W0, bb, A, ld, j, j, bb, 1.0, 1.0);
+      gb.add(pan, ld, W2, bb, A + (size_t)r2 * ld, ld, j, n2, bb, 1.0, 1.0);
+      // rows R2
+      gb.add(pan + r2, ld, W0, bb, A + r2, ld, n2, j, bb, 1.0, 1.0);
+      gb.add(pan + r2, ld, W2, bb, A + r2 + (size_t)r2 * ld, ld, n2, n2, bb, 1.0, 1.0);
+      // rows R1 (overwrite): A11_inv * W
+      gb.add(pan + j, ld, W0, bb, A + j, ld, bb, j, bb, 1.0, 0.0);
+      gb.add(pan + j, ld, W2, bb, A + j + (size_t)r2 * ld, ld, bb, n2, bb, 1.0, 0.0);
+    }
+    launch_copies(cb, ws, st, s);
+    launch_grouped_gemm(gb, false, false, ws, st, s);
+  }
+  gj_colswap_kernel<<<dim3(n, std::max(1, std::min(8, maxm / 256 + 1))), 256, 0, s>>>(d_desc);
+  CK_LAUNCH();
+}
+
+}  // namespace ifmm

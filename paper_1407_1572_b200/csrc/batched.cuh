@@ -1,0 +1,53 @@
+// Batched block utilities (copy / transpose / scale-accumulate / zero, 1-norms)
+// and the batched Gauss-Jordan inversion with partial pivoting used for the
+// IFMM pivot blocks S_i = [[P2P_ii, U_i], [U_i^T, 0]].
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace ifmm {
+
+// dst(i,j) = [accumulate ? dst(i,j) : 0] + alpha * (trans ? src(j,i) : src(i,j))
+// src == nullptr writes zeros (or leaves dst unchanged if accumulate).
+struct CopyDesc {
+  const double* src;
+  double* dst;
+  int rows, cols;
+  int lds, ldd;
+  int trans;
+  int accumulate;
+  double alpha;
+};
+
+struct CopyBatch {
+  std::vector<CopyDesc> d;
+  void add(const double* src, int lds, double* dst, int ldd, int rows, int cols, bool trans = false,
+           double alpha = 1.0, bool accumulate = false) {
+    if (rows <= 0 || cols <= 0) return;
+    d.push_back(CopyDesc{src, dst, rows, cols, lds, ldd, trans ? 1 : 0, accumulate ? 1 : 0, alpha});
+  }
+  void zero(double* dst, int ldd, int rows, int cols) { add(nullptr, 0, dst, ldd, rows, cols); }
+  void clear() { d.clear(); }
+};
+void launch_copies(CopyBatch& b, Arena& ws, Staging& st, cudaStream_t s);
+
+// Matrix descriptor for batched dense kernels (column-major).
+struct MatDesc {
+  double* A;
+  int m;
+  int lda;
+  int* ipiv;  // length m (GJ)
+  int tag;    // caller-defined (pivot id)
+};
+
+// 1-norm (max column abs sum) of every matrix -> out[p]
+void launch_norm1(const MatDesc* d_desc, int n, double* out, cudaStream_t s);
+
+// In-place inversion of every matrix by blocked Gauss-Jordan elimination with
+// partial pivoting.  `info[p]` = 0, or 1 + first column with an exact zero
+// pivot.  Host-side descriptors `h` (same content as d_desc) drive the GEMM
+// trailing updates.
+void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
+                        Staging& st, cudaStream_t s);
+
+}  // namespace ifmm

@@ -1,0 +1,396 @@
+// C ABI (include/ifmm_b200.h): exception -> status translation, handle
+// management, accessors and test hooks for the batched kernels.
+#include <cstring>
+#include <string>
+
+#include "../../include/ifmm_b200.h"
+#include "core.cuh"
+#include "cta_la.cuh"
+
+using ifmm::AcaOut;
+using ifmm::Arena;
+using ifmm::CtaShared;
+using ifmm::Error;
+using ifmm::FactorH;
+using ifmm::GemmBatch;
+using ifmm::InitLevel;
+using ifmm::KernelParams;
+using ifmm::LevelStatsH;
+using ifmm::MatDesc;
+using ifmm::RecordH;
+using ifmm::SingularPivot;
+using ifmm::Staging;
+using ifmm::StoreH;
+using ifmm::Topo;
+using ifmm::TreeH;
+using ifmm::invalid;
+using ifmm::ensure_device;
+using ifmm::default_stream;
+using ifmm::upload;
+
+struct ifmm_tree { TreeH* h; };
+struct ifmm_store { StoreH* h; };
+struct ifmm_factor { FactorH* h; };
+
+namespace ifmm {
+void matvec_release(StoreH* S);
+}
+
+static thread_local std::string g_err;
+static thread_local int g_sing_level = -1, g_sing_index = -1;
+static thread_local double g_sing_cond = 0.0;
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return IFMM_OK;
+  } catch (const SingularPivot& e) {
+    g_err = e.what();
+    g_sing_level = e.level;
+    g_sing_index = e.index;
+    g_sing_cond = e.cond;
+    return IFMM_SINGULAR_PIVOT;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return IFMM_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return IFMM_CUDA;
+  }
+}
+
+extern "C" {
+
+const char* ifmm_last_error(void) { return g_err.c_str(); }
+
+int ifmm_last_singular(int* level, int* index, double* cond) {
+  if (level) *level = g_sing_level;
+  if (index) *index = g_sing_index;
+  if (cond) *cond = g_sing_cond;
+  return IFMM_OK;
+}
+
+int ifmm_version(void) { return 1; }
+
+int ifmm_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------- tree
+int ifmm_tree_build(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out) {
+  return guard([&] {
+    if (!out) invalid("null output handle");
+    TreeH* h = ifmm::tree_build(points, n, dim, depth, ptr_kind == IFMM_PTR_DEVICE);
+    *out = new ifmm_tree{h};
+  });
+}
+
+int ifmm_tree_info(const ifmm_tree* t, int64_t* n, int* dim, int* depth) {
+  return guard([&] {
+    if (!t) invalid("null tree");
+    if (n) *n = t->h->N;
+    if (dim) *dim = t->h->dim;
+    if (depth) *depth = t->h->depth;
+  });
+}
+
+int ifmm_tree_permutation(const ifmm_tree* t, int64_t* perm) {
+  return guard([&] { memcpy(perm, t->h->perm.data(), sizeof(int64_t) * t->h->perm.size()); });
+}
+
+int ifmm_tree_leaf_offsets(const ifmm_tree* t, int64_t* off) {
+  return guard([&] { memcpy(off, t->h->leaf_off.data(), sizeof(int64_t) * t->h->leaf_off.size()); });
+}
+
+int ifmm_tree_lists(const ifmm_tree* t, int level, int32_t* nbr_off, int32_t* nbr, int32_t* il_off, int32_t* il,
+                    int64_t* sizes) {
+  return guard([&] {
+    if (level < 1 || level > t->h->depth) invalid("level out of range");
+    const Topo& T = t->h->lv[level];
+    if (sizes) {
+      sizes[0] = int64_t(T.nbr.size());
+      sizes[1] = int64_t(T.il.size());
+    }
+    if (nbr_off) memcpy(nbr_off, T.nbr_off.data(), sizeof(int) * T.nbr_off.size());
+    if (nbr) memcpy(nbr, T.nbr.data(), sizeof(int) * T.nbr.size());
+    if (il_off) memcpy(il_off, T.il_off.data(), sizeof(int) * T.il_off.size());
+    if (il) memcpy(il, T.il.data(), sizeof(int) * T.il.size());
+  });
+}
+
+int ifmm_tree_colours(const ifmm_tree* t, int level, int32_t* colours) {
+  return guard([&] {
+    if (level < 1 || level > t->h->depth) invalid("level out of range");
+    const Topo& T = t->h->lv[level];
+    memcpy(colours, T.colour.data(), sizeof(int) * T.colour.size());
+  });
+}
+
+void ifmm_tree_free(ifmm_tree* t) {
+  if (!t) return;
+  delete t->h;
+  delete t;
+}
+
+// ---------------------------------------------------------------- store
+int ifmm_store_init(ifmm_tree* t, int kernel_id, double a, double scale, double shift, int p, double tol,
+                    const int32_t* probe_table, int probe_maxm, ifmm_store** out) {
+  return guard([&] {
+    if (!t || !out) invalid("null handle");
+    if (!probe_table || probe_maxm < 1) invalid("ACA probe table required");
+    KernelParams kp{kernel_id, a, scale, shift};
+    StoreH* h = ifmm::store_init(t->h, kp, p, tol, probe_table, probe_maxm);
+    *out = new ifmm_store{h};
+  });
+}
+
+int ifmm_store_max_init_rank(const ifmm_store* s, int* r) {
+  return guard([&] { *r = s->h->max_init_rank; });
+}
+
+int ifmm_store_dims(const ifmm_store* s, int level, int32_t* n, int32_t* r) {
+  return guard([&] {
+    if (level < 2 || level > s->h->tree->depth) invalid("level out of range");
+    const InitLevel& L = s->h->lv[level];
+    if (n) memcpy(n, L.n.data(), sizeof(int) * L.nc);
+    if (r) memcpy(r, L.r0.data(), sizeof(int) * L.nc);
+  });
+}
+
+int ifmm_store_basis(const ifmm_store* s, int level, int index, double* out) {
+  return guard([&] {
+    if (level < 2 || level > s->h->tree->depth) invalid("level out of range");
+    const InitLevel& L = s->h->lv[level];
+    if (index < 0 || index >= L.nc) invalid("index out of range");
+    CK(cudaMemcpy(out, L.U[index], sizeof(double) * L.n[index] * L.r0[index], cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_store_m2l(const ifmm_store* s, int level, int i, int j, double* out) {
+  return guard([&] {
+    if (level < 2 || level > s->h->tree->depth) invalid("level out of range");
+    const InitLevel& L = s->h->lv[level];
+    const Topo& T = s->h->tree->lv[level];
+    for (int q = T.il_off[i]; q < T.il_off[i + 1]; q++)
+      if (T.il[q] == j) {
+        CK(cudaMemcpy(out, L.m2l[q], sizeof(double) * L.r0[i] * L.r0[j], cudaMemcpyDeviceToHost));
+        return;
+      }
+    invalid("(i, j) is not an interaction-list pair");
+  });
+}
+
+int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr_kind) {
+  return guard([&] { ifmm::matvec(s->h, x, y, nrhs, ptr_kind == IFMM_PTR_DEVICE); });
+}
+
+void ifmm_store_free(ifmm_store* s) {
+  if (!s) return;
+  matvec_release(s->h);
+  delete s->h;
+  delete s;
+}
+
+// ---------------------------------------------------------------- factor / solve
+int ifmm_factorize(ifmm_store* s, double tol, int flags, ifmm_factor** out) {
+  return guard([&] {
+    if (!s || !out) invalid("null handle");
+    FactorH* h = ifmm::factorize(s->h, tol, flags);
+    *out = new ifmm_factor{h};
+  });
+}
+
+int ifmm_factor_info(const ifmm_factor* f, int* r_m, int* top_dim, int64_t* n_records, double* ms) {
+  return guard([&] {
+    if (r_m) *r_m = f->h->r_m;
+    if (top_dim) *top_dim = f->h->top_dim;
+    if (n_records) *n_records = int64_t(f->h->recs.size());
+    if (ms) *ms = f->h->ms_total;
+  });
+}
+
+int ifmm_factor_level_stats(const ifmm_factor* f, int level, int32_t* out4) {
+  return guard([&] {
+    if (level < 2 || level >= int(f->h->stats.size())) invalid("level out of range");
+    const LevelStatsH& s = f->h->stats[level];
+    out4[0] = s.clusters;
+    out4[1] = s.max_rank;
+    out4[2] = s.compressed;
+    out4[3] = s.dense_kept;
+  });
+}
+
+int ifmm_factor_records(const ifmm_factor* f, int32_t* out5) {
+  return guard([&] {
+    size_t u = 0;
+    for (const RecordH& r : f->h->recs) {
+      out5[u++] = r.level;
+      out5[u++] = r.index;
+      out5[u++] = r.n;
+      out5[u++] = r.r;
+      out5[u++] = r.w;
+    }
+  });
+}
+
+int ifmm_factor_work(const ifmm_factor* f, double* out4) {
+  return guard([&] {
+    out4[0] = f->h->fl_exec;
+    out4[1] = f->h->fl_schur;
+    out4[2] = f->h->fl_ref;
+    out4[3] = f->h->solve_bytes;
+  });
+}
+
+int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int ptr_kind) {
+  return guard([&] { ifmm::solve(f->h, rhs, x, nrhs, ptr_kind == IFMM_PTR_DEVICE); });
+}
+
+void ifmm_factor_free(ifmm_factor* f) {
+  if (!f) return;
+  delete f->h;
+  delete f;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- test hooks
+__global__ void test_jacobi_kernel(double* a, int m, int n, double* v, double* sig, int* ord) {
+  __shared__ CtaShared sh;
+  ifmm::cta_jacobi(a, m, n, m, v, n, sig, ord, sh);
+}
+
+__global__ void test_qr_kernel(double* a, int m, int k, double* q, double* r, double* vv) {
+  __shared__ CtaShared sh;
+  ifmm::cta_qr(a, m, k, m, r, q, m, vv, sh);
+}
+
+__global__ void test_aca_kernel(const double* f, int m, int n, double tol, const int* probes, int kmax, double* uc,
+                                double* vc, double* scratch, int* out) {
+  __shared__ CtaShared sh;
+  double* rr = scratch;
+  double* cc = rr + n;
+  double* dots = cc + m;
+  int* usedr = reinterpret_cast<int*>(dots + kmax);
+  int* usedc = usedr + m;
+  AcaOut o = ifmm::cta_aca(f, m, 0, m, n, tol, probes, min(10, m), uc, vc, kmax, rr, cc, usedr, usedc, dots, sh);
+  if (threadIdx.x == 0) {
+    out[0] = o.k;
+    out[1] = o.converged;
+  }
+}
+
+extern "C" {
+
+int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t s = default_stream();
+    Arena ws(size_t(64) << 20);
+    Staging st;
+    std::vector<MatDesc> md(count);
+    size_t tot = 0;
+    for (int c = 0; c < count; c++) tot += size_t(m[c]) * m[c];
+    double* d = ws.alloc_n<double>(tot);
+    CK(cudaMemcpy(d, a, sizeof(double) * tot, cudaMemcpyHostToDevice));
+    size_t off = 0;
+    for (int c = 0; c < count; c++) {
+      md[c] = MatDesc{d + off, m[c], m[c], ws.alloc_n<int>(m[c]), c};
+      off += size_t(m[c]) * m[c];
+    }
+    const MatDesc* dmd = upload(ws, md, s, st);
+    int* dinfo = ws.alloc_n<int>(count);
+    ifmm::batched_gj_inverse(md, dmd, dinfo, ws, st, s);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(a, d, sizeof(double) * tot, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(info, dinfo, sizeof(int) * count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_test_gemm(int transA, int transB, int M, int N, int K, double alpha, const double* A, int lda,
+                   const double* B, int ldb, double beta, double* C, int ldc, int transC) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t s = default_stream();
+    Arena ws(size_t(64) << 20);
+    Staging st;
+    size_t na = size_t(lda) * (transA ? M : K), nb = size_t(ldb) * (transB ? K : N),
+           nc = size_t(ldc) * (transC ? M : N);
+    double *dA = ws.alloc_n<double>(na), *dB = ws.alloc_n<double>(nb), *dC = ws.alloc_n<double>(nc);
+    CK(cudaMemcpy(dA, A, sizeof(double) * na, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B, sizeof(double) * nb, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dC, C, sizeof(double) * nc, cudaMemcpyHostToDevice));
+    GemmBatch gb;
+    gb.add(dA, lda, dB, ldb, dC, ldc, M, N, K, alpha, beta, transC != 0);
+    ifmm::launch_grouped_gemm(gb, transA != 0, transB != 0, ws, st, s);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(C, dC, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_test_jacobi(double* a, int m, int n, double* v, double* sig) {
+  return guard([&] {
+    ensure_device();
+    Arena ws(size_t(16) << 20);
+    double *da = ws.alloc_n<double>(size_t(m) * n), *dv = ws.alloc_n<double>(size_t(n) * n),
+           *ds = ws.alloc_n<double>(n);
+    int* dord = ws.alloc_n<int>(n);
+    CK(cudaMemcpy(da, a, sizeof(double) * m * n, cudaMemcpyHostToDevice));
+    test_jacobi_kernel<<<1, 256>>>(da, m, n, dv, ds, dord);
+    CK_LAUNCH();
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(a, da, sizeof(double) * m * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(v, dv, sizeof(double) * n * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sig, ds, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_test_qr(const double* a, int m, int k, double* q, double* r) {
+  return guard([&] {
+    ensure_device();
+    Arena ws(size_t(16) << 20);
+    double *da = ws.alloc_n<double>(size_t(m) * k), *dq = ws.alloc_n<double>(size_t(m) * k),
+           *dr = ws.alloc_n<double>(size_t(k) * k), *dvv = ws.alloc_n<double>(k);
+    CK(cudaMemcpy(da, a, sizeof(double) * m * k, cudaMemcpyHostToDevice));
+    test_qr_kernel<<<1, 256>>>(da, m, k, dq, dr, dvv);
+    CK_LAUNCH();
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(q, dq, sizeof(double) * m * k, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r, dr, sizeof(double) * k * k, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_test_aca(const double* f, int m, int n, double tol, const int32_t* probes, int kmax, double* left,
+                  double* right, int32_t* rank, int32_t* incompressible) {
+  return guard([&] {
+    ensure_device();
+    Arena ws(size_t(16) << 20);
+    double* df = ws.alloc_n<double>(size_t(m) * n);
+    double *du = ws.alloc_n<double>(size_t(m) * kmax), *dv = ws.alloc_n<double>(size_t(n) * kmax);
+    double* scr = ws.alloc_n<double>(size_t(2) * (m + n) + kmax + 16);
+    int* dp = ws.alloc_n<int>(10);
+    int* dout = ws.alloc_n<int>(2);
+    CK(cudaMemcpy(df, f, sizeof(double) * m * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dp, probes, sizeof(int) * std::min(10, m), cudaMemcpyHostToDevice));
+    test_aca_kernel<<<1, 256>>>(df, m, n, tol, dp, kmax, du, dv, scr, dout);
+    CK_LAUNCH();
+    CK(cudaDeviceSynchronize());
+    int o[2];
+    CK(cudaMemcpy(o, dout, 8, cudaMemcpyDeviceToHost));
+    *rank = o[0];
+    *incompressible = (!o[1] && (o[0] >= std::min(m, n) || o[0] >= kmax) && tol > 0) ? 1 : 0;
+    CK(cudaMemcpy(left, du, sizeof(double) * m * o[0], cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(right, dv, sizeof(double) * n * o[0], cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

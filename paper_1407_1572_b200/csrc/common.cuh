@@ -1,0 +1,258 @@
+// Common infrastructure for the B200 IFMM library: error handling, device
+// arenas, launch helpers and warp/block reductions.  sm_100a only.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ifmm {
+
+// ---------------------------------------------------------------- errors
+enum Status : int {
+  IFMM_OK = 0,
+  IFMM_INVALID = 1,         // -> ValueError
+  IFMM_SINGULAR_PIVOT = 2,  // -> SingularPivotError(level, index, cond)
+  IFMM_CUDA = 3,            // -> RuntimeError
+  IFMM_OOM = 4,             // -> MemoryError
+  IFMM_NO_DEVICE = 5,       // -> RuntimeError (no CUDA device: no CPU fallback)
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct SingularPivot : Error {
+  int level, index;
+  double cond;
+  SingularPivot(int lv, int ix, double c, const std::string& m)
+      : Error(IFMM_SINGULAR_PIVOT, m), level(lv), index(ix), cond(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), what, file, line,
+             cudaGetErrorString(e));
+    throw Error(e == cudaErrorMemoryAllocation ? IFMM_OOM : IFMM_CUDA, buf);
+  }
+}
+#define CK(x) ::ifmm::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::ifmm::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+[[noreturn]] inline void invalid(const std::string& m) { throw Error(IFMM_INVALID, m); }
+
+// ---------------------------------------------------------------- arena
+// Bump allocator over large cudaMalloc slabs.  Reset releases everything at
+// once (per level / per batch workspaces); slabs are kept for reuse.
+class Arena {
+ public:
+  explicit Arena(size_t slab = size_t(256) << 20) : slab_(slab) {}
+  ~Arena() { release(); }
+  Arena(const Arena&) = delete;
+  Arena& operator=(const Arena&) = delete;
+
+  void* alloc(size_t bytes, size_t align = 256) {
+    if (bytes == 0) bytes = align;
+    for (;;) {
+      if (cur_ < slabs_.size()) {
+        Slab& s = slabs_[cur_];
+        size_t off = (s.used + align - 1) / align * align;
+        if (off + bytes <= s.size) {
+          s.used = off + bytes;
+          in_use_ += bytes;
+          return static_cast<char*>(s.ptr) + off;
+        }
+        ++cur_;
+        continue;
+      }
+      size_t sz = bytes > slab_ ? bytes : slab_;
+      void* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, sz);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        char buf[256];
+        snprintf(buf, sizeof buf, "device allocation of %.3f GB failed (arena holds %.3f GB)", sz / 1e9,
+                 reserved() / 1e9);
+        throw Error(IFMM_OOM, buf);
+      }
+      if (zero_stream_) {
+        e = cudaMemsetAsync(p, 0, sz, zero_stream_);
+        if (e != cudaSuccess) throw Error(IFMM_CUDA, "cudaMemsetAsync failed on arena slab");
+      }
+      slabs_.push_back({p, sz, 0});
+      cur_ = slabs_.size() - 1;
+    }
+  }
+  // When set, new slabs and the used part of recycled slabs are zeroed on `s`,
+  // so every allocation starts as zeros (stream-ordered).
+  void set_zero_stream(cudaStream_t s) { zero_stream_ = s; zero_ = true; }
+  template <class T>
+  T* alloc_n(size_t n) {
+    return static_cast<T*>(alloc(n * sizeof(T)));
+  }
+  void reset() {
+    for (auto& s : slabs_) {
+      if (zero_ && s.used) {
+        cudaError_t e = cudaMemsetAsync(s.ptr, 0, s.used, zero_stream_);
+        if (e != cudaSuccess) throw Error(IFMM_CUDA, "cudaMemsetAsync failed on arena reset");
+      }
+      s.used = 0;
+    }
+    cur_ = 0;
+    in_use_ = 0;
+  }
+  void release() {
+    for (auto& s : slabs_) cudaFree(s.ptr);
+    slabs_.clear();
+    cur_ = 0;
+    in_use_ = 0;
+  }
+  size_t reserved() const {
+    size_t t = 0;
+    for (auto& s : slabs_) t += s.size;
+    return t;
+  }
+  size_t in_use() const { return in_use_; }
+
+ private:
+  struct Slab {
+    void* ptr;
+    size_t size;
+    size_t used;
+  };
+  std::vector<Slab> slabs_;
+  size_t cur_ = 0;
+  size_t slab_;
+  size_t in_use_ = 0;
+  cudaStream_t zero_stream_ = nullptr;
+  bool zero_ = false;
+};
+
+// Host-pinned staging area for descriptor uploads.  Bump-allocated; reset()
+// only after the stream has been synchronised (the copies read from it).
+class Staging {
+ public:
+  ~Staging() {
+    for (auto& c : chunks_) cudaFreeHost(c.ptr);
+  }
+  void* get(size_t bytes) {
+    bytes = (bytes + 255) / 256 * 256;
+    for (;;) {
+      if (cur_ < chunks_.size()) {
+        Chunk& c = chunks_[cur_];
+        if (c.used + bytes <= c.size) {
+          void* p = static_cast<char*>(c.ptr) + c.used;
+          c.used += bytes;
+          return p;
+        }
+        ++cur_;
+        continue;
+      }
+      size_t sz = bytes > (size_t(64) << 20) ? bytes : (size_t(64) << 20);
+      void* p = nullptr;
+      CK(cudaMallocHost(&p, sz));
+      chunks_.push_back({p, sz, 0});
+      cur_ = chunks_.size() - 1;
+    }
+  }
+  void reset() {
+    for (auto& c : chunks_) c.used = 0;
+    cur_ = 0;
+  }
+
+ private:
+  struct Chunk {
+    void* ptr;
+    size_t size;
+    size_t used;
+  };
+  std::vector<Chunk> chunks_;
+  size_t cur_ = 0;
+};
+
+// Upload a host vector into the arena, async on `s` through pinned staging.
+template <class T>
+T* upload(Arena& a, const std::vector<T>& v, cudaStream_t s, Staging& st) {
+  T* d = a.alloc_n<T>(v.size() ? v.size() : 1);
+  if (!v.empty()) {
+    void* h = st.get(v.size() * sizeof(T));
+    memcpy(h, v.data(), v.size() * sizeof(T));
+    CK(cudaMemcpyAsync(d, h, v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  return d;
+}
+
+inline int ceil_div(long long a, long long b) { return int((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum; `red` must hold >= 32 doubles of shared memory.
+__device__ inline double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < nw ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// Block-wide argmax of |v| with the smallest index winning ties (numpy/LAPACK
+// idamax convention).  Entries with idx < 0 are ignored.  Returns index (or -1)
+// and writes the signed value at that index to *val.
+struct ArgMax {
+  double a;  // |value|, -1 for none
+  int i;
+};
+__device__ __forceinline__ ArgMax argmax_merge(ArgMax x, ArgMax y) {
+  if (y.a > x.a || (y.a == x.a && y.i >= 0 && (x.i < 0 || y.i < x.i))) return y;
+  return x;
+}
+__device__ inline ArgMax block_argmax(ArgMax v, ArgMax* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax w;
+    w.a = __shfl_xor_sync(0xffffffffu, v.a, o);
+    w.i = __shfl_xor_sync(0xffffffffu, v.i, o);
+    v = argmax_merge(v, w);
+  }
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    ArgMax t = lane < nw ? red[lane] : ArgMax{-1.0, -1};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax w;
+      w.a = __shfl_xor_sync(0xffffffffu, t.a, o);
+      w.i = __shfl_xor_sync(0xffffffffu, t.i, o);
+      t = argmax_merge(t, w);
+    }
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  ArgMax r = red[0];
+  __syncthreads();
+  return r;
+}
+
+}  // namespace ifmm

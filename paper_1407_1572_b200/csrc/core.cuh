@@ -1,0 +1,130 @@
+// Host-side handles of the B200 IFMM: tree, initial operator store,
+// factorization.  Device memory is owned by per-handle arenas.
+#pragma once
+#include <memory>
+
+#include "batched.cuh"
+#include "common.cuh"
+#include "kfun.cuh"
+
+namespace ifmm {
+
+constexpr int WIN1 = 7;  // relative grid offsets -3..3 per axis cover nbr + IL + fills
+
+struct Topo {
+  int k = 0, nc = 0, dim = 2;
+  std::vector<int> grid;             // nc*dim
+  std::vector<int> nbr_off, nbr;     // CSR, sorted, self included (ifmm/geometry.py:229-244)
+  std::vector<int> il_off, il;       // CSR, sorted (ifmm/geometry.py:245-262)
+  std::vector<int> colour;           // sum_d (g_d mod 3) 3^d
+  int win() const { int w = 1; for (int d = 0; d < dim; d++) w *= WIN1; return w; }
+  // window slot of j relative to i, or -1 if farther than 3 cells on an axis
+  int slot(int i, int j) const {
+    int s = 0, mul = 1;
+    for (int d = 0; d < dim; d++) {
+      int dd = grid[j * dim + d] - grid[i * dim + d];
+      if (dd < -3 || dd > 3) return -1;
+      s += (dd + 3) * mul;
+      mul *= WIN1;
+    }
+    return s;
+  }
+  bool in_il(int i, int j) const {
+    for (int t = il_off[i]; t < il_off[i + 1]; t++)
+      if (il[t] == j) return true;
+    return false;
+  }
+};
+
+struct TreeH {
+  int N = 0, dim = 2, depth = 0;
+  std::vector<Topo> lv;               // index k = 1..depth (0 unused)
+  std::vector<int64_t> perm;          // permuted position -> original index
+  std::vector<int64_t> leaf_off;      // 4^depth + 1
+  double* d_pts = nullptr;            // Morton-permuted, N x dim row-major
+  int64_t* d_perm = nullptr;
+  int64_t* d_leaf_off = nullptr;
+  Arena arena{size_t(64) << 20};
+  int nclusters(int k) const { return 1 << (dim * k); }
+  int64_t range_lo(int k, int i) const { return leaf_off[size_t(i) << (dim * (depth - k))]; }
+  int64_t range_hi(int k, int i) const { return leaf_off[size_t(i + 1) << (dim * (depth - k))]; }
+};
+
+// Initial (un-eliminated) operators, compact: exactly the reference's
+// OperatorStore after init_operators (ifmm/operators.py:164-274).
+struct InitLevel {
+  int k = 0, nc = 0;
+  std::vector<int> n, r0;              // particle dim, initial rank
+  std::vector<double*> U;              // n x r0 (ld n)
+  std::vector<int64_t> m2l_off;        // CSR over IL of each cluster (both orientations)
+  std::vector<double*> m2l;            // r0_i x r0_j (ld r0_i)
+  std::vector<int64_t> child_off;      // non-leaf: prefix of child r0 (nc*(2^d+1))
+};
+
+struct StoreH {
+  TreeH* tree = nullptr;
+  KernelParams kp{};
+  int p = 8;
+  double tol = 1e-14;
+  int max_init_rank = 0;
+  std::vector<InitLevel> lv;           // index k
+  std::vector<double*> leaf_p2p;       // nc_leaf * win: (i,j) for j in nbr(i), j >= i (ld n_i)
+  std::vector<int> probe_tab;          // ACA probe rows: row m -> 10 ints
+  int probe_maxm = 0;
+  int* d_probe = nullptr;
+  Arena arena{size_t(512) << 20};
+  cudaStream_t stream = nullptr;
+};
+
+struct LevelStatsH {
+  int clusters = 0, max_rank = 0, compressed = 0, dense_kept = 0;
+};
+
+struct RecordH {
+  int level, index, n, r, w;
+  double* sinv;      // n x n (ld n)
+  double* xtop;      // n x w (ld n)
+  int* pos;          // w absolute positions in the solve vector
+  int64_t xoff;      // absolute position of x_i
+};
+
+struct BatchH {
+  int level, colour, rec0, rec1;
+  const RecordH* d_recs;  // device copy of records[rec0..rec1)
+  int maxn, maxw;
+};
+
+struct FactorH {
+  StoreH* store = nullptr;
+  TreeH* tree = nullptr;
+  double tol = 0;
+  int r_m = 0;
+  std::vector<LevelStatsH> stats;      // index k
+  std::vector<RecordH> recs;
+  std::vector<BatchH> batches;
+  int64_t vec_size = 0;                // solve vector length
+  std::vector<int64_t> lvl_base;       // index k: base of level-k x slots; lvl_base[1] = top
+  int top_dim = 0;
+  double* top_inv = nullptr;
+  int64_t g_size = 0;                  // sum of record n (per rhs)
+  std::vector<int64_t> g_off;          // per record
+  int64_t* d_g_off = nullptr;
+  Arena arena{size_t(1) << 30};        // records, top inverse
+  cudaStream_t stream = nullptr;
+  // timing of the last factorization (ms) and work accounting
+  double ms_total = 0;
+  double fl_exec = 0, fl_schur = 0, fl_ref = 0, solve_bytes = 0;
+};
+
+// ------------------------------------------------------------ entry points
+TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_ptr);
+StoreH* store_init(TreeH* t, const KernelParams& kp, int p, double tol, const int* probe_tab, int probe_maxm);
+void matvec(StoreH* s, const double* x, double* y, int64_t nrhs, bool device_ptr);
+FactorH* factorize(StoreH* s, double tol, int flags);
+void solve(FactorH* f, const double* rhs, double* x, int64_t nrhs, bool device_ptr);
+
+// ------------------------------------------------------------ shared helpers
+cudaStream_t default_stream();
+void ensure_device();
+
+}  // namespace ifmm

@@ -1,0 +1,124 @@
+"""GPU factorization and solve (mirror of ifmm/solver.py).
+
+`factorize` runs the whole level-by-level, colour-batched elimination in
+libifmm_b200 (csrc/factor.cu); `solve` replays it for one or many right-hand
+sides (csrc/solve.cu).  Exceptions follow the reference: SingularPivotError
+for numerically singular pivots, ValueError for bad shapes.
+"""
+from __future__ import annotations
+
+import ctypes
+import logging
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import SingularPivotError
+from .geometry import ClusterTree
+from .operators import OperatorStore
+
+logger = logging.getLogger("ifmm")
+
+PIVOT_CONDITION_LIMIT = 1e12  # ifmm/solver.py:50
+
+__all__ = ["IfmmFactorization", "LevelStats", "SingularPivotError", "factorize", "solve"]
+
+
+@dataclass
+class LevelStats:
+    clusters: int = 0
+    max_rank: int = 0
+    fillins_compressed: int = 0
+    fillins_dense_kept: int = 0
+
+
+@dataclass
+class Record:
+    level: int
+    index: int
+    n: int
+    r: int
+    w: int
+
+
+@dataclass
+class IfmmFactorization:
+    store: OperatorStore
+    tree: ClusterTree
+    tol: float
+    handle: object = None
+    level_stats: dict = field(default_factory=dict)
+    r_m: int = 0
+    top_dim: int = 0
+    n_records: int = 0
+    factor_ms: float = 0.0
+
+    @property
+    def n(self) -> int:
+        return self.tree.n_points
+
+    @property
+    def records(self) -> list:
+        out = np.empty((self.n_records, 5), dtype=np.int32)
+        _lib.check(_lib.lib.ifmm_factor_records(self.handle, _lib.ptr(out)))
+        return [Record(*map(int, row)) for row in out]
+
+    @property
+    def work(self) -> dict:
+        """Executed / reference-equivalent FP64 flops and solve bytes per rhs."""
+        w = np.empty(4)
+        _lib.check(_lib.lib.ifmm_factor_work(self.handle, _lib.ptr(w)))
+        return {"flops_exec": w[0], "flops_schur": w[1], "flops_ref": w[2], "solve_bytes": w[3]}
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            _lib.lib.ifmm_factor_free(h)
+
+
+def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None, diagnostics: bool = False,
+              release_m2l: bool = True) -> IfmmFactorization:
+    """Eliminate the extended system on the GPU (ifmm/solver.py:106-153).
+
+    Unlike the reference the store's initial operators stay intact (the
+    elimination works on its own device copy), so `fmm_matvec(store, ...)`
+    remains valid afterwards.  `release_m2l` is accepted for API parity:
+    finished levels are always released."""
+    if tol is None:
+        tol = store.tol
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), 0, ctypes.byref(h)))
+    fact = IfmmFactorization(store=store, tree=tree, tol=float(tol), handle=h)
+    rm, top = ctypes.c_int(), ctypes.c_int()
+    nrec, ms = ctypes.c_int64(), ctypes.c_double()
+    _lib.check(_lib.lib.ifmm_factor_info(h, ctypes.byref(rm), ctypes.byref(top), ctypes.byref(nrec),
+                                         ctypes.byref(ms)))
+    fact.r_m, fact.top_dim, fact.n_records, fact.factor_ms = rm.value, top.value, nrec.value, ms.value
+    for k in range(tree.depth, 1, -1):
+        st = np.zeros(4, dtype=np.int32)
+        _lib.check(_lib.lib.ifmm_factor_level_stats(h, k, _lib.ptr(st)))
+        fact.level_stats[k] = LevelStats(*map(int, st))
+        if diagnostics:
+            s = fact.level_stats[k]
+            logger.info("level=%d,k_clusters=%d,max_rank=%d,fillins_compressed=%d,fillins_dense_kept=%d",
+                        k, s.clusters, s.max_rank, s.fillins_compressed, s.fillins_dense_kept)
+    return fact
+
+
+def solve(fact: IfmmFactorization, rhs):
+    """Solve the factored system (ifmm/solver.py:549-626).  `rhs` is (N,) (as
+    the reference) or (N, nrhs); numpy or torch (CUDA tensors stay on device).
+    Returns the solution in original point order."""
+    n = fact.tree.n_points
+    if isinstance(rhs, np.ndarray) or not type(rhs).__module__.startswith("torch"):
+        a = np.asarray(rhs, dtype=float)
+        if a.ndim not in (1, 2) or a.shape[0] != n:
+            raise ValueError(f"rhs must have shape ({n},)")
+    p_in, kind, nr, keep, is_torch, one_d = _lib.as_input(rhs, n)
+    out, p_out = _lib.alloc_output(keep, kind, n, nr, one_d)
+    _lib.check(_lib.lib.ifmm_solve(fact.handle, p_in, p_out, nr, kind))
+    if is_torch and kind == _lib.PTR_HOST:
+        import torch
+        out = torch.from_numpy(out)
+    return out[:, 0] if one_d else out

@@ -1,0 +1,121 @@
+"""GPU unit tests of the batched dense kernels through the C-ABI test hooks,
+against numpy/scipy fp64 references."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1407_1572_b200 import _lib
+    if _lib.lib.ifmm_device_count() == 0:
+        pytest.skip("no CUDA device")
+    return _lib
+
+
+@pytest.mark.parametrize("ta,tb,tc", [(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 1), (1, 0, 1)])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (64, 64, 16), (97, 130, 53), (200, 17, 300)])
+def test_gemm(L, ta, tb, tc, M, N, K):
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = rng.standard_normal((K, M) if ta else (M, K))
+    B = rng.standard_normal((N, K) if tb else (K, N))
+    C0 = rng.standard_normal((N, M) if tc else (M, N))
+    Af, Bf, Cf = (np.asfortranarray(x) for x in (A, B, C0))
+    C = Cf.copy(order="F")
+    L.check(L.lib.ifmm_test_gemm(ta, tb, M, N, K, -0.5, Af.ctypes.data_as(ctypes.c_void_p), Af.shape[0],
+                                 Bf.ctypes.data_as(ctypes.c_void_p), Bf.shape[0], 2.0,
+                                 C.ctypes.data_as(ctypes.c_void_p), C.shape[0], tc))
+    opA = A.T if ta else A
+    opB = B.T if tb else B
+    ref = -0.5 * opA @ opB + 2.0 * (C0.T if tc else C0)
+    got = C.T if tc else C
+    assert np.allclose(got, ref, rtol=1e-13, atol=1e-12)
+
+
+def _saddle(rng, n, r):
+    P = rng.standard_normal((n, n))
+    P = P + P.T + n * np.eye(n) * 0.1
+    U, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    S = np.zeros((n + r, n + r))
+    S[:n, :n] = P
+    S[:n, n:] = U
+    S[n:, :n] = U.T
+    return S
+
+
+def test_gj_inverse_batched_variable_sizes(L):
+    rng = np.random.default_rng(0)
+    mats = [_saddle(rng, n, r) for n, r in [(5, 2), (64, 40), (64, 64), (90, 31), (250, 70), (3, 0)]]
+    mats.append(rng.standard_normal((700, 700)))
+    sizes = np.array([m.shape[0] for m in mats], dtype=np.int32)
+    packed = np.concatenate([np.asfortranarray(m).ravel(order="F") for m in mats])
+    info = np.zeros(len(mats), dtype=np.int32)
+    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(sizes), len(mats), L.ptr(info)))
+    assert not info.any()
+    off = 0
+    for m in mats:
+        k = m.shape[0]
+        inv = packed[off:off + k * k].reshape((k, k), order="F")
+        off += k * k
+        ref = np.linalg.inv(m)
+        assert np.linalg.norm(inv - ref) <= 1e-10 * np.linalg.norm(ref) * max(1.0, np.linalg.cond(m) / 1e4)
+
+
+def test_gj_flags_singular(L):
+    A = np.zeros((4, 4))
+    A[0, 0] = A[1, 1] = 1.0
+    sizes = np.array([4], dtype=np.int32)
+    info = np.zeros(1, dtype=np.int32)
+    packed = A.ravel(order="F").copy()
+    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(sizes), 1, L.ptr(info)))
+    assert info[0] == 3
+
+
+@pytest.mark.parametrize("m,n", [(16, 16), (432, 16), (64, 40), (300, 64), (7, 3)])
+def test_jacobi_svd(L, m, n):
+    rng = np.random.default_rng(m + n)
+    A = rng.standard_normal((m, n)) @ np.diag(np.logspace(0, -12, n))
+    a = np.asfortranarray(A).copy(order="F")
+    V = np.empty((n, n), order="F")
+    sig = np.empty(n)
+    L.check(L.lib.ifmm_test_jacobi(L.ptr(a), m, n, L.ptr(V), L.ptr(sig)))
+    s_ref = np.linalg.svd(A, compute_uv=False)
+    assert np.allclose(np.sort(sig)[::-1], s_ref, rtol=1e-9, atol=1e-14 * s_ref[0])
+    assert np.allclose(a, A @ V, atol=1e-12 * s_ref[0])
+    assert np.allclose(V.T @ V, np.eye(n), atol=1e-12)
+
+
+@pytest.mark.parametrize("m,k", [(10, 3), (100, 16), (500, 64), (16, 16)])
+def test_householder_qr(L, m, k):
+    rng = np.random.default_rng(m * k)
+    A = rng.standard_normal((m, k))
+    Q = np.empty((m, k), order="F")
+    R = np.empty((k, k), order="F")
+    L.check(L.lib.ifmm_test_qr(L.ptr(np.asfortranarray(A)), m, k, L.ptr(Q), L.ptr(R)))
+    assert np.allclose(Q @ R, A, atol=1e-12)
+    assert np.allclose(Q.T @ Q, np.eye(k), atol=1e-12)
+    assert np.allclose(np.tril(R, -1), 0)
+
+
+@pytest.mark.parametrize("m,n,rank", [(40, 60, 5), (16, 120, 12), (200, 150, 30)])
+def test_aca_matches_oracle_crosses(L, m, n, rank):
+    from oracle import ifmm_oracle as O
+    rng = np.random.default_rng(m + n)
+    F = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n)) * np.logspace(0, -6, n)
+    _, probes = O.aca_probe_rows(m)
+    kmax = min(m, n)
+    left = np.empty((m, kmax), order="F")
+    right = np.empty((n, kmax), order="F")
+    rk = np.zeros(1, dtype=np.int32)
+    inc = np.zeros(1, dtype=np.int32)
+    L.check(L.lib.ifmm_test_aca(L.ptr(np.asfortranarray(F)), m, n, 1e-8, L.ptr(probes.astype(np.int32)), kmax,
+                                L.ptr(left), L.ptr(right), L.ptr(rk), L.ptr(inc)))
+    k = int(rk[0])
+    approx = left[:, :k] @ right[:, :k].T
+    assert np.linalg.norm(approx - F) <= 1e-6 * np.linalg.norm(F)
+    Lo, Ro, bad = O.aca_block(F, 1e-8)
+    assert not bad and not inc[0]
+    assert abs(k - Lo.shape[1]) <= 2
