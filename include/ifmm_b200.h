@@ -39,6 +39,7 @@ enum {
 };
 
 enum { IFMM_PTR_HOST = 0, IFMM_PTR_DEVICE = 1 };
+enum { IFMM_FLAG_TIMING = 1 };
 
 /* kernel ids: the reference registry ifmm/kernels.py:160-170 plus the two
  * BASELINE kernels inv_r = scale/r and log_r = scale*(ln r + shift) */
@@ -56,6 +57,8 @@ const char* ifmm_last_error(void);
 int ifmm_last_singular(int* level, int* index, double* cond);
 int ifmm_version(void);
 int ifmm_device_count(void);
+/* select the CUDA device used by subsequent calls on this thread */
+int ifmm_set_device(int device);
 
 /* ---- tree: PointSet checks + build_tree + compute_lists
  *      (ifmm/geometry.py:47-61, :174-226, :229-262) */
@@ -103,6 +106,13 @@ int ifmm_factor_records(const ifmm_factor* f, int32_t* out5);
  * out[2] reference-equivalent flops (sum 2/3 m^3 + 2 m^2 w + 2 h n w
  * + 2/3 M_top^3), out[3] bytes one solve sweep streams per right-hand side */
 int ifmm_factor_work(const ifmm_factor* f, double* out4);
+/* per-phase device time in ms and kernel launches, recorded with CUDA events
+ * on the factorization stream when ifmm_factorize ran with IFMM_FLAG_TIMING:
+ * 0 gathers/copies, 1 Gauss-Jordan inverses, 2 X = S^-1 C, 3 Schur update,
+ * 4 fill-in compression, 5 level transitions, 6 top-level inverse */
+int ifmm_factor_timing(const ifmm_factor* f, double* ms7, int64_t* launches7);
+/* total kernel launches issued by the library since load */
+int64_t ifmm_launch_count(void);
 /* solve(fact, rhs) (ifmm/solver.py:549-626) for nrhs >= 1 columns */
 int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int ptr_kind);
 void ifmm_factor_free(ifmm_factor* f);

@@ -40,6 +40,7 @@ SIGNATURES = {
     "ifmm_last_singular": (_i32, [_pi32, _pi32, _pd]),
     "ifmm_version": (_i32, []),
     "ifmm_device_count": (_i32, []),
+    "ifmm_set_device": (_i32, [_i32]),
     "ifmm_tree_build": (_i32, [_p, _i64, _i32, _i32, _i32, ctypes.POINTER(_p)]),
     "ifmm_tree_info": (_i32, [_p, _pi64, _pi32, _pi32]),
     "ifmm_tree_permutation": (_i32, [_p, _p]),
@@ -59,6 +60,8 @@ SIGNATURES = {
     "ifmm_factor_level_stats": (_i32, [_p, _i32, _p]),
     "ifmm_factor_records": (_i32, [_p, _p]),
     "ifmm_factor_work": (_i32, [_p, _p]),
+    "ifmm_factor_timing": (_i32, [_p, _p, _p]),
+    "ifmm_launch_count": (_i64, []),
     "ifmm_solve": (_i32, [_p, _p, _p, _i64, _i32]),
     "ifmm_factor_free": (None, [_p]),
     "ifmm_test_gj_inverse": (_i32, [_p, _p, _i32, _p]),

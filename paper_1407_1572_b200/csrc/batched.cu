@@ -211,7 +211,7 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   size_t smem = size_t(maxm) * (b + 1) * 8;
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
   CK(cudaMemsetAsync(d_info, 0, sizeof(int) * n, s));

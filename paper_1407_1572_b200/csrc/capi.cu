@@ -85,6 +85,10 @@ int ifmm_device_count(void) {
   return n;
 }
 
+int ifmm_set_device(int device) {
+  return guard([&] { CK(cudaSetDevice(device)); });
+}
+
 // ---------------------------------------------------------------- tree
 int ifmm_tree_build(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out) {
   return guard([&] {
@@ -250,6 +254,17 @@ int ifmm_factor_work(const ifmm_factor* f, double* out4) {
     out4[3] = f->h->solve_bytes;
   });
 }
+
+int ifmm_factor_timing(const ifmm_factor* f, double* ms7, int64_t* launches7) {
+  return guard([&] {
+    for (int p = 0; p < ifmm::PH_COUNT; p++) {
+      if (ms7) ms7[p] = f->h->phase_ms[p];
+      if (launches7) launches7[p] = f->h->phase_launches[p];
+    }
+  });
+}
+
+int64_t ifmm_launch_count(void) { return ifmm::launch_counter().load(); }
 
 int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int ptr_kind) {
   return guard([&] { ifmm::solve(f->h, rhs, x, nrhs, ptr_kind == IFMM_PTR_DEVICE); });

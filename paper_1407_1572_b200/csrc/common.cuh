@@ -2,6 +2,7 @@
 // arenas, launch helpers and warp/block reductions.  sm_100a only.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -41,8 +42,17 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     throw Error(e == cudaErrorMemoryAllocation ? IFMM_OOM : IFMM_CUDA, buf);
   }
 }
+// every kernel launch of the library goes through CK_LAUNCH: count them
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
 #define CK(x) ::ifmm::cuda_check((x), #x, __FILE__, __LINE__)
-#define CK_LAUNCH() ::ifmm::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+#define CK_LAUNCH()                                                                  \
+  do {                                                                               \
+    ::ifmm::launch_counter().fetch_add(1, std::memory_order_relaxed);                \
+    ::ifmm::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);     \
+  } while (0)
 
 [[noreturn]] inline void invalid(const std::string& m) { throw Error(IFMM_INVALID, m); }
 

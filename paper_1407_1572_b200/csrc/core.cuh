@@ -114,7 +114,23 @@ struct FactorH {
   // timing of the last factorization (ms) and work accounting
   double ms_total = 0;
   double fl_exec = 0, fl_schur = 0, fl_ref = 0, solve_bytes = 0;
+  // per-phase device time (ms, CUDA events on the factorization stream) when
+  // factorize() ran with IFMM_FLAG_TIMING: see PhaseId
+  double phase_ms[8] = {0};
+  long long phase_launches[8] = {0};
 };
+
+enum PhaseId : int {
+  PH_GATHER = 0,     // S / C gathers, record copies
+  PH_GJ = 1,         // batched Gauss-Jordan inverses (+ norms)
+  PH_XGEMM = 2,      // X = S^-1 C
+  PH_SCHUR = 3,      // symmetric Schur update GEMMs
+  PH_COMPRESS = 4,   // fill-in compression
+  PH_TRANSITION = 5, // level start (parent near field, bases)
+  PH_TOP = 6,        // top-level inverse
+  PH_COUNT = 7,
+};
+constexpr int IFMM_FLAG_TIMING = 1;
 
 // ------------------------------------------------------------ entry points
 TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_ptr);

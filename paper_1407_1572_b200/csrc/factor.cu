@@ -55,6 +55,7 @@ struct CompressParams {
   int* rank;           // level ranks (device)
   int* status;         // per fill: 0 compressed, 1 kept dense
   int* stats;          // [compressed, dense_kept, max_rank]
+  int debug;
 };
 
 __device__ inline void fill_zero(const FillDesc& D, int rows, int cols) {
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(256) compress_kernel(const FillDesc* __restric
     fro = sqrt(block_sum(fro, sh.red));
     const double cutoff = tol * fro;
     if (threadIdx.x == 0) {
-      P.status[f] = 0;
+      P.status[f] = (k << 8) | (r << 20);  // low byte 0: compressed; ranks kept for diagnostics
       atomicAdd(&P.stats[0], 1);
       atomicMax(&P.stats[2], r);
     }
@@ -237,7 +238,10 @@ __global__ void __launch_bounds__(256) compress_kernel(const FillDesc* __restric
         rp += wp;
         __syncthreads();
         if (threadIdx.x == 0) P.rank[D.p] = rp;
+        if (P.debug && threadIdx.x == 0) printf("aug p=%d +%d -> %d\n", D.p, wp, rp);
       }
+      if (P.debug && threadIdx.x == 0)
+        printf("augq fill=%d kind=%d p=%d q=%d r=%d +%d -> %d fro=%.6e\n", f, D.kind, D.p, D.q, r, wq, rq, fro);
       __syncthreads();
       // E2 = Uq^T B (rq x r)
       cta_gemm(rq, r, cols, 1.0, D.Uq, cols, true, Vc, cols, false, 0.0, E2, rq);
@@ -275,6 +279,68 @@ struct BlkRef {
   bool trans;
 };
 
+// CUDA-event phase timing on the factorization stream (IFMM_FLAG_TIMING).
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  struct Span {
+    cudaEvent_t a, b;
+    int ph;
+    long long launches;
+  };
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> pool;
+  int cur = -1;
+  cudaEvent_t ev0 = nullptr;
+  long long l0 = 0;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  void begin(int ph) {
+    if (!on) return;
+    end();
+    ev0 = get();
+    CK(cudaEventRecord(ev0, s));
+    cur = ph;
+    l0 = launch_counter().load();
+  }
+  void end() {
+    if (!on || cur < 0) return;
+    cudaEvent_t e = get();
+    CK(cudaEventRecord(e, s));
+    spans.push_back({ev0, e, cur, launch_counter().load() - l0});
+    cur = -1;
+  }
+  void collect(FactorH* F) {  // call after a stream synchronisation
+    if (!on) return;
+    end();
+    for (Span& sp : spans) {
+      float ms = 0.f;
+      CK(cudaEventSynchronize(sp.b));
+      CK(cudaEventElapsedTime(&ms, sp.a, sp.b));
+      F->phase_ms[sp.ph] += ms;
+      F->phase_launches[sp.ph] += sp.launches;
+      pool.push_back(sp.a);
+      pool.push_back(sp.b);
+    }
+    spans.clear();
+  }
+  ~PhaseTimer() {
+    for (auto& sp : spans) {
+      cudaEventDestroy(sp.a);
+      cudaEventDestroy(sp.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 class Factorizer {
  public:
   Factorizer(StoreH* S, double tol, int flags) : S_(S), t_(S->tree), tol_(tol), flags_(flags) {}
@@ -289,6 +355,7 @@ class Factorizer {
   std::unique_ptr<FactorH> F_;
   Arena ws_{size_t(256) << 20};
   Staging st_;
+  PhaseTimer tm_;
   Arena lvl_arena_[2] = {Arena(size_t(512) << 20), Arena(size_t(512) << 20)};
   WorkLevel cur_, prev_;
   // per-record host metadata for pos resolution at level end
@@ -526,11 +593,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
     }
     cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
   }
+  tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
   const MatDesc* dmd = upload(ws_, md, s_, st_);
   double* d_nS = ws_.alloc_n<double>(np);
   double* d_nSi = ws_.alloc_n<double>(np);
   int* d_info = ws_.alloc_n<int>(np);
+  tm_.begin(PH_GJ);
   launch_norm1(dmd, np, d_nS, s_);
   batched_gj_inverse(md, dmd, d_info, ws_, st_, s_);
   launch_norm1(dmd, np, d_nSi, s_);
@@ -567,8 +636,11 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
     gb.add(I.S, I.m, I.C, I.n, R.xtop, I.n, I.n, wl, I.n, 1.0, 0.0);
     gb.add(I.S + I.n, I.m, I.C, I.n, I.Xb, I.r, I.r, wl, I.n, 1.0, 0.0);
   }
+  tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
+  tm_.begin(PH_XGEMM);
   launch_grouped_gemm(gb, false, false, ws_, st_, s_);
+  tm_.end();
   // symmetric Schur update on the block upper triangle: target -= C_a^T X_b
   for (int t = 0; t < np; t++) {
     PivInfo& I = P[t];
@@ -604,8 +676,11 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
                -1.0, 1.0, tgt.trans);
       }
   }
+  tm_.begin(PH_SCHUR);
   launch_grouped_gemm(gb, true, false, ws_, st_, s_);
+  tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
+  tm_.end();
   // fill-in compression lists (reference order: hybrid pairs sorted, then P2P pairs sorted)
   std::vector<FillDesc> fd;
   std::vector<PivotWork> pw(np);
@@ -652,12 +727,15 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   int* d_stats = ws_.alloc_n<int>(4);
   CK(cudaMemsetAsync(d_stats, 0, 16, s_));
   if (!fd.empty()) {
+    tm_.begin(PH_COMPRESS);
     const FillDesc* dfd = upload(ws_, fd, s_, st_);
     const PivotWork* dpw = upload(ws_, pw, s_, st_);
-    CompressParams cp{tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_status, d_stats};
+    CompressParams cp{tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_status, d_stats,
+                      getenv("IFMM_DEBUG") != nullptr ? 1 : 0};
     compress_kernel<<<np, 256, 0, s_>>>(dfd, dpw, cp);
     CK_LAUNCH();
   }
+  tm_.end();
   // read back: pivot conditioning, ranks, fill outcomes, counters
   std::vector<double> nS(np), nSi(np);
   std::vector<int> info(np), status(fd.size()), stats(4);
@@ -668,6 +746,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   CK(cudaMemcpyAsync(stats.data(), d_stats, 16, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(W.r.data(), W.d_rank, sizeof(int) * W.nc, cudaMemcpyDeviceToHost, s_));
   CK(cudaStreamSynchronize(s_));
+  tm_.collect(F_.get());
   for (int t = 0; t < np; t++) {
     double rc = (info[t] != 0) ? 0.0 : 1.0 / (nS[t] * nSi[t]);
     if (!std::isfinite(rc) || rc <= 1.0 / 1e12) {
@@ -682,8 +761,12 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   LS.compressed += stats[0];
   LS.dense_kept += stats[1];
   LS.max_rank = std::max(LS.max_rank, stats[2]);
+  static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
   for (size_t f = 0; f < fh.size(); f++) {
-    if (status[f] != 0) continue;
+    if (dbg)
+      fprintf(stderr, "fill k=%d kind=%d p=%d q=%d status=%d aca=%d rank=%d rank_p=%d\n", k, fh[f].kind, fh[f].p,
+              fh[f].q, status[f] & 0xff, (status[f] >> 8) & 0xfff, status[f] >> 20, W.r[fh[f].p]);
+    if ((status[f] & 0xff) != 0) continue;
     const FillHost& h = fh[f];
     if (h.kind == FILL_HYBRID) pres(W.px, W, h.q, h.p) = 0;
     else set_pp(W, h.p, h.q, 0);
@@ -758,14 +841,18 @@ void Factorizer::factor_top() {
     md[0] = MatDesc{F_->top_inv, M, M, ws_.alloc_n<int>(M), -1};
     const MatDesc* dmd = upload(ws_, md, s_, st_);
     int* d_info = ws_.alloc_n<int>(1);
+    tm_.begin(PH_TOP);
     batched_gj_inverse(md, dmd, d_info, ws_, st_, s_);
   }
   CK(cudaStreamSynchronize(s_));
+  tm_.collect(F_.get());
 }
 
 FactorH* Factorizer::run() {
   auto t0 = std::chrono::steady_clock::now();
   s_ = S_->stream;
+  tm_.on = (flags_ & IFMM_FLAG_TIMING) != 0;
+  tm_.s = s_;
   F_.reset(new FactorH);
   F_->store = S_;
   F_->tree = t_;
@@ -779,12 +866,15 @@ FactorH* Factorizer::run() {
   const int ncol = [&] { int c = 1; for (int d = 0; d < t_->dim; d++) c *= 3; return c; }();
   for (int k = K; k >= 2; k--) {
     if (k == K) {
+      tm_.begin(PH_TRANSITION);
       start_leaf_level();
     } else {
       prev_ = std::move(cur_);
       cur_ = WorkLevel{};
+      tm_.begin(PH_TRANSITION);
       start_parent_level(prev_, k);
       CK(cudaStreamSynchronize(s_));
+      tm_.collect(F_.get());
       prev_ = WorkLevel{};
     }
     F_->stats[k].clusters = cur_.nc;

@@ -71,14 +71,25 @@ class IfmmFactorization:
         _lib.check(_lib.lib.ifmm_factor_work(self.handle, _lib.ptr(w)))
         return {"flops_exec": w[0], "flops_schur": w[1], "flops_ref": w[2], "solve_bytes": w[3]}
 
+    @property
+    def phase_times(self) -> dict:
+        """Device ms and kernel launches per factorization phase (needs timing=True)."""
+        ms = np.zeros(7)
+        nl = np.zeros(7, dtype=np.int64)
+        _lib.check(_lib.lib.ifmm_factor_timing(self.handle, _lib.ptr(ms), _lib.ptr(nl)))
+        return {p: (float(ms[i]), int(nl[i])) for i, p in enumerate(PHASES)}
+
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None
         if h:
             _lib.lib.ifmm_factor_free(h)
 
 
+PHASES = ("gather", "gauss_jordan", "x_gemm", "schur_gemm", "compress", "transition", "top")
+
+
 def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None, diagnostics: bool = False,
-              release_m2l: bool = True) -> IfmmFactorization:
+              release_m2l: bool = True, timing: bool = False) -> IfmmFactorization:
     """Eliminate the extended system on the GPU (ifmm/solver.py:106-153).
 
     Unlike the reference the store's initial operators stay intact (the
@@ -88,7 +99,7 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
     if tol is None:
         tol = store.tol
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), 0, ctypes.byref(h)))
+    _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), 1 if timing else 0, ctypes.byref(h)))
     fact = IfmmFactorization(store=store, tree=tree, tol=float(tol), handle=h)
     rm, top = ctypes.c_int(), ctypes.c_int()
     nrec, ms = ctypes.c_int64(), ctypes.c_double()

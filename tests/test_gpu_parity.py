@@ -66,7 +66,8 @@ def test_init_ranks_and_matvec(ifmm, name):
         assert np.array_equal(store.ranks(k), g[f"rank0_{k}"]), k
     mv = ifmm.fmm_matvec(store, tree, g["xm"])
     assert np.linalg.norm(mv - g["mv"]) <= 1e-12 * np.linalg.norm(g["mv"])
-    if "far_2_0" in g:
+    if "far_2_0" in g and int(g["depth"]) == 2:
+        # U M2L U^T is basis-invariant only where the particle axis is physical (leaf level)
         j = int(g["far_2_0_j"][0])
         U0, Uj = store.l2p[(2, 0)], store.l2p[(2, j)]
         far = U0 @ store.m2l[(2, 0, j)] @ Uj.T
@@ -100,8 +101,13 @@ def test_factor_solve_residual_and_solution(ifmm, name):
     diff = np.linalg.norm(x - xc) / np.linalg.norm(xc)
     morton_vs_colour = np.linalg.norm(g["x_morton"] - xc) / np.linalg.norm(xc)
     assert diff <= max(10 * tol, 2 * morton_vs_colour), (diff, morton_vs_colour)
-    # G5: ranks
-    assert abs(fact.r_m - int(g["rm_colour9"])) <= 0.25 * int(g["rm_colour9"]) + 1
+    # G5: ranks.  r_m (max ACA rank) is noise-driven near the cutoff: the CPU
+    # oracle itself drops from 28 to 16 on reglog_1k when its LU solves are
+    # replaced by an explicit inverse, so gate
+    # on the top-level dimension (sum of final level-2 ranks) and bound r_m above.
+    ref_top = int(g["top_colour9"])
+    assert abs(fact.top_dim - ref_top) <= 0.1 * ref_top, (fact.top_dim, ref_top)
+    assert fact.r_m <= 1.25 * int(g["rm_colour9"]) + 1
 
 
 def test_exact_mode_vs_dense_lu(ifmm):
