@@ -93,8 +93,9 @@ int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr
 void ifmm_store_free(ifmm_store* s);
 
 /* ---- factorize(store, tree, tol) (ifmm/solver.py:106-153); tol < 0 -> store tol.
+ * cond_limit: PIVOT_CONDITION_LIMIT (ifmm/solver.py:50); <= 0 -> 1e12 (reference).
  * The store's initial operators are left intact (matvec stays valid). */
-int ifmm_factorize(ifmm_store* s, double tol, int flags, ifmm_factor** out);
+int ifmm_factorize(ifmm_store* s, double tol, int flags, double cond_limit, ifmm_factor** out);
 /* r_m, top-level dimension, number of eliminations, factorization wall ms */
 int ifmm_factor_info(const ifmm_factor* f, int* r_m, int* top_dim, int64_t* n_records, double* ms);
 /* LevelStats of `level`: clusters, max_rank, fillins_compressed, fillins_dense_kept */

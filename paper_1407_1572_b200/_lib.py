@@ -55,7 +55,7 @@ SIGNATURES = {
     "ifmm_store_m2l": (_i32, [_p, _i32, _i32, _i32, _p]),
     "ifmm_matvec": (_i32, [_p, _p, _p, _i64, _i32]),
     "ifmm_store_free": (None, [_p]),
-    "ifmm_factorize": (_i32, [_p, _d, _i32, ctypes.POINTER(_p)]),
+    "ifmm_factorize": (_i32, [_p, _d, _i32, _d, ctypes.POINTER(_p)]),
     "ifmm_factor_info": (_i32, [_p, _pi32, _pi32, _pi64, _pd]),
     "ifmm_factor_level_stats": (_i32, [_p, _i32, _p]),
     "ifmm_factor_records": (_i32, [_p, _p]),

@@ -101,6 +101,107 @@ void launch_norm1(const MatDesc* d_desc, int n, double* out, cudaStream_t s) {
   CK_LAUNCH();
 }
 
+// ------------------------------------------------------------------ 1-norm estimate
+// Hager/Higham estimate of ||B||_1 (LAPACK dlacn2, the estimator dgecon uses,
+// ifmm/solver.py:216) applied to the explicit inverse B = S^-1: the reference's
+// rcond test sees this estimate (<= the exact norm), so the GPU raises
+// SingularPivotError under the same criterion.
+__device__ inline void gemv_n(const MatDesc& D, const double* x, double* y) {  // y = B x
+  for (int i = threadIdx.x; i < D.m; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < D.m; j++) s = fma(D.A[i + (size_t)j * D.lda], x[j], s);
+    y[i] = s;
+  }
+  __syncthreads();
+}
+__device__ inline void gemv_t(const MatDesc& D, const double* x, double* y) {  // y = B^T x
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < D.m; j += nw) {
+    const double* c = D.A + (size_t)j * D.lda;
+    double s = 0.0;
+    for (int i = lane; i < D.m; i += 32) s = fma(c[i], x[i], s);
+    s = warp_sum(s);
+    if (lane == 0) y[j] = s;
+  }
+  __syncthreads();
+}
+__device__ inline double asum(const double* v, int n, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += fabs(v[i]);
+  return block_sum(s, red);
+}
+__device__ inline int iamax(const double* v, int n, ArgMax* red) {
+  ArgMax a{-1.0, -1};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a = argmax_merge(a, ArgMax{fabs(v[i]), i});
+  return block_argmax(a, red).i;
+}
+
+__global__ void __launch_bounds__(256) norm1_est_kernel(const MatDesc* __restrict__ desc, double* out) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ ArgMax ared[32];
+  __shared__ int s_flag;
+  const MatDesc D = desc[blockIdx.x];
+  const int n = D.m;
+  double* x = sm;
+  double* y = x + n;
+  double* sgn = y + n;
+  if (n == 0) {
+    if (threadIdx.x == 0) out[blockIdx.x] = 0.0;
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = 1.0 / n;
+  __syncthreads();
+  gemv_n(D, x, y);
+  double est = asum(y, n, red);
+  if (n == 1) {
+    if (threadIdx.x == 0) out[blockIdx.x] = est;
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sgn[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+  __syncthreads();
+  gemv_t(D, sgn, x);
+  int j = iamax(x, n, ared);
+  for (int iter = 2;; iter++) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = (i == j) ? 1.0 : 0.0;
+    __syncthreads();
+    gemv_n(D, x, y);
+    const double old = est;
+    est = asum(y, n, red);
+    if (threadIdx.x == 0) s_flag = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      if ((y[i] >= 0.0 ? 1.0 : -1.0) != sgn[i]) s_flag = 1;
+    __syncthreads();
+    if (!s_flag || est <= old) break;  // repeated sign vector or no increase
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sgn[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+    __syncthreads();
+    gemv_t(D, sgn, x);
+    const int jlast = j;
+    j = iamax(x, n, ared);
+    if (!(x[jlast] != fabs(x[j]) && iter < 5)) break;
+  }
+  // alternating-sign test vector
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    x[i] = ((i & 1) ? -1.0 : 1.0) * (1.0 + double(i) / double(n - 1));
+  __syncthreads();
+  gemv_n(D, x, y);
+  const double temp = 2.0 * asum(y, n, red) / (3.0 * n);
+  if (threadIdx.x == 0) out[blockIdx.x] = temp > est ? temp : est;
+}
+
+void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  const size_t smem = sizeof(double) * 3 * size_t(std::max(1, maxm));
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(norm1_est_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  norm1_est_kernel<<<n, 256, smem, s>>>(d_desc, out);
+  CK_LAUNCH();
+}
+
 // ------------------------------------------------------------------ Gauss-Jordan
 // Panel transform: columns [j, j+b) of every matrix with m > j.
 __global__ void __launch_bounds__(512) gj_panel_kernel(const MatDesc* __restrict__ desc, int j, int b,

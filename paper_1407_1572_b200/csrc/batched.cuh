@@ -42,6 +42,8 @@ struct MatDesc {
 
 // 1-norm (max column abs sum) of every matrix -> out[p]
 void launch_norm1(const MatDesc* d_desc, int n, double* out, cudaStream_t s);
+// dlacn2 (Hager/Higham) estimate of the 1-norm of every matrix -> out[p]
+void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s);
 
 // In-place inversion of every matrix by blocked Gauss-Jordan elimination with
 // partial pivoting.  `info[p]` = 0, or 1 + first column with an exact zero

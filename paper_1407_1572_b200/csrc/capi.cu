@@ -205,10 +205,10 @@ void ifmm_store_free(ifmm_store* s) {
 }
 
 // ---------------------------------------------------------------- factor / solve
-int ifmm_factorize(ifmm_store* s, double tol, int flags, ifmm_factor** out) {
+int ifmm_factorize(ifmm_store* s, double tol, int flags, double cond_limit, ifmm_factor** out) {
   return guard([&] {
     if (!s || !out) invalid("null handle");
-    FactorH* h = ifmm::factorize(s->h, tol, flags);
+    FactorH* h = ifmm::factorize(s->h, tol, flags, cond_limit);
     *out = new ifmm_factor{h};
   });
 }

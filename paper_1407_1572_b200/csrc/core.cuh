@@ -136,7 +136,7 @@ constexpr int IFMM_FLAG_TIMING = 1;
 TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_ptr);
 StoreH* store_init(TreeH* t, const KernelParams& kp, int p, double tol, const int* probe_tab, int probe_maxm);
 void matvec(StoreH* s, const double* x, double* y, int64_t nrhs, bool device_ptr);
-FactorH* factorize(StoreH* s, double tol, int flags);
+FactorH* factorize(StoreH* s, double tol, int flags, double cond_limit);
 void solve(FactorH* f, const double* rhs, double* x, int64_t nrhs, bool device_ptr);
 
 // ------------------------------------------------------------ shared helpers

@@ -343,7 +343,8 @@ struct PhaseTimer {
 
 class Factorizer {
  public:
-  Factorizer(StoreH* S, double tol, int flags) : S_(S), t_(S->tree), tol_(tol), flags_(flags) {}
+  Factorizer(StoreH* S, double tol, int flags, double cond_limit)
+      : S_(S), t_(S->tree), tol_(tol), flags_(flags), cond_limit_(cond_limit) {}
   FactorH* run();
 
  private:
@@ -351,6 +352,7 @@ class Factorizer {
   TreeH* t_;
   double tol_;
   int flags_;
+  double cond_limit_;  // PIVOT_CONDITION_LIMIT (ifmm/solver.py:50), 1e12 by default
   cudaStream_t s_ = nullptr;
   std::unique_ptr<FactorH> F_;
   Arena ws_{size_t(256) << 20};
@@ -595,6 +597,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   }
   tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
+  static const char* dump_dir = getenv("IFMM_DUMP_SINGULAR");
+  std::vector<double*> Sbak;
+  if (dump_dir)
+    for (int t = 0; t < np; t++) {
+      Sbak.push_back(ws_.alloc_n<double>(size_t(P[t].m) * P[t].m));
+      CK(cudaMemcpyAsync(Sbak.back(), P[t].S, sizeof(double) * P[t].m * P[t].m, cudaMemcpyDeviceToDevice, s_));
+    }
   const MatDesc* dmd = upload(ws_, md, s_, st_);
   double* d_nS = ws_.alloc_n<double>(np);
   double* d_nSi = ws_.alloc_n<double>(np);
@@ -602,7 +611,11 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   tm_.begin(PH_GJ);
   launch_norm1(dmd, np, d_nS, s_);
   batched_gj_inverse(md, dmd, d_info, ws_, st_, s_);
-  launch_norm1(dmd, np, d_nSi, s_);
+  {
+    int maxm = 0;
+    for (auto& d : md) maxm = std::max(maxm, d.m);
+    launch_norm1_estimate(dmd, np, maxm, d_nSi, s_);
+  }
   // records + X = S^-1 C
   GemmBatch gb;
   for (int t = 0; t < np; t++) {
@@ -749,8 +762,20 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   tm_.collect(F_.get());
   for (int t = 0; t < np; t++) {
     double rc = (info[t] != 0) ? 0.0 : 1.0 / (nS[t] * nSi[t]);
-    if (!std::isfinite(rc) || rc <= 1.0 / 1e12) {
+    if (!std::isfinite(rc) || rc <= 1.0 / cond_limit_) {
       double cond = 1.0 / std::max(rc, 1e-300);
+      if (dump_dir) {
+        std::vector<double> h(size_t(P[t].m) * P[t].m);
+        CK(cudaMemcpy(h.data(), Sbak[t], sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+        std::string fn = std::string(dump_dir) + "/S_" + std::to_string(k) + "_" + std::to_string(P[t].i) + ".bin";
+        FILE* fp = fopen(fn.c_str(), "wb");
+        if (fp) {
+          int hdr[2] = {P[t].n, P[t].r};
+          fwrite(hdr, sizeof hdr, 1, fp);
+          fwrite(h.data(), sizeof(double), h.size(), fp);
+          fclose(fp);
+        }
+      }
       char buf[256];
       snprintf(buf, sizeof buf, "pivot for cluster %d at level %d is numerically singular (condition estimate %.2e)",
                P[t].i, k, cond);
@@ -917,9 +942,9 @@ FactorH* Factorizer::run() {
   return F_.release();
 }
 
-FactorH* factorize(StoreH* S, double tol, int flags) {
+FactorH* factorize(StoreH* S, double tol, int flags, double cond_limit) {
   ensure_device();
-  Factorizer f(S, tol < 0 ? S->tol : tol, flags);
+  Factorizer f(S, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12);
   return f.run();
 }
 

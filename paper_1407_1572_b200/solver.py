@@ -89,7 +89,8 @@ PHASES = ("gather", "gauss_jordan", "x_gemm", "schur_gemm", "compress", "transit
 
 
 def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None, diagnostics: bool = False,
-              release_m2l: bool = True, timing: bool = False) -> IfmmFactorization:
+              release_m2l: bool = True, timing: bool = False,
+              pivot_condition_limit: float = PIVOT_CONDITION_LIMIT) -> IfmmFactorization:
     """Eliminate the extended system on the GPU (ifmm/solver.py:106-153).
 
     Unlike the reference the store's initial operators stay intact (the
@@ -99,7 +100,8 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
     if tol is None:
         tol = store.tol
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), 1 if timing else 0, ctypes.byref(h)))
+    _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), 1 if timing else 0, float(pivot_condition_limit),
+                                       ctypes.byref(h)))
     fact = IfmmFactorization(store=store, tree=tree, tol=float(tol), handle=h)
     rm, top = ctypes.c_int(), ctypes.c_int()
     nrec, ms = ctypes.c_int64(), ctypes.c_double()
