@@ -136,13 +136,17 @@ __device__ inline int iamax(const double* v, int n, ArgMax* red) {
   return block_argmax(a, red).i;
 }
 
-__global__ void __launch_bounds__(256) norm1_est_kernel(const MatDesc* __restrict__ desc, double* out) {
+__global__ void __launch_bounds__(256) norm1_est_kernel(const MatDesc* __restrict__ desc, double* out,
+                                                        const double* __restrict__ normA, double limit) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   __shared__ ArgMax ared[32];
   __shared__ int s_flag;
   const MatDesc D = desc[blockIdx.x];
   const int n = D.m;
+  // out holds the exact ||B||_1 on entry; the estimate never exceeds it, so a
+  // pivot that passes with the exact norm passes with the estimate too
+  if (out[blockIdx.x] * normA[blockIdx.x] < limit) return;
   double* x = sm;
   double* y = x + n;
   double* sgn = y + n;
@@ -190,7 +194,8 @@ __global__ void __launch_bounds__(256) norm1_est_kernel(const MatDesc* __restric
   if (threadIdx.x == 0) out[blockIdx.x] = temp > est ? temp : est;
 }
 
-void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s) {
+void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, const double* normA, double limit,
+                           cudaStream_t s) {
   if (n <= 0) return;
   const size_t smem = sizeof(double) * 3 * size_t(std::max(1, maxm));
   static bool attr = false;
@@ -198,7 +203,7 @@ void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, 
     CK(cudaFuncSetAttribute(norm1_est_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  norm1_est_kernel<<<n, 256, smem, s>>>(d_desc, out);
+  norm1_est_kernel<<<n, 256, smem, s>>>(d_desc, out, normA, limit);
   CK_LAUNCH();
 }
 

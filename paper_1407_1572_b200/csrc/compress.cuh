@@ -1,0 +1,53 @@
+// Batched fill-in compression (ifmm/solver.py:319-434, 495-520).
+//
+// The reference compresses the fills of one elimination sequentially.  Their
+// true dependencies are narrower, and the batch is split along them:
+//   K1 ACA + QR/SVD recompression         -- every fill independent
+//   K2 new directions of hybrid fills      -- serial only per (pivot, q) chain
+//                                            (fills augment U_q in sorted order)
+//   K3 new directions of P2P fills         -- after all hybrids, serial per pivot
+//   K4 M2L absorption + drop               -- every fill independent: the basis
+//                                            prefix each fill saw is recorded
+// K1..K4 reproduce the reference's sequential order exactly (augmentation only
+// appends columns, so "U_q after fill f" is a prefix of the final U_q).
+#pragma once
+#include "common.cuh"
+
+namespace ifmm {
+
+enum FillKind : int { FILL_HYBRID = 0, FILL_P2P = 1 };
+
+struct FillDesc {
+  int kind, p, q;
+  double* F;    // fill block; F(a,b) = transF ? F[b + a*ldF] : F[a + b*ldF]
+  int ldF, transF;
+  int rows, cols;  // hybrid: r_p x n_q ; P2P: n_p x n_q
+  int n_p, n_q;
+  double* Up;   // n_p x cap (ld n_p)
+  double* Uq;   // n_q x cap (ld n_q)
+  double* M;    // M2L(p,q) storage
+  int ldM, transM;
+  double* out;  // left (rows x Kf) | right (cols x Kf) | sig (Kf)
+  int Kf;       // max crosses / stored rank
+};
+
+struct FillState {
+  int status;  // 0 compressed, 1 kept dense
+  int k, r;    // ACA crosses, recompressed rank
+  int rq, rp;  // basis ranks of q / p right after this fill's augmentation
+  double fro;  // ||left||_F
+};
+
+struct CompressBatch {
+  std::vector<FillDesc> fills;
+  std::vector<int> chain_off, chain;  // hybrid chains (fill indices, sorted by p)
+  std::vector<int> p2p_off, p2p;      // per pivot P2P fills (sorted)
+  std::vector<int> chain_q;           // q of each chain
+};
+
+// Runs K1..K4 on stream s.  rank: device ranks of the level (updated);
+// state: device FillState per fill (out); stats: [compressed, dense_kept, max_rank].
+void run_compression(CompressBatch& cb, double tol, const int* d_probes, int probe_maxm, int* d_rank,
+                     FillState* d_state, int* d_stats, Arena& ws, Staging& st, cudaStream_t s, int debug);
+
+}  // namespace ifmm

@@ -2,6 +2,7 @@
 // factorization.  Device memory is owned by per-handle arenas.
 #pragma once
 #include <memory>
+#include <mutex>
 
 #include "batched.cuh"
 #include "common.cuh"
@@ -61,7 +62,18 @@ struct InitLevel {
   std::vector<int64_t> child_off;      // non-leaf: prefix of child r0 (nc*(2^d+1))
 };
 
+// Device workspaces of factorize(), kept with the store so that repeated
+// factorizations (factor-once/solve-many is per factorization; benchmarks and
+// parameter sweeps refactorize) do not pay cudaMalloc/cudaFree every call.
+struct FactorWork {
+  std::mutex mu;
+  Arena ws{size_t(256) << 20};
+  Staging st;
+  Arena lvl[2] = {Arena(size_t(2) << 30), Arena(size_t(2) << 30)};
+};
+
 struct StoreH {
+  std::unique_ptr<FactorWork> work{new FactorWork};
   TreeH* tree = nullptr;
   KernelParams kp{};
   int p = 8;
@@ -109,7 +121,7 @@ struct FactorH {
   int64_t g_size = 0;                  // sum of record n (per rhs)
   std::vector<int64_t> g_off;          // per record
   int64_t* d_g_off = nullptr;
-  Arena arena{size_t(1) << 30};        // records, top inverse
+  Arena arena{size_t(4) << 30};        // records, top inverse
   cudaStream_t stream = nullptr;
   // timing of the last factorization (ms) and work accounting
   double ms_total = 0;
@@ -118,6 +130,7 @@ struct FactorH {
   // factorize() ran with IFMM_FLAG_TIMING: see PhaseId
   double phase_ms[8] = {0};
   long long phase_launches[8] = {0};
+  int deferred_batches = 0;  // colour batches split by the independence guard
 };
 
 enum PhaseId : int {

@@ -17,11 +17,91 @@ struct CtaShared {
 };
 
 // ------------------------------------------------------------- small helpers
-// Y(rows x cols, ldy) = alpha * op(A) * op(B) + beta*Y, plain FMA loops over
-// the block; used for the small products inside compression.
+// CTA-cooperative DMMA GEMM (mma.sync.m8n8k4.f64): every warp owns 16x16
+// output tiles (2x2 fragments); fragments are loaded straight from L1/L2.
+// One DMMA does 512 flops for 2 loads per lane, vs 2 flops per 2 loads for a
+// scalar loop -- the projections and deltas of the compression are otherwise
+// L1-throughput bound.
+template <bool TA, bool TB>
+__device__ inline void cta_mma_gemm(int rows, int cols, int kk, double alpha, const double* __restrict__ A, int lda,
+                                    const double* __restrict__ B, int ldb, double beta, double* Y, int ldy) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tm = (rows + 15) >> 4, tn = (cols + 15) >> 4;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int tile = warp; tile < tm * tn; tile += nw) {
+    const int i0 = (tile % tm) << 4, j0 = (tile / tm) << 4;
+    double acc[2][2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}};
+    for (int k0 = 0; k0 < kk; k0 += 4) {
+      const int k = k0 + fk;
+      double a[2], b[2];
+#pragma unroll
+      for (int m = 0; m < 2; m++) {
+        const int i = i0 + m * 8 + fr;
+        a[m] = (i < rows && k < kk) ? (TA ? A[k + (size_t)i * lda] : A[i + (size_t)k * lda]) : 0.0;
+      }
+#pragma unroll
+      for (int n = 0; n < 2; n++) {
+        const int j = j0 + n * 8 + fr;
+        b[n] = (j < cols && k < kk) ? (TB ? B[j + (size_t)k * ldb] : B[k + (size_t)j * ldb]) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 2; m++)
+#pragma unroll
+        for (int n = 0; n < 2; n++)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                       : "d"(a[m]), "d"(b[n]));
+    }
+#pragma unroll
+    for (int m = 0; m < 2; m++)
+#pragma unroll
+      for (int n = 0; n < 2; n++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int i = i0 + m * 8 + fr, j = j0 + n * 8 + 2 * fk + h;
+          if (i < rows && j < cols) {
+            double* y = Y + i + (size_t)j * ldy;
+            *y = (beta == 0.0 ? 0.0 : beta * *y) + alpha * acc[m][n][h];
+          }
+        }
+  }
+  __syncthreads();
+}
+
+// Y(rows x cols, ldy) = alpha * op(A) * op(B) + beta*Y for the small products
+// inside compression; DMMA tiles when the shape is worth it.
 // opA: A is (rows x kk) if !ta else stored (kk x rows).
 __device__ inline void cta_gemm(int rows, int cols, int kk, double alpha, const double* A, int lda, bool ta,
                                 const double* B, int ldb, bool tb, double beta, double* Y, int ldy) {
+  if (rows >= 8 && cols >= 8 && kk >= 8) {
+    if (ta) {
+      if (tb) cta_mma_gemm<true, true>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+      else cta_mma_gemm<true, false>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+    } else {
+      if (tb) cta_mma_gemm<false, true>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+      else cta_mma_gemm<false, false>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+    }
+    return;
+  }
+  if (ta && !tb) {
+    // Y = A^T B: both operands are read down contiguous columns -> one warp per
+    // output, lanes stride the contraction (coalesced), warp-shuffle reduction
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int o = warp; o < rows * cols; o += nw) {
+      const int i = o % rows, j = o / rows;
+      const double* a = A + (size_t)i * lda;
+      const double* b = B + (size_t)j * ldb;
+      double s = 0.0;
+      for (int t = lane; t < kk; t += 32) s = fma(a[t], b[t], s);
+      s = warp_sum(s);
+      if (lane == 0) {
+        double* y = Y + i + (size_t)j * ldy;
+        *y = (beta == 0.0 ? 0.0 : beta * *y) + alpha * s;
+      }
+    }
+    __syncthreads();
+    return;
+  }
   for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
     const int i = e % rows, j = e / rows;
     double s = 0.0;

@@ -24,241 +24,10 @@
 #include <cmath>
 
 #include "core.cuh"
+#include "compress.cuh"
 #include "cta_la.cuh"
 
 namespace ifmm {
-
-// ------------------------------------------------------------------ compression kernel
-enum FillKind : int { FILL_HYBRID = 0, FILL_P2P = 1 };
-
-struct FillDesc {
-  int kind, p, q;
-  double* F;     // fill block
-  int ldF, transF;
-  int n_p, n_q;
-  double* Up;    // n_p x cap (ld n_p)
-  double* Uq;    // n_q x cap (ld n_q)
-  double* M;     // M2L(p,q) storage
-  int ldM, transM;
-};
-
-struct PivotWork {
-  int f0, f1;
-  double* scratch;
-  int MX, K;
-};
-
-struct CompressParams {
-  double tol;          // ACA / truncation tolerance
-  const int* probes;   // (maxm+1) x 10 probe table
-  int probe_maxm;
-  int* rank;           // level ranks (device)
-  int* status;         // per fill: 0 compressed, 1 kept dense
-  int* stats;          // [compressed, dense_kept, max_rank]
-  int debug;
-};
-
-__device__ inline void fill_zero(const FillDesc& D, int rows, int cols) {
-  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
-    const int a = e % rows, b = e / rows;
-    if (D.transF) D.F[b + (size_t)a * D.ldF] = 0.0;
-    else D.F[a + (size_t)b * D.ldF] = 0.0;
-  }
-}
-
-// M2L(p,q) += X E^T  (X: rows x r, ld ldx ; E: cols x r, ld lde)
-__device__ inline void m2l_add_product(const FillDesc& D, const double* X, int ldx, const double* E, int lde, int rows,
-                                       int cols, int r) {
-  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
-    const int a = e % rows, b = e / rows;
-    double v = 0.0;
-    for (int t = 0; t < r; t++) v = fma(X[a + (size_t)t * ldx], E[b + (size_t)t * lde], v);
-    if (D.transM) D.M[b + (size_t)a * D.ldM] += v;
-    else D.M[a + (size_t)b * D.ldM] += v;
-  }
-}
-
-// New orthonormal directions of X (nU x r, in H) outside U (nU x rU), weighted
-// by `wsig` (per-column scale, or null for identity), appended to U.
-// Follows ifmm/solver.py:334-358 using the identity sv(M)=sv(res*diag(sig)).
-// Returns number of appended columns.
-__device__ int new_dirs_append(double* H, int nU, int r, double* U, int rU, const double* wsig, double cutoff,
-                               double* E, double* sig2, int* ord2, CtaShared& sh) {
-  const int cap = nU - rU;
-  if (cap <= 0 || r == 0) return 0;
-  cta_project_out(H, nU, nU, r, U, nU, rU, E);
-  cta_project_out(H, nU, nU, r, U, nU, rU, E);
-  if (wsig)
-    for (int e = threadIdx.x; e < nU * r; e += blockDim.x) H[e] *= wsig[e / nU];
-  __syncthreads();
-  cta_jacobi(H, nU, r, nU, nullptr, 0, sig2, ord2, sh);
-  int w = 0;
-  for (int t = 0; t < r; t++) w += (sig2[ord2[t]] > cutoff);
-  w = min(w, cap);
-  double* W = U + (size_t)rU * nU;
-  for (int e = threadIdx.x; e < nU * w; e += blockDim.x) {
-    const int i = e % nU, c = e / nU;
-    const int col = ord2[c];
-    W[i + (size_t)c * nU] = H[i + (size_t)col * nU] / sig2[col];
-  }
-  __syncthreads();
-  if (w > 0) cta_project_out(W, nU, nU, w, U, nU, rU, E);
-  return w;
-}
-
-__global__ void __launch_bounds__(256) compress_kernel(const FillDesc* __restrict__ fills,
-                                                       const PivotWork* __restrict__ work, CompressParams P) {
-  __shared__ CtaShared sh;
-  const PivotWork Wk = work[blockIdx.x];
-  const int MX = Wk.MX, K = Wk.K;
-  double* s = Wk.scratch;
-  double* Uc = s; s += (size_t)MX * K;
-  double* Vc = s; s += (size_t)MX * K;
-  double* left = s; s += (size_t)MX * K;
-  double* right = s; s += (size_t)MX * K;
-  double* H = s; s += (size_t)MX * K;
-  double* E1 = s; s += (size_t)MX * K;
-  double* E2 = s; s += (size_t)MX * K;
-  double* Rl = s; s += (size_t)K * K;
-  double* Rr = s; s += (size_t)K * K;
-  double* core = s; s += (size_t)K * K;
-  double* Jv = s; s += (size_t)K * K;
-  double* rr = s; s += MX;
-  double* cc = s; s += MX;
-  double* sig = s; s += MX + K;
-  double* sig2 = s; s += MX + K;
-  double* dots = s; s += K;
-  double* vv = s; s += K;
-  int* usedr = reinterpret_cast<int*>(s); s += MX;
-  int* usedc = reinterpret_cast<int*>(s); s += MX;
-  int* ord = reinterpret_cast<int*>(s); s += MX + K;
-  int* ord2 = reinterpret_cast<int*>(s); s += MX + K;
-  const double tol = P.tol;
-  for (int f = Wk.f0; f < Wk.f1; f++) {
-    const FillDesc D = fills[f];
-    const int rows = D.kind == FILL_HYBRID ? P.rank[D.p] : D.n_p;
-    const int cols = D.n_q;
-    if (rows == 0 || cols == 0) {
-      if (threadIdx.x == 0) {
-        P.status[f] = 0;
-        atomicAdd(&P.stats[0], 1);
-      }
-      __syncthreads();
-      continue;
-    }
-    if (tol == 0.0) {
-      // exact mode: bases are identities, the redirected fill is F itself
-      double mx = 0.0;
-      for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
-        const int a = e % rows, b = e / rows;
-        mx = fmax(mx, fabs(Fat(D.F, D.ldF, D.transF, a, b)));
-      }
-      mx = block_sum(mx > 0.0 ? 1.0 : 0.0, sh.red);
-      for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
-        const int a = e % rows, b = e / rows;
-        const double v = Fat(D.F, D.ldF, D.transF, a, b);
-        if (D.transM) D.M[b + (size_t)a * D.ldM] += v;
-        else D.M[a + (size_t)b * D.ldM] += v;
-      }
-      __syncthreads();
-      fill_zero(D, rows, cols);
-      if (threadIdx.x == 0) {
-        P.status[f] = 0;
-        atomicAdd(&P.stats[0], 1);
-        atomicMax(&P.stats[2], mx > 0.0 ? min(rows, cols) : 0);
-      }
-      __syncthreads();
-      continue;
-    }
-    const int mrow = rows < P.probe_maxm ? rows : P.probe_maxm;
-    const int* probes = P.probes + (size_t)mrow * 10;
-    const int nprobe = min(10, rows);
-    AcaOut ao = cta_aca(D.F, D.ldF, D.transF, rows, cols, tol, probes, nprobe, Uc, Vc, K, rr, cc, usedr, usedc, dots,
-                        sh);
-    const int k = ao.k;
-    const int full = min(rows, cols);
-    if (!ao.converged && (k >= full || k >= K)) {
-      if (threadIdx.x == 0) {
-        P.status[f] = 1;
-        atomicAdd(&P.stats[1], 1);
-      }
-      __syncthreads();
-      continue;
-    }
-    int r = 0;
-    if (k > 0) {
-      // recompression: QR of both factors, SVD of the core (ifmm/lowrank.py:164-171)
-      cta_qr(Uc, rows, k, rows, Rl, left, rows, vv, sh);   // left <- Ql (rows x k)
-      cta_qr(Vc, cols, k, cols, Rr, right, cols, vv, sh);  // right <- Qr (cols x k)
-      cta_gemm(k, k, k, 1.0, Rl, k, false, Rr, k, true, 0.0, core, k);
-      cta_jacobi(core, k, k, k, Jv, k, sig, ord, sh);
-      r = trunc_rank_dev(sig, ord, k, tol);
-      // Uc <- Ql * core(:, ord[:r]) ; Vc <- Qr * Jv(:, ord[:r])
-      for (int e = threadIdx.x; e < rows * r; e += blockDim.x) {
-        const int i = e % rows, c = e / rows;
-        const int col = ord[c];
-        double acc = 0.0;
-        for (int t = 0; t < k; t++) acc = fma(left[i + (size_t)t * rows], core[t + (size_t)col * k], acc);
-        Uc[i + (size_t)c * rows] = acc;
-      }
-      for (int e = threadIdx.x; e < cols * r; e += blockDim.x) {
-        const int i = e % cols, c = e / cols;
-        const int col = ord[c];
-        double acc = 0.0;
-        for (int t = 0; t < k; t++) acc = fma(right[i + (size_t)t * cols], Jv[t + (size_t)col * k], acc);
-        Vc[i + (size_t)c * cols] = acc;
-      }
-      for (int c = threadIdx.x; c < r; c += blockDim.x) dots[c] = sig[ord[c]];
-      __syncthreads();
-    }
-    // A = Uc (rows x r), B = Vc (cols x r, orthonormal), dots = singular values
-    double fro = 0.0;
-    for (int e = threadIdx.x; e < rows * r; e += blockDim.x) fro += Uc[e] * Uc[e];
-    fro = sqrt(block_sum(fro, sh.red));
-    const double cutoff = tol * fro;
-    if (threadIdx.x == 0) {
-      P.status[f] = (k << 8) | (r << 20);  // low byte 0: compressed; ranks kept for diagnostics
-      atomicAdd(&P.stats[0], 1);
-      atomicMax(&P.stats[2], r);
-    }
-    if (r > 0) {
-      // q side: directions of B weighted by A
-      int rq = P.rank[D.q];
-      for (int e = threadIdx.x; e < cols * r; e += blockDim.x) H[e] = Vc[e];
-      __syncthreads();
-      int wq = new_dirs_append(H, cols, r, D.Uq, rq, dots, cutoff, E1, sig2, ord2, sh);
-      rq += wq;
-      __syncthreads();
-      if (threadIdx.x == 0) P.rank[D.q] = rq;
-      int rp = D.kind == FILL_HYBRID ? rows : P.rank[D.p];
-      if (D.kind == FILL_P2P) {
-        for (int e = threadIdx.x; e < rows * r; e += blockDim.x) H[e] = Uc[e];
-        __syncthreads();
-        int wp = new_dirs_append(H, rows, r, D.Up, rp, nullptr, cutoff, E1, sig2, ord2, sh);
-        rp += wp;
-        __syncthreads();
-        if (threadIdx.x == 0) P.rank[D.p] = rp;
-        if (P.debug && threadIdx.x == 0) printf("aug p=%d +%d -> %d\n", D.p, wp, rp);
-      }
-      if (P.debug && threadIdx.x == 0)
-        printf("augq fill=%d kind=%d p=%d q=%d r=%d +%d -> %d fro=%.6e\n", f, D.kind, D.p, D.q, r, wq, rq, fro);
-      __syncthreads();
-      // E2 = Uq^T B (rq x r)
-      cta_gemm(rq, r, cols, 1.0, D.Uq, cols, true, Vc, cols, false, 0.0, E2, rq);
-      if (D.kind == FILL_HYBRID) {
-        // delta = A E2^T (rows x rq)
-        m2l_add_product(D, Uc, rows, E2, rq, rows, rq, r);
-      } else {
-        // delta = (Up^T A)(Uq^T B)^T  (rp x rq)
-        cta_gemm(rp, r, rows, 1.0, D.Up, rows, true, Uc, rows, false, 0.0, H, rp);
-        m2l_add_product(D, H, rp, E2, rq, rp, rq, r);
-      }
-      __syncthreads();
-    }
-    fill_zero(D, rows, cols);
-    __syncthreads();
-  }
-}
 
 // ------------------------------------------------------------------ work level
 struct WorkLevel {
@@ -344,7 +113,14 @@ struct PhaseTimer {
 class Factorizer {
  public:
   Factorizer(StoreH* S, double tol, int flags, double cond_limit)
-      : S_(S), t_(S->tree), tol_(tol), flags_(flags), cond_limit_(cond_limit) {}
+      : S_(S),
+        t_(S->tree),
+        tol_(tol),
+        flags_(flags),
+        cond_limit_(cond_limit),
+        ws_(S->work->ws),
+        st_(S->work->st),
+        lvl_arena_(S->work->lvl) {}
   FactorH* run();
 
  private:
@@ -355,10 +131,10 @@ class Factorizer {
   double cond_limit_;  // PIVOT_CONDITION_LIMIT (ifmm/solver.py:50), 1e12 by default
   cudaStream_t s_ = nullptr;
   std::unique_ptr<FactorH> F_;
-  Arena ws_{size_t(256) << 20};
-  Staging st_;
+  Arena& ws_;
+  Staging& st_;
+  Arena* lvl_arena_;  // [2], alternating between levels
   PhaseTimer tm_;
-  Arena lvl_arena_[2] = {Arena(size_t(512) << 20), Arena(size_t(512) << 20)};
   WorkLevel cur_, prev_;
   // per-record host metadata for pos resolution at level end
   struct SlotRef { int kind, j, dim; };  // kind 0: x_j, 1: y_j
@@ -415,9 +191,40 @@ class Factorizer {
     W.U.assign(W.nc, nullptr);
     W.d_rank = W.arena->alloc_n<int>(W.nc);
   }
+  std::vector<int> mark_;
+  int stamp_ = 0;
+  // x-partners (live, coupled through P2P) and y-partners (eliminated, coupled
+  // through M2P = P2L^T) of i, sorted (ifmm/solver.py:220-229); scans the 7x7 window
+  void partners(WorkLevel& W, int i, std::vector<int>& xp, std::vector<int>& yp) {
+    const Topo& T = *W.T;
+    const int dim = T.dim, k = W.k;
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int d = 0; d < dim; d++) {
+      lo[d] = std::max(0, T.grid[i * dim + d] - 3);
+      hi[d] = std::min((1 << k) - 1, T.grid[i * dim + d] + 3);
+    }
+    std::vector<int> cand;
+    int g[3];
+    for (g[0] = lo[0]; g[0] <= hi[0]; g[0]++)
+      for (g[1] = lo[1]; g[1] <= hi[1]; g[1]++)
+        for (g[2] = lo[2]; g[2] <= hi[2]; g[2]++) {
+          int64_t c = 0;
+          for (int b = 0; b < k; b++)
+            for (int ax = 0; ax < dim; ax++) c |= int64_t((g[ax] >> b) & 1) << (b * dim + ax);
+          cand.push_back(int(c));
+        }
+    std::sort(cand.begin(), cand.end());
+    xp.clear();
+    yp.clear();
+    for (int j : cand) {
+      if (j == i) continue;
+      if (!W.dead[j] && pp_present(W, i, j)) xp.push_back(j);
+      if (pres(W.px, W, i, j)) yp.push_back(j);
+    }
+  }
   void start_leaf_level();
   void start_parent_level(WorkLevel& C, int k);
-  void eliminate_batch(std::vector<int>& piv, int colour);
+  void eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred);
   void finish_level(int rec_begin);
   void factor_top();
 };
@@ -514,10 +321,37 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
   launch_copies(cb, ws_, st_, s_);
 }
 
-void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
+void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred) {
   WorkLevel& W = cur_;
   const Topo& T = *W.T;
   const int k = W.k;
+  // Independence guard: a batch may only contain eliminations whose touched
+  // sets {i} u partners(i) are pairwise disjoint (true for the 9-colouring as
+  // long as every partner is a neighbour; an incompressible well-separated
+  // fill kept dense can break it).  Conflicting pivots are deferred to a
+  // follow-up batch of the same colour, preserving their relative order.
+  {
+    std::vector<int> keep;
+    deferred.clear();
+    if (mark_.size() != size_t(W.nc)) mark_.assign(W.nc, -1);
+    ++stamp_;
+    for (int i : piv) {
+      std::vector<int> xp, yp;
+      partners(W, i, xp, yp);
+      bool clash = mark_[i] == stamp_;
+      for (int j : xp) clash |= mark_[j] == stamp_;
+      for (int j : yp) clash |= mark_[j] == stamp_;
+      if (clash) {
+        deferred.push_back(i);
+        continue;
+      }
+      mark_[i] = stamp_;
+      for (int j : xp) mark_[j] = stamp_;
+      for (int j : yp) mark_[j] = stamp_;
+      keep.push_back(i);
+    }
+    piv.swap(keep);
+  }
   const int np = int(piv.size());
   CK(cudaStreamSynchronize(s_));  // staging buffers of earlier uploads are free after this
   ws_.reset();
@@ -539,32 +373,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
     I.n = W.n[i];
     I.r = W.r[i];
     I.m = I.n + I.r;
-    // partners: scan the 7x7 window of i
-    std::vector<int> cand;
-    {
-      // enumerate window members of i
-      const int dim = T.dim;
-      int lo[3], hi[3];
-      for (int d = 0; d < dim; d++) {
-        lo[d] = std::max(0, T.grid[i * dim + d] - 3);
-        hi[d] = std::min((1 << k) - 1, T.grid[i * dim + d] + 3);
-      }
-      int g[3];
-      for (g[0] = lo[0]; g[0] <= hi[0]; g[0]++)
-        for (g[1] = (dim > 1 ? lo[1] : 0); g[1] <= (dim > 1 ? hi[1] : 0); g[1]++)
-          for (g[2] = (dim > 2 ? lo[2] : 0); g[2] <= (dim > 2 ? hi[2] : 0); g[2]++) {
-            int64_t c = 0;
-            for (int b = 0; b < k; b++)
-              for (int ax = 0; ax < dim; ax++) c |= int64_t((g[ax] >> b) & 1) << (b * dim + ax);
-            cand.push_back(int(c));
-          }
-      std::sort(cand.begin(), cand.end());
-    }
-    for (int j : cand) {
-      if (j == i) continue;
-      if (!W.dead[j] && pp_present(W, i, j)) I.xp.push_back(j);
-      if (pres(W.px, W, i, j)) I.yp.push_back(j);
-    }
+    partners(W, i, I.xp, I.yp);
     I.soff.assign(1, 0);
     for (int j : I.xp) I.soff.push_back(I.soff.back() + W.n[j]);
     for (int j : I.yp) I.soff.push_back(I.soff.back() + W.r[j]);
@@ -614,7 +423,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   {
     int maxm = 0;
     for (auto& d : md) maxm = std::max(maxm, d.m);
-    launch_norm1_estimate(dmd, np, maxm, d_nSi, s_);
+    launch_norm1(dmd, np, d_nSi, s_);
+    launch_norm1_estimate(dmd, np, maxm, d_nSi, d_nS, cond_limit_, s_);
   }
   // records + X = S^-1 C
   GemmBatch gb;
@@ -694,72 +504,96 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
   tm_.end();
-  // fill-in compression lists (reference order: hybrid pairs sorted, then P2P pairs sorted)
-  std::vector<FillDesc> fd;
-  std::vector<PivotWork> pw(np);
+  // fill-in compression (reference order: hybrid pairs sorted, then P2P pairs sorted)
+  CompressBatch cbz;
+  cbz.chain_off.assign(1, 0);
+  cbz.p2p_off.assign(1, 0);
   struct FillHost { int kind, p, q; };
   std::vector<FillHost> fh;
+  auto add_fill = [&](int kind, int p, int q) {
+    FillDesc D{};
+    D.kind = kind;
+    D.p = p;
+    D.q = q;
+    if (kind == FILL_HYBRID) {
+      BlkRef F = xy_ref(W, q, p, false);
+      D.F = F.p;
+      D.ldF = W.n[q];
+      D.transF = 1;
+      D.rows = W.r[p];
+    } else {
+      BlkRef F = p2p_ref(W, p, q, false);
+      D.F = F.p;
+      D.ldF = F.ld;
+      D.transF = 0;
+      D.rows = W.n[p];
+    }
+    D.cols = W.n[q];
+    D.n_p = W.n[p];
+    D.n_q = W.n[q];
+    D.Up = W.U[p];
+    D.Uq = W.U[q];
+    BlkRef M = m2l_ref(W, p, q, true);
+    D.M = M.p;
+    D.ldM = M.ld;
+    D.transM = M.trans ? 1 : 0;
+    D.Kf = std::max(1, std::min(96, std::min(D.rows, D.cols)));
+    D.out = ws_.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
+    cbz.fills.push_back(D);
+    fh.push_back({kind, p, q});
+    return int(cbz.fills.size()) - 1;
+  };
   for (int t = 0; t < np; t++) {
     PivInfo& I = P[t];
-    pw[t].f0 = int(fd.size());
     std::vector<int> ps(I.yp);
     ps.push_back(I.i);
     std::sort(ps.begin(), ps.end());
-    int MX = 1, K = 1;
+    std::vector<std::vector<int>> byq(I.xp.size());
     for (int p : ps)
-      for (int q : I.xp) {
-        if (!T.in_il(p, q)) continue;
-        BlkRef F = xy_ref(W, q, p, false);
-        BlkRef M = m2l_ref(W, p, q, true);
-        FillDesc D{FILL_HYBRID, p, q, F.p, W.n[q], 1, W.n[p], W.n[q], W.U[p], W.U[q], M.p, M.ld, M.trans ? 1 : 0};
-        fd.push_back(D);
-        fh.push_back({FILL_HYBRID, p, q});
-        MX = std::max(MX, std::max(W.n[p], W.n[q]));
-        K = std::max(K, std::min(W.n[p], W.n[q]));
+      for (size_t u = 0; u < I.xp.size(); u++)
+        if (T.in_il(p, I.xp[u])) byq[u].push_back(add_fill(FILL_HYBRID, p, I.xp[u]));
+    for (size_t u = 0; u < I.xp.size(); u++)
+      if (!byq[u].empty()) {
+        cbz.chain.insert(cbz.chain.end(), byq[u].begin(), byq[u].end());
+        cbz.chain_off.push_back(int(cbz.chain.size()));
+        cbz.chain_q.push_back(I.xp[u]);
       }
     for (size_t a = 0; a < I.xp.size(); a++)
-      for (size_t b = a + 1; b < I.xp.size(); b++) {
-        int p = I.xp[a], q = I.xp[b];
-        if (!T.in_il(p, q)) continue;
-        BlkRef F = p2p_ref(W, p, q, false);
-        BlkRef M = m2l_ref(W, p, q, true);
-        FillDesc D{FILL_P2P, p, q, F.p, F.ld, 0, W.n[p], W.n[q], W.U[p], W.U[q], M.p, M.ld, M.trans ? 1 : 0};
-        fd.push_back(D);
-        fh.push_back({FILL_P2P, p, q});
-        MX = std::max(MX, std::max(W.n[p], W.n[q]));
-        K = std::max(K, std::min(W.n[p], W.n[q]));
-      }
-    pw[t].f1 = int(fd.size());
-    K = std::min(K, 96);
-    pw[t].MX = MX;
-    pw[t].K = K;
-    const size_t per = 7 * size_t(MX) * K + 4 * size_t(K) * K + 2 * MX + 2 * (MX + K) + 2 * K + 4 * (MX + K) + 64;
-    pw[t].scratch = pw[t].f1 > pw[t].f0 ? ws_.alloc_n<double>(per) : nullptr;
+      for (size_t b = a + 1; b < I.xp.size(); b++)
+        if (T.in_il(I.xp[a], I.xp[b])) cbz.p2p.push_back(add_fill(FILL_P2P, I.xp[a], I.xp[b]));
+    cbz.p2p_off.push_back(int(cbz.p2p.size()));
   }
-  int* d_status = ws_.alloc_n<int>(std::max<size_t>(1, fd.size()));
+  const size_t nfill = cbz.fills.size();
+  FillState* d_state = ws_.alloc_n<FillState>(std::max<size_t>(1, nfill));
   int* d_stats = ws_.alloc_n<int>(4);
   CK(cudaMemsetAsync(d_stats, 0, 16, s_));
-  if (!fd.empty()) {
-    tm_.begin(PH_COMPRESS);
-    const FillDesc* dfd = upload(ws_, fd, s_, st_);
-    const PivotWork* dpw = upload(ws_, pw, s_, st_);
-    CompressParams cp{tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_status, d_stats,
-                      getenv("IFMM_DEBUG") != nullptr ? 1 : 0};
-    compress_kernel<<<np, 256, 0, s_>>>(dfd, dpw, cp);
-    CK_LAUNCH();
-  }
+  static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
+  tm_.begin(PH_COMPRESS);
+  run_compression(cbz, tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_state, d_stats, ws_, st_, s_, dbg ? 1 : 0);
   tm_.end();
   // read back: pivot conditioning, ranks, fill outcomes, counters
   std::vector<double> nS(np), nSi(np);
-  std::vector<int> info(np), status(fd.size()), stats(4);
+  std::vector<int> info(np), stats(4);
+  std::vector<FillState> state(nfill);
   CK(cudaMemcpyAsync(nS.data(), d_nS, sizeof(double) * np, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(nSi.data(), d_nSi, sizeof(double) * np, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(info.data(), d_info, sizeof(int) * np, cudaMemcpyDeviceToHost, s_));
-  if (!fd.empty()) CK(cudaMemcpyAsync(status.data(), d_status, sizeof(int) * fd.size(), cudaMemcpyDeviceToHost, s_));
+  if (nfill) CK(cudaMemcpyAsync(state.data(), d_state, sizeof(FillState) * nfill, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(stats.data(), d_stats, 16, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(W.r.data(), W.d_rank, sizeof(int) * W.nc, cudaMemcpyDeviceToHost, s_));
   CK(cudaStreamSynchronize(s_));
   tm_.collect(F_.get());
+  if (getenv("IFMM_COND_LOG")) {
+    double mx = 0, sum = 0;
+    int imx = -1, mmx = 0;
+    for (int t = 0; t < np; t++) {
+      double c = nS[t] * nSi[t];
+      sum += std::log10(std::max(c, 1.0));
+      if (c > mx) { mx = c; imx = P[t].i; mmx = P[t].m; }
+    }
+    fprintf(stderr, "cond level=%d colour=%d pivots=%d max=%.3e (cluster %d, m=%d) geo-mean=%.3e\n", k, colour, np, mx,
+            imx, mmx, std::pow(10.0, sum / np));
+  }
   for (int t = 0; t < np; t++) {
     double rc = (info[t] != 0) ? 0.0 : 1.0 / (nS[t] * nSi[t]);
     if (!std::isfinite(rc) || rc <= 1.0 / cond_limit_) {
@@ -786,12 +620,11 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour) {
   LS.compressed += stats[0];
   LS.dense_kept += stats[1];
   LS.max_rank = std::max(LS.max_rank, stats[2]);
-  static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
   for (size_t f = 0; f < fh.size(); f++) {
     if (dbg)
       fprintf(stderr, "fill k=%d kind=%d p=%d q=%d status=%d aca=%d rank=%d rank_p=%d\n", k, fh[f].kind, fh[f].p,
-              fh[f].q, status[f] & 0xff, (status[f] >> 8) & 0xfff, status[f] >> 20, W.r[fh[f].p]);
-    if ((status[f] & 0xff) != 0) continue;
+              fh[f].q, state[f].status, state[f].k, state[f].r, W.r[fh[f].p]);
+    if (state[f].status != 0) continue;
     const FillHost& h = fh[f];
     if (h.kind == FILL_HYBRID) pres(W.px, W, h.q, h.p) = 0;
     else set_pp(W, h.p, h.q, 0);
@@ -908,10 +741,14 @@ FactorH* Factorizer::run() {
       std::vector<int> piv;
       for (int i = 0; i < cur_.nc; i++)
         if (cur_.T->colour[i] == c) piv.push_back(i);
-      if (piv.empty()) continue;
-      const int r0 = int(F_->recs.size());
-      eliminate_batch(piv, c);
-      F_->batches.push_back(BatchH{k, c, r0, int(F_->recs.size()), nullptr, 0, 0});
+      std::vector<int> deferred;
+      while (!piv.empty()) {
+        const int r0 = int(F_->recs.size());
+        eliminate_batch(piv, c, deferred);
+        F_->batches.push_back(BatchH{k, c, r0, int(F_->recs.size()), nullptr, 0, 0});
+        if (!deferred.empty()) F_->deferred_batches++;
+        piv.swap(deferred);
+      }
     }
     finish_level(rec_begin);
     F_->r_m = std::max(F_->r_m, F_->stats[k].max_rank);
@@ -935,8 +772,7 @@ FactorH* Factorizer::run() {
   CK(cudaMemcpyAsync(F_->d_g_off, F_->g_off.data(), sizeof(int64_t) * F_->g_off.size(), cudaMemcpyHostToDevice, s_));
   CK(cudaStreamSynchronize(s_));
   cur_ = WorkLevel{};
-  lvl_arena_[0].release();
-  lvl_arena_[1].release();
+  // level arenas stay allocated with the store (zeroed again on next reset)
   F_->fl_exec += F_->fl_schur;
   F_->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return F_.release();
@@ -944,6 +780,7 @@ FactorH* Factorizer::run() {
 
 FactorH* factorize(StoreH* S, double tol, int flags, double cond_limit) {
   ensure_device();
+  std::lock_guard<std::mutex> lock(S->work->mu);  // one factorization per store at a time
   Factorizer f(S, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12);
   return f.run();
 }
