@@ -116,6 +116,12 @@ int ifmm_factor_timing(const ifmm_factor* f, double* ms7, int64_t* launches7);
 int64_t ifmm_launch_count(void);
 /* solve(fact, rhs) (ifmm/solver.py:549-626) for nrhs >= 1 columns */
 int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int ptr_kind);
+/* solve + iterative refinement with the store's compressed FMM operator
+ * (an extension; the reference solves once): x <- x + solve(b - A~ x) until
+ * ||b - A~ x|| / ||b|| <= target or max_iters refinement steps.  hist
+ * (max_iters + 1 doubles, may be null) receives the residual after each step. */
+int ifmm_solve_refined(ifmm_factor* f, ifmm_store* s, const double* rhs, double* x, int64_t nrhs, int ptr_kind,
+                       int max_iters, double target, double* hist, int* iters_done);
 void ifmm_factor_free(ifmm_factor* f);
 
 /* ---- test hooks for the batched kernels (host arrays in/out) */

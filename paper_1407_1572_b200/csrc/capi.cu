@@ -270,6 +270,15 @@ int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int p
   return guard([&] { ifmm::solve(f->h, rhs, x, nrhs, ptr_kind == IFMM_PTR_DEVICE); });
 }
 
+int ifmm_solve_refined(ifmm_factor* f, ifmm_store* s, const double* rhs, double* x, int64_t nrhs, int ptr_kind,
+                       int max_iters, double target, double* hist, int* iters_done) {
+  return guard([&] {
+    if (!f || !s) invalid("null handle");
+    if (s->h != f->h->store) invalid("store does not belong to this factorization");
+    ifmm::solve_refined(f->h, s->h, rhs, x, nrhs, ptr_kind == IFMM_PTR_DEVICE, max_iters, target, hist, iters_done);
+  });
+}
+
 void ifmm_factor_free(ifmm_factor* f) {
   if (!f) return;
   delete f->h;

@@ -151,6 +151,8 @@ StoreH* store_init(TreeH* t, const KernelParams& kp, int p, double tol, const in
 void matvec(StoreH* s, const double* x, double* y, int64_t nrhs, bool device_ptr);
 FactorH* factorize(StoreH* s, double tol, int flags, double cond_limit);
 void solve(FactorH* f, const double* rhs, double* x, int64_t nrhs, bool device_ptr);
+void solve_refined(FactorH* F, StoreH* S, const double* rhs, double* x, int64_t nrhs, bool device_ptr, int iters,
+                   double target, double* hist, int* done);
 
 // ------------------------------------------------------------ shared helpers
 cudaStream_t default_stream();

@@ -8,6 +8,7 @@
 // Vectors are (positions x nrhs) row-major; a level's y slots alias the next
 // level's x slots.
 #include <algorithm>
+#include <cmath>
 
 #include "core.cuh"
 
@@ -62,6 +63,75 @@ __global__ void __launch_bounds__(256) solve_bwd_kernel(const RecordH* __restric
     for (int c = 0; c < w; c++) s = fma(-R.xtop[t + (size_t)c * n], sv[c * nrhs + q], s);
     V[(R.xoff + t) * nrhs + q] = s;
   }
+}
+
+// ------------------------------------------------------------------ refinement
+__global__ void resid_kernel(const double* __restrict__ b, double* __restrict__ r, int64_t n, double* sums) {
+  // r = b - r ; sums[0] += |r|^2, sums[1] += |b|^2
+  __shared__ double red[32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = b[i] - r[i];
+    r[i] = v;
+    s0 += v * v;
+    s1 += b[i] * b[i];
+  }
+  s0 = block_sum(s0, red);
+  s1 = block_sum(s1, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&sums[0], s0);
+    atomicAdd(&sums[1], s1);
+  }
+}
+
+__global__ void axpy_kernel(double* __restrict__ x, const double* __restrict__ dx, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += dx[i];
+}
+
+void matvec(StoreH* S, const double* x, double* y, int64_t nrhs, bool device_ptr);
+
+// Iterative refinement with the compressed FMM operator of the store:
+// x <- x + IFMM^-1 (b - A~ x).  Each step divides the residual by the
+// factorization's relative error; hist[j] = ||b - A~ x_j|| / ||b||.
+void solve_refined(FactorH* F, StoreH* S, const double* rhs, double* x, int64_t nrhs, bool device_ptr, int iters,
+                   double target, double* hist, int* done) {
+  const int64_t n = int64_t(F->tree->N) * nrhs;
+  cudaStream_t s = F->stream;
+  Arena ws(size_t(64) << 20);
+  double *db, *dx;
+  if (device_ptr) {
+    db = const_cast<double*>(rhs);
+    dx = x;
+  } else {
+    db = ws.alloc_n<double>(n);
+    dx = ws.alloc_n<double>(n);
+    CK(cudaMemcpyAsync(db, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  }
+  double* r = ws.alloc_n<double>(n);
+  double* d = ws.alloc_n<double>(n);
+  double* sums = ws.alloc_n<double>(2);
+  const int grid = int(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  solve(F, db, dx, nrhs, true);
+  int it = 0;
+  for (;; it++) {
+    matvec(S, dx, r, nrhs, true);
+    CK(cudaMemsetAsync(sums, 0, 16, s));
+    resid_kernel<<<grid, 256, 0, s>>>(db, r, n, sums);
+    CK_LAUNCH();
+    double h[2];
+    CK(cudaMemcpyAsync(h, sums, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double rel = h[1] > 0 ? std::sqrt(h[0] / h[1]) : 0.0;
+    if (hist) hist[it] = rel;
+    if (it >= iters || rel <= target) break;
+    solve(F, r, d, nrhs, true);
+    axpy_kernel<<<grid, 256, 0, s>>>(dx, d, n);
+    CK_LAUNCH();
+  }
+  if (done) *done = it;
+  if (!device_ptr) CK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
 }
 
 void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_ptr) {

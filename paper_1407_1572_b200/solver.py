@@ -53,6 +53,7 @@ class IfmmFactorization:
     top_dim: int = 0
     n_records: int = 0
     factor_ms: float = 0.0
+    last_refinement: list = field(default_factory=list)
 
     @property
     def n(self) -> int:
@@ -119,10 +120,15 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
     return fact
 
 
-def solve(fact: IfmmFactorization, rhs):
+def solve(fact: IfmmFactorization, rhs, refine: int = 0, target: float = 0.0):
     """Solve the factored system (ifmm/solver.py:549-626).  `rhs` is (N,) (as
     the reference) or (N, nrhs); numpy or torch (CUDA tensors stay on device).
-    Returns the solution in original point order."""
+    Returns the solution in original point order.
+
+    refine > 0 (extension): up to `refine` steps of iterative refinement with
+    the store's compressed FMM operator, stopping once the relative residual
+    ||b - A~ x|| / ||b|| <= target; the residual history is left in
+    `fact.last_refinement`."""
     n = fact.tree.n_points
     if isinstance(rhs, np.ndarray) or not type(rhs).__module__.startswith("torch"):
         a = np.asarray(rhs, dtype=float)
@@ -130,7 +136,14 @@ def solve(fact: IfmmFactorization, rhs):
             raise ValueError(f"rhs must have shape ({n},)")
     p_in, kind, nr, keep, is_torch, one_d = _lib.as_input(rhs, n)
     out, p_out = _lib.alloc_output(keep, kind, n, nr, one_d)
-    _lib.check(_lib.lib.ifmm_solve(fact.handle, p_in, p_out, nr, kind))
+    if refine > 0:
+        hist = np.zeros(int(refine) + 1)
+        done = ctypes.c_int()
+        _lib.check(_lib.lib.ifmm_solve_refined(fact.handle, fact.store.handle, p_in, p_out, nr, kind, int(refine),
+                                               float(target), _lib.ptr(hist), ctypes.byref(done)))
+        fact.last_refinement = hist[:done.value + 1].tolist()
+    else:
+        _lib.check(_lib.lib.ifmm_solve(fact.handle, p_in, p_out, nr, kind))
     if is_torch and kind == _lib.PTR_HOST:
         import torch
         out = torch.from_numpy(out)

@@ -22,4 +22,6 @@ for it in range(reps):
     print(f"{name} rep {it}: residual {res:.3e} r_m {fact.r_m} top {fact.top_dim} ms {fact.factor_ms:.1f}", flush=True)
     print("   level stats:", {k: (s.max_rank, s.fillins_compressed, s.fillins_dense_kept)
                               for k, s in fact.level_stats.items()}, flush=True)
+    x2 = ifmm.solve(fact, b, refine=6, target=1e-9)
+    print("   refinement history:", ["%.2e" % v for v in fact.last_refinement], flush=True)
     del fact
