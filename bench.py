@@ -313,6 +313,7 @@ def main():
         "flops": {"exec": work["flops_exec"], "schur": work["flops_schur"], "reference_equiv": work["flops_ref"],
                   "fp64_tflops_step": work["flops_exec"] / t_step / 1e12},
         "phase_ms": {k: round(v[0], 3) for k, v in ph.items()},
+        "phase_ms_by_level": ft.phase_times_by_level,
         "roofline": {"kernel": "grouped_dgemm_kernel<true,false> (Schur update)", "bound": "tensor",
                      "achieved": achieved, "peak": fl_peak, "unit": "TFLOP/s",
                      "frac": (achieved / fl_peak) if achieved else None, "traffic": None,

@@ -112,6 +112,10 @@ int ifmm_factor_work(const ifmm_factor* f, double* out4);
  * 0 gathers/copies, 1 Gauss-Jordan inverses, 2 X = S^-1 C, 3 Schur update,
  * 4 fill-in compression, 5 level transitions, 6 top-level inverse */
 int ifmm_factor_timing(const ifmm_factor* f, double* ms7, int64_t* launches7);
+/* the same per level (level 1 = top-level inverse); ms9[7] = host time spent
+ * preparing the level's batches before their final sync, ms9[8] = time the
+ * host was blocked in those syncs (wall clock, recorded on every run) */
+int ifmm_factor_timing_level(const ifmm_factor* f, int level, double* ms9);
 /* total kernel launches issued by the library since load */
 int64_t ifmm_launch_count(void);
 /* solve(fact, rhs) (ifmm/solver.py:549-626) for nrhs >= 1 columns */
@@ -127,6 +131,8 @@ void ifmm_factor_free(ifmm_factor* f);
 /* ---- test hooks for the batched kernels (host arrays in/out) */
 /* in-place inverse of `count` column-major matrices of sizes m[c], packed */
 int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info);
+/* device time (best of reps, ms) of one batched inverse of the given matrices */
+int ifmm_bench_gj_inverse(const double* a, const int32_t* m, int count, int reps, double* ms);
 /* C = alpha op(A) op(B) + beta C, column-major, one problem */
 int ifmm_test_gemm(int transA, int transB, int M, int N, int K, double alpha, const double* A, int lda,
                    const double* B, int ldb, double beta, double* C, int ldc, int transC);

@@ -61,11 +61,13 @@ SIGNATURES = {
     "ifmm_factor_records": (_i32, [_p, _p]),
     "ifmm_factor_work": (_i32, [_p, _p]),
     "ifmm_factor_timing": (_i32, [_p, _p, _p]),
+    "ifmm_factor_timing_level": (_i32, [_p, _i32, _p]),
     "ifmm_launch_count": (_i64, []),
     "ifmm_solve": (_i32, [_p, _p, _p, _i64, _i32]),
     "ifmm_solve_refined": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _d, _p, _p]),
     "ifmm_factor_free": (None, [_p]),
     "ifmm_test_gj_inverse": (_i32, [_p, _p, _i32, _p]),
+    "ifmm_bench_gj_inverse": (_i32, [_p, _p, _i32, _i32, _p]),
     "ifmm_test_gemm": (_i32, [_i32, _i32, _i32, _i32, _i32, _d, _p, _i32, _p, _i32, _d, _p, _i32, _i32]),
     "ifmm_test_jacobi": (_i32, [_p, _i32, _i32, _p, _p]),
     "ifmm_test_qr": (_i32, [_p, _i32, _i32, _p, _p]),

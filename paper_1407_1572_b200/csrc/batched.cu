@@ -209,98 +209,397 @@ void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, 
 
 // ------------------------------------------------------------------ Gauss-Jordan
 // Panel transform: columns [j, j+b) of every matrix with m > j.
-__global__ void __launch_bounds__(512) gj_panel_kernel(const MatDesc* __restrict__ desc, int j, int b,
-                                                       int* info) {
+// Rows of the panel live in shared memory in their panel-start order; pivoting
+// is tracked as a position <-> row map (no physical swaps), so a column step
+// costs three barriers: candidate argmax, pivot-row preparation, elimination.
+// Outputs: the transformed panel in final row order, ipiv (LAPACK sequential
+// swap semantics, used for the final column unswap), and the list of row
+// moves new[dst] = old[src] (at most 2b) that the other columns must apply.
+struct RowMove {
+  int dst, src;
+};
+
+__global__ void __launch_bounds__(512) gj_panel_kernel(const MatDesc* __restrict__ desc, int j, int b, int* info,
+                                                       RowMove* moves, int* nmoves) {
   extern __shared__ double sm[];
-  __shared__ ArgMax red[32];
+  __shared__ double candv[32];
+  __shared__ int candr[32], candp[32];
+  __shared__ double prow[64];
+  __shared__ int s_cnt;
   const MatDesc D = desc[blockIdx.x];
   const int m = D.m;
   if (m <= j) return;
   const int bb = min(b, m - j);
   const int ld = bb + 1;  // odd row stride: conflict-free per-row access
-  double* P = sm;         // P[r*ld + c] = A(r, j+c)
-  for (int c = 0; c < bb; c++)
-    for (int r = threadIdx.x; r < m; r += blockDim.x) P[r * ld + c] = D.A[r + (size_t)(j + c) * D.lda];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  double* P = sm;                                   // P[r*ld + c] = A(r, j+c), r = panel-start row
+  int* pos = reinterpret_cast<int*>(P + (size_t)m * ld);  // row -> current position
+  int* at = pos + m;                                // position -> row
+  // load: every thread issues all bb loads of its rows back to back
+  for (int r = tid; r < m; r += nt) {
+    const double* src = D.A + r;
+#pragma unroll 8
+    for (int c = 0; c < bb; c++) P[r * ld + c] = src[(size_t)(j + c) * D.lda];
+    pos[r] = r;
+    at[r] = r;
+  }
+  if (tid == 0) s_cnt = 0;
   __syncthreads();
-  __shared__ int s_piv;
-  __shared__ double s_inv;
   for (int c = 0; c < bb; c++) {
     const int jc = j + c;
-    ArgMax am{-1.0, -1};
-    for (int r = jc + threadIdx.x; r < m; r += blockDim.x) am = argmax_merge(am, ArgMax{fabs(P[r * ld + c]), r});
-    am = block_argmax(am, red);
-    if (threadIdx.x == 0) {
-      int p = am.i < 0 ? jc : am.i;
-      s_piv = p;
-      D.ipiv[jc] = p;
-      double pv = P[p * ld + c];
-      if (pv == 0.0 || pv != pv) {
-        if (info[blockIdx.x] == 0) info[blockIdx.x] = jc + 1;
-        s_inv = 0.0;
-      } else {
-        s_inv = 1.0 / pv;
+    // (1) candidates among rows not yet used as pivots (position >= jc);
+    // ties -> smallest position (idamax on the swapped order)
+    double bv = -1.0;
+    int br = -1, bp = 0x7fffffff;
+    for (int r = tid; r < m; r += nt) {
+      const int pr = pos[r];
+      if (pr < jc) continue;
+      const double v = fabs(P[r * ld + c]);
+      if (v > bv || (v == bv && pr < bp)) { bv = v; br = r; bp = pr; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, br, o), op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ov > bv || (ov == bv && op < bp)) { bv = ov; br = orr; bp = op; }
+    }
+    if (lane == 0) { candv[warp] = bv; candr[warp] = br; candp[warp] = bp; }
+    __syncthreads();
+    // (2) every thread reduces the warp candidates (no extra barrier)
+    bv = -1.0; br = -1; bp = 0x7fffffff;
+    for (int w = 0; w < nw; w++)
+      if (candv[w] > bv || (candv[w] == bv && candp[w] < bp)) { bv = candv[w]; br = candr[w]; bp = candp[w]; }
+    if (warp == 0) {  // pivot row: scaled copy in prow (prow[c] = 1/pivot), broadcast after the barrier
+      const double pv = br >= 0 ? P[br * ld + c] : 0.0;
+      const bool sing = (pv == 0.0 || pv != pv);
+      const double inv = sing ? 0.0 : 1.0 / pv;
+      __syncwarp();
+      for (int cc = lane; cc < bb; cc += 32) {
+        const double v = (cc == c) ? inv : P[br * ld + cc] * inv;
+        prow[cc] = v;
+        P[br * ld + cc] = v;
+      }
+      if (lane == 0) {
+        if (sing && info[blockIdx.x] == 0) info[blockIdx.x] = jc + 1;
+        D.ipiv[jc] = bp;  // swap positions jc <-> bp
+        const int q = at[jc];
+        at[bp] = q;
+        pos[q] = bp;
+        at[jc] = br;
+        pos[br] = jc;
       }
     }
     __syncthreads();
-    const int p = s_piv;
-    if (p != jc)
-      for (int cc = threadIdx.x; cc < bb; cc += blockDim.x) {
-        double t = P[p * ld + cc];
-        P[p * ld + cc] = P[jc * ld + cc];
-        P[jc * ld + cc] = t;
-      }
-    __syncthreads();
-    const double inv = s_inv;
-    for (int cc = threadIdx.x; cc < bb; cc += blockDim.x) P[jc * ld + cc] = (cc == c) ? inv : P[jc * ld + cc] * inv;
-    __syncthreads();
-    for (int r = threadIdx.x; r < m; r += blockDim.x) {
-      if (r == jc) continue;
+    const double inv = prow[c];
+    // (3) eliminate column c from every other row
+    for (int r = tid; r < m; r += nt) {
+      if (r == br) continue;
       double* row = P + r * ld;
-      const double* prow = P + jc * ld;
       const double f = row[c];
       if (f != 0.0) {
-        for (int cc = 0; cc < bb; cc++)
-          if (cc != c) row[cc] -= f * prow[cc];
+#pragma unroll 4
+        for (int cc = 0; cc < bb; cc++) row[cc] -= f * prow[cc];
       }
       row[c] = -f * inv;
     }
     __syncthreads();
   }
-  for (int c = 0; c < bb; c++)
-    for (int r = threadIdx.x; r < m; r += blockDim.x) D.A[r + (size_t)(j + c) * D.lda] = P[r * ld + c];
+  // write back in final order; record the row moves (positions >= j only)
+  for (int l = tid; l < m; l += nt) {
+    const int r = at[l];
+    double* dst = D.A + l;
+#pragma unroll 8
+    for (int c = 0; c < bb; c++) dst[(size_t)(j + c) * D.lda] = P[r * ld + c];
+    if (r != l) {
+      const int k = atomicAdd(&s_cnt, 1);
+      moves[(size_t)blockIdx.x * 2 * b + k] = RowMove{l, r};
+    }
+  }
+  __syncthreads();
+  if (tid == 0) nmoves[blockIdx.x] = s_cnt;
 }
 
-// Apply the panel's row interchanges to every column outside the panel.
-__global__ void __launch_bounds__(256) gj_rowswap_kernel(const MatDesc* __restrict__ desc, int j, int b) {
+// Register-resident variant: thread t owns panel rows t, t+nt (R rows, B
+// columns in registers).  Per column: local candidate -> warp shuffle ->
+// barrier -> owner publishes the scaled pivot row -> barrier -> register
+// elimination (no barrier: every thread reads only its own rows next).
+// Ties are broken by row index; thread 0 keeps the position bookkeeping.
+template <int B, int R>
+__global__ void __launch_bounds__(R == 1 ? 512 : (R == 2 ? 384 : 256)) gj_panel_reg_kernel(
+    const MatDesc* __restrict__ desc, int j, int* info, RowMove* moves, int* nmoves) {
+  extern __shared__ int smi[];
+  __shared__ double candv[32];
+  __shared__ int candr[32];
+  __shared__ double prow[B];
+  __shared__ int s_cnt;
+  const MatDesc D = desc[blockIdx.x];
+  const int m = D.m;
+  if (m <= j) return;
+  const int bb = min(B, m - j);
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  int* pos = smi;     // row -> position
+  int* at = pos + m;  // position -> row
+  double v[R][B];
+  bool used[R];
+#pragma unroll
+  for (int k = 0; k < R; k++) {
+    const int r = tid + k * nt;
+    used[k] = !(r < m) || r < j;  // rows above the panel are already pivot rows
+#pragma unroll
+    for (int c = 0; c < B; c++) v[k][c] = (r < m && c < bb) ? D.A[r + (size_t)(j + c) * D.lda] : 0.0;
+  }
+  for (int r = tid; r < m; r += nt) {
+    pos[r] = r;
+    at[r] = r;
+  }
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < B; c++) {
+    if (c >= bb) break;
+    const int jc = j + c;
+    double bv = -1.0;
+    int br = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < R; k++) {
+      const double a = fabs(v[k][c]);
+      if (!used[k] && (a > bv)) { bv = a; br = tid + k * nt; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+      if (ov > bv || (ov == bv && orr < br)) { bv = ov; br = orr; }
+    }
+    if (lane == 0) { candv[warp] = bv; candr[warp] = br; }
+    __syncthreads();
+    bv = -1.0;
+    br = 0x7fffffff;
+    for (int w = 0; w < nw; w++)
+      if (candv[w] > bv || (candv[w] == bv && candr[w] < br)) { bv = candv[w]; br = candr[w]; }
+    if (br == 0x7fffffff) br = -1;
+    // owner of the pivot row publishes it scaled; thread 0 does the bookkeeping
+    const int kown = br >= 0 ? br / nt : -1;
+    if (br >= 0 && br % nt == tid) {
+#pragma unroll
+      for (int k = 0; k < R; k++)
+        if (k == kown) {
+          const double pv = v[k][c];
+          const bool sing = (pv == 0.0 || pv != pv);
+          const double inv = sing ? 0.0 : 1.0 / pv;
+          if (sing && info[blockIdx.x] == 0) info[blockIdx.x] = jc + 1;
+#pragma unroll
+          for (int cc = 0; cc < B; cc++) {
+            const double s = (cc == c) ? inv : v[k][cc] * inv;
+            prow[cc] = s;
+            v[k][cc] = s;
+          }
+          used[k] = true;
+        }
+    }
+    if (tid == 0) {
+      if (br < 0) {  // no candidate left (cannot happen for m > jc): keep identity
+        if (info[blockIdx.x] == 0) info[blockIdx.x] = jc + 1;
+        D.ipiv[jc] = jc;
+      } else {
+        const int bp = pos[br];
+        D.ipiv[jc] = bp;
+        const int q = at[jc];
+        at[bp] = q;
+        pos[q] = bp;
+        at[jc] = br;
+        pos[br] = jc;
+      }
+    }
+    __syncthreads();
+    const double inv = prow[c];
+#pragma unroll
+    for (int k = 0; k < R; k++) {
+      const int r = tid + k * nt;
+      if (r == br || r >= m) continue;
+      const double f = v[k][c];
+#pragma unroll
+      for (int cc = 0; cc < B; cc++)
+        if (cc != c) v[k][cc] = fma(-f, prow[cc], v[k][cc]);
+      v[k][c] = -f * inv;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < R; k++) {
+    const int r = tid + k * nt;
+    if (r >= m) continue;
+    const int l = pos[r];
+    double* dst = D.A + l;
+#pragma unroll
+    for (int c = 0; c < B; c++)
+      if (c < bb) dst[(size_t)(j + c) * D.lda] = v[k][c];
+    if (r != l) {
+      const int q = atomicAdd(&s_cnt, 1);
+      moves[(size_t)blockIdx.x * 2 * B + q] = RowMove{l, r};
+    }
+  }
+  __syncthreads();
+  if (tid == 0) nmoves[blockIdx.x] = s_cnt;
+}
+
+// Apply the panel's row moves to every column outside the panel and copy the
+// pivot-row block W = A[j:j+bb, :] (after the moves).  One warp per column.
+__global__ void __launch_bounds__(256) gj_move_copy_kernel(const MatDesc* __restrict__ desc, int j, int b,
+                                                           const RowMove* __restrict__ moves,
+                                                           const int* __restrict__ nmoves, double* const* W) {
   const MatDesc D = desc[blockIdx.x];
   if (D.m <= j) return;
   const int bb = min(b, D.m - j);
-  for (int col = threadIdx.x + blockIdx.y * blockDim.x; col < D.m; col += blockDim.x * gridDim.y) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cnt = nmoves[blockIdx.x];
+  const RowMove* mv = moves + (size_t)blockIdx.x * 2 * b;
+  double* w = W[blockIdx.x];
+  for (int col = warp + blockIdx.y * 8; col < D.m; col += 8 * gridDim.y) {
     if (col >= j && col < j + bb) continue;
     double* a = D.A + (size_t)col * D.lda;
-    for (int t = 0; t < bb; t++) {
-      int p = D.ipiv[j + t];
-      if (p != j + t) {
-        double x = a[j + t];
-        a[j + t] = a[p];
-        a[p] = x;
-      }
-    }
+    double v0 = 0.0, v1 = 0.0;
+    RowMove m0{-1, -1}, m1{-1, -1};
+    if (lane < cnt) { m0 = mv[lane]; v0 = a[m0.src]; }
+    if (lane + 32 < cnt) { m1 = mv[lane + 32]; v1 = a[m1.src]; }
+    __syncwarp();
+    if (m0.dst >= 0) a[m0.dst] = v0;
+    if (m1.dst >= 0) a[m1.dst] = v1;
+    __syncwarp();
+    for (int t = lane; t < bb; t += 32) w[t + (size_t)col * bb] = a[j + t];
   }
 }
 
-// Undo the row pivoting of the factorised matrix: inv(A) = inv(PA) P, i.e.
-// column swaps in reverse order.
-__global__ void __launch_bounds__(256) gj_colswap_kernel(const MatDesc* __restrict__ desc) {
-  const MatDesc D = desc[blockIdx.x];
-  for (int r = threadIdx.x + blockIdx.y * blockDim.x; r < D.m; r += blockDim.x * gridDim.y) {
-    for (int c = D.m - 1; c >= 0; c--) {
-      int p = D.ipiv[c];
-      if (p != c) {
-        double x = D.A[r + (size_t)c * D.lda];
-        D.A[r + (size_t)c * D.lda] = D.A[r + (size_t)p * D.lda];
-        D.A[r + (size_t)p * D.lda] = x;
+// Trailing update of one Gauss-Jordan panel step, all matrices of the batch in
+// one launch, indexed on the device (no per-step host descriptors):
+//   A[i, c] = [i not in R1] A[i, c] + sum_k A[i, j+k] W[k, c]   for c outside the panel
+// (rows R1 = [j, j+bb) hold A11^-1 in the panel columns, so the same formula
+// covers the overwrite A[R1, c] = A11^-1 W[:, c]).  64x64 DMMA tiles; the
+// virtual column index skips the panel columns.
+__global__ void __launch_bounds__(GTHREADS) gj_update_kernel(const MatDesc* __restrict__ desc,
+                                                             const int* __restrict__ tile0, int np, int j, int b,
+                                                             double* const* __restrict__ Wp) {
+  __shared__ double As[2][GBK][GPAD];
+  __shared__ double Bs[2][GBK][GPAD];
+  int lo = 0, hi = np - 1;
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tile0[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const MatDesc D = desc[lo];
+  const int m = D.m;
+  const int bb = min(b, m - j);
+  const int ncol = m - bb;  // virtual columns
+  const int tl = t - tile0[lo];
+  const int tilesM = (m + GBM - 1) / GBM;
+  const int i0 = (tl % tilesM) * GBM, v0 = (tl / tilesM) * GBN;
+  const double* __restrict__ W = Wp[lo];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int c = 0; c < 4; c++) acc[a][c][0] = acc[a][c][1] = 0.0;
+  double ra[8], rb[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int idx = tid + e * GTHREADS;
+      int i = idx & 63, k = idx >> 6;
+      int gi = i0 + i, gk = k0 + k;
+      ra[e] = (gi < m && gk < bb) ? D.A[gi + (size_t)(j + gk) * D.lda] : 0.0;
+      k = idx & 15;
+      const int vc = v0 + (idx >> 4);
+      gk = k0 + k;
+      const int col = vc < j ? vc : vc + bb;
+      rb[e] = (vc < ncol && gk < bb) ? W[gk + (size_t)col * bb] : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int idx = tid + e * GTHREADS;
+      As[buf][idx >> 6][idx & 63] = ra[e];
+      Bs[buf][idx & 15][idx >> 4] = rb[e];
+    }
+  };
+  const int nk = (bb + GBK - 1) / GBK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; kt++) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) load((kt + 1) * GBK);
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) fa[q] = As[buf][kk + (lane & 3)][wm + q * 8 + (lane >> 2)];
+#pragma unroll
+      for (int q = 0; q < 4; q++) fb[q] = Bs[buf][kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int y = 0; y < 4; y++)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
+                       : "d"(fa[x]), "d"(fb[y]));
+    }
+    if (kt + 1 < nk) {
+      store(buf ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; x++) {
+    const int gi = i0 + wm + x * 8 + (lane >> 2);
+    if (gi >= m) continue;
+    const bool r1 = gi >= j && gi < j + bb;
+#pragma unroll
+    for (int y = 0; y < 4; y++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int vc = v0 + wn + y * 8 + 2 * (lane & 3) + h;
+        if (vc >= ncol) continue;
+        const int col = vc < j ? vc : vc + bb;
+        double* c = D.A + gi + (size_t)col * D.lda;
+        *c = r1 ? acc[x][y][h] : *c + acc[x][y][h];
       }
+  }
+}
+
+// Undo the row pivoting of the inverted matrix: inv(A) = inv(PA) P, i.e. the
+// column swaps of ipiv in reverse order -- composed into one column gather.
+__global__ void gj_colperm_kernel(const MatDesc* __restrict__ desc, int* perm, int stride) {
+  const MatDesc D = desc[blockIdx.x];
+  if (threadIdx.x != 0) return;
+  int* src = perm + (size_t)blockIdx.x * stride;
+  for (int c = 0; c < D.m; c++) src[c] = c;
+  for (int c = D.m - 1; c >= 0; c--) {
+    const int p = D.ipiv[c];
+    const int t = src[c];
+    src[c] = src[p];
+    src[p] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) gj_colgather_kernel(const MatDesc* __restrict__ desc, const int* perm,
+                                                           int stride, double* const* T, int back) {
+  const MatDesc D = desc[blockIdx.x];
+  const int* src = perm + (size_t)blockIdx.x * stride;
+  double* t = T[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int col = warp + blockIdx.y * 8; col < D.m; col += 8 * gridDim.y) {
+    if (!back) {
+      const double* a = D.A + (size_t)src[col] * D.lda;
+      double* o = t + (size_t)col * D.m;
+      for (int r = lane; r < D.m; r += 32) o[r] = a[r];
+    } else {
+      const double* a = t + (size_t)col * D.m;
+      double* o = D.A + (size_t)col * D.lda;
+      for (int r = lane; r < D.m; r += 32) o[r] = a[r];
     }
   }
 }
@@ -311,51 +610,74 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   if (n == 0) return;
   int maxm = 0;
   for (auto& d : h) maxm = std::max(maxm, d.m);
-  int b = 32;
-  while (b > 4 && size_t(maxm) * (b + 1) * 8 > 200 * 1024) b /= 2;
-  if (size_t(maxm) * (b + 1) * 8 > 220 * 1024) invalid("pivot block too large for the Gauss-Jordan panel");
-  size_t smem = size_t(maxm) * (b + 1) * 8;
+  // panel variant: registers (one or two rows per thread) up to m = 1024,
+  // shared memory beyond (the top-level system)
+  int variant, b, threads;
+  size_t smem;
+  if (maxm <= 512) {
+    variant = 0;
+    b = 32;
+    threads = std::max(64, (maxm + 31) / 32 * 32);
+    smem = size_t(maxm) * 8;
+  } else if (maxm <= 768) {
+    variant = 1;
+    b = 32;
+    threads = ((maxm + 1) / 2 + 31) / 32 * 32;
+    smem = size_t(maxm) * 8;
+  } else {
+    variant = 2;
+    auto smem_for = [&](int bw) { return size_t(maxm) * (bw + 1) * 8 + size_t(maxm) * 8; };
+    b = 32;
+    while (b > 4 && smem_for(b) > 224 * 1024) b /= 2;
+    if (smem_for(b) > 224 * 1024) invalid("pivot block too large for the Gauss-Jordan panel");
+    smem = smem_for(b);
+    threads = 512;
+  }
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
     attr = true;
   }
   CK(cudaMemsetAsync(d_info, 0, sizeof(int) * n, s));
-  // scratch for the pivot-row block W (b x m per matrix)
+  // pivot-row block W (b x m per matrix), row moves, column-unswap scratch
   std::vector<double*> W(n);
   for (int p = 0; p < n; p++) W[p] = ws.alloc_n<double>(size_t(b) * h[p].m);
-  CopyBatch cb;
-  GemmBatch gb;
-  const int threads = maxm >= 256 ? 512 : 256;
+  double* const* dW = upload(ws, W, s, st);
+  RowMove* moves = static_cast<RowMove*>(ws.alloc(sizeof(RowMove) * size_t(n) * 2 * b));
+  int* nmoves = ws.alloc_n<int>(n);
+  std::vector<int> tile_pref[2];
+  const int gy = std::max(1, std::min(16, (maxm + 63) / 64));
   for (int j = 0; j < maxm; j += b) {
-    gj_panel_kernel<<<n, threads, smem, s>>>(d_desc, j, b, d_info);
+    if (variant == 0) gj_panel_reg_kernel<32, 1><<<n, threads, smem, s>>>(d_desc, j, d_info, moves, nmoves);
+    else if (variant == 1) gj_panel_reg_kernel<32, 2><<<n, threads, smem, s>>>(d_desc, j, d_info, moves, nmoves);
+    else gj_panel_kernel<<<n, threads, smem, s>>>(d_desc, j, b, d_info, moves, nmoves);
     CK_LAUNCH();
-    gj_rowswap_kernel<<<dim3(n, std::max(1, std::min(8, maxm / 256 + 1))), 256, 0, s>>>(d_desc, j, b);
+    gj_move_copy_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, j, b, moves, nmoves, dW);
     CK_LAUNCH();
+    // tile prefix of this step (matrices with m <= j contribute nothing)
+    std::vector<int>& t0 = tile_pref[(j / b) & 1];
+    t0.assign(n + 1, 0);
     for (int p = 0; p < n; p++) {
-      const MatDesc& D = h[p];
-      if (D.m <= j) continue;
-      const int bb = std::min(b, D.m - j), m = D.m, r2 = j + bb, n2 = m - r2;
-      double* A = D.A;
-      const int ld = D.lda;
-      cb.add(A + j, ld, W[p], bb, bb, m);  // W = A[R1, :]
-      const double* pan = A + (size_t)j * ld;  // A[:, J]
-      const double* W0 = W[p];
-      const double* W2 = W[p] + (size_t)r2 * bb;
-      // rows R0
-      gb.add(pan, ld, W0, bb, A, ld, j, j, bb, 1.0, 1.0);
-      gb.add(pan, ld, W2, bb, A + (size_t)r2 * ld, ld, j, n2, bb, 1.0, 1.0);
-      // rows R2
-      gb.add(pan + r2, ld, W0, bb, A + r2, ld, n2, j, bb, 1.0, 1.0);
-      gb.add(pan + r2, ld, W2, bb, A + r2 + (size_t)r2 * ld, ld, n2, n2, bb, 1.0, 1.0);
-      // rows R1 (overwrite): A11_inv * W
-      gb.add(pan + j, ld, W0, bb, A + j, ld, bb, j, bb, 1.0, 0.0);
-      gb.add(pan + j, ld, W2, bb, A + j + (size_t)r2 * ld, ld, bb, n2, bb, 1.0, 0.0);
+      const int m = h[p].m;
+      const int tiles = m > j ? ceil_div(m, GBM) * ceil_div(m - std::min(b, m - j), GBN) : 0;
+      t0[p + 1] = t0[p] + tiles;
     }
-    launch_copies(cb, ws, st, s);
-    launch_grouped_gemm(gb, false, false, ws, st, s);
+    if (t0[n] > 0) {
+      const int* dt0 = upload(ws, t0, s, st);
+      gj_update_kernel<<<t0[n], GTHREADS, 0, s>>>(d_desc, dt0, n, j, b, dW);
+      CK_LAUNCH();
+    }
   }
-  gj_colswap_kernel<<<dim3(n, std::max(1, std::min(8, maxm / 256 + 1))), 256, 0, s>>>(d_desc);
+  // undo the row pivoting as one column gather per matrix (through scratch)
+  int* perm = ws.alloc_n<int>(size_t(n) * maxm);
+  std::vector<double*> T(n);
+  for (int p = 0; p < n; p++) T[p] = ws.alloc_n<double>(size_t(h[p].m) * h[p].m);
+  double* const* dT = upload(ws, T, s, st);
+  gj_colperm_kernel<<<n, 32, 0, s>>>(d_desc, perm, maxm);
+  CK_LAUNCH();
+  gj_colgather_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, perm, maxm, dT, 0);
+  CK_LAUNCH();
+  gj_colgather_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, perm, maxm, dT, 1);
   CK_LAUNCH();
 }
 

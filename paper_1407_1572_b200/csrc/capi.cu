@@ -24,6 +24,7 @@ using ifmm::StoreH;
 using ifmm::Topo;
 using ifmm::TreeH;
 using ifmm::invalid;
+using ifmm::batched_gj_inverse;
 using ifmm::ensure_device;
 using ifmm::default_stream;
 using ifmm::upload;
@@ -264,6 +265,16 @@ int ifmm_factor_timing(const ifmm_factor* f, double* ms7, int64_t* launches7) {
   });
 }
 
+int ifmm_factor_timing_level(const ifmm_factor* f, int level, double* ms9) {
+  return guard([&] {
+    for (int p = 0; p < ifmm::PH_COUNT; p++)
+      ms9[p] = (level >= 0 && size_t(level) < f->h->phase_lvl_ms.size()) ? f->h->phase_lvl_ms[level][p] : 0.0;
+    const bool h = level >= 0 && size_t(level) < f->h->host_lvl_ms.size();
+    ms9[7] = h ? f->h->host_lvl_ms[level][0] : 0.0;
+    ms9[8] = h ? f->h->host_lvl_ms[level][1] : 0.0;
+  });
+}
+
 int64_t ifmm_launch_count(void) { return ifmm::launch_counter().load(); }
 
 int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int ptr_kind) {
@@ -337,6 +348,49 @@ int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info) 
     CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(a, d, sizeof(double) * tot, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(info, dinfo, sizeof(int) * count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_bench_gj_inverse(const double* a, const int32_t* m, int count, int reps, double* ms) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t s = default_stream();
+    Arena ws(size_t(64) << 20);
+    Staging st;
+    size_t tot = 0;
+    for (int c = 0; c < count; c++) tot += size_t(m[c]) * m[c];
+    double* src = ws.alloc_n<double>(tot);
+    double* d = ws.alloc_n<double>(tot);
+    CK(cudaMemcpy(src, a, sizeof(double) * tot, cudaMemcpyHostToDevice));
+    std::vector<MatDesc> md(count);
+    size_t off = 0;
+    for (int c = 0; c < count; c++) {
+      md[c] = MatDesc{d + off, m[c], m[c], ws.alloc_n<int>(m[c]), c};
+      off += size_t(m[c]) * m[c];
+    }
+    const MatDesc* dmd = upload(ws, md, s, st);
+    int* dinfo = ws.alloc_n<int>(count);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double best = 1e30;
+    for (int r = 0; r < reps; r++) {
+      CK(cudaMemcpyAsync(d, src, sizeof(double) * tot, cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      const size_t mark = ws.in_use();
+      (void)mark;
+      CK(cudaEventRecord(e0, s));
+      batched_gj_inverse(md, dmd, dinfo, ws, st, s);
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, e0, e1));
+      best = std::min(best, double(t));
+      st.reset();
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = best;
   });
 }
 

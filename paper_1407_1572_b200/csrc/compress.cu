@@ -6,6 +6,18 @@
 
 namespace ifmm {
 
+__device__ int g_prof_on = 0;
+__device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
+#define PROF_T0() long long _pt = g_prof_on ? clock64() : 0
+#define PROF_ACC(i) \
+  do {                                                                  \
+    if (g_prof_on) {                                                    \
+      const long long _n = clock64();                                   \
+      if (threadIdx.x == 0) atomicAdd(&g_cyc[i], (unsigned long long)(_n - _pt)); \
+      _pt = _n;                                                         \
+    }                                                                   \
+  } while (0)
+
 constexpr int CTMAX = 512;  // compression CTAs: 128 threads for small fills, 512 at coarse levels
 
 // ------------------------------------------------------------------ K1
@@ -53,8 +65,10 @@ __global__ void __launch_bounds__(CTMAX) aca_recompress_kernel(const FillDesc* _
       continue;
     }
     const int mrow = rows < probe_maxm ? rows : probe_maxm;
+    PROF_T0();
     AcaOut ao = cta_aca(D.F, D.ldF, D.transF, rows, cols, tol, probes + (size_t)mrow * 10, min(10, rows), Uc, Vc,
                         D.Kf, rr, cc, usedr, usedc, dots, sh);
+    PROF_ACC(0);
     const int k = ao.k;
     S.k = k;
     if (!ao.converged && (k >= min(rows, cols) || k >= D.Kf)) {
@@ -70,9 +84,11 @@ __global__ void __launch_bounds__(CTMAX) aca_recompress_kernel(const FillDesc* _
     if (k > 0) {
       cta_qr(Uc, rows, k, rows, Rl, Ql, rows, vv, sh);
       cta_qr(Vc, cols, k, cols, Rr, Qr, cols, vv, sh);
+      PROF_ACC(1);
       cta_gemm(k, k, k, 1.0, Rl, k, false, Rr, k, true, 0.0, core, k);
       cta_jacobi(core, k, k, k, Jv, k, sig, ord, sh);
       r = trunc_rank_dev(sig, ord, k, tol);
+      PROF_ACC(2);
       for (int e = threadIdx.x; e < rows * r; e += blockDim.x) {
         const int i = e % rows, c = e / rows;
         const int col = ord[c];
@@ -93,6 +109,7 @@ __global__ void __launch_bounds__(CTMAX) aca_recompress_kernel(const FillDesc* _
     double fro = 0.0;
     for (int e = threadIdx.x; e < rows * r; e += blockDim.x) fro += left[e] * left[e];
     fro = sqrt(block_sum(fro, sh.red));
+    PROF_ACC(3);
     S.r = r;
     S.fro = fro;
     if (threadIdx.x == 0) state[f] = S;
@@ -108,14 +125,18 @@ __device__ int new_dirs(double* H, int nU, int r, const double* wsig, double* U,
                         double* R, double* E, double* sig, int* ord, double* vv, CtaShared& sh) {
   const int cap = nU - rU;
   if (cap <= 0 || r == 0) return 0;
+  PROF_T0();
   cta_project_out(H, nU, nU, r, U, nU, rU, E);
   cta_project_out(H, nU, nU, r, U, nU, rU, E);
+  PROF_ACC(4);
   if (wsig) {
     for (int e = threadIdx.x; e < nU * r; e += blockDim.x) H[e] *= wsig[e / nU];
     __syncthreads();
   }
   cta_qr(H, nU, r, nU, R, Q, nU, vv, sh);  // H = Q R
+  PROF_ACC(5);
   cta_jacobi(R, r, r, r, nullptr, 0, sig, ord, sh);  // R V = U_R S
+  PROF_ACC(6);
   int w = 0;
   for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
   w = min(w, cap);
@@ -129,6 +150,7 @@ __device__ int new_dirs(double* H, int nU, int r, const double* wsig, double* U,
   }
   __syncthreads();
   if (w > 0) cta_project_out(W, nU, nU, w, U, nU, rU, E);
+  PROF_ACC(7);
   return w;
 }
 
@@ -293,6 +315,13 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   static const bool narrow = getenv("IFMM_BS128") != nullptr;  // debug: force 128-thread CTAs
   const int bs_fill = narrow ? 128 : (MX >= 256 && nf < 2048) ? 512 : (MX >= 128 ? 256 : 128);
   const int bs_dirs = narrow ? 128 : MX >= 256 ? 512 : (MX >= 128 ? 256 : 128);
+  static const bool prof = getenv("IFMM_PROF") != nullptr;
+  if (prof) {
+    const int one = 1;
+    unsigned long long z[16] = {0};
+    CK(cudaMemcpyToSymbolAsync(g_prof_on, &one, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyToSymbolAsync(g_cyc, z, sizeof z, 0, cudaMemcpyHostToDevice, s));
+  }
   const FillDesc* dfd = upload(ws, cb.fills, s, st);
   // K1
   {
@@ -358,6 +387,14 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     double* scr = ws.alloc_n<double>(slot * grid);
     delta_kernel<<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats);
     CK_LAUNCH();
+  }
+  if (prof) {
+    unsigned long long c[16];
+    CK(cudaMemcpyFromSymbolAsync(c, g_cyc, sizeof c, 0, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "prof MX=%d nf=%d chains=%zu p2p=%zu | aca %.1f qr %.1f core %.1f rest %.1f | proj %.1f qr %.1f jac %.1f W %.1f Mcyc\n",
+            MX, nf, cb.chain_off.size() - 1, cb.p2p.size(), c[0] / 1e6, c[1] / 1e6, c[2] / 1e6, c[3] / 1e6, c[4] / 1e6,
+            c[5] / 1e6, c[6] / 1e6, c[7] / 1e6);
   }
 }
 

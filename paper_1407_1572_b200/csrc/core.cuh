@@ -1,6 +1,7 @@
 // Host-side handles of the B200 IFMM: tree, initial operator store,
 // factorization.  Device memory is owned by per-handle arenas.
 #pragma once
+#include <array>
 #include <memory>
 #include <mutex>
 
@@ -131,6 +132,8 @@ struct FactorH {
   double phase_ms[8] = {0};
   long long phase_launches[8] = {0};
   int deferred_batches = 0;  // colour batches split by the independence guard
+  std::vector<std::array<double, 8>> phase_lvl_ms;  // [level][phase]
+  std::vector<std::array<double, 2>> host_lvl_ms;   // [level]: host busy until the final sync, time blocked in it
 };
 
 enum PhaseId : int {

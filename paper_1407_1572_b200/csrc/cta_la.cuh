@@ -233,6 +233,10 @@ __device__ inline void cta_jacobi(double* A, int m, int n, int lda, double* V, i
         if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        // a rotation below rounding level changes nothing: columns of very
+        // different norms otherwise keep |ga|/sqrt(al*be) ~ eps*sqrt(al/be)
+        // and never pass the relative test
+        if (fabs(t) < 1e-16) continue;
         const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
         for (int i = lane; i < m; i += 32) {
           const double xi = x[i], yi = y[i];

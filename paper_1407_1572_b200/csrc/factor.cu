@@ -87,14 +87,16 @@ struct PhaseTimer {
     spans.push_back({ev0, e, cur, launch_counter().load() - l0});
     cur = -1;
   }
-  void collect(FactorH* F) {  // call after a stream synchronisation
+  void collect(FactorH* F, int level) {  // call after a stream synchronisation
     if (!on) return;
     end();
+    if (F->phase_lvl_ms.size() <= size_t(level)) F->phase_lvl_ms.resize(level + 1, std::array<double, 8>{});
     for (Span& sp : spans) {
       float ms = 0.f;
       CK(cudaEventSynchronize(sp.b));
       CK(cudaEventElapsedTime(&ms, sp.a, sp.b));
       F->phase_ms[sp.ph] += ms;
+      F->phase_lvl_ms[level][sp.ph] += ms;
       F->phase_launches[sp.ph] += sp.launches;
       pool.push_back(sp.a);
       pool.push_back(sp.b);
@@ -322,6 +324,7 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
 }
 
 void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred) {
+  const auto t_batch0 = std::chrono::steady_clock::now();
   WorkLevel& W = cur_;
   const Topo& T = *W.T;
   const int k = W.k;
@@ -572,6 +575,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   run_compression(cbz, tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_state, d_stats, ws_, st_, s_, dbg ? 1 : 0);
   tm_.end();
   // read back: pivot conditioning, ranks, fill outcomes, counters
+  const auto t_sync0 = std::chrono::steady_clock::now();
   std::vector<double> nS(np), nSi(np);
   std::vector<int> info(np), stats(4);
   std::vector<FillState> state(nfill);
@@ -582,7 +586,11 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   CK(cudaMemcpyAsync(stats.data(), d_stats, 16, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(W.r.data(), W.d_rank, sizeof(int) * W.nc, cudaMemcpyDeviceToHost, s_));
   CK(cudaStreamSynchronize(s_));
-  tm_.collect(F_.get());
+  const auto t_sync1 = std::chrono::steady_clock::now();
+  if (F_->host_lvl_ms.size() <= size_t(k)) F_->host_lvl_ms.resize(k + 1, std::array<double, 2>{});
+  F_->host_lvl_ms[k][0] += std::chrono::duration<double, std::milli>(t_sync0 - t_batch0).count();
+  F_->host_lvl_ms[k][1] += std::chrono::duration<double, std::milli>(t_sync1 - t_sync0).count();
+  tm_.collect(F_.get(), k);
   if (getenv("IFMM_COND_LOG")) {
     double mx = 0, sum = 0;
     int imx = -1, mmx = 0;
@@ -703,7 +711,7 @@ void Factorizer::factor_top() {
     batched_gj_inverse(md, dmd, d_info, ws_, st_, s_);
   }
   CK(cudaStreamSynchronize(s_));
-  tm_.collect(F_.get());
+  tm_.collect(F_.get(), 1);
 }
 
 FactorH* Factorizer::run() {
@@ -732,7 +740,7 @@ FactorH* Factorizer::run() {
       tm_.begin(PH_TRANSITION);
       start_parent_level(prev_, k);
       CK(cudaStreamSynchronize(s_));
-      tm_.collect(F_.get());
+      tm_.collect(F_.get(), k);
       prev_ = WorkLevel{};
     }
     F_->stats[k].clusters = cur_.nc;

@@ -4,9 +4,11 @@
 //   top     : y = T^-1 v_top
 //   backward: x_i = g_i - X_top v[pos]     (batches and levels in reverse)
 // Using X_top = (S^-1 C)_top for both sweeps (S symmetric) means a record is
-// only Sinv_nn (n x n) + X_top (n x w): the solve streams each record twice.
-// Vectors are (positions x nrhs) row-major; a level's y slots alias the next
-// level's x slots.
+// only Sinv_nn (n x n) + X_top (n x w): the solve streams each record twice
+// and is HBM-bound.  The GEMVs keep all warps busy: warps split the columns,
+// lanes own rows with register accumulators, partial sums meet in shared
+// memory.  Vectors are (positions x nrhs) row-major; right-hand sides are
+// processed in chunks of RC; a level's y slots alias the next level's x slots.
 #include <algorithm>
 #include <cmath>
 
@@ -17,51 +19,128 @@ namespace ifmm {
 void launch_permute(const double* in, double* out, const int64_t* perm, int64_t n, int nrhs, bool inverse,
                     cudaStream_t s);
 
-__global__ void __launch_bounds__(256) solve_fwd_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                        const int64_t* __restrict__ g_off, double* V, double* G,
-                                                        int nrhs) {
-  extern __shared__ double sb[];  // n x nrhs
-  const RecordH R = recs[blockIdx.x];
-  const int n = R.n, w = R.w;
-  double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
-  for (int e = threadIdx.x; e < n * nrhs; e += blockDim.x) sb[e] = V[R.xoff * nrhs + e];
-  __syncthreads();
-  // g = Sinv b : thread per (row t, rhs q), coalesced down the columns of Sinv
-  for (int e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
-    const int t = e % n, q = e / n;
-    double s = 0.0;
-    for (int c = 0; c < n; c++) s = fma(R.sinv[t + (size_t)c * n], sb[c * nrhs + q], s);
-    g[(size_t)t * nrhs + q] = s;
-  }
-  // v[pos] -= X_top^T b : warp per column
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int e = warp; e < w * nrhs; e += nw) {
-    const int c = e / nrhs, q = e % nrhs;
-    const double* x = R.xtop + (size_t)c * n;
-    double s = 0.0;
-    for (int t = lane; t < n; t += 32) s = fma(x[t], sb[t * nrhs + q], s);
-    s = warp_sum(s);
-    if (lane == 0) V[(int64_t)R.pos[c] * nrhs + q] -= s;
+constexpr int SB = 256;       // threads per solve CTA
+constexpr int SWARPS = SB / 32;
+constexpr int RC = 4;         // right-hand sides per pass
+constexpr int MAXJ = 8;       // rows per lane per pass (256 rows per row block)
+
+// y[t, q] (t < n, q < nq) = sum_c A[t + c*lda] x(c, q)  (A column-major n x w);
+// x(c, q) from the `xat` accessor, result written by `emit(t, q, value)`.
+template <class XAt, class Emit>
+__device__ inline void cta_gemv_cols(const double* __restrict__ A, int n, int w, size_t lda, XAt xat, int nq,
+                                     double* red, Emit emit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t0 = 0; t0 < n; t0 += 32 * MAXJ) {
+    double acc[MAXJ][RC];
+#pragma unroll
+    for (int j = 0; j < MAXJ; j++)
+#pragma unroll
+      for (int q = 0; q < RC; q++) acc[j][q] = 0.0;
+    // warps take chunks of 32 columns; the chunk's x values are fetched once
+    // (lane u loads column cb+u) and broadcast with shuffles
+    for (int cb = warp * 32; cb < w; cb += SWARPS * 32) {
+      double xl[RC];
+#pragma unroll
+      for (int q = 0; q < RC; q++) xl[q] = (cb + lane < w && q < nq) ? xat(cb + lane, q) : 0.0;
+      const int cmax = min(32, w - cb);
+      for (int u = 0; u < cmax; u++) {
+        const double* col = A + (size_t)(cb + u) * lda;
+        double xv[RC];
+#pragma unroll
+        for (int q = 0; q < RC; q++) xv[q] = __shfl_sync(0xffffffffu, xl[q], u);
+#pragma unroll
+        for (int j = 0; j < MAXJ; j++) {
+          const int t = t0 + lane + 32 * j;
+          if (t < n) {
+            const double a = col[t];
+#pragma unroll
+            for (int q = 0; q < RC; q++) acc[j][q] = fma(a, xv[q], acc[j][q]);
+          }
+        }
+      }
+    }
+    // cross-warp reduction: red[warp][row][q]
+#pragma unroll
+    for (int j = 0; j < MAXJ; j++) {
+      const int tl = lane + 32 * j;
+#pragma unroll
+      for (int q = 0; q < RC; q++) if (t0 + tl < n) red[(tl * SWARPS + warp) * RC + q] = acc[j][q];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * MAXJ * nq; e += SB) {
+      const int tl = e / nq, q = e % nq;
+      const int t = t0 + tl;
+      if (t < n) {
+        double s = 0.0;
+        for (int w2 = 0; w2 < SWARPS; w2++) s += red[(tl * SWARPS + w2) * RC + q];
+        emit(t, q, s);
+      }
+    }
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(256) solve_bwd_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                        const int64_t* __restrict__ g_off, double* V,
-                                                        const double* G, int nrhs) {
-  extern __shared__ double sv[];  // w x nrhs gathered partner values
+__global__ void __launch_bounds__(SB) solve_fwd_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                       const int64_t* __restrict__ g_off, double* V, double* G,
+                                                       int nrhs, int red_rows) {
+  extern __shared__ double sm[];
+  double* red = sm;                         // min(maxn, 256) x SWARPS x RC
+  double* bsh = red + red_rows * SWARPS * RC;  // n x RC
+  const RecordH R = recs[blockIdx.x];
+  const int n = R.n, w = R.w;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
+  for (int q0 = 0; q0 < nrhs; q0 += RC) {
+    const int nq = min(RC, nrhs - q0);
+    for (int e = threadIdx.x; e < n * RC; e += SB) {
+      const int c = e / RC, q = e % RC;
+      bsh[e] = q < nq ? V[(R.xoff + c) * nrhs + q0 + q] : 0.0;
+    }
+    __syncthreads();
+    // g = Sinv b
+    cta_gemv_cols(R.sinv, n, n, (size_t)n, [&](int c, int q) { return bsh[c * RC + q]; }, nq, red,
+                  [&](int t, int q, double v) { g[(size_t)t * nrhs + q0 + q] = v; });
+    // v[pos] -= X_top^T b : warp per column, 2 columns in flight
+    for (int c = warp; c < w; c += SWARPS) {
+      const double* x = R.xtop + (size_t)c * n;
+      double s[RC];
+#pragma unroll
+      for (int q = 0; q < RC; q++) s[q] = 0.0;
+      for (int t = lane; t < n; t += 32) {
+        const double a = x[t];
+#pragma unroll
+        for (int q = 0; q < RC; q++) s[q] = fma(a, bsh[t * RC + q], s[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < RC; q++)
+        if (q < nq) s[q] = warp_sum(s[q]);
+      if (lane < nq) {
+        double sv = s[0];
+#pragma unroll
+        for (int q = 1; q < RC; q++)
+          if (lane == q) sv = s[q];
+        V[(int64_t)R.pos[c] * nrhs + q0 + lane] -= sv;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(SB) solve_bwd_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                       const int64_t* __restrict__ g_off, double* V,
+                                                       const double* G, int nrhs, int red_rows) {
+  extern __shared__ double sm[];
+  double* red = sm;                         // min(maxn, 256) x SWARPS x RC
   const RecordH R = recs[blockIdx.x];
   const int n = R.n, w = R.w;
   const double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
-  for (int e = threadIdx.x; e < w * nrhs; e += blockDim.x) {
-    const int c = e / nrhs, q = e % nrhs;
-    sv[e] = V[(int64_t)R.pos[c] * nrhs + q];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
-    const int t = e % n, q = e / n;
-    double s = g[(size_t)t * nrhs + q];
-    for (int c = 0; c < w; c++) s = fma(-R.xtop[t + (size_t)c * n], sv[c * nrhs + q], s);
-    V[(R.xoff + t) * nrhs + q] = s;
+  for (int q0 = 0; q0 < nrhs; q0 += RC) {
+    const int nq = min(RC, nrhs - q0);
+    // partner values are gathered on the fly (the coupling width can exceed shared memory)
+    cta_gemv_cols(R.xtop, n, w, (size_t)n, [&](int c, int q) { return V[(int64_t)R.pos[c] * nrhs + q0 + q]; }, nq,
+                  red, [&](int t, int q, double v) {
+      V[(R.xoff + t) * nrhs + q0 + q] = g[(size_t)t * nrhs + q0 + q] - v;
+    });
   }
 }
 
@@ -161,9 +240,10 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     attr = true;
   }
   for (const BatchH& b : F->batches) {
-    const size_t smem = sizeof(double) * size_t(b.maxn) * nr;
-    if (smem > 200 * 1024) invalid("solve: too many right-hand sides for one pass");
-    solve_fwd_kernel<<<b.rec1 - b.rec0, 256, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
+    const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
+    const size_t smem = sizeof(double) * (size_t(rr) * SWARPS * RC + size_t(b.maxn) * RC);
+    if (smem > 200 * 1024) invalid("solve: pivot block too large for the solve kernel");
+    solve_fwd_kernel<<<b.rec1 - b.rec0, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
   }
   // top: y = T^-1 b on the level-1 slots (viewed column-major as nrhs x M)
@@ -180,9 +260,9 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
   }
   for (auto it = F->batches.rbegin(); it != F->batches.rend(); ++it) {
     const BatchH& b = *it;
-    const size_t smem = sizeof(double) * size_t(b.maxw) * nr;
-    if (smem > 200 * 1024) invalid("solve: too many right-hand sides for one pass");
-    solve_bwd_kernel<<<b.rec1 - b.rec0, 256, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
+    const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
+    const size_t smem = sizeof(double) * size_t(rr) * SWARPS * RC;
+    solve_bwd_kernel<<<b.rec1 - b.rec0, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
   }
   launch_permute(V + F->lvl_base[t->depth] * nr, dout, t->d_perm, N, nr, true, s);

@@ -80,6 +80,17 @@ class IfmmFactorization:
         _lib.check(_lib.lib.ifmm_factor_timing(self.handle, _lib.ptr(ms), _lib.ptr(nl)))
         return {p: (float(ms[i]), int(nl[i])) for i, p in enumerate(PHASES)}
 
+    @property
+    def phase_times_by_level(self) -> dict:
+        """{level: {phase: ms}} (level 1 = top-level inverse); needs timing=True."""
+        out = {}
+        for k in range(1, self.tree.depth + 1):
+            ms = np.zeros(9)
+            _lib.check(_lib.lib.ifmm_factor_timing_level(self.handle, k, _lib.ptr(ms)))
+            if ms.any():
+                out[k] = {p: round(float(ms[i]), 3) for i, p in enumerate(PHASES + ("host_busy", "host_wait"))}
+        return out
+
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None
         if h:
