@@ -2,12 +2,23 @@
 #include <algorithm>
 
 #include "compress.cuh"
+
+namespace ifmm {
+__device__ int g_prof_on = 0;
+__device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
+}  // namespace ifmm
+// debug: Jacobi sweep statistics (sweeps, calls, columns) under IFMM_PROF
+#define IFMM_JACOBI_STATS(sw, ncol)                               \
+  do {                                                            \
+    if (g_prof_on && threadIdx.x == 0) {                          \
+      atomicAdd(&g_cyc[8], (unsigned long long)(sw));             \
+      atomicAdd(&g_cyc[9], 1ull);                                 \
+      atomicAdd(&g_cyc[10], (unsigned long long)(ncol));          \
+    }                                                             \
+  } while (0)
 #include "cta_la.cuh"
 
 namespace ifmm {
-
-__device__ int g_prof_on = 0;
-__device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
 #define PROF_T0() long long _pt = g_prof_on ? clock64() : 0
 #define PROF_ACC(i) \
   do {                                                                  \
@@ -392,9 +403,9 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     unsigned long long c[16];
     CK(cudaMemcpyFromSymbolAsync(c, g_cyc, sizeof c, 0, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    fprintf(stderr, "prof MX=%d nf=%d chains=%zu p2p=%zu | aca %.1f qr %.1f core %.1f rest %.1f | proj %.1f qr %.1f jac %.1f W %.1f Mcyc\n",
+    fprintf(stderr, "prof MX=%d nf=%d chains=%zu p2p=%zu | aca %.1f qr %.1f core %.1f rest %.1f | proj %.1f qr %.1f jac %.1f W %.1f Mcyc | jacobi calls %llu avg sweeps %.2f avg cols %.1f\n",
             MX, nf, cb.chain_off.size() - 1, cb.p2p.size(), c[0] / 1e6, c[1] / 1e6, c[2] / 1e6, c[3] / 1e6, c[4] / 1e6,
-            c[5] / 1e6, c[6] / 1e6, c[7] / 1e6);
+            c[5] / 1e6, c[6] / 1e6, c[7] / 1e6, c[9], c[9] ? double(c[8]) / c[9] : 0.0, c[9] ? double(c[10]) / c[9] : 0.0);
   }
 }
 

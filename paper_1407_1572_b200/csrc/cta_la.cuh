@@ -258,7 +258,12 @@ __device__ inline void cta_jacobi(double* A, int m, int n, int lda, double* V, i
     }
     const int rotated = sh.flag;
     __syncthreads();
-    if (!rotated) break;
+    if (!rotated) {
+#ifdef IFMM_JACOBI_STATS
+      IFMM_JACOBI_STATS(sweep + 1, n);
+#endif
+      break;
+    }
   }
   for (int c = warp; c < n; c += nw) {
     const double* x = A + (size_t)c * lda;
