@@ -129,6 +129,8 @@ int ifmm_solve_refined(ifmm_factor* f, ifmm_store* s, const double* rhs, double*
 void ifmm_factor_free(ifmm_factor* f);
 
 /* ---- test hooks for the batched kernels (host arrays in/out) */
+/* run the Jacobi / QR / ACA hooks on one warp (1) or a 256-thread CTA (0) */
+int ifmm_test_set_group(int warp);
 /* in-place inverse of `count` column-major matrices of sizes m[c], packed */
 int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info);
 /* device time (best of reps, ms) of one batched inverse of the given matrices */

@@ -299,16 +299,23 @@ void ifmm_factor_free(ifmm_factor* f) {
 }  // extern "C"
 
 // ---------------------------------------------------------------- test hooks
+// The small-matrix routines run either CTA-wide (256 threads) or on one warp,
+// as the compression kernels use them; ifmm_test_set_group selects which.
+static int g_test_warp = 0;
+
+template <class G>
 __global__ void test_jacobi_kernel(double* a, int m, int n, double* v, double* sig, int* ord) {
   __shared__ CtaShared sh;
-  ifmm::cta_jacobi(a, m, n, m, v, n, sig, ord, sh);
+  ifmm::g_jacobi_small(G::make_for_test(sh), a, m, n, m, v, n, sig, ord);
 }
 
+template <class G>
 __global__ void test_qr_kernel(double* a, int m, int k, double* q, double* r, double* vv) {
   __shared__ CtaShared sh;
-  ifmm::cta_qr(a, m, k, m, r, q, m, vv, sh);
+  ifmm::g_qr(G::make_for_test(sh), a, m, k, m, r, q, m, vv);
 }
 
+template <class G>
 __global__ void test_aca_kernel(const double* f, int m, int n, double tol, const int* probes, int kmax, double* uc,
                                 double* vc, double* scratch, int* out) {
   __shared__ CtaShared sh;
@@ -317,14 +324,26 @@ __global__ void test_aca_kernel(const double* f, int m, int n, double tol, const
   double* dots = cc + m;
   int* usedr = reinterpret_cast<int*>(dots + kmax);
   int* usedc = usedr + m;
-  AcaOut o = ifmm::cta_aca(f, m, 0, m, n, tol, probes, min(10, m), uc, vc, kmax, rr, cc, usedr, usedc, dots, sh);
+  AcaOut o = ifmm::g_aca(G::make_for_test(sh), f, m, 0, m, n, tol, probes, min(10, m), uc, vc, kmax, rr, cc, usedr,
+                         usedc, dots);
   if (threadIdx.x == 0) {
     out[0] = o.k;
     out[1] = o.converged;
   }
 }
 
+#define TEST_LAUNCH(kern, ...)                                            \
+  do {                                                                    \
+    if (g_test_warp) kern<ifmm::WarpGroup><<<1, 32>>>(__VA_ARGS__);       \
+    else kern<ifmm::CtaGroup><<<1, 256>>>(__VA_ARGS__);                   \
+  } while (0)
+
 extern "C" {
+
+int ifmm_test_set_group(int warp) {
+  g_test_warp = warp != 0;
+  return IFMM_OK;
+}
 
 int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info) {
   return guard([&] {
@@ -423,7 +442,7 @@ int ifmm_test_jacobi(double* a, int m, int n, double* v, double* sig) {
            *ds = ws.alloc_n<double>(n);
     int* dord = ws.alloc_n<int>(n);
     CK(cudaMemcpy(da, a, sizeof(double) * m * n, cudaMemcpyHostToDevice));
-    test_jacobi_kernel<<<1, 256>>>(da, m, n, dv, ds, dord);
+    TEST_LAUNCH(test_jacobi_kernel, da, m, n, dv, ds, dord);
     CK_LAUNCH();
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(a, da, sizeof(double) * m * n, cudaMemcpyDeviceToHost));
@@ -439,7 +458,7 @@ int ifmm_test_qr(const double* a, int m, int k, double* q, double* r) {
     double *da = ws.alloc_n<double>(size_t(m) * k), *dq = ws.alloc_n<double>(size_t(m) * k),
            *dr = ws.alloc_n<double>(size_t(k) * k), *dvv = ws.alloc_n<double>(k);
     CK(cudaMemcpy(da, a, sizeof(double) * m * k, cudaMemcpyHostToDevice));
-    test_qr_kernel<<<1, 256>>>(da, m, k, dq, dr, dvv);
+    TEST_LAUNCH(test_qr_kernel, da, m, k, dq, dr, dvv);
     CK_LAUNCH();
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(q, dq, sizeof(double) * m * k, cudaMemcpyDeviceToHost));
@@ -459,7 +478,7 @@ int ifmm_test_aca(const double* f, int m, int n, double tol, const int32_t* prob
     int* dout = ws.alloc_n<int>(2);
     CK(cudaMemcpy(df, f, sizeof(double) * m * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dp, probes, sizeof(int) * std::min(10, m), cudaMemcpyHostToDevice));
-    test_aca_kernel<<<1, 256>>>(df, m, n, tol, dp, kmax, du, dv, scr, dout);
+    TEST_LAUNCH(test_aca_kernel, df, m, n, tol, dp, kmax, du, dv, scr, dout);
     CK_LAUNCH();
     CK(cudaDeviceSynchronize());
     int o[2];

@@ -5,12 +5,13 @@
 
 namespace ifmm {
 __device__ int g_prof_on = 0;
+__device__ int g_jac_reg = 0;  // IFMM_JACOBI_REG=1: register-resident Jacobi for <= 16 columns (measured slower)
 __device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
 }  // namespace ifmm
 // debug: Jacobi sweep statistics (sweeps, calls, columns) under IFMM_PROF
-#define IFMM_JACOBI_STATS(sw, ncol)                               \
+#define IFMM_JACOBI_STATS(sw, ncol, leader)                       \
   do {                                                            \
-    if (g_prof_on && threadIdx.x == 0) {                          \
+    if (g_prof_on && (leader)) {                                  \
       atomicAdd(&g_cyc[8], (unsigned long long)(sw));             \
       atomicAdd(&g_cyc[9], 1ull);                                 \
       atomicAdd(&g_cyc[10], (unsigned long long)(ncol));          \
@@ -24,20 +25,41 @@ namespace ifmm {
   do {                                                                  \
     if (g_prof_on) {                                                    \
       const long long _n = clock64();                                   \
-      if (threadIdx.x == 0) atomicAdd(&g_cyc[i], (unsigned long long)(_n - _pt)); \
+      if (g.rank() == 0) atomicAdd(&g_cyc[i], (unsigned long long)(_n - _pt)); \
       _pt = _n;                                                         \
     }                                                                   \
   } while (0)
 
 constexpr int CTMAX = 512;  // compression CTAs: 128 threads for small fills, 512 at coarse levels
+constexpr int WARP_KCAP = 32;  // ACA crosses a warp worker holds; fills needing more are redone by a CTA
+
+// Worker = the group that owns one fill / chain / pivot: a whole CTA, or one
+// warp of it (fine levels).  id/count enumerate workers over the grid.
+template <class G> struct Worker;
+template <> struct Worker<CtaGroup> {
+  __device__ static int id() { return blockIdx.x; }
+  __device__ static int count() { return gridDim.x; }
+  __device__ static CtaGroup make(CtaShared& sh) { return CtaGroup{sh}; }
+};
+template <> struct Worker<WarpGroup> {
+  __device__ static int id() { return blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); }
+  __device__ static int count() { return gridDim.x * (blockDim.x >> 5); }
+  __device__ static WarpGroup make(CtaShared&) { return WarpGroup{}; }
+};
 
 // ------------------------------------------------------------------ K1
-__global__ void __launch_bounds__(CTMAX) aca_recompress_kernel(const FillDesc* __restrict__ fills, int nf,
+// ACA of the redirected fill, QR of both cross factors, Jacobi SVD of the
+// k x k core, truncation (ifmm/lowrank.py:174-263, :137-144).  kcap < Kf
+// (warp workers): a fill whose ACA reaches kcap crosses unconverged is marked
+// status 2 and redone by the CTA pass (redo = true) with the full Kf.
+template <class G>
+__global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_kernel(const FillDesc* __restrict__ fills, int nf,
                                                             FillState* state, double tol, const int* probes,
                                                             int probe_maxm, double* scratch, size_t slot,
-                                                            int MR, int MC, int KK) {
+                                                            int MR, int MC, int KK, int redo) {
   __shared__ CtaShared sh;
-  double* s = scratch + slot * blockIdx.x;
+  const G g = Worker<G>::make(sh);
+  double* s = scratch + slot * Worker<G>::id();
   double* Uc = s; s += (size_t)MR * KK;
   double* Ql = s; s += (size_t)MR * KK;
   double* Vc = s; s += (size_t)MC * KK;
@@ -54,38 +76,46 @@ __global__ void __launch_bounds__(CTMAX) aca_recompress_kernel(const FillDesc* _
   int* usedr = reinterpret_cast<int*>(s); s += MR;
   int* usedc = reinterpret_cast<int*>(s); s += MC;
   int* ord = reinterpret_cast<int*>(s);
-  for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+  for (int f = Worker<G>::id(); f < nf; f += Worker<G>::count()) {
+    if (redo && state[f].status != 2) continue;
     const FillDesc D = fills[f];
     const int rows = D.rows, cols = D.cols;
     FillState S{0, 0, 0, 0, 0, 0.0};
     if (rows == 0 || cols == 0) {
-      if (threadIdx.x == 0) state[f] = S;
-      __syncthreads();
+      if (g.rank() == 0) state[f] = S;
+      g.sync();
       continue;
     }
     if (tol == 0.0) {  // exact mode: the redirected fill is F itself (bases are identities)
       double nz = 0.0;
-      for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+      for (int e = g.rank(); e < rows * cols; e += g.size()) {
         const int a = e % rows, b = e / rows;
         nz += Fat(D.F, D.ldF, D.transF, a, b) != 0.0;
       }
-      nz = block_sum(nz, sh.red);
+      nz = g.sum(nz);
       S.r = nz > 0.0 ? min(rows, cols) : 0;
-      if (threadIdx.x == 0) state[f] = S;
-      __syncthreads();
+      if (g.rank() == 0) state[f] = S;
+      g.sync();
       continue;
     }
     const int mrow = rows < probe_maxm ? rows : probe_maxm;
+    const int kmax = min(D.Kf, KK);
     PROF_T0();
-    AcaOut ao = cta_aca(D.F, D.ldF, D.transF, rows, cols, tol, probes + (size_t)mrow * 10, min(10, rows), Uc, Vc,
-                        D.Kf, rr, cc, usedr, usedc, dots, sh);
+    AcaOut ao = g_aca(g, D.F, D.ldF, D.transF, rows, cols, tol, probes + (size_t)mrow * 10, min(10, rows), Uc, Vc,
+                      kmax, rr, cc, usedr, usedc, dots);
     PROF_ACC(0);
     const int k = ao.k;
     S.k = k;
+    if (!ao.converged && kmax < D.Kf && k >= kmax && k < min(rows, cols)) {
+      S.status = 2;  // needs more crosses than this worker holds
+      if (g.rank() == 0) state[f] = S;
+      g.sync();
+      continue;
+    }
     if (!ao.converged && (k >= min(rows, cols) || k >= D.Kf)) {
       S.status = 1;
-      if (threadIdx.x == 0) state[f] = S;
-      __syncthreads();
+      if (g.rank() == 0) state[f] = S;
+      g.sync();
       continue;
     }
     int r = 0;
@@ -93,38 +123,38 @@ __global__ void __launch_bounds__(CTMAX) aca_recompress_kernel(const FillDesc* _
     double* right = D.out + (size_t)rows * D.Kf;
     double* sv = right + (size_t)cols * D.Kf;
     if (k > 0) {
-      cta_qr(Uc, rows, k, rows, Rl, Ql, rows, vv, sh);
-      cta_qr(Vc, cols, k, cols, Rr, Qr, cols, vv, sh);
+      g_qr(g, Uc, rows, k, rows, Rl, Ql, rows, vv);
+      g_qr(g, Vc, cols, k, cols, Rr, Qr, cols, vv);
       PROF_ACC(1);
-      cta_gemm(k, k, k, 1.0, Rl, k, false, Rr, k, true, 0.0, core, k);
-      cta_jacobi(core, k, k, k, Jv, k, sig, ord, sh);
+      g_gemm(g, k, k, k, 1.0, Rl, k, false, Rr, k, true, 0.0, core, k);
+      g_jacobi_small(g, core, k, k, k, Jv, k, sig, ord, g_jac_reg != 0);
       r = trunc_rank_dev(sig, ord, k, tol);
       PROF_ACC(2);
-      for (int e = threadIdx.x; e < rows * r; e += blockDim.x) {
+      for (int e = g.rank(); e < rows * r; e += g.size()) {
         const int i = e % rows, c = e / rows;
         const int col = ord[c];
         double acc = 0.0;
         for (int t = 0; t < k; t++) acc = fma(Ql[i + (size_t)t * rows], core[t + (size_t)col * k], acc);
         left[i + (size_t)c * rows] = acc;
       }
-      for (int e = threadIdx.x; e < cols * r; e += blockDim.x) {
+      for (int e = g.rank(); e < cols * r; e += g.size()) {
         const int i = e % cols, c = e / cols;
         const int col = ord[c];
         double acc = 0.0;
         for (int t = 0; t < k; t++) acc = fma(Qr[i + (size_t)t * cols], Jv[t + (size_t)col * k], acc);
         right[i + (size_t)c * cols] = acc;
       }
-      for (int c = threadIdx.x; c < r; c += blockDim.x) sv[c] = sig[ord[c]];
-      __syncthreads();
+      for (int c = g.rank(); c < r; c += g.size()) sv[c] = sig[ord[c]];
+      g.sync();
     }
     double fro = 0.0;
-    for (int e = threadIdx.x; e < rows * r; e += blockDim.x) fro += left[e] * left[e];
-    fro = sqrt(block_sum(fro, sh.red));
+    for (int e = g.rank(); e < rows * r; e += g.size()) fro += left[e] * left[e];
+    fro = sqrt(g.sum(fro));
     PROF_ACC(3);
     S.r = r;
     S.fro = fro;
-    if (threadIdx.x == 0) state[f] = S;
-    __syncthreads();
+    if (g.rank() == 0) state[f] = S;
+    g.sync();
   }
 }
 
@@ -132,35 +162,36 @@ __global__ void __launch_bounds__(CTMAX) aca_recompress_kernel(const FillDesc* _
 // H (nU x r): directions to add (already weighted).  Appends w <= cap columns
 // to U (nU x cap, ld nU) after its first rU columns; ifmm/solver.py:334-358.
 // Two-pass projection, then QR + Jacobi on the small R factor.
-__device__ int new_dirs(double* H, int nU, int r, const double* wsig, double* U, int rU, double cutoff, double* Q,
-                        double* R, double* E, double* sig, int* ord, double* vv, CtaShared& sh) {
+template <class G>
+__device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig, double* U, int rU, double cutoff,
+                        double* Q, double* R, double* E, double* sig, int* ord, double* vv) {
   const int cap = nU - rU;
   if (cap <= 0 || r == 0) return 0;
   PROF_T0();
-  cta_project_out(H, nU, nU, r, U, nU, rU, E);
-  cta_project_out(H, nU, nU, r, U, nU, rU, E);
+  g_project_out(g, H, nU, nU, r, U, nU, rU, E);
+  g_project_out(g, H, nU, nU, r, U, nU, rU, E);
   PROF_ACC(4);
   if (wsig) {
-    for (int e = threadIdx.x; e < nU * r; e += blockDim.x) H[e] *= wsig[e / nU];
-    __syncthreads();
+    for (int e = g.rank(); e < nU * r; e += g.size()) H[e] *= wsig[e / nU];
+    g.sync();
   }
-  cta_qr(H, nU, r, nU, R, Q, nU, vv, sh);  // H = Q R
+  g_qr(g, H, nU, r, nU, R, Q, nU, vv);  // H = Q R
   PROF_ACC(5);
-  cta_jacobi(R, r, r, r, nullptr, 0, sig, ord, sh);  // R V = U_R S
+  g_jacobi_small(g, R, r, r, r, nullptr, 0, sig, ord, g_jac_reg != 0);  // R V = U_R S
   PROF_ACC(6);
   int w = 0;
   for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
   w = min(w, cap);
   double* W = U + (size_t)rU * nU;
-  for (int e = threadIdx.x; e < nU * w; e += blockDim.x) {
+  for (int e = g.rank(); e < nU * w; e += g.size()) {
     const int i = e % nU, c = e / nU;
     const int col = ord[c];
     double acc = 0.0;
     for (int t = 0; t < r; t++) acc = fma(Q[i + (size_t)t * nU], R[t + (size_t)col * r], acc);
     W[i + (size_t)c * nU] = acc / sig[col];
   }
-  __syncthreads();
-  if (w > 0) cta_project_out(W, nU, nU, w, U, nU, rU, E);
+  g.sync();
+  if (w > 0) g_project_out(g, W, nU, nU, w, U, nU, rU, E);
   PROF_ACC(7);
   return w;
 }
@@ -181,95 +212,76 @@ __device__ inline DirScratch carve_dirs(double* s, int MX, int KK) {
   return d;
 }
 
-// ------------------------------------------------------------------ K2
-__global__ void __launch_bounds__(CTMAX) hybrid_dirs_kernel(const FillDesc* __restrict__ fills,
-                                                         const int* __restrict__ chain_off,
-                                                         const int* __restrict__ chain, int nchains,
-                                                         FillState* state, int* rank, double tol, double* scratch,
-                                                         size_t slot, int MX, int KK, int debug) {
+// ------------------------------------------------------------------ K2+K3
+// Basis augmentation, one chain per cluster c of the batch.  A hybrid fill
+// (q = c) and the q side of a P2P fill (a, c) append directions of the fill's
+// weighted right factor to U_c; the p side of a P2P fill (c, b) appends
+// directions of its left factor.  Each step depends only on the earlier steps
+// of the same cluster, so chains run in parallel and a P2P fill's two sides
+// proceed independently -- the reference's sequential order restricted to
+// each basis (ifmm/solver.py:334-358, 495-520).  Task = fill * 2 + side
+// (0: q side, 1: p side).
+template <class G>
+__global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks)
+    augment_kernel(const FillDesc* __restrict__ fills, const int* __restrict__ aug_off, const int* __restrict__ aug,
+                   int nchains, FillState* state, int* rank, double tol, double* scratch, size_t slot, int MX, int KK,
+                   int debug) {
   __shared__ CtaShared sh;
-  DirScratch d = carve_dirs(scratch + slot * blockIdx.x, MX, KK);
-  for (int c = blockIdx.x; c < nchains; c += gridDim.x) {
-    const int f0 = chain_off[c], f1 = chain_off[c + 1];
-    const int q = fills[chain[f0]].q;
-    int rq = rank[q];
-    for (int u = f0; u < f1; u++) {
-      const int f = chain[u];
+  const G g = Worker<G>::make(sh);
+  DirScratch d = carve_dirs(scratch + slot * Worker<G>::id(), MX, KK);
+  for (int c = Worker<G>::id(); c < nchains; c += Worker<G>::count()) {
+    const int t0 = aug_off[c], t1 = aug_off[c + 1];
+    const int side0 = aug[t0] & 1;
+    const int cl = side0 ? fills[aug[t0] >> 1].p : fills[aug[t0] >> 1].q;
+    int rc = rank[cl];
+    for (int u = t0; u < t1; u++) {
+      const int f = aug[u] >> 1, side = aug[u] & 1;
       const FillDesc D = fills[f];
-      const FillState S = state[f];
-      if (S.status == 0 && S.r > 0 && tol > 0.0) {
+      const int r = state[f].r, status = state[f].status;
+      const double fro = state[f].fro;
+      if (status == 0 && r > 0 && tol > 0.0) {
         const double* right = D.out + (size_t)D.rows * D.Kf;
-        const double* sv = right + (size_t)D.cols * D.Kf;
-        for (int e = threadIdx.x; e < D.cols * S.r; e += blockDim.x) d.H[e] = right[e];
-        __syncthreads();
-        const int w = new_dirs(d.H, D.cols, S.r, sv, D.Uq, rq, tol * S.fro, d.Q, d.R, d.E, d.sig, d.ord, d.vv, sh);
-        if (debug && threadIdx.x == 0) printf("augq kind=0 p=%d q=%d r=%d +%d -> %d\n", D.p, q, S.r, w, rq + w);
-        rq += w;
+        const double* H0 = side ? D.out : right;
+        const int nU = side ? D.rows : D.cols;
+        for (int e = g.rank(); e < nU * r; e += g.size()) d.H[e] = H0[e];
+        g.sync();
+        const double* wsig = side ? nullptr : right + (size_t)D.cols * D.Kf;
+        const int w = new_dirs(g, d.H, nU, r, wsig, side ? D.Up : D.Uq, rc, tol * fro, d.Q, d.R, d.E, d.sig, d.ord,
+                               d.vv);
+        if (debug && g.rank() == 0)
+          printf("aug kind=%d side=%d p=%d q=%d r=%d +%d -> %d\n", D.kind, side, D.p, D.q, r, w, rc + w);
+        rc += w;
       }
-      if (threadIdx.x == 0) state[f].rq = rq;
-      __syncthreads();
+      if (g.rank() == 0) {
+        if (side) state[f].rp = rc;
+        else state[f].rq = rc;
+      }
+      g.sync();
     }
-    if (threadIdx.x == 0) rank[q] = rq;
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------ K3
-__global__ void __launch_bounds__(CTMAX) p2p_dirs_kernel(const FillDesc* __restrict__ fills,
-                                                      const int* __restrict__ p2p_off, const int* __restrict__ p2p,
-                                                      int ngroups, FillState* state, int* rank, double tol,
-                                                      double* scratch, size_t slot, int MX, int KK, int debug) {
-  __shared__ CtaShared sh;
-  DirScratch d = carve_dirs(scratch + slot * blockIdx.x, MX, KK);
-  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    for (int u = p2p_off[g]; u < p2p_off[g + 1]; u++) {
-      const int f = p2p[u];
-      const FillDesc D = fills[f];
-      const FillState S = state[f];
-      int rq = rank[D.q], rp = rank[D.p];
-      if (S.status == 0 && S.r > 0 && tol > 0.0) {
-        const double* left = D.out;
-        const double* right = D.out + (size_t)D.rows * D.Kf;
-        const double* sv = right + (size_t)D.cols * D.Kf;
-        for (int e = threadIdx.x; e < D.cols * S.r; e += blockDim.x) d.H[e] = right[e];
-        __syncthreads();
-        const int wq = new_dirs(d.H, D.cols, S.r, sv, D.Uq, rq, tol * S.fro, d.Q, d.R, d.E, d.sig, d.ord, d.vv, sh);
-        rq += wq;
-        for (int e = threadIdx.x; e < D.rows * S.r; e += blockDim.x) d.H[e] = left[e];
-        __syncthreads();
-        const int wp = new_dirs(d.H, D.rows, S.r, nullptr, D.Up, rp, tol * S.fro, d.Q, d.R, d.E, d.sig, d.ord, d.vv,
-                                sh);
-        rp += wp;
-        if (debug && threadIdx.x == 0)
-          printf("augq kind=1 p=%d q=%d r=%d +%d -> %d | p +%d -> %d\n", D.p, D.q, S.r, wq, rq, wp, rp);
-      }
-      if (threadIdx.x == 0) {
-        state[f].rq = rq;
-        state[f].rp = rp;
-        rank[D.q] = rq;
-        rank[D.p] = rp;
-      }
-      __syncthreads();
-    }
+    if (g.rank() == 0) rank[cl] = rc;
+    g.sync();
   }
 }
 
 // ------------------------------------------------------------------ K4
-__global__ void __launch_bounds__(CTMAX) delta_kernel(const FillDesc* __restrict__ fills, int nf,
+template <class G>
+__global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) delta_kernel(const FillDesc* __restrict__ fills, int nf,
                                                    const FillState* __restrict__ state, double tol, double* scratch,
                                                    size_t slot, int MX, int KK, int* stats) {
-  double* Eq = scratch + slot * blockIdx.x;
+  __shared__ CtaShared sh;
+  const G g = Worker<G>::make(sh);
+  double* Eq = scratch + slot * Worker<G>::id();
   double* Ep = Eq + (size_t)MX * KK;
-  for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+  for (int f = Worker<G>::id(); f < nf; f += Worker<G>::count()) {
     const FillDesc D = fills[f];
     const FillState S = state[f];
     if (S.status != 0) {
-      if (threadIdx.x == 0) atomicAdd(&stats[1], 1);
+      if (g.rank() == 0) atomicAdd(&stats[1], 1);
       continue;
     }
     const int rows = D.rows, cols = D.cols;
     if (tol == 0.0) {
-      for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+      for (int e = g.rank(); e < rows * cols; e += g.size()) {
         const int a = e % rows, b = e / rows;
         const double v = Fat(D.F, D.ldF, D.transF, a, b);
         if (D.transM) D.M[b + (size_t)a * D.ldM] += v;
@@ -279,30 +291,30 @@ __global__ void __launch_bounds__(CTMAX) delta_kernel(const FillDesc* __restrict
       const int r = S.r, rq = S.rq;
       const double* left = D.out;
       const double* right = D.out + (size_t)rows * D.Kf;
-      cta_gemm(rq, r, cols, 1.0, D.Uq, cols, true, right, cols, false, 0.0, Eq, rq);  // Uq^T B
+      g_gemm(g, rq, r, cols, 1.0, D.Uq, cols, true, right, cols, false, 0.0, Eq, rq);  // Uq^T B
       const double* X = left;
       int rx = rows, ldx = rows;
       if (D.kind == FILL_P2P) {
-        cta_gemm(S.rp, r, rows, 1.0, D.Up, rows, true, left, rows, false, 0.0, Ep, S.rp);  // Up^T A
+        g_gemm(g, S.rp, r, rows, 1.0, D.Up, rows, true, left, rows, false, 0.0, Ep, S.rp);  // Up^T A
         X = Ep;
         rx = S.rp;
         ldx = S.rp;
       }
       // M2L(p,q) += X Eq^T   (owner stores (q,p): M += Eq X^T)
-      if (D.transM) cta_gemm(rq, rx, r, 1.0, Eq, rq, false, X, ldx, true, 1.0, D.M, D.ldM);
-      else cta_gemm(rx, rq, r, 1.0, X, ldx, false, Eq, rq, true, 1.0, D.M, D.ldM);
+      if (D.transM) g_gemm(g, rq, rx, r, 1.0, Eq, rq, false, X, ldx, true, 1.0, D.M, D.ldM);
+      else g_gemm(g, rx, rq, r, 1.0, X, ldx, false, Eq, rq, true, 1.0, D.M, D.ldM);
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    g.sync();
+    for (int e = g.rank(); e < rows * cols; e += g.size()) {
       const int a = e % rows, b = e / rows;
       if (D.transF) D.F[b + (size_t)a * D.ldF] = 0.0;
       else D.F[a + (size_t)b * D.ldF] = 0.0;
     }
-    if (threadIdx.x == 0) {
+    if (g.rank() == 0) {
       atomicAdd(&stats[0], 1);
       atomicMax(&stats[2], S.r);
     }
-    __syncthreads();
+    g.sync();
   }
 }
 
@@ -321,12 +333,23 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     MX = std::max(MX, std::max(D.n_p, D.n_q));
   }
   MX = std::max(MX, std::max(MR, MC));
-  // block size: small fills (leaf level, thousands of them) want many small
-  // CTAs; coarse levels have few, large fills -> wide CTAs shorten each step
+  // Worker shape.  Fine levels (thousands of fills of a few dozen rows): one
+  // warp per fill / chain / pivot, 4 warps per CTA -- no block barriers and
+  // many fills in flight per SM.  Coarse levels (few, large fills): one wide
+  // CTA per fill shortens each step of the dependent chains.
   static const bool narrow = getenv("IFMM_BS128") != nullptr;  // debug: force 128-thread CTAs
+  static const int warp_mx = getenv("IFMM_WARP_MX") ? atoi(getenv("IFMM_WARP_MX")) : 0;
+  const bool wmode = !narrow && MX <= warp_mx;
   const int bs_fill = narrow ? 128 : (MX >= 256 && nf < 2048) ? 512 : (MX >= 128 ? 256 : 128);
   const int bs_dirs = narrow ? 128 : MX >= 256 ? 512 : (MX >= 128 ? 256 : 128);
+  constexpr int WPB = 4;  // warps per CTA in warp mode
   static const bool prof = getenv("IFMM_PROF") != nullptr;
+  static const int jac_reg = getenv("IFMM_JACOBI_REG") ? atoi(getenv("IFMM_JACOBI_REG")) : 0;
+  static bool jac_set = false;
+  if (!jac_set) {
+    CK(cudaMemcpyToSymbolAsync(g_jac_reg, &jac_reg, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    jac_set = true;
+  }
   if (prof) {
     const int one = 1;
     unsigned long long z[16] = {0};
@@ -334,69 +357,97 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     CK(cudaMemcpyToSymbolAsync(g_cyc, z, sizeof z, 0, cudaMemcpyHostToDevice, s));
   }
   const FillDesc* dfd = upload(ws, cb.fills, s, st);
+  // grid for `work` items: CTA workers, or warp workers packed WPB per CTA
+  auto grid_for = [&](int work, int cta_per_sm, int warps_per_sm) {
+    return wmode ? resident_grid(ceil_div(work, WPB), warps_per_sm / WPB) : resident_grid(work, cta_per_sm);
+  };
+  auto workers = [&](int grid) { return wmode ? grid * WPB : grid; };
   // K1
   {
-    const size_t slot = 2 * size_t(MR) * KK + 2 * size_t(MC) * KK + 4 * size_t(KK) * KK + 2 * size_t(MR + MC) +
-                        4 * size_t(KK) + 64;
-    const int grid = resident_grid(nf, 8);
-    double* scr = ws.alloc_n<double>(slot * grid);
-    aca_recompress_kernel<<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr, slot, MR, MC,
-                                                   KK);
-    CK_LAUNCH();
+    auto k1_slot = [&](int kk) {
+      return 2 * size_t(MR) * kk + 2 * size_t(MC) * kk + 4 * size_t(kk) * kk + 2 * size_t(MR + MC) +
+             4 * size_t(kk) + 64;
+    };
+    if (wmode) {
+      const int kw = std::min(KK, WARP_KCAP);
+      const size_t slot = k1_slot(kw);
+      const int grid = grid_for(nf, 8, 32);
+      double* scr = ws.alloc_n<double>(slot * workers(grid));
+      aca_recompress_kernel<WarpGroup><<<grid, 32 * WPB, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
+                                                                   slot, MR, MC, kw, 0);
+      CK_LAUNCH();
+      if (KK > kw) {  // fills whose ACA outgrew the warp's cross cap
+        const size_t cslot = k1_slot(KK);
+        const int cgrid = resident_grid(nf, 2);
+        double* cscr = ws.alloc_n<double>(cslot * cgrid);
+        aca_recompress_kernel<CtaGroup><<<cgrid, 128, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, cscr,
+                                                               cslot, MR, MC, KK, 1);
+        CK_LAUNCH();
+      }
+    } else {
+      const size_t slot = k1_slot(KK);
+      const int grid = resident_grid(nf, 8);
+      double* scr = ws.alloc_n<double>(slot * grid);
+      aca_recompress_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
+                                                               slot, MR, MC, KK, 0);
+      CK_LAUNCH();
+    }
   }
   const size_t dslot = 3 * size_t(MX) * KK + size_t(KK) * KK + 3 * size_t(KK) + 64;
-  // K2
-  const int nch = int(cb.chain_off.size()) - 1;
-  if (nch > 0) {
-    const int* dco = upload(ws, cb.chain_off, s, st);
-    const int* dch = upload(ws, cb.chain, s, st);
-    const int grid = resident_grid(nch, 8);
-    double* scr = ws.alloc_n<double>(dslot * grid);
-    hybrid_dirs_kernel<<<grid, bs_dirs, 0, s>>>(dfd, dco, dch, nch, d_state, d_rank, tol, scr, dslot, MX, KK, debug);
-    CK_LAUNCH();
-  }
-  // K3: P2P fills in dependency waves.  Within a pivot, a fill waits only for
-  // earlier fills sharing one of its two clusters (they augment the same
-  // basis); fills of different pivots never share clusters.
-  const int ng = int(cb.p2p_off.size()) - 1;
-  if (ng > 0 && !cb.p2p.empty()) {
-    std::vector<int> wave(cb.p2p.size(), 0);
-    int nwave = 0;
-    static const bool serial = getenv("IFMM_P2P_SERIAL") != nullptr;  // debug: one P2P fill per wave and pivot
-    for (int g = 0; g < ng; g++)
-      for (int u = cb.p2p_off[g]; u < cb.p2p_off[g + 1]; u++) {
-        const FillDesc& D = cb.fills[cb.p2p[u]];
-        int w = 0;
-        for (int v = cb.p2p_off[g]; v < u; v++) {
-          const FillDesc& E = cb.fills[cb.p2p[v]];
-          if (E.p == D.p || E.p == D.q || E.q == D.p || E.q == D.q || serial) w = std::max(w, wave[v] + 1);
-        }
-        wave[u] = w;
-        nwave = std::max(nwave, w + 1);
+  const int bs_d = wmode ? 32 * WPB : bs_dirs;
+  // K2+K3: per-cluster augmentation chains.  Order inside a chain: the
+  // cluster's hybrid fills (sorted), then the P2P fills touching it in the
+  // pivot's pair order; clusters of different pivots of a batch are disjoint.
+  {
+    int maxc = 0;
+    for (const FillDesc& D : cb.fills) maxc = std::max(maxc, std::max(D.p, D.q));
+    std::vector<int> cid(size_t(maxc) + 1, -1);
+    std::vector<std::vector<int>> tasks;
+    auto push = [&](int cl, int task) {
+      int& c = cid[cl];
+      if (c < 0) {
+        c = int(tasks.size());
+        tasks.emplace_back();
       }
-    const int grid_max = resident_grid(int(cb.p2p.size()), 8);
-    double* scr = ws.alloc_n<double>(dslot * grid_max);
-    for (int w = 0; w < nwave; w++) {
+      tasks[c].push_back(task);
+    };
+    const int nch = int(cb.chain_off.size()) - 1;
+    for (int c = 0; c < nch; c++)
+      for (int u = cb.chain_off[c]; u < cb.chain_off[c + 1]; u++) push(cb.fills[cb.chain[u]].q, cb.chain[u] * 2);
+    for (int f : cb.p2p) {
+      push(cb.fills[f].q, f * 2);
+      push(cb.fills[f].p, f * 2 + 1);
+    }
+    if (!tasks.empty()) {
       std::vector<int> off(1, 0), lst;
-      for (size_t u = 0; u < cb.p2p.size(); u++)
-        if (wave[u] == w) {
-          lst.push_back(cb.p2p[u]);
-          off.push_back(int(lst.size()));
-        }
-      const int* dpo = upload(ws, off, s, st);
-      const int* dpp = upload(ws, lst, s, st);
-      const int n = int(lst.size());
-      p2p_dirs_kernel<<<std::min(n, grid_max), bs_dirs, 0, s>>>(dfd, dpo, dpp, n, d_state, d_rank, tol, scr, dslot,
-                                                                 MX, KK, debug);
+      lst.reserve(2 * cb.fills.size());
+      for (auto& t : tasks) {
+        lst.insert(lst.end(), t.begin(), t.end());
+        off.push_back(int(lst.size()));
+      }
+      const int* doff = upload(ws, off, s, st);
+      const int* dlst = upload(ws, lst, s, st);
+      const int n = int(tasks.size());
+      const int grid = grid_for(n, 8, 32);
+      double* scr = ws.alloc_n<double>(dslot * workers(grid));
+      if (wmode)
+        augment_kernel<WarpGroup><<<grid, bs_d, 0, s>>>(dfd, doff, dlst, n, d_state, d_rank, tol, scr, dslot, MX, KK,
+                                                          debug);
+      else
+        augment_kernel<CtaGroup><<<grid, bs_d, 0, s>>>(dfd, doff, dlst, n, d_state, d_rank, tol, scr, dslot, MX, KK,
+                                                         debug);
       CK_LAUNCH();
     }
   }
   // K4
   {
     const size_t slot = 2 * size_t(MX) * KK + 64;
-    const int grid = resident_grid(nf, 8);
-    double* scr = ws.alloc_n<double>(slot * grid);
-    delta_kernel<<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats);
+    const int grid = grid_for(nf, 8, 32);
+    double* scr = ws.alloc_n<double>(slot * workers(grid));
+    if (wmode)
+      delta_kernel<WarpGroup><<<grid, 32 * WPB, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats);
+    else
+      delta_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats);
     CK_LAUNCH();
   }
   if (prof) {

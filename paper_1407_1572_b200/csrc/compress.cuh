@@ -3,9 +3,10 @@
 // The reference compresses the fills of one elimination sequentially.  Their
 // true dependencies are narrower, and the batch is split along them:
 //   K1 ACA + QR/SVD recompression         -- every fill independent
-//   K2 new directions of hybrid fills      -- serial only per (pivot, q) chain
-//                                            (fills augment U_q in sorted order)
-//   K3 new directions of P2P fills         -- after all hybrids, serial per pivot
+//   K2+K3 basis augmentation               -- serial only per cluster: chain c
+//                                            holds the steps that append to U_c
+//                                            (hybrid fills into c, then the
+//                                            sides of the P2P fills touching c)
 //   K4 M2L absorption + drop               -- every fill independent: the basis
 //                                            prefix each fill saw is recorded
 // K1..K4 reproduce the reference's sequential order exactly (augmentation only

@@ -1,8 +1,11 @@
-// CTA-cooperative dense linear algebra on column-major matrices held in global
-// (L1/L2-resident) scratch: Householder QR, one-sided Jacobi SVD, partially
-// pivoted ACA.  Every routine must be called by all threads of the block.
-// Used by the fill-in compression kernel (one CTA per pivot) and the
-// Chebyshev basis construction (one CTA per cluster).
+// Cooperative dense linear algebra on column-major matrices held in global
+// (L1/L2-resident) scratch: DMMA GEMM, Householder QR, one-sided Jacobi SVD,
+// partially pivoted ACA.  Every routine is a template over an execution group
+// G -- a whole CTA (CtaGroup) or a single warp (WarpGroup) -- and must be
+// called by all threads of the group.  The compression kernels run one warp
+// per fill for the many small fills of the fine levels (no block barriers,
+// 4-16x more fills in flight per SM) and one CTA per fill at coarse levels;
+// the Chebyshev basis construction uses CTAs.
 #pragma once
 #include "common.cuh"
 
@@ -16,16 +19,56 @@ struct CtaShared {
   double dval[4];
 };
 
+__device__ __forceinline__ ArgMax warp_argmax(ArgMax v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax w;
+    w.a = __shfl_xor_sync(0xffffffffu, v.a, o);
+    w.i = __shfl_xor_sync(0xffffffffu, v.i, o);
+    v = argmax_merge(v, w);
+  }
+  return v;
+}
+
+struct CtaGroup {
+  static constexpr int kMaxThreads = 512, kMinBlocks = 2;  // launch bounds of kernels templated on the group
+  CtaShared& sh;
+  __device__ int rank() const { return threadIdx.x; }
+  __device__ int size() const { return blockDim.x; }
+  __device__ int lane() const { return threadIdx.x & 31; }
+  __device__ int warp() const { return threadIdx.x >> 5; }
+  __device__ int nwarps() const { return blockDim.x >> 5; }
+  __device__ void sync() const { __syncthreads(); }
+  __device__ double sum(double v) const { return block_sum(v, sh.red); }
+  __device__ ArgMax argmax(ArgMax v) const { return block_argmax(v, sh.am); }
+  __device__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
+  __device__ static CtaGroup make_for_test(CtaShared& sh) { return CtaGroup{sh}; }
+};
+
+struct WarpGroup {
+  static constexpr int kMaxThreads = 128, kMinBlocks = 4;
+  __device__ int rank() const { return threadIdx.x & 31; }
+  __device__ int size() const { return 32; }
+  __device__ int lane() const { return threadIdx.x & 31; }
+  __device__ int warp() const { return 0; }
+  __device__ int nwarps() const { return 1; }
+  __device__ void sync() const { __syncwarp(); }
+  __device__ double sum(double v) const { return warp_sum(v); }
+  __device__ ArgMax argmax(ArgMax v) const { return warp_argmax(v); }
+  __device__ bool any(bool p) const { return __any_sync(0xffffffffu, p) != 0; }
+  __device__ static WarpGroup make_for_test(CtaShared&) { return WarpGroup{}; }
+};
+
 // ------------------------------------------------------------- small helpers
 // CTA-cooperative DMMA GEMM (mma.sync.m8n8k4.f64): every warp owns 16x16
 // output tiles (2x2 fragments); fragments are loaded straight from L1/L2.
 // One DMMA does 512 flops for 2 loads per lane, vs 2 flops per 2 loads for a
 // scalar loop -- the projections and deltas of the compression are otherwise
 // L1-throughput bound.
-template <bool TA, bool TB>
-__device__ inline void cta_mma_gemm(int rows, int cols, int kk, double alpha, const double* __restrict__ A, int lda,
+template <bool TA, bool TB, class G>
+__device__ inline void g_mma_gemm(const G& g, int rows, int cols, int kk, double alpha, const double* __restrict__ A, int lda,
                                     const double* __restrict__ B, int ldb, double beta, double* Y, int ldy) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = g.lane(), warp = g.warp(), nw = g.nwarps();
   const int tm = (rows + 15) >> 4, tn = (cols + 15) >> 4;
   const int fr = lane >> 2, fk = lane & 3;
   for (int tile = warp; tile < tm * tn; tile += nw) {
@@ -65,28 +108,29 @@ __device__ inline void cta_mma_gemm(int rows, int cols, int kk, double alpha, co
           }
         }
   }
-  __syncthreads();
+  g.sync();
 }
 
 // Y(rows x cols, ldy) = alpha * op(A) * op(B) + beta*Y for the small products
 // inside compression; DMMA tiles when the shape is worth it.
 // opA: A is (rows x kk) if !ta else stored (kk x rows).
-__device__ inline void cta_gemm(int rows, int cols, int kk, double alpha, const double* A, int lda, bool ta,
+template <class G>
+__device__ inline void g_gemm(const G& g, int rows, int cols, int kk, double alpha, const double* A, int lda, bool ta,
                                 const double* B, int ldb, bool tb, double beta, double* Y, int ldy) {
   if (rows >= 8 && cols >= 8 && kk >= 8) {
     if (ta) {
-      if (tb) cta_mma_gemm<true, true>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
-      else cta_mma_gemm<true, false>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+      if (tb) g_mma_gemm<true, true>(g, rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+      else g_mma_gemm<true, false>(g, rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
     } else {
-      if (tb) cta_mma_gemm<false, true>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
-      else cta_mma_gemm<false, false>(rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+      if (tb) g_mma_gemm<false, true>(g, rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
+      else g_mma_gemm<false, false>(g, rows, cols, kk, alpha, A, lda, B, ldb, beta, Y, ldy);
     }
     return;
   }
   if (ta && !tb) {
     // Y = A^T B: both operands are read down contiguous columns -> one warp per
     // output, lanes stride the contraction (coalesced), warp-shuffle reduction
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = g.lane(), warp = g.warp(), nw = g.nwarps();
     for (int o = warp; o < rows * cols; o += nw) {
       const int i = o % rows, j = o / rows;
       const double* a = A + (size_t)i * lda;
@@ -99,10 +143,10 @@ __device__ inline void cta_gemm(int rows, int cols, int kk, double alpha, const 
         *y = (beta == 0.0 ? 0.0 : beta * *y) + alpha * s;
       }
     }
-    __syncthreads();
+    g.sync();
     return;
   }
-  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+  for (int e = g.rank(); e < rows * cols; e += g.size()) {
     const int i = e % rows, j = e / rows;
     double s = 0.0;
     for (int t = 0; t < kk; t++) {
@@ -113,29 +157,30 @@ __device__ inline void cta_gemm(int rows, int cols, int kk, double alpha, const 
     double* y = Y + i + (size_t)j * ldy;
     *y = (beta == 0.0 ? 0.0 : beta * *y) + alpha * s;
   }
-  __syncthreads();
+  g.sync();
 }
 
 // X(n x k) -= U (U^T X), U n x r.  Scratch E >= r*k.
-__device__ inline void cta_project_out(double* X, int ldx, int n, int k, const double* U, int ldu, int r,
+template <class G>
+__device__ inline void g_project_out(const G& g, double* X, int ldx, int n, int k, const double* U, int ldu, int r,
                                        double* E) {
   if (r == 0 || k == 0) return;
-  cta_gemm(r, k, n, 1.0, U, ldu, true, X, ldx, false, 0.0, E, r);
-  cta_gemm(n, k, r, -1.0, U, ldu, false, E, r, false, 1.0, X, ldx);
+  g_gemm(g, r, k, n, 1.0, U, ldu, true, X, ldx, false, 0.0, E, r);
+  g_gemm(g, n, k, r, -1.0, U, ldu, false, E, r, false, 1.0, X, ldx);
 }
 
 // ------------------------------------------------------------- Householder QR
 // A (m x k, lda) is overwritten by the reflectors.  Outputs R (k x k, ld k,
 // upper) and, if Q != nullptr, the thin Q (m x k, ldq).  vv: scratch >= k.
-__device__ inline void cta_qr(double* A, int m, int k, int lda, double* R, double* Q, int ldq, double* vv,
-                              CtaShared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+template <class G>
+__device__ inline void g_qr(const G& g, double* A, int m, int k, int lda, double* R, double* Q, int ldq, double* vv) {
+  const int lane = g.lane(), warp = g.warp(), nw = g.nwarps();
   for (int j = 0; j < k && j < m; j++) {
     double* x = A + j + (size_t)j * lda;
     const int len = m - j;
     double s = 0.0;
-    for (int i = threadIdx.x; i < len; i += blockDim.x) s += x[i] * x[i];
-    s = block_sum(s, sh.red);
+    for (int i = g.rank(); i < len; i += g.size()) s += x[i] * x[i];
+    s = g.sum(s);
     const double alpha = sqrt(s);
     const double x0 = x[0];
     double beta = 0.0, vtv = 0.0;
@@ -144,13 +189,13 @@ __device__ inline void cta_qr(double* A, int m, int k, int lda, double* R, doubl
       // v = x - beta e1 ; vtv = s - x0^2 + (x0-beta)^2
       vtv = s - x0 * x0 + (x0 - beta) * (x0 - beta);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    g.sync();
+    if (g.rank() == 0) {
       x[0] = x0 - beta;
       vv[j] = vtv;
       R[j + (size_t)j * k] = alpha > 0.0 ? beta : x0;
     }
-    __syncthreads();
+    g.sync();
     if (vtv > 0.0) {
       for (int c = j + 1 + warp; c < k; c += nw) {
         double* y = A + j + (size_t)c * lda;
@@ -161,22 +206,22 @@ __device__ inline void cta_qr(double* A, int m, int k, int lda, double* R, doubl
         for (int i = lane; i < len; i += 32) y[i] -= f * x[i];
       }
     }
-    __syncthreads();
+    g.sync();
   }
   // R strictly-upper part
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+  for (int e = g.rank(); e < k * k; e += g.size()) {
     const int i = e % k, c = e / k;
     if (i < c) R[i + (size_t)c * k] = (i < m) ? A[i + (size_t)c * lda] : 0.0;
     else if (i > c) R[i + (size_t)c * k] = 0.0;
     else if (i >= m) R[i + (size_t)c * k] = 0.0;
   }
-  __syncthreads();
+  g.sync();
   if (Q == nullptr) return;
-  for (int e = threadIdx.x; e < m * k; e += blockDim.x) {
+  for (int e = g.rank(); e < m * k; e += g.size()) {
     const int i = e % m, c = e / m;
     Q[i + (size_t)c * ldq] = (i == c) ? 1.0 : 0.0;
   }
-  __syncthreads();
+  g.sync();
   for (int j = min(k, m) - 1; j >= 0; j--) {
     const double vtv = vv[j];
     if (vtv <= 0.0) continue;
@@ -190,7 +235,7 @@ __device__ inline void cta_qr(double* A, int m, int k, int lda, double* R, doubl
       const double f = 2.0 * d / vtv;
       for (int i = lane; i < len; i += 32) y[i] -= f * x[i];
     }
-    __syncthreads();
+    g.sync();
   }
 }
 
@@ -200,22 +245,28 @@ __device__ inline void cta_qr(double* A, int m, int k, int lda, double* R, doubl
 // if non-null, sig[j] = ||A_out(:,j)||, ord[0..n) = column indices sorted by
 // decreasing sig (ties: lower index first).  Round-robin pairing; warps own
 // disjoint column pairs.
-__device__ inline void cta_jacobi(double* A, int m, int n, int lda, double* V, int ldv, double* sig, int* ord,
-                                  CtaShared& sh, int max_sweeps = 40) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+template <class G>
+__device__ inline void g_jacobi(const G& g, double* A, int m, int n, int lda, double* V, int ldv, double* sig,
+                                int* ord, int max_sweeps = 40) {
+  const int lane = g.lane(), warp = g.warp(), nw = g.nwarps();
   if (V)
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) V[(e % n) + (size_t)(e / n) * ldv] = (e % n == e / n);
+    for (int e = g.rank(); e < n * n; e += g.size()) V[(e % n) + (size_t)(e / n) * ldv] = (e % n == e / n);
   const int nn = n + (n & 1);  // even number of players (dummy = n)
-  __syncthreads();
+  g.sync();
   for (int sweep = 0; sweep < max_sweeps && n > 1; sweep++) {
-    if (threadIdx.x == 0) sh.flag = 0;
-    __syncthreads();
+    bool rot = false;
     for (int round = 0; round < nn - 1; round++) {
       for (int pr = warp; pr < nn / 2; pr += nw) {
         // circle method: player nn-1 fixed, others rotate
-        int a = (pr == 0) ? nn - 1 : (round + pr) % (nn - 1);
-        int b = (round + nn - 1 - pr) % (nn - 1);
-        if (pr == 0) b = round % (nn - 1);
+        // (round + pr) and (round + nn - 1 - pr) are < 2 (nn - 1): one
+        // conditional subtraction instead of an integer modulo
+        int a = round + pr, b = round + nn - 1 - pr;
+        if (a >= nn - 1) a -= nn - 1;
+        if (b >= nn - 1) b -= nn - 1;
+        if (pr == 0) {
+          a = nn - 1;
+          b = round;
+        }
         if (a >= n || b >= n || a == b) continue;
         if (a > b) { int t = a; a = b; b = t; }
         double* x = A + (size_t)a * lda;
@@ -252,15 +303,13 @@ __device__ inline void cta_jacobi(double* A, int m, int n, int lda, double* V, i
             vy[i] = s * xi + c * yi;
           }
         }
-        if (lane == 0) sh.flag = 1;
+        rot = true;
       }
-      __syncthreads();
+      g.sync();
     }
-    const int rotated = sh.flag;
-    __syncthreads();
-    if (!rotated) {
+    if (!g.any(rot)) {
 #ifdef IFMM_JACOBI_STATS
-      IFMM_JACOBI_STATS(sweep + 1, n);
+      IFMM_JACOBI_STATS(sweep + 1, n, g.rank() == 0);
 #endif
       break;
     }
@@ -272,14 +321,145 @@ __device__ inline void cta_jacobi(double* A, int m, int n, int lda, double* V, i
     s = warp_sum(s);
     if (lane == 0) sig[c] = sqrt(s);
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+  g.sync();
+  for (int c = g.rank(); c < n; c += g.size()) {
     int rank = 0;
     const double sc = sig[c];
     for (int o = 0; o < n; o++) rank += (sig[o] > sc) || (sig[o] == sc && o < c);
     ord[rank] = c;
   }
-  __syncthreads();
+  g.sync();
+}
+
+// Register-resident one-sided Jacobi for m <= M, n <= 32, run by ONE warp:
+// lane j holds column j of A (and of V).  Round r of the circle method pairs
+// player r with nn-1 and p with (2r - p) mod (nn-1) otherwise (nn = n rounded
+// up to even; nn-1 rounds cover every pair once).  Partners exchange columns
+// with shuffles and both compute the pair's rotation from the same values in
+// the same order, so they agree bit for bit -- no reductions, no barriers.
+// Same rotation formula and skip rules as g_jacobi.
+template <int M, bool WANT_V>
+__device__ __noinline__ void warp_jacobi_reg(double* A, int m, int n, int lda, double* V, int ldv, double* sig,
+                                             int* ord, int max_sweeps) {
+  constexpr bool KEEP = M <= 16;  // keep the partner column in registers
+  const int lane = threadIdx.x & 31;
+  const bool own = lane < n;
+  double x[M], v[WANT_V ? M : 1];
+#pragma unroll
+  for (int i = 0; i < M; i++) x[i] = (own && i < m) ? A[i + (size_t)lane * lda] : 0.0;
+  if (WANT_V) {
+#pragma unroll
+    for (int i = 0; i < M; i++) v[i] = (i == lane) ? 1.0 : 0.0;
+  }
+  const int nn = n + (n & 1), np = nn - 1;
+  for (int sweep = 0; sweep < max_sweeps && n > 1; sweep++) {
+    bool rot = false;
+    for (int r = 0; r < np; r++) {
+      int P;
+      if (lane == np) P = r;
+      else if (lane == r) P = np;
+      else {
+        P = 2 * r - lane;  // in (-np, 2 np)
+        if (P < 0) P += np;
+        if (P >= np) P -= np;
+      }
+      const bool act = own && P < n;
+      const int src = act ? P : lane;
+      const bool low = lane < P;
+      double y[KEEP ? M : 1];
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int i = 0; i < M; i++) {
+        if (i < m) {  // warp-uniform
+          const double o = __shfl_sync(0xffffffffu, x[i], src);
+          if (KEEP) y[i] = o;
+          const double xl = low ? x[i] : o, yh = low ? o : x[i];
+          al = fma(xl, xl, al);
+          be = fma(yh, yh, be);
+          ga = fma(xl, yh, ga);
+        }
+      }
+      double c = 1.0, sn = 0.0;
+      bool doit = act && !(ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be));
+      if (doit) {
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        if (fabs(t) < 1e-16) doit = false;
+        c = 1.0 / sqrt(1.0 + t * t);
+        sn = c * t;
+      }
+      rot |= doit;
+      if (!__any_sync(0xffffffffu, doit)) continue;
+#pragma unroll
+      for (int i = 0; i < M; i++) {
+        if (i < m) {
+          const double o = KEEP ? y[i] : __shfl_sync(0xffffffffu, x[i], src);
+          if (doit) x[i] = low ? c * x[i] - sn * o : sn * o + c * x[i];
+        }
+      }
+      if (WANT_V) {
+#pragma unroll
+        for (int i = 0; i < M; i++) {
+          if (i < n) {
+            const double o = __shfl_sync(0xffffffffu, v[i], src);
+            if (doit) v[i] = low ? c * v[i] - sn * o : sn * o + c * v[i];
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, rot)) {
+#ifdef IFMM_JACOBI_STATS
+      IFMM_JACOBI_STATS(sweep + 1, n, lane == 0);
+#endif
+      break;
+    }
+  }
+  double nrm = 0.0;
+#pragma unroll
+  for (int i = 0; i < M; i++) nrm = fma(x[i], x[i], nrm);
+  nrm = sqrt(nrm);
+  int rank = 0;
+  for (int o = 0; o < n; o++) {
+    const double so = __shfl_sync(0xffffffffu, nrm, o);
+    rank += (so > nrm) || (so == nrm && o < lane);
+  }
+  if (own) {
+#pragma unroll
+    for (int i = 0; i < M; i++)
+      if (i < m) A[i + (size_t)lane * lda] = x[i];
+    if (WANT_V) {
+#pragma unroll
+      for (int i = 0; i < M; i++)
+        if (i < n) V[i + (size_t)lane * ldv] = v[i];
+    }
+    sig[lane] = nrm;
+    ord[rank] = lane;
+  }
+}
+
+// Jacobi entry used by the compression: register path for small problems
+// (warp 0 of a CTA group does it while the others wait), else g_jacobi.
+template <class G>
+__device__ inline void g_jacobi_small(const G& g, double* A, int m, int n, int lda, double* V, int ldv, double* sig,
+                                      int* ord, bool use_reg = true, int max_sweeps = 40) {
+  // rows held per lane: m (plus n for the V columns)
+  const int mm = V ? max(m, n) : m;
+  // measured: the single-warp register path wins ~2x for <= 16 columns and
+  // loses to the CTA's warp-parallel pair rounds beyond that
+  if (use_reg && n <= 16 && mm <= 16) {
+    if (g.warp() == 0) {
+      if (mm <= 8) {
+        if (V) warp_jacobi_reg<8, true>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
+        else warp_jacobi_reg<8, false>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
+      } else if (mm <= 16) {
+        if (V) warp_jacobi_reg<16, true>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
+        else warp_jacobi_reg<16, false>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
+      }
+    }
+    g.sync();
+    return;
+  }
+  g_jacobi(g, A, m, n, lda, V, ldv, sig, ord, max_sweeps);
 }
 
 // Smallest r with s[r]/s[0] < tol (s sorted decreasing); ifmm/lowrank.py:137-144
@@ -309,56 +489,54 @@ __device__ inline double Fat(const double* F, int ld, int trans, int a, int b) {
   return trans ? F[b + (size_t)a * ld] : F[a + (size_t)b * ld];
 }
 
-__device__ inline AcaOut cta_aca(const double* F, int ld, int trans, int m, int n, double tol,
+template <class G>
+__device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, int m, int n, double tol,
                                  const int* probes, int nprobe, double* Uc, double* Vc, int kmax, double* rr,
-                                 double* cc, int* usedr, int* usedc, double* dots, CtaShared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                                 double* cc, int* usedr, int* usedc, double* dots) {
+  const int lane = g.lane(), warp = g.warp(), nw = g.nwarps();
   const int full = min(m, n);
   AcaOut out{0, 0};
   if (m == 0 || n == 0) {
     out.converged = 0;
     return out;
   }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) usedr[i] = 0;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) usedc[j] = 0;
+  for (int i = g.rank(); i < m; i += g.size()) usedr[i] = 0;
+  for (int j = g.rank(); j < n; j += g.size()) usedc[j] = 0;
   // first row: probe with the largest max-abs entry (first in probe order on ties)
-  if (threadIdx.x == 0) sh.ival[0] = probes[0];
-  __syncthreads();
+  int next;
   {
     double best = -1.0;
     int bi = probes[0];
     for (int t = 0; t < nprobe; t++) {
       const int i = probes[t];
       ArgMax am{-1.0, -1};
-      for (int j = threadIdx.x; j < n; j += blockDim.x) am = argmax_merge(am, ArgMax{fabs(Fat(F, ld, trans, i, j)), j});
-      am = block_argmax(am, sh.am);
+      for (int j = g.rank(); j < n; j += g.size()) am = argmax_merge(am, ArgMax{fabs(Fat(F, ld, trans, i, j)), j});
+      am = g.argmax(am);
       if (am.a > best) {
         best = am.a;
         bi = i;
       }
     }
-    if (threadIdx.x == 0) sh.ival[0] = bi;
+    next = bi;  // identical in every thread: the argmax is broadcast
   }
-  __syncthreads();
-  int next = sh.ival[0];
   int k = 0, strikes = 0, nused = 0;
   double nsq = 0.0;
   bool done = false;
   const int kcap = min(full, kmax);
   while (k < kcap) {
     const int i = next;
-    if (threadIdx.x == 0) usedr[i] = 1;
+    if (g.rank() == 0) usedr[i] = 1;
     nused++;
     // residual row (sequential subtraction over crosses, as the reference)
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int j = g.rank(); j < n; j += g.size()) {
       double v = Fat(F, ld, trans, i, j);
       for (int t = 0; t < k; t++) v = __dsub_rn(v, __dmul_rn(Uc[i + (size_t)t * m], Vc[j + (size_t)t * n]));
       rr[j] = usedc[j] ? 0.0 : v;
     }
-    __syncthreads();
+    g.sync();
     ArgMax am{-1.0, -1};
-    for (int j = threadIdx.x; j < n; j += blockDim.x) am = argmax_merge(am, ArgMax{fabs(rr[j]), j});
-    am = block_argmax(am, sh.am);
+    for (int j = g.rank(); j < n; j += g.size()) am = argmax_merge(am, ArgMax{fabs(rr[j]), j});
+    am = g.argmax(am);
     const int j = am.i;
     const double piv = rr[j];
     const double tiny = nsq > 0.0 ? 1e-15 * sqrt(nsq) : 1e-300;
@@ -371,9 +549,9 @@ __device__ inline AcaOut cta_aca(const double* F, int ld, int trans, int m, int 
       // deterministic substitute for the reference's random restart row:
       // the lowest-index unused row
       ArgMax lo{-1.0, -1};
-      for (int r = threadIdx.x; r < m; r += blockDim.x)
+      for (int r = g.rank(); r < m; r += g.size())
         if (!usedr[r]) lo = argmax_merge(lo, ArgMax{1.0, r});
-      lo = block_argmax(lo, sh.am);
+      lo = g.argmax(lo);
       next = lo.i;
       if (next < 0) {
         done = true;
@@ -382,22 +560,22 @@ __device__ inline AcaOut cta_aca(const double* F, int ld, int trans, int m, int 
       continue;
     }
     strikes = 0;
-    if (threadIdx.x == 0) usedc[j] = 1;
+    if (g.rank() == 0) usedc[j] = 1;
     // residual column, new cross
     double* u = Uc + (size_t)k * m;
     double* v = Vc + (size_t)k * n;
-    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    for (int r = g.rank(); r < m; r += g.size()) {
       double x = Fat(F, ld, trans, r, j);
       for (int t = 0; t < k; t++) x = __dsub_rn(x, __dmul_rn(Vc[j + (size_t)t * n], Uc[r + (size_t)t * m]));
       u[r] = x / piv;
     }
-    for (int c = threadIdx.x; c < n; c += blockDim.x) v[c] = rr[c];
-    __syncthreads();
+    for (int c = g.rank(); c < n; c += g.size()) v[c] = rr[c];
+    g.sync();
     double su = 0.0, sv = 0.0;
-    for (int r = threadIdx.x; r < m; r += blockDim.x) su += u[r] * u[r];
-    for (int c = threadIdx.x; c < n; c += blockDim.x) sv += v[c] * v[c];
-    su = block_sum(su, sh.red);
-    sv = block_sum(sv, sh.red);
+    for (int r = g.rank(); r < m; r += g.size()) su += u[r] * u[r];
+    for (int c = g.rank(); c < n; c += g.size()) sv += v[c] * v[c];
+    su = g.sum(su);
+    sv = g.sum(sv);
     const double csq = su * sv;
     if (k > 0) {
       for (int t = warp; t < k; t += nw) {
@@ -410,11 +588,11 @@ __device__ inline AcaOut cta_aca(const double* F, int ld, int trans, int m, int 
         dv = warp_sum(dv);
         if (lane == 0) dots[t] = fabs(du) * fabs(dv);
       }
-      __syncthreads();
+      g.sync();
       double cross = 0.0;
       for (int t = 0; t < k; t++) cross += dots[t];
       nsq += csq + 2.0 * cross;
-      __syncthreads();
+      g.sync();
     } else {
       nsq = csq;
     }
@@ -424,22 +602,41 @@ __device__ inline AcaOut cta_aca(const double* F, int ld, int trans, int m, int 
       break;
     }
     ArgMax nx{-1.0, -1};
-    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    for (int r = g.rank(); r < m; r += g.size()) {
       const double a = (usedr[r] || r == i) ? -1.0 : fabs(u[r]);
       nx = argmax_merge(nx, ArgMax{a, r});
     }
-    nx = block_argmax(nx, sh.am);
+    nx = g.argmax(nx);
     if (nx.i < 0 || nx.a < 0.0) {
       done = true;
       break;
     }
     next = nx.i;
   }
-  __syncthreads();
+  g.sync();
   out.k = k;
   out.converged = done ? 1 : 0;
   // not converged below full rank because of the kmax cap -> report as not converged
   return out;
+}
+
+// CTA-wide entry points (basis construction, test hooks)
+__device__ inline void cta_gemm(int rows, int cols, int kk, double alpha, const double* A, int lda, bool ta,
+                                const double* B, int ldb, bool tb, double beta, double* Y, int ldy, CtaShared& sh) {
+  g_gemm(CtaGroup{sh}, rows, cols, kk, alpha, A, lda, ta, B, ldb, tb, beta, Y, ldy);
+}
+__device__ inline void cta_qr(double* A, int m, int k, int lda, double* R, double* Q, int ldq, double* vv,
+                              CtaShared& sh) {
+  g_qr(CtaGroup{sh}, A, m, k, lda, R, Q, ldq, vv);
+}
+__device__ inline void cta_jacobi(double* A, int m, int n, int lda, double* V, int ldv, double* sig, int* ord,
+                                  CtaShared& sh, int max_sweeps = 40) {
+  g_jacobi(CtaGroup{sh}, A, m, n, lda, V, ldv, sig, ord, max_sweeps);
+}
+__device__ inline AcaOut cta_aca(const double* F, int ld, int trans, int m, int n, double tol, const int* probes,
+                                 int nprobe, double* Uc, double* Vc, int kmax, double* rr, double* cc, int* usedr,
+                                 int* usedc, double* dots, CtaShared& sh) {
+  return g_aca(CtaGroup{sh}, F, ld, trans, m, n, tol, probes, nprobe, Uc, Vc, kmax, rr, cc, usedr, usedc, dots);
 }
 
 }  // namespace ifmm

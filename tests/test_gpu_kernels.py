@@ -16,6 +16,14 @@ def L():
     return _lib
 
 
+@pytest.fixture(params=["cta", "warp"])
+def group(request, L):
+    """Run the small-matrix hooks CTA-wide or on one warp (fine-level workers)."""
+    L.check(L.lib.ifmm_test_set_group(1 if request.param == "warp" else 0))
+    yield request.param
+    L.check(L.lib.ifmm_test_set_group(0))
+
+
 @pytest.mark.parametrize("ta,tb,tc", [(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 1), (1, 0, 1)])
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (64, 64, 16), (97, 130, 53), (200, 17, 300)])
 def test_gemm(L, ta, tb, tc, M, N, K):
@@ -74,8 +82,9 @@ def test_gj_flags_singular(L):
     assert info[0] == 3
 
 
-@pytest.mark.parametrize("m,n", [(16, 16), (432, 16), (64, 40), (300, 64), (7, 3)])
-def test_jacobi_svd(L, m, n):
+@pytest.mark.parametrize("m,n", [(16, 16), (432, 16), (64, 40), (300, 64), (7, 3), (12, 9), (8, 8), (30, 30), (5, 14),
+                                 (32, 32), (2, 2), (1, 1)])
+def test_jacobi_svd(L, group, m, n):
     rng = np.random.default_rng(m + n)
     A = rng.standard_normal((m, n)) @ np.diag(np.logspace(0, -12, n))
     a = np.asfortranarray(A).copy(order="F")
@@ -83,13 +92,15 @@ def test_jacobi_svd(L, m, n):
     sig = np.empty(n)
     L.check(L.lib.ifmm_test_jacobi(L.ptr(a), m, n, L.ptr(V), L.ptr(sig)))
     s_ref = np.linalg.svd(A, compute_uv=False)
-    assert np.allclose(np.sort(sig)[::-1], s_ref, rtol=1e-9, atol=1e-14 * s_ref[0])
+    s_got = np.sort(sig)[::-1]
+    assert np.allclose(s_got[:len(s_ref)], s_ref, rtol=1e-9, atol=1e-14 * s_ref[0])
+    assert np.all(s_got[len(s_ref):] <= 1e-12 * s_ref[0])  # m < n: the extra columns are rotated to zero
     assert np.allclose(a, A @ V, atol=1e-12 * s_ref[0])
     assert np.allclose(V.T @ V, np.eye(n), atol=1e-12)
 
 
 @pytest.mark.parametrize("m,k", [(10, 3), (100, 16), (500, 64), (16, 16)])
-def test_householder_qr(L, m, k):
+def test_householder_qr(L, group, m, k):
     rng = np.random.default_rng(m * k)
     A = rng.standard_normal((m, k))
     Q = np.empty((m, k), order="F")
@@ -101,7 +112,7 @@ def test_householder_qr(L, m, k):
 
 
 @pytest.mark.parametrize("m,n,rank", [(40, 60, 5), (16, 120, 12), (200, 150, 30)])
-def test_aca_matches_oracle_crosses(L, m, n, rank):
+def test_aca_matches_oracle_crosses(L, group, m, n, rank):
     from oracle import ifmm_oracle as O
     rng = np.random.default_rng(m + n)
     F = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n)) * np.logspace(0, -6, n)
