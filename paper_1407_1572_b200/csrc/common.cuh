@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -56,9 +58,82 @@ inline std::atomic<long long>& launch_counter() {
 
 [[noreturn]] inline void invalid(const std::string& m) { throw Error(IFMM_INVALID, m); }
 
+// ---------------------------------------------------------------- slab cache
+// Process-wide cache of device slabs.  cudaMalloc of multi-GB slabs costs
+// tens of ms and cudaFree synchronises the device, so arenas (factorization
+// records, per-call workspaces) return their slabs here and later arenas
+// reuse them; the cache is flushed when an allocation would otherwise fail.
+// A slab is only released after the work using it has been synchronised (the
+// C API is synchronous), so reuse needs no stream ordering.
+struct SlabCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free;  // (device, bytes) -> ptr
+  size_t cached = 0;
+  static constexpr size_t kMaxCached = size_t(64) << 30;
+};
+inline SlabCache& slab_cache() {
+  static SlabCache* c = new SlabCache();  // never destroyed: slabs outlive static teardown
+  return *c;
+}
+inline void slab_cache_flush(int dev) {
+  SlabCache& c = slab_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  for (auto it = c.free.begin(); it != c.free.end();) {
+    if (it->first.first == dev) {
+      cudaFree(it->second);
+      c.cached -= it->first.second;
+      it = c.free.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+// A cached slab of at least `bytes` (and at most 2x), else a new one; *got =
+// its size.  Returns nullptr if the device is out of memory even after a flush.
+inline void* slab_get(size_t bytes, size_t* got) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SlabCache& c = slab_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.free.lower_bound({dev, bytes});
+    if (it != c.free.end() && it->first.first == dev && it->first.second <= 2 * bytes) {
+      void* p = it->second;
+      *got = it->first.second;
+      c.cached -= *got;
+      c.free.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    slab_cache_flush(dev);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  *got = bytes;
+  return p;
+}
+inline void slab_put(void* p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SlabCache& c = slab_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  if (c.cached + bytes > SlabCache::kMaxCached) {
+    cudaFree(p);
+    return;
+  }
+  c.free.insert({{dev, bytes}, p});
+  c.cached += bytes;
+}
+
 // ---------------------------------------------------------------- arena
-// Bump allocator over large cudaMalloc slabs.  Reset releases everything at
-// once (per level / per batch workspaces); slabs are kept for reuse.
+// Bump allocator over large device slabs (from the slab cache).  Reset releases
+// everything at once (per level / per batch workspaces); slabs are kept for
+// reuse and go back to the cache when the arena is destroyed.
 class Arena {
  public:
   explicit Arena(size_t slab = size_t(256) << 20) : slab_(slab) {}
@@ -81,10 +156,9 @@ class Arena {
         continue;
       }
       size_t sz = bytes > slab_ ? bytes : slab_;
-      void* p = nullptr;
-      cudaError_t e = cudaMalloc(&p, sz);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
+      void* p = slab_get(sz, &sz);
+      cudaError_t e = cudaSuccess;
+      if (p == nullptr) {
         char buf[256];
         snprintf(buf, sizeof buf, "device allocation of %.3f GB failed (arena holds %.3f GB)", sz / 1e9,
                  reserved() / 1e9);
@@ -117,7 +191,7 @@ class Arena {
     in_use_ = 0;
   }
   void release() {
-    for (auto& s : slabs_) cudaFree(s.ptr);
+    for (auto& s : slabs_) slab_put(s.ptr, s.size);
     slabs_.clear();
     cur_ = 0;
     in_use_ = 0;

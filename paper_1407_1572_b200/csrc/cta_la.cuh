@@ -252,12 +252,18 @@ __device__ inline void g_jacobi(const G& g, double* A, int m, int n, int lda, do
   if (V)
     for (int e = g.rank(); e < n * n; e += g.size()) V[(e % n) + (size_t)(e / n) * ldv] = (e % n == e / n);
   const int nn = n + (n & 1);  // even number of players (dummy = n)
+  // segment width: next power of two >= m (4..32); short columns leave most
+  // of a warp idle otherwise
+  const int W = m <= 4 ? 4 : m <= 8 ? 8 : m <= 16 ? 16 : 32;
+  const int spw = 32 / W, seg = lane / W, sl = lane & (W - 1);
   g.sync();
   for (int sweep = 0; sweep < max_sweeps && n > 1; sweep++) {
     bool rot = false;
     for (int round = 0; round < nn - 1; round++) {
-      for (int pr = warp; pr < nn / 2; pr += nw) {
-        // circle method: player nn-1 fixed, others rotate
+      // each warp runs spw pairs at once, one per W-lane segment
+      for (int base = warp * spw; base < nn / 2; base += nw * spw) {
+        const int pr = base + seg;
+        // circle method: player nn-1 fixed, others rotate.
         // (round + pr) and (round + nn - 1 - pr) are < 2 (nn - 1): one
         // conditional subtraction instead of an integer modulo
         int a = round + pr, b = round + nn - 1 - pr;
@@ -267,21 +273,24 @@ __device__ inline void g_jacobi(const G& g, double* A, int m, int n, int lda, do
           a = nn - 1;
           b = round;
         }
-        if (a >= n || b >= n || a == b) continue;
+        const bool valid = pr < nn / 2 && a < n && b < n && a != b;
         if (a > b) { int t = a; a = b; b = t; }
         double* x = A + (size_t)a * lda;
         double* y = A + (size_t)b * lda;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < m; i += 32) {
-          const double xi = x[i], yi = y[i];
-          al += xi * xi;
-          be += yi * yi;
-          ga += xi * yi;
+        if (valid)
+          for (int i = sl; i < m; i += W) {
+            const double xi = x[i], yi = y[i];
+            al += xi * xi;
+            be += yi * yi;
+            ga += xi * yi;
+          }
+        for (int o = W >> 1; o > 0; o >>= 1) {  // all lanes: segment-local butterflies
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+        if (!valid || ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         // a rotation below rounding level changes nothing: columns of very
@@ -289,7 +298,7 @@ __device__ inline void g_jacobi(const G& g, double* A, int m, int n, int lda, do
         // and never pass the relative test
         if (fabs(t) < 1e-16) continue;
         const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        for (int i = lane; i < m; i += 32) {
+        for (int i = sl; i < m; i += W) {
           const double xi = x[i], yi = y[i];
           x[i] = c * xi - s * yi;
           y[i] = s * xi + c * yi;
@@ -297,7 +306,7 @@ __device__ inline void g_jacobi(const G& g, double* A, int m, int n, int lda, do
         if (V) {
           double* vx = V + (size_t)a * ldv;
           double* vy = V + (size_t)b * ldv;
-          for (int i = lane; i < n; i += 32) {
+          for (int i = sl; i < n; i += W) {
             const double xi = vx[i], yi = vy[i];
             vx[i] = c * xi - s * yi;
             vy[i] = s * xi + c * yi;
