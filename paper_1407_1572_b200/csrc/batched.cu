@@ -62,11 +62,156 @@ void launch_grouped_gemm(GemmBatch& b, bool transA, bool transB, Arena& ws, Stag
   if (b.probs.empty()) return;
   const GemmProb* dp = upload(ws, b.probs, s, st);
   int np = int(b.probs.size());
-  if (!transA && !transB) grouped_dgemm_kernel<false, false><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
-  else if (transA && !transB) grouped_dgemm_kernel<true, false><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
-  else if (!transA && transB) grouped_dgemm_kernel<false, true><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
-  else grouped_dgemm_kernel<true, true><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+  static const bool v1 = getenv("IFMM_GEMM_V1") != nullptr;  // debug: register-staged kernel
+  if (v1) {
+    if (!transA && !transB) grouped_dgemm_kernel<false, false><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+    else if (transA && !transB) grouped_dgemm_kernel<true, false><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+    else if (!transA && transB) grouped_dgemm_kernel<false, true><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+    else grouped_dgemm_kernel<true, true><<<b.tiles, GTHREADS, 0, s>>>(dp, np);
+    CK_LAUNCH();
+    b.clear();
+    return;
+  }
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(grouped_dgemm_v2_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GSMEM)));
+    CK(cudaFuncSetAttribute(grouped_dgemm_v2_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GSMEM)));
+    CK(cudaFuncSetAttribute(grouped_dgemm_v2_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GSMEM)));
+    CK(cudaFuncSetAttribute(grouped_dgemm_v2_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GSMEM)));
+    attr = true;
+  }
+  const int* dtp = upload(ws, b.tile_prob, s, st);
+  if (!transA && !transB) grouped_dgemm_v2_kernel<false, false><<<b.tiles, GTHREADS, GSMEM, s>>>(dp, dtp);
+  else if (transA && !transB) grouped_dgemm_v2_kernel<true, false><<<b.tiles, GTHREADS, GSMEM, s>>>(dp, dtp);
+  else if (!transA && transB) grouped_dgemm_v2_kernel<false, true><<<b.tiles, GTHREADS, GSMEM, s>>>(dp, dtp);
+  else grouped_dgemm_v2_kernel<true, true><<<b.tiles, GTHREADS, GSMEM, s>>>(dp, dtp);
   CK_LAUNCH();
+  b.clear();
+}
+
+// Concatenated Schur update kernel (see gemm.cuh, SchurBatch)
+__device__ __forceinline__ int tri_index(int a, int b, int ns) { return a * ns - (a * (a - 1)) / 2 + (b - a); }
+
+__global__ void __launch_bounds__(GTHREADS, 3)
+    schur_concat_kernel(const SchurPiv* __restrict__ pivs, const int2* __restrict__ tiles,
+                        const int* __restrict__ soff_pool, const SchurTgt* __restrict__ tab_pool) {
+  extern __shared__ double gsm[];
+  __shared__ int rslot[GBM], roff[GBM], cslot[GBN], coff[GBN];
+  const int2 tt = tiles[blockIdx.x];
+  const SchurPiv P = pivs[tt.x];
+  const int i0 = (tt.y >> 16) * GBM, j0 = (tt.y & 0xffff) * GBN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int* soff = soff_pool + P.soff0;
+  {  // slot and in-slot offset of the tile's rows (threads 0..63) and columns (64..127)
+    const int e = tid & 63;
+    const int g = (tid < 64 ? i0 : j0) + e;
+    int lo = 0, hi = P.ns - 1;  // largest a with soff[a] <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (soff[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    if (tid < 64) { rslot[e] = lo; roff[e] = g - soff[lo]; }
+    else { cslot[e] = lo; coff[e] = g - soff[lo]; }
+  }
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  auto Asm = [&](int st) { return gsm + (size_t)st * 2 * GTILE_D; };
+  auto Bsm = [&](int st) { return gsm + (size_t)st * 2 * GTILE_D + GTILE_D; };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nk = (P.n + GBK - 1) / GBK;
+#pragma unroll
+  for (int st = 0; st < GSTAGES - 1; st++) {
+    if (st < nk) {
+      load_operand<true>(Asm(st), P.C, P.n, P.wr, P.n, i0, st * GBK, tid);
+      load_operand<true>(Bsm(st), P.X, P.n, P.w, P.n, j0, st * GBK, tid);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; kt++) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = kt + GSTAGES - 1;
+      if (nt < nk) {
+        const int st = nt % GSTAGES;
+        load_operand<true>(Asm(st), P.C, P.n, P.wr, P.n, i0, nt * GBK, tid);
+        load_operand<true>(Bsm(st), P.X, P.n, P.w, P.n, j0, nt * GBK, tid);
+      }
+      cp_async_commit();
+    }
+    const double* As = Asm(kt % GSTAGES);
+    const double* Bs = Bsm(kt % GSTAGES);
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int m = 0; m < 4; m++) fa[m] = frag<true>(As, wm + m * 8 + (lane >> 2), kk + (lane & 3));
+#pragma unroll
+      for (int n = 0; n < 4; n++) fb[n] = frag<true>(Bs, wn + n * 8 + (lane >> 2), kk + (lane & 3));
+#pragma unroll
+      for (int m = 0; m < 4; m++)
+#pragma unroll
+        for (int n = 0; n < 4; n++)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+              : "d"(fa[m]), "d"(fb[n]));
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // rslot/cslot (written before the main loop) visible
+  const SchurTgt* tab = tab_pool + P.tab0;
+  // per row group: resolve the 8 target addresses and issue their loads
+  // together, then the stores (a load behind an unrelated store would wait
+  // for it: the compiler cannot prove the targets distinct)
+#pragma unroll
+  for (int m = 0; m < 4; m++) {
+    const int li = wm + m * 8 + (lane >> 2);
+    const bool rok = i0 + li < P.wr;
+    const int a = rslot[li], ia = roff[li];
+    double* ptr[8];
+    double old[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int lj = wn + (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
+      const int b = cslot[lj];
+      ptr[e] = nullptr;
+      if (rok && j0 + lj < P.w && a <= b) {
+        const SchurTgt T = tab[tri_index(a, b, P.ns)];
+        const int jb = coff[lj];
+        ptr[e] = T.trans ? T.p + jb + (size_t)ia * T.ld : T.p + ia + (size_t)jb * T.ld;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; e++) old[e] = ptr[e] ? *ptr[e] : 0.0;
+#pragma unroll
+    for (int e = 0; e < 8; e++)
+      if (ptr[e]) *ptr[e] = old[e] - acc[m][e >> 1][e & 1];
+  }
+}
+
+void launch_schur(SchurBatch& b, Arena& ws, Staging& st, cudaStream_t s) {
+  if (b.tiles.empty()) {
+    b.clear();
+    return;
+  }
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(schur_concat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GSMEM)));
+    attr = true;
+  }
+  const SchurPiv* dp = upload(ws, b.pivs, s, st);
+  const int2* dt = upload(ws, b.tiles, s, st);
+  const int* dso = upload(ws, b.soff, s, st);
+  const SchurTgt* dtab = upload(ws, b.tab, s, st);
+  for (size_t off = 0; off < b.tiles.size(); off += 2147483647u) {
+    const unsigned g = unsigned(std::min<size_t>(b.tiles.size() - off, 2147483647u));
+    schur_concat_kernel<<<g, GTHREADS, GSMEM, s>>>(dp, dt + off, dso, dtab);
+    CK_LAUNCH();
+  }
   b.clear();
 }
 

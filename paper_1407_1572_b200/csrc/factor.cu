@@ -467,12 +467,16 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   tm_.begin(PH_XGEMM);
   launch_grouped_gemm(gb, false, false, ws_, st_, s_);
   tm_.end();
-  // symmetric Schur update on the block upper triangle: target -= C_a^T X_b
+  // symmetric Schur update on the block upper triangle: target -= C_a^T X_b,
+  // one concatenated product per pivot (IFMM_SCHUR_GROUPED: one GEMM per block)
+  static const bool per_block = getenv("IFMM_SCHUR_GROUPED") != nullptr;
+  SchurBatch sbat;
   for (int t = 0; t < np; t++) {
     PivInfo& I = P[t];
     const RecordH& R = F_->recs[I.rec];
     const int nx = int(I.xp.size()), ny = int(I.yp.size());
     const int ns = nx + ny + 1;
+    const int pv = per_block ? -1 : sbat.begin_pivot(I.C, R.xtop, I.n, I.soff);
     auto slot_cluster = [&](int s) { return s < nx ? I.xp[s] : (s < nx + ny ? I.yp[s - nx] : I.i); };
     for (int a = 0; a < ns; a++)
       for (int b = a; b < ns; b++) {
@@ -498,12 +502,17 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         }
         if (da == 0 || db == 0) continue;
         F_->fl_schur += 2.0 * I.n * da * db;
-        gb.add(I.C + size_t(I.soff[a]) * I.n, I.n, R.xtop + size_t(I.soff[b]) * I.n, I.n, tgt.p, tgt.ld, da, db, I.n,
-               -1.0, 1.0, tgt.trans);
+        if (per_block)
+          gb.add(I.C + size_t(I.soff[a]) * I.n, I.n, R.xtop + size_t(I.soff[b]) * I.n, I.n, tgt.p, tgt.ld, da, db,
+                 I.n, -1.0, 1.0, tgt.trans);
+        else
+          sbat.set_target(pv, a, b, tgt.p, tgt.ld, tgt.trans);
       }
+    if (!per_block) sbat.finish_pivot(pv);
   }
   tm_.begin(PH_SCHUR);
-  launch_grouped_gemm(gb, true, false, ws_, st_, s_);
+  if (per_block) launch_grouped_gemm(gb, true, false, ws_, st_, s_);
+  else launch_schur(sbat, ws_, st_, s_);
   tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
   tm_.end();

@@ -21,7 +21,9 @@ pts = 2.0 * np.random.default_rng(0).random((N, 2)) - 1.0
 b = np.random.default_rng([0, 1]).standard_normal(N)
 tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
 store = ifmm.init_operators(tree, ifmm.baseline_kernel(kern, N), p=p, tol=tol)
+fact = None
 for r in range(reps):
+    fact = None  # free the previous factorization first (as bench.py does): its slabs return to the cache
     t0 = time.perf_counter()
     fact = ifmm.factorize(store, tree, pivot_condition_limit=1e15, timing=(r == reps - 1))
     t1 = time.perf_counter()
@@ -32,3 +34,7 @@ print(f"{name}: residual {res:.3e} r_m {fact.r_m} top {fact.top_dim}")
 print("phases:", {k: round(v[0], 1) for k, v in fact.phase_times.items()})
 for k, d in sorted(fact.phase_times_by_level.items(), reverse=True):
     print(f"  level {k}: " + " ".join(f"{p}={v:.1f}" for p, v in d.items() if v))
+w = fact.work
+ph = fact.phase_times
+print(f"schur {w['flops_schur'] / 1e12:.3f} TF in {ph['schur_gemm'][0]:.1f} ms = "
+      f"{w['flops_schur'] / ph['schur_gemm'][0] / 1e9:.1f} TF/s")
