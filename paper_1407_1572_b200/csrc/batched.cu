@@ -749,6 +749,104 @@ __global__ void __launch_bounds__(256) gj_colgather_kernel(const MatDesc* __rest
   }
 }
 
+// v2 trailing update (see gemm.cuh for the cp.async operand layouts): grid
+// (matrix, tile); the rank-b update A(:, v) += P W(:, v) over the virtual
+// columns v (all but the panel), P = A(:, j:j+b) i-contiguous, W k-contiguous.
+// Rows of the pivot block are overwritten (beta = 0), the others accumulated.
+__global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc* __restrict__ desc, int j, int b,
+                                                                   double* const* __restrict__ Wp) {
+  extern __shared__ double gsm[];
+  const MatDesc D = desc[blockIdx.x];
+  const int m = D.m;
+  if (m <= j) return;
+  const int bb = min(b, m - j);
+  const int ncol = m - bb;  // virtual columns
+  const int tilesM = (m + GBM - 1) / GBM;
+  const int tl = blockIdx.y;
+  if (tl >= tilesM * ((ncol + GBN - 1) / GBN)) return;
+  const int i0 = (tl % tilesM) * GBM, v0 = (tl / tilesM) * GBN;
+  const double* __restrict__ W = Wp[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  auto Asm = [&](int st) { return gsm + (size_t)st * 2 * GTILE_D; };
+  auto Bsm = [&](int st) { return gsm + (size_t)st * 2 * GTILE_D + GTILE_D; };
+  const double* Pan = D.A + (size_t)j * D.lda;
+  auto load_w = [&](double* sm, int k0) {
+#pragma unroll
+    for (int e = 0; e < (GBN * GBK) / GTHREADS; e++) {
+      const int c = tid + e * GTHREADS;
+      const int k = c & (GBK - 1), r = c / GBK;
+      const int vc = v0 + r, gk = k0 + k;
+      const int col = vc < j ? vc : vc + bb;
+      const bool ok = vc < ncol && gk < bb;
+      cp_async8(sm + r * KP + k, W + gk + (size_t)col * bb, ok);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int c = 0; c < 4; c++) acc[a][c][0] = acc[a][c][1] = 0.0;
+  const int nk = (bb + GBK - 1) / GBK;
+#pragma unroll
+  for (int st = 0; st < GSTAGES - 1; st++) {
+    if (st < nk) {
+      load_operand<false>(Asm(st), Pan, D.lda, m, bb, i0, st * GBK, tid);
+      load_w(Bsm(st), st * GBK);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; kt++) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = kt + GSTAGES - 1;
+      if (nt < nk) {
+        const int st = nt % GSTAGES;
+        load_operand<false>(Asm(st), Pan, D.lda, m, bb, i0, nt * GBK, tid);
+        load_w(Bsm(st), nt * GBK);
+      }
+      cp_async_commit();
+    }
+    const double* As = Asm(kt % GSTAGES);
+    const double* Bs = Bsm(kt % GSTAGES);
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) fa[q] = frag<false>(As, wm + q * 8 + (lane >> 2), kk + (lane & 3));
+#pragma unroll
+      for (int q = 0; q < 4; q++) fb[q] = frag<true>(Bs, wn + q * 8 + (lane >> 2), kk + (lane & 3));
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int y = 0; y < 4; y++)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
+                       : "d"(fa[x]), "d"(fb[y]));
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int x = 0; x < 4; x++) {
+    const int gi = i0 + wm + x * 8 + (lane >> 2);
+    const bool r1 = gi >= j && gi < j + bb;
+    double* ptr[8];
+    double old[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int vc = v0 + wn + (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
+      const int col = vc < j ? vc : vc + bb;
+      ptr[e] = (gi < m && vc < ncol) ? D.A + gi + (size_t)col * D.lda : nullptr;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; e++) old[e] = (ptr[e] && !r1) ? *ptr[e] : 0.0;
+#pragma unroll
+    for (int e = 0; e < 8; e++)
+      if (ptr[e]) *ptr[e] = old[e] + acc[x][e >> 1][e & 1];
+  }
+}
+
 void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
                         Staging& st, cudaStream_t s) {
   const int n = int(h.size());
@@ -781,6 +879,7 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+    CK(cudaFuncSetAttribute(gj_update_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GSMEM)));
     attr = true;
   }
   CK(cudaMemsetAsync(d_info, 0, sizeof(int) * n, s));
@@ -799,18 +898,31 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
     CK_LAUNCH();
     gj_move_copy_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, j, b, moves, nmoves, dW);
     CK_LAUNCH();
-    // tile prefix of this step (matrices with m <= j contribute nothing)
-    std::vector<int>& t0 = tile_pref[(j / b) & 1];
-    t0.assign(n + 1, 0);
-    for (int p = 0; p < n; p++) {
-      const int m = h[p].m;
-      const int tiles = m > j ? ceil_div(m, GBM) * ceil_div(m - std::min(b, m - j), GBN) : 0;
-      t0[p + 1] = t0[p] + tiles;
-    }
-    if (t0[n] > 0) {
-      const int* dt0 = upload(ws, t0, s, st);
-      gj_update_kernel<<<t0[n], GTHREADS, 0, s>>>(d_desc, dt0, n, j, b, dW);
-      CK_LAUNCH();
+    static const bool v1 = getenv("IFMM_GJ_UPDATE_V1") != nullptr;  // debug: register-staged update
+    if (v1) {
+      // tile prefix of this step (matrices with m <= j contribute nothing)
+      std::vector<int>& t0 = tile_pref[(j / b) & 1];
+      t0.assign(n + 1, 0);
+      for (int p = 0; p < n; p++) {
+        const int m = h[p].m;
+        const int tiles = m > j ? ceil_div(m, GBM) * ceil_div(m - std::min(b, m - j), GBN) : 0;
+        t0[p + 1] = t0[p] + tiles;
+      }
+      if (t0[n] > 0) {
+        const int* dt0 = upload(ws, t0, s, st);
+        gj_update_kernel<<<t0[n], GTHREADS, 0, s>>>(d_desc, dt0, n, j, b, dW);
+        CK_LAUNCH();
+      }
+    } else {
+      int maxt = 0;  // tiles of the largest matrix still active at this step
+      for (int p = 0; p < n; p++) {
+        const int m = h[p].m;
+        if (m > j) maxt = std::max(maxt, ceil_div(m, GBM) * ceil_div(m - std::min(b, m - j), GBN));
+      }
+      if (maxt > 0) {
+        gj_update_v2_kernel<<<dim3(n, maxt), GTHREADS, GSMEM, s>>>(d_desc, j, b, dW);
+        CK_LAUNCH();
+      }
     }
   }
   // undo the row pivoting as one column gather per matrix (through scratch)

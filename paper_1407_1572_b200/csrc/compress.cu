@@ -175,6 +175,19 @@ __device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig
     for (int e = g.rank(); e < nU * r; e += g.size()) H[e] *= wsig[e / nU];
     g.sync();
   }
+  {
+    // sigma_max(H) <= ||H||_F: if the projected, weighted directions are all
+    // below the cutoff there is nothing to add (exact; ~30% of the fine-level
+    // steps), skip the QR and SVD
+    double f2 = 0.0;
+    for (int e = g.rank(); e < nU * r; e += g.size()) f2 += H[e] * H[e];
+    f2 = g.sum(f2);
+    if (g_prof_on && g.rank() == 0) {
+      atomicAdd(&g_cyc[11], 1ull);
+      if (sqrt(f2) <= cutoff) atomicAdd(&g_cyc[13], 1ull);
+    }
+    if (sqrt(f2) <= cutoff) return 0;
+  }
   g_qr(g, H, nU, r, nU, R, Q, nU, vv);  // H = Q R
   PROF_ACC(5);
   g_jacobi_small(g, R, r, r, r, nullptr, 0, sig, ord, g_jac_reg != 0);  // R V = U_R S
@@ -182,6 +195,7 @@ __device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig
   int w = 0;
   for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
   w = min(w, cap);
+  if (g_prof_on && g.rank() == 0 && w == 0) atomicAdd(&g_cyc[12], 1ull);
   double* W = U + (size_t)rU * nU;
   for (int e = g.rank(); e < nU * w; e += g.size()) {
     const int i = e % nU, c = e / nU;
@@ -454,9 +468,9 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     unsigned long long c[16];
     CK(cudaMemcpyFromSymbolAsync(c, g_cyc, sizeof c, 0, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    fprintf(stderr, "prof MX=%d nf=%d chains=%zu p2p=%zu | aca %.1f qr %.1f core %.1f rest %.1f | proj %.1f qr %.1f jac %.1f W %.1f Mcyc | jacobi calls %llu avg sweeps %.2f avg cols %.1f\n",
+    fprintf(stderr, "prof MX=%d nf=%d chains=%zu p2p=%zu | aca %.1f qr %.1f core %.1f rest %.1f | proj %.1f qr %.1f jac %.1f W %.1f Mcyc | jacobi calls %llu avg sweeps %.2f avg cols %.1f | aug steps %llu w=0 %llu fro<=cut %llu\n",
             MX, nf, cb.chain_off.size() - 1, cb.p2p.size(), c[0] / 1e6, c[1] / 1e6, c[2] / 1e6, c[3] / 1e6, c[4] / 1e6,
-            c[5] / 1e6, c[6] / 1e6, c[7] / 1e6, c[9], c[9] ? double(c[8]) / c[9] : 0.0, c[9] ? double(c[10]) / c[9] : 0.0);
+            c[5] / 1e6, c[6] / 1e6, c[7] / 1e6, c[9], c[9] ? double(c[8]) / c[9] : 0.0, c[9] ? double(c[10]) / c[9] : 0.0, c[11], c[12], c[13]);
   }
 }
 

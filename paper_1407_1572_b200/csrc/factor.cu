@@ -441,7 +441,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     R.w = I.w;
     R.sinv = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * std::max(1, I.n));
     R.xtop = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
-    R.pos = F_->arena.alloc_n<int>(I.w);
+    R.pos = nullptr;  // set by finish_level (one block per level)
     I.rec = int(F_->recs.size());
     F_->recs.push_back(R);
     std::vector<SlotRef> sl;
@@ -675,13 +675,9 @@ void Factorizer::finish_level(int rec_begin) {
     }
   }
   if (!posall.empty()) {
-    void* h = st_.get(sizeof(int) * posall.size());
-    memcpy(h, posall.data(), sizeof(int) * posall.size());
-    // records' pos arrays are separate allocations: copy each
-    for (size_t rr = rec_begin, u = 0; rr < F_->recs.size(); rr++, u++) {
-      RecordH& R = F_->recs[rr];
-      CK(cudaMemcpyAsync(R.pos, static_cast<int*>(h) + posoff[u], sizeof(int) * R.w, cudaMemcpyHostToDevice, s_));
-    }
+    // the level's position arrays live in one block: one copy
+    int* d = upload(F_->arena, posall, s_, st_);
+    for (size_t rr = rec_begin, u = 0; rr < F_->recs.size(); rr++, u++) F_->recs[rr].pos = d + posoff[u];
   }
   CK(cudaStreamSynchronize(s_));
   st_.reset();
@@ -725,6 +721,7 @@ void Factorizer::factor_top() {
 
 FactorH* Factorizer::run() {
   auto t0 = std::chrono::steady_clock::now();
+  if (getenv("IFMM_HOST_PROF")) fprintf(stderr, "host factorize begin\n");
   s_ = S_->stream;
   tm_.on = (flags_ & IFMM_FLAG_TIMING) != 0;
   tm_.s = s_;
@@ -739,7 +736,12 @@ FactorH* Factorizer::run() {
   F_->lvl_base[K] = 0;
   F_->r_m = S_->max_init_rank;
   const int ncol = [&] { int c = 1; for (int d = 0; d < t_->dim; d++) c *= 3; return c; }();
+  static const bool hprof = getenv("IFMM_HOST_PROF") != nullptr;  // debug: host time outside the batches
+  auto since = [](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
   for (int k = K; k >= 2; k--) {
+    const auto tl0 = std::chrono::steady_clock::now();
     if (k == K) {
       tm_.begin(PH_TRANSITION);
       start_leaf_level();
@@ -752,6 +754,7 @@ FactorH* Factorizer::run() {
       tm_.collect(F_.get(), k);
       prev_ = WorkLevel{};
     }
+    if (hprof) fprintf(stderr, "host level %d: start %.1f ms\n", k, since(tl0));
     F_->stats[k].clusters = cur_.nc;
     const int rec_begin = int(F_->recs.size());
     for (int c = 0; c < ncol; c++) {
@@ -767,10 +770,15 @@ FactorH* Factorizer::run() {
         piv.swap(deferred);
       }
     }
+    const auto tf0 = std::chrono::steady_clock::now();
     finish_level(rec_begin);
+    if (hprof) fprintf(stderr, "host level %d: finish %.1f ms, level total %.1f ms\n", k, since(tf0), since(tl0));
     F_->r_m = std::max(F_->r_m, F_->stats[k].max_rank);
   }
+  const auto tt0 = std::chrono::steady_clock::now();
   factor_top();
+  if (hprof) fprintf(stderr, "host top %.1f ms\n", since(tt0));
+  const auto tr0 = std::chrono::steady_clock::now();
   // device copies of the batch record tables
   for (BatchH& b : F_->batches) {
     std::vector<RecordH> v(F_->recs.begin() + b.rec0, F_->recs.begin() + b.rec1);
@@ -788,7 +796,10 @@ FactorH* Factorizer::run() {
   F_->d_g_off = F_->arena.alloc_n<int64_t>(F_->g_off.size());
   CK(cudaMemcpyAsync(F_->d_g_off, F_->g_off.data(), sizeof(int64_t) * F_->g_off.size(), cudaMemcpyHostToDevice, s_));
   CK(cudaStreamSynchronize(s_));
+  if (hprof) fprintf(stderr, "host record tables %.1f ms\n", since(tr0));
+  const auto tc0 = std::chrono::steady_clock::now();
   cur_ = WorkLevel{};
+  if (hprof) fprintf(stderr, "host release %.1f ms\n", since(tc0));
   // level arenas stay allocated with the store (zeroed again on next reset)
   F_->fl_exec += F_->fl_schur;
   F_->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
