@@ -410,10 +410,16 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(const MatDesc* __restrict
     }
     if (lane == 0) { candv[warp] = bv; candr[warp] = br; candp[warp] = bp; }
     __syncthreads();
-    // (2) every thread reduces the warp candidates (no extra barrier)
-    bv = -1.0; br = -1; bp = 0x7fffffff;
-    for (int w = 0; w < nw; w++)
-      if (candv[w] > bv || (candv[w] == bv && candp[w] < bp)) { bv = candv[w]; br = candr[w]; bp = candp[w]; }
+    // (2) every warp reduces the warp candidates with shuffles (no extra barrier)
+    bv = lane < nw ? candv[lane] : -1.0;
+    br = lane < nw ? candr[lane] : -1;
+    bp = lane < nw ? candp[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, br, o), op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ov > bv || (ov == bv && op < bp)) { bv = ov; br = orr; bp = op; }
+    }
     if (warp == 0) {  // pivot row: scaled copy in prow (prow[c] = 1/pivot), broadcast after the barrier
       const double pv = br >= 0 ? P[br * ld + c] : 0.0;
       const bool sing = (pv == 0.0 || pv != pv);
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(R == 1 ? 512 : (R == 2 ? 384 : 256)) gj_panel_
   extern __shared__ int smi[];
   __shared__ double candv[32];
   __shared__ int candr[32];
-  __shared__ double prow[B];
+  __shared__ __align__(16) double prow[B];
   __shared__ int s_cnt;
   const MatDesc D = desc[blockIdx.x];
   const int m = D.m;
@@ -518,10 +524,15 @@ __global__ void __launch_bounds__(R == 1 ? 512 : (R == 2 ? 384 : 256)) gj_panel_
     }
     if (lane == 0) { candv[warp] = bv; candr[warp] = br; }
     __syncthreads();
-    bv = -1.0;
-    br = 0x7fffffff;
-    for (int w = 0; w < nw; w++)
-      if (candv[w] > bv || (candv[w] == bv && candr[w] < br)) { bv = candv[w]; br = candr[w]; }
+    // every warp reduces the nw candidates with shuffles (same result everywhere)
+    bv = lane < nw ? candv[lane] : -1.0;
+    br = lane < nw ? candr[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+      if (ov > bv || (ov == bv && orr < br)) { bv = ov; br = orr; }
+    }
     if (br == 0x7fffffff) br = -1;
     // owner of the pivot row publishes it scaled; thread 0 does the bookkeeping
     const int kown = br >= 0 ? br / nt : -1;
@@ -557,16 +568,35 @@ __global__ void __launch_bounds__(R == 1 ? 512 : (R == 2 ? 384 : 256)) gj_panel_
       }
     }
     __syncthreads();
-    const double inv = prow[c];
+    if (R == 1) {
+      double pr[B];  // pivot row in registers, 16-byte broadcast reads
 #pragma unroll
-    for (int k = 0; k < R; k++) {
-      const int r = tid + k * nt;
-      if (r == br || r >= m) continue;
-      const double f = v[k][c];
+      for (int cc = 0; cc < B; cc += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&prow[cc]);
+        pr[cc] = t2.x;
+        pr[cc + 1] = t2.y;
+      }
+      const double inv = pr[c];
+      const int r = tid;
+      if (r != br && r < m) {
+        const double f = v[0][c];
 #pragma unroll
-      for (int cc = 0; cc < B; cc++)
-        if (cc != c) v[k][cc] = fma(-f, prow[cc], v[k][cc]);
-      v[k][c] = -f * inv;
+        for (int cc = 0; cc < B; cc++)
+          if (cc != c) v[0][cc] = fma(-f, pr[cc], v[0][cc]);
+        v[0][c] = -f * inv;
+      }
+    } else {  // two rows per thread: no room for a register copy of the row
+      const double inv = prow[c];
+#pragma unroll
+      for (int k = 0; k < R; k++) {
+        const int r = tid + k * nt;
+        if (r == br || r >= m) continue;
+        const double f = v[k][c];
+#pragma unroll
+        for (int cc = 0; cc < B; cc++)
+          if (cc != c) v[k][cc] = fma(-f, prow[cc], v[k][cc]);
+        v[k][c] = -f * inv;
+      }
     }
   }
   __syncthreads();
@@ -753,14 +783,28 @@ __global__ void __launch_bounds__(256) gj_colgather_kernel(const MatDesc* __rest
 // (matrix, tile); the rank-b update A(:, v) += P W(:, v) over the virtual
 // columns v (all but the panel), P = A(:, j:j+b) i-contiguous, W k-contiguous.
 // Rows of the pivot block are overwritten (beta = 0), the others accumulated.
+// mode 0: all columns but the panel; 1: only the next panel's columns (the
+// look-ahead part); 2: all but the panel and the next panel.  Column u of the
+// mode's range maps to matrix column colmap(u).
+__device__ __forceinline__ int gj_cols(int mode, int j, int bb, int b2, int m) {
+  return mode == 0 ? m - bb : (mode == 1 ? b2 : m - bb - b2);
+}
+__device__ __forceinline__ int gj_colmap(int mode, int u, int j, int bb, int b2) {
+  if (mode == 1) return j + bb + u;
+  if (u < j) return u;
+  return u + bb + (mode == 2 ? b2 : 0);
+}
+
 __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc* __restrict__ desc, int j, int b,
-                                                                   double* const* __restrict__ Wp) {
+                                                                   double* const* __restrict__ Wp, int mode) {
   extern __shared__ double gsm[];
   const MatDesc D = desc[blockIdx.x];
   const int m = D.m;
   if (m <= j) return;
   const int bb = min(b, m - j);
-  const int ncol = m - bb;  // virtual columns
+  const int b2 = min(b, m - j - bb);  // width of the next panel
+  const int ncol = gj_cols(mode, j, bb, b2, m);
+  if (ncol <= 0) return;
   const int tilesM = (m + GBM - 1) / GBM;
   const int tl = blockIdx.y;
   if (tl >= tilesM * ((ncol + GBN - 1) / GBN)) return;
@@ -777,7 +821,7 @@ __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc
       const int c = tid + e * GTHREADS;
       const int k = c & (GBK - 1), r = c / GBK;
       const int vc = v0 + r, gk = k0 + k;
-      const int col = vc < j ? vc : vc + bb;
+      const int col = gj_colmap(mode, vc, j, bb, b2);
       const bool ok = vc < ncol && gk < bb;
       cp_async8(sm + r * KP + k, W + gk + (size_t)col * bb, ok);
     }
@@ -836,7 +880,7 @@ __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc
 #pragma unroll
     for (int e = 0; e < 8; e++) {
       const int vc = v0 + wn + (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
-      const int col = vc < j ? vc : vc + bb;
+      const int col = gj_colmap(mode, vc, j, bb, b2);
       ptr[e] = (gi < m && vc < ncol) ? D.A + gi + (size_t)col * D.lda : nullptr;
     }
 #pragma unroll
@@ -848,7 +892,7 @@ __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc
 }
 
 void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
-                        Staging& st, cudaStream_t s) {
+                        Staging& st, cudaStream_t s, const GjSide* side) {
   const int n = int(h.size());
   if (n == 0) return;
   int maxm = 0;
@@ -857,7 +901,8 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   // shared memory beyond (the top-level system)
   int variant, b, threads;
   size_t smem;
-  if (maxm <= 512) {
+  static const int reg1_max = getenv("IFMM_GJ_R1_MAX") ? atoi(getenv("IFMM_GJ_R1_MAX")) : 512;  // tuning
+  if (maxm <= reg1_max) {
     variant = 0;
     b = 32;
     threads = std::max(64, (maxm + 31) / 32 * 32);
@@ -870,7 +915,10 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   } else {
     variant = 2;
     auto smem_for = [&](int bw) { return size_t(maxm) * (bw + 1) * 8 + size_t(maxm) * 8; };
-    b = 32;
+    // narrow panels: the shared-memory panel rewrites m x b entries per pivot
+    // step, so its traffic grows with b (the wider update is cheap here)
+    static const int bsm = getenv("IFMM_GJ_SMEM_B") ? atoi(getenv("IFMM_GJ_SMEM_B")) : 16;
+    b = bsm;
     while (b > 4 && smem_for(b) > 224 * 1024) b /= 2;
     if (smem_for(b) > 224 * 1024) invalid("pivot block too large for the Gauss-Jordan panel");
     smem = smem_for(b);
@@ -891,14 +939,39 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   int* nmoves = ws.alloc_n<int>(n);
   std::vector<int> tile_pref[2];
   const int gy = std::max(1, std::min(16, (maxm + 63) / 64));
-  for (int j = 0; j < maxm; j += b) {
-    if (variant == 0) gj_panel_reg_kernel<32, 1><<<n, threads, smem, s>>>(d_desc, j, d_info, moves, nmoves);
-    else if (variant == 1) gj_panel_reg_kernel<32, 2><<<n, threads, smem, s>>>(d_desc, j, d_info, moves, nmoves);
-    else gj_panel_kernel<<<n, threads, smem, s>>>(d_desc, j, b, d_info, moves, nmoves);
+  auto panel = [&](int j, cudaStream_t ps) {
+    if (variant == 0) gj_panel_reg_kernel<32, 1><<<n, threads, smem, ps>>>(d_desc, j, d_info, moves, nmoves);
+    else if (variant == 1) gj_panel_reg_kernel<32, 2><<<n, threads, smem, ps>>>(d_desc, j, d_info, moves, nmoves);
+    else gj_panel_kernel<<<n, threads, smem, ps>>>(d_desc, j, b, d_info, moves, nmoves);
     CK_LAUNCH();
+  };
+  // tiles of the largest matrix for an update mode at step j
+  auto max_tiles = [&](int j, int mode) {
+    int mt = 0;
+    for (int p = 0; p < n; p++) {
+      const int m = h[p].m;
+      if (m <= j) continue;
+      const int bb = std::min(b, m - j), b2 = std::min(b, m - j - bb);
+      const int nc = mode == 0 ? m - bb : (mode == 1 ? b2 : m - bb - b2);
+      if (nc > 0) mt = std::max(mt, ceil_div(m, GBM) * ceil_div(nc, GBN));
+    }
+    return mt;
+  };
+  auto update = [&](int j, int mode) {
+    const int mt = max_tiles(j, mode);
+    if (mt > 0) {
+      gj_update_v2_kernel<<<dim3(n, mt), GTHREADS, GSMEM, s>>>(d_desc, j, b, dW, mode);
+      CK_LAUNCH();
+    }
+  };
+  static const bool v1 = getenv("IFMM_GJ_UPDATE_V1") != nullptr;  // debug: register-staged update
+  static const bool no_la = getenv("IFMM_GJ_NO_LOOKAHEAD") != nullptr;  // debug: serial panel/update
+  const bool look = side && side->s && !v1 && !no_la;
+  panel(0, s);
+  for (int j = 0; j < maxm; j += b) {
     gj_move_copy_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, j, b, moves, nmoves, dW);
     CK_LAUNCH();
-    static const bool v1 = getenv("IFMM_GJ_UPDATE_V1") != nullptr;  // debug: register-staged update
+    const bool more = j + b < maxm;
     if (v1) {
       // tile prefix of this step (matrices with m <= j contribute nothing)
       std::vector<int>& t0 = tile_pref[(j / b) & 1];
@@ -913,16 +986,20 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
         gj_update_kernel<<<t0[n], GTHREADS, 0, s>>>(d_desc, dt0, n, j, b, dW);
         CK_LAUNCH();
       }
+      if (more) panel(j + b, s);
+    } else if (look && more) {
+      // look-ahead: the next panel's columns first, then that panel on the
+      // high-priority side stream concurrently with the rest of the update
+      update(j, 1);
+      CK(cudaEventRecord(side->e_cols, s));
+      CK(cudaStreamWaitEvent(side->s, side->e_cols, 0));
+      panel(j + b, side->s);
+      CK(cudaEventRecord(side->e_panel, side->s));
+      update(j, 2);
+      CK(cudaStreamWaitEvent(s, side->e_panel, 0));
     } else {
-      int maxt = 0;  // tiles of the largest matrix still active at this step
-      for (int p = 0; p < n; p++) {
-        const int m = h[p].m;
-        if (m > j) maxt = std::max(maxt, ceil_div(m, GBM) * ceil_div(m - std::min(b, m - j), GBN));
-      }
-      if (maxt > 0) {
-        gj_update_v2_kernel<<<dim3(n, maxt), GTHREADS, GSMEM, s>>>(d_desc, j, b, dW);
-        CK_LAUNCH();
-      }
+      update(j, 0);
+      if (more) panel(j + b, s);
     }
   }
   // undo the row pivoting as one column gather per matrix (through scratch)

@@ -51,8 +51,26 @@ void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, 
 // In-place inversion of every matrix by blocked Gauss-Jordan elimination with
 // partial pivoting.  `info[p]` = 0, or 1 + first column with an exact zero
 // pivot.  Host-side descriptors `h` (same content as d_desc) drive the GEMM
-// trailing updates.
+// trailing updates.  With `side` (a high-priority stream and two events) the
+// panel of step j+1 runs concurrently with the bulk of step j's update.
+struct GjSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t e_cols = nullptr, e_panel = nullptr;
+  void ensure() {
+    if (s) return;
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&e_cols, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e_panel, cudaEventDisableTiming));
+  }
+  ~GjSide() {
+    if (e_cols) cudaEventDestroy(e_cols);
+    if (e_panel) cudaEventDestroy(e_panel);
+    if (s) cudaStreamDestroy(s);
+  }
+};
 void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
-                        Staging& st, cudaStream_t s);
+                        Staging& st, cudaStream_t s, const GjSide* side = nullptr);
 
 }  // namespace ifmm

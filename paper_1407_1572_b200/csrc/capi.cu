@@ -302,6 +302,12 @@ void ifmm_factor_free(ifmm_factor* f) {
 // The small-matrix routines run either CTA-wide (256 threads) or on one warp,
 // as the compression kernels use them; ifmm_test_set_group selects which.
 static int g_test_warp = 0;
+// the test / bench hooks use the look-ahead Gauss-Jordan like the factorization
+static ifmm::GjSide* test_gj_side() {
+  static ifmm::GjSide* g = new ifmm::GjSide();  // never destroyed: outlives the CUDA context teardown
+  g->ensure();
+  return g;
+}
 
 template <class G>
 __global__ void test_jacobi_kernel(double* a, int m, int n, double* v, double* sig, int* ord) {
@@ -363,7 +369,7 @@ int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info) 
     }
     const MatDesc* dmd = upload(ws, md, s, st);
     int* dinfo = ws.alloc_n<int>(count);
-    ifmm::batched_gj_inverse(md, dmd, dinfo, ws, st, s);
+    ifmm::batched_gj_inverse(md, dmd, dinfo, ws, st, s, test_gj_side());
     CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(a, d, sizeof(double) * tot, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(info, dinfo, sizeof(int) * count, cudaMemcpyDeviceToHost));
@@ -399,7 +405,7 @@ int ifmm_bench_gj_inverse(const double* a, const int32_t* m, int count, int reps
       const size_t mark = ws.in_use();
       (void)mark;
       CK(cudaEventRecord(e0, s));
-      batched_gj_inverse(md, dmd, dinfo, ws, st, s);
+      batched_gj_inverse(md, dmd, dinfo, ws, st, s, test_gj_side());
       CK(cudaEventRecord(e1, s));
       CK(cudaEventSynchronize(e1));
       float t = 0.f;

@@ -68,6 +68,7 @@ struct InitLevel {
 // parameter sweeps refactorize) do not pay cudaMalloc/cudaFree every call.
 struct FactorWork {
   std::mutex mu;
+  GjSide gj_side;  // look-ahead stream of the Gauss-Jordan inverses
   Arena ws{size_t(256) << 20};
   Staging st;
   Arena lvl[2] = {Arena(size_t(2) << 30), Arena(size_t(2) << 30)};

@@ -422,7 +422,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   int* d_info = ws_.alloc_n<int>(np);
   tm_.begin(PH_GJ);
   launch_norm1(dmd, np, d_nS, s_);
-  batched_gj_inverse(md, dmd, d_info, ws_, st_, s_);
+  S_->work->gj_side.ensure();
+  batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &S_->work->gj_side);
   {
     int maxm = 0;
     for (auto& d : md) maxm = std::max(maxm, d.m);
@@ -713,7 +714,8 @@ void Factorizer::factor_top() {
     const MatDesc* dmd = upload(ws_, md, s_, st_);
     int* d_info = ws_.alloc_n<int>(1);
     tm_.begin(PH_TOP);
-    batched_gj_inverse(md, dmd, d_info, ws_, st_, s_);
+    S_->work->gj_side.ensure();
+    batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &S_->work->gj_side);
   }
   CK(cudaStreamSynchronize(s_));
   tm_.collect(F_.get(), 1);
