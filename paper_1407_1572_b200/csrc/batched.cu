@@ -14,12 +14,24 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyDesc* __restrict__ 
   const CopyDesc D = desc[blockIdx.x];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   if (!D.trans || D.src == nullptr) {
+    // four independent elements per lane in flight: loads first, then stores
+    // (a load behind an unrelated store would wait for it)
     for (int j = ty; j < D.cols; j += 8) {
       double* dcol = D.dst + (size_t)j * D.ldd;
       const double* scol = D.src ? D.src + (size_t)j * D.lds : nullptr;
-      for (int i = tx; i < D.rows; i += 32) {
-        double v = scol ? D.alpha * scol[i] : 0.0;
-        if (D.accumulate) dcol[i] += v; else dcol[i] = v;
+      for (int i0 = tx; i0 < D.rows; i0 += 128) {
+        double v[4], o[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int i = i0 + 32 * u;
+          v[u] = (scol && i < D.rows) ? scol[i] : 0.0;
+          o[u] = (D.accumulate && i < D.rows) ? dcol[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int i = i0 + 32 * u;
+          if (i < D.rows) dcol[i] = o[u] + D.alpha * v[u];
+        }
       }
     }
     return;
@@ -47,6 +59,28 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyDesc* __restrict__ 
 
 void launch_copies(CopyBatch& b, Arena& ws, Staging& st, cudaStream_t s) {
   if (b.d.empty()) return;
+  // one CTA per descriptor: split large blocks into column chunks (<= 16K
+  // elements, multiples of 32 columns) so big gathers spread over the GPU
+  {
+    constexpr long long kChunk = 16384;
+    std::vector<CopyDesc> out;
+    out.reserve(b.d.size());
+    for (const CopyDesc& D : b.d) {
+      if ((long long)D.rows * D.cols <= kChunk) {
+        out.push_back(D);
+        continue;
+      }
+      int cw = int(std::max<long long>(32, kChunk / std::max(1, D.rows) / 32 * 32));
+      for (int j0 = 0; j0 < D.cols; j0 += cw) {
+        CopyDesc C = D;
+        C.cols = std::min(cw, D.cols - j0);
+        C.dst = D.dst + (size_t)j0 * D.ldd;
+        if (D.src) C.src = D.trans ? D.src + j0 : D.src + (size_t)j0 * D.lds;
+        out.push_back(C);
+      }
+    }
+    b.d.swap(out);
+  }
   const CopyDesc* dd = upload(ws, b.d, s, st);
   size_t n = b.d.size();
   for (size_t off = 0; off < n; off += 2147483647u) {

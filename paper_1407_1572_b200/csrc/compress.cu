@@ -5,6 +5,7 @@
 
 namespace ifmm {
 __device__ int g_prof_on = 0;
+__device__ int g_jac_rt = 1;   // IFMM_JACOBI_RT=0: Jacobi on R (columns) in new_dirs
 __device__ int g_jac_reg = 0;  // IFMM_JACOBI_REG=1: register-resident Jacobi for <= 16 columns (measured slower)
 __device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
 }  // namespace ifmm
@@ -190,20 +191,41 @@ __device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig
   }
   g_qr(g, H, nU, r, nU, R, Q, nU, vv);  // H = Q R
   PROF_ACC(5);
-  g_jacobi_small(g, R, r, r, r, nullptr, 0, sig, ord, g_jac_reg != 0);  // R V = U_R S
-  PROF_ACC(6);
-  int w = 0;
-  for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
-  w = min(w, cap);
-  if (g_prof_on && g.rank() == 0 && w == 0) atomicAdd(&g_cyc[12], 1ull);
   double* W = U + (size_t)rU * nU;
-  for (int e = g.rank(); e < nU * w; e += g.size()) {
-    const int i = e % nU, c = e / nU;
-    const int col = ord[c];
-    double acc = 0.0;
-    for (int t = 0; t < r; t++) acc = fma(Q[i + (size_t)t * nU], R[t + (size_t)col * r], acc);
-    W[i + (size_t)c * nU] = acc / sig[col];
+  int w = 0;
+  if (g_jac_rt) {
+    // one-sided Jacobi on R^T with the rotations accumulated: R^T V = X, so V
+    // holds the left singular vectors of R and ||X(:,j)|| its singular values.
+    // The rows of the triangular R are far closer to orthogonal than its
+    // columns (QR-preconditioned Jacobi): fewer sweeps, and W = Q V needs no
+    // division by sigma.
+    for (int e = g.rank(); e < r * r; e += g.size()) E[e] = R[(e / r) + (size_t)(e % r) * r];
+    g.sync();
+    g_jacobi(g, E, r, r, r, R, r, sig, ord);  // V -> R
+    PROF_ACC(6);
+    for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
+    w = min(w, cap);
+    for (int e = g.rank(); e < nU * w; e += g.size()) {
+      const int i = e % nU, c = e / nU;
+      const double* v = R + (size_t)ord[c] * r;
+      double acc = 0.0;
+      for (int t = 0; t < r; t++) acc = fma(Q[i + (size_t)t * nU], v[t], acc);
+      W[i + (size_t)c * nU] = acc;
+    }
+  } else {
+    g_jacobi_small(g, R, r, r, r, nullptr, 0, sig, ord, g_jac_reg != 0);  // R V = U_R S
+    PROF_ACC(6);
+    for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
+    w = min(w, cap);
+    for (int e = g.rank(); e < nU * w; e += g.size()) {
+      const int i = e % nU, c = e / nU;
+      const int col = ord[c];
+      double acc = 0.0;
+      for (int t = 0; t < r; t++) acc = fma(Q[i + (size_t)t * nU], R[t + (size_t)col * r], acc);
+      W[i + (size_t)c * nU] = acc / sig[col];
+    }
   }
+  if (g_prof_on && g.rank() == 0 && w == 0) atomicAdd(&g_cyc[12], 1ull);
   g.sync();
   if (w > 0) g_project_out(g, W, nU, nU, w, U, nU, rU, E);
   PROF_ACC(7);
@@ -359,8 +381,10 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   constexpr int WPB = 4;  // warps per CTA in warp mode
   static const bool prof = getenv("IFMM_PROF") != nullptr;
   static const int jac_reg = getenv("IFMM_JACOBI_REG") ? atoi(getenv("IFMM_JACOBI_REG")) : 0;
+  static const int jac_rt = getenv("IFMM_JACOBI_RT") ? atoi(getenv("IFMM_JACOBI_RT")) : 1;
   static bool jac_set = false;
   if (!jac_set) {
+    CK(cudaMemcpyToSymbolAsync(g_jac_rt, &jac_rt, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyToSymbolAsync(g_jac_reg, &jac_reg, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     jac_set = true;
   }
