@@ -21,12 +21,12 @@ void launch_permute(const double* in, double* out, const int64_t* perm, int64_t 
 
 constexpr int SB = 256;       // threads per solve CTA
 constexpr int SWARPS = SB / 32;
-constexpr int RC = 4;         // right-hand sides per pass
+constexpr int RCMAX = 4;      // right-hand sides per pass (RC = 1 for a single rhs)
 constexpr int MAXJ = 8;       // rows per lane per pass (256 rows per row block)
 
 // y[t, q] (t < n, q < nq) = sum_c A[t + c*lda] x(c, q)  (A column-major n x w);
 // x(c, q) from the `xat` accessor, result written by `emit(t, q, value)`.
-template <class XAt, class Emit>
+template <int RC, class XAt, class Emit>
 __device__ inline void cta_gemv_cols(const double* __restrict__ A, int n, int w, size_t lda, XAt xat, int nq,
                                      double* red, Emit emit) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -80,6 +80,17 @@ __device__ inline void cta_gemv_cols(const double* __restrict__ A, int n, int w,
   }
 }
 
+// Records are split over gridDim.y CTAs (coarse levels have few, large
+// records): chunk y of the forward sweep computes rows [r0, r1) of Sinv b and
+// columns [c0, c1) of X_top^T b; chunk y of the backward sweep rows [r0, r1)
+// of x.  Every output has exactly one writer (deterministic).
+__device__ __forceinline__ void chunk_range(int len, int y, int ny, int gran, int& lo, int& hi) {
+  const int per = ((len + ny - 1) / ny + gran - 1) / gran * gran;
+  lo = min(len, y * per);
+  hi = min(len, lo + per);
+}
+
+template <int RC>
 __global__ void __launch_bounds__(SB) solve_fwd_kernel(const RecordH* __restrict__ recs, int rec0,
                                                        const int64_t* __restrict__ g_off, double* V, double* G,
                                                        int nrhs, int red_rows) {
@@ -89,7 +100,13 @@ __global__ void __launch_bounds__(SB) solve_fwd_kernel(const RecordH* __restrict
   const RecordH R = recs[blockIdx.x];
   const int n = R.n, w = R.w;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int r0, r1, c0, c1;
+  chunk_range(n, blockIdx.y, gridDim.y, 32, r0, r1);
+  chunk_range(w, blockIdx.y, gridDim.y, 8, c0, c1);
   double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
+  // segment of W lanes per X_top column (short columns: several per warp)
+  const int W = n > 128 ? 32 : (n > 64 ? 16 : 8);
+  const int seg = lane / W, sl = lane & (W - 1), spw = 32 / W;
   for (int q0 = 0; q0 < nrhs; q0 += RC) {
     const int nq = min(RC, nrhs - q0);
     for (int e = threadIdx.x; e < n * RC; e += SB) {
@@ -97,35 +114,42 @@ __global__ void __launch_bounds__(SB) solve_fwd_kernel(const RecordH* __restrict
       bsh[e] = q < nq ? V[(R.xoff + c) * nrhs + q0 + q] : 0.0;
     }
     __syncthreads();
-    // g = Sinv b
-    cta_gemv_cols(R.sinv, n, n, (size_t)n, [&](int c, int q) { return bsh[c * RC + q]; }, nq, red,
-                  [&](int t, int q, double v) { g[(size_t)t * nrhs + q0 + q] = v; });
-    // v[pos] -= X_top^T b : warp per column, 2 columns in flight
-    for (int c = warp; c < w; c += SWARPS) {
-      const double* x = R.xtop + (size_t)c * n;
+    // g[r0:r1] = Sinv[r0:r1, :] b
+    if (r1 > r0)
+      cta_gemv_cols<RC>(R.sinv + r0, r1 - r0, n, (size_t)n, [&](int c, int q) { return bsh[c * RC + q]; }, nq, red,
+                    [&](int t, int q, double v) { g[(size_t)(r0 + t) * nrhs + q0 + q] = v; });
+    // v[pos[c]] -= X_top(:, c)^T b for c in [c0, c1)
+    for (int cb = c0 + warp * spw; cb < c1; cb += SWARPS * spw) {
+      const int c = cb + seg;
+      const bool ok = c < c1;
+      const double* x = R.xtop + (size_t)(ok ? c : c0) * n;
       double s[RC];
 #pragma unroll
       for (int q = 0; q < RC; q++) s[q] = 0.0;
-      for (int t = lane; t < n; t += 32) {
-        const double a = x[t];
+      if (ok)
+        for (int t = sl; t < n; t += W) {
+          const double a = x[t];
 #pragma unroll
-        for (int q = 0; q < RC; q++) s[q] = fma(a, bsh[t * RC + q], s[q]);
-      }
+          for (int q = 0; q < RC; q++)
+            if (q < nq) s[q] = fma(a, bsh[t * RC + q], s[q]);
+        }
 #pragma unroll
       for (int q = 0; q < RC; q++)
-        if (q < nq) s[q] = warp_sum(s[q]);
-      if (lane < nq) {
+        if (q < nq)
+          for (int o = W >> 1; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+      if (ok && sl < nq) {
         double sv = s[0];
 #pragma unroll
         for (int q = 1; q < RC; q++)
-          if (lane == q) sv = s[q];
-        V[(int64_t)R.pos[c] * nrhs + q0 + lane] -= sv;
+          if (sl == q) sv = s[q];
+        V[(int64_t)R.pos[c] * nrhs + q0 + sl] -= sv;
       }
     }
     __syncthreads();
   }
 }
 
+template <int RC>
 __global__ void __launch_bounds__(SB) solve_bwd_kernel(const RecordH* __restrict__ recs, int rec0,
                                                        const int64_t* __restrict__ g_off, double* V,
                                                        const double* G, int nrhs, int red_rows) {
@@ -133,14 +157,18 @@ __global__ void __launch_bounds__(SB) solve_bwd_kernel(const RecordH* __restrict
   double* red = sm;                         // min(maxn, 256) x SWARPS x RC
   const RecordH R = recs[blockIdx.x];
   const int n = R.n, w = R.w;
+  int r0, r1;
+  chunk_range(n, blockIdx.y, gridDim.y, 32, r0, r1);
+  if (r1 <= r0) return;
   const double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
   for (int q0 = 0; q0 < nrhs; q0 += RC) {
     const int nq = min(RC, nrhs - q0);
     // partner values are gathered on the fly (the coupling width can exceed shared memory)
-    cta_gemv_cols(R.xtop, n, w, (size_t)n, [&](int c, int q) { return V[(int64_t)R.pos[c] * nrhs + q0 + q]; }, nq,
-                  red, [&](int t, int q, double v) {
-      V[(R.xoff + t) * nrhs + q0 + q] = g[(size_t)t * nrhs + q0 + q] - v;
-    });
+    cta_gemv_cols<RC>(R.xtop + r0, r1 - r0, w, (size_t)n,
+                  [&](int c, int q) { return V[(int64_t)R.pos[c] * nrhs + q0 + q]; }, nq, red,
+                  [&](int t, int q, double v) {
+                    V[(R.xoff + r0 + t) * nrhs + q0 + q] = g[(size_t)(r0 + t) * nrhs + q0 + q] - v;
+                  });
   }
 }
 
@@ -213,6 +241,14 @@ void solve_refined(FactorH* F, StoreH* S, const double* rhs, double* x, int64_t 
   CK(cudaStreamSynchronize(s));
 }
 
+// CTAs per record: enough to fill the GPU (~4 per SM) for batches of few,
+// large records, at least 32 rows per chunk
+static int solve_chunks(const BatchH& b) {
+  const int nrec = std::max(1, b.rec1 - b.rec0);
+  const int want = (148 * 4 + nrec - 1) / nrec;
+  return std::max(1, std::min(want, (b.maxn + 31) / 32));
+}
+
 void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_ptr) {
   TreeH* t = F->tree;
   const int64_t N = t->N;
@@ -235,15 +271,20 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
   launch_permute(din, V + F->lvl_base[t->depth] * nr, t->d_perm, N, nr, false, s);
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(solve_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(solve_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(solve_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(solve_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(solve_fwd_kernel<RCMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(solve_bwd_kernel<RCMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
+  const int RC = nr == 1 ? 1 : RCMAX;
   for (const BatchH& b : F->batches) {
     const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
     const size_t smem = sizeof(double) * (size_t(rr) * SWARPS * RC + size_t(b.maxn) * RC);
     if (smem > 200 * 1024) invalid("solve: pivot block too large for the solve kernel");
-    solve_fwd_kernel<<<b.rec1 - b.rec0, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
+    const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));
+    if (RC == 1) solve_fwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
+    else solve_fwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
   }
   // top: y = T^-1 b on the level-1 slots (viewed column-major as nrhs x M)
@@ -253,7 +294,10 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     double* tmp = ws.alloc_n<double>(size_t(M) * nr);
     CK(cudaMemcpyAsync(tmp, vt, sizeof(double) * M * nr, cudaMemcpyDeviceToDevice, s));
     GemmBatch gb;
-    Staging st;
+    // pinned staging for the GEMM descriptors: kept across calls (a fresh
+    // cudaMallocHost per solve costs milliseconds and its free synchronises)
+    static thread_local Staging st;
+    st.reset();
     gb.add(tmp, nr, F->top_inv, M, vt, nr, nr, M, M, 1.0, 0.0);
     launch_grouped_gemm(gb, false, true, ws, st, s);
     CK(cudaStreamSynchronize(s));
@@ -262,7 +306,9 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     const BatchH& b = *it;
     const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
     const size_t smem = sizeof(double) * size_t(rr) * SWARPS * RC;
-    solve_bwd_kernel<<<b.rec1 - b.rec0, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
+    const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));
+    if (RC == 1) solve_bwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
+    else solve_bwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
   }
   launch_permute(V + F->lvl_base[t->depth] * nr, dout, t->d_perm, N, nr, true, s);

@@ -93,8 +93,9 @@ class IfmmFactorization:
 
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None
-        if h:
-            _lib.lib.ifmm_factor_free(h)
+        lib = getattr(_lib, "lib", None)
+        if h and lib is not None:  # at interpreter shutdown the module may already be torn down
+            lib.ifmm_factor_free(h)
 
 
 PHASES = ("gather", "gauss_jordan", "x_gemm", "schur_gemm", "compress", "transition", "top")
