@@ -250,33 +250,31 @@ void launch_schur(SchurBatch& b, Arena& ws, Staging& st, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ norms
+// 1-norm (max column abs sum) of every matrix: grid (matrix, 64-column chunk);
+// chunk maxima merge with an integer atomicMax on the bit patterns, which
+// orders non-negative doubles exactly (and lets a NaN column win)
 __global__ void __launch_bounds__(256) norm1_kernel(const MatDesc* __restrict__ desc, double* out) {
-  __shared__ double red[32];
   const MatDesc D = desc[blockIdx.x];
-  double best = 0.0;
-  for (int c = threadIdx.x >> 5; c < D.m; c += blockDim.x >> 5) {
-    double s = 0.0;
-    for (int r = threadIdx.x & 31; r < D.m; r += 32) s += fabs(D.A[r + (size_t)c * D.lda]);
-    s = warp_sum(s);
-    best = fmax(best, s);
-  }
-  // block max via the sum helper on a max-reduce: reuse smem manually
+  const int c0 = blockIdx.y * 64;
+  if (c0 >= D.m) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) red[wid] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) b = fmax(b, red[w]);
-    // NaN propagates as non-finite norm
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++)
-      if (red[w] != red[w]) b = red[w];
-    out[blockIdx.x] = b;
+  double best = 0.0;
+  for (int c = c0 + wid; c < min(D.m, c0 + 64); c += 8) {
+    double s = 0.0;
+    for (int r = lane; r < D.m; r += 32) s += fabs(D.A[r + (size_t)c * D.lda]);
+    s = warp_sum(s);
+    best = (s != s || best != best) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(best, s);
   }
+  if (lane == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out + blockIdx.x),
+              static_cast<unsigned long long>(__double_as_longlong(best)));
 }
 
-void launch_norm1(const MatDesc* d_desc, int n, double* out, cudaStream_t s) {
+
+void launch_norm1(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s) {
   if (n <= 0) return;
-  norm1_kernel<<<n, 256, 0, s>>>(d_desc, out);
+  CK(cudaMemsetAsync(out, 0, sizeof(double) * n, s));
+  norm1_kernel<<<dim3(n, std::max(1, (maxm + 63) / 64)), 256, 0, s>>>(d_desc, out);
   CK_LAUNCH();
 }
 

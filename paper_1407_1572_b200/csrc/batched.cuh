@@ -41,7 +41,7 @@ struct MatDesc {
 };
 
 // 1-norm (max column abs sum) of every matrix -> out[p]
-void launch_norm1(const MatDesc* d_desc, int n, double* out, cudaStream_t s);
+void launch_norm1(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s);
 // dlacn2 (Hager/Higham) estimate of the 1-norm of every matrix -> out[p]; out
 // holds the exact norm on entry and is only replaced where
 // exact * normA[p] >= limit (the estimate is <= the exact norm)

@@ -376,8 +376,11 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   static const bool narrow = getenv("IFMM_BS128") != nullptr;  // debug: force 128-thread CTAs
   static const int warp_mx = getenv("IFMM_WARP_MX") ? atoi(getenv("IFMM_WARP_MX")) : 0;
   const bool wmode = !narrow && MX <= warp_mx;
-  const int bs_fill = narrow ? 128 : (MX >= 256 && nf < 2048) ? 512 : (MX >= 128 ? 256 : 128);
-  const int bs_dirs = narrow ? 128 : MX >= 256 ? 512 : (MX >= 128 ? 256 : 128);
+  // fine levels: small CTAs, many fills in flight per SM (IFMM_BS_SMALL: tuning)
+  static const int bs_small = getenv("IFMM_BS_SMALL") ? atoi(getenv("IFMM_BS_SMALL")) : 128;
+  const int per_sm = 8 * 128 / bs_small;  // resident CTAs per SM at 64 registers
+  const int bs_fill = narrow ? 128 : (MX >= 256 && nf < 2048) ? 512 : (MX >= 128 ? 256 : bs_small);
+  const int bs_dirs = narrow ? 128 : MX >= 256 ? 512 : (MX >= 128 ? 256 : bs_small);
   constexpr int WPB = 4;  // warps per CTA in warp mode
   static const bool prof = getenv("IFMM_PROF") != nullptr;
   static const int jac_reg = getenv("IFMM_JACOBI_REG") ? atoi(getenv("IFMM_JACOBI_REG")) : 0;
@@ -424,7 +427,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       }
     } else {
       const size_t slot = k1_slot(KK);
-      const int grid = resident_grid(nf, 8);
+      const int grid = resident_grid(nf, bs_fill == bs_small ? per_sm : 8);
       double* scr = ws.alloc_n<double>(slot * grid);
       aca_recompress_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
                                                                slot, MR, MC, KK, 0);
@@ -466,7 +469,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       const int* doff = upload(ws, off, s, st);
       const int* dlst = upload(ws, lst, s, st);
       const int n = int(tasks.size());
-      const int grid = grid_for(n, 8, 32);
+      const int grid = grid_for(n, bs_d == bs_small ? per_sm : 8, 32);
       double* scr = ws.alloc_n<double>(dslot * workers(grid));
       if (wmode)
         augment_kernel<WarpGroup><<<grid, bs_d, 0, s>>>(dfd, doff, dlst, n, d_state, d_rank, tol, scr, dslot, MX, KK,
@@ -480,7 +483,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   // K4
   {
     const size_t slot = 2 * size_t(MX) * KK + 64;
-    const int grid = grid_for(nf, 8, 32);
+    const int grid = grid_for(nf, bs_fill == bs_small ? per_sm : 8, 32);
     double* scr = ws.alloc_n<double>(slot * workers(grid));
     if (wmode)
       delta_kernel<WarpGroup><<<grid, 32 * WPB, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats);

@@ -13,6 +13,7 @@ namespace ifmm {
 
 struct CtaShared {
   double red[32];
+  double red2[32];
   ArgMax am[32];
   int flag;
   int ival[4];
@@ -42,6 +43,25 @@ struct CtaGroup {
   __device__ double sum(double v) const { return block_sum(v, sh.red); }
   __device__ ArgMax argmax(ArgMax v) const { return block_argmax(v, sh.am); }
   __device__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
+  // combine warp-reduced partials (identical in every lane) over the group:
+  // two sums and an argmax in one publish/reduce round (two barriers)
+  __device__ void combine(double& a, double& b, ArgMax& c) const {
+    __syncthreads();
+    if (lane() == 0) {
+      sh.red[warp()] = a;
+      sh.red2[warp()] = b;
+      sh.am[warp()] = c;
+    }
+    __syncthreads();
+    a = 0.0;
+    b = 0.0;
+    c = ArgMax{-1.0, -1};
+    for (int w = 0; w < nwarps(); w++) {
+      a += sh.red[w];
+      b += sh.red2[w];
+      c = argmax_merge(c, sh.am[w]);
+    }
+  }
   __device__ static CtaGroup make_for_test(CtaShared& sh) { return CtaGroup{sh}; }
 };
 
@@ -56,6 +76,7 @@ struct WarpGroup {
   __device__ double sum(double v) const { return warp_sum(v); }
   __device__ ArgMax argmax(ArgMax v) const { return warp_argmax(v); }
   __device__ bool any(bool p) const { return __any_sync(0xffffffffu, p) != 0; }
+  __device__ void combine(double&, double&, ArgMax&) const { __syncwarp(); }  // already warp-reduced
   __device__ static WarpGroup make_for_test(CtaShared&) { return WarpGroup{}; }
 };
 
@@ -580,28 +601,35 @@ __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, i
     }
     for (int c = g.rank(); c < n; c += g.size()) v[c] = rr[c];
     g.sync();
+    // one combined reduction: ||u||^2, ||v||^2, the next row (largest |u|
+    // among unused rows) and the cross terms |u.u_t||v.v_t| of the estimate
     double su = 0.0, sv = 0.0;
-    for (int r = g.rank(); r < m; r += g.size()) su += u[r] * u[r];
+    ArgMax nx{-1.0, -1};
+    for (int r = g.rank(); r < m; r += g.size()) {
+      su += u[r] * u[r];
+      const double a = (usedr[r] || r == i) ? -1.0 : fabs(u[r]);
+      nx = argmax_merge(nx, ArgMax{a, r});
+    }
     for (int c = g.rank(); c < n; c += g.size()) sv += v[c] * v[c];
-    su = g.sum(su);
-    sv = g.sum(sv);
+    su = warp_sum(su);
+    sv = warp_sum(sv);
+    nx = warp_argmax(nx);
+    for (int t = warp; t < k; t += nw) {
+      double du = 0.0, dv = 0.0;
+      const double* ut = Uc + (size_t)t * m;
+      const double* vt = Vc + (size_t)t * n;
+      for (int r = lane; r < m; r += 32) du += u[r] * ut[r];
+      for (int c = lane; c < n; c += 32) dv += v[c] * vt[c];
+      du = warp_sum(du);
+      dv = warp_sum(dv);
+      if (lane == 0) dots[t] = fabs(du) * fabs(dv);
+    }
+    g.combine(su, sv, nx);  // also publishes dots[]
     const double csq = su * sv;
     if (k > 0) {
-      for (int t = warp; t < k; t += nw) {
-        double du = 0.0, dv = 0.0;
-        const double* ut = Uc + (size_t)t * m;
-        const double* vt = Vc + (size_t)t * n;
-        for (int r = lane; r < m; r += 32) du += u[r] * ut[r];
-        for (int c = lane; c < n; c += 32) dv += v[c] * vt[c];
-        du = warp_sum(du);
-        dv = warp_sum(dv);
-        if (lane == 0) dots[t] = fabs(du) * fabs(dv);
-      }
-      g.sync();
       double cross = 0.0;
       for (int t = 0; t < k; t++) cross += dots[t];
       nsq += csq + 2.0 * cross;
-      g.sync();
     } else {
       nsq = csq;
     }
@@ -610,12 +638,6 @@ __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, i
       done = true;
       break;
     }
-    ArgMax nx{-1.0, -1};
-    for (int r = g.rank(); r < m; r += g.size()) {
-      const double a = (usedr[r] || r == i) ? -1.0 : fabs(u[r]);
-      nx = argmax_merge(nx, ArgMax{a, r});
-    }
-    nx = g.argmax(nx);
     if (nx.i < 0 || nx.a < 0.0) {
       done = true;
       break;

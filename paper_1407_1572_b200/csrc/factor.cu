@@ -138,6 +138,14 @@ class Factorizer {
   Arena* lvl_arena_;  // [2], alternating between levels
   PhaseTimer tm_;
   WorkLevel cur_, prev_;
+  // debug (IFMM_HOST_PROF): host ms per section of eliminate_batch, per level
+  double hsec_[8] = {0};
+  std::chrono::steady_clock::time_point hmark_;
+  void hmark(int sec) {
+    const auto now = std::chrono::steady_clock::now();
+    hsec_[sec] += std::chrono::duration<double, std::milli>(now - hmark_).count();
+    hmark_ = now;
+  }
   // per-record host metadata for pos resolution at level end
   struct SlotRef { int kind, j, dim; };  // kind 0: x_j, 1: y_j
   std::vector<std::vector<SlotRef>> rec_slots_;
@@ -325,6 +333,7 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
 
 void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred) {
   const auto t_batch0 = std::chrono::steady_clock::now();
+  hmark_ = t_batch0;
   WorkLevel& W = cur_;
   const Topo& T = *W.T;
   const int k = W.k;
@@ -356,9 +365,11 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     piv.swap(keep);
   }
   const int np = int(piv.size());
+  hmark(0);
   CK(cudaStreamSynchronize(s_));  // staging buffers of earlier uploads are free after this
   ws_.reset();
   st_.reset();
+  hmark(1);
   struct PivInfo {
     int i, n, r, m, w;
     std::vector<int> xp, yp;
@@ -407,6 +418,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     }
     cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
   }
+  hmark(2);
   tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
   static const char* dump_dir = getenv("IFMM_DUMP_SINGULAR");
@@ -420,16 +432,15 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   double* d_nS = ws_.alloc_n<double>(np);
   double* d_nSi = ws_.alloc_n<double>(np);
   int* d_info = ws_.alloc_n<int>(np);
+  int maxm = 0;
+  for (auto& d : md) maxm = std::max(maxm, d.m);
   tm_.begin(PH_GJ);
-  launch_norm1(dmd, np, d_nS, s_);
+  launch_norm1(dmd, np, maxm, d_nS, s_);
   S_->work->gj_side.ensure();
   batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &S_->work->gj_side);
-  {
-    int maxm = 0;
-    for (auto& d : md) maxm = std::max(maxm, d.m);
-    launch_norm1(dmd, np, d_nSi, s_);
-    launch_norm1_estimate(dmd, np, maxm, d_nSi, d_nS, cond_limit_, s_);
-  }
+  launch_norm1(dmd, np, maxm, d_nSi, s_);
+  launch_norm1_estimate(dmd, np, maxm, d_nSi, d_nS, cond_limit_, s_);
+  hmark(3);
   // records + X = S^-1 C
   GemmBatch gb;
   for (int t = 0; t < np; t++) {
@@ -517,6 +528,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
   tm_.end();
+  hmark(4);
   // fill-in compression (reference order: hybrid pairs sorted, then P2P pairs sorted)
   CompressBatch cbz;
   cbz.chain_off.assign(1, 0);
@@ -581,9 +593,11 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   int* d_stats = ws_.alloc_n<int>(4);
   CK(cudaMemsetAsync(d_stats, 0, 16, s_));
   static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
+  hmark(5);
   tm_.begin(PH_COMPRESS);
   run_compression(cbz, tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_state, d_stats, ws_, st_, s_, dbg ? 1 : 0);
   tm_.end();
+  hmark(6);
   // read back: pivot conditioning, ranks, fill outcomes, counters
   const auto t_sync0 = std::chrono::steady_clock::now();
   std::vector<double> nS(np), nSi(np);
@@ -648,6 +662,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     else set_pp(W, h.p, h.q, 0);
   }
   for (int t = 0; t < np; t++) W.dead[P[t].i] = 1;
+  hmark(7);
   (void)colour;
 }
 
@@ -774,7 +789,12 @@ FactorH* Factorizer::run() {
     }
     const auto tf0 = std::chrono::steady_clock::now();
     finish_level(rec_begin);
-    if (hprof) fprintf(stderr, "host level %d: finish %.1f ms, level total %.1f ms\n", k, since(tf0), since(tl0));
+    if (hprof) {
+      fprintf(stderr, "host level %d: finish %.1f ms, level total %.1f ms\n", k, since(tf0), since(tl0));
+      fprintf(stderr, "  batches: guard %.1f sync %.1f gather %.1f gj %.1f rec+x+schur %.1f fills %.1f compress %.1f readback %.1f\n",
+              hsec_[0], hsec_[1], hsec_[2], hsec_[3], hsec_[4], hsec_[5], hsec_[6], hsec_[7]);
+    }
+    for (double& h : hsec_) h = 0.0;
     F_->r_m = std::max(F_->r_m, F_->stats[k].max_rank);
   }
   const auto tt0 = std::chrono::steady_clock::now();
