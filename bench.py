@@ -283,6 +283,13 @@ def main():
     schur_ms, schur_launches = ph["schur_gemm"]
     achieved = work["flops_schur"] / (schur_ms * 1e-3) / 1e12 if schur_ms > 0 else None
     fac_ms_dev = sum(v[0] for v in ph.values())
+    # DRAM traffic of one Schur launch from the committed ncu --set full capture
+    traffic = {}
+    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_schur_l5_ncu.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh)
+        traffic["source"] = os.path.relpath(tp, os.path.dirname(os.path.abspath(__file__)))
     # solve: HBM roofline
     hb, hb_src = hbm_peak()
     ts = []
@@ -314,10 +321,17 @@ def main():
                   "fp64_tflops_step": work["flops_exec"] / t_step / 1e12},
         "phase_ms": {k: round(v[0], 3) for k, v in ph.items()},
         "phase_ms_by_level": ft.phase_times_by_level,
-        "roofline": {"kernel": "grouped_dgemm_kernel<true,false> (Schur update)", "bound": "tensor",
+        "roofline": {"kernel": "schur_concat_kernel (Schur update T = C^T S^-1 C, DMMA m8n8k4)", "bound": "tensor",
                      "achieved": achieved, "peak": fl_peak, "unit": "TFLOP/s",
-                     "frac": (achieved / fl_peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / fl_peak) if achieved else None,
+                     "traffic": traffic.get("dram_bytes_per_launch"),
+                     "traffic_launch": traffic.get("kernel"),
+                     "traffic_algorithmic_bytes": traffic.get("algorithmic_bytes_per_launch"),
+                     "traffic_source": traffic.get("source"),
+                     "launches": schur_launches,
                      "share_of_factor": schur_ms / fac_ms_dev if fac_ms_dev else None,
+                     "achieved_source": "executed upper-triangle flops / CUDA-event time of the Schur launches "
+                                        "on the library stream",
                      "peak_source": "measured live: cuBLAS DGEMM 8192^3 (torch.matmul float64)"},
         "solve_roofline": {"bound": "hbm", "ms": solve_ms, "bytes": work["solve_bytes"],
                            "achieved": work["solve_bytes"] / (solve_ms * 1e-3) / 1e9, "peak": hb, "unit": "GB/s",

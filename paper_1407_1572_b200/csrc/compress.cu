@@ -165,12 +165,16 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
 // Two-pass projection, then QR + Jacobi on the small R factor.
 template <class G>
 __device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig, double* U, int rU, double cutoff,
-                        double* Q, double* R, double* E, double* sig, int* ord, double* vv) {
+                        double* Q, double* R, double* E, double* sig, int* ord, double* vv, int pre = 0) {
   const int cap = nU - rU;
   if (cap <= 0 || r == 0) return 0;
   PROF_T0();
-  g_project_out(g, H, nU, nU, r, U, nU, rU, E);
-  g_project_out(g, H, nU, nU, r, U, nU, rU, E);
+  // the first `pre` columns of U were projected out (twice) by the parallel
+  // pre-pass; (I - W W^T)(I - U0 U0^T) = I - U U^T for W orthogonal to U0
+  if (rU > pre) {
+    g_project_out(g, H, nU, nU, r, U + (size_t)pre * nU, nU, rU - pre, E);
+    g_project_out(g, H, nU, nU, r, U + (size_t)pre * nU, nU, rU - pre, E);
+  }
   PROF_ACC(4);
   if (wsig) {
     for (int e = g.rank(); e < nU * r; e += g.size()) H[e] *= wsig[e / nU];
@@ -257,11 +261,47 @@ __device__ inline DirScratch carve_dirs(double* s, int MX, int KK) {
 // proceed independently -- the reference's sequential order restricted to
 // each basis (ifmm/solver.py:334-358, 495-520).  Task = fill * 2 + side
 // (0: q side, 1: p side).
+// Pre-pass of the augmentation: for every task, H = the fill factor that
+// task appends (right factor weighted by sigma for a q side, left factor for
+// a p side) with the cluster's batch-initial basis U0 = U(:, :rank0) projected
+// out twice.  Independent across tasks (the serial chains then only project
+// against the columns appended during the batch).  Hbuf[t] holds nU x Kf.
+template <class G>
+__global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks)
+    augment_prep_kernel(const FillDesc* __restrict__ fills, const int* __restrict__ aug, int ntasks,
+                        const FillState* __restrict__ state, const int* __restrict__ rank, double tol,
+                        double* const* __restrict__ Hbuf, double* scratch, size_t slot) {
+  __shared__ CtaShared sh;
+  const G g = Worker<G>::make(sh);
+  double* E = scratch + slot * Worker<G>::id();
+  for (int u = Worker<G>::id(); u < ntasks; u += Worker<G>::count()) {
+    const int f = aug[u] >> 1, side = aug[u] & 1;
+    const FillDesc D = fills[f];
+    const int r = state[f].r, status = state[f].status;
+    if (status != 0 || r == 0 || tol <= 0.0) continue;
+    const int nU = side ? D.rows : D.cols;
+    const int cl = side ? D.p : D.q;
+    const int r0 = rank[cl];
+    double* H = Hbuf[u];
+    const double* right = D.out + (size_t)D.rows * D.Kf;
+    const double* src = side ? D.out : right;
+    const double* wsig = side ? nullptr : right + (size_t)D.cols * D.Kf;
+    for (int e = g.rank(); e < nU * r; e += g.size()) H[e] = wsig ? src[e] * wsig[e / nU] : src[e];
+    g.sync();
+    if (r0 > 0 && r0 < nU) {
+      const double* U = side ? D.Up : D.Uq;
+      g_project_out(g, H, nU, nU, r, U, nU, r0, E);
+      g_project_out(g, H, nU, nU, r, U, nU, r0, E);
+    }
+    g.sync();
+  }
+}
+
 template <class G>
 __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks)
     augment_kernel(const FillDesc* __restrict__ fills, const int* __restrict__ aug_off, const int* __restrict__ aug,
                    int nchains, FillState* state, int* rank, double tol, double* scratch, size_t slot, int MX, int KK,
-                   int debug) {
+                   int debug, double* const* __restrict__ Hbuf) {
   __shared__ CtaShared sh;
   const G g = Worker<G>::make(sh);
   DirScratch d = carve_dirs(scratch + slot * Worker<G>::id(), MX, KK);
@@ -269,21 +309,18 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks)
     const int t0 = aug_off[c], t1 = aug_off[c + 1];
     const int side0 = aug[t0] & 1;
     const int cl = side0 ? fills[aug[t0] >> 1].p : fills[aug[t0] >> 1].q;
-    int rc = rank[cl];
+    const int r0 = rank[cl];  // batch-initial rank: already projected out by the pre-pass
+    int rc = r0;
     for (int u = t0; u < t1; u++) {
       const int f = aug[u] >> 1, side = aug[u] & 1;
       const FillDesc D = fills[f];
       const int r = state[f].r, status = state[f].status;
       const double fro = state[f].fro;
       if (status == 0 && r > 0 && tol > 0.0) {
-        const double* right = D.out + (size_t)D.rows * D.Kf;
-        const double* H0 = side ? D.out : right;
         const int nU = side ? D.rows : D.cols;
-        for (int e = g.rank(); e < nU * r; e += g.size()) d.H[e] = H0[e];
-        g.sync();
-        const double* wsig = side ? nullptr : right + (size_t)D.cols * D.Kf;
-        const int w = new_dirs(g, d.H, nU, r, wsig, side ? D.Up : D.Uq, rc, tol * fro, d.Q, d.R, d.E, d.sig, d.ord,
-                               d.vv);
+        // r0 == nU: the pre-pass skipped (no room); new_dirs returns 0 anyway
+        const int w = new_dirs(g, Hbuf[u], nU, r, nullptr, side ? D.Up : D.Uq, rc, tol * fro, d.Q, d.R, d.E, d.sig,
+                               d.ord, d.vv, r0 < nU ? r0 : 0);
         if (debug && g.rank() == 0)
           printf("aug kind=%d side=%d p=%d q=%d r=%d +%d -> %d\n", D.kind, side, D.p, D.q, r, w, rc + w);
         rc += w;
@@ -379,8 +416,12 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   // fine levels: small CTAs, many fills in flight per SM (IFMM_BS_SMALL: tuning)
   static const int bs_small = getenv("IFMM_BS_SMALL") ? atoi(getenv("IFMM_BS_SMALL")) : 128;
   const int per_sm = 8 * 128 / bs_small;  // resident CTAs per SM at 64 registers
-  const int bs_fill = narrow ? 128 : (MX >= 256 && nf < 2048) ? 512 : (MX >= 128 ? 256 : bs_small);
-  const int bs_dirs = narrow ? 128 : MX >= 256 ? 512 : (MX >= 128 ? 256 : bs_small);
+  // coarse levels: per-step latency of few long chains dominates -> widest CTAs
+  // for the largest blocks (measured: 1024 wins for MX >= ~800, loses at 265-570)
+  static const int bs_big_env = getenv("IFMM_BS_BIG") ? atoi(getenv("IFMM_BS_BIG")) : 0;  // tuning override
+  const int bs_big = bs_big_env ? bs_big_env : (MX >= 700 ? 1024 : 512);
+  const int bs_fill = narrow ? 128 : (MX >= 256 && nf < 2048) ? bs_big : (MX >= 128 ? 256 : bs_small);
+  const int bs_dirs = narrow ? 128 : MX >= 256 ? bs_big : (MX >= 128 ? 256 : bs_small);
   constexpr int WPB = 4;  // warps per CTA in warp mode
   static const bool prof = getenv("IFMM_PROF") != nullptr;
   static const int jac_reg = getenv("IFMM_JACOBI_REG") ? atoi(getenv("IFMM_JACOBI_REG")) : 0;
@@ -459,6 +500,11 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       push(cb.fills[f].q, f * 2);
       push(cb.fills[f].p, f * 2 + 1);
     }
+    if (prof && !tasks.empty()) {
+      size_t mx = 0, tot = 0;
+      for (auto& t : tasks) { mx = std::max(mx, t.size()); tot += t.size(); }
+      fprintf(stderr, "chains %zu tasks %zu max len %zu avg %.2f\n", tasks.size(), tot, mx, double(tot) / tasks.size());
+    }
     if (!tasks.empty()) {
       std::vector<int> off(1, 0), lst;
       lst.reserve(2 * cb.fills.size());
@@ -469,14 +515,34 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       const int* doff = upload(ws, off, s, st);
       const int* dlst = upload(ws, lst, s, st);
       const int n = int(tasks.size());
+      const int ntask = int(lst.size());
+      // per-task direction buffers (nU x Kf: the fill's rank is only known on the device)
+      std::vector<double*> hb(lst.size());
+      for (size_t u = 0; u < lst.size(); u++) {
+        const FillDesc& D = cb.fills[lst[u] >> 1];
+        hb[u] = ws.alloc_n<double>(size_t((lst[u] & 1) ? D.rows : D.cols) * D.Kf);
+      }
+      double* const* dhb = upload(ws, hb, s, st);
+      {
+        const size_t pslot = size_t(MX) * KK + 64;
+        const int pgrid = grid_for(ntask, bs_d == bs_small ? per_sm : 8, 32);
+        double* pscr = ws.alloc_n<double>(pslot * workers(pgrid));
+        if (wmode)
+          augment_prep_kernel<WarpGroup><<<pgrid, bs_d, 0, s>>>(dfd, dlst, ntask, d_state, d_rank, tol, dhb, pscr,
+                                                                  pslot);
+        else
+          augment_prep_kernel<CtaGroup><<<pgrid, bs_d, 0, s>>>(dfd, dlst, ntask, d_state, d_rank, tol, dhb, pscr,
+                                                                 pslot);
+        CK_LAUNCH();
+      }
       const int grid = grid_for(n, bs_d == bs_small ? per_sm : 8, 32);
       double* scr = ws.alloc_n<double>(dslot * workers(grid));
       if (wmode)
         augment_kernel<WarpGroup><<<grid, bs_d, 0, s>>>(dfd, doff, dlst, n, d_state, d_rank, tol, scr, dslot, MX, KK,
-                                                          debug);
+                                                          debug, dhb);
       else
         augment_kernel<CtaGroup><<<grid, bs_d, 0, s>>>(dfd, doff, dlst, n, d_state, d_rank, tol, scr, dslot, MX, KK,
-                                                         debug);
+                                                         debug, dhb);
       CK_LAUNCH();
     }
   }

@@ -32,7 +32,7 @@ __device__ __forceinline__ ArgMax warp_argmax(ArgMax v) {
 }
 
 struct CtaGroup {
-  static constexpr int kMaxThreads = 512, kMinBlocks = 2;  // launch bounds of kernels templated on the group
+  static constexpr int kMaxThreads = 1024, kMinBlocks = 1;  // launch bounds of kernels templated on the group (64 registers)
   CtaShared& sh;
   __device__ int rank() const { return threadIdx.x; }
   __device__ int size() const { return blockDim.x; }
