@@ -91,6 +91,19 @@ void launch_copies(CopyBatch& b, Arena& ws, Staging& st, cudaStream_t s) {
   b.clear();
 }
 
+// ------------------------------------------------------------------ positions
+__global__ void pos_expand_kernel(const PosRun* __restrict__ runs, int n, int* pos) {
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
+    const PosRun R = runs[r];
+    for (int u = threadIdx.x & 31; u < R.dim; u += 32) pos[R.out + u] = int(R.base + u);
+  }
+}
+void launch_pos_expand(const PosRun* d_runs, int n, int* pos, cudaStream_t s) {
+  if (n <= 0) return;
+  pos_expand_kernel<<<std::min(148 * 8, (n + 7) / 8), 256, 0, s>>>(d_runs, n, pos);
+  CK_LAUNCH();
+}
+
 // ------------------------------------------------------------------ gemm launch
 void launch_grouped_gemm(GemmBatch& b, bool transA, bool transB, Arena& ws, Staging& st, cudaStream_t s) {
   if (b.probs.empty()) return;

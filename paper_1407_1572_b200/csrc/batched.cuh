@@ -31,6 +31,13 @@ struct CopyBatch {
 };
 void launch_copies(CopyBatch& b, Arena& ws, Staging& st, cudaStream_t s);
 
+// pos[out + u] = base + u for u < dim (solve partner positions)
+struct PosRun {
+  int64_t base, out;
+  int dim, pad;
+};
+void launch_pos_expand(const PosRun* d_runs, int n, int* pos, cudaStream_t s);
+
 // Matrix descriptor for batched dense kernels (column-major).
 struct MatDesc {
   double* A;

@@ -1,6 +1,7 @@
 // Host-side handles of the B200 IFMM: tree, initial operator store,
 // factorization.  Device memory is owned by per-handle arenas.
 #pragma once
+#include <algorithm>
 #include <array>
 #include <memory>
 #include <mutex>
@@ -31,7 +32,48 @@ struct Topo {
     }
     return s;
   }
+  // per cluster: bit s set iff the window slot s holds an interaction-list
+  // member (built by prepare(), so in_il is a bit test instead of a scan)
+  std::vector<uint64_t> il_mask;
+  // per cluster: the clusters of its 7^dim window, sorted (CSR)
+  std::vector<int> wc_off, wc;
+  void prepare() {
+    if (!wc_off.empty() || nc == 0) return;
+    if (win() <= 64) il_mask.assign(nc, 0);  // 3-D windows (343 slots) keep the scan
+    for (int i = 0; i < nc && !il_mask.empty(); i++)
+      for (int t = il_off[i]; t < il_off[i + 1]; t++) {
+        const int sl = slot(i, il[t]);
+        if (sl >= 0) il_mask[i] |= uint64_t(1) << sl;
+      }
+    wc_off.assign(nc + 1, 0);
+    wc.clear();
+    std::vector<int> cand;
+    for (int i = 0; i < nc; i++) {
+      int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+      for (int d = 0; d < dim; d++) {
+        lo[d] = std::max(0, grid[i * dim + d] - 3);
+        hi[d] = std::min((1 << k) - 1, grid[i * dim + d] + 3);
+      }
+      cand.clear();
+      int g[3];
+      for (g[0] = lo[0]; g[0] <= hi[0]; g[0]++)
+        for (g[1] = lo[1]; g[1] <= hi[1]; g[1]++)
+          for (g[2] = lo[2]; g[2] <= hi[2]; g[2]++) {
+            int64_t c = 0;
+            for (int b = 0; b < k; b++)
+              for (int ax = 0; ax < dim; ax++) c |= int64_t((g[ax] >> b) & 1) << (b * dim + ax);
+            cand.push_back(int(c));
+          }
+      std::sort(cand.begin(), cand.end());
+      wc.insert(wc.end(), cand.begin(), cand.end());
+      wc_off[i + 1] = int(wc.size());
+    }
+  }
   bool in_il(int i, int j) const {
+    if (!il_mask.empty()) {
+      const int sl = slot(i, j);
+      return sl >= 0 && ((il_mask[i] >> sl) & 1);
+    }
     for (int t = il_off[i]; t < il_off[i + 1]; t++)
       if (il[t] == j) return true;
     return false;

@@ -207,26 +207,10 @@ class Factorizer {
   // through M2P = P2L^T) of i, sorted (ifmm/solver.py:220-229); scans the 7x7 window
   void partners(WorkLevel& W, int i, std::vector<int>& xp, std::vector<int>& yp) {
     const Topo& T = *W.T;
-    const int dim = T.dim, k = W.k;
-    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (int d = 0; d < dim; d++) {
-      lo[d] = std::max(0, T.grid[i * dim + d] - 3);
-      hi[d] = std::min((1 << k) - 1, T.grid[i * dim + d] + 3);
-    }
-    std::vector<int> cand;
-    int g[3];
-    for (g[0] = lo[0]; g[0] <= hi[0]; g[0]++)
-      for (g[1] = lo[1]; g[1] <= hi[1]; g[1]++)
-        for (g[2] = lo[2]; g[2] <= hi[2]; g[2]++) {
-          int64_t c = 0;
-          for (int b = 0; b < k; b++)
-            for (int ax = 0; ax < dim; ax++) c |= int64_t((g[ax] >> b) & 1) << (b * dim + ax);
-          cand.push_back(int(c));
-        }
-    std::sort(cand.begin(), cand.end());
     xp.clear();
     yp.clear();
-    for (int j : cand) {
+    for (int t = T.wc_off[i]; t < T.wc_off[i + 1]; t++) {
+      const int j = T.wc[t];
       if (j == i) continue;
       if (!W.dead[j] && pp_present(W, i, j)) xp.push_back(j);
       if (pres(W.px, W, i, j)) yp.push_back(j);
@@ -679,20 +663,27 @@ void Factorizer::finish_level(int rec_begin) {
   const int64_t yb = xb + xoff[W.nc];
   F_->lvl_base[k - 1] = yb;
   F_->vec_size = yb + yoff[W.nc];
-  std::vector<int> posall;
+  // partner positions: each record's pos array is the concatenation of its
+  // slots' ranges [base, base + dim); ship one (base, dim, out) triple per slot
+  // and expand on the device into one block for the level
+  std::vector<PosRun> runs;
   std::vector<int64_t> posoff;
+  int64_t total = 0;
   for (size_t rr = rec_begin; rr < F_->recs.size(); rr++) {
     RecordH& R = F_->recs[rr];
     R.xoff = xb + xoff[R.index];
-    posoff.push_back(int64_t(posall.size()));
+    posoff.push_back(total);
     for (const SlotRef& sr : rec_slots_[rr]) {
-      int64_t base = sr.kind == 0 ? xb + xoff[sr.j] : yb + yoff[sr.j];
-      for (int u = 0; u < sr.dim; u++) posall.push_back(int(base + u));
+      if (sr.dim <= 0) continue;
+      const int64_t base = sr.kind == 0 ? xb + xoff[sr.j] : yb + yoff[sr.j];
+      runs.push_back(PosRun{base, total, sr.dim, 0});
+      total += sr.dim;
     }
   }
-  if (!posall.empty()) {
-    // the level's position arrays live in one block: one copy
-    int* d = upload(F_->arena, posall, s_, st_);
+  if (total > 0) {
+    int* d = F_->arena.alloc_n<int>(size_t(total));
+    const PosRun* druns = upload(ws_, runs, s_, st_);
+    launch_pos_expand(druns, int(runs.size()), d, s_);
     for (size_t rr = rec_begin, u = 0; rr < F_->recs.size(); rr++, u++) F_->recs[rr].pos = d + posoff[u];
   }
   CK(cudaStreamSynchronize(s_));

@@ -177,6 +177,7 @@ static void build_lists(TreeH* t) {
       }
       T.il_off.push_back(int(T.il.size()));
     }
+    T.prepare();  // window lists + interaction-list masks for the factorization
   }
 }
 
