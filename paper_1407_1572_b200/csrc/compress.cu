@@ -5,7 +5,8 @@
 
 namespace ifmm {
 __device__ int g_prof_on = 0;
-__device__ int g_jac_rt = 1;   // IFMM_JACOBI_RT=0: Jacobi on R (columns) in new_dirs
+__device__ int g_jac_rt = 1;
+__device__ int g_gram = 1;    // IFMM_GRAM=0: Householder QRs in the K1 recompression   // IFMM_JACOBI_RT=0: Jacobi on R (columns) in new_dirs
 __device__ int g_jac_reg = 0;  // IFMM_JACOBI_REG=1: register-resident Jacobi for <= 16 columns (measured slower)
 __device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
 }  // namespace ifmm
@@ -47,6 +48,116 @@ template <> struct Worker<WarpGroup> {
   __device__ static int count() { return gridDim.x * (blockDim.x >> 5); }
   __device__ static WarpGroup make(CtaShared&) { return WarpGroup{}; }
 };
+
+// ------------------------------------------------------------------ Gram recompression
+// Column-scaled Cholesky of a k x k Gram matrix G (ld ldg, k <= 96) by ONE
+// warp, in place: with d = sqrt(diag(G)) (precomputed by the caller),
+// Ghat = G / (d_i d_j) = Lhat Lhat^T; on exit the lower triangle holds Lhat
+// (upper triangle zeroed).  Returns false when Ghat is numerically singular
+// (pivot^2 <= 1e-12, i.e. cond of the scaled factor > 1e6); the caller then
+// falls back to Householder QR.  The result is identical on every lane.
+__device__ bool warp_chol_scaled(double* Gm, int k, int ldg, const double* d) {
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < k; i++)
+    if (!(d[i] > 0.0)) return false;
+  for (int e = lane; e < k * k; e += 32) {
+    const int i = e % k, j = e / k;
+    Gm[i + (size_t)j * ldg] /= d[i] * d[j];
+  }
+  __syncwarp();
+  for (int j = 0; j < k; j++) {
+    double t[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      const int i = lane + 32 * q;
+      double v = 0.0;
+      if (i < k && i >= j) {
+        v = Gm[i + (size_t)j * ldg];
+        for (int p = 0; p < j; p++) v -= Gm[i + (size_t)p * ldg] * Gm[j + (size_t)p * ldg];
+      }
+      t[q] = v;
+    }
+    const int qj = j >> 5;
+    const double mine = qj == 0 ? t[0] : (qj == 1 ? t[1] : t[2]);
+    const double dj = __shfl_sync(0xffffffffu, mine, j & 31);
+    if (!(dj > 1e-12)) return false;  // uniform across the warp
+    const double piv = sqrt(dj);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      const int i = lane + 32 * q;
+      if (i < k && i >= j) Gm[i + (size_t)j * ldg] = (i == j) ? piv : t[q] / piv;
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < k * k; e += 32) {
+    const int i = e % k, j = e / k;
+    if (i < j) Gm[i + (size_t)j * ldg] = 0.0;
+  }
+  __syncwarp();
+  return true;
+}
+
+// Recompression of the ACA crosses F ~= Uc Vc^T through their Gram matrices:
+// Gu = Lu Lu^T, Gv = Lv Lv^T (column-scaled Cholesky), core = Lu^T Lv,
+// core V = X (one-sided Jacobi), left = Uc Lu^-T X(:, ord), right =
+// Vc Lv^-T V(:, ord) -- the same factors as QR(Uc), QR(Vc), SVD(R_u R_v^T)
+// (ifmm/lowrank.py:137-171) without the two Householder QRs.  Returns the
+// truncated rank, or -1 when a Gram matrix is too ill-conditioned.
+template <class G>
+__device__ int gram_recompress(const G& g, const double* Uc, const double* Vc, int rows, int cols, int k,
+                               double* Gu, double* Gv, int ldg, double* core, double* Jv, double* sig, int* ord,
+                               double tol, double* Zl, double* Zr, double* left, double* right, double* sv,
+                               double* du, double* dv) {
+  const int warp = g.warp(), nw = g.nwarps();
+  // diagonal scales (kept: the Cholesky overwrites the Gram in place)
+  for (int i = g.rank(); i < k; i += g.size()) {
+    du[i] = sqrt(fmax(Gu[i + (size_t)i * ldg], 0.0));
+    dv[i] = sqrt(fmax(Gv[i + (size_t)i * ldg], 0.0));
+  }
+  g.sync();
+  bool ok = true;
+  if (k > 96) return -1;
+  if (nw >= 2) {
+    if (warp == 0) ok = warp_chol_scaled(Gu, k, ldg, du);
+    else if (warp == 1) ok = warp_chol_scaled(Gv, k, ldg, dv);
+  } else {
+    ok = warp_chol_scaled(Gu, k, ldg, du) && warp_chol_scaled(Gv, k, ldg, dv);
+  }
+  if (g.any(!ok)) return -1;
+  // unscale: L = D^-1 Lhat (row i times the original sqrt(G_ii))
+  for (int e = g.rank(); e < k * k; e += g.size()) {
+    const int i = e % k, j = e / k;
+    Gu[i + (size_t)j * ldg] *= du[i];
+    Gv[i + (size_t)j * ldg] *= dv[i];
+  }
+  g.sync();
+  // core = Lu^T Lv (k x k)
+  g_gemm(g, k, k, k, 1.0, Gu, ldg, true, Gv, ldg, false, 0.0, core, k);
+  g_jacobi(g, core, k, k, k, Jv, k, sig, ord);
+  const int r = trunc_rank_dev(sig, ord, k, tol);
+  // Zl = Lu^-T X(:, ord[:r]),  Zr = Lv^-T V(:, ord[:r]): one thread per column
+  for (int c = g.rank(); c < 2 * r; c += g.size()) {
+    const bool isl = c < r;
+    const int cc = isl ? c : c - r;
+    const double* L = isl ? Gu : Gv;
+    const double* B = (isl ? core : Jv) + (size_t)ord[cc] * k;
+    double* Z = (isl ? Zl : Zr) + (size_t)cc * k;
+    for (int i = k - 1; i >= 0; i--) {  // L^T Z = B, back substitution
+      double v = B[i];
+      for (int p = i + 1; p < k; p++) v -= L[p + (size_t)i * ldg] * Z[p];
+      Z[i] = v / L[i + (size_t)i * ldg];
+    }
+  }
+  g.sync();
+  if (r > 0) {
+    g_gemm(g, rows, r, k, 1.0, Uc, rows, false, Zl, k, false, 0.0, left, rows);
+    g_gemm(g, cols, r, k, 1.0, Vc, cols, false, Zr, k, false, 0.0, right, cols);
+  }
+  for (int c = g.rank(); c < r; c += g.size()) sv[c] = sig[ord[c]];
+  g.sync();
+  return r;
+}
 
 // ------------------------------------------------------------------ K1
 // ACA of the redirected fill, QR of both cross factors, Jacobi SVD of the
@@ -103,7 +214,7 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
     const int kmax = min(D.Kf, KK);
     PROF_T0();
     AcaOut ao = g_aca(g, D.F, D.ldF, D.transF, rows, cols, tol, probes + (size_t)mrow * 10, min(10, rows), Uc, Vc,
-                      kmax, rr, cc, usedr, usedc, dots);
+                      kmax, rr, cc, usedr, usedc, dots, g_gram ? Rl : nullptr, g_gram ? Rr : nullptr, KK);
     PROF_ACC(0);
     const int k = ao.k;
     S.k = k;
@@ -123,7 +234,15 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
     double* left = D.out;
     double* right = D.out + (size_t)rows * D.Kf;
     double* sv = right + (size_t)cols * D.Kf;
-    if (k > 0) {
+    int rg = -1;
+    if (k > 0 && g_gram) {
+      rg = gram_recompress(g, Uc, Vc, rows, cols, k, Rl, Rr, KK, core, Jv, sig, ord, tol, Ql, Qr, left, right, sv,
+                           rr, cc);
+      PROF_ACC(1);
+    }
+    if (rg >= 0) {
+      r = rg;
+    } else if (k > 0) {
       g_qr(g, Uc, rows, k, rows, Rl, Ql, rows, vv);
       g_qr(g, Vc, cols, k, cols, Rr, Qr, cols, vv);
       PROF_ACC(1);
@@ -429,6 +548,8 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   static bool jac_set = false;
   if (!jac_set) {
     CK(cudaMemcpyToSymbolAsync(g_jac_rt, &jac_rt, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    static const int gram = getenv("IFMM_GRAM") ? atoi(getenv("IFMM_GRAM")) : 1;
+    CK(cudaMemcpyToSymbolAsync(g_gram, &gram, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyToSymbolAsync(g_jac_reg, &jac_reg, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     jac_set = true;
   }

@@ -522,7 +522,10 @@ __device__ inline double Fat(const double* F, int ld, int trans, int a, int b) {
 template <class G>
 __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, int m, int n, double tol,
                                  const int* probes, int nprobe, double* Uc, double* Vc, int kmax, double* rr,
-                                 double* cc, int* usedr, int* usedc, double* dots) {
+                                 double* cc, int* usedr, int* usedc, double* dots, double* Gu = nullptr,
+                                 double* Gv = nullptr, int ldg = 0) {
+  // Gu/Gv (optional, ld ldg): Gram matrices U_c^T U_c and V_c^T V_c of the
+  // crosses, filled from the products the Frobenius estimate computes anyway
   const int lane = g.lane(), warp = g.warp(), nw = g.nwarps();
   const int full = min(m, n);
   AcaOut out{0, 0};
@@ -622,9 +625,19 @@ __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, i
       for (int c = lane; c < n; c += 32) dv += v[c] * vt[c];
       du = warp_sum(du);
       dv = warp_sum(dv);
-      if (lane == 0) dots[t] = fabs(du) * fabs(dv);
+      if (lane == 0) {
+        dots[t] = fabs(du) * fabs(dv);
+        if (Gu) {
+          Gu[t + (size_t)k * ldg] = Gu[k + (size_t)t * ldg] = du;
+          Gv[t + (size_t)k * ldg] = Gv[k + (size_t)t * ldg] = dv;
+        }
+      }
     }
     g.combine(su, sv, nx);  // also publishes dots[]
+    if (Gu && g.rank() == 0) {
+      Gu[k + (size_t)k * ldg] = su;
+      Gv[k + (size_t)k * ldg] = sv;
+    }
     const double csq = su * sv;
     if (k > 0) {
       double cross = 0.0;
