@@ -263,6 +263,11 @@ def main():
     torch.cuda.synchronize()
     refine_s = time.perf_counter() - t1
     refine_hist = list(fact.last_refinement)
+    r_m, top_dim = fact.r_m, fact.top_dim
+    # free the last factorization first so later ones reuse its device slabs
+    # (as every timed step does); the e2e timing would otherwise include fresh
+    # multi-GB allocations
+    del fact
 
     # e2e through the public API with host buffers
     e2e_times = []
@@ -316,7 +321,7 @@ def main():
         "refined_solve": {"target": 10 * tol, "steps": len(refine_hist) - 1, "residual_history": refine_hist,
                           "seconds": refine_s,
                           "note": "extension: x += solve(b - A~x) with the store's FMM operator; not in value"},
-        "r_m": fact.r_m, "top_dim": fact.top_dim, "t_assembly_s": t_a,
+        "r_m": r_m, "top_dim": top_dim, "t_assembly_s": t_a,
         "flops": {"exec": work["flops_exec"], "schur": work["flops_schur"], "reference_equiv": work["flops_ref"],
                   "fp64_tflops_step": work["flops_exec"] / t_step / 1e12},
         "phase_ms": {k: round(v[0], 3) for k, v in ph.items()},
