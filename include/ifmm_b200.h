@@ -145,6 +145,11 @@ int ifmm_test_qr(const double* a, int m, int k, double* q, double* r);
 /* ACA + recompression of F (m x n): returns rank, left (m x rank), right (n x rank) */
 int ifmm_test_aca(const double* f, int m, int n, double tol, const int32_t* probes, int kmax, double* left,
                   double* right, int32_t* rank, int32_t* incompressible);
+/* fill compression K1 on one m x n fill (ACA + recompression, ifmm/lowrank.py:137-263):
+ * gram = 1 via the cross Gram matrices (Householder fallback), 0 via Householder QRs;
+ * F ~= left (m x rank) right^T (n x rank), sv = kept singular values, status 1 = kept dense */
+int ifmm_test_recompress(const double* f, int m, int n, double tol, const int32_t* probes, int gram, double* left,
+                         double* right, double* sv, int32_t* rank, int32_t* status);
 
 #ifdef __cplusplus
 }

@@ -70,6 +70,7 @@ SIGNATURES = {
     "ifmm_bench_gj_inverse": (_i32, [_p, _p, _i32, _i32, _p]),
     "ifmm_test_gemm": (_i32, [_i32, _i32, _i32, _i32, _i32, _d, _p, _i32, _p, _i32, _d, _p, _i32, _i32]),
     "ifmm_test_set_group": (_i32, [_i32]),
+    "ifmm_test_recompress": (_i32, [_p, _i32, _i32, _d, _p, _i32, _p, _p, _p, _p, _p]),
     "ifmm_test_jacobi": (_i32, [_p, _i32, _i32, _p, _p]),
     "ifmm_test_qr": (_i32, [_p, _i32, _i32, _p, _p]),
     "ifmm_test_aca": (_i32, [_p, _i32, _i32, _d, _p, _i32, _p, _p, _p, _p]),

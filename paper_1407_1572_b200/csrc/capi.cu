@@ -5,6 +5,7 @@
 
 #include "../../include/ifmm_b200.h"
 #include "core.cuh"
+#include "compress.cuh"
 #include "cta_la.cuh"
 
 using ifmm::AcaOut;
@@ -493,6 +494,35 @@ int ifmm_test_aca(const double* f, int m, int n, double tol, const int32_t* prob
     *incompressible = (!o[1] && (o[0] >= std::min(m, n) || o[0] >= kmax) && tol > 0) ? 1 : 0;
     CK(cudaMemcpy(left, du, sizeof(double) * m * o[0], cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(right, dv, sizeof(double) * n * o[0], cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_test_recompress(const double* f, int m, int n, double tol, const int32_t* probes, int gram, double* left,
+                         double* right, double* sv, int32_t* rank, int32_t* status) {
+  return guard([&] {
+    ensure_device();
+    if (m < 1 || n < 1) invalid("fill must be non-empty");
+    cudaStream_t s = default_stream();
+    Arena ws(size_t(16) << 20);
+    Staging st;
+    const int kf = std::max(1, std::min(96, std::min(m, n)));
+    double* df = ws.alloc_n<double>(size_t(m) * n);
+    double* dout = ws.alloc_n<double>(size_t(m + n + 1) * kf);
+    int* dp = ws.alloc_n<int>(size_t(m + 1) * 10);  // probe table: row m only
+    auto* dstate = ws.alloc_n<ifmm::FillState>(1);
+    std::vector<int> tab(size_t(m + 1) * 10, 0);
+    for (int t = 0; t < std::min(10, m); t++) tab[size_t(m) * 10 + t] = probes[t];
+    CK(cudaMemcpy(df, f, sizeof(double) * m * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dp, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
+    ifmm::test_recompress_one(df, m, n, tol, dp, m, gram, dout, dstate, ws, st, s);
+    CK(cudaStreamSynchronize(s));
+    ifmm::FillState S;
+    CK(cudaMemcpy(&S, dstate, sizeof S, cudaMemcpyDeviceToHost));
+    *rank = S.r;
+    *status = S.status;
+    CK(cudaMemcpy(left, dout, sizeof(double) * size_t(m) * S.r, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(right, dout + size_t(m) * kf, sizeof(double) * size_t(n) * S.r, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sv, dout + size_t(m + n) * kf, sizeof(double) * S.r, cudaMemcpyDeviceToHost));
   });
 }
 

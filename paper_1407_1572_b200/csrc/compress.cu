@@ -510,6 +510,36 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) delta_kernel(co
   }
 }
 
+// ------------------------------------------------------------------ test hook
+// K1 on one fill F (m x n, column-major, device): gram = 1 through the Gram
+// matrices (with the Householder fallback), 0 through the Householder QRs.
+void test_recompress_one(const double* dF, int m, int n, double tol, const int* d_probes, int probe_maxm, int gram,
+                         double* d_out, FillState* d_state, Arena& ws, Staging& st, cudaStream_t s) {
+  const int g0 = gram;
+  CK(cudaMemcpyToSymbolAsync(g_gram, &g0, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+  FillDesc D{};
+  D.kind = FILL_P2P;
+  D.F = const_cast<double*>(dF);
+  D.ldF = m;
+  D.transF = 0;
+  D.rows = m;
+  D.cols = n;
+  D.n_p = m;
+  D.n_q = n;
+  D.Kf = std::max(1, std::min(96, std::min(m, n)));
+  D.out = d_out;
+  std::vector<FillDesc> v(1, D);
+  const FillDesc* dfd = upload(ws, v, s, st);
+  const int KK = D.Kf;
+  const size_t slot = 2 * size_t(m) * KK + 2 * size_t(n) * KK + 4 * size_t(KK) * KK + 2 * size_t(m + n) +
+                      4 * size_t(KK) + 64;
+  double* scr = ws.alloc_n<double>(slot);
+  aca_recompress_kernel<CtaGroup><<<1, 128, 0, s>>>(dfd, 1, d_state, tol, d_probes, probe_maxm, scr, slot, m, n, KK, 0);
+  CK_LAUNCH();
+  const int one = 1;  // restore the default
+  CK(cudaMemcpyToSymbolAsync(g_gram, &one, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+}
+
 // ------------------------------------------------------------------ host
 static int resident_grid(int work, int per_sm) { return std::max(1, std::min(work, 148 * per_sm)); }
 

@@ -51,4 +51,9 @@ struct CompressBatch {
 void run_compression(CompressBatch& cb, double tol, const int* d_probes, int probe_maxm, int* d_rank,
                      FillState* d_state, int* d_stats, Arena& ws, Staging& st, cudaStream_t s, int debug);
 
+// test hook: K1 (ACA + recompression) on one m x n fill; d_out holds
+// left (m x Kf) | right (n x Kf) | sv (Kf), Kf = min(96, m, n)
+void test_recompress_one(const double* dF, int m, int n, double tol, const int* d_probes, int probe_maxm, int gram,
+                         double* d_out, FillState* d_state, Arena& ws, Staging& st, cudaStream_t s);
+
 }  // namespace ifmm

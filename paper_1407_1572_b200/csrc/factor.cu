@@ -190,6 +190,9 @@ class Factorizer {
     W.win = W.T->win();
     W.arena = &lvl_arena_[k & 1];
     W.arena->set_zero_stream(s_);
+    static const bool hp = getenv("IFMM_HOST_PROF") != nullptr;
+    if (hp) fprintf(stderr, "level %d arena: zeroing %.2f GB (reserved %.2f GB)\n", k, W.arena->in_use() / 1e9,
+                    W.arena->reserved() / 1e9);
     W.arena->reset();
     W.p2p.assign(size_t(W.nc) * W.win, nullptr);
     W.m2l.assign(size_t(W.nc) * W.win, nullptr);

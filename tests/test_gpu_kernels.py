@@ -130,3 +130,42 @@ def test_aca_matches_oracle_crosses(L, group, m, n, rank):
     Lo, Ro, bad = O.aca_block(F, 1e-8)
     assert not bad and not inc[0]
     assert abs(k - Lo.shape[1]) <= 2
+
+
+@pytest.mark.parametrize("m,n,rank,decay", [(64, 64, 8, 1e-3), (90, 40, 12, 1e-5), (200, 150, 20, 1e-2),
+                                            (16, 120, 5, 1e-7), (64, 64, 30, 1e-1)])
+def test_fill_recompression_gram_vs_householder(L, m, n, rank, decay):
+    """K1 (ACA + recompression) on one fill: the Gram/Cholesky path and the
+    Householder path truncate to the same rank and approximate F to the
+    tolerance; the kept singular values match numpy's SVD of F."""
+    from oracle import ifmm_oracle as O
+    rng = np.random.default_rng(m * n + rank)
+    s = np.logspace(0, np.log10(decay), rank)
+    F = (rng.standard_normal((m, rank)) * s) @ rng.standard_normal((rank, n))
+    _, probes = O.aca_probe_rows(m)
+    tol = 1e-6
+    out = {}
+    for gram in (1, 0):
+        kf = min(96, m, n)
+        left = np.zeros((m, kf), order="F")
+        right = np.zeros((n, kf), order="F")
+        sv = np.zeros(kf)
+        rk = np.zeros(1, dtype=np.int32)
+        st = np.zeros(1, dtype=np.int32)
+        L.check(L.lib.ifmm_test_recompress(L.ptr(np.asfortranarray(F)), m, n, tol,
+                                           L.ptr(probes.astype(np.int32)), gram, L.ptr(left), L.ptr(right),
+                                           L.ptr(sv), L.ptr(rk), L.ptr(st)))
+        r = int(rk[0])
+        assert st[0] == 0
+        approx = left[:, :r] @ right[:, :r].T
+        assert np.linalg.norm(approx - F) <= 10 * tol * np.linalg.norm(F)
+        # right factor orthonormal, left = U * sigma
+        assert np.allclose(right[:, :r].T @ right[:, :r], np.eye(r), atol=1e-10)
+        out[gram] = (r, sv[:r].copy())
+    (rg, sg), (rh, sh) = out[1], out[0]
+    assert rg == rh
+    s_ref = np.linalg.svd(F, compute_uv=False)[:rg]
+    # the ACA stops at the tolerance: singular values within ~tol * sigma_1
+    assert np.allclose(sg, s_ref, rtol=1e-6, atol=10 * tol * s_ref[0])
+    # both paths recompress the same crosses
+    assert np.allclose(sg, sh, rtol=1e-9, atol=1e-10 * s_ref[0])
