@@ -56,7 +56,7 @@ template <> struct Worker<WarpGroup> {
 // (upper triangle zeroed).  Returns false when Ghat is numerically singular
 // (pivot^2 <= 1e-12, i.e. cond of the scaled factor > 1e6); the caller then
 // falls back to Householder QR.  The result is identical on every lane.
-__device__ bool warp_chol_scaled(double* Gm, int k, int ldg, const double* d) {
+__device__ bool warp_chol_scaled(double* Gm, int k, int ldg, const double* d, double min_piv2 = 1e-12) {
   const int lane = threadIdx.x & 31;
   for (int i = 0; i < k; i++)
     if (!(d[i] > 0.0)) return false;
@@ -80,7 +80,7 @@ __device__ bool warp_chol_scaled(double* Gm, int k, int ldg, const double* d) {
     const int qj = j >> 5;
     const double mine = qj == 0 ? t[0] : (qj == 1 ? t[1] : t[2]);
     const double dj = __shfl_sync(0xffffffffu, mine, j & 31);
-    if (!(dj > 1e-12)) return false;  // uniform across the warp
+    if (!(dj > min_piv2)) return false;  // uniform across the warp
     const double piv = sqrt(dj);
     __syncwarp();
 #pragma unroll
@@ -312,10 +312,52 @@ __device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig
     }
     if (sqrt(f2) <= cutoff) return 0;
   }
-  g_qr(g, H, nU, r, nU, R, Q, nU, vv);  // H = Q R
-  PROF_ACC(5);
   double* W = U + (size_t)rU * nU;
   int w = 0;
+  if (g_gram && r <= 96 && nU >= 128) {  // measured: slower than Householder for the small leaf bases
+    // Gram route: G = H^T H = L L^T (column-scaled Cholesky), H = Q L^T with
+    // Q = H L^-T never formed.  Jacobi on L (= R^T) gives V (left singular
+    // vectors of R) and sigma; W = Q V(:, kept) = H (L^-T V(:, kept)).
+    // Only for a well-conditioned scaled factor (pivot^2 >= 1e-8): the kept
+    // directions are then orthonormal to ~1e-8 before the final projection.
+    g_gemm(g, r, r, nU, 1.0, H, nU, true, H, nU, false, 0.0, R, r);  // G -> R (r x r, ld r)
+    for (int i = g.rank(); i < r; i += g.size()) vv[i] = sqrt(fmax(R[i + (size_t)i * r], 0.0));
+    g.sync();
+    bool ok = true;
+    if (g.warp() == 0) ok = warp_chol_scaled(R, r, r, vv, 1e-8);
+    if (!g.any(!ok)) {
+      for (int e = g.rank(); e < r * r; e += g.size()) {  // unscale: L = D^-1 Lhat ; E = L (Jacobi input)
+        const int i = e % r;
+        R[e] *= vv[i];
+        E[e] = R[e];
+      }
+      g.sync();
+      PROF_ACC(5);
+      g_jacobi(g, E, r, r, r, Q, r, sig, ord);  // V -> Q (r x r)
+      PROF_ACC(6);
+      for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
+      w = min(w, cap);
+      // Z = L^-T V(:, ord[:w]) into E (r x w), one thread per column
+      for (int c = g.rank(); c < w; c += g.size()) {
+        const double* B = Q + (size_t)ord[c] * r;
+        double* Z = E + (size_t)c * r;
+        for (int i = r - 1; i >= 0; i--) {
+          double v = B[i];
+          for (int p = i + 1; p < r; p++) v -= R[p + (size_t)i * r] * Z[p];
+          Z[i] = v / R[i + (size_t)i * r];
+        }
+      }
+      g.sync();
+      if (w > 0) g_gemm(g, nU, w, r, 1.0, H, nU, false, E, r, false, 0.0, W, nU);
+      if (g_prof_on && g.rank() == 0 && w == 0) atomicAdd(&g_cyc[12], 1ull);
+      g.sync();
+      if (w > 0) g_project_out(g, W, nU, nU, w, U, nU, rU, E);
+      PROF_ACC(7);
+      return w;
+    }
+  }
+  g_qr(g, H, nU, r, nU, R, Q, nU, vv);  // H = Q R
+  PROF_ACC(5);
   if (g_jac_rt) {
     // one-sided Jacobi on R^T with the rotations accumulated: R^T V = X, so V
     // holds the left singular vectors of R and ||X(:,j)|| its singular values.
