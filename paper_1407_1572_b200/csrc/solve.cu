@@ -43,6 +43,7 @@ __device__ inline void cta_gemv_cols(const double* __restrict__ A, int n, int w,
 #pragma unroll
       for (int q = 0; q < RC; q++) xl[q] = (cb + lane < w && q < nq) ? xat(cb + lane, q) : 0.0;
       const int cmax = min(32, w - cb);
+#pragma unroll 8
       for (int u = 0; u < cmax; u++) {
         const double* col = A + (size_t)(cb + u) * lda;
         double xv[RC];
@@ -91,7 +92,7 @@ __device__ __forceinline__ void chunk_range(int len, int y, int ny, int gran, in
 }
 
 template <int RC>
-__global__ void __launch_bounds__(SB) solve_fwd_kernel(const RecordH* __restrict__ recs, int rec0,
+__global__ void __launch_bounds__(SB, RC == 1 ? 4 : 2) solve_fwd_kernel(const RecordH* __restrict__ recs, int rec0,
                                                        const int64_t* __restrict__ g_off, double* V, double* G,
                                                        int nrhs, int red_rows) {
   extern __shared__ double sm[];
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(SB) solve_fwd_kernel(const RecordH* __restrict
 #pragma unroll
       for (int q = 0; q < RC; q++) s[q] = 0.0;
       if (ok)
+#pragma unroll 8
         for (int t = sl; t < n; t += W) {
           const double a = x[t];
 #pragma unroll
@@ -149,8 +151,51 @@ __global__ void __launch_bounds__(SB) solve_fwd_kernel(const RecordH* __restrict
   }
 }
 
+// Single right-hand side forward sweep.  S (hence S^-1 and its block
+// S^-1_nn) is symmetric, so g = S^-1_nn b is a set of column dots as well:
+// the record [S^-1_nn | X_top] is one n x (n + w) column block and every
+// output is the dot of one column with b -- W-lane segments per column, no
+// cross-warp reduction, one barrier.  Chunk y of gridDim.y owns a range of
+// the n + w columns.
+__global__ void __launch_bounds__(SB, 4) solve_fwd1_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                           const int64_t* __restrict__ g_off, double* V, double* G) {
+  extern __shared__ double sm[];
+  double* bsh = sm;  // n
+  const RecordH R = recs[blockIdx.x];
+  const int n = R.n, w = R.w, nc = n + w;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c0, c1;
+  chunk_range(nc, blockIdx.y, gridDim.y, 8, c0, c1);
+  if (c1 <= c0) return;
+  double* g = G + g_off[rec0 + blockIdx.x];
+  for (int e = threadIdx.x; e < n; e += SB) bsh[e] = V[R.xoff + e];
+  __syncthreads();
+  const int W = n > 128 ? 32 : (n > 64 ? 16 : 8);
+  const int seg = lane / W, sl = lane & (W - 1), spw = 32 / W;
+  for (int cb = c0 + warp * spw; cb < c1; cb += SWARPS * spw) {
+    const int c = cb + seg;
+    const bool ok = c < c1;
+    const double* x = ok ? (c < n ? R.sinv + (size_t)c * n : R.xtop + (size_t)(c - n) * n) : R.sinv;
+    double s0 = 0.0, s1 = 0.0;
+    if (ok) {
+      int t = sl;
+      for (; t + W < n; t += 2 * W) {  // two independent loads in flight per step
+        s0 = fma(x[t], bsh[t], s0);
+        s1 = fma(x[t + W], bsh[t + W], s1);
+      }
+      if (t < n) s0 = fma(x[t], bsh[t], s0);
+    }
+    double sv = s0 + s1;
+    for (int o = W >> 1; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+    if (ok && sl == 0) {
+      if (c < n) g[c] = sv;
+      else V[(int64_t)R.pos[c - n]] -= sv;
+    }
+  }
+}
+
 template <int RC>
-__global__ void __launch_bounds__(SB) solve_bwd_kernel(const RecordH* __restrict__ recs, int rec0,
+__global__ void __launch_bounds__(SB, RC == 1 ? 4 : 2) solve_bwd_kernel(const RecordH* __restrict__ recs, int rec0,
                                                        const int64_t* __restrict__ g_off, double* V,
                                                        const double* G, int nrhs, int red_rows) {
   extern __shared__ double sm[];
@@ -283,7 +328,10 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     const size_t smem = sizeof(double) * (size_t(rr) * SWARPS * RC + size_t(b.maxn) * RC);
     if (smem > 200 * 1024) invalid("solve: pivot block too large for the solve kernel");
     const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));
-    if (RC == 1) solve_fwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
+    static const bool fwd_old = getenv("IFMM_SOLVE_FWD_GEMV") != nullptr;  // debug: S^-1 b as a GEMV
+    if (RC == 1 && !fwd_old)
+      solve_fwd1_kernel<<<grid, SB, sizeof(double) * size_t(b.maxn), s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+    else if (RC == 1) solve_fwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     else solve_fwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
   }
