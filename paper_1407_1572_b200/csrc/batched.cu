@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(const MatDesc* __restrict
 // elimination (no barrier: every thread reads only its own rows next).
 // Ties are broken by row index; thread 0 keeps the position bookkeeping.
 template <int B, int R>
-__global__ void __launch_bounds__(R == 1 ? 512 : (R == 2 ? 384 : 256)) gj_panel_reg_kernel(
+__global__ void __launch_bounds__(R == 1 ? (B <= 16 ? 1024 : 512) : (R == 2 ? 384 : 256)) gj_panel_reg_kernel(
     const MatDesc* __restrict__ desc, int j, int* info, RowMove* moves, int* nmoves) {
   extern __shared__ int smi[];
   __shared__ double candv[32];
@@ -957,6 +957,13 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
     b = 32;
     threads = ((maxm + 1) / 2 + 31) / 32 * 32;
     smem = size_t(maxm) * 8;
+  } else if (maxm <= 1024 && !getenv("IFMM_GJ_SMEM_PANEL")) {
+    // one row per thread in registers, 16-wide panels (the shared-memory
+    // panel rewrites m x b entries per pivot step)
+    variant = 4;
+    b = 16;
+    threads = (maxm + 31) / 32 * 32;
+    smem = size_t(maxm) * 8;
   } else {
     variant = 2;
     auto smem_for = [&](int bw) { return size_t(maxm) * (bw + 1) * 8 + size_t(maxm) * 8; };
@@ -986,6 +993,7 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   const int gy = std::max(1, std::min(16, (maxm + 63) / 64));
   auto panel = [&](int j, cudaStream_t ps) {
     if (variant == 0) gj_panel_reg_kernel<32, 1><<<n, threads, smem, ps>>>(d_desc, j, d_info, moves, nmoves);
+    else if (variant == 4) gj_panel_reg_kernel<16, 1><<<n, threads, smem, ps>>>(d_desc, j, d_info, moves, nmoves);
     else if (variant == 1) gj_panel_reg_kernel<32, 2><<<n, threads, smem, ps>>>(d_desc, j, d_info, moves, nmoves);
     else gj_panel_kernel<<<n, threads, smem, ps>>>(d_desc, j, b, d_info, moves, nmoves);
     CK_LAUNCH();

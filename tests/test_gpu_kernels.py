@@ -72,6 +72,20 @@ def test_gj_inverse_batched_variable_sizes(L):
         assert np.linalg.norm(inv - ref) <= 1e-10 * np.linalg.norm(ref) * max(1.0, np.linalg.cond(m) / 1e4)
 
 
+@pytest.mark.parametrize("m", [900, 1024, 1100])
+def test_gj_inverse_large_single(L, m):
+    """Single large pivots (top levels): 16-wide register panel up to m = 1024,
+    shared-memory panel beyond."""
+    rng = np.random.default_rng(m)
+    A = rng.standard_normal((m, m)) + m ** 0.5 * np.eye(m)
+    packed = np.asfortranarray(A).ravel(order="F").copy()
+    info = np.zeros(1, dtype=np.int32)
+    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(np.array([m], dtype=np.int32)), 1, L.ptr(info)))
+    assert info[0] == 0
+    inv = packed.reshape((m, m), order="F")
+    assert np.linalg.norm(inv @ A - np.eye(m)) <= 1e-11 * m
+
+
 def test_gj_flags_singular(L):
     A = np.zeros((4, 4))
     A[0, 0] = A[1, 1] = 1.0
