@@ -690,6 +690,56 @@ __global__ void __launch_bounds__(256) gj_move_copy_kernel(const MatDesc* __rest
   }
 }
 
+// Two-level variant of the row moves + W copy: columns [c_lo, c_hi) of every
+// matrix (c relative to j0: c_lo = j0 + lo_off ... ), minus [x_lo, x_hi),
+// get the row moves of list 1 then (if nl == 2) list 2 applied; W (wb x m,
+// ld wb) receives rows [j0 + w_off, j0 + w_off + wb) of those columns.
+// Offsets are relative to the outer panel start j0; widths are clipped per
+// matrix (wb = min(wwant, m - j0 - w_off)).
+__global__ void __launch_bounds__(256) gj_move_copy2_kernel(const MatDesc* __restrict__ desc, int j0, int c_lo_off,
+                                                            int c_hi_off, int x_lo_off, int x_hi_off, int b,
+                                                            const RowMove* __restrict__ mv1,
+                                                            const int* __restrict__ nm1,
+                                                            const RowMove* __restrict__ mv2,
+                                                            const int* __restrict__ nm2, int w_off, int wwant,
+                                                            double* const* W, int g1_off, int g2_off) {
+  const MatDesc D = desc[blockIdx.x];
+  if (D.m <= j0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // column range; negative offsets mean "from 0" / positive >= m mean "to m"
+  const int c_lo = c_lo_off < 0 ? 0 : min(D.m, j0 + c_lo_off);
+  const int c_hi = c_hi_off < 0 ? D.m : min(D.m, j0 + c_hi_off);
+  const int x_lo = min(D.m, j0 + x_lo_off), x_hi = min(D.m, j0 + x_hi_off);
+  const int wr0 = j0 + w_off;
+  const int wb = max(0, min(wwant, D.m - wr0));
+  // a list only exists for a matrix whose panel at j0 + g*_off exists (the
+  // panel kernel leaves the move counts of smaller matrices untouched)
+  const int c1 = (nm1 && D.m > j0 + g1_off) ? nm1[blockIdx.x] : 0;
+  const int c2 = (nm2 && D.m > j0 + g2_off) ? nm2[blockIdx.x] : 0;
+  const RowMove* l1 = mv1 ? mv1 + (size_t)blockIdx.x * 2 * b : nullptr;
+  const RowMove* l2 = mv2 ? mv2 + (size_t)blockIdx.x * 2 * b : nullptr;
+  double* w = W[blockIdx.x];
+  for (int col = c_lo + warp + blockIdx.y * 8; col < c_hi; col += 8 * gridDim.y) {
+    if (col >= x_lo && col < x_hi) continue;
+    double* a = D.A + (size_t)col * D.lda;
+#pragma unroll
+    for (int li = 0; li < 2; li++) {
+      const RowMove* mv = li == 0 ? l1 : l2;
+      const int cnt = li == 0 ? c1 : c2;
+      if (cnt == 0) continue;
+      double v0 = 0.0, v1 = 0.0;
+      RowMove m0{-1, -1}, m1{-1, -1};
+      if (lane < cnt) { m0 = mv[lane]; v0 = a[m0.src]; }
+      if (lane + 32 < cnt) { m1 = mv[lane + 32]; v1 = a[m1.src]; }
+      __syncwarp();
+      if (m0.dst >= 0) a[m0.dst] = v0;
+      if (m1.dst >= 0) a[m1.dst] = v1;
+      __syncwarp();
+    }
+    for (int t = lane; t < wb; t += 32) w[t + (size_t)col * wb] = a[wr0 + t];
+  }
+}
+
 // Trailing update of one Gauss-Jordan panel step, all matrices of the batch in
 // one launch, indexed on the device (no per-step host descriptors):
 //   A[i, c] = [i not in R1] A[i, c] + sum_k A[i, j+k] W[k, c]   for c outside the panel
@@ -829,7 +879,8 @@ __global__ void __launch_bounds__(256) gj_colgather_kernel(const MatDesc* __rest
 // columns v (all but the panel), P = A(:, j:j+b) i-contiguous, W k-contiguous.
 // Rows of the pivot block are overwritten (beta = 0), the others accumulated.
 // mode 0: all columns but the panel; 1: only the next panel's columns (the
-// look-ahead part); 2: all but the panel and the next panel.  Column u of the
+// look-ahead part); 2: all but the panel and the next panel; 4: only the
+// previous panel's columns [j - b, j) (two-level scheme).  Column u of the
 // mode's range maps to matrix column colmap(u).
 __device__ __forceinline__ int gj_cols(int mode, int j, int bb, int b2, int m) {
   return mode == 0 ? m - bb : (mode == 1 ? b2 : m - bb - b2);
@@ -848,7 +899,8 @@ __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc
   if (m <= j) return;
   const int bb = min(b, m - j);
   const int b2 = min(b, m - j - bb);  // width of the next panel
-  const int ncol = gj_cols(mode, j, bb, b2, m);
+  // mode 4: the previous inner panel's columns [j - b, j)
+  const int ncol = mode == 4 ? min(b, j) : gj_cols(mode, j, bb, b2, m);
   if (ncol <= 0) return;
   const int tilesM = (m + GBM - 1) / GBM;
   const int tl = blockIdx.y;
@@ -866,7 +918,7 @@ __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc
       const int c = tid + e * GTHREADS;
       const int k = c & (GBK - 1), r = c / GBK;
       const int vc = v0 + r, gk = k0 + k;
-      const int col = gj_colmap(mode, vc, j, bb, b2);
+      const int col = mode == 4 ? j - min(b, j) + vc : gj_colmap(mode, vc, j, bb, b2);
       const bool ok = vc < ncol && gk < bb;
       cp_async8(sm + r * KP + k, W + gk + (size_t)col * bb, ok);
     }
@@ -925,7 +977,7 @@ __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc
 #pragma unroll
     for (int e = 0; e < 8; e++) {
       const int vc = v0 + wn + (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
-      const int col = gj_colmap(mode, vc, j, bb, b2);
+      const int col = mode == 4 ? j - min(b, j) + vc : gj_colmap(mode, vc, j, bb, b2);
       ptr[e] = (gi < m && vc < ncol) ? D.A + gi + (size_t)col * D.lda : nullptr;
     }
 #pragma unroll
@@ -1019,7 +1071,66 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   };
   static const bool v1 = getenv("IFMM_GJ_UPDATE_V1") != nullptr;  // debug: register-staged update
   static const bool no_la = getenv("IFMM_GJ_NO_LOOKAHEAD") != nullptr;  // debug: serial panel/update
+  static const bool one_level = getenv("IFMM_GJ_ONE_LEVEL") != nullptr;  // debug: rank-b updates only
   const bool look = side && side->s && !v1 && !no_la;
+  // two-level for large batches (bandwidth-bound updates); few large matrices
+  // are panel-latency-bound and keep the one-level look-ahead (measured)
+  if (!v1 && !one_level && variant != 2 && n >= 64) {
+    // Two-level blocking: an outer panel of 2b columns is processed as two
+    // inner panels (each inner step updates only the other inner panel), then
+    // the rest of the matrix gets ONE rank-2b update with the processed outer
+    // panel and the original pivot rows (blocked Gauss-Jordan: the composed
+    // transform is x + (P - E) x_piv).  Half the trailing-update traffic.
+    const int B2 = 2 * b;
+    RowMove* moves2 = static_cast<RowMove*>(ws.alloc(sizeof(RowMove) * size_t(n) * 2 * b));
+    int* nmoves2 = ws.alloc_n<int>(n);
+    std::vector<double*> Wo(n);
+    for (int p = 0; p < n; p++) Wo[p] = ws.alloc_n<double>(size_t(B2) * h[p].m);
+    double* const* dWo = upload(ws, Wo, s, st);
+    auto panel_to = [&](int j, RowMove* mv, int* nm) {
+      if (variant == 0) gj_panel_reg_kernel<32, 1><<<n, threads, smem, s>>>(d_desc, j, d_info, mv, nm);
+      else if (variant == 4) gj_panel_reg_kernel<16, 1><<<n, threads, smem, s>>>(d_desc, j, d_info, mv, nm);
+      else gj_panel_reg_kernel<32, 2><<<n, threads, smem, s>>>(d_desc, j, d_info, mv, nm);
+      CK_LAUNCH();
+    };
+    auto upd = [&](int j, int bw, double* const* dw, int mode) {
+      int mt = 0;
+      for (int p = 0; p < n; p++) {
+        const int m = h[p].m;
+        if (m <= j) continue;
+        const int bb = std::min(bw, m - j), b2 = std::min(bw, m - j - bb);
+        const int nc = mode == 4 ? std::min(bw, j) : (mode == 0 ? m - bb : (mode == 1 ? b2 : m - bb - b2));
+        if (nc > 0) mt = std::max(mt, ceil_div(m, GBM) * ceil_div(nc, GBN));
+      }
+      if (mt > 0) {
+        gj_update_v2_kernel<<<dim3(n, mt), GTHREADS, GSMEM, s>>>(d_desc, j, bw, dw, mode);
+        CK_LAUNCH();
+      }
+    };
+    for (int J = 0; J < maxm; J += B2) {
+      panel_to(J, moves, nmoves);
+      const bool second = J + b < maxm;
+      if (second) {
+        // moves 1 on inner panel 2 + its pivot rows; inner update of panel 2
+        gj_move_copy2_kernel<<<dim3(n, 1), 256, 0, s>>>(d_desc, J, b, B2, 0, 0, b, moves, nmoves, nullptr, nullptr,
+                                                        0, b, dW, 0, 0);
+        CK_LAUNCH();
+        upd(J, b, dW, 1);
+        panel_to(J + b, moves2, nmoves2);
+        // moves 2 on inner panel 1 + its pivot rows; inner update of panel 1
+        gj_move_copy2_kernel<<<dim3(n, 1), 256, 0, s>>>(d_desc, J, 0, b, 0, 0, b, moves2, nmoves2, nullptr,
+                                                        nullptr, b, b, dW, b, 0);
+        CK_LAUNCH();
+        upd(J + b, b, dW, 4);
+      }
+      // the rest: moves 1 then 2, original pivot rows (2b of them), one rank-2b update
+      gj_move_copy2_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, J, -1, -1, 0, B2, b, moves, nmoves,
+                                                       second ? moves2 : nullptr, second ? nmoves2 : nullptr, 0, B2,
+                                                       dWo, 0, b);
+      CK_LAUNCH();
+      upd(J, B2, dWo, 0);
+    }
+  } else {
   panel(0, s);
   for (int j = 0; j < maxm; j += b) {
     gj_move_copy_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, j, b, moves, nmoves, dW);
@@ -1055,6 +1166,7 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
       if (more) panel(j + b, s);
     }
   }
+  }  // one-level path
   // undo the row pivoting as one column gather per matrix (through scratch)
   int* perm = ws.alloc_n<int>(size_t(n) * maxm);
   std::vector<double*> T(n);

@@ -72,6 +72,25 @@ def test_gj_inverse_batched_variable_sizes(L):
         assert np.linalg.norm(inv - ref) <= 1e-10 * np.linalg.norm(ref) * max(1.0, np.linalg.cond(m) / 1e4)
 
 
+def test_gj_inverse_large_batch_mixed_sizes(L):
+    """>= 64 matrices take the two-level path; sizes ending inside the first
+    or second inner panel of an outer step must not pick up stale row moves."""
+    rng = np.random.default_rng(7)
+    sizes = [int(x) for x in rng.integers(40, 140, size=80)] + [64, 96, 97, 127, 128, 129]
+    mats = [_saddle(rng, max(1, m - m // 3), m // 3) for m in sizes]
+    sz = np.array([x.shape[0] for x in mats], dtype=np.int32)
+    packed = np.concatenate([np.asfortranarray(x).ravel(order="F") for x in mats])
+    info = np.zeros(len(mats), dtype=np.int32)
+    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(sz), len(mats), L.ptr(info)))
+    assert not info.any()
+    off = 0
+    for x in mats:
+        k = x.shape[0]
+        inv = packed[off:off + k * k].reshape((k, k), order="F")
+        off += k * k
+        assert np.linalg.norm(inv @ x - np.eye(k)) <= 1e-9 * k * max(1.0, np.linalg.cond(x) / 1e4)
+
+
 @pytest.mark.parametrize("m", [900, 1024, 1100])
 def test_gj_inverse_large_single(L, m):
     """Single large pivots (top levels): 16-wide register panel up to m = 1024,
