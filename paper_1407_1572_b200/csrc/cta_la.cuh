@@ -14,6 +14,7 @@ namespace ifmm {
 struct CtaShared {
   double red[32];
   double red2[32];
+  double pmax[32 * 10];  // per-warp probe-row maxima (ACA start row)
   ArgMax am[32];
   int flag;
   int ival[4];
@@ -62,6 +63,18 @@ struct CtaGroup {
       c = argmax_merge(c, sh.am[w]);
     }
   }
+  // max over the group of v[0..np) (warp-reduced first), identical everywhere
+  __device__ void max10(double (&v)[10], int np) const {
+    __syncthreads();
+    if (lane() == 0)
+      for (int t = 0; t < np; t++) sh.pmax[warp() * 10 + t] = v[t];
+    __syncthreads();
+    for (int t = 0; t < np; t++) {
+      double m = -1.0;
+      for (int w = 0; w < nwarps(); w++) m = fmax(m, sh.pmax[w * 10 + t]);
+      v[t] = m;
+    }
+  }
   __device__ static CtaGroup make_for_test(CtaShared& sh) { return CtaGroup{sh}; }
 };
 
@@ -77,6 +90,7 @@ struct WarpGroup {
   __device__ ArgMax argmax(ArgMax v) const { return warp_argmax(v); }
   __device__ bool any(bool p) const { return __any_sync(0xffffffffu, p) != 0; }
   __device__ void combine(double&, double&, ArgMax&) const { __syncwarp(); }  // already warp-reduced
+  __device__ void max10(double (&)[10], int) const {}                          // already warp-reduced
   __device__ static WarpGroup make_for_test(CtaShared&) { return WarpGroup{}; }
 };
 
@@ -538,19 +552,27 @@ __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, i
   // first row: probe with the largest max-abs entry (first in probe order on ties)
   int next;
   {
+    // the probe row with the largest max-abs entry (first in probe order on
+    // ties): all probe maxima in one pass and one group reduction
+    double pm[10];
+#pragma unroll
+    for (int t = 0; t < 10; t++) pm[t] = -1.0;
+#pragma unroll
+    for (int t = 0; t < 10; t++)
+      if (t < nprobe) {
+        const int i = probes[t];
+        for (int j = g.rank(); j < n; j += g.size()) pm[t] = fmax(pm[t], fabs(Fat(F, ld, trans, i, j)));
+        for (int o = 16; o > 0; o >>= 1) pm[t] = fmax(pm[t], __shfl_xor_sync(0xffffffffu, pm[t], o));
+      }
+    g.max10(pm, nprobe);
     double best = -1.0;
     int bi = probes[0];
-    for (int t = 0; t < nprobe; t++) {
-      const int i = probes[t];
-      ArgMax am{-1.0, -1};
-      for (int j = g.rank(); j < n; j += g.size()) am = argmax_merge(am, ArgMax{fabs(Fat(F, ld, trans, i, j)), j});
-      am = g.argmax(am);
-      if (am.a > best) {
-        best = am.a;
-        bi = i;
+    for (int t = 0; t < nprobe; t++)
+      if (pm[t] > best) {
+        best = pm[t];
+        bi = probes[t];
       }
-    }
-    next = bi;  // identical in every thread: the argmax is broadcast
+    next = bi;  // identical in every thread
   }
   int k = 0, strikes = 0, nused = 0;
   double nsq = 0.0;
