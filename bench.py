@@ -41,7 +41,7 @@ CONFIGS = {
 }
 METRIC = "IFMM factor+solve seconds at N=1M 2D"
 CPU_SAMPLE = (16384, 4)   # cpu_baseline sample: C3 parameters at N=16,384 (depth 4)
-REF_SAMPLE = (4096, 3)    # --impl reference per-step sample: C3 parameters at N=4,096 (depth 3)
+REF_SAMPLE = (16384, 4)   # --impl reference per-step sample: C3 parameters at N=16,384 (depth 4), ~9 s
 
 
 def dist_env():
@@ -168,7 +168,7 @@ def run_reference(args, cfg):
                                    f"reference) factor+solve at N={ns} depth {ds} with {args.config} parameters, "
                                    f"1 BLAS thread (multi-threaded BLAS is 4x slower, SURVEY finding 8), "
                                    f"scaled x{N // ns} to N={N} (linear: a lower bound, per-point work grows "
-                                   f"with depth)"},
+                                   f"with depth; BASELINE.md extrapolates the reference at N=1M to 40-60 min)"},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
