@@ -431,7 +431,8 @@ template <class G>
 __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks)
     augment_prep_kernel(const FillDesc* __restrict__ fills, const int* __restrict__ aug, int ntasks,
                         const FillState* __restrict__ state, const int* __restrict__ rank, double tol,
-                        double* const* __restrict__ Hbuf, double* scratch, size_t slot) {
+                        double* const* __restrict__ Hbuf, double* scratch, size_t slot,
+                        double* const* __restrict__ Ebuf, int* __restrict__ r0buf) {
   __shared__ CtaShared sh;
   const G g = Worker<G>::make(sh);
   double* E = scratch + slot * Worker<G>::id();
@@ -447,13 +448,24 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks)
     const double* right = D.out + (size_t)D.rows * D.Kf;
     const double* src = side ? D.out : right;
     const double* wsig = side ? nullptr : right + (size_t)D.cols * D.Kf;
-    for (int e = g.rank(); e < nU * r; e += g.size()) H[e] = wsig ? src[e] * wsig[e / nU] : src[e];
+    for (int e = g.rank(); e < nU * r; e += g.size()) H[e] = src[e];
     g.sync();
-    if (r0 > 0 && r0 < nU) {
+    // project the UNweighted factor (the weights commute with the projection)
+    // so the first-pass coefficients U0^T F are exactly what K4 needs for the
+    // M2L absorption: saved in Ebuf (r0 x r), K4 only computes the rows of
+    // columns appended during the batch
+    const bool proj = r0 > 0 && r0 < nU;
+    if (proj) {
       const double* U = side ? D.Up : D.Uq;
-      g_project_out(g, H, nU, nU, r, U, nU, r0, E);
+      double* E1 = Ebuf[u];
+      g_gemm(g, r0, r, nU, 1.0, U, nU, true, H, nU, false, 0.0, E1, r0);
+      g_gemm(g, nU, r, r0, -1.0, U, nU, false, E1, r0, false, 1.0, H, nU);
       g_project_out(g, H, nU, nU, r, U, nU, r0, E);
     }
+    if (wsig) {
+      for (int e = g.rank(); e < nU * r; e += g.size()) H[e] *= wsig[e / nU];
+    }
+    if (g.rank() == 0) r0buf[u] = proj ? r0 : 0;
     g.sync();
   }
 }
@@ -501,7 +513,9 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks)
 template <class G>
 __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) delta_kernel(const FillDesc* __restrict__ fills, int nf,
                                                    const FillState* __restrict__ state, double tol, double* scratch,
-                                                   size_t slot, int MX, int KK, int* stats) {
+                                                   size_t slot, int MX, int KK, int* stats,
+                                                   const int* __restrict__ taskq, const int* __restrict__ taskp,
+                                                   double* const* __restrict__ Ebuf, const int* __restrict__ r0buf) {
   __shared__ CtaShared sh;
   const G g = Worker<G>::make(sh);
   double* Eq = scratch + slot * Worker<G>::id();
@@ -525,11 +539,22 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) delta_kernel(co
       const int r = S.r, rq = S.rq;
       const double* left = D.out;
       const double* right = D.out + (size_t)rows * D.Kf;
-      g_gemm(g, rq, r, cols, 1.0, D.Uq, cols, true, right, cols, false, 0.0, Eq, rq);  // Uq^T B
+      // Uq^T B: rows of the batch-initial basis come from the augmentation
+      // pre-pass (Ebuf), only the rows of appended columns are computed here
+      auto coeffs = [&](const double* Ub, int ld, const double* Fx, int rr, int t, double* Eo) {
+        const int r0 = (t >= 0 && Ebuf) ? min(r0buf[t], rr) : 0;
+        if (r0 > 0) {
+          const double* E1 = Ebuf[t];
+          for (int e = g.rank(); e < r0 * r; e += g.size()) Eo[(e % r0) + (size_t)(e / r0) * rr] = E1[e];
+        }
+        if (rr > r0) g_gemm(g, rr - r0, r, ld, 1.0, Ub + (size_t)r0 * ld, ld, true, Fx, ld, false, 0.0, Eo + r0, rr);
+        g.sync();
+      };
+      coeffs(D.Uq, cols, right, rq, taskq ? taskq[f] : -1, Eq);
       const double* X = left;
       int rx = rows, ldx = rows;
       if (D.kind == FILL_P2P) {
-        g_gemm(g, S.rp, r, rows, 1.0, D.Up, rows, true, left, rows, false, 0.0, Ep, S.rp);  // Up^T A
+        coeffs(D.Up, rows, left, S.rp, taskp ? taskp[f] : -1, Ep);  // Up^T A
         X = Ep;
         rx = S.rp;
         ldx = S.rp;
@@ -670,6 +695,9 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   }
   const size_t dslot = 3 * size_t(MX) * KK + size_t(KK) * KK + 3 * size_t(KK) + 64;
   const int bs_d = wmode ? 32 * WPB : bs_dirs;
+  std::vector<int> tq, tp;  // fill -> q-side / p-side augmentation task (-1: none)
+  double* const* d_eb = nullptr;
+  int* d_r0 = nullptr;
   // K2+K3: per-cluster augmentation chains.  Order inside a chain: the
   // cluster's hybrid fills (sorted), then the P2P fills touching it in the
   // pivot's pair order; clusters of different pivots of a batch are disjoint.
@@ -716,16 +744,31 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
         hb[u] = ws.alloc_n<double>(size_t((lst[u] & 1) ? D.rows : D.cols) * D.Kf);
       }
       double* const* dhb = upload(ws, hb, s, st);
+      // first-pass coefficients U0^T F per task (r0 x Kf, r0 = batch-initial
+      // rank from the host copy) + the fill -> task maps for K4
+      std::vector<double*> eb(lst.size(), nullptr);
+      tq.assign(cb.fills.size(), -1);
+      tp.assign(cb.fills.size(), -1);
+      for (size_t u = 0; u < lst.size(); u++) {
+        const int f = lst[u] >> 1, side = lst[u] & 1;
+        const FillDesc& D = cb.fills[f];
+        const int r0 = cb.rank_host ? cb.rank_host[side ? D.p : D.q] : 0;
+        if (r0 > 0) eb[u] = ws.alloc_n<double>(size_t(r0) * D.Kf);
+        (side ? tp : tq)[f] = int(u);
+      }
+      d_eb = upload(ws, eb, s, st);
+      d_r0 = ws.alloc_n<int>(lst.size());
+      CK(cudaMemsetAsync(d_r0, 0, sizeof(int) * lst.size(), s));
       {
         const size_t pslot = size_t(MX) * KK + 64;
         const int pgrid = grid_for(ntask, bs_d == bs_small ? per_sm : 8, 32);
         double* pscr = ws.alloc_n<double>(pslot * workers(pgrid));
         if (wmode)
           augment_prep_kernel<WarpGroup><<<pgrid, bs_d, 0, s>>>(dfd, dlst, ntask, d_state, d_rank, tol, dhb, pscr,
-                                                                  pslot);
+                                                                  pslot, d_eb, d_r0);
         else
           augment_prep_kernel<CtaGroup><<<pgrid, bs_d, 0, s>>>(dfd, dlst, ntask, d_state, d_rank, tol, dhb, pscr,
-                                                                 pslot);
+                                                                 pslot, d_eb, d_r0);
         CK_LAUNCH();
       }
       const int grid = grid_for(n, bs_d == bs_small ? per_sm : 8, 32);
@@ -744,10 +787,14 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     const size_t slot = 2 * size_t(MX) * KK + 64;
     const int grid = grid_for(nf, bs_fill == bs_small ? per_sm : 8, 32);
     double* scr = ws.alloc_n<double>(slot * workers(grid));
+    const int* dtq = tq.empty() ? nullptr : upload(ws, tq, s, st);
+    const int* dtp = tp.empty() ? nullptr : upload(ws, tp, s, st);
     if (wmode)
-      delta_kernel<WarpGroup><<<grid, 32 * WPB, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats);
+      delta_kernel<WarpGroup><<<grid, 32 * WPB, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats, dtq, dtp,
+                                                          d_eb, d_r0);
     else
-      delta_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats);
+      delta_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, scr, slot, MX, KK, d_stats, dtq, dtp,
+                                                        d_eb, d_r0);
     CK_LAUNCH();
   }
   if (prof) {

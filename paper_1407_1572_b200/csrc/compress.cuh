@@ -44,6 +44,7 @@ struct CompressBatch {
   std::vector<int> chain_off, chain;  // hybrid chains (fill indices, sorted by p)
   std::vector<int> p2p_off, p2p;      // per pivot P2P fills (sorted)
   std::vector<int> chain_q;           // q of each chain
+  const int* rank_host = nullptr;     // host copy of the level's ranks at batch start
 };
 
 // Runs K1..K4 on stream s.  rank: device ranks of the level (updated);

@@ -575,6 +575,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         if (T.in_il(I.xp[a], I.xp[b])) cbz.p2p.push_back(add_fill(FILL_P2P, I.xp[a], I.xp[b]));
     cbz.p2p_off.push_back(int(cbz.p2p.size()));
   }
+  cbz.rank_host = W.r.data();
   const size_t nfill = cbz.fills.size();
   FillState* d_state = ws_.alloc_n<FillState>(std::max<size_t>(1, nfill));
   int* d_stats = ws_.alloc_n<int>(4);
