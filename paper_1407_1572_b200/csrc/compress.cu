@@ -636,7 +636,8 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   // for the largest blocks (measured: 1024 wins for MX >= ~800, loses at 265-570)
   static const int bs_big_env = getenv("IFMM_BS_BIG") ? atoi(getenv("IFMM_BS_BIG")) : 0;  // tuning override
   const int bs_big = bs_big_env ? bs_big_env : (MX >= 700 ? 1024 : 512);
-  const int bs_fill = narrow ? 128 : (MX >= 256 && nf < 2048) ? bs_big : (MX >= 128 ? 256 : bs_small);
+  static const int nf_big = getenv("IFMM_K1_NF_BIG") ? atoi(getenv("IFMM_K1_NF_BIG")) : 2048;  // tuning
+  const int bs_fill = narrow ? 128 : (MX >= 256 && nf < nf_big) ? bs_big : (MX >= 128 ? 256 : bs_small);
   const int bs_dirs = narrow ? 128 : MX >= 256 ? bs_big : (MX >= 128 ? 256 : bs_small);
   constexpr int WPB = 4;  // warps per CTA in warp mode
   static const bool prof = getenv("IFMM_PROF") != nullptr;
