@@ -148,17 +148,25 @@ __global__ void __launch_bounds__(GTHREADS, 3)
   const SchurPiv P = pivs[tt.x];
   const int i0 = (tt.y >> 16) * GBM, j0 = (tt.y & 0xffff) * GBN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // slot offsets staged in shared memory (one coalesced load) so the
+  // per-thread binary searches below do not chain global-memory latencies
+  __shared__ int s_soff[129];
   const int* soff = soff_pool + P.soff0;
+  const bool stage = P.ns < 128;
+  if (stage)
+    for (int a = tid; a <= P.ns; a += GTHREADS) s_soff[a] = soff[a];
+  __syncthreads();
+  const int* so = stage ? s_soff : soff;
   {  // slot and in-slot offset of the tile's rows (threads 0..63) and columns (64..127)
     const int e = tid & 63;
     const int g = (tid < 64 ? i0 : j0) + e;
     int lo = 0, hi = P.ns - 1;  // largest a with soff[a] <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (soff[mid] <= g) lo = mid; else hi = mid - 1;
+      if (so[mid] <= g) lo = mid; else hi = mid - 1;
     }
-    if (tid < 64) { rslot[e] = lo; roff[e] = g - soff[lo]; }
-    else { cslot[e] = lo; coff[e] = g - soff[lo]; }
+    if (tid < 64) { rslot[e] = lo; roff[e] = g - so[lo]; }
+    else { cslot[e] = lo; coff[e] = g - so[lo]; }
   }
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
   auto Asm = [&](int st) { return gsm + (size_t)st * 2 * GTILE_D; };
