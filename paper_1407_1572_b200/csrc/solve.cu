@@ -13,6 +13,7 @@
 #include <cmath>
 
 #include "core.cuh"
+#include "gemm.cuh"
 
 namespace ifmm {
 
@@ -217,6 +218,173 @@ __global__ void __launch_bounds__(SB, RC == 1 ? 4 : 2) solve_bwd_kernel(const Re
   }
 }
 
+// ------------------------------------------------------------------ many rhs
+// Multi-rhs sweeps as DMMA GEMMs: each record is read once
+// per chunk of up to 32 right-hand sides instead of once per 4, which turns the
+// HBM-bound sweeps compute-bound (8 flop/B at 32 rhs).  64 x 32 output tiles,
+// 4 warps x (16 x 32), cp.async-staged operands (layouts as in gemm.cuh).
+constexpr int MQ = 32;             // rhs per chunk
+constexpr int QP = MQ + 4;         // pitch of the [k][q] operand tile (== 4 mod 16)
+constexpr int MM_STAGES = 3;
+constexpr int MM_A = GBM * KP;     // A tile doubles ([row][k], pitch KP)
+constexpr int MM_B = GBK * QP;     // B tile doubles ([k][q], pitch QP)
+constexpr size_t MM_SMEM = sizeof(double) * size_t(MM_STAGES) * (MM_A + MM_B);
+
+__device__ __forceinline__ void mm_mma(const double* As, const double* Bs, double (&acc)[2][4][2], int warp,
+                                       int lane) {
+#pragma unroll
+  for (int kk = 0; kk < GBK; kk += 4) {
+    double fa[2], fb[4];
+#pragma unroll
+    for (int m = 0; m < 2; m++) fa[m] = As[(warp * 16 + m * 8 + (lane >> 2)) * KP + kk + (lane & 3)];
+#pragma unroll
+    for (int n = 0; n < 4; n++) fb[n] = Bs[(kk + (lane & 3)) * QP + n * 8 + (lane >> 2)];
+#pragma unroll
+    for (int m = 0; m < 2; m++)
+#pragma unroll
+      for (int n = 0; n < 4; n++)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                     : "d"(fa[m]), "d"(fb[n]));
+  }
+}
+
+// forward: Out = [S^-1_nn | X_top]^T B (rows c < n -> G, c >= n -> V[pos] -= ),
+// B = V(xoff : xoff + n, q0 : q0 + nq).  grid (record, 64-row tile, rhs chunk)
+__global__ void __launch_bounds__(GTHREADS) solve_fwd_mm_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                                const int64_t* __restrict__ g_off, double* V,
+                                                                double* G, int nrhs) {
+  extern __shared__ double msm[];
+  const RecordH R = recs[blockIdx.x];
+  const int n = R.n, w = R.w, nc = n + w;
+  const int c0 = blockIdx.y * GBM;
+  if (c0 >= nc || n == 0) return;
+  const int q0 = blockIdx.z * MQ, nq = min(MQ, nrhs - q0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
+  const double* Bv = V + R.xoff * nrhs + q0;
+  auto load = [&](int st, int k0) {
+    double* As = msm + (size_t)st * (MM_A + MM_B);
+    double* Bs = As + MM_A;
+#pragma unroll
+    for (int e = 0; e < (GBM * GBK) / GTHREADS; e++) {  // A: column c of [S^-1 | X_top], k-contiguous
+      const int cidx = tid + e * GTHREADS, k = cidx & (GBK - 1), r = cidx / GBK;
+      const int c = c0 + r, gk = k0 + k;
+      const bool ok = c < nc && gk < n;
+      const double* src = c < n ? R.sinv + gk + (size_t)c * n : R.xtop + gk + (size_t)(c - n) * n;
+      cp_async8(As + r * KP + k, src, ok);
+    }
+#pragma unroll
+    for (int e = 0; e < (GBK * MQ) / GTHREADS; e++) {  // B: rows of V, q-contiguous
+      const int cidx = tid + e * GTHREADS, q = cidx & (MQ - 1), k = cidx / MQ;
+      const int gk = k0 + k;
+      cp_async8(Bs + k * QP + q, Bv + (size_t)gk * nrhs + q, gk < n && q < nq);
+    }
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nk = (n + GBK - 1) / GBK;
+#pragma unroll
+  for (int st = 0; st < MM_STAGES - 1; st++) {
+    if (st < nk) load(st, st * GBK);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; kt++) {
+    cp_async_wait<MM_STAGES - 2>();
+    __syncthreads();
+    if (kt + MM_STAGES - 1 < nk) load((kt + MM_STAGES - 1) % MM_STAGES, (kt + MM_STAGES - 1) * GBK);
+    cp_async_commit();
+    const double* As = msm + (size_t)(kt % MM_STAGES) * (MM_A + MM_B);
+    mm_mma(As, As + MM_A, acc, warp, lane);
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int m = 0; m < 2; m++) {
+    const int c = c0 + warp * 16 + m * 8 + (lane >> 2);
+    if (c >= nc) continue;
+    double* row = c < n ? g + (size_t)c * nrhs + q0 : V + (int64_t)R.pos[c - n] * nrhs + q0;
+    const bool sub = c >= n;
+    double old[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int q = (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
+      old[e] = (sub && q < nq) ? row[q] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int q = (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
+      if (q < nq) row[q] = sub ? old[e] - acc[m][e >> 1][e & 1] : acc[m][e >> 1][e & 1];
+    }
+  }
+}
+
+// backward: x(t, q) = G(t, q) - sum_c X_top(t, c) V(pos[c], q).
+// grid (record, 64-row tile of n, rhs chunk); K = w with row-gathered B
+__global__ void __launch_bounds__(GTHREADS) solve_bwd_mm_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                                const int64_t* __restrict__ g_off, double* V,
+                                                                const double* G, int nrhs) {
+  extern __shared__ double msm[];
+  const RecordH R = recs[blockIdx.x];
+  const int n = R.n, w = R.w;
+  const int t0 = blockIdx.y * GBM;
+  if (t0 >= n) return;
+  const int q0 = blockIdx.z * MQ, nq = min(MQ, nrhs - q0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
+  auto load = [&](int st, int k0) {
+    double* As = msm + (size_t)st * (MM_A + MM_B);
+    double* Bs = As + MM_A;
+#pragma unroll
+    for (int e = 0; e < (GBM * GBK) / GTHREADS; e++) {  // A: X_top(t, c), t-contiguous -> stored [t][k]
+      const int cidx = tid + e * GTHREADS, r = cidx & (GBM - 1), k = cidx / GBM;
+      const int t = t0 + r, gk = k0 + k;
+      cp_async8(As + r * KP + k, R.xtop + t + (size_t)gk * n, t < n && gk < w);
+    }
+#pragma unroll
+    for (int e = 0; e < (GBK * MQ) / GTHREADS; e++) {  // B: V(pos[c], q)
+      const int cidx = tid + e * GTHREADS, q = cidx & (MQ - 1), k = cidx / MQ;
+      const int gk = k0 + k;
+      const bool ok = gk < w && q < nq;
+      const double* src = ok ? V + (int64_t)R.pos[gk] * nrhs + q0 + q : V;
+      cp_async8(Bs + k * QP + q, src, ok);
+    }
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nk = (w + GBK - 1) / GBK;
+#pragma unroll
+  for (int st = 0; st < MM_STAGES - 1; st++) {
+    if (st < nk) load(st, st * GBK);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; kt++) {
+    cp_async_wait<MM_STAGES - 2>();
+    __syncthreads();
+    if (kt + MM_STAGES - 1 < nk) load((kt + MM_STAGES - 1) % MM_STAGES, (kt + MM_STAGES - 1) * GBK);
+    cp_async_commit();
+    const double* As = msm + (size_t)(kt % MM_STAGES) * (MM_A + MM_B);
+    mm_mma(As, As + MM_A, acc, warp, lane);
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int m = 0; m < 2; m++) {
+    const int t = t0 + warp * 16 + m * 8 + (lane >> 2);
+    if (t >= n) continue;
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int q = (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
+      if (q < nq)
+        V[(R.xoff + t) * nrhs + q0 + q] = g[(size_t)t * nrhs + q0 + q] - acc[m][e >> 1][e & 1];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ refinement
 __global__ void resid_kernel(const double* __restrict__ b, double* __restrict__ r, int64_t n, double* sums) {
   // r = b - r ; sums[0] += |r|^2, sums[1] += |b|^2
@@ -323,7 +491,23 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     attr = true;
   }
   const int RC = nr == 1 ? 1 : RCMAX;
+  // many right-hand sides: DMMA sweeps (IFMM_SOLVE_MM_MIN: tuning / debug)
+  static const int mm_min = getenv("IFMM_SOLVE_MM_MIN") ? atoi(getenv("IFMM_SOLVE_MM_MIN")) : 2;
+  const bool mm = nr >= mm_min;
+  static bool mm_attr = false;
+  if (mm && !mm_attr) {
+    CK(cudaFuncSetAttribute(solve_fwd_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(MM_SMEM)));
+    CK(cudaFuncSetAttribute(solve_bwd_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(MM_SMEM)));
+    mm_attr = true;
+  }
+  const int nqc = (nr + MQ - 1) / MQ;
   for (const BatchH& b : F->batches) {
+    if (mm) {
+      const dim3 grid(b.rec1 - b.rec0, (b.maxn + b.maxw + GBM - 1) / GBM, nqc);
+      solve_fwd_mm_kernel<<<grid, GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
+      CK_LAUNCH();
+      continue;
+    }
     const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
     const size_t smem = sizeof(double) * (size_t(rr) * SWARPS * RC + size_t(b.maxn) * RC);
     if (smem > 200 * 1024) invalid("solve: pivot block too large for the solve kernel");
@@ -352,6 +536,12 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
   }
   for (auto it = F->batches.rbegin(); it != F->batches.rend(); ++it) {
     const BatchH& b = *it;
+    if (mm) {
+      const dim3 grid(b.rec1 - b.rec0, (b.maxn + GBM - 1) / GBM, nqc);
+      solve_bwd_mm_kernel<<<grid, GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
+      CK_LAUNCH();
+      continue;
+    }
     const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
     const size_t smem = sizeof(double) * size_t(rr) * SWARPS * RC;
     const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));

@@ -130,6 +130,20 @@ def test_multi_rhs_solve(ifmm):
         assert np.linalg.norm(X[:, c] - x) <= 1e-13 * np.linalg.norm(x)
 
 
+@pytest.mark.parametrize("nrhs", [9, 40])
+def test_many_rhs_solve_gemm_path(ifmm, nrhs):
+    """nrhs >= 2 takes the DMMA sweeps (32-column rhs chunks): every column
+    equals the single-rhs solve to rounding."""
+    g, pts, tree = _setup(ifmm, "c1_invr")
+    store = ifmm.init_operators(tree, _kernel(ifmm, g), p=int(g["p"]), tol=float(g["tol"]))
+    fact = ifmm.factorize(store, tree)
+    B = np.random.default_rng(nrhs).standard_normal((len(pts), nrhs))
+    X = ifmm.solve(fact, B)
+    for c in (0, nrhs // 2, nrhs - 1):
+        x = ifmm.solve(fact, B[:, c])
+        assert np.linalg.norm(X[:, c] - x) <= 1e-11 * np.linalg.norm(x)
+
+
 def test_solve_is_deterministic(ifmm):
     g, pts, tree = _setup(ifmm, "c1_invr")
     outs = []
