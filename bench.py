@@ -319,6 +319,21 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     solve_ms = float(np.median(ts))
+    # extension: 32 right-hand sides through the DMMA sweeps
+    b32 = torch.from_numpy(np.random.default_rng([0, 2]).standard_normal((N, 32))).cuda()
+    ifmm.solve(ft, b32)
+    t32 = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        ifmm.solve(ft, b32)
+        e1.record()
+        torch.cuda.synchronize()
+        t32.append(e0.elapsed_time(e1))
+    solve32_ms = float(np.median(t32))
+    # 2 flops per record element and rhs in each sweep: solve_bytes / 8 elements per rhs
+    solve32_flops = 2.0 * work["solve_bytes"] / 8.0 * 32
 
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -354,6 +369,11 @@ def main():
         "solve_roofline": {"bound": "hbm", "ms": solve_ms, "bytes": work["solve_bytes"],
                            "achieved": work["solve_bytes"] / (solve_ms * 1e-3) / 1e9, "peak": hb, "unit": "GB/s",
                            "frac": work["solve_bytes"] / (solve_ms * 1e-3) / 1e9 / hb, "peak_source": hb_src},
+        "solve_32rhs": {"ms": solve32_ms, "tflops": solve32_flops / (solve32_ms * 1e-3) / 1e12,
+                        "frac_of_fp64_peak": solve32_flops / (solve32_ms * 1e-3) / 1e12 / fl_peak,
+                        "vs_32_single_solves": 32 * solve_ms / solve32_ms,
+                        "note": "extension (SURVEY 8f item 1): one factorization, 32 rhs as DMMA GEMM sweeps; "
+                                "not in value"},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 8 * N * nrhs, "d2h_bytes_per_step": 8 * N * nrhs},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
