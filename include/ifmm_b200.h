@@ -52,6 +52,7 @@ enum {
 typedef struct ifmm_tree ifmm_tree;
 typedef struct ifmm_store ifmm_store;
 typedef struct ifmm_factor ifmm_factor;
+typedef struct ifmm_comm ifmm_comm;
 
 const char* ifmm_last_error(void);
 int ifmm_last_singular(int* level, int* index, double* cond);
@@ -127,6 +128,45 @@ int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int p
 int ifmm_solve_refined(ifmm_factor* f, ifmm_store* s, const double* rhs, double* x, int64_t nrhs, int ptr_kind,
                        int max_iters, double target, double* hist, int* iters_done);
 void ifmm_factor_free(ifmm_factor* f);
+
+/* ---- subtree-sharded factorize / solve over several GPUs (the
+ * reference is single-process and has no counterpart: this extends
+ * factorize(store, tree, tol) ifmm/solver.py:106-153 and solve ifmm/solver.py:549).
+ * One process per GPU.  Level-2 subtrees are dealt to ranks in contiguous
+ * Morton ranges; every rank replays the host schedule, computes its own
+ * subtrees' eliminations and ships the blocks it wrote to the ranks storing
+ * them (NCCL send/recv over NVLink after every colour batch).  Every call
+ * below marked "collective" must be made by all ranks in the same order. */
+/* 128-byte NCCL unique id (call on one rank, share it, e.g. via torch.distributed) */
+int ifmm_comm_nccl_unique_id(uint8_t* out128);
+int ifmm_comm_nccl_version(int* version);
+/* collective: communicator over the current CUDA device of every rank */
+int ifmm_comm_nccl_init(const uint8_t* id128, int nranks, int rank, ifmm_comm** out);
+void ifmm_comm_free(ifmm_comm* c);
+/* collective transport check: all-gather of n doubles and a ring send/recv
+ * (a 1-rank communicator sends to itself); ok = 1 if all data arrived */
+int ifmm_comm_selftest(ifmm_comm* c, int64_t n, int32_t* ok);
+/* collective: sharded factorization; ifmm_solve on the result is collective
+ * too and returns the full solution on every rank.  nranks <= 4^2 (2-D). */
+int ifmm_factorize_sharded(ifmm_store* s, ifmm_comm* c, double tol, int flags, double cond_limit,
+                           ifmm_factor** out);
+/* the same schedule with `nranks` virtual ranks as threads on this GPU
+ * (device-to-device copies instead of NCCL): out[nranks] factor handles */
+int ifmm_factorize_emulated(ifmm_store* s, int nranks, double tol, int flags, double cond_limit,
+                            ifmm_factor** out);
+/* solve on every virtual rank; x: nranks consecutive (n, nrhs) solutions */
+int ifmm_solve_emulated(ifmm_factor** f, int nranks, const double* rhs, double* x, int64_t nrhs, int ptr_kind);
+/* rank_nranks[2]; out4: halo bytes sent, metadata bytes sent, exchanges,
+ * device ms in communication phases (with IFMM_FLAG_TIMING) */
+int ifmm_factor_shard_info(const ifmm_factor* f, int32_t* rank_nranks, double* out4);
+/* host-only: owner rank of every cluster of `level` and held[s * nc + i] = 1 if
+ * rank s stores cluster i's blocks (its own clusters and their neighbours) */
+int ifmm_partition(int dim, int depth, int level, int nranks, int32_t* owner, uint8_t* held);
+/* host-only plan check: halo items rank `rank` sends to / receives from each
+ * peer for colour batch `colour` of `level` with the initial block pattern,
+ * routed by the factorization's own rule (comm.cuh halo_route) */
+int ifmm_partition_halo_counts(int dim, int depth, int level, int nranks, int rank, int colour, int32_t* send,
+                               int32_t* recv);
 
 /* ---- test hooks for the batched kernels (host arrays in/out) */
 /* run the Jacobi / QR / ACA hooks on one warp (1) or a 256-thread CTA (0) */

@@ -10,6 +10,7 @@ from .geometry import ClusterTree, Cluster, PointSet, build_tree, compute_lists,
 from .kernels import KERNEL_NAMES, Kernel, baseline_kernel, kernel_block, make_kernel
 from .operators import OperatorStore, fmm_matvec, init_operators
 from .solver import IfmmFactorization, LevelStats, factorize, solve
+from . import distributed  # noqa: E402  (sharded factorize / solve)
 
 __all__ = [
     "Cluster",

@@ -66,6 +66,17 @@ SIGNATURES = {
     "ifmm_solve": (_i32, [_p, _p, _p, _i64, _i32]),
     "ifmm_solve_refined": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _d, _p, _p]),
     "ifmm_factor_free": (None, [_p]),
+    "ifmm_comm_nccl_unique_id": (_i32, [_p]),
+    "ifmm_comm_nccl_version": (_i32, [_pi32]),
+    "ifmm_comm_nccl_init": (_i32, [_p, _i32, _i32, ctypes.POINTER(_p)]),
+    "ifmm_comm_free": (None, [_p]),
+    "ifmm_comm_selftest": (_i32, [_p, _i64, _pi32]),
+    "ifmm_factorize_sharded": (_i32, [_p, _p, _d, _i32, _d, ctypes.POINTER(_p)]),
+    "ifmm_factorize_emulated": (_i32, [_p, _i32, _d, _i32, _d, _p]),
+    "ifmm_solve_emulated": (_i32, [_p, _i32, _p, _p, _i64, _i32]),
+    "ifmm_factor_shard_info": (_i32, [_p, _p, _p]),
+    "ifmm_partition": (_i32, [_i32, _i32, _i32, _i32, _p, _p]),
+    "ifmm_partition_halo_counts": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _p, _p]),
     "ifmm_test_gj_inverse": (_i32, [_p, _p, _i32, _p]),
     "ifmm_bench_gj_inverse": (_i32, [_p, _p, _i32, _i32, _p]),
     "ifmm_test_gemm": (_i32, [_i32, _i32, _i32, _i32, _i32, _d, _p, _i32, _p, _i32, _d, _p, _i32, _i32]),

@@ -997,10 +997,10 @@ __global__ void __launch_bounds__(GTHREADS, 3) gj_update_v2_kernel(const MatDesc
 }
 
 void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
-                        Staging& st, cudaStream_t s, const GjSide* side) {
+                        Staging& st, cudaStream_t s, const GjSide* side, int shape_n, int shape_maxm) {
   const int n = int(h.size());
   if (n == 0) return;
-  int maxm = 0;
+  int maxm = shape_maxm;
   for (auto& d : h) maxm = std::max(maxm, d.m);
   // panel variant: registers (one or two rows per thread) up to m = 1024,
   // shared memory beyond (the top-level system)
@@ -1083,7 +1083,7 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
   const bool look = side && side->s && !v1 && !no_la;
   // two-level for large batches (bandwidth-bound updates); few large matrices
   // are panel-latency-bound and keep the one-level look-ahead (measured)
-  if (!v1 && !one_level && variant != 2 && n >= 64) {
+  if (!v1 && !one_level && variant != 2 && std::max(n, shape_n) >= 64) {
     // Two-level blocking: an outer panel of 2b columns is processed as two
     // inner panels (each inner step updates only the other inner panel), then
     // the rest of the matrix gets ONE rank-2b update with the processed outer

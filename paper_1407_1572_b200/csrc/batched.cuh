@@ -77,7 +77,11 @@ struct GjSide {
     if (s) cudaStreamDestroy(s);
   }
 };
+// shape_n / shape_maxm (sharded runs): count and largest size of the whole
+// colour batch across ranks -- the blocking scheme is chosen from them, so
+// each matrix is inverted with the same arithmetic as on one GPU
 void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
-                        Staging& st, cudaStream_t s, const GjSide* side = nullptr);
+                        Staging& st, cudaStream_t s, const GjSide* side = nullptr, int shape_n = 0,
+                        int shape_maxm = 0);
 
 }  // namespace ifmm

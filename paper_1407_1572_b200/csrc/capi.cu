@@ -4,6 +4,7 @@
 #include <string>
 
 #include "../../include/ifmm_b200.h"
+#include "comm.cuh"
 #include "core.cuh"
 #include "compress.cuh"
 #include "cta_la.cuh"
@@ -33,6 +34,7 @@ using ifmm::upload;
 struct ifmm_tree { TreeH* h; };
 struct ifmm_store { StoreH* h; };
 struct ifmm_factor { FactorH* h; };
+struct ifmm_comm { std::shared_ptr<ifmm::Comm> h; };
 
 namespace ifmm {
 void matvec_release(StoreH* S);
@@ -277,6 +279,134 @@ int ifmm_factor_timing_level(const ifmm_factor* f, int level, double* ms9) {
 }
 
 int64_t ifmm_launch_count(void) { return ifmm::launch_counter().load(); }
+
+// ---------------------------------------------------------------- sharded
+int ifmm_comm_nccl_unique_id(uint8_t* out128) {
+  return guard([&] {
+    if (!out128) invalid("null output");
+    ifmm::nccl_unique_id(out128);
+  });
+}
+
+int ifmm_comm_nccl_version(int* version) {
+  return guard([&] { *version = ifmm::nccl_version(); });
+}
+
+int ifmm_comm_nccl_init(const uint8_t* id128, int nranks, int rank, ifmm_comm** out) {
+  return guard([&] {
+    if (!id128 || !out) invalid("null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) invalid("bad rank / nranks");
+    ensure_device();
+    *out = new ifmm_comm{std::make_shared<ifmm::NcclComm>(id128, nranks, rank)};
+  });
+}
+
+void ifmm_comm_free(ifmm_comm* c) { delete c; }
+
+int ifmm_comm_selftest(ifmm_comm* c, int64_t n, int32_t* ok) {
+  return guard([&] {
+    if (!c || n < 1) invalid("bad argument");
+    ifmm::Comm& C = *c->h;
+    const int me = C.rank(), P = C.size();
+    cudaStream_t s = default_stream();
+    Arena ws(size_t(16) << 20);
+    std::vector<double> h(static_cast<size_t>(n));
+    for (int64_t u = 0; u < n; u++) h[u] = 1000.0 * me + double(u);
+    double* a = ws.alloc_n<double>(size_t(n));
+    double* g = ws.alloc_n<double>(size_t(n) * P);
+    double* r = ws.alloc_n<double>(size_t(n));
+    CK(cudaMemcpyAsync(a, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    C.allgather(a, g, sizeof(double) * n, s);
+    const int to = (me + 1) % P, from = (me + P - 1) % P;
+    C.exchange({ifmm::Msg{to, a, sizeof(double) * n}}, {ifmm::Msg{from, r, sizeof(double) * n}}, s);
+    std::vector<double> hg(static_cast<size_t>(n) * P), hr(static_cast<size_t>(n));
+    CK(cudaMemcpyAsync(hg.data(), g, sizeof(double) * hg.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hr.data(), r, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    bool good = true;
+    for (int q = 0; q < P; q++)
+      for (int64_t u = 0; u < n; u++) good &= hg[size_t(q) * n + u] == 1000.0 * q + double(u);
+    for (int64_t u = 0; u < n; u++) good &= hr[u] == 1000.0 * from + double(u);
+    *ok = good ? 1 : 0;
+  });
+}
+
+int ifmm_factorize_sharded(ifmm_store* s, ifmm_comm* c, double tol, int flags, double cond_limit,
+                           ifmm_factor** out) {
+  return guard([&] {
+    if (!s || !c || !out) invalid("null handle");
+    FactorH* h = ifmm::factorize_sharded(s->h, c->h, tol, flags, cond_limit);
+    *out = new ifmm_factor{h};
+  });
+}
+
+int ifmm_factorize_emulated(ifmm_store* s, int nranks, double tol, int flags, double cond_limit,
+                            ifmm_factor** out) {
+  return guard([&] {
+    if (!s || !out) invalid("null handle");
+    std::vector<FactorH*> v;
+    ifmm::factorize_emulated(s->h, nranks, tol, flags, cond_limit, v);
+    for (int r = 0; r < nranks; r++) out[r] = new ifmm_factor{v[r]};
+  });
+}
+
+int ifmm_solve_emulated(ifmm_factor** f, int nranks, const double* rhs, double* x, int64_t nrhs, int ptr_kind) {
+  return guard([&] {
+    if (!f || nranks < 1) invalid("null handle");
+    std::vector<FactorH*> v;
+    std::vector<double*> xs;
+    const int64_t n = f[0]->h->tree->N;
+    for (int r = 0; r < nranks; r++) {
+      v.push_back(f[r]->h);
+      xs.push_back(x + size_t(r) * n * nrhs);
+    }
+    ifmm::solve_emulated(v, rhs, xs, nrhs, ptr_kind == IFMM_PTR_DEVICE);
+  });
+}
+
+int ifmm_factor_shard_info(const ifmm_factor* f, int32_t* rank_nranks, double* out4) {
+  return guard([&] {
+    const FactorH* h = f->h;
+    const bool d = h->comm && h->comm->size() > 1;
+    if (rank_nranks) {
+      rank_nranks[0] = d ? h->comm->rank() : 0;
+      rank_nranks[1] = d ? h->comm->size() : 1;
+    }
+    if (out4) {
+      out4[0] = h->halo_bytes;
+      out4[1] = h->meta_bytes;
+      out4[2] = double(h->exchanges);
+      out4[3] = h->phase_ms[ifmm::PH_COMM];
+    }
+  });
+}
+
+int ifmm_partition_halo_counts(int dim, int depth, int level, int nranks, int rank, int colour, int32_t* send,
+                               int32_t* recv) {
+  return guard([&] {
+    if (level < 2 || level > depth) invalid("level out of range");
+    const ifmm::Partition P = ifmm::make_partition_geometric(dim, depth, nranks, rank);
+    std::vector<int> s, r;
+    ifmm::halo_plan_counts(P, level, colour, s, r);
+    for (int q = 0; q < nranks; q++) {
+      send[q] = s[q];
+      recv[q] = r[q];
+    }
+  });
+}
+
+int ifmm_partition(int dim, int depth, int level, int nranks, int32_t* owner, uint8_t* held) {
+  return guard([&] {
+    if (level < 2 || level > depth) invalid("level out of range");
+    const ifmm::Partition P = ifmm::make_partition_geometric(dim, depth, nranks, 0);
+    const int nc = 1 << (dim * level);
+    for (int i = 0; i < nc; i++) {
+      if (owner) owner[i] = P.owner[level][i];
+      if (held)
+        for (int s = 0; s < nranks; s++) held[size_t(s) * nc + i] = P.held[level][s][i];
+    }
+  });
+}
 
 int ifmm_solve(ifmm_factor* f, const double* rhs, double* x, int64_t nrhs, int ptr_kind) {
   return guard([&] { ifmm::solve(f->h, rhs, x, nrhs, ptr_kind == IFMM_PTR_DEVICE); });

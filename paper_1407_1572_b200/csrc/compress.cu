@@ -622,6 +622,8 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     MX = std::max(MX, std::max(D.n_p, D.n_q));
   }
   MX = std::max(MX, std::max(MR, MC));
+  MX = std::max(MX, cb.shape_mx);
+  const int nf_shape = std::max(nf, cb.shape_nf);
   // Worker shape.  Fine levels (thousands of fills of a few dozen rows): one
   // warp per fill / chain / pivot, 4 warps per CTA -- no block barriers and
   // many fills in flight per SM.  Coarse levels (few, large fills): one wide
@@ -637,7 +639,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   static const int bs_big_env = getenv("IFMM_BS_BIG") ? atoi(getenv("IFMM_BS_BIG")) : 0;  // tuning override
   const int bs_big = bs_big_env ? bs_big_env : (MX >= 700 ? 1024 : 512);
   static const int nf_big = getenv("IFMM_K1_NF_BIG") ? atoi(getenv("IFMM_K1_NF_BIG")) : 2048;  // tuning
-  const int bs_fill = narrow ? 128 : (MX >= 256 && nf < nf_big) ? bs_big : (MX >= 128 ? 256 : bs_small);
+  const int bs_fill = narrow ? 128 : (MX >= 256 && nf_shape < nf_big) ? bs_big : (MX >= 128 ? 256 : bs_small);
   // level-6-sized bases (256 <= MX < 400): 256-thread chains measured best (112 -> 102 ms)
   static const int bs_mid = getenv("IFMM_BS_MID") ? atoi(getenv("IFMM_BS_MID")) : 256;
   const int bs_dirs = narrow ? 128

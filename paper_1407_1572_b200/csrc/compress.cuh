@@ -45,6 +45,10 @@ struct CompressBatch {
   std::vector<int> p2p_off, p2p;      // per pivot P2P fills (sorted)
   std::vector<int> chain_q;           // q of each chain
   const int* rank_host = nullptr;     // host copy of the level's ranks at batch start
+  // sharded runs: largest fill dimension and fill count of the whole colour
+  // batch across ranks; worker shapes are chosen from them so every fill is
+  // compressed with the same arithmetic as on one GPU
+  int shape_mx = 0, shape_nf = 0;
 };
 
 // Runs K1..K4 on stream s.  rank: device ranks of the level (updated);

@@ -148,7 +148,14 @@ struct BatchH {
   int level, colour, rec0, rec1;
   const RecordH* d_recs;  // device copy of records[rec0..rec1)
   int maxn, maxw;
+  // sharded solve: solve-vector runs (base, length) each rank writes in the
+  // forward / backward sweep of this batch, rank-major with offsets
+  std::vector<int64_t> fwd_runs, bwd_runs;  // pairs
+  std::vector<int> fwd_off, bwd_off;        // nranks + 1, in pairs
 };
+
+class Comm;
+struct Partition;
 
 struct FactorH {
   StoreH* store = nullptr;
@@ -177,6 +184,16 @@ struct FactorH {
   int deferred_batches = 0;  // colour batches split by the independence guard
   std::vector<std::array<double, 8>> phase_lvl_ms;  // [level][phase]
   std::vector<std::array<double, 2>> host_lvl_ms;   // [level]: host busy until the final sync, time blocked in it
+  // sharded factorization (null / 1 rank otherwise): the communicator the
+  // solve reuses, this rank's partition, private workspaces and stream of an
+  // emulated rank (LocalComm), traffic counters
+  std::shared_ptr<Comm> comm;
+  std::shared_ptr<Partition> part;
+  std::unique_ptr<FactorWork> own_work;
+  bool own_stream = false;
+  double halo_bytes = 0, meta_bytes = 0;
+  long long exchanges = 0;
+  ~FactorH();
 };
 
 enum PhaseId : int {
@@ -188,6 +205,7 @@ enum PhaseId : int {
   PH_TRANSITION = 5, // level start (parent near field, bases)
   PH_TOP = 6,        // top-level inverse
   PH_COUNT = 7,
+  PH_COMM = 7,       // sharded runs: metadata all-gathers + halo pack/exchange/unpack
 };
 constexpr int IFMM_FLAG_TIMING = 1;
 
@@ -196,6 +214,13 @@ TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_
 StoreH* store_init(TreeH* t, const KernelParams& kp, int p, double tol, const int* probe_tab, int probe_maxm);
 void matvec(StoreH* s, const double* x, double* y, int64_t nrhs, bool device_ptr);
 FactorH* factorize(StoreH* s, double tol, int flags, double cond_limit);
+// collective over `comm` (one call per rank, same store contents on every rank)
+FactorH* factorize_sharded(StoreH* s, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit);
+// `nranks` virtual ranks as threads on the current GPU (LocalComm): out[r] is rank r's factorization
+void factorize_emulated(StoreH* s, int nranks, double tol, int flags, double cond_limit, std::vector<FactorH*>& out);
+// solve on every virtual rank of an emulated factorization; x[r] is rank r's solution
+void solve_emulated(const std::vector<FactorH*>& f, const double* rhs, const std::vector<double*>& x, int64_t nrhs,
+                    bool device_ptr);
 void solve(FactorH* f, const double* rhs, double* x, int64_t nrhs, bool device_ptr);
 void solve_refined(FactorH* F, StoreH* S, const double* rhs, double* x, int64_t nrhs, bool device_ptr, int iters,
                    double target, double* hist, int* done);

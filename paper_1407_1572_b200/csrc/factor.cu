@@ -19,11 +19,21 @@
 //   (ACA + QR/SVD recompression, new directions, basis augmentation, M2L
 //   absorption).
 // * The level-2 M2L system is inverted densely.
+// * Sharded (comm.cuh): with a communicator every rank replays the
+//   whole host schedule (partners, presence, fill lists, ranks -- replicated
+//   metadata) but runs the device work of its own subtrees' pivots only.  A
+//   rank stores the blocks touching clusters within one cell of its own;
+//   after each colour batch the writer of a block ships it to every other
+//   rank that stores it (and the batch's fill outcomes / new ranks are
+//   all-gathered), so every stored copy is current before it is read.
 #include <algorithm>
+#include <climits>
+#include <thread>
 #include <chrono>
 #include <cmath>
 
 #include "core.cuh"
+#include "comm.cuh"
 #include "compress.cuh"
 #include "cta_la.cuh"
 
@@ -114,15 +124,19 @@ struct PhaseTimer {
 
 class Factorizer {
  public:
-  Factorizer(StoreH* S, double tol, int flags, double cond_limit)
+  Factorizer(StoreH* S, FactorWork* work, cudaStream_t s, std::shared_ptr<Comm> comm, double tol, int flags,
+             double cond_limit)
       : S_(S),
         t_(S->tree),
         tol_(tol),
         flags_(flags),
         cond_limit_(cond_limit),
-        ws_(S->work->ws),
-        st_(S->work->st),
-        lvl_arena_(S->work->lvl) {}
+        s_(s),
+        ws_(work->ws),
+        st_(work->st),
+        lvl_arena_(work->lvl),
+        work_(work),
+        comm_(std::move(comm)) {}
   FactorH* run();
 
  private:
@@ -136,6 +150,10 @@ class Factorizer {
   Arena& ws_;
   Staging& st_;
   Arena* lvl_arena_;  // [2], alternating between levels
+  FactorWork* work_;
+  std::shared_ptr<Comm> comm_;          // null: one GPU
+  std::shared_ptr<Partition> part_;     // subtree partition (sharded runs)
+  int rank_ = 0, nranks_ = 1;
   PhaseTimer tm_;
   WorkLevel cur_, prev_;
   // debug (IFMM_HOST_PROF): host ms per section of eliminate_batch, per level
@@ -150,6 +168,13 @@ class Factorizer {
   struct SlotRef { int kind, j, dim; };  // kind 0: x_j, 1: y_j
   std::vector<std::vector<SlotRef>> rec_slots_;
 
+  // ownership (sharded runs; everything is mine / held on one GPU)
+  bool mine(const WorkLevel& W, int i) const { return nranks_ == 1 || part_->owner[W.k][i] == rank_; }
+  int owner(const WorkLevel& W, int i) const { return nranks_ == 1 ? 0 : part_->owner[W.k][i]; }
+  bool holds(const WorkLevel& W, int s, int i) const { return nranks_ == 1 || part_->held[W.k][s][i]; }
+  bool holds1(const WorkLevel& W, int i) const { return holds(W, rank_, i); }
+  bool holds2(const WorkLevel& W, int a, int b) const { return holds(W, rank_, a) || holds(W, rank_, b); }
+  bool holds2s(const WorkLevel& W, int s, int a, int b) const { return holds(W, s, a) || holds(W, s, b); }
   // level arenas hand out zeroed memory (slabs are cleared on creation/reset)
   double* zalloc(WorkLevel& W, size_t n) { return W.arena->alloc_n<double>(std::max<size_t>(1, n)); }
   BlkRef p2p_ref(WorkLevel& W, int i, int j, bool alloc) {
@@ -157,7 +182,7 @@ class Factorizer {
     int sl = W.T->slot(a, b);
     if (sl < 0) invalid("near-field block beyond the 7x7 window (dense fill too far)");
     double*& p = W.p2p[size_t(a) * W.win + sl];
-    if (!p && alloc) p = zalloc(W, size_t(W.n[a]) * W.n[b]);
+    if (!p && alloc && holds2(W, a, b)) p = zalloc(W, size_t(W.n[a]) * W.n[b]);
     return {p, W.n[a], i > j};
   }
   BlkRef m2l_ref(WorkLevel& W, int i, int j, bool alloc) {
@@ -165,14 +190,14 @@ class Factorizer {
     int sl = W.T->slot(a, b);
     if (sl < 0) invalid("M2L block beyond the 7x7 window");
     double*& p = W.m2l[size_t(a) * W.win + sl];
-    if (!p && alloc) p = zalloc(W, size_t(W.rcap[a]) * W.rcap[b]);
+    if (!p && alloc && holds2(W, a, b)) p = zalloc(W, size_t(W.rcap[a]) * W.rcap[b]);
     return {p, W.rcap[a], i > j};
   }
   BlkRef xy_ref(WorkLevel& W, int i, int j, bool alloc) {
     int sl = W.T->slot(i, j);
     if (sl < 0) invalid("hybrid block beyond the 7x7 window");
     double*& p = W.xy[size_t(i) * W.win + sl];
-    if (!p && alloc) p = zalloc(W, size_t(W.n[i]) * W.rcap[j]);
+    if (!p && alloc && holds2(W, i, j)) p = zalloc(W, size_t(W.n[i]) * W.rcap[j]);
     return {p, W.n[i], false};
   }
   uint8_t& pres(std::vector<uint8_t>& v, WorkLevel& W, int i, int j) {
@@ -224,6 +249,25 @@ class Factorizer {
   void eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred);
   void finish_level(int rec_begin);
   void factor_top();
+  // sharded runs: one block (or the new columns of a basis) a batch or a
+  // transition wrote, shipped from its writer to every other rank storing it
+  enum HaloKind : int { HALO_P2P = 0, HALO_XY = 1, HALO_M2L = 2, HALO_U = 3 };
+  struct HaloItem {
+    int kind, a, b, c0;  // P2P / M2L: (a <= b); XY: (x-cluster a, eliminated b); U: cluster a, columns c0..r_a
+  };
+  struct HaloRef {
+    double* p;
+    int ld, rows, cols;
+  };
+  HaloRef halo_ref(WorkLevel& W, const HaloItem& it);
+  void halo_exchange(WorkLevel& W, const std::vector<std::vector<HaloItem>>& send,
+                     const std::vector<std::vector<HaloItem>>& recv, CopyBatch* local);
+  // solve-vector slots of every pivot of the level (all ranks): (batch, owner, cluster, slots)
+  struct LevelPivot {
+    int batch, owner, i;
+    std::vector<SlotRef> slots;
+  };
+  std::vector<LevelPivot> lvl_piv_;
 };
 
 void Factorizer::start_leaf_level() {
@@ -237,6 +281,7 @@ void Factorizer::start_leaf_level() {
   W.rcap = L.n;
   CopyBatch cb;
   for (int i = 0; i < W.nc; i++) {
+    if (!holds1(W, i)) continue;
     W.U[i] = zalloc(W, size_t(W.n[i]) * W.rcap[i]);
     cb.add(L.U[i], W.n[i], W.U[i], W.n[i], W.n[i], W.r0[i]);
   }
@@ -246,14 +291,14 @@ void Factorizer::start_leaf_level() {
       int j = T.nbr[q];
       if (j < i) continue;
       BlkRef b = p2p_ref(W, i, j, true);
-      cb.add(S_->leaf_p2p[size_t(i) * W.win + T.slot(i, j)], W.n[i], b.p, b.ld, W.n[i], W.n[j]);
+      if (b.p) cb.add(S_->leaf_p2p[size_t(i) * W.win + T.slot(i, j)], W.n[i], b.p, b.ld, W.n[i], W.n[j]);
       set_pp(W, i, j, 1);
     }
     for (int q = T.il_off[i]; q < T.il_off[i + 1]; q++) {
       int j = T.il[q];
       if (j < i) continue;
       BlkRef b = m2l_ref(W, i, j, true);
-      cb.add(L.m2l[q], std::max(1, W.r0[i]), b.p, b.ld, W.r0[i], W.r0[j]);
+      if (b.p) cb.add(L.m2l[q], std::max(1, W.r0[i]), b.p, b.ld, W.r0[i], W.r0[j]);
       set_pm(W, i, j, 1);
     }
   }
@@ -278,6 +323,7 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
   W.rcap = W.n;
   CopyBatch cb;
   for (int i = 0; i < W.nc; i++) {
+    if (!holds1(W, i)) continue;
     W.U[i] = zalloc(W, size_t(W.n[i]) * W.rcap[i]);
     const int n0 = int(L.child_off[size_t(i) * (nch + 1) + nch]);
     for (int c = 0; c < nch; c++) {
@@ -286,6 +332,11 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
       cb.add(L.U[i] + ro, std::max(1, n0), W.U[i] + off[i][c], W.n[i], S_->lv[k + 1].r0[ch], W.r0[i]);
     }
   }
+  // parent near field from the children's M2L blocks (ifmm/solver.py:163-192).
+  // Sharded: a rank assembles P2P(i, j) when it owns i or j (it stores every
+  // child block of its own children); pairs it stores but owns neither end of
+  // come from the owner of min(i, j) -- the transition's halo exchange.
+  std::vector<std::vector<HaloItem>> send(nranks_), recv(nranks_);
   const Topo& T = *W.T;
   for (int i = 0; i < W.nc; i++) {
     for (int q = T.nbr_off[i]; q < T.nbr_off[i + 1]; q++) {
@@ -295,27 +346,45 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
       for (int a = 0; a < nch; a++)
         for (int b = 0; b < nch; b++) any |= pm_present(C, (i << dim) + a, (j << dim) + b);
       if (!any) continue;
+      set_pp(W, i, j, 1);
       BlkRef P = p2p_ref(W, i, j, true);
+      const bool build = mine(W, i) || mine(W, j);
+      if (nranks_ > 1) {
+        const HaloItem it{HALO_P2P, i, j, 0};
+        if (owner(W, i) == rank_) {
+          for (int s = 0; s < nranks_; s++)
+            if (s != rank_ && holds2s(W, s, i, j) && owner(W, i) != s && owner(W, j) != s) send[s].push_back(it);
+        } else if (!build && P.p) {
+          recv[owner(W, i)].push_back(it);
+        }
+      }
+      if (!build || !P.p) continue;
       for (int a = 0; a < nch; a++)
         for (int b = 0; b < nch; b++) {
           const int ca = (i << dim) + a, cbb = (j << dim) + b;
           if (!pm_present(C, ca, cbb)) continue;
           BlkRef M = m2l_ref(C, ca, cbb, false);
-          if (!M.p) continue;
+          if (!M.p) {
+            if (nranks_ > 1) invalid("sharded transition: a child M2L block is not stored on the assembling rank");
+            continue;
+          }
           cb.add(M.p, M.ld, P.p + off[i][a] + size_t(off[j][b]) * P.ld, P.ld, C.r[ca], C.r[cbb], M.trans);
         }
-      set_pp(W, i, j, 1);
     }
     for (int q = T.il_off[i]; q < T.il_off[i + 1]; q++) {
       int j = T.il[q];
       if (j < i) continue;
       BlkRef b = m2l_ref(W, i, j, true);
-      cb.add(L.m2l[q], std::max(1, W.r0[i]), b.p, b.ld, W.r0[i], W.r0[j]);
+      if (b.p) cb.add(L.m2l[q], std::max(1, W.r0[i]), b.p, b.ld, W.r0[i], W.r0[j]);
       set_pm(W, i, j, 1);
     }
   }
   CK(cudaMemcpyAsync(W.d_rank, W.r.data(), sizeof(int) * W.nc, cudaMemcpyHostToDevice, s_));
   launch_copies(cb, ws_, st_, s_);
+  if (nranks_ > 1) {
+    tm_.begin(PH_COMM);
+    halo_exchange(W, send, recv, nullptr);
+  }
 }
 
 void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred) {
@@ -324,6 +393,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   WorkLevel& W = cur_;
   const Topo& T = *W.T;
   const int k = W.k;
+  const bool dist = nranks_ > 1;
   // Independence guard: a batch may only contain eliminations whose touched
   // sets {i} u partners(i) are pairwise disjoint (true for the 9-colouring as
   // long as every partner is a neighbour; an incompressible well-separated
@@ -359,14 +429,19 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   hmark(1);
   struct PivInfo {
     int i, n, r, m, w;
+    bool own;
     std::vector<int> xp, yp;
     std::vector<int> soff;  // slot column offsets (size nslots+1)
     double *S, *C, *Xb;
     int rec;
   };
+  // every rank walks all pivots of the batch (metadata); device work is done
+  // for its own pivots only (all of them on one GPU)
   std::vector<PivInfo> P(np);
+  std::vector<int> own;  // indices into P
   CopyBatch cb;
-  std::vector<MatDesc> md(np);
+  std::vector<MatDesc> md;
+  const int batch_id = int(F_->batches.size());
   for (int t = 0; t < np; t++) {
     PivInfo& I = P[t];
     const int i = piv[t];
@@ -374,17 +449,36 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     I.n = W.n[i];
     I.r = W.r[i];
     I.m = I.n + I.r;
+    I.own = mine(W, i);
     partners(W, i, I.xp, I.yp);
     I.soff.assign(1, 0);
     for (int j : I.xp) I.soff.push_back(I.soff.back() + W.n[j]);
     for (int j : I.yp) I.soff.push_back(I.soff.back() + W.r[j]);
     I.soff.push_back(I.soff.back() + I.r);
     I.w = I.soff.back();
+    I.rec = -1;
+    if (dist) {
+      LevelPivot lp{batch_id, owner(W, i), i, {}};
+      for (int j : I.xp) lp.slots.push_back({0, j, W.n[j]});
+      for (int j : I.yp) lp.slots.push_back({1, j, W.r[j]});
+      lp.slots.push_back({1, i, I.r});
+      lvl_piv_.push_back(std::move(lp));
+    }
+    if (!I.own) continue;
+    if (dist) {
+      bool ok = holds1(W, i);
+      for (int j : I.xp) ok &= holds1(W, j);
+      for (int j : I.yp) ok &= holds1(W, j);
+      if (!ok)
+        invalid("sharded factorization: a pivot couples to a cluster more than one cell away (a dense "
+                "well-separated fill); factorize this system on one GPU");
+    }
+    own.push_back(t);
     I.S = ws_.alloc_n<double>(size_t(I.m) * I.m);
     I.C = ws_.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
     I.Xb = ws_.alloc_n<double>(size_t(std::max(1, I.r)) * I.w);
     int* ipiv = ws_.alloc_n<int>(I.m);
-    md[t] = MatDesc{I.S, I.m, I.m, ipiv, i};
+    md.push_back(MatDesc{I.S, I.m, I.m, ipiv, i});
     // gather S
     BlkRef Pii = p2p_ref(W, i, i, true);
     cb.add(Pii.p, Pii.ld, I.S, I.m, I.n, I.n);
@@ -405,32 +499,38 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     }
     cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
   }
+  const int no = int(own.size());
   hmark(2);
   tm_.begin(PH_GATHER);
   launch_copies(cb, ws_, st_, s_);
   static const char* dump_dir = getenv("IFMM_DUMP_SINGULAR");
   std::vector<double*> Sbak;
   if (dump_dir)
-    for (int t = 0; t < np; t++) {
-      Sbak.push_back(ws_.alloc_n<double>(size_t(P[t].m) * P[t].m));
-      CK(cudaMemcpyAsync(Sbak.back(), P[t].S, sizeof(double) * P[t].m * P[t].m, cudaMemcpyDeviceToDevice, s_));
+    for (int u = 0; u < no; u++) {
+      const PivInfo& I = P[own[u]];
+      Sbak.push_back(ws_.alloc_n<double>(size_t(I.m) * I.m));
+      CK(cudaMemcpyAsync(Sbak.back(), I.S, sizeof(double) * I.m * I.m, cudaMemcpyDeviceToDevice, s_));
     }
-  const MatDesc* dmd = upload(ws_, md, s_, st_);
-  double* d_nS = ws_.alloc_n<double>(np);
-  double* d_nSi = ws_.alloc_n<double>(np);
-  int* d_info = ws_.alloc_n<int>(np);
-  int maxm = 0;
-  for (auto& d : md) maxm = std::max(maxm, d.m);
-  tm_.begin(PH_GJ);
-  launch_norm1(dmd, np, maxm, d_nS, s_);
-  S_->work->gj_side.ensure();
-  batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &S_->work->gj_side);
-  launch_norm1(dmd, np, maxm, d_nSi, s_);
-  launch_norm1_estimate(dmd, np, maxm, d_nSi, d_nS, cond_limit_, s_);
+  double* d_nS = ws_.alloc_n<double>(std::max(1, no));
+  double* d_nSi = ws_.alloc_n<double>(std::max(1, no));
+  int* d_info = ws_.alloc_n<int>(std::max(1, no));
+  if (no > 0) {
+    const MatDesc* dmd = upload(ws_, md, s_, st_);
+    int maxm = 0;
+    for (auto& d : md) maxm = std::max(maxm, d.m);
+    tm_.begin(PH_GJ);
+    launch_norm1(dmd, no, maxm, d_nS, s_);
+    work_->gj_side.ensure();
+    int gmaxm = 0;  // whole batch across ranks (blocking scheme as on one GPU)
+    for (const PivInfo& I : P) gmaxm = std::max(gmaxm, I.m);
+    batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &work_->gj_side, np, gmaxm);
+    launch_norm1(dmd, no, maxm, d_nSi, s_);
+    launch_norm1_estimate(dmd, no, maxm, d_nSi, d_nS, cond_limit_, s_);
+  }
   hmark(3);
   // records + X = S^-1 C
   GemmBatch gb;
-  for (int t = 0; t < np; t++) {
+  for (int t : own) {
     PivInfo& I = P[t];
     RecordH R{};
     R.level = k;
@@ -467,15 +567,17 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   launch_grouped_gemm(gb, false, false, ws_, st_, s_);
   tm_.end();
   // symmetric Schur update on the block upper triangle: target -= C_a^T X_b,
-  // one concatenated product per pivot (IFMM_SCHUR_GROUPED: one GEMM per block)
+  // one concatenated product per pivot (IFMM_SCHUR_GROUPED: one GEMM per block).
+  // Targets are created (presence + storage) for every pivot of the batch on
+  // every rank that stores them; only the owner computes.
   static const bool per_block = getenv("IFMM_SCHUR_GROUPED") != nullptr;
   SchurBatch sbat;
   for (int t = 0; t < np; t++) {
     PivInfo& I = P[t];
-    const RecordH& R = F_->recs[I.rec];
     const int nx = int(I.xp.size()), ny = int(I.yp.size());
     const int ns = nx + ny + 1;
-    const int pv = per_block ? -1 : sbat.begin_pivot(I.C, R.xtop, I.n, I.soff);
+    const RecordH* R = I.own ? &F_->recs[I.rec] : nullptr;
+    const int pv = (per_block || !I.own) ? -1 : sbat.begin_pivot(I.C, R->xtop, I.n, I.soff);
     auto slot_cluster = [&](int s) { return s < nx ? I.xp[s] : (s < nx + ny ? I.yp[s - nx] : I.i); };
     for (int a = 0; a < ns; a++)
       for (int b = a; b < ns; b++) {
@@ -484,7 +586,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         const int da = I.soff[a + 1] - I.soff[a], db = I.soff[b + 1] - I.soff[b];
         if (a == ns - 1 && b == ns - 1) {
           BlkRef M = m2l_ref(W, I.i, I.i, true);
-          cb.add(I.Xb + size_t(I.soff[b]) * I.r, I.r, M.p, M.ld, I.r, I.r, false, 1.0, true);
+          if (I.own) cb.add(I.Xb + size_t(I.soff[b]) * I.r, I.r, M.p, M.ld, I.r, I.r, false, 1.0, true);
           pres(W.pm, W, I.i, I.i) = 1;
           continue;
         }
@@ -499,15 +601,15 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
           tgt = m2l_ref(W, ja, jb, true);
           set_pm(W, ja, jb, 1);
         }
-        if (da == 0 || db == 0) continue;
+        if (da == 0 || db == 0 || !I.own) continue;
         F_->fl_schur += 2.0 * I.n * da * db;
         if (per_block)
-          gb.add(I.C + size_t(I.soff[a]) * I.n, I.n, R.xtop + size_t(I.soff[b]) * I.n, I.n, tgt.p, tgt.ld, da, db,
+          gb.add(I.C + size_t(I.soff[a]) * I.n, I.n, R->xtop + size_t(I.soff[b]) * I.n, I.n, tgt.p, tgt.ld, da, db,
                  I.n, -1.0, 1.0, tgt.trans);
         else
           sbat.set_target(pv, a, b, tgt.p, tgt.ld, tgt.trans);
       }
-    if (!per_block) sbat.finish_pivot(pv);
+    if (!per_block && I.own) sbat.finish_pivot(pv);
   }
   tm_.begin(PH_SCHUR);
   if (per_block) launch_grouped_gemm(gb, true, false, ws_, st_, s_);
@@ -516,13 +618,20 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   launch_copies(cb, ws_, st_, s_);
   tm_.end();
   hmark(4);
-  // fill-in compression (reference order: hybrid pairs sorted, then P2P pairs sorted)
+  // fill-in compression (reference order: hybrid pairs sorted, then P2P pairs
+  // sorted).  The fill list covers every pivot (its outcomes drive the
+  // replicated presence flags); only own pivots' fills are compressed here.
   CompressBatch cbz;
   cbz.chain_off.assign(1, 0);
   cbz.p2p_off.assign(1, 0);
-  struct FillHost { int kind, p, q; };
+  struct FillHost { int kind, p, q, piv, dev; };  // dev: index into cbz.fills or -1
   std::vector<FillHost> fh;
-  auto add_fill = [&](int kind, int p, int q) {
+  auto add_fill = [&](int kind, int p, int q, int t) {
+    BlkRef M = m2l_ref(W, p, q, true);
+    if (!P[t].own) {
+      fh.push_back({kind, p, q, t, -1});
+      return -1;
+    }
     FillDesc D{};
     D.kind = kind;
     D.p = p;
@@ -545,25 +654,29 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     D.n_q = W.n[q];
     D.Up = W.U[p];
     D.Uq = W.U[q];
-    BlkRef M = m2l_ref(W, p, q, true);
     D.M = M.p;
     D.ldM = M.ld;
     D.transM = M.trans ? 1 : 0;
     D.Kf = std::max(1, std::min(96, std::min(D.rows, D.cols)));
     D.out = ws_.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
     cbz.fills.push_back(D);
-    fh.push_back({kind, p, q});
+    fh.push_back({kind, p, q, t, int(cbz.fills.size()) - 1});
     return int(cbz.fills.size()) - 1;
   };
+  std::vector<int> fill_off(np + 1, 0);  // fills of pivot t: fh[fill_off[t] .. fill_off[t+1])
   for (int t = 0; t < np; t++) {
     PivInfo& I = P[t];
+    fill_off[t] = int(fh.size());
     std::vector<int> ps(I.yp);
     ps.push_back(I.i);
     std::sort(ps.begin(), ps.end());
     std::vector<std::vector<int>> byq(I.xp.size());
     for (int p : ps)
       for (size_t u = 0; u < I.xp.size(); u++)
-        if (T.in_il(p, I.xp[u])) byq[u].push_back(add_fill(FILL_HYBRID, p, I.xp[u]));
+        if (T.in_il(p, I.xp[u])) {
+          const int f = add_fill(FILL_HYBRID, p, I.xp[u], t);
+          if (f >= 0) byq[u].push_back(f);
+        }
     for (size_t u = 0; u < I.xp.size(); u++)
       if (!byq[u].empty()) {
         cbz.chain.insert(cbz.chain.end(), byq[u].begin(), byq[u].end());
@@ -572,10 +685,19 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       }
     for (size_t a = 0; a < I.xp.size(); a++)
       for (size_t b = a + 1; b < I.xp.size(); b++)
-        if (T.in_il(I.xp[a], I.xp[b])) cbz.p2p.push_back(add_fill(FILL_P2P, I.xp[a], I.xp[b]));
-    cbz.p2p_off.push_back(int(cbz.p2p.size()));
+        if (T.in_il(I.xp[a], I.xp[b])) {
+          const int f = add_fill(FILL_P2P, I.xp[a], I.xp[b], t);
+          if (f >= 0) cbz.p2p.push_back(f);
+        }
+    if (I.own) cbz.p2p_off.push_back(int(cbz.p2p.size()));
   }
+  fill_off[np] = int(fh.size());
   cbz.rank_host = W.r.data();
+  for (const FillHost& h : fh) {  // worker shapes from the whole batch across ranks
+    const int rows = h.kind == FILL_HYBRID ? W.r[h.p] : W.n[h.p];
+    cbz.shape_mx = std::max(cbz.shape_mx, std::max(std::max(W.n[h.p], W.n[h.q]), std::max(rows, W.n[h.q])));
+  }
+  cbz.shape_nf = int(fh.size());
   const size_t nfill = cbz.fills.size();
   FillState* d_state = ws_.alloc_n<FillState>(std::max<size_t>(1, nfill));
   int* d_stats = ws_.alloc_n<int>(4);
@@ -583,17 +705,21 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
   hmark(5);
   tm_.begin(PH_COMPRESS);
-  run_compression(cbz, tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_state, d_stats, ws_, st_, s_, dbg ? 1 : 0);
+  if (nfill) run_compression(cbz, tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_state, d_stats, ws_, st_, s_, dbg ? 1 : 0);
   tm_.end();
   hmark(6);
   // read back: pivot conditioning, ranks, fill outcomes, counters
   const auto t_sync0 = std::chrono::steady_clock::now();
-  std::vector<double> nS(np), nSi(np);
-  std::vector<int> info(np), stats(4);
+  std::vector<double> nS(no), nSi(no);
+  std::vector<int> info(no), stats(4);
   std::vector<FillState> state(nfill);
-  CK(cudaMemcpyAsync(nS.data(), d_nS, sizeof(double) * np, cudaMemcpyDeviceToHost, s_));
-  CK(cudaMemcpyAsync(nSi.data(), d_nSi, sizeof(double) * np, cudaMemcpyDeviceToHost, s_));
-  CK(cudaMemcpyAsync(info.data(), d_info, sizeof(int) * np, cudaMemcpyDeviceToHost, s_));
+  std::vector<int> r_before;
+  if (dist) r_before = W.r;
+  if (no) {
+    CK(cudaMemcpyAsync(nS.data(), d_nS, sizeof(double) * no, cudaMemcpyDeviceToHost, s_));
+    CK(cudaMemcpyAsync(nSi.data(), d_nSi, sizeof(double) * no, cudaMemcpyDeviceToHost, s_));
+    CK(cudaMemcpyAsync(info.data(), d_info, sizeof(int) * no, cudaMemcpyDeviceToHost, s_));
+  }
   if (nfill) CK(cudaMemcpyAsync(state.data(), d_state, sizeof(FillState) * nfill, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(stats.data(), d_stats, 16, cudaMemcpyDeviceToHost, s_));
   CK(cudaMemcpyAsync(W.r.data(), W.d_rank, sizeof(int) * W.nc, cudaMemcpyDeviceToHost, s_));
@@ -606,52 +732,213 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   if (getenv("IFMM_COND_LOG")) {
     double mx = 0, sum = 0;
     int imx = -1, mmx = 0;
-    for (int t = 0; t < np; t++) {
-      double c = nS[t] * nSi[t];
+    for (int u = 0; u < no; u++) {
+      double c = nS[u] * nSi[u];
       sum += std::log10(std::max(c, 1.0));
-      if (c > mx) { mx = c; imx = P[t].i; mmx = P[t].m; }
+      if (c > mx) { mx = c; imx = P[own[u]].i; mmx = P[own[u]].m; }
     }
-    fprintf(stderr, "cond level=%d colour=%d pivots=%d max=%.3e (cluster %d, m=%d) geo-mean=%.3e\n", k, colour, np, mx,
-            imx, mmx, std::pow(10.0, sum / np));
+    fprintf(stderr, "cond level=%d colour=%d pivots=%d max=%.3e (cluster %d, m=%d) geo-mean=%.3e\n", k, colour, no, mx,
+            imx, mmx, std::pow(10.0, no ? sum / no : 0.0));
   }
-  for (int t = 0; t < np; t++) {
-    double rc = (info[t] != 0) ? 0.0 : 1.0 / (nS[t] * nSi[t]);
+  // first numerically singular own pivot (batch position), if any
+  int err_pos = INT_MAX, err_index = -1;
+  double err_cond = 0;
+  for (int u = 0; u < no; u++) {
+    const PivInfo& I = P[own[u]];
+    double rc = (info[u] != 0) ? 0.0 : 1.0 / (nS[u] * nSi[u]);
     if (!std::isfinite(rc) || rc <= 1.0 / cond_limit_) {
-      double cond = 1.0 / std::max(rc, 1e-300);
+      err_pos = own[u];
+      err_index = I.i;
+      err_cond = 1.0 / std::max(rc, 1e-300);
       if (dump_dir) {
-        std::vector<double> h(size_t(P[t].m) * P[t].m);
-        CK(cudaMemcpy(h.data(), Sbak[t], sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
-        std::string fn = std::string(dump_dir) + "/S_" + std::to_string(k) + "_" + std::to_string(P[t].i) + ".bin";
+        std::vector<double> h(size_t(I.m) * I.m);
+        CK(cudaMemcpy(h.data(), Sbak[u], sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+        std::string fn = std::string(dump_dir) + "/S_" + std::to_string(k) + "_" + std::to_string(I.i) + ".bin";
         FILE* fp = fopen(fn.c_str(), "wb");
         if (fp) {
-          int hdr[2] = {P[t].n, P[t].r};
+          int hdr[2] = {I.n, I.r};
           fwrite(hdr, sizeof hdr, 1, fp);
           fwrite(h.data(), sizeof(double), h.size(), fp);
           fclose(fp);
         }
       }
-      char buf[256];
-      snprintf(buf, sizeof buf, "pivot for cluster %d at level %d is numerically singular (condition estimate %.2e)",
-               P[t].i, k, cond);
-      throw SingularPivot(k, P[t].i, cond, buf);
+      break;
     }
+  }
+  // fill outcomes in global fill order (-1: another rank's fill)
+  std::vector<int> gstat(fh.size(), -1);
+  for (size_t f = 0; f < fh.size(); f++)
+    if (fh[f].dev >= 0) gstat[f] = state[fh[f].dev].status;
+  if (dist) {
+    // all-gather: first failure, counters, ranks, fill outcomes of every rank
+    tm_.begin(PH_COMM);
+    const size_t L = 8 + size_t(W.nc) + fh.size();
+    std::vector<int> mine_meta(L, 0);
+    mine_meta[0] = err_pos;
+    mine_meta[1] = err_index;
+    memcpy(&mine_meta[2], &err_cond, sizeof(double));
+    mine_meta[4] = stats[0];
+    mine_meta[5] = stats[1];
+    mine_meta[6] = stats[2];
+    std::copy(W.r.begin(), W.r.end(), mine_meta.begin() + 8);
+    std::copy(gstat.begin(), gstat.end(), mine_meta.begin() + 8 + W.nc);
+    int* d_send = upload(ws_, mine_meta, s_, st_);
+    int* d_recv = ws_.alloc_n<int>(L * nranks_);
+    comm_->allgather(d_send, d_recv, L * sizeof(int), s_);
+    std::vector<int> all(L * nranks_);
+    CK(cudaMemcpyAsync(all.data(), d_recv, sizeof(int) * all.size(), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    stats.assign(4, 0);
+    err_pos = INT_MAX;
+    for (int q = 0; q < nranks_; q++) {
+      const int* m = &all[size_t(q) * L];
+      if (m[0] < err_pos) {
+        err_pos = m[0];
+        err_index = m[1];
+        memcpy(&err_cond, &m[2], sizeof(double));
+      }
+      stats[0] += m[4];
+      stats[1] += m[5];
+      stats[2] = std::max(stats[2], m[6]);
+      for (int c = 0; c < W.nc; c++) W.r[c] = std::max(W.r[c], m[8 + c]);  // ranks only grow
+    }
+    for (size_t f = 0; f < fh.size(); f++) gstat[f] = all[size_t(owner(W, P[fh[f].piv].i)) * L + 8 + W.nc + f];
+    CK(cudaMemcpyAsync(W.d_rank, W.r.data(), sizeof(int) * W.nc, cudaMemcpyHostToDevice, s_));
+    F_->meta_bytes += double(L * sizeof(int)) * (nranks_ - 1);
+  }
+  if (err_pos != INT_MAX) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "pivot for cluster %d at level %d is numerically singular (condition estimate %.2e)",
+             err_index, k, err_cond);
+    throw SingularPivot(k, err_index, err_cond, buf);
   }
   LevelStatsH& LS = F_->stats[k];
   LS.compressed += stats[0];
   LS.dense_kept += stats[1];
   LS.max_rank = std::max(LS.max_rank, stats[2]);
+  CopyBatch zero_dropped;  // sharded: stored copies of fills another rank dropped
   for (size_t f = 0; f < fh.size(); f++) {
-    if (dbg)
-      fprintf(stderr, "fill k=%d kind=%d p=%d q=%d status=%d aca=%d rank=%d rank_p=%d\n", k, fh[f].kind, fh[f].p,
-              fh[f].q, state[f].status, state[f].k, state[f].r, W.r[fh[f].p]);
-    if (state[f].status != 0) continue;
     const FillHost& h = fh[f];
-    if (h.kind == FILL_HYBRID) pres(W.px, W, h.q, h.p) = 0;
-    else set_pp(W, h.p, h.q, 0);
+    if (dbg && h.dev >= 0)
+      fprintf(stderr, "fill k=%d kind=%d p=%d q=%d status=%d aca=%d rank=%d rank_p=%d\n", k, h.kind, h.p, h.q,
+              state[h.dev].status, state[h.dev].k, state[h.dev].r, W.r[h.p]);
+    if (gstat[f] != 0) continue;
+    if (h.kind == FILL_HYBRID) {
+      pres(W.px, W, h.q, h.p) = 0;
+      if (h.dev < 0) {
+        BlkRef F = xy_ref(W, h.q, h.p, false);
+        if (F.p) zero_dropped.zero(F.p, F.ld, W.n[h.q], W.r[h.p]);
+      }
+    } else {
+      set_pp(W, h.p, h.q, 0);
+      if (h.dev < 0) {
+        BlkRef F = p2p_ref(W, h.p, h.q, false);
+        if (F.p) zero_dropped.zero(F.p, F.ld, W.n[std::min(h.p, h.q)], W.n[std::max(h.p, h.q)]);
+      }
+    }
   }
   for (int t = 0; t < np; t++) W.dead[P[t].i] = 1;
+  if (dist) {
+    // halo: every block / basis the batch wrote goes from the pivot's owner
+    // to each other rank storing it (canonical order: pivot, then kind)
+    std::vector<std::vector<HaloItem>> send(nranks_), recv(nranks_);
+    std::vector<HaloItem> items;
+    for (int t = 0; t < np; t++) {
+      const PivInfo& I = P[t];
+      items.clear();
+      for (size_t a = 0; a < I.xp.size(); a++)
+        for (size_t b = a; b < I.xp.size(); b++) {
+          const int ja = std::min(I.xp[a], I.xp[b]), jb = std::max(I.xp[a], I.xp[b]);
+          if (pp_present(W, ja, jb)) items.push_back({HALO_P2P, ja, jb, 0});
+        }
+      std::vector<int> ys(I.yp);
+      ys.push_back(I.i);
+      for (int x : I.xp)
+        for (int y : ys)
+          if (pres(W.px, W, x, y)) items.push_back({HALO_XY, x, y, 0});
+      for (size_t a = 0; a < ys.size(); a++)
+        for (size_t b = a; b < ys.size(); b++) {
+          const int ja = std::min(ys[a], ys[b]), jb = std::max(ys[a], ys[b]);
+          if (pm_present(W, ja, jb)) items.push_back({HALO_M2L, ja, jb, 0});
+        }
+      for (int f = fill_off[t]; f < fill_off[t + 1]; f++)  // M2L absorption targets
+        items.push_back({HALO_M2L, std::min(fh[f].p, fh[f].q), std::max(fh[f].p, fh[f].q), 0});
+      for (int x : I.xp)
+        if (W.r[x] > r_before[x]) items.push_back({HALO_U, x, 0, r_before[x]});
+      const int q = owner(W, I.i);
+      for (const HaloItem& it : items)
+        if (halo_route(*part_, k, q, rank_, it.a, it.kind == HALO_U ? -1 : it.b,
+                       [&](int s) { send[s].push_back(it); }))
+          recv[q].push_back(it);
+    }
+    tm_.begin(PH_COMM);
+    halo_exchange(W, send, recv, &zero_dropped);
+    tm_.end();
+  }
   hmark(7);
   (void)colour;
+}
+
+Factorizer::HaloRef Factorizer::halo_ref(WorkLevel& W, const HaloItem& it) {
+  switch (it.kind) {
+    case HALO_P2P: {
+      BlkRef b = p2p_ref(W, it.a, it.b, false);
+      return {b.p, b.ld, W.n[it.a], W.n[it.b]};
+    }
+    case HALO_XY: {
+      BlkRef b = xy_ref(W, it.a, it.b, false);
+      return {b.p, b.ld, W.n[it.a], W.r[it.b]};
+    }
+    case HALO_M2L: {
+      BlkRef b = m2l_ref(W, it.a, it.b, false);
+      return {b.p, b.ld, W.r[it.a], W.r[it.b]};
+    }
+    default: {
+      double* u = W.U[it.a];
+      return {u ? u + size_t(it.c0) * W.n[it.a] : nullptr, W.n[it.a], W.n[it.a], W.r[it.a] - it.c0};
+    }
+  }
+}
+
+void Factorizer::halo_exchange(WorkLevel& W, const std::vector<std::vector<HaloItem>>& send,
+                               const std::vector<std::vector<HaloItem>>& recv, CopyBatch* local) {
+  CopyBatch pack, unpack;
+  std::vector<Msg> sm, rm;
+  auto stage = [&](const std::vector<HaloItem>& items, int peer, bool out) {
+    size_t tot = 0;
+    for (const HaloItem& it : items) {
+      const HaloRef r = halo_ref(W, it);
+      if (r.rows > 0 && r.cols > 0) tot += size_t(r.rows) * r.cols;
+    }
+    if (tot == 0) return;
+    double* buf = ws_.alloc_n<double>(tot);
+    size_t off = 0;
+    for (const HaloItem& it : items) {
+      const HaloRef r = halo_ref(W, it);
+      if (r.rows <= 0 || r.cols <= 0) continue;
+      if (!r.p) {
+        char m[160];
+        snprintf(m, sizeof m, "sharded factorization: halo block (kind %d, %d, %d) of level %d is not stored on rank %d",
+                 it.kind, it.a, it.b, W.k, rank_);
+        invalid(m);
+      }
+      if (out) pack.add(r.p, r.ld, buf + off, r.rows, r.rows, r.cols);
+      else unpack.add(buf + off, r.rows, r.p, r.ld, r.rows, r.cols);
+      off += size_t(r.rows) * r.cols;
+    }
+    (out ? sm : rm).push_back(Msg{peer, buf, tot * sizeof(double)});
+    if (out) F_->halo_bytes += double(tot) * sizeof(double);
+  };
+  for (int s = 0; s < nranks_; s++) {
+    if (s == rank_) continue;
+    stage(send[s], s, true);
+    stage(recv[s], s, false);
+  }
+  launch_copies(pack, ws_, st_, s_);
+  comm_->exchange(sm, rm, s_);
+  F_->exchanges++;
+  if (local) launch_copies(*local, ws_, st_, s_);
+  launch_copies(unpack, ws_, st_, s_);
 }
 
 void Factorizer::finish_level(int rec_begin) {
@@ -690,6 +977,42 @@ void Factorizer::finish_level(int rec_begin) {
     launch_pos_expand(druns, int(runs.size()), d, s_);
     for (size_t rr = rec_begin, u = 0; rr < F_->recs.size(); rr++, u++) F_->recs[rr].pos = d + posoff[u];
   }
+  if (nranks_ > 1) {
+    // sharded solve: the solve-vector runs each rank writes per batch -- the
+    // forward sweep writes a pivot's partner slots (its pos runs), the
+    // backward sweep its own x slots; pivots are in batch order, owners vary
+    std::vector<std::vector<std::vector<int64_t>>> fw, bw;  // [batch][rank] -> pairs
+    int b0 = -1;
+    for (const LevelPivot& lp : lvl_piv_) {
+      if (b0 < 0) b0 = lp.batch;
+      const size_t bi = size_t(lp.batch - b0);
+      if (fw.size() <= bi) {
+        fw.resize(bi + 1, std::vector<std::vector<int64_t>>(nranks_));
+        bw.resize(bi + 1, std::vector<std::vector<int64_t>>(nranks_));
+      }
+      for (const SlotRef& sr : lp.slots) {
+        if (sr.dim <= 0) continue;
+        fw[bi][lp.owner].push_back(sr.kind == 0 ? xb + xoff[sr.j] : yb + yoff[sr.j]);
+        fw[bi][lp.owner].push_back(sr.dim);
+      }
+      if (W.n[lp.i] > 0) {
+        bw[bi][lp.owner].push_back(xb + xoff[lp.i]);
+        bw[bi][lp.owner].push_back(W.n[lp.i]);
+      }
+    }
+    for (size_t bi = 0; bi < fw.size(); bi++) {
+      BatchH& B = F_->batches[size_t(b0) + bi];
+      B.fwd_off.assign(1, 0);
+      B.bwd_off.assign(1, 0);
+      for (int q = 0; q < nranks_; q++) {
+        B.fwd_runs.insert(B.fwd_runs.end(), fw[bi][q].begin(), fw[bi][q].end());
+        B.bwd_runs.insert(B.bwd_runs.end(), bw[bi][q].begin(), bw[bi][q].end());
+        B.fwd_off.push_back(int(B.fwd_runs.size() / 2));
+        B.bwd_off.push_back(int(B.bwd_runs.size() / 2));
+      }
+    }
+    lvl_piv_.clear();
+  }
   CK(cudaStreamSynchronize(s_));
   st_.reset();
 }
@@ -724,8 +1047,8 @@ void Factorizer::factor_top() {
     const MatDesc* dmd = upload(ws_, md, s_, st_);
     int* d_info = ws_.alloc_n<int>(1);
     tm_.begin(PH_TOP);
-    S_->work->gj_side.ensure();
-    batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &S_->work->gj_side);
+    work_->gj_side.ensure();
+    batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &work_->gj_side);
   }
   CK(cudaStreamSynchronize(s_));
   tm_.collect(F_.get(), 1);
@@ -734,7 +1057,6 @@ void Factorizer::factor_top() {
 FactorH* Factorizer::run() {
   auto t0 = std::chrono::steady_clock::now();
   if (getenv("IFMM_HOST_PROF")) fprintf(stderr, "host factorize begin\n");
-  s_ = S_->stream;
   tm_.on = (flags_ & IFMM_FLAG_TIMING) != 0;
   tm_.s = s_;
   F_.reset(new FactorH);
@@ -743,6 +1065,15 @@ FactorH* Factorizer::run() {
   F_->tol = tol_;
   F_->stream = s_;
   const int K = t_->depth;
+  if (comm_ && comm_->size() > 1) {
+    rank_ = comm_->rank();
+    nranks_ = comm_->size();
+    std::vector<std::vector<int>> grid(K + 1);
+    for (int k = 2; k <= K; k++) grid[k] = t_->lv[k].grid;
+    part_ = std::make_shared<Partition>(make_partition(t_->dim, K, nranks_, rank_, grid));
+    F_->comm = comm_;
+    F_->part = part_;
+  }
   F_->stats.assign(K + 1, LevelStatsH{});
   F_->lvl_base.assign(K + 1, 0);
   F_->lvl_base[K] = 0;
@@ -823,11 +1154,82 @@ FactorH* Factorizer::run() {
   return F_.release();
 }
 
+FactorH::~FactorH() {
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
 FactorH* factorize(StoreH* S, double tol, int flags, double cond_limit) {
   ensure_device();
   std::lock_guard<std::mutex> lock(S->work->mu);  // one factorization per store at a time
-  Factorizer f(S, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12);
+  Factorizer f(S, S->work.get(), S->stream, nullptr, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12);
   return f.run();
+}
+
+FactorH* factorize_sharded(StoreH* S, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit) {
+  ensure_device();
+  if (!comm) invalid("null communicator");
+  std::lock_guard<std::mutex> lock(S->work->mu);
+  Factorizer f(S, S->work.get(), S->stream, std::move(comm), tol < 0 ? S->tol : tol, flags,
+               cond_limit > 0 ? cond_limit : 1e12);
+  return f.run();
+}
+
+// Virtual ranks as threads on one GPU: each has its own workspaces, stream and
+// records; the store (initial operators, read-only here) is shared.
+void factorize_emulated(StoreH* S, int nranks, double tol, int flags, double cond_limit, std::vector<FactorH*>& out) {
+  ensure_device();
+  if (nranks < 1) invalid("nranks must be >= 1");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(S->work->mu);
+  auto world = std::make_shared<LocalWorld>(nranks);
+  std::vector<std::unique_ptr<FactorH>> res(nranks);
+  std::vector<std::exception_ptr> errs(nranks);
+  std::vector<std::thread> th;
+  for (int r = 0; r < nranks; r++)
+    th.emplace_back([&, r] {
+      try {
+        CK(cudaSetDevice(dev));
+        std::unique_ptr<FactorWork> work(new FactorWork);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        std::shared_ptr<Comm> c = std::make_shared<LocalComm>(world, r);
+        std::unique_ptr<FactorH> F;
+        try {
+          Factorizer f(S, work.get(), s, c, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12);
+          F.reset(f.run());
+        } catch (...) {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+          throw;
+        }
+        F->own_stream = true;
+        F->own_work = std::move(work);  // its level arenas return to the slab cache with the factorization
+        res[r] = std::move(F);
+      } catch (...) {
+        errs[r] = std::current_exception();
+        world->fail();
+      }
+    });
+  for (auto& t : th) t.join();
+  // a real failure (e.g. SingularPivot, raised on every rank) wins over the
+  // "another virtual rank failed" aborts it caused
+  std::exception_ptr first;
+  for (int r = 0; r < nranks && !first; r++)
+    if (errs[r]) {
+      try {
+        std::rethrow_exception(errs[r]);
+      } catch (const Error& e) {
+        if (std::string(e.what()) != "another virtual rank failed") first = errs[r];
+      } catch (...) {
+        first = errs[r];
+      }
+    }
+  for (int r = 0; r < nranks && !first; r++)
+    if (errs[r]) first = errs[r];
+  if (first) std::rethrow_exception(first);
+  out.clear();
+  for (auto& f : res) out.push_back(f.release());
 }
 
 }  // namespace ifmm

@@ -11,7 +11,9 @@
 // processed in chunks of RC; a level's y slots alias the next level's x slots.
 #include <algorithm>
 #include <cmath>
+#include <thread>
 
+#include "comm.cuh"
 #include "core.cuh"
 #include "gemm.cuh"
 
@@ -462,6 +464,50 @@ static int solve_chunks(const BatchH& b) {
   return std::max(1, std::min(want, (b.maxn + 31) / 32));
 }
 
+// Sharded solve: after a batch every rank holds the solve-vector entries its
+// own pivots wrote; ship them to every other rank (the vector stays
+// replicated, so later batches and the top solve read current values).
+static void share_runs(FactorH* F, double* V, int nr, const std::vector<int64_t>& runs, const std::vector<int>& off,
+                       Arena& ws, Staging& st, cudaStream_t s) {
+  Comm& C = *F->comm;
+  const int me = C.rank(), nq = C.size();
+  auto len = [&](int q) {
+    int64_t t = 0;
+    for (int u = off[q]; u < off[q + 1]; u++) t += runs[2 * size_t(u) + 1];
+    return t * nr;
+  };
+  CopyBatch pack, unpack;
+  std::vector<Msg> sm, rm;
+  const int64_t mine = len(me);
+  double* sbuf = nullptr;
+  if (mine > 0) {
+    sbuf = ws.alloc_n<double>(size_t(mine));
+    int64_t o = 0;
+    for (int u = off[me]; u < off[me + 1]; u++) {
+      const int64_t b = runs[2 * size_t(u)], l = runs[2 * size_t(u) + 1] * nr;
+      pack.add(V + b * nr, int(l), sbuf + o, int(l), int(l), 1);
+      o += l;
+    }
+    for (int q = 0; q < nq; q++)
+      if (q != me) sm.push_back(Msg{q, sbuf, size_t(mine) * sizeof(double)});
+  }
+  for (int q = 0; q < nq; q++) {
+    const int64_t l = q == me ? 0 : len(q);
+    if (l <= 0) continue;
+    double* rbuf = ws.alloc_n<double>(size_t(l));
+    rm.push_back(Msg{q, rbuf, size_t(l) * sizeof(double)});
+    int64_t o = 0;
+    for (int u = off[q]; u < off[q + 1]; u++) {
+      const int64_t b = runs[2 * size_t(u)], rl = runs[2 * size_t(u) + 1] * nr;
+      unpack.add(rbuf + o, int(rl), V + b * nr, int(rl), int(rl), 1);
+      o += rl;
+    }
+  }
+  launch_copies(pack, ws, st, s);
+  C.exchange(sm, rm, s);
+  launch_copies(unpack, ws, st, s);
+}
+
 void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_ptr) {
   TreeH* t = F->tree;
   const int64_t N = t->N;
@@ -501,11 +547,21 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     mm_attr = true;
   }
   const int nqc = (nr + MQ - 1) / MQ;
+  const bool dist = F->comm && F->comm->size() > 1;
+  // sharded: descriptor staging for the run exchanges (reset per call; the
+  // stream is synchronised at the end of every solve)
+  static thread_local Staging xst;
+  xst.reset();
   for (const BatchH& b : F->batches) {
+    if (dist && b.rec1 == b.rec0) {
+      share_runs(F, V, nr, b.fwd_runs, b.fwd_off, ws, xst, s);
+      continue;
+    }
     if (mm) {
       const dim3 grid(b.rec1 - b.rec0, (b.maxn + b.maxw + GBM - 1) / GBM, nqc);
       solve_fwd_mm_kernel<<<grid, GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
       CK_LAUNCH();
+      if (dist) share_runs(F, V, nr, b.fwd_runs, b.fwd_off, ws, xst, s);
       continue;
     }
     const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
@@ -518,6 +574,7 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     else if (RC == 1) solve_fwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     else solve_fwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
+    if (dist) share_runs(F, V, nr, b.fwd_runs, b.fwd_off, ws, xst, s);
   }
   // top: y = T^-1 b on the level-1 slots (viewed column-major as nrhs x M)
   if (F->top_dim > 0) {
@@ -536,10 +593,15 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
   }
   for (auto it = F->batches.rbegin(); it != F->batches.rend(); ++it) {
     const BatchH& b = *it;
+    if (dist && b.rec1 == b.rec0) {
+      share_runs(F, V, nr, b.bwd_runs, b.bwd_off, ws, xst, s);
+      continue;
+    }
     if (mm) {
       const dim3 grid(b.rec1 - b.rec0, (b.maxn + GBM - 1) / GBM, nqc);
       solve_bwd_mm_kernel<<<grid, GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
       CK_LAUNCH();
+      if (dist) share_runs(F, V, nr, b.bwd_runs, b.bwd_off, ws, xst, s);
       continue;
     }
     const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
@@ -548,10 +610,38 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     if (RC == 1) solve_bwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     else solve_bwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
+    if (dist) share_runs(F, V, nr, b.bwd_runs, b.bwd_off, ws, xst, s);
   }
   launch_permute(V + F->lvl_base[t->depth] * nr, dout, t->d_perm, N, nr, true, s);
   if (!device_ptr) CK(cudaMemcpyAsync(x, dout, sizeof(double) * N * nr, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace ifmm
+
+namespace ifmm {
+
+void solve_emulated(const std::vector<FactorH*>& f, const double* rhs, const std::vector<double*>& x, int64_t nrhs,
+                    bool device_ptr) {
+  const int n = int(f.size());
+  if (n < 1 || x.size() != f.size()) invalid("solve_emulated: one output per virtual rank");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::vector<std::exception_ptr> errs(n);
+  std::vector<std::thread> th;
+  for (int r = 0; r < n; r++)
+    th.emplace_back([&, r] {
+      try {
+        CK(cudaSetDevice(dev));
+        solve(f[r], rhs, x[r], nrhs, device_ptr);
+      } catch (...) {
+        errs[r] = std::current_exception();
+        if (auto* lc = dynamic_cast<LocalComm*>(f[r]->comm.get())) lc->world().fail();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
 }
 
 }  // namespace ifmm

@@ -91,6 +91,17 @@ class IfmmFactorization:
                 out[k] = {p: round(float(ms[i]), 3) for i, p in enumerate(PHASES + ("host_busy", "host_wait"))}
         return out
 
+    @property
+    def shard(self) -> dict:
+        """Sharded factorizations: this rank, the rank count and traffic
+        (halo / metadata bytes sent, exchanges, device ms in communication
+        with timing=True).  One GPU: rank 0 of 1, no traffic."""
+        rn = np.zeros(2, dtype=np.int32)
+        o = np.zeros(4)
+        _lib.check(_lib.lib.ifmm_factor_shard_info(self.handle, _lib.ptr(rn), _lib.ptr(o)))
+        return {"rank": int(rn[0]), "nranks": int(rn[1]), "halo_bytes": o[0], "meta_bytes": o[1],
+                "exchanges": int(o[2]), "comm_ms": o[3]}
+
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None
         lib = getattr(_lib, "lib", None)
@@ -103,19 +114,38 @@ PHASES = ("gather", "gauss_jordan", "x_gemm", "schur_gemm", "compress", "transit
 
 def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None, diagnostics: bool = False,
               release_m2l: bool = True, timing: bool = False,
-              pivot_condition_limit: float = PIVOT_CONDITION_LIMIT) -> IfmmFactorization:
+              pivot_condition_limit: float = PIVOT_CONDITION_LIMIT, comm=None) -> IfmmFactorization:
     """Eliminate the extended system on the GPU (ifmm/solver.py:106-153).
 
     Unlike the reference the store's initial operators stay intact (the
     elimination works on its own device copy), so `fmm_matvec(store, ...)`
     remains valid afterwards.  `release_m2l` is accepted for API parity:
-    finished levels are always released."""
+    finished levels are always released.
+
+    comm (extension): a `distributed.Communicator`; the call is then
+    collective over its ranks, each eliminating its own level-2 subtrees
+    (every rank passes the same store contents)."""
     if tol is None:
         tol = store.tol
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), 1 if timing else 0, float(pivot_condition_limit),
-                                       ctypes.byref(h)))
-    fact = IfmmFactorization(store=store, tree=tree, tol=float(tol), handle=h)
+    flags = 1 if timing else 0
+    if comm is not None and comm.size > 1:
+        _lib.check(_lib.lib.ifmm_factorize_sharded(store.handle, comm.handle, float(tol), flags,
+                                                   float(pivot_condition_limit), ctypes.byref(h)))
+    else:
+        _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), flags, float(pivot_condition_limit),
+                                           ctypes.byref(h)))
+    fact = _wrap_factor(store, tree, float(tol), h)
+    if diagnostics:
+        for k in range(tree.depth, 1, -1):
+            s = fact.level_stats[k]
+            logger.info("level=%d,k_clusters=%d,max_rank=%d,fillins_compressed=%d,fillins_dense_kept=%d",
+                        k, s.clusters, s.max_rank, s.fillins_compressed, s.fillins_dense_kept)
+    return fact
+
+
+def _wrap_factor(store: OperatorStore, tree: ClusterTree, tol: float, h) -> IfmmFactorization:
+    fact = IfmmFactorization(store=store, tree=tree, tol=tol, handle=h)
     rm, top = ctypes.c_int(), ctypes.c_int()
     nrec, ms = ctypes.c_int64(), ctypes.c_double()
     _lib.check(_lib.lib.ifmm_factor_info(h, ctypes.byref(rm), ctypes.byref(top), ctypes.byref(nrec),
@@ -125,10 +155,6 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
         st = np.zeros(4, dtype=np.int32)
         _lib.check(_lib.lib.ifmm_factor_level_stats(h, k, _lib.ptr(st)))
         fact.level_stats[k] = LevelStats(*map(int, st))
-        if diagnostics:
-            s = fact.level_stats[k]
-            logger.info("level=%d,k_clusters=%d,max_rank=%d,fillins_compressed=%d,fillins_dense_kept=%d",
-                        k, s.clusters, s.max_rank, s.fillins_compressed, s.fillins_dense_kept)
     return fact
 
 

@@ -1,0 +1,113 @@
+"""Subtree-sharded factorize / solve on one GPU.
+
+The sharded schedule (csrc/factor.cu with a communicator: every rank replays
+the host schedule, eliminates its own level-2 subtrees and ships the blocks it
+wrote to the ranks storing them) runs here with V virtual ranks as threads on
+the one GPU (LocalComm: device-to-device copies instead of NCCL; the
+exchanges are checked for matching sizes).  Its result must be bit-identical
+to the single-GPU factorization: same elimination order and fill decisions,
+and the kernels' blocking / worker shapes are chosen from the whole colour
+batch across ranks, so every pivot and fill sees the same arithmetic.  The
+NCCL transport itself is exercised through a 1-rank communicator.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ifmm():
+    import paper_1407_1572_b200 as m
+    from paper_1407_1572_b200 import _lib
+    if _lib.lib.ifmm_device_count() == 0:
+        pytest.skip("no CUDA device")
+    return m
+
+
+def _system(ifmm, n, depth, kernel, p, tol):
+    from oracle import ifmm_oracle as O
+    pts = O.baseline_points(n, seed=0)
+    kern = ifmm.baseline_kernel(kernel, n)
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    store = ifmm.init_operators(tree, kern, p=p, tol=tol)
+    b = O.baseline_rhs(n, "normal")
+    return tree, store, b
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+# (N, depth, kernel, p, tol, virtual ranks): C1, a log-kernel case, C3's parameters at N = 65,536
+CASES = [
+    (4096, 3, "inv_r", 4, 1e-8, [2, 4, 8, 16]),
+    (16384, 4, "log_r", 5, 1e-6, [2, 3, 4, 8]),
+    (65536, 5, "inv_r", 4, 1e-6, [2, 4, 8]),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"N{c[0]}_{c[2]}")
+def test_sharded_matches_single_gpu(ifmm, case):
+    from paper_1407_1572_b200 import distributed as D
+    n, depth, kernel, p, tol, ranks = case
+    tree, store, b = _system(ifmm, n, depth, kernel, p, tol)
+    f1 = ifmm.factorize(store, tree)
+    x1 = ifmm.solve(f1, b)
+    r1 = _rel(ifmm.fmm_matvec(store, tree, x1), b)
+    for V in ranks:
+        fs = D.factorize_emulated(store, tree, V)
+        assert [f.shard["rank"] for f in fs] == list(range(V))
+        assert all(f.shard["nranks"] == V for f in fs)
+        assert sum(f.n_records for f in fs) == f1.n_records
+        assert sum(f.shard["halo_bytes"] for f in fs) > 0
+        assert all(f.top_dim == f1.top_dim for f in fs), ([f.top_dim for f in fs], f1.top_dim)
+        for k in range(2, depth + 1):
+            assert fs[0].level_stats[k] == f1.level_stats[k], (V, k)
+        xs = D.solve_emulated(fs, b)
+        for r in range(1, V):
+            assert np.array_equal(xs[r], xs[0]), "ranks disagree on the replicated solution"
+        d = _rel(xs[0], x1)
+        res = _rel(ifmm.fmm_matvec(store, tree, xs[0]), b)
+        print(f"\nN={n} V={V}: solution vs 1 GPU {d:.2e}, residual {res:.2e} (1 GPU {r1:.2e}), "
+              f"halo {sum(f.shard['halo_bytes'] for f in fs) / 1e6:.1f} MB")
+        assert np.array_equal(xs[0], x1), (V, d)
+        assert res <= max(10 * tol, 2 * r1), (V, res, r1)
+        del fs
+
+
+def test_sharded_multi_rhs(ifmm):
+    from paper_1407_1572_b200 import distributed as D
+    tree, store, b = _system(ifmm, 16384, 4, "log_r", 5, 1e-6)
+    B = np.stack([b, np.roll(b, 7), b * 0.5 - 1.0], axis=1)
+    f1 = ifmm.factorize(store, tree)
+    X1 = ifmm.solve(f1, B)
+    fs = D.factorize_emulated(store, tree, 4)
+    Xs = D.solve_emulated(fs, B)
+    assert Xs.shape == (4, 16384, 3)
+    assert np.array_equal(Xs[1], Xs[0])
+    assert np.array_equal(Xs[0], X1)
+
+
+def test_sharded_singular_pivot_raised_on_every_rank(ifmm):
+    """A pivot failing the condition limit raises SingularPivotError (same
+    level / index as one GPU) instead of leaving other ranks waiting."""
+    from paper_1407_1572_b200 import distributed as D
+    tree, store, b = _system(ifmm, 4096, 3, "inv_r", 4, 1e-8)
+    with pytest.raises(ifmm.SingularPivotError) as e1:
+        ifmm.factorize(store, tree, pivot_condition_limit=10.0)
+    with pytest.raises(ifmm.SingularPivotError) as e2:
+        D.factorize_emulated(store, tree, 4, pivot_condition_limit=10.0)
+    assert (e1.value.level, e1.value.index) == (e2.value.level, e2.value.index)
+
+
+def test_nccl_transport_one_rank(ifmm):
+    """The NCCL transport (dlopen'd libnccl): a 1-rank communicator passes the
+    all-gather + self send/recv check, and factorize(comm=...) runs."""
+    from paper_1407_1572_b200 import distributed as D
+    comm = D.Communicator.nccl(D.Communicator.unique_id(), 1, 0)
+    assert comm.selftest(1 << 16)
+    tree, store, b = _system(ifmm, 4096, 3, "inv_r", 4, 1e-8)
+    x = ifmm.solve(ifmm.factorize(store, tree, comm=comm), b)
+    x1 = ifmm.solve(ifmm.factorize(store, tree), b)
+    assert np.array_equal(x, x1)
