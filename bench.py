@@ -12,8 +12,10 @@ quadtree depth 7, Chebyshev p = 4, eps = 1e-6).  Synthetic seeded data.
 Own arm: tree + operators are built once (t_a, reported), then W warm-up and
 K timed steps with inputs resident in HBM (value, ms_per_step); e2e repeats
 the step through the public API with host numpy buffers (H2D rhs, D2H x).
-Under torchrun every rank solves its own replica (north_star's subtree
-partition is not in this round: "replicas only"), timing is max over ranks.
+Under torchrun (--gpus N > 1) the ranks factorize ONE system together: the
+subtree-sharded path (paper_1407_1572_b200.distributed) with NCCL
+halo exchanges after every colour batch -- strong scaling, timing is the max
+over ranks.
 --impl reference times the reference algorithm (the CPU oracle restatement,
 Morton order, bit-exact with /root/reference) on a bounded sample on rank 0.
 """
@@ -217,8 +219,13 @@ def main():
     store = ifmm.init_operators(tree, kernel, p=p, tol=tol)
     t_a = time.perf_counter() - t0
 
+    comm = None
+    if ws > 1:
+        from paper_1407_1572_b200.distributed import Communicator
+        comm = Communicator.from_torch()
+
     def step(rhs):
-        fact = ifmm.factorize(store, tree, pivot_condition_limit=cond_limit)
+        fact = ifmm.factorize(store, tree, pivot_condition_limit=cond_limit, comm=comm)
         x = ifmm.solve(fact, rhs)
         return fact, x
 
@@ -276,6 +283,7 @@ def main():
     refine_s = time.perf_counter() - t1
     refine_hist = list(fact.last_refinement)
     r_m, top_dim = fact.r_m, fact.top_dim
+    shard = fact.shard
     # free the last factorization first so later ones reuse its device slabs
     # (as every timed step does); the e2e timing would otherwise include fresh
     # multi-GB allocations
@@ -286,16 +294,27 @@ def main():
     for _ in range(max(1, min(args.steps, 2))):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        f2 = ifmm.factorize(store, tree, pivot_condition_limit=cond_limit)
+        f2 = ifmm.factorize(store, tree, pivot_condition_limit=cond_limit, comm=comm)
         xh = ifmm.solve(f2, b_host)
         e2e_times.append(time.perf_counter() - t1)
         del f2
     e2e = float(np.mean(e2e_times))
+    if ws > 1:
+        te = torch.tensor([e2e], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = float(te.item())
 
     # instrumented factorization: per-phase device time for the roofline
-    ft = ifmm.factorize(store, tree, timing=True, pivot_condition_limit=cond_limit)
+    ft = ifmm.factorize(store, tree, timing=True, pivot_condition_limit=cond_limit, comm=comm)
     ph = ft.phase_times
     work = ft.work
+    shard_t = ft.shard
+    work_all = dict(work)
+    if ws > 1:  # per-rank work -> whole job
+        wt = torch.tensor([work["flops_exec"], work["flops_schur"], work["flops_ref"], work["solve_bytes"]],
+                          dtype=torch.float64, device="cuda")
+        dist.all_reduce(wt)
+        work_all = dict(zip(("flops_exec", "flops_schur", "flops_ref", "solve_bytes"), wt.tolist()))
     fl_peak = measured_fp64_peak()
     schur_ms, schur_launches = ph["schur_gemm"]
     achieved = work["flops_schur"] / (schur_ms * 1e-3) / 1e12 if schur_ms > 0 else None
@@ -337,11 +356,13 @@ def main():
 
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
+        "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded uniform points in [0,1]^2, N(0,1) rhs)",
         "config": {"workload": args.config, "N": N, "kernel": "1/|x-y|" if kern == "inv_r" else "log|x-y|",
                    "diag": "sqrt(N)", "depth": depth, "p": p, "eps": tol, "nrhs": nrhs,
-                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "parallelism": f"subtree{ws} (level-2 subtrees per rank, NCCL halo exchange per colour batch)"
+                   if ws > 1 else "single",
                    "pivot_condition_limit": cond_limit if math.isfinite(cond_limit) else "disabled",
                    "pivot_condition_note": cond_note,
                    "l2": "factor state (GBs) >> 126 MB L2; no flush needed"},
@@ -350,8 +371,13 @@ def main():
                           "seconds": refine_s,
                           "note": "extension: x += solve(b - A~x) with the store's FMM operator; not in value"},
         "r_m": r_m, "top_dim": top_dim, "t_assembly_s": t_a,
-        "flops": {"exec": work["flops_exec"], "schur": work["flops_schur"], "reference_equiv": work["flops_ref"],
-                  "fp64_tflops_step": work["flops_exec"] / t_step / 1e12},
+        "flops": {"exec": work_all["flops_exec"], "schur": work_all["flops_schur"],
+                  "reference_equiv": work_all["flops_ref"],
+                  "fp64_tflops_step": work_all["flops_exec"] / t_step / 1e12,
+                  "scope": "whole job (summed over ranks)" if ws > 1 else "one GPU"},
+        "shard": {"rank0_halo_bytes_per_factorization": shard["halo_bytes"],
+                  "rank0_meta_bytes": shard["meta_bytes"], "exchanges": shard["exchanges"],
+                  "rank0_comm_ms": shard_t["comm_ms"]} if ws > 1 else None,
         "phase_ms": {k: round(v[0], 3) for k, v in ph.items()},
         "phase_ms_by_level": ft.phase_times_by_level,
         "roofline": {"kernel": "schur_concat_kernel (Schur update T = C^T S^-1 C, DMMA m8n8k4)", "bound": "tensor",
