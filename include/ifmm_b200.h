@@ -89,6 +89,9 @@ int ifmm_store_dims(const ifmm_store* s, int level, int32_t* n, int32_t* r);
 int ifmm_store_basis(const ifmm_store* s, int level, int index, double* out);
 /* M2L block (r_i x r_j, column-major) of interaction-list pair (i, j) */
 int ifmm_store_m2l(const ifmm_store* s, int level, int i, int j, double* out);
+/* leaf near-field block P2P(i, j) (n_i x n_j, column-major) of neighbour pair
+ * (i, j) (OperatorStore.p2p, ifmm/operators.py:180-194; stored once per pair) */
+int ifmm_store_p2p(const ifmm_store* s, int i, int j, double* out);
 /* fmm_matvec (ifmm/operators.py:282-330): y = A~ x, x/y (n, nrhs) */
 int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr_kind);
 void ifmm_store_free(ifmm_store* s);

@@ -8,7 +8,8 @@ from ._lib import SingularPivotError
 from .estimator import IfmmSolver, default_depth
 from .geometry import ClusterTree, Cluster, PointSet, build_tree, compute_lists, morton_decode, morton_encode
 from .kernels import KERNEL_NAMES, Kernel, baseline_kernel, kernel_block, make_kernel
-from .operators import OperatorStore, fmm_matvec, init_operators
+from .operators import (OperatorStore, assemble_extended_dense, dump_extended, extended_layout, extended_restrict_x,
+                        extended_rhs, fmm_matvec, init_operators)
 from .solver import IfmmFactorization, LevelStats, factorize, solve
 from . import distributed  # noqa: E402  (sharded factorize / solve)
 
@@ -25,7 +26,12 @@ __all__ = [
     "SingularPivotError",
     "baseline_kernel",
     "build_tree",
+    "assemble_extended_dense",
     "compute_lists",
+    "dump_extended",
+    "extended_layout",
+    "extended_restrict_x",
+    "extended_rhs",
     "default_depth",
     "factorize",
     "fmm_matvec",

@@ -53,6 +53,7 @@ SIGNATURES = {
     "ifmm_store_dims": (_i32, [_p, _i32, _p, _p]),
     "ifmm_store_basis": (_i32, [_p, _i32, _i32, _p]),
     "ifmm_store_m2l": (_i32, [_p, _i32, _i32, _i32, _p]),
+    "ifmm_store_p2p": (_i32, [_p, _i32, _i32, _p]),
     "ifmm_matvec": (_i32, [_p, _p, _p, _i64, _i32]),
     "ifmm_store_free": (None, [_p]),
     "ifmm_factorize": (_i32, [_p, _d, _i32, _d, ctypes.POINTER(_p)]),

@@ -197,6 +197,30 @@ int ifmm_store_m2l(const ifmm_store* s, int level, int i, int j, double* out) {
   });
 }
 
+int ifmm_store_p2p(const ifmm_store* s, int i, int j, double* out) {
+  return guard([&] {
+    const StoreH* S = s->h;
+    const int K = S->tree->depth;
+    const Topo& T = S->tree->lv[K];
+    const InitLevel& L = S->lv[K];
+    if (i < 0 || j < 0 || i >= T.nc || j >= T.nc) invalid("index out of range");
+    const int a = std::min(i, j), b = std::max(i, j), sl = T.slot(a, b);
+    const double* blk = sl >= 0 ? S->leaf_p2p[size_t(a) * T.win() + sl] : nullptr;
+    bool nb = false;
+    for (int q = T.nbr_off[i]; q < T.nbr_off[i + 1]; q++) nb |= T.nbr[q] == j;
+    if (!nb || !blk) invalid("(i, j) is not a leaf neighbour pair");
+    const int na = L.n[a], nbb = L.n[b];
+    std::vector<double> h(size_t(na) * nbb);
+    CK(cudaMemcpy(h.data(), blk, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+    if (i == a) {
+      memcpy(out, h.data(), sizeof(double) * h.size());
+    } else {  // stored once as (a, b): return the transpose, n_i x n_j column-major
+      for (int c = 0; c < na; c++)
+        for (int r = 0; r < nbb; r++) out[r + size_t(c) * nbb] = h[c + size_t(r) * na];
+    }
+  });
+}
+
 int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr_kind) {
   return guard([&] { ifmm::matvec(s->h, x, y, nrhs, ptr_kind == IFMM_PTR_DEVICE); });
 }

@@ -181,3 +181,37 @@ def test_estimator_roundtrip(ifmm):
     b = np.random.default_rng(1).standard_normal(2048)
     x = est.solve(b)
     assert np.linalg.norm(est.matvec(x) - b) <= 1e-6 * np.linalg.norm(b)
+
+
+def test_extended_system_export(ifmm, tmp_path):
+    """assemble_extended_dense / extended_rhs / extended_restrict_x /
+    dump_extended (ifmm/operators.py:333-486) on the GPU store vs the
+    reference's own (tests/golden/extended_256.npz, oracle/gen_golden_extended.py):
+    identical slot layout and leaf kernel rows, same nonzero count, and the
+    extended solve gives the reference's original unknowns (basis-invariant)."""
+    from oracle import ifmm_oracle as O
+    g = load_golden("extended_256")
+    N, depth = int(g["N"]), int(g["depth"])
+    pts = O.baseline_points(N, seed=0)
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    store = ifmm.init_operators(tree, ifmm.make_kernel("log", a=float(g["a"])), p=int(g["p"]), tol=float(g["tol"]))
+    A, slots = ifmm.assemble_extended_dense(store, tree)
+    sym = {"x": 0, "y": 1, "z": 2}
+    assert np.array_equal(np.array([[sym[s], k, i, d] for s, k, i, d in slots]), g["slots"])
+    n0 = slots[0][3]
+    assert np.allclose(A[:n0, :n0], g["leaf0_rows"][:, :n0], rtol=1e-14, atol=0)
+    assert np.count_nonzero(A) == int(g["nnz"])
+    xe = np.linalg.solve(A, ifmm.extended_rhs(store, tree, g["b"]))
+    x = ifmm.extended_restrict_x(store, tree, xe)
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+    res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - g["b"]) / np.linalg.norm(g["b"])
+    assert res <= max(1e-10, 10 * float(g["resid"]))
+    path = tmp_path / "ext.txt"
+    ifmm.dump_extended(store, tree, str(path))
+    lines = path.read_text().splitlines()
+    assert lines[0] == f"# extended system, dimension {A.shape[0]}"
+    assert len(lines) == 1 + np.count_nonzero(A)
+    r, c, v = lines[1].split()
+    assert A[int(r), int(c)] == float(v)
+    with pytest.raises(ValueError, match="exceeds cap"):
+        ifmm.assemble_extended_dense(store, tree, cap=100)
