@@ -208,7 +208,17 @@ class Factorizer {
   void set_pm(WorkLevel& W, int i, int j, uint8_t v) { int a = std::min(i, j), b = std::max(i, j); pres(W.pm, W, a, b) = v; }
   bool pm_present(WorkLevel& W, int i, int j) { int a = std::min(i, j), b = std::max(i, j); return pres(W.pm, W, a, b); }
 
+  // IFMM_HOST_PROF: host ms between marks of the level start
+  std::chrono::steady_clock::time_point hp_t_;
+  void hprof_mark(const char* what) {
+    static const bool on = getenv("IFMM_HOST_PROF") != nullptr;
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    if (what) fprintf(stderr, "  host %s: %.2f ms\n", what, std::chrono::duration<double, std::milli>(now - hp_t_).count());
+    hp_t_ = now;
+  }
   void init_level_alloc(WorkLevel& W, int k) {
+    hprof_mark(nullptr);
     W.k = k;
     W.T = &t_->lv[k];
     W.nc = W.T->nc;
@@ -219,6 +229,7 @@ class Factorizer {
     if (hp) fprintf(stderr, "level %d arena: zeroing %.2f GB (reserved %.2f GB)\n", k, W.arena->in_use() / 1e9,
                     W.arena->reserved() / 1e9);
     W.arena->reset();
+    hprof_mark("arena reset");
     W.p2p.assign(size_t(W.nc) * W.win, nullptr);
     W.m2l.assign(size_t(W.nc) * W.win, nullptr);
     W.xy.assign(size_t(W.nc) * W.win, nullptr);
@@ -228,6 +239,7 @@ class Factorizer {
     W.dead.assign(W.nc, 0);
     W.U.assign(W.nc, nullptr);
     W.d_rank = W.arena->alloc_n<int>(W.nc);
+    hprof_mark("tables");
   }
   std::vector<int> mark_;
   int stamp_ = 0;
@@ -303,7 +315,9 @@ void Factorizer::start_leaf_level() {
     }
   }
   CK(cudaMemcpyAsync(W.d_rank, W.r.data(), sizeof(int) * W.nc, cudaMemcpyHostToDevice, s_));
+  hprof_mark("leaf descriptors");
   launch_copies(cb, ws_, st_, s_);
+  hprof_mark("leaf upload+launch");
 }
 
 void Factorizer::start_parent_level(WorkLevel& C, int k) {
@@ -380,7 +394,9 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
     }
   }
   CK(cudaMemcpyAsync(W.d_rank, W.r.data(), sizeof(int) * W.nc, cudaMemcpyHostToDevice, s_));
+  hprof_mark("parent descriptors");
   launch_copies(cb, ws_, st_, s_);
+  hprof_mark("parent upload+launch");
   if (nranks_ > 1) {
     tm_.begin(PH_COMM);
     halo_exchange(W, send, recv, nullptr);
@@ -435,13 +451,17 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     double *S, *C, *Xb;
     int rec;
   };
-  // every rank walks all pivots of the batch (metadata); device work is done
-  // for its own pivots only (all of them on one GPU)
+  // Every rank walks all pivots of the batch (metadata); device work is done
+  // for its own pivots only (all of them on one GPU).  The batch's fills are
+  // determined by the partner sets: hybrid (p in yp u {i}, q in xp, q in
+  // IL(p)) then P2P (xp pairs in each other's IL), in the reference order.
   std::vector<PivInfo> P(np);
   std::vector<int> own;  // indices into P
-  CopyBatch cb;
-  std::vector<MatDesc> md;
+  struct FillHost { int kind, p, q, piv, dev; };  // dev: index among this rank's fills, or -1
+  std::vector<FillHost> fh;
+  std::vector<int> fill_off(np + 1, 0);  // fills of pivot t: fh[fill_off[t] .. fill_off[t+1])
   const int batch_id = int(F_->batches.size());
+  int n_own_fills = 0, gmaxm = 0, shape_mx = 0;
   for (int t = 0; t < np; t++) {
     PivInfo& I = P[t];
     const int i = piv[t];
@@ -450,13 +470,14 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     I.r = W.r[i];
     I.m = I.n + I.r;
     I.own = mine(W, i);
+    I.rec = -1;
     partners(W, i, I.xp, I.yp);
     I.soff.assign(1, 0);
     for (int j : I.xp) I.soff.push_back(I.soff.back() + W.n[j]);
     for (int j : I.yp) I.soff.push_back(I.soff.back() + W.r[j]);
     I.soff.push_back(I.soff.back() + I.r);
     I.w = I.soff.back();
-    I.rec = -1;
+    gmaxm = std::max(gmaxm, I.m);
     if (dist) {
       LevelPivot lp{batch_id, owner(W, i), i, {}};
       for (int j : I.xp) lp.slots.push_back({0, j, W.n[j]});
@@ -464,6 +485,21 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       lp.slots.push_back({1, i, I.r});
       lvl_piv_.push_back(std::move(lp));
     }
+    fill_off[t] = int(fh.size());
+    std::vector<int> ps(I.yp);
+    ps.push_back(I.i);
+    std::sort(ps.begin(), ps.end());
+    auto note = [&](int kind, int p, int q) {
+      fh.push_back({kind, p, q, t, I.own ? n_own_fills++ : -1});
+      const int rows = kind == FILL_HYBRID ? W.r[p] : W.n[p];
+      shape_mx = std::max(shape_mx, std::max(std::max(W.n[p], W.n[q]), rows));
+    };
+    for (int p : ps)
+      for (int q : I.xp)
+        if (T.in_il(p, q)) note(FILL_HYBRID, p, q);
+    for (size_t u = 0; u < I.xp.size(); u++)
+      for (size_t v = u + 1; v < I.xp.size(); v++)
+        if (T.in_il(I.xp[u], I.xp[v])) note(FILL_P2P, I.xp[u], I.xp[v]);
     if (!I.own) continue;
     if (dist) {
       bool ok = holds1(W, i);
@@ -474,240 +510,269 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
                 "well-separated fill); factorize this system on one GPU");
     }
     own.push_back(t);
-    I.S = ws_.alloc_n<double>(size_t(I.m) * I.m);
-    I.C = ws_.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
-    I.Xb = ws_.alloc_n<double>(size_t(std::max(1, I.r)) * I.w);
-    int* ipiv = ws_.alloc_n<int>(I.m);
-    md.push_back(MatDesc{I.S, I.m, I.m, ipiv, i});
-    // gather S
-    BlkRef Pii = p2p_ref(W, i, i, true);
-    cb.add(Pii.p, Pii.ld, I.S, I.m, I.n, I.n);
-    cb.add(W.U[i], I.n, I.S + size_t(I.n) * I.m, I.m, I.n, I.r);
-    cb.add(W.U[i], I.n, I.S + I.n, I.m, I.r, I.n, true);
-    cb.zero(I.S + I.n + size_t(I.n) * I.m, I.m, I.r, I.r);
-    // gather C_top (n x w)
-    int s = 0;
-    for (int j : I.xp) {
-      BlkRef b = p2p_ref(W, i, j, false);
-      cb.add(b.p, b.ld, I.C + size_t(I.soff[s]) * I.n, I.n, I.n, W.n[j], b.trans);
-      s++;
-    }
-    for (int j : I.yp) {
-      BlkRef b = xy_ref(W, i, j, false);
-      cb.add(b.p, b.ld, I.C + size_t(I.soff[s]) * I.n, I.n, I.n, W.r[j]);
-      s++;
-    }
-    cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
   }
+  fill_off[np] = int(fh.size());
   const int no = int(own.size());
-  hmark(2);
-  tm_.begin(PH_GATHER);
-  launch_copies(cb, ws_, st_, s_);
-  static const char* dump_dir = getenv("IFMM_DUMP_SINGULAR");
-  std::vector<double*> Sbak;
-  if (dump_dir)
-    for (int u = 0; u < no; u++) {
-      const PivInfo& I = P[own[u]];
-      Sbak.push_back(ws_.alloc_n<double>(size_t(I.m) * I.m));
-      CK(cudaMemcpyAsync(Sbak.back(), I.S, sizeof(double) * I.m * I.m, cudaMemcpyDeviceToDevice, s_));
-    }
+  // per-batch device results of this rank's pivots / fills
   double* d_nS = ws_.alloc_n<double>(std::max(1, no));
   double* d_nSi = ws_.alloc_n<double>(std::max(1, no));
   int* d_info = ws_.alloc_n<int>(std::max(1, no));
-  if (no > 0) {
-    const MatDesc* dmd = upload(ws_, md, s_, st_);
-    int maxm = 0;
-    for (auto& d : md) maxm = std::max(maxm, d.m);
-    tm_.begin(PH_GJ);
-    launch_norm1(dmd, no, maxm, d_nS, s_);
-    work_->gj_side.ensure();
-    int gmaxm = 0;  // whole batch across ranks (blocking scheme as on one GPU)
-    for (const PivInfo& I : P) gmaxm = std::max(gmaxm, I.m);
-    batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &work_->gj_side, np, gmaxm);
-    launch_norm1(dmd, no, maxm, d_nSi, s_);
-    launch_norm1_estimate(dmd, no, maxm, d_nSi, d_nS, cond_limit_, s_);
-  }
-  hmark(3);
-  // records + X = S^-1 C
-  GemmBatch gb;
-  for (int t : own) {
-    PivInfo& I = P[t];
-    RecordH R{};
-    R.level = k;
-    R.index = I.i;
-    R.n = I.n;
-    R.r = I.r;
-    R.w = I.w;
-    R.sinv = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * std::max(1, I.n));
-    R.xtop = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
-    R.pos = nullptr;  // set by finish_level (one block per level)
-    I.rec = int(F_->recs.size());
-    F_->recs.push_back(R);
-    std::vector<SlotRef> sl;
-    for (int j : I.xp) sl.push_back({0, j, W.n[j]});
-    for (int j : I.yp) sl.push_back({1, j, W.r[j]});
-    sl.push_back({1, I.i, I.r});
-    rec_slots_.push_back(sl);
-    const int wl = I.w - I.r;
-    {
-      const double m = I.m, n = I.n, w = I.w, h = wl;
-      F_->fl_exec += 2.0 * m * m * m + 2.0 * m * n * h;
-      F_->fl_ref += 2.0 / 3.0 * m * m * m + 2.0 * m * m * w + 2.0 * h * n * w;
-      F_->solve_bytes += 8.0 * (n * n + 2.0 * n * w);
-    }
-    cb.add(I.S, I.m, R.sinv, I.n, I.n, I.n);
-    cb.add(I.S + size_t(I.n) * I.m, I.m, R.xtop + size_t(wl) * I.n, I.n, I.n, I.r, false, -1.0);
-    cb.add(I.S + I.n + size_t(I.n) * I.m, I.m, I.Xb + size_t(wl) * I.r, I.r, I.r, I.r, false, -1.0);
-    gb.add(I.S, I.m, I.C, I.n, R.xtop, I.n, I.n, wl, I.n, 1.0, 0.0);
-    gb.add(I.S + I.n, I.m, I.C, I.n, I.Xb, I.r, I.r, wl, I.n, 1.0, 0.0);
-  }
-  tm_.begin(PH_GATHER);
-  launch_copies(cb, ws_, st_, s_);
-  tm_.begin(PH_XGEMM);
-  launch_grouped_gemm(gb, false, false, ws_, st_, s_);
-  tm_.end();
-  // symmetric Schur update on the block upper triangle: target -= C_a^T X_b,
-  // one concatenated product per pivot (IFMM_SCHUR_GROUPED: one GEMM per block).
-  // Targets are created (presence + storage) for every pivot of the batch on
-  // every rank that stores them; only the owner computes.
-  static const bool per_block = getenv("IFMM_SCHUR_GROUPED") != nullptr;
-  SchurBatch sbat;
-  for (int t = 0; t < np; t++) {
-    PivInfo& I = P[t];
-    const int nx = int(I.xp.size()), ny = int(I.yp.size());
-    const int ns = nx + ny + 1;
-    const RecordH* R = I.own ? &F_->recs[I.rec] : nullptr;
-    const int pv = (per_block || !I.own) ? -1 : sbat.begin_pivot(I.C, R->xtop, I.n, I.soff);
-    auto slot_cluster = [&](int s) { return s < nx ? I.xp[s] : (s < nx + ny ? I.yp[s - nx] : I.i); };
-    for (int a = 0; a < ns; a++)
-      for (int b = a; b < ns; b++) {
-        const bool ax = a < nx, bx = b < nx;
-        const int ja = slot_cluster(a), jb = slot_cluster(b);
-        const int da = I.soff[a + 1] - I.soff[a], db = I.soff[b + 1] - I.soff[b];
-        if (a == ns - 1 && b == ns - 1) {
-          BlkRef M = m2l_ref(W, I.i, I.i, true);
-          if (I.own) cb.add(I.Xb + size_t(I.soff[b]) * I.r, I.r, M.p, M.ld, I.r, I.r, false, 1.0, true);
-          pres(W.pm, W, I.i, I.i) = 1;
-          continue;
-        }
-        BlkRef tgt;
-        if (ax && bx) {
-          tgt = p2p_ref(W, ja, jb, true);
-          set_pp(W, ja, jb, 1);
-        } else if (ax && !bx) {
-          tgt = xy_ref(W, ja, jb, true);
-          pres(W.px, W, ja, jb) = 1;
-        } else {
-          tgt = m2l_ref(W, ja, jb, true);
-          set_pm(W, ja, jb, 1);
-        }
-        if (da == 0 || db == 0 || !I.own) continue;
-        F_->fl_schur += 2.0 * I.n * da * db;
-        if (per_block)
-          gb.add(I.C + size_t(I.soff[a]) * I.n, I.n, R->xtop + size_t(I.soff[b]) * I.n, I.n, tgt.p, tgt.ld, da, db,
-                 I.n, -1.0, 1.0, tgt.trans);
-        else
-          sbat.set_target(pv, a, b, tgt.p, tgt.ld, tgt.trans);
-      }
-    if (!per_block && I.own) sbat.finish_pivot(pv);
-  }
-  tm_.begin(PH_SCHUR);
-  if (per_block) launch_grouped_gemm(gb, true, false, ws_, st_, s_);
-  else launch_schur(sbat, ws_, st_, s_);
-  tm_.begin(PH_GATHER);
-  launch_copies(cb, ws_, st_, s_);
-  tm_.end();
-  hmark(4);
-  // fill-in compression (reference order: hybrid pairs sorted, then P2P pairs
-  // sorted).  The fill list covers every pivot (its outcomes drive the
-  // replicated presence flags); only own pivots' fills are compressed here.
-  CompressBatch cbz;
-  cbz.chain_off.assign(1, 0);
-  cbz.p2p_off.assign(1, 0);
-  struct FillHost { int kind, p, q, piv, dev; };  // dev: index into cbz.fills or -1
-  std::vector<FillHost> fh;
-  auto add_fill = [&](int kind, int p, int q, int t) {
-    BlkRef M = m2l_ref(W, p, q, true);
-    if (!P[t].own) {
-      fh.push_back({kind, p, q, t, -1});
-      return -1;
-    }
-    FillDesc D{};
-    D.kind = kind;
-    D.p = p;
-    D.q = q;
-    if (kind == FILL_HYBRID) {
-      BlkRef F = xy_ref(W, q, p, false);
-      D.F = F.p;
-      D.ldF = W.n[q];
-      D.transF = 1;
-      D.rows = W.r[p];
-    } else {
-      BlkRef F = p2p_ref(W, p, q, false);
-      D.F = F.p;
-      D.ldF = F.ld;
-      D.transF = 0;
-      D.rows = W.n[p];
-    }
-    D.cols = W.n[q];
-    D.n_p = W.n[p];
-    D.n_q = W.n[q];
-    D.Up = W.U[p];
-    D.Uq = W.U[q];
-    D.M = M.p;
-    D.ldM = M.ld;
-    D.transM = M.trans ? 1 : 0;
-    D.Kf = std::max(1, std::min(96, std::min(D.rows, D.cols)));
-    D.out = ws_.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
-    cbz.fills.push_back(D);
-    fh.push_back({kind, p, q, t, int(cbz.fills.size()) - 1});
-    return int(cbz.fills.size()) - 1;
-  };
-  std::vector<int> fill_off(np + 1, 0);  // fills of pivot t: fh[fill_off[t] .. fill_off[t+1])
-  for (int t = 0; t < np; t++) {
-    PivInfo& I = P[t];
-    fill_off[t] = int(fh.size());
-    std::vector<int> ps(I.yp);
-    ps.push_back(I.i);
-    std::sort(ps.begin(), ps.end());
-    std::vector<std::vector<int>> byq(I.xp.size());
-    for (int p : ps)
-      for (size_t u = 0; u < I.xp.size(); u++)
-        if (T.in_il(p, I.xp[u])) {
-          const int f = add_fill(FILL_HYBRID, p, I.xp[u], t);
-          if (f >= 0) byq[u].push_back(f);
-        }
-    for (size_t u = 0; u < I.xp.size(); u++)
-      if (!byq[u].empty()) {
-        cbz.chain.insert(cbz.chain.end(), byq[u].begin(), byq[u].end());
-        cbz.chain_off.push_back(int(cbz.chain.size()));
-        cbz.chain_q.push_back(I.xp[u]);
-      }
-    for (size_t a = 0; a < I.xp.size(); a++)
-      for (size_t b = a + 1; b < I.xp.size(); b++)
-        if (T.in_il(I.xp[a], I.xp[b])) {
-          const int f = add_fill(FILL_P2P, I.xp[a], I.xp[b], t);
-          if (f >= 0) cbz.p2p.push_back(f);
-        }
-    if (I.own) cbz.p2p_off.push_back(int(cbz.p2p.size()));
-  }
-  fill_off[np] = int(fh.size());
-  cbz.rank_host = W.r.data();
-  for (const FillHost& h : fh) {  // worker shapes from the whole batch across ranks
-    const int rows = h.kind == FILL_HYBRID ? W.r[h.p] : W.n[h.p];
-    cbz.shape_mx = std::max(cbz.shape_mx, std::max(std::max(W.n[h.p], W.n[h.q]), std::max(rows, W.n[h.q])));
-  }
-  cbz.shape_nf = int(fh.size());
-  const size_t nfill = cbz.fills.size();
+  const size_t nfill = size_t(n_own_fills);
   FillState* d_state = ws_.alloc_n<FillState>(std::max<size_t>(1, nfill));
   int* d_stats = ws_.alloc_n<int>(4);
   CK(cudaMemsetAsync(d_stats, 0, 16, s_));
+  static const char* dump_dir = getenv("IFMM_DUMP_SINGULAR");
   static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
-  hmark(5);
-  tm_.begin(PH_COMPRESS);
-  if (nfill) run_compression(cbz, tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_state, d_stats, ws_, st_, s_, dbg ? 1 : 0);
-  tm_.end();
-  hmark(6);
+  static const bool per_block = getenv("IFMM_SCHUR_GROUPED") != nullptr;  // debug: one GEMM per Schur block
+  std::vector<double*> Sbak(no, nullptr);
+  hmark(2);
+  // Own pivots are processed in chunks: every phase of a chunk is launched
+  // before the host prepares the next one, so host descriptor work overlaps
+  // device work (a batch of 1,820 leaf pivots otherwise leaves the GPU idle
+  // while its descriptors are built).  Pivots of a batch are independent, and
+  // kernel shapes come from the whole batch (np, gmaxm, shape_mx, fh.size()),
+  // so chunking changes no arithmetic.
+  // measured at C3: chunks of 384 leaf pivots cost more (launch tails, per-chunk host work) than the
+  // overlap gains, so one chunk per batch by default (IFMM_CHUNK: experiments)
+  static const int chunk_target = getenv("IFMM_CHUNK") ? std::max(1, atoi(getenv("IFMM_CHUNK"))) : (1 << 30);
+  const int nchunks = std::max(1, (no + chunk_target - 1) / chunk_target);
+  for (int ch = 0; ch < nchunks && no > 0; ch++) {
+    const int u0 = int(int64_t(no) * ch / nchunks), u1 = int(int64_t(no) * (ch + 1) / nchunks);
+    const int nc_ = u1 - u0;
+    CopyBatch cb;
+    std::vector<MatDesc> md;
+    for (int u = u0; u < u1; u++) {
+      PivInfo& I = P[own[u]];
+      const int i = I.i;
+      I.S = ws_.alloc_n<double>(size_t(I.m) * I.m);
+      I.C = ws_.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
+      I.Xb = ws_.alloc_n<double>(size_t(std::max(1, I.r)) * I.w);
+      int* ipiv = ws_.alloc_n<int>(I.m);
+      md.push_back(MatDesc{I.S, I.m, I.m, ipiv, i});
+      // gather S
+      BlkRef Pii = p2p_ref(W, i, i, true);
+      cb.add(Pii.p, Pii.ld, I.S, I.m, I.n, I.n);
+      cb.add(W.U[i], I.n, I.S + size_t(I.n) * I.m, I.m, I.n, I.r);
+      cb.add(W.U[i], I.n, I.S + I.n, I.m, I.r, I.n, true);
+      cb.zero(I.S + I.n + size_t(I.n) * I.m, I.m, I.r, I.r);
+      // gather C_top (n x w)
+      int s = 0;
+      for (int j : I.xp) {
+        BlkRef b = p2p_ref(W, i, j, false);
+        cb.add(b.p, b.ld, I.C + size_t(I.soff[s]) * I.n, I.n, I.n, W.n[j], b.trans);
+        s++;
+      }
+      for (int j : I.yp) {
+        BlkRef b = xy_ref(W, i, j, false);
+        cb.add(b.p, b.ld, I.C + size_t(I.soff[s]) * I.n, I.n, I.n, W.r[j]);
+        s++;
+      }
+      cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
+    }
+    tm_.begin(PH_GATHER);
+    launch_copies(cb, ws_, st_, s_);
+    if (dump_dir)
+      for (int u = u0; u < u1; u++) {
+        const PivInfo& I = P[own[u]];
+        Sbak[u] = ws_.alloc_n<double>(size_t(I.m) * I.m);
+        CK(cudaMemcpyAsync(Sbak[u], I.S, sizeof(double) * I.m * I.m, cudaMemcpyDeviceToDevice, s_));
+      }
+    {
+      const MatDesc* dmd = upload(ws_, md, s_, st_);
+      int maxm = 0;
+      for (auto& d : md) maxm = std::max(maxm, d.m);
+      tm_.begin(PH_GJ);
+      launch_norm1(dmd, nc_, maxm, d_nS + u0, s_);
+      work_->gj_side.ensure();
+      // blocking scheme from the whole batch (across chunks and ranks): same arithmetic as one launch
+      batched_gj_inverse(md, dmd, d_info + u0, ws_, st_, s_, &work_->gj_side, np, gmaxm);
+      launch_norm1(dmd, nc_, maxm, d_nSi + u0, s_);
+      launch_norm1_estimate(dmd, nc_, maxm, d_nSi + u0, d_nS + u0, cond_limit_, s_);
+    }
+    hmark(3);
+    // records + X = S^-1 C
+    GemmBatch gb;
+    for (int u = u0; u < u1; u++) {
+      PivInfo& I = P[own[u]];
+      RecordH R{};
+      R.level = k;
+      R.index = I.i;
+      R.n = I.n;
+      R.r = I.r;
+      R.w = I.w;
+      R.sinv = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * std::max(1, I.n));
+      R.xtop = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
+      R.pos = nullptr;  // set by finish_level (one block per level)
+      I.rec = int(F_->recs.size());
+      F_->recs.push_back(R);
+      std::vector<SlotRef> sl;
+      for (int j : I.xp) sl.push_back({0, j, W.n[j]});
+      for (int j : I.yp) sl.push_back({1, j, W.r[j]});
+      sl.push_back({1, I.i, I.r});
+      rec_slots_.push_back(sl);
+      const int wl = I.w - I.r;
+      {
+        const double m = I.m, n = I.n, w = I.w, h = wl;
+        F_->fl_exec += 2.0 * m * m * m + 2.0 * m * n * h;
+        F_->fl_ref += 2.0 / 3.0 * m * m * m + 2.0 * m * m * w + 2.0 * h * n * w;
+        F_->solve_bytes += 8.0 * (n * n + 2.0 * n * w);
+      }
+      cb.add(I.S, I.m, R.sinv, I.n, I.n, I.n);
+      cb.add(I.S + size_t(I.n) * I.m, I.m, R.xtop + size_t(wl) * I.n, I.n, I.n, I.r, false, -1.0);
+      cb.add(I.S + I.n + size_t(I.n) * I.m, I.m, I.Xb + size_t(wl) * I.r, I.r, I.r, I.r, false, -1.0);
+      gb.add(I.S, I.m, I.C, I.n, R.xtop, I.n, I.n, wl, I.n, 1.0, 0.0);
+      gb.add(I.S + I.n, I.m, I.C, I.n, I.Xb, I.r, I.r, wl, I.n, 1.0, 0.0);
+    }
+    tm_.begin(PH_GATHER);
+    launch_copies(cb, ws_, st_, s_);
+    tm_.begin(PH_XGEMM);
+    launch_grouped_gemm(gb, false, false, ws_, st_, s_);
+    tm_.end();
+    // symmetric Schur update on the block upper triangle: target -= C_a^T X_b,
+    // one concatenated product per pivot (IFMM_SCHUR_GROUPED: one GEMM per block)
+    SchurBatch sbat;
+    for (int u = u0; u < u1; u++) {
+      PivInfo& I = P[own[u]];
+      const int nx = int(I.xp.size()), ny = int(I.yp.size());
+      const int ns = nx + ny + 1;
+      const RecordH& R = F_->recs[I.rec];
+      const int pv = per_block ? -1 : sbat.begin_pivot(I.C, R.xtop, I.n, I.soff);
+      auto slot_cluster = [&](int s) { return s < nx ? I.xp[s] : (s < nx + ny ? I.yp[s - nx] : I.i); };
+      for (int a = 0; a < ns; a++)
+        for (int b = a; b < ns; b++) {
+          const bool ax = a < nx, bx = b < nx;
+          const int ja = slot_cluster(a), jb = slot_cluster(b);
+          const int da = I.soff[a + 1] - I.soff[a], db = I.soff[b + 1] - I.soff[b];
+          if (a == ns - 1 && b == ns - 1) {
+            BlkRef M = m2l_ref(W, I.i, I.i, true);
+            cb.add(I.Xb + size_t(I.soff[b]) * I.r, I.r, M.p, M.ld, I.r, I.r, false, 1.0, true);
+            pres(W.pm, W, I.i, I.i) = 1;
+            continue;
+          }
+          BlkRef tgt;
+          if (ax && bx) {
+            tgt = p2p_ref(W, ja, jb, true);
+            set_pp(W, ja, jb, 1);
+          } else if (ax && !bx) {
+            tgt = xy_ref(W, ja, jb, true);
+            pres(W.px, W, ja, jb) = 1;
+          } else {
+            tgt = m2l_ref(W, ja, jb, true);
+            set_pm(W, ja, jb, 1);
+          }
+          if (da == 0 || db == 0) continue;
+          F_->fl_schur += 2.0 * I.n * da * db;
+          if (per_block)
+            gb.add(I.C + size_t(I.soff[a]) * I.n, I.n, R.xtop + size_t(I.soff[b]) * I.n, I.n, tgt.p, tgt.ld, da,
+                   db, I.n, -1.0, 1.0, tgt.trans);
+          else
+            sbat.set_target(pv, a, b, tgt.p, tgt.ld, tgt.trans);
+        }
+      if (!per_block) sbat.finish_pivot(pv);
+    }
+    tm_.begin(PH_SCHUR);
+    if (per_block) launch_grouped_gemm(gb, true, false, ws_, st_, s_);
+    else launch_schur(sbat, ws_, st_, s_);
+    tm_.begin(PH_GATHER);
+    launch_copies(cb, ws_, st_, s_);
+    tm_.end();
+    hmark(4);
+    // fill-in compression of the chunk's fills (chains are per cluster, and
+    // the chunk's clusters are disjoint from every other pivot's)
+    CompressBatch cbz;
+    cbz.chain_off.assign(1, 0);
+    cbz.p2p_off.assign(1, 0);
+    int dev0 = -1;
+    for (int u = u0; u < u1; u++) {
+      const int t = own[u];
+      PivInfo& I = P[t];
+      std::vector<std::vector<int>> byq(I.xp.size());
+      for (int f = fill_off[t]; f < fill_off[t + 1]; f++) {
+        const FillHost& h = fh[f];
+        if (dev0 < 0) dev0 = h.dev;
+        BlkRef M = m2l_ref(W, h.p, h.q, true);
+        FillDesc D{};
+        D.kind = h.kind;
+        D.p = h.p;
+        D.q = h.q;
+        if (h.kind == FILL_HYBRID) {
+          BlkRef F = xy_ref(W, h.q, h.p, false);
+          D.F = F.p;
+          D.ldF = W.n[h.q];
+          D.transF = 1;
+          D.rows = W.r[h.p];
+        } else {
+          BlkRef F = p2p_ref(W, h.p, h.q, false);
+          D.F = F.p;
+          D.ldF = F.ld;
+          D.transF = 0;
+          D.rows = W.n[h.p];
+        }
+        D.cols = W.n[h.q];
+        D.n_p = W.n[h.p];
+        D.n_q = W.n[h.q];
+        D.Up = W.U[h.p];
+        D.Uq = W.U[h.q];
+        D.M = M.p;
+        D.ldM = M.ld;
+        D.transM = M.trans ? 1 : 0;
+        D.Kf = std::max(1, std::min(96, std::min(D.rows, D.cols)));
+        D.out = ws_.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
+        const int fi = int(cbz.fills.size());
+        cbz.fills.push_back(D);
+        if (h.kind == FILL_HYBRID) {
+          const size_t x = size_t(std::find(I.xp.begin(), I.xp.end(), h.q) - I.xp.begin());
+          byq[x].push_back(fi);
+        } else {
+          cbz.p2p.push_back(fi);
+        }
+      }
+      for (size_t x = 0; x < I.xp.size(); x++)
+        if (!byq[x].empty()) {
+          cbz.chain.insert(cbz.chain.end(), byq[x].begin(), byq[x].end());
+          cbz.chain_off.push_back(int(cbz.chain.size()));
+          cbz.chain_q.push_back(I.xp[x]);
+        }
+      cbz.p2p_off.push_back(int(cbz.p2p.size()));
+    }
+    cbz.rank_host = W.r.data();
+    cbz.shape_mx = shape_mx;  // worker shapes from the whole batch (across chunks and ranks)
+    cbz.shape_nf = int(fh.size());
+    hmark(5);
+    tm_.begin(PH_COMPRESS);
+    if (!cbz.fills.empty())
+      run_compression(cbz, tol_, S_->d_probe, S_->probe_maxm, W.d_rank, d_state + dev0, d_stats, ws_, st_, s_,
+                      dbg ? 1 : 0);
+    tm_.end();
+    hmark(6);
+  }
+  // the other ranks' pivots: Schur targets and fill M2L blocks exist here too
+  // (presence flags; storage where this rank holds them)
+  for (int t = 0; t < np; t++) {
+    PivInfo& I = P[t];
+    if (I.own) continue;
+    const int nx = int(I.xp.size()), ny = int(I.yp.size());
+    const int ns = nx + ny + 1;
+    auto slot_cluster = [&](int s) { return s < nx ? I.xp[s] : (s < nx + ny ? I.yp[s - nx] : I.i); };
+    for (int a = 0; a < ns; a++)
+      for (int b = a; b < ns; b++) {
+        const int ja = slot_cluster(a), jb = slot_cluster(b);
+        if (a == ns - 1 && b == ns - 1) {
+          m2l_ref(W, I.i, I.i, true);
+          pres(W.pm, W, I.i, I.i) = 1;
+        } else if (a < nx && b < nx) {
+          p2p_ref(W, ja, jb, true);
+          set_pp(W, ja, jb, 1);
+        } else if (a < nx) {
+          xy_ref(W, ja, jb, true);
+          pres(W.px, W, ja, jb) = 1;
+        } else {
+          m2l_ref(W, ja, jb, true);
+          set_pm(W, ja, jb, 1);
+        }
+      }
+    for (int f = fill_off[t]; f < fill_off[t + 1]; f++) m2l_ref(W, fh[f].p, fh[f].q, true);
+  }
   // read back: pivot conditioning, ranks, fill outcomes, counters
   const auto t_sync0 = std::chrono::steady_clock::now();
   std::vector<double> nS(no), nSi(no);

@@ -179,15 +179,22 @@ __global__ void __launch_bounds__(SB, 4) solve_fwd1_kernel(const RecordH* __rest
     const int c = cb + seg;
     const bool ok = c < c1;
     const double* x = ok ? (c < n ? R.sinv + (size_t)c * n : R.xtop + (size_t)(c - n) * n) : R.sinv;
-    double s0 = 0.0, s1 = 0.0;
-    if (ok) {
-      int t = sl;
-      for (; t + W < n; t += 2 * W) {  // two independent loads in flight per step
-        s0 = fma(x[t], bsh[t], s0);
-        s1 = fma(x[t + W], bsh[t + W], s1);
-      }
-      if (t < n) s0 = fma(x[t], bsh[t], s0);
+    // all of the lane's elements of the column in flight at once (W is chosen
+    // so that 8 W >= n up to n = 256), streaming loads: records are read once
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int t = sl + u * W;
+      a[u] = (ok && t < n) ? __ldcs(x + t) : 0.0;
     }
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      const int t = sl + u * W;
+      if (t < n) s0 = fma(a[u], bsh[t], s0);
+      if (t + W < n) s1 = fma(a[u + 1], bsh[t + W], s1);
+    }
+    for (int t = sl + 8 * W; ok && t < n; t += W) s0 = fma(__ldcs(x + t), bsh[t], s0);
     double sv = s0 + s1;
     for (int o = W >> 1; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
     if (ok && sl == 0) {
@@ -217,6 +224,63 @@ __global__ void __launch_bounds__(SB, RC == 1 ? 4 : 2) solve_bwd_kernel(const Re
                   [&](int t, int q, double v) {
                     V[(R.xoff + r0 + t) * nrhs + q0 + q] = g[(size_t)(r0 + t) * nrhs + q0 + q] - v;
                   });
+  }
+}
+
+// Single right-hand side backward sweep: x = g - X_top v[pos] for the rows
+// [r0, r1) of chunk blockIdx.y.  Lanes own rows (J per lane), warps split the
+// columns; CB columns of loads are issued before their FMAs (streaming loads,
+// J x CB in flight per lane) -- the generic GEMV keeps too few bytes in flight
+// for the 64-row leaf records.  Partial sums meet in shared memory.
+template <int J>
+__global__ void __launch_bounds__(SB, J <= 4 ? 3 : 2) solve_bwd1_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                                       const int64_t* __restrict__ g_off, double* V,
+                                                                       const double* __restrict__ G) {
+  constexpr int CB = J <= 2 ? 8 : (J <= 4 ? 4 : 2);
+  extern __shared__ double red[];  // (32 J) x SWARPS
+  const RecordH R = recs[blockIdx.x];
+  const int n = R.n, w = R.w;
+  int r0, r1;
+  chunk_range(n, blockIdx.y, gridDim.y, 32, r0, r1);
+  if (r1 <= r0) return;
+  const double* g = G + g_off[rec0 + blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t0 = r0; t0 < r1; t0 += 32 * J) {
+    double acc[J];
+#pragma unroll
+    for (int j = 0; j < J; j++) acc[j] = 0.0;
+    for (int cb = warp * 32; cb < w; cb += SWARPS * 32) {
+      const double xl = (cb + lane < w) ? V[(int64_t)R.pos[cb + lane]] : 0.0;
+      const int cmax = min(32, w - cb);
+      for (int u0 = 0; u0 < cmax; u0 += CB) {
+        double a[CB][J];
+#pragma unroll
+        for (int u = 0; u < CB; u++) {
+          const double* col = R.xtop + (size_t)(cb + u0 + u) * n;
+#pragma unroll
+          for (int j = 0; j < J; j++) {
+            const int t = t0 + lane + 32 * j;
+            a[u][j] = (u0 + u < cmax && t < r1) ? __ldcs(col + t) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < CB; u++) {
+          const double xv = __shfl_sync(0xffffffffu, xl, (u0 + u) & 31);
+#pragma unroll
+          for (int j = 0; j < J; j++) acc[j] = fma(a[u][j], xv, acc[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < J; j++) red[(lane + 32 * j) * SWARPS + warp] = acc[j];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * J && t0 + e < r1; e += SB) {
+      double s = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < SWARPS; w2++) s += red[e * SWARPS + w2];
+      V[R.xoff + t0 + e] = g[t0 + e] - s;
+    }
+    __syncthreads();
   }
 }
 
@@ -569,8 +633,14 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     if (smem > 200 * 1024) invalid("solve: pivot block too large for the solve kernel");
     const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));
     static const bool fwd_old = getenv("IFMM_SOLVE_FWD_GEMV") != nullptr;  // debug: S^-1 b as a GEMV
-    if (RC == 1 && !fwd_old)
-      solve_fwd1_kernel<<<grid, SB, sizeof(double) * size_t(b.maxn), s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+    if (RC == 1 && !fwd_old) {
+      // column dots split finely: >= 8 CTAs per SM in total (few large records
+      // at coarse levels would otherwise leave most SMs idle), >= 32 columns each
+      const int nrec = std::max(1, b.rec1 - b.rec0);
+      const int want = std::max(2, (148 * 8 + nrec - 1) / nrec);
+      const dim3 g1(b.rec1 - b.rec0, std::max(1, std::min(want, (b.maxn + b.maxw) / 32)));
+      solve_fwd1_kernel<<<g1, SB, sizeof(double) * size_t(b.maxn), s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+    }
     else if (RC == 1) solve_fwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     else solve_fwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
@@ -607,7 +677,17 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
     const size_t smem = sizeof(double) * size_t(rr) * SWARPS * RC;
     const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));
-    if (RC == 1) solve_bwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
+    static const bool bwd_old = getenv("IFMM_SOLVE_BWD_OLD") != nullptr;  // debug: generic GEMV
+    if (RC == 1 && !bwd_old) {
+      // rows per lane from the chunk height (<= 64 rows: 2, <= 128: 4, else 8)
+      const int rows = (b.maxn + grid.y - 1) / grid.y;
+      if (rows <= 64)
+        solve_bwd1_kernel<2><<<grid, SB, sizeof(double) * 64 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+      else if (rows <= 128)
+        solve_bwd1_kernel<4><<<grid, SB, sizeof(double) * 128 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+      else
+        solve_bwd1_kernel<8><<<grid, SB, sizeof(double) * 256 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+    } else if (RC == 1) solve_bwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     else solve_bwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
     if (dist) share_runs(F, V, nr, b.bwd_runs, b.bwd_off, ws, xst, s);
