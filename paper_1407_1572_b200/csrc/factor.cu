@@ -157,7 +157,7 @@ class Factorizer {
   PhaseTimer tm_;
   WorkLevel cur_, prev_;
   // debug (IFMM_HOST_PROF): host ms per section of eliminate_batch, per level
-  double hsec_[8] = {0};
+  double hsec_[16] = {0};
   std::chrono::steady_clock::time_point hmark_;
   void hmark(int sec) {
     const auto now = std::chrono::steady_clock::now();
@@ -245,12 +245,18 @@ class Factorizer {
   int stamp_ = 0;
   // x-partners (live, coupled through P2P) and y-partners (eliminated, coupled
   // through M2P = P2L^T) of i, sorted (ifmm/solver.py:220-229); scans the 7x7 window
+  // Without a dense-kept well-separated fill at this level every coupling is
+  // between neighbours (distance-2 fills are always interaction-list pairs and
+  // are compressed), so the 3^d neighbour list replaces the 7^d window scan.
   void partners(WorkLevel& W, int i, std::vector<int>& xp, std::vector<int>& yp) {
     const Topo& T = *W.T;
     xp.clear();
     yp.clear();
-    for (int t = T.wc_off[i]; t < T.wc_off[i + 1]; t++) {
-      const int j = T.wc[t];
+    const bool near = F_->stats[W.k].dense_kept == 0;
+    const int t0 = near ? T.nbr_off[i] : T.wc_off[i], t1 = near ? T.nbr_off[i + 1] : T.wc_off[i + 1];
+    const int* lst = near ? T.nbr.data() : T.wc.data();
+    for (int t = t0; t < t1; t++) {
+      const int j = lst[t];
       if (j == i) continue;
       if (!W.dead[j] && pp_present(W, i, j)) xp.push_back(j);
       if (pres(W.px, W, i, j)) yp.push_back(j);
@@ -415,13 +421,14 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   // long as every partner is a neighbour; an incompressible well-separated
   // fill kept dense can break it).  Conflicting pivots are deferred to a
   // follow-up batch of the same colour, preserving their relative order.
+  std::vector<std::vector<int>> gxp, gyp;  // partners of the kept pivots (reused below)
   {
     std::vector<int> keep;
     deferred.clear();
     if (mark_.size() != size_t(W.nc)) mark_.assign(W.nc, -1);
     ++stamp_;
+    std::vector<int> xp, yp;
     for (int i : piv) {
-      std::vector<int> xp, yp;
       partners(W, i, xp, yp);
       bool clash = mark_[i] == stamp_;
       for (int j : xp) clash |= mark_[j] == stamp_;
@@ -434,6 +441,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       for (int j : xp) mark_[j] = stamp_;
       for (int j : yp) mark_[j] = stamp_;
       keep.push_back(i);
+      gxp.push_back(xp);
+      gyp.push_back(yp);
     }
     piv.swap(keep);
   }
@@ -471,7 +480,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     I.m = I.n + I.r;
     I.own = mine(W, i);
     I.rec = -1;
-    partners(W, i, I.xp, I.yp);
+    I.xp.swap(gxp[t]);
+    I.yp.swap(gyp[t]);
     I.soff.assign(1, 0);
     for (int j : I.xp) I.soff.push_back(I.soff.back() + W.n[j]);
     for (int j : I.yp) I.soff.push_back(I.soff.back() + W.r[j]);
@@ -525,7 +535,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
   static const bool per_block = getenv("IFMM_SCHUR_GROUPED") != nullptr;  // debug: one GEMM per Schur block
   std::vector<double*> Sbak(no, nullptr);
-  hmark(2);
+  hmark(11);
   // Own pivots are processed in chunks: every phase of a chunk is launched
   // before the host prepares the next one, so host descriptor work overlaps
   // device work (a batch of 1,820 leaf pivots otherwise leaves the GPU idle
@@ -569,8 +579,10 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       }
       cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
     }
+    hmark(12);
     tm_.begin(PH_GATHER);
     launch_copies(cb, ws_, st_, s_);
+    hmark(2);
     if (dump_dir)
       for (int u = u0; u < u1; u++) {
         const PivInfo& I = P[own[u]];
@@ -623,11 +635,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       gb.add(I.S, I.m, I.C, I.n, R.xtop, I.n, I.n, wl, I.n, 1.0, 0.0);
       gb.add(I.S + I.n, I.m, I.C, I.n, I.Xb, I.r, I.r, wl, I.n, 1.0, 0.0);
     }
+    hmark(8);
     tm_.begin(PH_GATHER);
     launch_copies(cb, ws_, st_, s_);
     tm_.begin(PH_XGEMM);
     launch_grouped_gemm(gb, false, false, ws_, st_, s_);
     tm_.end();
+    hmark(9);
     // symmetric Schur update on the block upper triangle: target -= C_a^T X_b,
     // one concatenated product per pivot (IFMM_SCHUR_GROUPED: one GEMM per block)
     SchurBatch sbat;
@@ -670,6 +684,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         }
       if (!per_block) sbat.finish_pivot(pv);
     }
+    hmark(10);
     tm_.begin(PH_SCHUR);
     if (per_block) launch_grouped_gemm(gb, true, false, ws_, st_, s_);
     else launch_schur(sbat, ws_, st_, s_);
@@ -790,6 +805,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   CK(cudaMemcpyAsync(W.r.data(), W.d_rank, sizeof(int) * W.nc, cudaMemcpyDeviceToHost, s_));
   CK(cudaStreamSynchronize(s_));
   const auto t_sync1 = std::chrono::steady_clock::now();
+  hmark(13);
   if (F_->host_lvl_ms.size() <= size_t(k)) F_->host_lvl_ms.resize(k + 1, std::array<double, 2>{});
   F_->host_lvl_ms[k][0] += std::chrono::duration<double, std::milli>(t_sync0 - t_batch0).count();
   F_->host_lvl_ms[k][1] += std::chrono::duration<double, std::milli>(t_sync1 - t_sync0).count();
@@ -1182,8 +1198,10 @@ FactorH* Factorizer::run() {
     finish_level(rec_begin);
     if (hprof) {
       fprintf(stderr, "host level %d: finish %.1f ms, level total %.1f ms\n", k, since(tf0), since(tl0));
-      fprintf(stderr, "  batches: guard %.1f sync %.1f gather %.1f gj %.1f rec+x+schur %.1f fills %.1f compress %.1f readback %.1f\n",
-              hsec_[0], hsec_[1], hsec_[2], hsec_[3], hsec_[4], hsec_[5], hsec_[6], hsec_[7]);
+      fprintf(stderr, "  batches: guard %.1f sync %.1f meta %.1f gatherdesc %.1f gatherlaunch %.1f gj %.1f records %.1f "
+              "xlaunch %.1f schurloop %.1f schurlaunch %.1f fills %.1f compress %.1f wait %.1f post %.1f\n",
+              hsec_[0], hsec_[1], hsec_[11], hsec_[12], hsec_[2], hsec_[3], hsec_[8], hsec_[9], hsec_[10], hsec_[4],
+              hsec_[5], hsec_[6], hsec_[13], hsec_[7]);
     }
     for (double& h : hsec_) h = 0.0;
     F_->r_m = std::max(F_->r_m, F_->stats[k].max_rank);
