@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
     PROF_ACC(0);
     const int k = ao.k;
     S.k = k;
-    if (!ao.converged && kmax < D.Kf && k >= kmax && k < min(rows, cols)) {
+    if (!ao.converged && k >= kmax && k < min(rows, cols) && (kmax < D.Kf || D.Kf < D.kfull)) {
       S.status = 2;  // needs more crosses than this worker holds
       if (g.rank() == 0) state[f] = S;
       g.sync();
@@ -594,6 +594,7 @@ void test_recompress_one(const double* dF, int m, int n, double tol, const int* 
   D.n_p = m;
   D.n_q = n;
   D.Kf = std::max(1, std::min(96, std::min(m, n)));
+  D.kfull = D.Kf;
   D.out = d_out;
   std::vector<FillDesc> v(1, D);
   const FillDesc* dfd = upload(ws, v, s, st);
@@ -652,10 +653,18 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   static bool jac_set = false;
   if (!jac_set) {
     CK(cudaMemcpyToSymbolAsync(g_jac_rt, &jac_rt, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-    static const int gram = getenv("IFMM_GRAM") ? atoi(getenv("IFMM_GRAM")) : 1;
-    CK(cudaMemcpyToSymbolAsync(g_gram, &gram, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyToSymbolAsync(g_jac_reg, &jac_reg, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     jac_set = true;
+  }
+  {
+    // The Gram routes (K1 recompression through the cross Gram matrices, new
+    // directions through H^T H) lose accuracy ~ eps * cond^2; that is far below
+    // the truncation for tol >= 1e-9, but at tolerances near machine precision
+    // (the reference default 1e-14) the duplicated directions make pivots
+    // singular, so the Householder routes run there.
+    static const int gram_env = getenv("IFMM_GRAM") ? atoi(getenv("IFMM_GRAM")) : 1;
+    const int gram = (gram_env != 0 && tol >= 1e-9) ? 1 : 0;
+    CK(cudaMemcpyToSymbolAsync(g_gram, &gram, sizeof(int), 0, cudaMemcpyHostToDevice, s));
   }
   if (prof) {
     const int one = 1;
@@ -664,6 +673,8 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     CK(cudaMemcpyToSymbolAsync(g_cyc, z, sizeof z, 0, cudaMemcpyHostToDevice, s));
   }
   const FillDesc* dfd = upload(ws, cb.fills, s, st);
+  bool may_redo = false;  // fills whose reference cross cap exceeds this pass's buffers
+  for (const FillDesc& D : cb.fills) may_redo |= D.kfull > D.Kf;
   // grid for `work` items: CTA workers, or warp workers packed WPB per CTA
   auto grid_for = [&](int work, int cta_per_sm, int warps_per_sm) {
     return wmode ? resident_grid(ceil_div(work, WPB), warps_per_sm / WPB) : resident_grid(work, cta_per_sm);
@@ -698,6 +709,32 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       aca_recompress_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
                                                                slot, MR, MC, KK, 0);
       CK_LAUNCH();
+    }
+    if (may_redo) {
+      // fills that used all Kf (<= 96) crosses of the first pass without
+      // converging continue up to the reference's min(m, n) crosses with
+      // buffers of that size (few fills, coarse levels at high accuracy)
+      std::vector<FillState> hs(nf);
+      CK(cudaMemcpyAsync(hs.data(), d_state, sizeof(FillState) * nf, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      int nredo = 0;
+      for (int f = 0; f < nf; f++) {
+        FillDesc& D = cb.fills[f];
+        if (hs[f].status != 2 || D.kfull <= D.Kf) continue;
+        D.Kf = D.kfull;
+        D.out = ws.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
+        KK = std::max(KK, D.Kf);
+        nredo++;
+      }
+      if (nredo > 0) {
+        dfd = upload(ws, cb.fills, s, st);
+        const size_t slot = k1_slot(KK);
+        const int grid = std::max(1, std::min(nredo, 148));
+        double* scr = ws.alloc_n<double>(slot * grid);
+        aca_recompress_kernel<CtaGroup><<<grid, bs_big, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
+                                                                slot, MR, MC, KK, 1);
+        CK_LAUNCH();
+      }
     }
   }
   const size_t dslot = 3 * size_t(MX) * KK + size_t(KK) * KK + 3 * size_t(KK) + 64;

@@ -29,7 +29,9 @@ struct FillDesc {
   double* M;    // M2L(p,q) storage
   int ldM, transM;
   double* out;  // left (rows x Kf) | right (cols x Kf) | sig (Kf)
-  int Kf;       // max crosses / stored rank
+  int Kf;       // max crosses / stored rank of this pass (buffer capacity of `out`)
+  int kfull;    // the reference's cap: min(rows, cols) (ifmm/lowrank.py:188-191); a fill whose
+                // ACA reaches Kf < kfull crosses unconverged is redone with a kfull buffer
 };
 
 struct FillState {

@@ -28,6 +28,7 @@
 //   all-gathered), so every stored copy is current before it is read.
 #include <algorithm>
 #include <climits>
+#include <unordered_map>
 #include <thread>
 #include <chrono>
 #include <cmath>
@@ -48,6 +49,11 @@ struct WorkLevel {
   std::vector<double*> p2p, m2l, xy;  // nc*win
   std::vector<uint8_t> pp, pm, px;
   std::vector<uint8_t> dead;
+  // Pairs beyond the 7^d window (dense couplings that chained past +-3 cells)
+  // get table entries appended after the window part: ordered pair -> index,
+  // and per-cluster adjacency for the partner scan.
+  std::unordered_map<uint64_t, int> ovf;
+  std::vector<std::vector<int>> ovf_adj;
   int* d_rank = nullptr;
   Arena* arena = nullptr;  // zero-initialised blocks
 };
@@ -177,36 +183,65 @@ class Factorizer {
   bool holds2s(const WorkLevel& W, int s, int a, int b) const { return holds(W, s, a) || holds(W, s, b); }
   // level arenas hand out zeroed memory (slabs are cleared on creation/reset)
   double* zalloc(WorkLevel& W, size_t n) { return W.arena->alloc_n<double>(std::max<size_t>(1, n)); }
+  // Table index of the ordered pair (a, b): its window slot, else its overflow
+  // entry (created on demand when `create`), else -1.
+  int64_t pidx(WorkLevel& W, int a, int b, bool create) {
+    const int sl = W.T->slot(a, b);
+    if (sl >= 0) return int64_t(a) * W.win + sl;
+    const uint64_t key = (uint64_t(uint32_t(a)) << 32) | uint32_t(b);
+    auto it = W.ovf.find(key);
+    if (it != W.ovf.end()) return it->second;
+    if (!create) return -1;
+    const int64_t ix = int64_t(W.p2p.size());
+    W.ovf.emplace(key, int(ix));
+    W.p2p.push_back(nullptr);
+    W.m2l.push_back(nullptr);
+    W.xy.push_back(nullptr);
+    W.pp.push_back(0);
+    W.pm.push_back(0);
+    W.px.push_back(0);
+    if (W.ovf_adj.empty()) W.ovf_adj.resize(W.nc);
+    W.ovf_adj[a].push_back(b);
+    if (a != b) W.ovf_adj[b].push_back(a);
+    return ix;
+  }
   BlkRef p2p_ref(WorkLevel& W, int i, int j, bool alloc) {
     int a = std::min(i, j), b = std::max(i, j);
-    int sl = W.T->slot(a, b);
-    if (sl < 0) invalid("near-field block beyond the 7x7 window (dense fill too far)");
-    double*& p = W.p2p[size_t(a) * W.win + sl];
+    const int64_t ix = pidx(W, a, b, alloc);
+    if (ix < 0) return {nullptr, W.n[a], i > j};
+    double*& p = W.p2p[size_t(ix)];
     if (!p && alloc && holds2(W, a, b)) p = zalloc(W, size_t(W.n[a]) * W.n[b]);
     return {p, W.n[a], i > j};
   }
   BlkRef m2l_ref(WorkLevel& W, int i, int j, bool alloc) {
     int a = std::min(i, j), b = std::max(i, j);
-    int sl = W.T->slot(a, b);
-    if (sl < 0) invalid("M2L block beyond the 7x7 window");
-    double*& p = W.m2l[size_t(a) * W.win + sl];
+    const int64_t ix = pidx(W, a, b, alloc);
+    if (ix < 0) return {nullptr, W.rcap[a], i > j};
+    double*& p = W.m2l[size_t(ix)];
     if (!p && alloc && holds2(W, a, b)) p = zalloc(W, size_t(W.rcap[a]) * W.rcap[b]);
     return {p, W.rcap[a], i > j};
   }
   BlkRef xy_ref(WorkLevel& W, int i, int j, bool alloc) {
-    int sl = W.T->slot(i, j);
-    if (sl < 0) invalid("hybrid block beyond the 7x7 window");
-    double*& p = W.xy[size_t(i) * W.win + sl];
+    const int64_t ix = pidx(W, i, j, alloc);
+    if (ix < 0) return {nullptr, W.n[i], false};
+    double*& p = W.xy[size_t(ix)];
     if (!p && alloc && holds2(W, i, j)) p = zalloc(W, size_t(W.n[i]) * W.rcap[j]);
     return {p, W.n[i], false};
   }
-  uint8_t& pres(std::vector<uint8_t>& v, WorkLevel& W, int i, int j) {
-    return v[size_t(i) * W.win + W.T->slot(i, j)];
+  bool get_pres(const std::vector<uint8_t>& v, WorkLevel& W, int i, int j) {
+    const int64_t ix = pidx(W, i, j, false);
+    return ix >= 0 && v[size_t(ix)];
   }
-  bool pp_present(WorkLevel& W, int i, int j) { int a = std::min(i, j), b = std::max(i, j); return pres(W.pp, W, a, b); }
-  void set_pp(WorkLevel& W, int i, int j, uint8_t v) { int a = std::min(i, j), b = std::max(i, j); pres(W.pp, W, a, b) = v; }
-  void set_pm(WorkLevel& W, int i, int j, uint8_t v) { int a = std::min(i, j), b = std::max(i, j); pres(W.pm, W, a, b) = v; }
-  bool pm_present(WorkLevel& W, int i, int j) { int a = std::min(i, j), b = std::max(i, j); return pres(W.pm, W, a, b); }
+  void set_pres(std::vector<uint8_t>& v, WorkLevel& W, int i, int j, uint8_t val) {
+    const int64_t ix = pidx(W, i, j, val != 0);
+    if (ix >= 0) v[size_t(ix)] = val;
+  }
+  bool pp_present(WorkLevel& W, int i, int j) { return get_pres(W.pp, W, std::min(i, j), std::max(i, j)); }
+  void set_pp(WorkLevel& W, int i, int j, uint8_t v) { set_pres(W.pp, W, std::min(i, j), std::max(i, j), v); }
+  void set_pm(WorkLevel& W, int i, int j, uint8_t v) { set_pres(W.pm, W, std::min(i, j), std::max(i, j), v); }
+  bool pm_present(WorkLevel& W, int i, int j) { return get_pres(W.pm, W, std::min(i, j), std::max(i, j)); }
+  bool px_present(WorkLevel& W, int i, int j) { return get_pres(W.px, W, i, j); }
+  void set_px(WorkLevel& W, int i, int j, uint8_t v) { set_pres(W.px, W, i, j, v); }
 
   // IFMM_HOST_PROF: host ms between marks of the level start
   std::chrono::steady_clock::time_point hp_t_;
@@ -236,6 +271,8 @@ class Factorizer {
     W.pp.assign(size_t(W.nc) * W.win, 0);
     W.pm.assign(size_t(W.nc) * W.win, 0);
     W.px.assign(size_t(W.nc) * W.win, 0);
+    W.ovf.clear();
+    W.ovf_adj.clear();
     W.dead.assign(W.nc, 0);
     W.U.assign(W.nc, nullptr);
     W.d_rank = W.arena->alloc_n<int>(W.nc);
@@ -259,7 +296,19 @@ class Factorizer {
       const int j = lst[t];
       if (j == i) continue;
       if (!W.dead[j] && pp_present(W, i, j)) xp.push_back(j);
-      if (pres(W.px, W, i, j)) yp.push_back(j);
+      if (px_present(W, i, j)) yp.push_back(j);
+    }
+    if (!near && !W.ovf_adj.empty() && !W.ovf_adj[i].empty()) {  // couplings beyond the window
+      std::vector<int> o(W.ovf_adj[i]);
+      std::sort(o.begin(), o.end());
+      o.erase(std::unique(o.begin(), o.end()), o.end());
+      for (int j : o) {
+        if (j == i || W.T->slot(i, j) >= 0) continue;
+        if (!W.dead[j] && pp_present(W, i, j)) xp.push_back(j);
+        if (px_present(W, i, j)) yp.push_back(j);
+      }
+      std::sort(xp.begin(), xp.end());
+      std::sort(yp.begin(), yp.end());
     }
   }
   void start_leaf_level();
@@ -660,7 +709,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
           if (a == ns - 1 && b == ns - 1) {
             BlkRef M = m2l_ref(W, I.i, I.i, true);
             cb.add(I.Xb + size_t(I.soff[b]) * I.r, I.r, M.p, M.ld, I.r, I.r, false, 1.0, true);
-            pres(W.pm, W, I.i, I.i) = 1;
+            set_pres(W.pm, W, I.i, I.i, 1);
             continue;
           }
           BlkRef tgt;
@@ -669,7 +718,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
             set_pp(W, ja, jb, 1);
           } else if (ax && !bx) {
             tgt = xy_ref(W, ja, jb, true);
-            pres(W.px, W, ja, jb) = 1;
+            set_px(W, ja, jb, 1);
           } else {
             tgt = m2l_ref(W, ja, jb, true);
             set_pm(W, ja, jb, 1);
@@ -732,6 +781,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         D.ldM = M.ld;
         D.transM = M.trans ? 1 : 0;
         D.Kf = std::max(1, std::min(96, std::min(D.rows, D.cols)));
+        D.kfull = std::max(1, std::min(D.rows, D.cols));
         D.out = ws_.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
         const int fi = int(cbz.fills.size());
         cbz.fills.push_back(D);
@@ -774,13 +824,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         const int ja = slot_cluster(a), jb = slot_cluster(b);
         if (a == ns - 1 && b == ns - 1) {
           m2l_ref(W, I.i, I.i, true);
-          pres(W.pm, W, I.i, I.i) = 1;
+          set_pres(W.pm, W, I.i, I.i, 1);
         } else if (a < nx && b < nx) {
           p2p_ref(W, ja, jb, true);
           set_pp(W, ja, jb, 1);
         } else if (a < nx) {
           xy_ref(W, ja, jb, true);
-          pres(W.px, W, ja, jb) = 1;
+          set_px(W, ja, jb, 1);
         } else {
           m2l_ref(W, ja, jb, true);
           set_pm(W, ja, jb, 1);
@@ -905,7 +955,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
               state[h.dev].status, state[h.dev].k, state[h.dev].r, W.r[h.p]);
     if (gstat[f] != 0) continue;
     if (h.kind == FILL_HYBRID) {
-      pres(W.px, W, h.q, h.p) = 0;
+      set_px(W, h.q, h.p, 0);
       if (h.dev < 0) {
         BlkRef F = xy_ref(W, h.q, h.p, false);
         if (F.p) zero_dropped.zero(F.p, F.ld, W.n[h.q], W.r[h.p]);
@@ -936,7 +986,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       ys.push_back(I.i);
       for (int x : I.xp)
         for (int y : ys)
-          if (pres(W.px, W, x, y)) items.push_back({HALO_XY, x, y, 0});
+          if (px_present(W, x, y)) items.push_back({HALO_XY, x, y, 0});
       for (size_t a = 0; a < ys.size(); a++)
         for (size_t b = a; b < ys.size(); b++) {
           const int ja = std::min(ys[a], ys[b]), jb = std::max(ys[a], ys[b]);
