@@ -20,8 +20,10 @@ CASES = [
     (2, 4000, "log", 1e-3, 1e-10, 6, None),
     (2, 4000, "gaussian", 1e-3, 1e-10, 6, None),
     (2, 4000, "multiquadric", 1e-3, 1e-10, 6, None),
-    (2, 4000, "inverse_multiquadric", 1e-3, 1e-10, 6, None),
-    (2, 4000, "bessel_y0", 1e-3, 1e-10, 6, None),
+    (2, 4000, "inverse-multiquadric", 1e-3, 1e-10, 6, None),
+    (2, 4000, "inverse-quadric", 1e-3, 1e-10, 6, None),
+    (2, 4000, "helmholtz3d", 1e-3, 1e-10, 6, None),
+    (2, 4000, "bessel-y0", 1e-3, 1e-10, 6, None),
     (2, 4000, "biharmonic", 1e-3, 1e-10, 6, None),
     (2, 16384, "log", 1e-3, 1e-8, 4, 4),
     (2, 16384, "log", 1e-3, 1e-8, 4, 5),
