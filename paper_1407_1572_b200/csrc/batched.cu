@@ -61,8 +61,10 @@ void launch_copies(CopyBatch& b, Arena& ws, Staging& st, cudaStream_t s) {
   if (b.d.empty()) return;
   // one CTA per descriptor: split large blocks into column chunks (<= 16K
   // elements, multiples of 32 columns) so big gathers spread over the GPU
-  {
-    constexpr long long kChunk = 16384;
+  constexpr long long kChunk = 16384;
+  bool split = false;
+  for (const CopyDesc& D : b.d) split |= (long long)D.rows * D.cols > kChunk;
+  if (split) {
     std::vector<CopyDesc> out;
     out.reserve(b.d.size());
     for (const CopyDesc& D : b.d) {

@@ -347,11 +347,13 @@ void Factorizer::start_leaf_level() {
   W.r = L.r0;
   W.rcap = L.n;
   CopyBatch cb;
+  cb.d.reserve(size_t(W.nc) * 20);
   for (int i = 0; i < W.nc; i++) {
     if (!holds1(W, i)) continue;
     W.U[i] = zalloc(W, size_t(W.n[i]) * W.rcap[i]);
     cb.add(L.U[i], W.n[i], W.U[i], W.n[i], W.n[i], W.r0[i]);
   }
+  hprof_mark("leaf U");
   const Topo& T = *W.T;
   for (int i = 0; i < W.nc; i++) {
     for (int q = T.nbr_off[i]; q < T.nbr_off[i + 1]; q++) {
@@ -391,6 +393,7 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
   }
   W.rcap = W.n;
   CopyBatch cb;
+  cb.d.reserve(size_t(W.nc) * (4 + 9 * (1 << (2 * dim))));
   for (int i = 0; i < W.nc; i++) {
     if (!holds1(W, i)) continue;
     W.U[i] = zalloc(W, size_t(W.n[i]) * W.rcap[i]);
@@ -411,10 +414,20 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
     for (int q = T.nbr_off[i]; q < T.nbr_off[i + 1]; q++) {
       int j = T.nbr[q];
       if (j < i) continue;
-      bool any = false;
+      // present child M2L blocks of the pair (one table lookup each)
+      int nblk = 0;
+      int64_t bix[64];
+      int bab[64];
       for (int a = 0; a < nch; a++)
-        for (int b = 0; b < nch; b++) any |= pm_present(C, (i << dim) + a, (j << dim) + b);
-      if (!any) continue;
+        for (int b = 0; b < nch; b++) {
+          const int ca = (i << dim) + a, cbb = (j << dim) + b;
+          const int64_t ix = pidx(C, std::min(ca, cbb), std::max(ca, cbb), false);
+          if (ix >= 0 && C.pm[size_t(ix)]) {
+            bix[nblk] = ix;
+            bab[nblk++] = a * nch + b;
+          }
+        }
+      if (nblk == 0) continue;
       set_pp(W, i, j, 1);
       BlkRef P = p2p_ref(W, i, j, true);
       const bool build = mine(W, i) || mine(W, j);
@@ -428,17 +441,18 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
         }
       }
       if (!build || !P.p) continue;
-      for (int a = 0; a < nch; a++)
-        for (int b = 0; b < nch; b++) {
-          const int ca = (i << dim) + a, cbb = (j << dim) + b;
-          if (!pm_present(C, ca, cbb)) continue;
-          BlkRef M = m2l_ref(C, ca, cbb, false);
-          if (!M.p) {
-            if (nranks_ > 1) invalid("sharded transition: a child M2L block is not stored on the assembling rank");
-            continue;
-          }
-          cb.add(M.p, M.ld, P.p + off[i][a] + size_t(off[j][b]) * P.ld, P.ld, C.r[ca], C.r[cbb], M.trans);
+      for (int u = 0; u < nblk; u++) {
+        const int a = bab[u] / nch, b = bab[u] % nch;
+        const int ca = (i << dim) + a, cbb = (j << dim) + b;
+        const double* mp = C.m2l[size_t(bix[u])];
+        if (!mp) {
+          if (nranks_ > 1) invalid("sharded transition: a child M2L block is not stored on the assembling rank");
+          continue;
         }
+        // stored once as (min, max) with ld = rcap of the smaller index
+        const int lo = std::min(ca, cbb);
+        cb.add(mp, C.rcap[lo], P.p + off[i][a] + size_t(off[j][b]) * P.ld, P.ld, C.r[ca], C.r[cbb], ca > cbb);
+      }
     }
     for (int q = T.il_off[i]; q < T.il_off[i + 1]; q++) {
       int j = T.il[q];
