@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(SB, RC == 1 ? 4 : 2) solve_fwd_kernel(const Re
 // output is the dot of one column with b -- W-lane segments per column, no
 // cross-warp reduction, one barrier.  Chunk y of gridDim.y owns a range of
 // the n + w columns.
-__global__ void __launch_bounds__(SB, 4) solve_fwd1_kernel(const RecordH* __restrict__ recs, int rec0,
+__global__ void __launch_bounds__(SB, 3) solve_fwd1_kernel(const RecordH* __restrict__ recs, int rec0,
                                                            const int64_t* __restrict__ g_off, double* V, double* G) {
   extern __shared__ double sm[];
   double* bsh = sm;  // n
@@ -175,31 +175,57 @@ __global__ void __launch_bounds__(SB, 4) solve_fwd1_kernel(const RecordH* __rest
   __syncthreads();
   const int W = n > 128 ? 32 : (n > 64 ? 16 : 8);
   const int seg = lane / W, sl = lane & (W - 1), spw = 32 / W;
-  for (int cb = c0 + warp * spw; cb < c1; cb += SWARPS * spw) {
-    const int c = cb + seg;
-    const bool ok = c < c1;
-    const double* x = ok ? (c < n ? R.sinv + (size_t)c * n : R.xtop + (size_t)(c - n) * n) : R.sinv;
-    // all of the lane's elements of the column in flight at once (W is chosen
-    // so that 8 W >= n up to n = 256), streaming loads: records are read once
-    double a[8];
+  // two columns per segment and step: 16 loads per lane in flight (the sweep
+  // is latency-bound on long-scoreboard stalls with one)
+  const int stride = SWARPS * spw;
+  auto colp = [&](int c) { return c < n ? R.sinv + (size_t)c * n : R.xtop + (size_t)(c - n) * n; };
+  for (int cb = c0 + warp * spw; cb < c1; cb += 2 * stride) {
+    const int c = cb + seg, c2 = c + stride;
+    const bool ok = c < c1, ok2 = c2 < c1;
+    const double* x = colp(ok ? c : c0);
+    const double* x2 = colp(ok2 ? c2 : c0);
+    // all of the lane's elements of both columns in flight at once (W is
+    // chosen so that 8 W >= n up to n = 256), streaming loads: read once
+    double a[8], a2[8];
 #pragma unroll
     for (int u = 0; u < 8; u++) {
       const int t = sl + u * W;
       a[u] = (ok && t < n) ? __ldcs(x + t) : 0.0;
+      a2[u] = (ok2 && t < n) ? __ldcs(x2 + t) : 0.0;
     }
-    double s0 = 0.0, s1 = 0.0;
+    double s0 = 0.0, s1 = 0.0, r0 = 0.0, r1 = 0.0;
 #pragma unroll
     for (int u = 0; u < 8; u += 2) {
       const int t = sl + u * W;
-      if (t < n) s0 = fma(a[u], bsh[t], s0);
-      if (t + W < n) s1 = fma(a[u + 1], bsh[t + W], s1);
+      if (t < n) {
+        const double bt = bsh[t];
+        s0 = fma(a[u], bt, s0);
+        r0 = fma(a2[u], bt, r0);
+      }
+      if (t + W < n) {
+        const double bt = bsh[t + W];
+        s1 = fma(a[u + 1], bt, s1);
+        r1 = fma(a2[u + 1], bt, r1);
+      }
     }
-    for (int t = sl + 8 * W; ok && t < n; t += W) s0 = fma(__ldcs(x + t), bsh[t], s0);
-    double sv = s0 + s1;
-    for (int o = W >> 1; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-    if (ok && sl == 0) {
-      if (c < n) g[c] = sv;
-      else V[(int64_t)R.pos[c - n]] -= sv;
+    for (int t = sl + 8 * W; t < n; t += W) {
+      if (ok) s0 = fma(__ldcs(x + t), bsh[t], s0);
+      if (ok2) r0 = fma(__ldcs(x2 + t), bsh[t], r0);
+    }
+    double sv = s0 + s1, sv2 = r0 + r1;
+    for (int o = W >> 1; o > 0; o >>= 1) {
+      sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      sv2 += __shfl_xor_sync(0xffffffffu, sv2, o);
+    }
+    if (sl == 0) {
+      if (ok) {
+        if (c < n) g[c] = sv;
+        else V[(int64_t)R.pos[c - n]] -= sv;
+      }
+      if (ok2) {
+        if (c2 < n) g[c2] = sv2;
+        else V[(int64_t)R.pos[c2 - n]] -= sv2;
+      }
     }
   }
 }
