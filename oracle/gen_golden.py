@@ -36,6 +36,8 @@ CASES = {
     "exact_512": (512, "inv_r", 0.001, 2, 4, 0.0),
     "reglog_1k": (1024, "log", 0.001, 2, 4, 1e-10),
     "d4_invr": (16384, "inv_r", 0.001, 4, 4, 1e-6),
+    # BASELINE C2 itself (N = 65,536, log|x-y|, depth 5, p = 5, eps = 1e-6)
+    "c2_log": (65536, "log_r", 0.001, 5, 5, 1e-6),
 }
 
 

@@ -38,7 +38,7 @@ def _setup(ifmm, name):
     return g, pts, tree
 
 
-CASES = ["c1_invr", "log_2k", "exact_512", "reglog_1k", "d4_invr"]
+CASES = ["c1_invr", "log_2k", "exact_512", "reglog_1k", "d4_invr", "c2_log"]
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -84,7 +84,7 @@ def test_matvec_multi_rhs_equals_columns(ifmm):
         assert np.linalg.norm(Y[:, c] - y) <= 1e-14 * np.linalg.norm(y)
 
 
-@pytest.mark.parametrize("name", ["c1_invr", "log_2k", "reglog_1k", "d4_invr"])
+@pytest.mark.parametrize("name", ["c1_invr", "log_2k", "reglog_1k", "d4_invr", "c2_log"])
 def test_factor_solve_residual_and_solution(ifmm, name):
     g, pts, tree = _setup(ifmm, name)
     tol = float(g["tol"])

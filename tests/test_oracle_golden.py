@@ -17,7 +17,7 @@ def _setup(name):
     return g, pts, O.build_tree(pts, depth), golden_kernel(g)
 
 
-@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("name", CASES + ["c2_log"])  # C2 itself: tree/lists only (its oracle run takes minutes)
 def test_tree_lists_bit_exact(name):
     g, pts, T, _ = _setup(name)
     assert np.array_equal(T.perm, g["perm"])
