@@ -710,34 +710,42 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
                                                                slot, MR, MC, KK, 0);
       CK_LAUNCH();
     }
-    if (may_redo) {
-      // fills that used all Kf (<= 96) crosses of the first pass without
-      // converging continue up to the reference's min(m, n) crosses with
-      // buffers of that size (few fills, coarse levels at high accuracy)
-      std::vector<FillState> hs(nf);
-      CK(cudaMemcpyAsync(hs.data(), d_state, sizeof(FillState) * nf, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      int nredo = 0;
-      for (int f = 0; f < nf; f++) {
-        FillDesc& D = cb.fills[f];
-        if (hs[f].status != 2 || D.kfull <= D.Kf) continue;
-        D.Kf = D.kfull;
-        D.out = ws.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
-        KK = std::max(KK, D.Kf);
-        nredo++;
-      }
-      if (nredo > 0) {
-        dfd = upload(ws, cb.fills, s, st);
-        const size_t slot = k1_slot(KK);
-        const int grid = std::max(1, std::min(nredo, 148));
-        double* scr = ws.alloc_n<double>(slot * grid);
-        aca_recompress_kernel<CtaGroup><<<grid, bs_big, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
-                                                                slot, MR, MC, KK, 1);
-        CK_LAUNCH();
-      }
-    }
   }
-  const size_t dslot = 3 * size_t(MX) * KK + size_t(KK) * KK + 3 * size_t(KK) + 64;
+  // Fills that used all Kf (<= 96) crosses of the first pass without
+  // converging continue up to the reference's min(m, n) crosses with buffers of
+  // that size (few fills, coarse levels at high accuracy).  Checked after the
+  // host has prepared the augmentation launches (the readback waits for K1).
+  std::vector<char> redone;
+  bool redo_checked = false;
+  auto redo_pass = [&]() {
+    if (!may_redo || redo_checked) return false;
+    redo_checked = true;
+    std::vector<FillState> hs(nf);
+    CK(cudaMemcpyAsync(hs.data(), d_state, sizeof(FillState) * nf, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int nredo = 0;
+    redone.assign(nf, 0);
+    for (int f = 0; f < nf; f++) {
+      FillDesc& D = cb.fills[f];
+      if (hs[f].status != 2 || D.kfull <= D.Kf) continue;
+      D.Kf = D.kfull;
+      D.out = ws.alloc_n<double>(size_t(D.rows + D.cols + 1) * D.Kf);
+      KK = std::max(KK, D.Kf);
+      redone[f] = 1;
+      nredo++;
+    }
+    if (nredo == 0) return false;
+    dfd = upload(ws, cb.fills, s, st);
+    const size_t slot = 2 * size_t(MR) * KK + 2 * size_t(MC) * KK + 4 * size_t(KK) * KK + 2 * size_t(MR + MC) +
+                        4 * size_t(KK) + 64;
+    const int grid = std::max(1, std::min(nredo, 148));
+    double* scr = ws.alloc_n<double>(slot * grid);
+    aca_recompress_kernel<CtaGroup><<<grid, bs_big, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr, slot,
+                                                            MR, MC, KK, 1);
+    CK_LAUNCH();
+    return true;
+  };
+  size_t dslot = 0;
   const int bs_d = wmode ? 32 * WPB : bs_dirs;
   std::vector<int> tq, tp;  // fill -> q-side / p-side augmentation task (-1: none)
   double* const* d_eb = nullptr;
@@ -787,7 +795,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
         const FillDesc& D = cb.fills[lst[u] >> 1];
         hb[u] = ws.alloc_n<double>(size_t((lst[u] & 1) ? D.rows : D.cols) * D.Kf);
       }
-      double* const* dhb = upload(ws, hb, s, st);
+      double* const* dhb = upload(ws, hb, s, st);  // re-uploaded if a fill is redone
       // first-pass coefficients U0^T F per task (r0 x Kf, r0 = batch-initial
       // rank from the host copy) + the fill -> task maps for K4
       std::vector<double*> eb(lst.size(), nullptr);
@@ -803,6 +811,19 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       d_eb = upload(ws, eb, s, st);
       d_r0 = ws.alloc_n<int>(lst.size());
       CK(cudaMemsetAsync(d_r0, 0, sizeof(int) * lst.size(), s));
+      if (redo_pass()) {  // grown fills need larger direction / coefficient buffers
+        for (size_t u = 0; u < lst.size(); u++) {
+          const int f = lst[u] >> 1, side = lst[u] & 1;
+          if (!redone[f]) continue;
+          const FillDesc& D = cb.fills[f];
+          hb[u] = ws.alloc_n<double>(size_t(side ? D.rows : D.cols) * D.Kf);
+          const int r0 = cb.rank_host ? cb.rank_host[side ? D.p : D.q] : 0;
+          if (r0 > 0) eb[u] = ws.alloc_n<double>(size_t(r0) * D.Kf);
+        }
+        dhb = upload(ws, hb, s, st);
+        d_eb = upload(ws, eb, s, st);
+      }
+      dslot = 3 * size_t(MX) * KK + size_t(KK) * KK + 3 * size_t(KK) + 64;
       {
         const size_t pslot = size_t(MX) * KK + 64;
         const int pgrid = grid_for(ntask, bs_d == bs_small ? per_sm : 8, 32);
@@ -826,6 +847,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       CK_LAUNCH();
     }
   }
+  redo_pass();  // batches without augmentation tasks
   // K4
   {
     const size_t slot = 2 * size_t(MX) * KK + 64;

@@ -242,6 +242,29 @@ class Factorizer {
   bool pm_present(WorkLevel& W, int i, int j) { return get_pres(W.pm, W, std::min(i, j), std::max(i, j)); }
   bool px_present(WorkLevel& W, int i, int j) { return get_pres(W.px, W, i, j); }
   void set_px(WorkLevel& W, int i, int j, uint8_t v) { set_pres(W.px, W, i, j, v); }
+  // Schur target of kind 0 (P2P), 1 (hybrid x-y) or 2 (M2L): created (storage
+  // where held, presence flag) with a single table lookup
+  BlkRef schur_target(WorkLevel& W, int kind, int i, int j) {
+    const int a = kind == 1 ? i : std::min(i, j), b = kind == 1 ? j : std::max(i, j);
+    const size_t ix = size_t(pidx(W, a, b, true));
+    const bool held = holds2(W, a, b);
+    if (kind == 0) {
+      W.pp[ix] = 1;
+      double*& p = W.p2p[ix];
+      if (!p && held) p = zalloc(W, size_t(W.n[a]) * W.n[b]);
+      return {p, W.n[a], i > j};
+    }
+    if (kind == 1) {
+      W.px[ix] = 1;
+      double*& p = W.xy[ix];
+      if (!p && held) p = zalloc(W, size_t(W.n[i]) * W.rcap[j]);
+      return {p, W.n[i], false};
+    }
+    W.pm[ix] = 1;
+    double*& p = W.m2l[ix];
+    if (!p && held) p = zalloc(W, size_t(W.rcap[a]) * W.rcap[b]);
+    return {p, W.rcap[a], i > j};
+  }
 
   // IFMM_HOST_PROF: host ms between marks of the level start
   std::chrono::steady_clock::time_point hp_t_;
@@ -726,17 +749,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
             set_pres(W.pm, W, I.i, I.i, 1);
             continue;
           }
-          BlkRef tgt;
-          if (ax && bx) {
-            tgt = p2p_ref(W, ja, jb, true);
-            set_pp(W, ja, jb, 1);
-          } else if (ax && !bx) {
-            tgt = xy_ref(W, ja, jb, true);
-            set_px(W, ja, jb, 1);
-          } else {
-            tgt = m2l_ref(W, ja, jb, true);
-            set_pm(W, ja, jb, 1);
-          }
+          const BlkRef tgt = schur_target(W, (ax && bx) ? 0 : (ax ? 1 : 2), ja, jb);
           if (da == 0 || db == 0) continue;
           F_->fl_schur += 2.0 * I.n * da * db;
           if (per_block)
@@ -839,15 +852,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         if (a == ns - 1 && b == ns - 1) {
           m2l_ref(W, I.i, I.i, true);
           set_pres(W.pm, W, I.i, I.i, 1);
-        } else if (a < nx && b < nx) {
-          p2p_ref(W, ja, jb, true);
-          set_pp(W, ja, jb, 1);
-        } else if (a < nx) {
-          xy_ref(W, ja, jb, true);
-          set_px(W, ja, jb, 1);
         } else {
-          m2l_ref(W, ja, jb, true);
-          set_pm(W, ja, jb, 1);
+          schur_target(W, (a < nx && b < nx) ? 0 : (a < nx ? 1 : 2), ja, jb);
         }
       }
     for (int f = fill_off[t]; f < fill_off[t + 1]; f++) m2l_ref(W, fh[f].p, fh[f].q, true);
