@@ -218,12 +218,14 @@ def test_extended_system_export(ifmm, tmp_path):
         ifmm.assemble_extended_dense(store, tree, cap=100)
 
 
-def test_reference_default_configuration(ifmm):
+@pytest.mark.parametrize("name", ["default_4k", "default_8k"])
+def test_reference_default_configuration(ifmm, name):
     """IfmmSolver() with the reference's own defaults (log, a = 1e-3, tol = 1e-14,
     p = 8): near-exact compression, incompressible fills kept dense, couplings
     past the 7x7 window, fills needing more than 96 ACA crosses.  Against the
-    reference's solution (tests/golden/default_4k.npz, oracle/gen_golden_default.py)."""
-    g = load_golden("default_4k")
+    reference's solution (tests/golden/default_*k.npz, oracle/gen_golden_default.py;
+    the reference takes 9 s / 256 s on one core for N = 4,000 / 8,000)."""
+    g = load_golden(name)
     n = int(g["n"])
     X = 2.0 * np.random.default_rng(0).random((n, 2)) - 1.0
     est = ifmm.IfmmSolver().fit(X)
