@@ -225,7 +225,8 @@ class Factorizer {
     const int64_t ix = pidx(W, i, j, alloc);
     if (ix < 0) return {nullptr, W.n[i], false};
     double*& p = W.xy[size_t(ix)];
-    if (!p && alloc && holds2(W, i, j)) p = zalloc(W, size_t(W.n[i]) * W.rcap[j]);
+    // hybrid blocks are only created with j already eliminated: its rank is final
+    if (!p && alloc && holds2(W, i, j)) p = zalloc(W, size_t(W.n[i]) * std::max(1, W.r[j]));
     return {p, W.n[i], false};
   }
   bool get_pres(const std::vector<uint8_t>& v, WorkLevel& W, int i, int j) {
@@ -257,7 +258,7 @@ class Factorizer {
     if (kind == 1) {
       W.px[ix] = 1;
       double*& p = W.xy[ix];
-      if (!p && held) p = zalloc(W, size_t(W.n[i]) * W.rcap[j]);
+      if (!p && held) p = zalloc(W, size_t(W.n[i]) * std::max(1, W.r[j]));  // j eliminated: final rank
       return {p, W.n[i], false};
     }
     W.pm[ix] = 1;
