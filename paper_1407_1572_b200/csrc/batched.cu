@@ -1033,7 +1033,7 @@ void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, in
     // step, so its traffic grows with b (the wider update is cheap here)
     static const int bsm = getenv("IFMM_GJ_SMEM_B") ? atoi(getenv("IFMM_GJ_SMEM_B")) : 16;
     b = bsm;
-    while (b > 4 && smem_for(b) > 224 * 1024) b /= 2;
+    while (b > 1 && smem_for(b) > 224 * 1024) b /= 2;  // very large pivots (3-D top levels): narrower panels
     if (smem_for(b) > 224 * 1024) invalid("pivot block too large for the Gauss-Jordan panel");
     smem = smem_for(b);
     threads = 512;

@@ -91,10 +91,10 @@ def test_gj_inverse_large_batch_mixed_sizes(L):
         assert np.linalg.norm(inv @ x - np.eye(k)) <= 1e-9 * k * max(1.0, np.linalg.cond(x) / 1e4)
 
 
-@pytest.mark.parametrize("m", [900, 1024, 1100])
+@pytest.mark.parametrize("m", [900, 1024, 1100, 5200])
 def test_gj_inverse_large_single(L, m):
     """Single large pivots (top levels): 16-wide register panel up to m = 1024,
-    shared-memory panel beyond."""
+    shared-memory panel beyond (narrower panels above m ~ 4,800)."""
     rng = np.random.default_rng(m)
     A = rng.standard_normal((m, m)) + m ** 0.5 * np.eye(m)
     packed = np.asfortranarray(A).ravel(order="F").copy()
