@@ -47,6 +47,7 @@ struct WorkLevel {
   std::vector<int> n, r, rcap, r0;
   std::vector<double*> U;
   std::vector<double*> p2p, m2l, xy;  // nc*win
+  std::vector<int> m2l_ld;            // leading dimension of each allocated M2L block
   std::vector<uint8_t> pp, pm, px;
   std::vector<uint8_t> dead;
   // Pairs beyond the 7^d window (dense couplings that chained past +-3 cells)
@@ -196,6 +197,7 @@ class Factorizer {
     W.ovf.emplace(key, int(ix));
     W.p2p.push_back(nullptr);
     W.m2l.push_back(nullptr);
+    W.m2l_ld.push_back(0);
     W.xy.push_back(nullptr);
     W.pp.push_back(0);
     W.pm.push_back(0);
@@ -218,8 +220,11 @@ class Factorizer {
     const int64_t ix = pidx(W, a, b, alloc);
     if (ix < 0) return {nullptr, W.rcap[a], i > j};
     double*& p = W.m2l[size_t(ix)];
-    if (!p && alloc && holds2(W, a, b)) p = zalloc(W, size_t(W.rcap[a]) * W.rcap[b]);
-    return {p, W.rcap[a], i > j};
+    if (!p && alloc && holds2(W, a, b)) {  // live endpoints: capacity layout (ranks may grow)
+      p = zalloc(W, size_t(W.rcap[a]) * W.rcap[b]);
+      W.m2l_ld[size_t(ix)] = W.rcap[a];
+    }
+    return {p, p ? W.m2l_ld[size_t(ix)] : W.rcap[a], i > j};
   }
   BlkRef xy_ref(WorkLevel& W, int i, int j, bool alloc) {
     const int64_t ix = pidx(W, i, j, alloc);
@@ -263,8 +268,13 @@ class Factorizer {
     }
     W.pm[ix] = 1;
     double*& p = W.m2l[ix];
-    if (!p && held) p = zalloc(W, size_t(W.rcap[a]) * W.rcap[b]);
-    return {p, W.rcap[a], i > j};
+    if (!p && held) {
+      // Schur targets of kind 2 couple y / z slots: both clusters are
+      // eliminated (or being eliminated), their ranks final -- no capacity
+      p = zalloc(W, size_t(std::max(1, W.r[a])) * std::max(1, W.r[b]));
+      W.m2l_ld[ix] = std::max(1, W.r[a]);
+    }
+    return {p, p ? W.m2l_ld[ix] : W.rcap[a], i > j};
   }
 
   // IFMM_HOST_PROF: host ms between marks of the level start
@@ -291,6 +301,7 @@ class Factorizer {
     hprof_mark("arena reset");
     W.p2p.assign(size_t(W.nc) * W.win, nullptr);
     W.m2l.assign(size_t(W.nc) * W.win, nullptr);
+    W.m2l_ld.assign(size_t(W.nc) * W.win, 0);
     W.xy.assign(size_t(W.nc) * W.win, nullptr);
     W.pp.assign(size_t(W.nc) * W.win, 0);
     W.pm.assign(size_t(W.nc) * W.win, 0);
@@ -473,9 +484,9 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
           if (nranks_ > 1) invalid("sharded transition: a child M2L block is not stored on the assembling rank");
           continue;
         }
-        // stored once as (min, max) with ld = rcap of the smaller index
-        const int lo = std::min(ca, cbb);
-        cb.add(mp, C.rcap[lo], P.p + off[i][a] + size_t(off[j][b]) * P.ld, P.ld, C.r[ca], C.r[cbb], ca > cbb);
+        // stored once as (min, max), leading dimension per block
+        cb.add(mp, C.m2l_ld[size_t(bix[u])], P.p + off[i][a] + size_t(off[j][b]) * P.ld, P.ld, C.r[ca], C.r[cbb],
+               ca > cbb);
       }
     }
     for (int q = T.il_off[i]; q < T.il_off[i + 1]; q++) {
