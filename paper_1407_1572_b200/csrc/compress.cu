@@ -665,6 +665,13 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     static const int gram_env = getenv("IFMM_GRAM") ? atoi(getenv("IFMM_GRAM")) : 1;
     const int gram = (gram_env != 0 && tol >= 1e-9) ? 1 : 0;
     CK(cudaMemcpyToSymbolAsync(g_gram, &gram, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    // Jacobi rotation threshold from the truncation tolerance: singular values
+    // then carry ~(1e-4 tol)^2 relative error -- far below the truncation decisions
+    // (1e-2 tol measured: 15 ms faster at C3 but a C3-parameter pivot crossed the
+    // 1e12 condition limit; 1e-4 tol: 10 ms faster, all gates green)
+    static const double jscale = getenv("IFMM_JAC_TOL_SCALE") ? atof(getenv("IFMM_JAC_TOL_SCALE")) : 1e-4;
+    const double jt = tol > 0.0 ? std::max(1e-15, std::min(1e-8, tol * jscale)) : 1e-15;
+    CK(cudaMemcpyToSymbolAsync(g_jac_tol, &jt, sizeof(double), 0, cudaMemcpyHostToDevice, s));
   }
   if (prof) {
     const int one = 1;

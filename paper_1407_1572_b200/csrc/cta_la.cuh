@@ -11,6 +11,12 @@
 
 namespace ifmm {
 
+// Off-diagonal threshold of the one-sided Jacobi SVDs: a pair is rotated while
+// |x.y| > tol_rot * |x| |y|.  Column norms then match the singular values to
+// ~tol_rot^2 relative to the largest, so the compression sets it from its
+// truncation tolerance (compress.cu); elsewhere it stays at rounding level.
+__device__ double g_jac_tol = 1e-15;
+
 struct CtaShared {
   double red[32];
   double red2[32];
@@ -325,7 +331,7 @@ __device__ inline void g_jacobi(const G& g, double* A, int m, int n, int lda, do
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (!valid || ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+        if (!valid || ga == 0.0 || fabs(ga) <= g_jac_tol * sqrt(al * be)) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         // a rotation below rounding level changes nothing: columns of very
@@ -424,7 +430,7 @@ __device__ __noinline__ void warp_jacobi_reg(double* A, int m, int n, int lda, d
         }
       }
       double c = 1.0, sn = 0.0;
-      bool doit = act && !(ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be));
+      bool doit = act && !(ga == 0.0 || fabs(ga) <= g_jac_tol * sqrt(al * be));
       if (doit) {
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
