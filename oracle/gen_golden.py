@@ -38,6 +38,9 @@ CASES = {
     "d4_invr": (16384, "inv_r", 0.001, 4, 4, 1e-6),
     # BASELINE C2 itself (N = 65,536, log|x-y|, depth 5, p = 5, eps = 1e-6)
     "c2_log": (65536, "log_r", 0.001, 5, 5, 1e-6),
+    # C3's parameters one level shallower (N = 262,144, depth 6): the largest case the reference
+    # finishes in minutes (C3 itself needs ~1 h and ~70 GB)
+    "c3_262k": (262144, "inv_r", 0.001, 6, 4, 1e-6),
 }
 
 
