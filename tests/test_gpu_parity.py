@@ -84,10 +84,11 @@ def test_matvec_multi_rhs_equals_columns(ifmm):
         assert np.linalg.norm(Y[:, c] - y) <= 1e-14 * np.linalg.norm(y)
 
 
-@pytest.mark.parametrize("name", ["c1_invr", "log_2k", "reglog_1k", "d4_invr", "c2_log"])
+@pytest.mark.parametrize("name", ["c1_invr", "log_2k", "reglog_1k", "d4_invr", "c2_log", "c3_262k"])
 def test_factor_solve_residual_and_solution(ifmm, name):
     g, pts, tree = _setup(ifmm, name)
     tol = float(g["tol"])
+    assert np.array_equal(tree.point_permutation, g["perm"])
     store = ifmm.init_operators(tree, _kernel(ifmm, g), p=int(g["p"]), tol=tol)
     fact = ifmm.factorize(store, tree)
     x = ifmm.solve(fact, g["b"])
