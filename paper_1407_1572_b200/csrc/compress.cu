@@ -6,6 +6,7 @@
 namespace ifmm {
 __device__ int g_prof_on = 0;
 __device__ int g_jac_rt = 1;
+__device__ double g_gram_piv = 1e-14;  // K1 Gram route: scaled pivots^2 >= g_gram_piv / tol
 __device__ int g_gram = 1;    // IFMM_GRAM=0: Householder QRs in the K1 recompression   // IFMM_JACOBI_RT=0: Jacobi on R (columns) in new_dirs
 __device__ int g_jac_reg = 0;  // IFMM_JACOBI_REG=1: register-resident Jacobi for <= 16 columns (measured slower)
 __device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
@@ -118,11 +119,16 @@ __device__ int gram_recompress(const G& g, const double* Uc, const double* Vc, i
   g.sync();
   bool ok = true;
   if (k > 96) return -1;
+  // The factors carry ~eps * cond^2 of the column-scaled crosses: accept the
+  // Gram route only while that stays 100x below the truncation tolerance
+  // (scaled pivots^2 >= 1e-14 / tol; clustered inputs produce ill-conditioned
+  // crosses whose Gram factors otherwise corrupt the augmented bases)
+  const double min_piv2 = fmax(1e-12, g_gram_piv / tol);
   if (nw >= 2) {
-    if (warp == 0) ok = warp_chol_scaled(Gu, k, ldg, du);
-    else if (warp == 1) ok = warp_chol_scaled(Gv, k, ldg, dv);
+    if (warp == 0) ok = warp_chol_scaled(Gu, k, ldg, du, min_piv2);
+    else if (warp == 1) ok = warp_chol_scaled(Gv, k, ldg, dv, min_piv2);
   } else {
-    ok = warp_chol_scaled(Gu, k, ldg, du) && warp_chol_scaled(Gv, k, ldg, dv);
+    ok = warp_chol_scaled(Gu, k, ldg, du, min_piv2) && warp_chol_scaled(Gv, k, ldg, dv, min_piv2);
   }
   if (g.any(!ok)) return -1;
   // unscale: L = D^-1 Lhat (row i times the original sqrt(G_ii))
@@ -314,7 +320,7 @@ __device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig
   }
   double* W = U + (size_t)rU * nU;
   int w = 0;
-  if (g_gram && r <= 96 && nU >= 128) {  // measured: slower than Householder for the small leaf bases
+  if (g_gram == 1 && r <= 96 && nU >= 128) {  // measured: slower than Householder for the small leaf bases
     // Gram route: G = H^T H = L L^T (column-scaled Cholesky), H = Q L^T with
     // Q = H L^-T never formed.  Jacobi on L (= R^T) gives V (left singular
     // vectors of R) and sigma; W = Q V(:, kept) = H (L^-T V(:, kept)).
@@ -663,8 +669,11 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     // (the reference default 1e-14) the duplicated directions make pivots
     // singular, so the Householder routes run there.
     static const int gram_env = getenv("IFMM_GRAM") ? atoi(getenv("IFMM_GRAM")) : 1;
-    const int gram = (gram_env != 0 && tol >= 1e-9) ? 1 : 0;
+    // IFMM_GRAM=0: Householder everywhere; 2: Gram only in the K1 recompression
+    const int gram = (gram_env != 0 && tol >= 1e-9) ? gram_env : 0;
     CK(cudaMemcpyToSymbolAsync(g_gram, &gram, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    static const double gpiv = getenv("IFMM_GRAM_PIV") ? atof(getenv("IFMM_GRAM_PIV")) : 1e-14;
+    CK(cudaMemcpyToSymbolAsync(g_gram_piv, &gpiv, sizeof(double), 0, cudaMemcpyHostToDevice, s));
     // Jacobi rotation threshold from the truncation tolerance: singular values
     // then carry ~(1e-4 tol)^2 relative error -- far below the truncation decisions
     // (1e-2 tol measured: 15 ms faster at C3 but a C3-parameter pivot crossed the

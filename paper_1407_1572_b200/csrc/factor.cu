@@ -908,6 +908,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   double err_cond = 0;
   for (int u = 0; u < no; u++) {
     const PivInfo& I = P[own[u]];
+    if (I.m == 0) continue;  // an empty cluster (clustered inputs): nothing to eliminate
     double rc = (info[u] != 0) ? 0.0 : 1.0 / (nS[u] * nSi[u]);
     if (!std::isfinite(rc) || rc <= 1.0 / cond_limit_) {
       err_pos = own[u];
