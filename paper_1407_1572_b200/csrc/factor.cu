@@ -1009,6 +1009,12 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     std::vector<HaloItem> items;
     for (int t = 0; t < np; t++) {
       const PivInfo& I = P[t];
+      if (!I.own) {  // every item of a pivot lies among {i} u partners: none stored here -> none received
+        bool any = holds1(W, I.i);
+        for (int j : I.xp) any = any || holds1(W, j);
+        for (int j : I.yp) any = any || holds1(W, j);
+        if (!any) continue;
+      }
       items.clear();
       for (size_t a = 0; a < I.xp.size(); a++)
         for (size_t b = a; b < I.xp.size(); b++) {
