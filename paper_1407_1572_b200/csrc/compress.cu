@@ -174,7 +174,7 @@ template <class G>
 __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_kernel(const FillDesc* __restrict__ fills, int nf,
                                                             FillState* state, double tol, const int* probes,
                                                             int probe_maxm, double* scratch, size_t slot,
-                                                            int MR, int MC, int KK, int redo) {
+                                                            int MR, int MC, int KK, int redo, int phase) {
   __shared__ CtaShared sh;
   const G g = Worker<G>::make(sh);
   double* s = scratch + slot * Worker<G>::id();
@@ -198,7 +198,26 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
     if (redo && state[f].status != 2) continue;
     const FillDesc D = fills[f];
     const int rows = D.rows, cols = D.cols;
+    int k;
     FillState S{0, 0, 0, 0, 0, 0.0};
+    PROF_T0();
+    if (phase == 1) {
+      // recompression pass: crosses staged in the output factors by phase 0
+      S = state[f];
+      if (S.status != 0 || S.r != -1) continue;
+      k = S.k;
+      const double* gu = D.out + (size_t)rows * k;
+      const double* gv = D.out + (size_t)rows * D.Kf + (size_t)cols * k;
+      for (int e = g.rank(); e < rows * k; e += g.size()) Uc[e] = D.out[e];
+      for (int e = g.rank(); e < cols * k; e += g.size()) Vc[e] = D.out[(size_t)rows * D.Kf + e];
+      if (g_gram)
+        for (int e = g.rank(); e < k * k; e += g.size()) {
+          const int i = e % k, j = e / k;
+          Rl[i + (size_t)j * KK] = gu[e];
+          Rr[i + (size_t)j * KK] = gv[e];
+        }
+      g.sync();
+    } else {
     if (rows == 0 || cols == 0) {
       if (g.rank() == 0) state[f] = S;
       g.sync();
@@ -218,11 +237,11 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
     }
     const int mrow = rows < probe_maxm ? rows : probe_maxm;
     const int kmax = min(D.Kf, KK);
-    PROF_T0();
+    if (g_prof_on) _pt = clock64();
     AcaOut ao = g_aca(g, D.F, D.ldF, D.transF, rows, cols, tol, probes + (size_t)mrow * 10, min(10, rows), Uc, Vc,
                       kmax, rr, cc, usedr, usedc, dots, g_gram ? Rl : nullptr, g_gram ? Rr : nullptr, KK);
     PROF_ACC(0);
-    const int k = ao.k;
+    k = ao.k;
     S.k = k;
     if (!ao.converged && k >= kmax && k < min(rows, cols) && (kmax < D.Kf || D.Kf < D.kfull)) {
       S.status = 2;  // needs more crosses than this worker holds
@@ -236,6 +255,27 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
       g.sync();
       continue;
     }
+    // ACA pass: stage the crosses and their Gram matrices (ld k) in the output
+    // factors for phase 1 (r = -1 marks a staged fill); a fill whose Gram
+    // matrices do not fit behind its crosses is finished here
+    if (phase == 0 && k > 0 && (size_t)k * k <= (size_t)rows * (D.Kf - k) &&
+        (size_t)k * k <= (size_t)cols * (D.Kf - k) + D.Kf) {
+      double* gu = D.out + (size_t)rows * k;
+      double* gv = D.out + (size_t)rows * D.Kf + (size_t)cols * k;
+      for (int e = g.rank(); e < rows * k; e += g.size()) D.out[e] = Uc[e];
+      for (int e = g.rank(); e < cols * k; e += g.size()) D.out[(size_t)rows * D.Kf + e] = Vc[e];
+      if (g_gram)
+        for (int e = g.rank(); e < k * k; e += g.size()) {
+          const int i = e % k, j = e / k;
+          gu[e] = Rl[i + (size_t)j * KK];
+          gv[e] = Rr[i + (size_t)j * KK];
+        }
+      S.r = -1;
+      if (g.rank() == 0) state[f] = S;
+      g.sync();
+      continue;
+    }
+    }  // phase != 1
     int r = 0;
     double* left = D.out;
     double* right = D.out + (size_t)rows * D.Kf;
@@ -608,7 +648,7 @@ void test_recompress_one(const double* dF, int m, int n, double tol, const int* 
   const size_t slot = 2 * size_t(m) * KK + 2 * size_t(n) * KK + 4 * size_t(KK) * KK + 2 * size_t(m + n) +
                       4 * size_t(KK) + 64;
   double* scr = ws.alloc_n<double>(slot);
-  aca_recompress_kernel<CtaGroup><<<1, 128, 0, s>>>(dfd, 1, d_state, tol, d_probes, probe_maxm, scr, slot, m, n, KK, 0);
+  aca_recompress_kernel<CtaGroup><<<1, 128, 0, s>>>(dfd, 1, d_state, tol, d_probes, probe_maxm, scr, slot, m, n, KK, 0, 2);
   CK_LAUNCH();
   const int one = 1;  // restore the default
   CK(cudaMemcpyToSymbolAsync(g_gram, &one, sizeof(int), 0, cudaMemcpyHostToDevice, s));
@@ -708,23 +748,34 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       const int grid = grid_for(nf, 8, 32);
       double* scr = ws.alloc_n<double>(slot * workers(grid));
       aca_recompress_kernel<WarpGroup><<<grid, 32 * WPB, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
-                                                                   slot, MR, MC, kw, 0);
+                                                                   slot, MR, MC, kw, 0, 2);
       CK_LAUNCH();
       if (KK > kw) {  // fills whose ACA outgrew the warp's cross cap
         const size_t cslot = k1_slot(KK);
         const int cgrid = resident_grid(nf, 2);
         double* cscr = ws.alloc_n<double>(cslot * cgrid);
         aca_recompress_kernel<CtaGroup><<<cgrid, 128, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, cscr,
-                                                               cslot, MR, MC, KK, 1);
+                                                               cslot, MR, MC, KK, 1, 2);
         CK_LAUNCH();
       }
     } else {
       const size_t slot = k1_slot(KK);
       const int grid = resident_grid(nf, bs_fill == bs_small ? per_sm : 8);
       double* scr = ws.alloc_n<double>(slot * grid);
-      aca_recompress_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
-                                                               slot, MR, MC, KK, 0);
-      CK_LAUNCH();
+      // ACA and recompression as two passes over the fills: every CTA on an SM
+      // then runs the same (smaller) code region (IFMM_K1_SPLIT=0: one pass)
+      static const int split_env = getenv("IFMM_K1_SPLIT") ? atoi(getenv("IFMM_K1_SPLIT")) : 1;
+      if (split_env == 2 || (split_env && bs_fill == bs_small)) {  // measured: a gain at the leaf level only
+        for (int ph = 0; ph < 2; ph++) {
+          aca_recompress_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
+                                                                   slot, MR, MC, KK, 0, ph);
+          CK_LAUNCH();
+        }
+      } else {
+        aca_recompress_kernel<CtaGroup><<<grid, bs_fill, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr,
+                                                                 slot, MR, MC, KK, 0, 2);
+        CK_LAUNCH();
+      }
     }
   }
   // Fills that used all Kf (<= 96) crosses of the first pass without
@@ -757,7 +808,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     const int grid = std::max(1, std::min(nredo, 148));
     double* scr = ws.alloc_n<double>(slot * grid);
     aca_recompress_kernel<CtaGroup><<<grid, bs_big, 0, s>>>(dfd, nf, d_state, tol, d_probes, probe_maxm, scr, slot,
-                                                            MR, MC, KK, 1);
+                                                            MR, MC, KK, 1, 2);
     CK_LAUNCH();
     return true;
   };

@@ -30,7 +30,8 @@ for r in range(reps):
     print(f"rep {r}: factorize wall {1e3 * (t1 - t0):.1f} ms (lib {fact.factor_ms:.1f} ms)", flush=True)
 x = ifmm.solve(fact, b)
 res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
-print(f"{name}: residual {res:.3e} r_m {fact.r_m} top {fact.top_dim}")
+import hashlib  # noqa: E402
+print(f"{name}: residual {res:.3e} r_m {fact.r_m} top {fact.top_dim} x {hashlib.md5(x.tobytes()).hexdigest()[:12]}")
 print("phases:", {k: round(v[0], 1) for k, v in fact.phase_times.items()})
 for k, d in sorted(fact.phase_times_by_level.items(), reverse=True):
     print(f"  level {k}: " + " ".join(f"{p}={v:.1f}" for p, v in d.items() if v))
