@@ -601,6 +601,10 @@ class Factor:
     stats: dict = field(default_factory=dict)
     r_m: int = 0
     order: str = "morton"
+    cond_limit: float = COND_LIMIT
+    on_singular: str = "raise"      # "record": note the violation and continue (C3 study)
+    singular: list = field(default_factory=list)
+    max_cond: dict = field(default_factory=dict)
 
 
 def _parent_near(st: Blocks, k):
@@ -722,8 +726,12 @@ def _eliminate(st: Blocks, k, i, tol, fac: Factor, stats: Stats, ils, dead):
     S[n:, :n] = U.T
     lu = lu_factor(S)
     rc = dgecon(lu[0], np.linalg.norm(S, 1), norm="1")[0]
-    if not np.isfinite(rc) or rc <= 1.0 / COND_LIMIT:
-        raise SingularPivot(k, i, 1.0 / max(rc, 1e-300))
+    cond = 1.0 / max(rc, 1e-300) if np.isfinite(rc) else math.inf
+    fac.max_cond[k] = max(fac.max_cond.get(k, 0.0), cond)
+    if not np.isfinite(rc) or rc <= 1.0 / fac.cond_limit:
+        if fac.on_singular != "record":
+            raise SingularPivot(k, i, cond)
+        fac.singular.append((k, i, cond))
     xp = sorted(j for j in st.pp.get((k, i), ()) if j != i and not dead[j])
     yp = sorted(st.plc.get((k, i), ()))
     cols = [("x", j, st.get("p2p", k, i, j)) for j in xp] + [("y", j, st.get("m2p", k, i, j)) for j in yp]
@@ -787,11 +795,14 @@ def _top(fac: Factor):
     fac.top_off = off
 
 
-def factorize(st: Blocks, tol=None, order="morton", release_m2l=True) -> Factor:
-    """ifmm/solver.py:106-153 with a selectable intra-level order."""
+def factorize(st: Blocks, tol=None, order="morton", release_m2l=True, cond_limit=COND_LIMIT,
+              on_singular="raise", progress=None) -> Factor:
+    """ifmm/solver.py:106-153 with a selectable intra-level order.  `on_singular="record"`
+    keeps going past a pivot the reference would reject (ifmm/solver.py:214-218) and lists it
+    in `fac.singular`; `progress(k, fac)` is called after each level."""
     tree = st.tree
     tol = st.tol if tol is None else tol
-    fac = Factor(st, tree, tol, order=order)
+    fac = Factor(st, tree, tol, order=order, cond_limit=cond_limit, on_singular=on_singular)
     fac.r_m = st.max_init_rank
     K = tree.depth
     for k in range(K, 1, -1):
@@ -808,6 +819,8 @@ def factorize(st: Blocks, tol=None, order="morton", release_m2l=True) -> Factor:
             for i in batch:
                 _eliminate(st, k, int(i), tol, fac, stats, ils, dead)
         fac.r_m = max(fac.r_m, stats.max_rank)
+        if progress is not None:
+            progress(k, fac)
     _top(fac)
     if release_m2l:
         for key in [kk for kk in st.blk["m2l"] if kk[0] == 2]:
