@@ -174,10 +174,14 @@ int ifmm_partition_halo_counts(int dim, int depth, int level, int nranks, int ra
 /* ---- test hooks for the batched kernels (host arrays in/out) */
 /* run the Jacobi / QR / ACA hooks on one warp (1) or a 256-thread CTA (0) */
 int ifmm_test_set_group(int warp);
-/* in-place inverse of `count` column-major matrices of sizes m[c], packed */
-int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info);
-/* device time (best of reps, ms) of one batched inverse of the given matrices */
-int ifmm_bench_gj_inverse(const double* a, const int32_t* m, int count, int reps, double* ms);
+/* in-place batched LU (partial pivoting) of `count` column-major matrices of sizes m[c],
+   packed; perm (sum m[c]): row l of P A is row perm[l] of A; info: 0 or 1 + first zero
+   pivot column; inv_norm1: dlacn2 estimate of ||A^-1||_1 (the pivot-condition test) */
+int ifmm_test_lu(double* a, const int32_t* m, int count, int32_t* perm, int32_t* info, double* inv_norm1);
+/* X = S^-1 [[C, 0], [0, -I_r]] for one factored pivot of size n + r (lu, perm from
+   ifmm_test_lu; C n x wl column-major): xtop n x (wl + r), xbot r x (wl + r) */
+int ifmm_test_lu_solve_x(const double* lu, const int32_t* perm, int n, int r, const double* c, int wl,
+                         double* xtop, double* xbot);
 /* C = alpha op(A) op(B) + beta C, column-major, one problem */
 int ifmm_test_gemm(int transA, int transB, int M, int N, int K, double alpha, const double* A, int lda,
                    const double* B, int ldb, double beta, double* C, int ldc, int transC);

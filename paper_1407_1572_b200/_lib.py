@@ -78,8 +78,8 @@ SIGNATURES = {
     "ifmm_factor_shard_info": (_i32, [_p, _p, _p]),
     "ifmm_partition": (_i32, [_i32, _i32, _i32, _i32, _p, _p]),
     "ifmm_partition_halo_counts": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _p, _p]),
-    "ifmm_test_gj_inverse": (_i32, [_p, _p, _i32, _p]),
-    "ifmm_bench_gj_inverse": (_i32, [_p, _p, _i32, _i32, _p]),
+    "ifmm_test_lu": (_i32, [_p, _p, _i32, _p, _p, _p]),
+    "ifmm_test_lu_solve_x": (_i32, [_p, _p, _i32, _i32, _p, _i32, _p, _p]),
     "ifmm_test_gemm": (_i32, [_i32, _i32, _i32, _i32, _i32, _d, _p, _i32, _p, _i32, _d, _p, _i32, _i32]),
     "ifmm_test_set_group": (_i32, [_i32]),
     "ifmm_test_recompress": (_i32, [_p, _i32, _i32, _d, _p, _i32, _p, _p, _p, _p, _p]),

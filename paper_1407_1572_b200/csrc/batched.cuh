@@ -1,6 +1,5 @@
 // Batched block utilities (copy / transpose / scale-accumulate / zero, 1-norms)
-// and the batched Gauss-Jordan inversion with partial pivoting used for the
-// IFMM pivot blocks S_i = [[P2P_ii, U_i], [U_i^T, 0]].
+// and the descriptor of the batched dense kernels (lu.cuh).
 #pragma once
 #include "common.cuh"
 #include "gemm.cuh"
@@ -43,45 +42,10 @@ struct MatDesc {
   double* A;
   int m;
   int lda;
-  int* ipiv;  // length m (GJ)
+  int* ipiv;  // length m: row permutation of the LU (lu.cuh)
   int tag;    // caller-defined (pivot id)
 };
 
 // 1-norm (max column abs sum) of every matrix -> out[p]
 void launch_norm1(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s);
-// dlacn2 (Hager/Higham) estimate of the 1-norm of every matrix -> out[p]; out
-// holds the exact norm on entry and is only replaced where
-// exact * normA[p] >= limit (the estimate is <= the exact norm)
-void launch_norm1_estimate(const MatDesc* d_desc, int n, int maxm, double* out, const double* normA, double limit,
-                           cudaStream_t s);
-
-// In-place inversion of every matrix by blocked Gauss-Jordan elimination with
-// partial pivoting.  `info[p]` = 0, or 1 + first column with an exact zero
-// pivot.  Host-side descriptors `h` (same content as d_desc) drive the GEMM
-// trailing updates.  With `side` (a high-priority stream and two events) the
-// panel of step j+1 runs concurrently with the bulk of step j's update.
-struct GjSide {
-  cudaStream_t s = nullptr;
-  cudaEvent_t e_cols = nullptr, e_panel = nullptr;
-  void ensure() {
-    if (s) return;
-    int lo = 0, hi = 0;
-    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
-    CK(cudaEventCreateWithFlags(&e_cols, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&e_panel, cudaEventDisableTiming));
-  }
-  ~GjSide() {
-    if (e_cols) cudaEventDestroy(e_cols);
-    if (e_panel) cudaEventDestroy(e_panel);
-    if (s) cudaStreamDestroy(s);
-  }
-};
-// shape_n / shape_maxm (sharded runs): count and largest size of the whole
-// colour batch across ranks -- the blocking scheme is chosen from them, so
-// each matrix is inverted with the same arithmetic as on one GPU
-void batched_gj_inverse(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws,
-                        Staging& st, cudaStream_t s, const GjSide* side = nullptr, int shape_n = 0,
-                        int shape_maxm = 0);
-
 }  // namespace ifmm

@@ -6,6 +6,7 @@
 #include "../../include/ifmm_b200.h"
 #include "comm.cuh"
 #include "core.cuh"
+#include "lu.cuh"
 #include "compress.cuh"
 #include "cta_la.cuh"
 
@@ -26,7 +27,6 @@ using ifmm::StoreH;
 using ifmm::Topo;
 using ifmm::TreeH;
 using ifmm::invalid;
-using ifmm::batched_gj_inverse;
 using ifmm::ensure_device;
 using ifmm::default_stream;
 using ifmm::upload;
@@ -457,13 +457,6 @@ void ifmm_factor_free(ifmm_factor* f) {
 // The small-matrix routines run either CTA-wide (256 threads) or on one warp,
 // as the compression kernels use them; ifmm_test_set_group selects which.
 static int g_test_warp = 0;
-// the test / bench hooks use the look-ahead Gauss-Jordan like the factorization
-static ifmm::GjSide* test_gj_side() {
-  static ifmm::GjSide* g = new ifmm::GjSide();  // never destroyed: outlives the CUDA context teardown
-  g->ensure();
-  return g;
-}
-
 template <class G>
 __global__ void test_jacobi_kernel(double* a, int m, int n, double* v, double* sig, int* ord) {
   __shared__ CtaShared sh;
@@ -506,71 +499,69 @@ int ifmm_test_set_group(int warp) {
   return IFMM_OK;
 }
 
-int ifmm_test_gj_inverse(double* a, const int32_t* m, int count, int32_t* info) {
+// Batched LU (the pivot factorization): a[] holds `count` column-major
+// matrices back to back, overwritten by their L\U factors; perm[] (sum of m)
+// receives each row permutation, info[] the zero-pivot flags, inv_norm1[] the
+// dlacn2 estimate of ||A^-1||_1 that the pivot-condition test uses.
+int ifmm_test_lu(double* a, const int32_t* m, int count, int32_t* perm, int32_t* info, double* inv_norm1) {
   return guard([&] {
     ensure_device();
     cudaStream_t s = default_stream();
     Arena ws(size_t(64) << 20);
     Staging st;
     std::vector<MatDesc> md(count);
-    size_t tot = 0;
-    for (int c = 0; c < count; c++) tot += size_t(m[c]) * m[c];
-    double* d = ws.alloc_n<double>(tot);
-    CK(cudaMemcpy(d, a, sizeof(double) * tot, cudaMemcpyHostToDevice));
-    size_t off = 0;
+    size_t tot = 0, totm = 0;
+    int maxm = 0;
     for (int c = 0; c < count; c++) {
-      md[c] = MatDesc{d + off, m[c], m[c], ws.alloc_n<int>(m[c]), c};
+      tot += size_t(m[c]) * m[c];
+      totm += size_t(m[c]);
+      maxm = std::max(maxm, int(m[c]));
+    }
+    double* d = ws.alloc_n<double>(tot);
+    int* dp = ws.alloc_n<int>(std::max<size_t>(1, totm));
+    CK(cudaMemcpy(d, a, sizeof(double) * tot, cudaMemcpyHostToDevice));
+    size_t off = 0, offm = 0;
+    for (int c = 0; c < count; c++) {
+      md[c] = MatDesc{d + off, m[c], m[c], dp + offm, c};
       off += size_t(m[c]) * m[c];
+      offm += size_t(m[c]);
     }
     const MatDesc* dmd = upload(ws, md, s, st);
     int* dinfo = ws.alloc_n<int>(count);
-    ifmm::batched_gj_inverse(md, dmd, dinfo, ws, st, s, test_gj_side());
+    double* dn = ws.alloc_n<double>(count);
+    ifmm::batched_lu(md, dmd, dinfo, ws, st, s);
+    ifmm::launch_lu_inv_norm1(dmd, count, maxm, dn, s);
     CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(a, d, sizeof(double) * tot, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(perm, dp, sizeof(int) * totm, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(info, dinfo, sizeof(int) * count, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(inv_norm1, dn, sizeof(double) * count, cudaMemcpyDeviceToHost));
   });
 }
 
-int ifmm_bench_gj_inverse(const double* a, const int32_t* m, int count, int reps, double* ms) {
+// X = S^-1 [[C, 0], [0, -I_r]] for one factored pivot (lu, perm from
+// ifmm_test_lu): xtop (n x w) and xbot (r x w), w = wl + r.
+int ifmm_test_lu_solve_x(const double* lu, const int32_t* perm, int n, int r, const double* c, int wl, double* xtop,
+                         double* xbot) {
   return guard([&] {
     ensure_device();
     cudaStream_t s = default_stream();
     Arena ws(size_t(64) << 20);
     Staging st;
-    size_t tot = 0;
-    for (int c = 0; c < count; c++) tot += size_t(m[c]) * m[c];
-    double* src = ws.alloc_n<double>(tot);
-    double* d = ws.alloc_n<double>(tot);
-    CK(cudaMemcpy(src, a, sizeof(double) * tot, cudaMemcpyHostToDevice));
-    std::vector<MatDesc> md(count);
-    size_t off = 0;
-    for (int c = 0; c < count; c++) {
-      md[c] = MatDesc{d + off, m[c], m[c], ws.alloc_n<int>(m[c]), c};
-      off += size_t(m[c]) * m[c];
-    }
-    const MatDesc* dmd = upload(ws, md, s, st);
-    int* dinfo = ws.alloc_n<int>(count);
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    double best = 1e30;
-    for (int r = 0; r < reps; r++) {
-      CK(cudaMemcpyAsync(d, src, sizeof(double) * tot, cudaMemcpyDeviceToDevice, s));
-      CK(cudaStreamSynchronize(s));
-      const size_t mark = ws.in_use();
-      (void)mark;
-      CK(cudaEventRecord(e0, s));
-      batched_gj_inverse(md, dmd, dinfo, ws, st, s, test_gj_side());
-      CK(cudaEventRecord(e1, s));
-      CK(cudaEventSynchronize(e1));
-      float t = 0.f;
-      CK(cudaEventElapsedTime(&t, e0, e1));
-      best = std::min(best, double(t));
-      st.reset();
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    *ms = best;
+    const int m = n + r, w = wl + r;
+    double* dlu = ws.alloc_n<double>(size_t(m) * m);
+    int* dp = ws.alloc_n<int>(m);
+    double* dc = ws.alloc_n<double>(size_t(std::max(1, n)) * std::max(1, wl));
+    double* dt = ws.alloc_n<double>(size_t(std::max(1, n)) * w);
+    double* db = ws.alloc_n<double>(size_t(std::max(1, r)) * w);
+    CK(cudaMemcpy(dlu, lu, sizeof(double) * m * m, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dp, perm, sizeof(int) * m, cudaMemcpyHostToDevice));
+    if (n * wl > 0) CK(cudaMemcpy(dc, c, sizeof(double) * n * wl, cudaMemcpyHostToDevice));
+    std::vector<ifmm::XSolveDesc> xd{ifmm::XSolveDesc{dlu, dp, dc, dt, db, m, n, r, wl, w, 0}};
+    ifmm::launch_lu_solve_x(xd, ws, st, s);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(xtop, dt, sizeof(double) * n * w, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(xbot, db, sizeof(double) * r * w, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -110,7 +110,6 @@ struct InitLevel {
 // parameter sweeps refactorize) do not pay cudaMalloc/cudaFree every call.
 struct FactorWork {
   std::mutex mu;
-  GjSide gj_side;  // look-ahead stream of the Gauss-Jordan inverses
   Arena ws{size_t(256) << 20};
   Staging st;
   Arena lvl[2] = {Arena(size_t(2) << 30), Arena(size_t(2) << 30)};
@@ -136,10 +135,15 @@ struct LevelStatsH {
   int clusters = 0, max_rank = 0, compressed = 0, dense_kept = 0;
 };
 
+// Solve record of one elimination (the reference's _Record, ifmm/solver.py:63-74):
+// the LU factors of S_i with their row permutation, and the coupling panel C
+// (P2P_ij of the live neighbours | M2P_ij of the eliminated partners) the
+// sweeps multiply with; partner positions in the solve vector.
 struct RecordH {
   int level, index, n, r, w;
-  double* sinv;      // n x n (ld n)
-  double* xtop;      // n x w (ld n)
+  double* lu;        // m x m (ld m), m = n + r: L (unit) and U of P S
+  int* perm;         // m: row l of P S is row perm[l] of S
+  double* c;         // n x w (ld n); columns [w - r, w) are zero
   int* pos;          // w absolute positions in the solve vector
   int64_t xoff;      // absolute position of x_i
 };
@@ -147,7 +151,7 @@ struct RecordH {
 struct BatchH {
   int level, colour, rec0, rec1;
   const RecordH* d_recs;  // device copy of records[rec0..rec1)
-  int maxn, maxw;
+  int maxn, maxw, maxm;
   // sharded solve: solve-vector runs (base, length) each rank writes in the
   // forward / backward sweep of this batch, rank-major with offsets
   std::vector<int64_t> fwd_runs, bwd_runs;  // pairs
@@ -168,11 +172,12 @@ struct FactorH {
   int64_t vec_size = 0;                // solve vector length
   std::vector<int64_t> lvl_base;       // index k: base of level-k x slots; lvl_base[1] = top
   int top_dim = 0;
-  double* top_inv = nullptr;
+  double* top_lu = nullptr;            // LU of the level-2 system (M x M)
+  int* top_perm = nullptr;
   int64_t g_size = 0;                  // sum of record n (per rhs)
   std::vector<int64_t> g_off;          // per record
   int64_t* d_g_off = nullptr;
-  Arena arena{size_t(4) << 30};        // records, top inverse
+  Arena arena{size_t(4) << 30};        // records, top factors
   cudaStream_t stream = nullptr;
   // timing of the last factorization (ms) and work accounting
   double ms_total = 0;
@@ -198,12 +203,12 @@ struct FactorH {
 
 enum PhaseId : int {
   PH_GATHER = 0,     // S / C gathers, record copies
-  PH_GJ = 1,         // batched Gauss-Jordan inverses (+ norms)
-  PH_XGEMM = 2,      // X = S^-1 C
+  PH_GJ = 1,         // batched LU of the pivots (+ norms, condition estimates)
+  PH_XGEMM = 2,      // X = S^-1 C (LU solves on the coupling panel)
   PH_SCHUR = 3,      // symmetric Schur update GEMMs
   PH_COMPRESS = 4,   // fill-in compression
   PH_TRANSITION = 5, // level start (parent near field, bases)
-  PH_TOP = 6,        // top-level inverse
+  PH_TOP = 6,        // top-level LU
   PH_COUNT = 7,
   PH_COMM = 7,       // sharded runs: metadata all-gathers + halo pack/exchange/unpack
 };

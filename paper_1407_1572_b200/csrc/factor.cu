@@ -35,6 +35,7 @@
 
 #include "core.cuh"
 #include "comm.cuh"
+#include "lu.cuh"
 #include "compress.cuh"
 #include "cta_la.cuh"
 
@@ -555,7 +556,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     bool own;
     std::vector<int> xp, yp;
     std::vector<int> soff;  // slot column offsets (size nslots+1)
-    double *S, *C, *Xb;
+    double *S, *C, *Xt, *Xb;
+    int* perm;
     int rec;
   };
   // Every rank walks all pivots of the batch (metadata); device work is done
@@ -629,34 +631,30 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   FillState* d_state = ws_.alloc_n<FillState>(std::max<size_t>(1, nfill));
   int* d_stats = ws_.alloc_n<int>(4);
   CK(cudaMemsetAsync(d_stats, 0, 16, s_));
-  static const char* dump_dir = getenv("IFMM_DUMP_SINGULAR");
   static const bool dbg = getenv("IFMM_DEBUG") != nullptr;
-  static const bool per_block = getenv("IFMM_SCHUR_GROUPED") != nullptr;  // debug: one GEMM per Schur block
-  std::vector<double*> Sbak(no, nullptr);
   hmark(11);
-  // Own pivots are processed in chunks: every phase of a chunk is launched
-  // before the host prepares the next one, so host descriptor work overlaps
-  // device work (a batch of 1,820 leaf pivots otherwise leaves the GPU idle
-  // while its descriptors are built).  Pivots of a batch are independent, and
-  // kernel shapes come from the whole batch (np, gmaxm, shape_mx, fh.size()),
-  // so chunking changes no arithmetic.
-  // measured at C3: chunks of 384 leaf pivots cost more (launch tails, per-chunk host work) than the
-  // overlap gains, so one chunk per batch by default (IFMM_CHUNK: experiments)
-  static const int chunk_target = getenv("IFMM_CHUNK") ? std::max(1, atoi(getenv("IFMM_CHUNK"))) : (1 << 30);
-  const int nchunks = std::max(1, (no + chunk_target - 1) / chunk_target);
+  // Own pivots are processed in one chunk per batch (host descriptor work for
+  // a chunk is launched before the next one is built; measured at C3, smaller
+  // chunks cost more in launch tails than they gain in overlap).  Pivots of a
+  // batch are independent, and kernel shapes come from the whole batch (np,
+  // gmaxm, shape_mx, fh.size()), so the arithmetic does not depend on chunking.
+  const int nchunks = 1;
   for (int ch = 0; ch < nchunks && no > 0; ch++) {
     const int u0 = int(int64_t(no) * ch / nchunks), u1 = int(int64_t(no) * (ch + 1) / nchunks);
     const int nc_ = u1 - u0;
     CopyBatch cb;
     std::vector<MatDesc> md;
+    std::vector<XSolveDesc> xd;
     for (int u = u0; u < u1; u++) {
       PivInfo& I = P[own[u]];
       const int i = I.i;
-      I.S = ws_.alloc_n<double>(size_t(I.m) * I.m);
-      I.C = ws_.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
+      // S (factored in place) and the coupling panel C stay with the solve record
+      I.S = F_->arena.alloc_n<double>(size_t(std::max(1, I.m)) * I.m);
+      I.perm = F_->arena.alloc_n<int>(std::max(1, I.m));
+      I.C = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
+      I.Xt = ws_.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
       I.Xb = ws_.alloc_n<double>(size_t(std::max(1, I.r)) * I.w);
-      int* ipiv = ws_.alloc_n<int>(I.m);
-      md.push_back(MatDesc{I.S, I.m, I.m, ipiv, i});
+      md.push_back(MatDesc{I.S, I.m, I.m, I.perm, i});
       // gather S
       BlkRef Pii = p2p_ref(W, i, i, true);
       cb.add(Pii.p, Pii.ld, I.S, I.m, I.n, I.n);
@@ -676,32 +674,24 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         s++;
       }
       cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
+      xd.push_back(XSolveDesc{I.S, I.perm, I.C, I.Xt, I.Xb, I.m, I.n, I.r, I.w - I.r, I.w, 0});
     }
     hmark(12);
     tm_.begin(PH_GATHER);
     launch_copies(cb, ws_, st_, s_);
     hmark(2);
-    if (dump_dir)
-      for (int u = u0; u < u1; u++) {
-        const PivInfo& I = P[own[u]];
-        Sbak[u] = ws_.alloc_n<double>(size_t(I.m) * I.m);
-        CK(cudaMemcpyAsync(Sbak[u], I.S, sizeof(double) * I.m * I.m, cudaMemcpyDeviceToDevice, s_));
-      }
     {
       const MatDesc* dmd = upload(ws_, md, s_, st_);
       int maxm = 0;
       for (auto& d : md) maxm = std::max(maxm, d.m);
       tm_.begin(PH_GJ);
       launch_norm1(dmd, nc_, maxm, d_nS + u0, s_);
-      work_->gj_side.ensure();
-      // blocking scheme from the whole batch (across chunks and ranks): same arithmetic as one launch
-      batched_gj_inverse(md, dmd, d_info + u0, ws_, st_, s_, &work_->gj_side, np, gmaxm);
-      launch_norm1(dmd, nc_, maxm, d_nSi + u0, s_);
-      launch_norm1_estimate(dmd, nc_, maxm, d_nSi + u0, d_nS + u0, cond_limit_, s_);
+      // panel width from the whole batch (across chunks and ranks): same arithmetic as one launch
+      batched_lu(md, dmd, d_info + u0, ws_, st_, s_, gmaxm);
+      launch_lu_inv_norm1(dmd, nc_, maxm, d_nSi + u0, s_);
     }
     hmark(3);
-    // records + X = S^-1 C
-    GemmBatch gb;
+    // records + X = S^-1 C (getrs on the coupling panel)
     for (int u = u0; u < u1; u++) {
       PivInfo& I = P[own[u]];
       RecordH R{};
@@ -710,8 +700,9 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       R.n = I.n;
       R.r = I.r;
       R.w = I.w;
-      R.sinv = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * std::max(1, I.n));
-      R.xtop = F_->arena.alloc_n<double>(size_t(std::max(1, I.n)) * I.w);
+      R.lu = I.S;
+      R.perm = I.perm;
+      R.c = I.C;
       R.pos = nullptr;  // set by finish_level (one block per level)
       I.rec = int(F_->recs.size());
       F_->recs.push_back(R);
@@ -720,24 +711,16 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       for (int j : I.yp) sl.push_back({1, j, W.r[j]});
       sl.push_back({1, I.i, I.r});
       rec_slots_.push_back(sl);
-      const int wl = I.w - I.r;
       {
-        const double m = I.m, n = I.n, w = I.w, h = wl;
-        F_->fl_exec += 2.0 * m * m * m + 2.0 * m * n * h;
+        const double m = I.m, n = I.n, w = I.w, h = I.w - I.r;
+        F_->fl_exec += 2.0 / 3.0 * m * m * m + 2.0 * m * m * w;
         F_->fl_ref += 2.0 / 3.0 * m * m * m + 2.0 * m * m * w + 2.0 * h * n * w;
-        F_->solve_bytes += 8.0 * (n * n + 2.0 * n * w);
+        F_->solve_bytes += 8.0 * (2.0 * m * m + 2.0 * n * h);
       }
-      cb.add(I.S, I.m, R.sinv, I.n, I.n, I.n);
-      cb.add(I.S + size_t(I.n) * I.m, I.m, R.xtop + size_t(wl) * I.n, I.n, I.n, I.r, false, -1.0);
-      cb.add(I.S + I.n + size_t(I.n) * I.m, I.m, I.Xb + size_t(wl) * I.r, I.r, I.r, I.r, false, -1.0);
-      gb.add(I.S, I.m, I.C, I.n, R.xtop, I.n, I.n, wl, I.n, 1.0, 0.0);
-      gb.add(I.S + I.n, I.m, I.C, I.n, I.Xb, I.r, I.r, wl, I.n, 1.0, 0.0);
     }
     hmark(8);
-    tm_.begin(PH_GATHER);
-    launch_copies(cb, ws_, st_, s_);
     tm_.begin(PH_XGEMM);
-    launch_grouped_gemm(gb, false, false, ws_, st_, s_);
+    launch_lu_solve_x(xd, ws_, st_, s_);
     tm_.end();
     hmark(9);
     // symmetric Schur update on the block upper triangle: target -= C_a^T X_b,
@@ -747,8 +730,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       PivInfo& I = P[own[u]];
       const int nx = int(I.xp.size()), ny = int(I.yp.size());
       const int ns = nx + ny + 1;
-      const RecordH& R = F_->recs[I.rec];
-      const int pv = per_block ? -1 : sbat.begin_pivot(I.C, R.xtop, I.n, I.soff);
+      const int pv = sbat.begin_pivot(I.C, I.Xt, I.n, I.soff);
       auto slot_cluster = [&](int s) { return s < nx ? I.xp[s] : (s < nx + ny ? I.yp[s - nx] : I.i); };
       for (int a = 0; a < ns; a++)
         for (int b = a; b < ns; b++) {
@@ -764,18 +746,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
           const BlkRef tgt = schur_target(W, (ax && bx) ? 0 : (ax ? 1 : 2), ja, jb);
           if (da == 0 || db == 0) continue;
           F_->fl_schur += 2.0 * I.n * da * db;
-          if (per_block)
-            gb.add(I.C + size_t(I.soff[a]) * I.n, I.n, R.xtop + size_t(I.soff[b]) * I.n, I.n, tgt.p, tgt.ld, da,
-                   db, I.n, -1.0, 1.0, tgt.trans);
-          else
-            sbat.set_target(pv, a, b, tgt.p, tgt.ld, tgt.trans);
+          sbat.set_target(pv, a, b, tgt.p, tgt.ld, tgt.trans);
         }
-      if (!per_block) sbat.finish_pivot(pv);
+      sbat.finish_pivot(pv);
     }
     hmark(10);
     tm_.begin(PH_SCHUR);
-    if (per_block) launch_grouped_gemm(gb, true, false, ws_, st_, s_);
-    else launch_schur(sbat, ws_, st_, s_);
+    launch_schur(sbat, ws_, st_, s_);
     tm_.begin(PH_GATHER);
     launch_copies(cb, ws_, st_, s_);
     tm_.end();
@@ -914,18 +891,6 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       err_pos = own[u];
       err_index = I.i;
       err_cond = 1.0 / std::max(rc, 1e-300);
-      if (dump_dir) {
-        std::vector<double> h(size_t(I.m) * I.m);
-        CK(cudaMemcpy(h.data(), Sbak[u], sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
-        std::string fn = std::string(dump_dir) + "/S_" + std::to_string(k) + "_" + std::to_string(I.i) + ".bin";
-        FILE* fp = fopen(fn.c_str(), "wb");
-        if (fp) {
-          int hdr[2] = {I.n, I.r};
-          fwrite(hdr, sizeof hdr, 1, fp);
-          fwrite(h.data(), sizeof(double), h.size(), fp);
-          fclose(fp);
-        }
-      }
       break;
     }
   }
@@ -1195,8 +1160,9 @@ void Factorizer::factor_top() {
   F_->top_dim = M;
   ws_.reset();
   st_.reset();
-  F_->top_inv = F_->arena.alloc_n<double>(size_t(std::max(1, M)) * std::max(1, M));
-  CK(cudaMemsetAsync(F_->top_inv, 0, sizeof(double) * std::max(1, M) * std::max(1, M), s_));
+  F_->top_lu = F_->arena.alloc_n<double>(size_t(std::max(1, M)) * std::max(1, M));
+  F_->top_perm = F_->arena.alloc_n<int>(std::max(1, M));
+  CK(cudaMemsetAsync(F_->top_lu, 0, sizeof(double) * std::max(1, M) * std::max(1, M), s_));
   CopyBatch cb;
   for (int i = 0; i < W.nc; i++)
     for (int j = 0; j < W.nc; j++) {
@@ -1205,23 +1171,32 @@ void Factorizer::factor_top() {
       if (!pm_present(W, i, j)) continue;
       BlkRef b = m2l_ref(W, i, j, false);
       if (!b.p) continue;
-      cb.add(b.p, b.ld, F_->top_inv + off[i] + size_t(off[j]) * M, M, W.r[i], W.r[j], b.trans);
+      cb.add(b.p, b.ld, F_->top_lu + off[i] + size_t(off[j]) * M, M, W.r[i], W.r[j], b.trans);
     }
   launch_copies(cb, ws_, st_, s_);
-  F_->fl_exec += 2.0 * double(M) * M * M;
+  F_->fl_exec += 2.0 / 3.0 * double(M) * M * M;
   F_->fl_ref += 2.0 / 3.0 * double(M) * M * M;
   F_->solve_bytes += 8.0 * double(M) * M;
+  int info = 0;
   if (M > 0) {
+    // dense LU of the level-2 system (ifmm/solver.py:528-546: lu_factor)
     std::vector<MatDesc> md(1);
-    md[0] = MatDesc{F_->top_inv, M, M, ws_.alloc_n<int>(M), -1};
+    md[0] = MatDesc{F_->top_lu, M, M, F_->top_perm, -1};
     const MatDesc* dmd = upload(ws_, md, s_, st_);
     int* d_info = ws_.alloc_n<int>(1);
     tm_.begin(PH_TOP);
-    work_->gj_side.ensure();
-    batched_gj_inverse(md, dmd, d_info, ws_, st_, s_, &work_->gj_side);
+    batched_lu(md, dmd, d_info, ws_, st_, s_);
+    CK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, s_));
   }
   CK(cudaStreamSynchronize(s_));
   tm_.collect(F_.get(), 1);
+  if (info != 0) {
+    // scipy's lu_factor only warns on an exactly singular top system and the
+    // solve then returns inf/nan; here the factorization fails loudly instead
+    char buf[160];
+    snprintf(buf, sizeof buf, "the level-2 top system is exactly singular (zero pivot in column %d)", info - 1);
+    throw SingularPivot(1, info - 1, INFINITY, buf);
+  }
 }
 
 FactorH* Factorizer::run() {
@@ -1278,7 +1253,7 @@ FactorH* Factorizer::run() {
       while (!piv.empty()) {
         const int r0 = int(F_->recs.size());
         eliminate_batch(piv, c, deferred);
-        F_->batches.push_back(BatchH{k, c, r0, int(F_->recs.size()), nullptr, 0, 0});
+        F_->batches.push_back(BatchH{k, c, r0, int(F_->recs.size()), nullptr, 0, 0, 0});
         if (!deferred.empty()) F_->deferred_batches++;
         piv.swap(deferred);
       }
@@ -1308,6 +1283,7 @@ FactorH* Factorizer::run() {
     for (auto& r : v) {
       b.maxn = std::max(b.maxn, r.n);
       b.maxw = std::max(b.maxw, r.w);
+      b.maxm = std::max(b.maxm, r.n + r.r);
     }
   }
   F_->g_off.resize(F_->recs.size() + 1, 0);

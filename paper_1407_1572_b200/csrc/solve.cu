@@ -1,14 +1,13 @@
 // Solve with the factored IFMM (ifmm/solver.py:549-626), level-wise and
-// batch-parallel: for every colour batch one CTA per eliminated cluster.
-//   forward : g_i = Sinv_nn b_i ; v[pos] -= X_top^T b_i     (z rows start at 0)
-//   top     : y = T^-1 v_top
-//   backward: x_i = g_i - X_top v[pos]     (batches and levels in reverse)
-// Using X_top = (S^-1 C)_top for both sweeps (S symmetric) means a record is
-// only Sinv_nn (n x n) + X_top (n x w): the solve streams each record twice
-// and is HBM-bound.  The GEMVs keep all warps busy: warps split the columns,
-// lanes own rows with register accumulators, partial sums meet in shared
-// memory.  Vectors are (positions x nrhs) row-major; right-hand sides are
-// processed in chunks of RC; a level's y slots alias the next level's x slots.
+// batch-parallel, with the LU factors of every pivot (the reference's
+// lu_solve, :583,613):
+//   forward : g = S^-1 [b_i; 0] (LU solves); g_top -> G, g_bot -> own z slots;
+//             v[pos] -= C^T g_top (partner slots, ifmm/solver.py:586-589)
+//   top     : y = T^-1 v_top (LU of the level-2 system)
+//   backward: t = C v[pos]; x_i = g_top - (S^-1 [t; -y_i])_top
+// The record is the LU of S (m x m), its row permutation and the coupling
+// panel C (n x w): each sweep streams both once.  Vectors are (positions x
+// nrhs) row-major; a level's y slots alias the next level's x slots.
 #include <algorithm>
 #include <cmath>
 #include <thread>
@@ -16,6 +15,7 @@
 #include "comm.cuh"
 #include "core.cuh"
 #include "gemm.cuh"
+#include "lu.cuh"
 
 namespace ifmm {
 
@@ -24,168 +24,138 @@ void launch_permute(const double* in, double* out, const int64_t* perm, int64_t 
 
 constexpr int SB = 256;       // threads per solve CTA
 constexpr int SWARPS = SB / 32;
-constexpr int RCMAX = 4;      // right-hand sides per pass (RC = 1 for a single rhs)
-constexpr int MAXJ = 8;       // rows per lane per pass (256 rows per row block)
 
-// y[t, q] (t < n, q < nq) = sum_c A[t + c*lda] x(c, q)  (A column-major n x w);
-// x(c, q) from the `xat` accessor, result written by `emit(t, q, value)`.
-template <int RC, class XAt, class Emit>
-__device__ inline void cta_gemv_cols(const double* __restrict__ A, int n, int w, size_t lda, XAt xat, int nq,
-                                     double* red, Emit emit) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int t0 = 0; t0 < n; t0 += 32 * MAXJ) {
-    double acc[MAXJ][RC];
-#pragma unroll
-    for (int j = 0; j < MAXJ; j++)
-#pragma unroll
-      for (int q = 0; q < RC; q++) acc[j][q] = 0.0;
-    // warps take chunks of 32 columns; the chunk's x values are fetched once
-    // (lane u loads column cb+u) and broadcast with shuffles
-    for (int cb = warp * 32; cb < w; cb += SWARPS * 32) {
-      double xl[RC];
-#pragma unroll
-      for (int q = 0; q < RC; q++) xl[q] = (cb + lane < w && q < nq) ? xat(cb + lane, q) : 0.0;
-      const int cmax = min(32, w - cb);
-#pragma unroll 8
-      for (int u = 0; u < cmax; u++) {
-        const double* col = A + (size_t)(cb + u) * lda;
-        double xv[RC];
-#pragma unroll
-        for (int q = 0; q < RC; q++) xv[q] = __shfl_sync(0xffffffffu, xl[q], u);
-#pragma unroll
-        for (int j = 0; j < MAXJ; j++) {
-          const int t = t0 + lane + 32 * j;
-          if (t < n) {
-            const double a = col[t];
-#pragma unroll
-            for (int q = 0; q < RC; q++) acc[j][q] = fma(a, xv[q], acc[j][q]);
-          }
-        }
-      }
-    }
-    // cross-warp reduction: red[warp][row][q]
-#pragma unroll
-    for (int j = 0; j < MAXJ; j++) {
-      const int tl = lane + 32 * j;
-#pragma unroll
-      for (int q = 0; q < RC; q++) if (t0 + tl < n) red[(tl * SWARPS + warp) * RC + q] = acc[j][q];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < 32 * MAXJ * nq; e += SB) {
-      const int tl = e / nq, q = e % nq;
-      const int t = t0 + tl;
-      if (t < n) {
-        double s = 0.0;
-        for (int w2 = 0; w2 < SWARPS; w2++) s += red[(tl * SWARPS + w2) * RC + q];
-        emit(t, q, s);
-      }
-    }
-    __syncthreads();
+// ------------------------------------------------------------------ pivot solves
+// g = S^-1 [b; 0] (forward) and h = S^-1 [t; -y_i] (backward) with the LU
+// factors of the record (ifmm/solver.py:583,613: lu_solve).  One CTA per
+// record (and chunk of right-hand sides); rows are gathered in pivot order.
+//   forward : g_top -> G, g_bot -> own z slots (V[pos[wl + t]] += g[n + t])
+//   backward: x_i = g_top - h_top -> V[xoff + t]
+__device__ __forceinline__ double rec_rhs(const RecordH& R, bool fwd, int i, int wl, const double* V,
+                                          const double* T, int64_t nrhs, int q) {
+  if (fwd) return i < R.n ? V[(R.xoff + i) * nrhs + q] : 0.0;
+  return i < R.n ? T[(size_t)i * nrhs + q] : -V[(int64_t)R.pos[wl + i - R.n] * nrhs + q];
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(SB, 3) rec_solve_vec_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                           const int64_t* __restrict__ g_off, double* V, double* G,
+                                                           const double* __restrict__ T) {
+  extern __shared__ double y[];
+  const RecordH R = recs[blockIdx.x];
+  const int n = R.n, r = R.r, m = n + r, wl = R.w - r;
+  if (m == 0) return;
+  const int64_t go = g_off[rec0 + blockIdx.x];
+  for (int l = threadIdx.x; l < m; l += blockDim.x) y[l] = rec_rhs(R, FWD, R.perm[l], wl, V, T + go, 1, 0);
+  __syncthreads();
+  cta_trsv_lower_unit(R.lu, m, m, y);
+  cta_trsv_upper(R.lu, m, m, y);
+  if (FWD) {
+    for (int t = threadIdx.x; t < n; t += blockDim.x) G[go + t] = y[t];
+    for (int t = threadIdx.x; t < r; t += blockDim.x) V[R.pos[wl + t]] += y[n + t];
+  } else {
+    for (int t = threadIdx.x; t < n; t += blockDim.x) V[R.xoff + t] = G[go + t] - y[t];
   }
 }
 
+// nrhs >= 2: TW right-hand sides per CTA, DMMA tile solves (lu.cuh)
+template <int TW, bool FWD>
+__global__ void __launch_bounds__(SB, 3) rec_solve_tile_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                            const int64_t* __restrict__ g_off, double* V, double* G,
+                                                            const double* __restrict__ T, int nrhs, double* scratch,
+                                                            size_t per) {
+  extern __shared__ double sm[];
+  const RecordH R = recs[blockIdx.x];
+  const int n = R.n, r = R.r, m = n + r, wl = R.w - r;
+  if (m == 0) return;
+  const int q0 = blockIdx.y * TW, nq = min(TW, nrhs - q0);
+  const int xm = m | 1;
+  double* X = scratch ? scratch + per * (blockIdx.x * (size_t)gridDim.y + blockIdx.y) : sm;
+  const int64_t go = g_off[rec0 + blockIdx.x];
+  for (int e = threadIdx.x; e < TW * m; e += blockDim.x) {
+    const int c = e / m, l = e - c * m;
+    X[(size_t)c * xm + l] = c < nq ? rec_rhs(R, FWD, R.perm[l], wl, V, T + go * nrhs, nrhs, q0 + c) : 0.0;
+  }
+  __syncthreads();
+  cta_tile_lu_solve<TW>(R.lu, m, m, X, xm);
+  for (int e = threadIdx.x; e < TW * m; e += blockDim.x) {
+    const int c = e / m, l = e - c * m;
+    if (c >= nq) continue;
+    const double v = X[(size_t)c * xm + l];
+    if (FWD) {
+      if (l < n) G[(go + l) * nrhs + q0 + c] = v;
+      else V[(int64_t)R.pos[wl + l - n] * nrhs + q0 + c] += v;
+    } else if (l < n) {
+      double* o = V + (R.xoff + l) * nrhs + q0 + c;
+      *o = G[(go + l) * nrhs + q0 + c] - v;
+    }
+  }
+}
+
+// Top-level system y = T^-1 v (ifmm/solver.py:592-598), in place on the
+// level-1 slots (M x nrhs row-major)
+__global__ void __launch_bounds__(SB) top_solve_vec_kernel(const double* __restrict__ LU, const int* __restrict__ perm,
+                                                           int M, double* v) {
+  extern __shared__ double y[];
+  for (int l = threadIdx.x; l < M; l += blockDim.x) y[l] = v[perm[l]];
+  __syncthreads();
+  cta_trsv_lower_unit(LU, M, M, y);
+  cta_trsv_upper(LU, M, M, y);
+  for (int l = threadIdx.x; l < M; l += blockDim.x) v[l] = y[l];
+}
+template <int TW>
+__global__ void __launch_bounds__(SB) top_solve_tile_kernel(const double* __restrict__ LU,
+                                                            const int* __restrict__ perm, int M, const double* vin,
+                                                            double* vout, int nrhs, double* scratch, size_t per) {
+  extern __shared__ double sm[];
+  const int q0 = blockIdx.x * TW, nq = min(TW, nrhs - q0);
+  const int xm = M | 1;
+  double* X = scratch ? scratch + per * blockIdx.x : sm;
+  for (int e = threadIdx.x; e < TW * M; e += blockDim.x) {
+    const int c = e / M, l = e - c * M;
+    X[(size_t)c * xm + l] = c < nq ? vin[(size_t)perm[l] * nrhs + q0 + c] : 0.0;
+  }
+  __syncthreads();
+  cta_tile_lu_solve<TW>(LU, M, M, X, xm);
+  for (int e = threadIdx.x; e < TW * M; e += blockDim.x) {
+    const int c = e / M, l = e - c * M;
+    if (c < nq) vout[(size_t)l * nrhs + q0 + c] = X[(size_t)c * xm + l];
+  }
+}
+
+// ------------------------------------------------------------------ coupling GEMVs (one rhs)
 // Records are split over gridDim.y CTAs (coarse levels have few, large
-// records): chunk y of the forward sweep computes rows [r0, r1) of Sinv b and
-// columns [c0, c1) of X_top^T b; chunk y of the backward sweep rows [r0, r1)
-// of x.  Every output has exactly one writer (deterministic).
+// records).  Every output has exactly one writer (deterministic).
 __device__ __forceinline__ void chunk_range(int len, int y, int ny, int gran, int& lo, int& hi) {
   const int per = ((len + ny - 1) / ny + gran - 1) / gran * gran;
   lo = min(len, y * per);
   hi = min(len, lo + per);
 }
 
-template <int RC>
-__global__ void __launch_bounds__(SB, RC == 1 ? 4 : 2) solve_fwd_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                       const int64_t* __restrict__ g_off, double* V, double* G,
-                                                       int nrhs, int red_rows) {
-  extern __shared__ double sm[];
-  double* red = sm;                         // min(maxn, 256) x SWARPS x RC
-  double* bsh = red + red_rows * SWARPS * RC;  // n x RC
+// forward partner update: V[pos[c]] -= C(:, c)^T g_top for c < wl.  Column
+// dots, W-lane segments per column (short columns: several per warp), two
+// columns per segment in flight (streaming loads).
+__global__ void __launch_bounds__(SB, 3) cpl_fwd1_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                         const int64_t* __restrict__ g_off, double* V,
+                                                         const double* __restrict__ G) {
+  extern __shared__ double bsh[];  // n
   const RecordH R = recs[blockIdx.x];
-  const int n = R.n, w = R.w;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int r0, r1, c0, c1;
-  chunk_range(n, blockIdx.y, gridDim.y, 32, r0, r1);
-  chunk_range(w, blockIdx.y, gridDim.y, 8, c0, c1);
-  double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
-  // segment of W lanes per X_top column (short columns: several per warp)
-  const int W = n > 128 ? 32 : (n > 64 ? 16 : 8);
-  const int seg = lane / W, sl = lane & (W - 1), spw = 32 / W;
-  for (int q0 = 0; q0 < nrhs; q0 += RC) {
-    const int nq = min(RC, nrhs - q0);
-    for (int e = threadIdx.x; e < n * RC; e += SB) {
-      const int c = e / RC, q = e % RC;
-      bsh[e] = q < nq ? V[(R.xoff + c) * nrhs + q0 + q] : 0.0;
-    }
-    __syncthreads();
-    // g[r0:r1] = Sinv[r0:r1, :] b
-    if (r1 > r0)
-      cta_gemv_cols<RC>(R.sinv + r0, r1 - r0, n, (size_t)n, [&](int c, int q) { return bsh[c * RC + q]; }, nq, red,
-                    [&](int t, int q, double v) { g[(size_t)(r0 + t) * nrhs + q0 + q] = v; });
-    // v[pos[c]] -= X_top(:, c)^T b for c in [c0, c1)
-    for (int cb = c0 + warp * spw; cb < c1; cb += SWARPS * spw) {
-      const int c = cb + seg;
-      const bool ok = c < c1;
-      const double* x = R.xtop + (size_t)(ok ? c : c0) * n;
-      double s[RC];
-#pragma unroll
-      for (int q = 0; q < RC; q++) s[q] = 0.0;
-      if (ok)
-#pragma unroll 8
-        for (int t = sl; t < n; t += W) {
-          const double a = x[t];
-#pragma unroll
-          for (int q = 0; q < RC; q++)
-            if (q < nq) s[q] = fma(a, bsh[t * RC + q], s[q]);
-        }
-#pragma unroll
-      for (int q = 0; q < RC; q++)
-        if (q < nq)
-          for (int o = W >> 1; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
-      if (ok && sl < nq) {
-        double sv = s[0];
-#pragma unroll
-        for (int q = 1; q < RC; q++)
-          if (sl == q) sv = s[q];
-        V[(int64_t)R.pos[c] * nrhs + q0 + sl] -= sv;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Single right-hand side forward sweep.  S (hence S^-1 and its block
-// S^-1_nn) is symmetric, so g = S^-1_nn b is a set of column dots as well:
-// the record [S^-1_nn | X_top] is one n x (n + w) column block and every
-// output is the dot of one column with b -- W-lane segments per column, no
-// cross-warp reduction, one barrier.  Chunk y of gridDim.y owns a range of
-// the n + w columns.
-__global__ void __launch_bounds__(SB, 3) solve_fwd1_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                           const int64_t* __restrict__ g_off, double* V, double* G) {
-  extern __shared__ double sm[];
-  double* bsh = sm;  // n
-  const RecordH R = recs[blockIdx.x];
-  const int n = R.n, w = R.w, nc = n + w;
+  const int n = R.n, wl = R.w - R.r;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int c0, c1;
-  chunk_range(nc, blockIdx.y, gridDim.y, 8, c0, c1);
-  if (c1 <= c0) return;
-  double* g = G + g_off[rec0 + blockIdx.x];
-  for (int e = threadIdx.x; e < n; e += SB) bsh[e] = V[R.xoff + e];
+  chunk_range(wl, blockIdx.y, gridDim.y, 8, c0, c1);
+  if (c1 <= c0 || n == 0) return;
+  const double* g = G + g_off[rec0 + blockIdx.x];
+  for (int e = threadIdx.x; e < n; e += SB) bsh[e] = g[e];
   __syncthreads();
   const int W = n > 128 ? 32 : (n > 64 ? 16 : 8);
   const int seg = lane / W, sl = lane & (W - 1), spw = 32 / W;
-  // two columns per segment and step: 16 loads per lane in flight (the sweep
-  // is latency-bound on long-scoreboard stalls with one)
   const int stride = SWARPS * spw;
-  auto colp = [&](int c) { return c < n ? R.sinv + (size_t)c * n : R.xtop + (size_t)(c - n) * n; };
   for (int cb = c0 + warp * spw; cb < c1; cb += 2 * stride) {
     const int c = cb + seg, c2 = c + stride;
     const bool ok = c < c1, ok2 = c2 < c1;
-    const double* x = colp(ok ? c : c0);
-    const double* x2 = colp(ok2 ? c2 : c0);
-    // all of the lane's elements of both columns in flight at once (W is
-    // chosen so that 8 W >= n up to n = 256), streaming loads: read once
+    const double* x = R.c + (size_t)(ok ? c : c0) * n;
+    const double* x2 = R.c + (size_t)(ok2 ? c2 : c0) * n;
     double a[8], a2[8];
 #pragma unroll
     for (int u = 0; u < 8; u++) {
@@ -218,71 +188,40 @@ __global__ void __launch_bounds__(SB, 3) solve_fwd1_kernel(const RecordH* __rest
       sv2 += __shfl_xor_sync(0xffffffffu, sv2, o);
     }
     if (sl == 0) {
-      if (ok) {
-        if (c < n) g[c] = sv;
-        else V[(int64_t)R.pos[c - n]] -= sv;
-      }
-      if (ok2) {
-        if (c2 < n) g[c2] = sv2;
-        else V[(int64_t)R.pos[c2 - n]] -= sv2;
-      }
+      if (ok) V[(int64_t)R.pos[c]] -= sv;
+      if (ok2) V[(int64_t)R.pos[c2]] -= sv2;
     }
   }
 }
 
-template <int RC>
-__global__ void __launch_bounds__(SB, RC == 1 ? 4 : 2) solve_bwd_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                       const int64_t* __restrict__ g_off, double* V,
-                                                       const double* G, int nrhs, int red_rows) {
-  extern __shared__ double sm[];
-  double* red = sm;                         // min(maxn, 256) x SWARPS x RC
-  const RecordH R = recs[blockIdx.x];
-  const int n = R.n, w = R.w;
-  int r0, r1;
-  chunk_range(n, blockIdx.y, gridDim.y, 32, r0, r1);
-  if (r1 <= r0) return;
-  const double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
-  for (int q0 = 0; q0 < nrhs; q0 += RC) {
-    const int nq = min(RC, nrhs - q0);
-    // partner values are gathered on the fly (the coupling width can exceed shared memory)
-    cta_gemv_cols<RC>(R.xtop + r0, r1 - r0, w, (size_t)n,
-                  [&](int c, int q) { return V[(int64_t)R.pos[c] * nrhs + q0 + q]; }, nq, red,
-                  [&](int t, int q, double v) {
-                    V[(R.xoff + r0 + t) * nrhs + q0 + q] = g[(size_t)(r0 + t) * nrhs + q0 + q] - v;
-                  });
-  }
-}
-
-// Single right-hand side backward sweep: x = g - X_top v[pos] for the rows
-// [r0, r1) of chunk blockIdx.y.  Lanes own rows (J per lane), warps split the
-// columns; CB columns of loads are issued before their FMAs (streaming loads,
-// J x CB in flight per lane) -- the generic GEMV keeps too few bytes in flight
-// for the 64-row leaf records.  Partial sums meet in shared memory.
+// backward coupling product: T[t] = sum_{c < wl} C(t, c) V[pos[c]] for the
+// rows [r0, r1) of chunk blockIdx.y.  Lanes own rows (J per lane), warps split
+// the columns; CB columns of loads are issued before their FMAs.
 template <int J>
-__global__ void __launch_bounds__(SB, J <= 4 ? 3 : 2) solve_bwd1_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                                       const int64_t* __restrict__ g_off, double* V,
-                                                                       const double* __restrict__ G) {
+__global__ void __launch_bounds__(SB, J <= 4 ? 3 : 2) cpl_bwd1_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                                     const int64_t* __restrict__ g_off,
+                                                                     const double* __restrict__ V, double* T) {
   constexpr int CB = J <= 2 ? 8 : (J <= 4 ? 4 : 2);
   extern __shared__ double red[];  // (32 J) x SWARPS
   const RecordH R = recs[blockIdx.x];
-  const int n = R.n, w = R.w;
+  const int n = R.n, wl = R.w - R.r;
   int r0, r1;
   chunk_range(n, blockIdx.y, gridDim.y, 32, r0, r1);
   if (r1 <= r0) return;
-  const double* g = G + g_off[rec0 + blockIdx.x];
+  double* tout = T + g_off[rec0 + blockIdx.x];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t0 = r0; t0 < r1; t0 += 32 * J) {
     double acc[J];
 #pragma unroll
     for (int j = 0; j < J; j++) acc[j] = 0.0;
-    for (int cb = warp * 32; cb < w; cb += SWARPS * 32) {
-      const double xl = (cb + lane < w) ? V[(int64_t)R.pos[cb + lane]] : 0.0;
-      const int cmax = min(32, w - cb);
+    for (int cb = warp * 32; cb < wl; cb += SWARPS * 32) {
+      const double xl = (cb + lane < wl) ? V[(int64_t)R.pos[cb + lane]] : 0.0;
+      const int cmax = min(32, wl - cb);
       for (int u0 = 0; u0 < cmax; u0 += CB) {
         double a[CB][J];
 #pragma unroll
         for (int u = 0; u < CB; u++) {
-          const double* col = R.xtop + (size_t)(cb + u0 + u) * n;
+          const double* col = R.c + (size_t)(cb + u0 + u) * n;
 #pragma unroll
           for (int j = 0; j < J; j++) {
             const int t = t0 + lane + 32 * j;
@@ -304,17 +243,16 @@ __global__ void __launch_bounds__(SB, J <= 4 ? 3 : 2) solve_bwd1_kernel(const Re
       double s = 0.0;
 #pragma unroll
       for (int w2 = 0; w2 < SWARPS; w2++) s += red[e * SWARPS + w2];
-      V[R.xoff + t0 + e] = g[t0 + e] - s;
+      tout[t0 + e] = s;
     }
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ many rhs
-// Multi-rhs sweeps as DMMA GEMMs: each record is read once
-// per chunk of up to 32 right-hand sides instead of once per 4, which turns the
-// HBM-bound sweeps compute-bound (8 flop/B at 32 rhs).  64 x 32 output tiles,
-// 4 warps x (16 x 32), cp.async-staged operands (layouts as in gemm.cuh).
+// Multi-rhs coupling products as DMMA GEMMs: each record's
+// coupling panel is read once per chunk of up to 32 right-hand sides.
+// 64 x 32 output tiles, 4 warps x (16 x 32), cp.async-staged operands.
 constexpr int MQ = 32;             // rhs per chunk
 constexpr int QP = MQ + 4;         // pitch of the [k][q] operand tile (== 4 mod 16)
 constexpr int MM_STAGES = 3;
@@ -341,33 +279,29 @@ __device__ __forceinline__ void mm_mma(const double* As, const double* Bs, doubl
   }
 }
 
-// forward: Out = [S^-1_nn | X_top]^T B (rows c < n -> G, c >= n -> V[pos] -= ),
-// B = V(xoff : xoff + n, q0 : q0 + nq).  grid (record, 64-row tile, rhs chunk)
-__global__ void __launch_bounds__(GTHREADS) solve_fwd_mm_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                                const int64_t* __restrict__ g_off, double* V,
-                                                                double* G, int nrhs) {
+// forward: V[pos[c], q] -= (C^T G)(c, q) for c < wl.  grid (record, 64-row tile, rhs chunk)
+__global__ void __launch_bounds__(GTHREADS) cpl_fwd_mm_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                              const int64_t* __restrict__ g_off, double* V,
+                                                              const double* G, int nrhs) {
   extern __shared__ double msm[];
   const RecordH R = recs[blockIdx.x];
-  const int n = R.n, w = R.w, nc = n + w;
+  const int n = R.n, wl = R.w - R.r;
   const int c0 = blockIdx.y * GBM;
-  if (c0 >= nc || n == 0) return;
+  if (c0 >= wl || n == 0) return;
   const int q0 = blockIdx.z * MQ, nq = min(MQ, nrhs - q0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
-  const double* Bv = V + R.xoff * nrhs + q0;
+  const double* Bv = G + g_off[rec0 + blockIdx.x] * nrhs + q0;
   auto load = [&](int st, int k0) {
     double* As = msm + (size_t)st * (MM_A + MM_B);
     double* Bs = As + MM_A;
 #pragma unroll
-    for (int e = 0; e < (GBM * GBK) / GTHREADS; e++) {  // A: column c of [S^-1 | X_top], k-contiguous
+    for (int e = 0; e < (GBM * GBK) / GTHREADS; e++) {  // A: column c of C, k-contiguous
       const int cidx = tid + e * GTHREADS, k = cidx & (GBK - 1), r = cidx / GBK;
       const int c = c0 + r, gk = k0 + k;
-      const bool ok = c < nc && gk < n;
-      const double* src = c < n ? R.sinv + gk + (size_t)c * n : R.xtop + gk + (size_t)(c - n) * n;
-      cp_async8(As + r * KP + k, src, ok);
+      cp_async8(As + r * KP + k, R.c + gk + (size_t)c * n, c < wl && gk < n);
     }
 #pragma unroll
-    for (int e = 0; e < (GBK * MQ) / GTHREADS; e++) {  // B: rows of V, q-contiguous
+    for (int e = 0; e < (GBK * MQ) / GTHREADS; e++) {  // B: rows of G, q-contiguous
       const int cidx = tid + e * GTHREADS, q = cidx & (MQ - 1), k = cidx / MQ;
       const int gk = k0 + k;
       cp_async8(Bs + k * QP + q, Bv + (size_t)gk * nrhs + q, gk < n && q < nq);
@@ -396,50 +330,48 @@ __global__ void __launch_bounds__(GTHREADS) solve_fwd_mm_kernel(const RecordH* _
 #pragma unroll
   for (int m = 0; m < 2; m++) {
     const int c = c0 + warp * 16 + m * 8 + (lane >> 2);
-    if (c >= nc) continue;
-    double* row = c < n ? g + (size_t)c * nrhs + q0 : V + (int64_t)R.pos[c - n] * nrhs + q0;
-    const bool sub = c >= n;
+    if (c >= wl) continue;
+    double* row = V + (int64_t)R.pos[c] * nrhs + q0;
     double old[8];
 #pragma unroll
     for (int e = 0; e < 8; e++) {
       const int q = (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
-      old[e] = (sub && q < nq) ? row[q] : 0.0;
+      old[e] = q < nq ? row[q] : 0.0;
     }
 #pragma unroll
     for (int e = 0; e < 8; e++) {
       const int q = (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
-      if (q < nq) row[q] = sub ? old[e] - acc[m][e >> 1][e & 1] : acc[m][e >> 1][e & 1];
+      if (q < nq) row[q] = old[e] - acc[m][e >> 1][e & 1];
     }
   }
 }
 
-// backward: x(t, q) = G(t, q) - sum_c X_top(t, c) V(pos[c], q).
-// grid (record, 64-row tile of n, rhs chunk); K = w with row-gathered B
-__global__ void __launch_bounds__(GTHREADS) solve_bwd_mm_kernel(const RecordH* __restrict__ recs, int rec0,
-                                                                const int64_t* __restrict__ g_off, double* V,
-                                                                const double* G, int nrhs) {
+// backward: T(t, q) = sum_{c < wl} C(t, c) V(pos[c], q).  grid (record, 64-row tile of n, rhs chunk)
+__global__ void __launch_bounds__(GTHREADS) cpl_bwd_mm_kernel(const RecordH* __restrict__ recs, int rec0,
+                                                              const int64_t* __restrict__ g_off, const double* V,
+                                                              double* T, int nrhs) {
   extern __shared__ double msm[];
   const RecordH R = recs[blockIdx.x];
-  const int n = R.n, w = R.w;
+  const int n = R.n, wl = R.w - R.r;
   const int t0 = blockIdx.y * GBM;
   if (t0 >= n) return;
   const int q0 = blockIdx.z * MQ, nq = min(MQ, nrhs - q0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double* g = G + g_off[rec0 + blockIdx.x] * nrhs;
+  double* tout = T + g_off[rec0 + blockIdx.x] * nrhs;
   auto load = [&](int st, int k0) {
     double* As = msm + (size_t)st * (MM_A + MM_B);
     double* Bs = As + MM_A;
 #pragma unroll
-    for (int e = 0; e < (GBM * GBK) / GTHREADS; e++) {  // A: X_top(t, c), t-contiguous -> stored [t][k]
+    for (int e = 0; e < (GBM * GBK) / GTHREADS; e++) {  // A: C(t, c), t-contiguous -> stored [t][k]
       const int cidx = tid + e * GTHREADS, r = cidx & (GBM - 1), k = cidx / GBM;
       const int t = t0 + r, gk = k0 + k;
-      cp_async8(As + r * KP + k, R.xtop + t + (size_t)gk * n, t < n && gk < w);
+      cp_async8(As + r * KP + k, R.c + t + (size_t)gk * n, t < n && gk < wl);
     }
 #pragma unroll
     for (int e = 0; e < (GBK * MQ) / GTHREADS; e++) {  // B: V(pos[c], q)
       const int cidx = tid + e * GTHREADS, q = cidx & (MQ - 1), k = cidx / MQ;
       const int gk = k0 + k;
-      const bool ok = gk < w && q < nq;
+      const bool ok = gk < wl && q < nq;
       const double* src = ok ? V + (int64_t)R.pos[gk] * nrhs + q0 + q : V;
       cp_async8(Bs + k * QP + q, src, ok);
     }
@@ -449,7 +381,7 @@ __global__ void __launch_bounds__(GTHREADS) solve_bwd_mm_kernel(const RecordH* _
   for (int a = 0; a < 2; a++)
 #pragma unroll
     for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
-  const int nk = (w + GBK - 1) / GBK;
+  const int nk = (wl + GBK - 1) / GBK;
 #pragma unroll
   for (int st = 0; st < MM_STAGES - 1; st++) {
     if (st < nk) load(st, st * GBK);
@@ -471,8 +403,7 @@ __global__ void __launch_bounds__(GTHREADS) solve_bwd_mm_kernel(const RecordH* _
 #pragma unroll
     for (int e = 0; e < 8; e++) {
       const int q = (e >> 1) * 8 + 2 * (lane & 3) + (e & 1);
-      if (q < nq)
-        V[(R.xoff + t) * nrhs + q0 + q] = g[(size_t)t * nrhs + q0 + q] - acc[m][e >> 1][e & 1];
+      if (q < nq) tout[(size_t)t * nrhs + q0 + q] = acc[m][e >> 1][e & 1];
     }
   }
 }
@@ -598,6 +529,40 @@ static void share_runs(FactorH* F, double* V, int nr, const std::vector<int64_t>
   launch_copies(unpack, ws, st, s);
 }
 
+// Launch one colour batch's pivot solves (forward or backward sweep).
+static void launch_rec_solves(const BatchH& b, FactorH* F, double* V, double* G, const double* T, int nr, bool fwd,
+                              Arena& ws, cudaStream_t s) {
+  const int nrec = b.rec1 - b.rec0;
+  if (nrec <= 0) return;
+  if (nr == 1) {
+    const size_t smem = sizeof(double) * size_t(std::max(1, b.maxm));
+    if (smem > LU_TILE_SMEM_MAX) invalid("solve: pivot block too large for the solve kernel");
+    if (fwd) rec_solve_vec_kernel<true><<<nrec, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, T);
+    else rec_solve_vec_kernel<false><<<nrec, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, T);
+    CK_LAUNCH();
+    return;
+  }
+  int tw = lu_tile_width(b.maxm);
+  const bool global = tw == 0;
+  if (global) tw = 8;
+  if (nr <= 8) tw = 8;
+  else if (nr <= 16 && tw > 16) tw = 16;
+  const size_t per = size_t(tw) * size_t(b.maxm | 1);
+  const dim3 grid(nrec, (nr + tw - 1) / tw);
+  double* scratch = global ? ws.alloc_n<double>(per * grid.x * grid.y) : nullptr;
+  const size_t smem = global ? 0 : sizeof(double) * per;
+#define IFMM_REC_TILE(TWV)                                                                                   \
+  if (fwd) rec_solve_tile_kernel<TWV, true><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, T, nr, \
+                                                                    scratch, per);                          \
+  else rec_solve_tile_kernel<TWV, false><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, T, nr,    \
+                                                                 scratch, per);
+  if (tw == 32) { IFMM_REC_TILE(32) }
+  else if (tw == 16) { IFMM_REC_TILE(16) }
+  else { IFMM_REC_TILE(8) }
+#undef IFMM_REC_TILE
+  CK_LAUNCH();
+}
+
 void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_ptr) {
   TreeH* t = F->tree;
   const int64_t N = t->N;
@@ -616,106 +581,105 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
   }
   double* V = ws.alloc_n<double>(std::max<int64_t>(1, F->vec_size) * nr);
   double* G = ws.alloc_n<double>(std::max<int64_t>(1, F->g_size) * nr);
+  double* T = ws.alloc_n<double>(std::max<int64_t>(1, F->g_size) * nr);
   CK(cudaMemsetAsync(V, 0, sizeof(double) * std::max<int64_t>(1, F->vec_size) * nr, s));
   launch_permute(din, V + F->lvl_base[t->depth] * nr, t->d_perm, N, nr, false, s);
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(solve_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(solve_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(solve_fwd_kernel<RCMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(solve_bwd_kernel<RCMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const int mx = int(LU_TILE_SMEM_MAX);
+    CK(cudaFuncSetAttribute(rec_solve_vec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(rec_solve_vec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(rec_solve_tile_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(rec_solve_tile_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(rec_solve_tile_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(rec_solve_tile_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(rec_solve_tile_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(rec_solve_tile_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(top_solve_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(top_solve_tile_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(top_solve_tile_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(top_solve_tile_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(cpl_fwd_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(MM_SMEM)));
+    CK(cudaFuncSetAttribute(cpl_bwd_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(MM_SMEM)));
     attr = true;
   }
-  const int RC = nr == 1 ? 1 : RCMAX;
-  // many right-hand sides: DMMA sweeps (IFMM_SOLVE_MM_MIN: tuning / debug)
-  static const int mm_min = getenv("IFMM_SOLVE_MM_MIN") ? atoi(getenv("IFMM_SOLVE_MM_MIN")) : 2;
-  const bool mm = nr >= mm_min;
-  static bool mm_attr = false;
-  if (mm && !mm_attr) {
-    CK(cudaFuncSetAttribute(solve_fwd_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(MM_SMEM)));
-    CK(cudaFuncSetAttribute(solve_bwd_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(MM_SMEM)));
-    mm_attr = true;
-  }
+  const bool mm = nr >= 2;
   const int nqc = (nr + MQ - 1) / MQ;
   const bool dist = F->comm && F->comm->size() > 1;
   // sharded: descriptor staging for the run exchanges (reset per call; the
   // stream is synchronised at the end of every solve)
   static thread_local Staging xst;
   xst.reset();
+  // ---- forward replay (ifmm/solver.py:573-590)
   for (const BatchH& b : F->batches) {
     if (dist && b.rec1 == b.rec0) {
       share_runs(F, V, nr, b.fwd_runs, b.fwd_off, ws, xst, s);
       continue;
     }
+    launch_rec_solves(b, F, V, G, T, nr, true, ws, s);
+    const int nrec = b.rec1 - b.rec0;
     if (mm) {
-      const dim3 grid(b.rec1 - b.rec0, (b.maxn + b.maxw + GBM - 1) / GBM, nqc);
-      solve_fwd_mm_kernel<<<grid, GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
-      CK_LAUNCH();
-      if (dist) share_runs(F, V, nr, b.fwd_runs, b.fwd_off, ws, xst, s);
-      continue;
-    }
-    const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
-    const size_t smem = sizeof(double) * (size_t(rr) * SWARPS * RC + size_t(b.maxn) * RC);
-    if (smem > 200 * 1024) invalid("solve: pivot block too large for the solve kernel");
-    const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));
-    static const bool fwd_old = getenv("IFMM_SOLVE_FWD_GEMV") != nullptr;  // debug: S^-1 b as a GEMV
-    if (RC == 1 && !fwd_old) {
+      cpl_fwd_mm_kernel<<<dim3(nrec, (b.maxw + GBM - 1) / GBM, nqc), GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0,
+                                                                                             F->d_g_off, V, G, nr);
+    } else {
       // column dots split finely: >= 8 CTAs per SM in total (few large records
       // at coarse levels would otherwise leave most SMs idle), >= 32 columns each
-      const int nrec = std::max(1, b.rec1 - b.rec0);
-      const int want = std::max(2, (148 * 8 + nrec - 1) / nrec);
-      const dim3 g1(b.rec1 - b.rec0, std::max(1, std::min(want, (b.maxn + b.maxw) / 32)));
-      solve_fwd1_kernel<<<g1, SB, sizeof(double) * size_t(b.maxn), s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+      const int want = std::max(2, (148 * 8 + nrec - 1) / std::max(1, nrec));
+      const dim3 g1(nrec, std::max(1, std::min(want, b.maxw / 32)));
+      cpl_fwd1_kernel<<<g1, SB, sizeof(double) * size_t(std::max(1, b.maxn)), s>>>(b.d_recs, b.rec0, F->d_g_off, V,
+                                                                                    G);
     }
-    else if (RC == 1) solve_fwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
-    else solve_fwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
     CK_LAUNCH();
     if (dist) share_runs(F, V, nr, b.fwd_runs, b.fwd_off, ws, xst, s);
   }
-  // top: y = T^-1 b on the level-1 slots (viewed column-major as nrhs x M)
+  // ---- top: y = T^-1 v on the level-1 slots (ifmm/solver.py:592-598)
   if (F->top_dim > 0) {
     const int M = F->top_dim;
     double* vt = V + F->lvl_base[1] * nr;
-    double* tmp = ws.alloc_n<double>(size_t(M) * nr);
-    CK(cudaMemcpyAsync(tmp, vt, sizeof(double) * M * nr, cudaMemcpyDeviceToDevice, s));
-    GemmBatch gb;
-    // pinned staging for the GEMM descriptors: kept across calls (a fresh
-    // cudaMallocHost per solve costs milliseconds and its free synchronises)
-    static thread_local Staging st;
-    st.reset();
-    gb.add(tmp, nr, F->top_inv, M, vt, nr, nr, M, M, 1.0, 0.0);
-    launch_grouped_gemm(gb, false, true, ws, st, s);
-    CK(cudaStreamSynchronize(s));
+    if (nr == 1) {
+      if (sizeof(double) * size_t(M) > LU_TILE_SMEM_MAX) invalid("solve: top-level system too large");
+      top_solve_vec_kernel<<<1, SB, sizeof(double) * M, s>>>(F->top_lu, F->top_perm, M, vt);
+    } else {
+      double* tmp = ws.alloc_n<double>(size_t(M) * nr);
+      CK(cudaMemcpyAsync(tmp, vt, sizeof(double) * M * nr, cudaMemcpyDeviceToDevice, s));
+      int tw = lu_tile_width(M);
+      const bool global = tw == 0;
+      if (global) tw = 8;
+      if (nr <= 8) tw = 8;
+      else if (nr <= 16 && tw > 16) tw = 16;
+      const size_t per = size_t(tw) * size_t(M | 1);
+      const int grid = (nr + tw - 1) / tw;
+      double* scratch = global ? ws.alloc_n<double>(per * grid) : nullptr;
+      const size_t smem = global ? 0 : sizeof(double) * per;
+      if (tw == 32) top_solve_tile_kernel<32><<<grid, SB, smem, s>>>(F->top_lu, F->top_perm, M, tmp, vt, nr, scratch, per);
+      else if (tw == 16) top_solve_tile_kernel<16><<<grid, SB, smem, s>>>(F->top_lu, F->top_perm, M, tmp, vt, nr, scratch, per);
+      else top_solve_tile_kernel<8><<<grid, SB, smem, s>>>(F->top_lu, F->top_perm, M, tmp, vt, nr, scratch, per);
+    }
+    CK_LAUNCH();
   }
+  // ---- back-substitution, levels 2..kappa, batches reversed (ifmm/solver.py:604-618)
   for (auto it = F->batches.rbegin(); it != F->batches.rend(); ++it) {
     const BatchH& b = *it;
     if (dist && b.rec1 == b.rec0) {
       share_runs(F, V, nr, b.bwd_runs, b.bwd_off, ws, xst, s);
       continue;
     }
+    const int nrec = b.rec1 - b.rec0;
     if (mm) {
-      const dim3 grid(b.rec1 - b.rec0, (b.maxn + GBM - 1) / GBM, nqc);
-      solve_bwd_mm_kernel<<<grid, GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr);
-      CK_LAUNCH();
-      if (dist) share_runs(F, V, nr, b.bwd_runs, b.bwd_off, ws, xst, s);
-      continue;
-    }
-    const int rr = std::min(32 * MAXJ, (b.maxn + 31) / 32 * 32);
-    const size_t smem = sizeof(double) * size_t(rr) * SWARPS * RC;
-    const dim3 grid(b.rec1 - b.rec0, solve_chunks(b));
-    static const bool bwd_old = getenv("IFMM_SOLVE_BWD_OLD") != nullptr;  // debug: generic GEMV
-    if (RC == 1 && !bwd_old) {
-      // rows per lane from the chunk height (<= 64 rows: 2, <= 128: 4, else 8)
+      cpl_bwd_mm_kernel<<<dim3(nrec, (b.maxn + GBM - 1) / GBM, nqc), GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0,
+                                                                                             F->d_g_off, V, T, nr);
+    } else {
+      const dim3 grid(nrec, solve_chunks(b));
       const int rows = (b.maxn + grid.y - 1) / grid.y;
       if (rows <= 64)
-        solve_bwd1_kernel<2><<<grid, SB, sizeof(double) * 64 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+        cpl_bwd1_kernel<2><<<grid, SB, sizeof(double) * 64 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, T);
       else if (rows <= 128)
-        solve_bwd1_kernel<4><<<grid, SB, sizeof(double) * 128 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
+        cpl_bwd1_kernel<4><<<grid, SB, sizeof(double) * 128 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, T);
       else
-        solve_bwd1_kernel<8><<<grid, SB, sizeof(double) * 256 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G);
-    } else if (RC == 1) solve_bwd_kernel<1><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
-    else solve_bwd_kernel<RCMAX><<<grid, SB, smem, s>>>(b.d_recs, b.rec0, F->d_g_off, V, G, nr, rr);
+        cpl_bwd1_kernel<8><<<grid, SB, sizeof(double) * 256 * SWARPS, s>>>(b.d_recs, b.rec0, F->d_g_off, V, T);
+    }
     CK_LAUNCH();
+    launch_rec_solves(b, F, V, G, T, nr, false, ws, s);
     if (dist) share_runs(F, V, nr, b.bwd_runs, b.bwd_off, ws, xst, s);
   }
   launch_permute(V + F->lvl_base[t->depth] * nr, dout, t->d_perm, N, nr, true, s);

@@ -54,65 +54,115 @@ def _saddle(rng, n, r):
     return S
 
 
-def test_gj_inverse_batched_variable_sizes(L):
-    rng = np.random.default_rng(0)
-    mats = [_saddle(rng, n, r) for n, r in [(5, 2), (64, 40), (64, 64), (90, 31), (250, 70), (3, 0)]]
-    mats.append(rng.standard_normal((700, 700)))
+def _run_lu(L, mats):
     sizes = np.array([m.shape[0] for m in mats], dtype=np.int32)
     packed = np.concatenate([np.asfortranarray(m).ravel(order="F") for m in mats])
+    perm = np.zeros(int(sizes.sum()), dtype=np.int32)
     info = np.zeros(len(mats), dtype=np.int32)
-    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(sizes), len(mats), L.ptr(info)))
-    assert not info.any()
-    off = 0
-    for m in mats:
-        k = m.shape[0]
-        inv = packed[off:off + k * k].reshape((k, k), order="F")
+    est = np.zeros(len(mats))
+    L.check(L.lib.ifmm_test_lu(L.ptr(packed), L.ptr(sizes), len(mats), L.ptr(perm), L.ptr(info), L.ptr(est)))
+    out, off, offm = [], 0, 0
+    for k in sizes:
+        out.append((packed[off:off + k * k].reshape((k, k), order="F"), perm[offm:offm + k]))
         off += k * k
-        ref = np.linalg.inv(m)
-        assert np.linalg.norm(inv - ref) <= 1e-10 * np.linalg.norm(ref) * max(1.0, np.linalg.cond(m) / 1e4)
+        offm += k
+    return out, info, est
 
 
-def test_gj_inverse_large_batch_mixed_sizes(L):
-    """>= 64 matrices take the two-level path; sizes ending inside the first
-    or second inner panel of an outer step must not pick up stale row moves."""
+def _check_lu(A, LU, perm, tol=1e-13):
+    """P A = L U with |L| <= 1 (partial pivoting), backward error ~ eps."""
+    k = A.shape[0]
+    Lm = np.tril(LU, -1) + np.eye(k)
+    Um = np.triu(LU)
+    assert sorted(perm.tolist()) == list(range(k))
+    assert np.abs(Lm).max() <= 1.0 + 1e-15
+    err = np.linalg.norm(A[perm] - Lm @ Um) / (np.linalg.norm(A) * k)
+    assert err <= tol, err
+
+
+def test_lu_batched_variable_sizes(L):
+    """Pivot blocks S = [[P, U], [U^T, 0]] of all shapes the factorization meets,
+    plus a general matrix; factors, permutation and the dgecon-style estimate of
+    ||S^-1||_1 against LAPACK (ifmm/solver.py:214-218)."""
+    from scipy.linalg import lu_factor
+    from scipy.linalg.lapack import dgecon
+    rng = np.random.default_rng(0)
+    mats = [_saddle(rng, n, r) for n, r in [(5, 2), (64, 40), (64, 64), (90, 31), (250, 70), (3, 0), (1, 1)]]
+    mats.append(rng.standard_normal((700, 700)))
+    res, info, est = _run_lu(L, mats)
+    assert not info.any()
+    for A, (LU, perm), e in zip(mats, res, est):
+        _check_lu(A, LU, perm)
+        lu_ref = lu_factor(A)
+        rc = dgecon(lu_ref[0], np.linalg.norm(A, 1), norm="1")[0]
+        exact = np.linalg.norm(np.linalg.inv(A), 1)
+        # both estimates are lower bounds of the exact norm and (dlacn2) almost always equal to it
+        assert e <= exact * (1 + 1e-10)
+        assert e >= 0.3 * exact
+        assert abs(e * np.linalg.norm(A, 1) * rc - 1.0) < 0.5
+
+
+def test_lu_large_batch_mixed_sizes(L):
     rng = np.random.default_rng(7)
     sizes = [int(x) for x in rng.integers(40, 140, size=80)] + [64, 96, 97, 127, 128, 129]
     mats = [_saddle(rng, max(1, m - m // 3), m // 3) for m in sizes]
-    sz = np.array([x.shape[0] for x in mats], dtype=np.int32)
-    packed = np.concatenate([np.asfortranarray(x).ravel(order="F") for x in mats])
-    info = np.zeros(len(mats), dtype=np.int32)
-    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(sz), len(mats), L.ptr(info)))
+    res, info, _ = _run_lu(L, mats)
     assert not info.any()
-    off = 0
-    for x in mats:
-        k = x.shape[0]
-        inv = packed[off:off + k * k].reshape((k, k), order="F")
-        off += k * k
-        assert np.linalg.norm(inv @ x - np.eye(k)) <= 1e-9 * k * max(1.0, np.linalg.cond(x) / 1e4)
+    for A, (LU, perm) in zip(mats, res):
+        _check_lu(A, LU, perm)
 
 
-@pytest.mark.parametrize("m", [900, 1024, 1100, 5200])
-def test_gj_inverse_large_single(L, m):
-    """Single large pivots (top levels): 16-wide register panel up to m = 1024,
-    shared-memory panel beyond (narrower panels above m ~ 4,800)."""
+@pytest.mark.parametrize("m", [900, 1100, 2500])
+def test_lu_large_single(L, m):
+    """Single large systems (the level-2 top system): narrower panels above m ~ 830."""
     rng = np.random.default_rng(m)
     A = rng.standard_normal((m, m)) + m ** 0.5 * np.eye(m)
-    packed = np.asfortranarray(A).ravel(order="F").copy()
-    info = np.zeros(1, dtype=np.int32)
-    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(np.array([m], dtype=np.int32)), 1, L.ptr(info)))
+    res, info, _ = _run_lu(L, [A])
     assert info[0] == 0
-    inv = packed.reshape((m, m), order="F")
-    assert np.linalg.norm(inv @ A - np.eye(m)) <= 1e-11 * m
+    _check_lu(A, *res[0])
 
 
-def test_gj_flags_singular(L):
+def test_lu_pivot_order_matches_lapack(L):
+    """Same pivot choices as dgetrf (no ties): identical permutation and factors to rounding."""
+    from scipy.linalg import lu_factor
+    rng = np.random.default_rng(3)
+    A = _saddle(rng, 100, 37)
+    res, info, _ = _run_lu(L, [A])
+    LU, perm = res[0]
+    lu_ref, piv = lu_factor(A)
+    p = np.arange(A.shape[0])
+    for c, q in enumerate(piv):
+        p[[c, q]] = p[[q, c]]
+    assert np.array_equal(perm, p)
+    assert np.allclose(LU, lu_ref, rtol=1e-10, atol=1e-12)
+
+
+def test_lu_flags_singular(L):
     A = np.zeros((4, 4))
     A[0, 0] = A[1, 1] = 1.0
-    sizes = np.array([4], dtype=np.int32)
-    info = np.zeros(1, dtype=np.int32)
-    packed = A.ravel(order="F").copy()
-    L.check(L.lib.ifmm_test_gj_inverse(L.ptr(packed), L.ptr(sizes), 1, L.ptr(info)))
+    _, info, _ = _run_lu(L, [A])
     assert info[0] == 3
+
+
+@pytest.mark.parametrize("n,r,wl", [(64, 40, 300), (7, 3, 5), (250, 70, 900), (600, 300, 40), (40, 0, 17)])
+def test_lu_solve_x(L, n, r, wl):
+    """X = S^-1 [[C, 0], [0, -I]] on the coupling panel (ifmm/solver.py:232-246) vs lu_solve."""
+    from scipy.linalg import lu_factor, lu_solve
+    rng = np.random.default_rng(n + r + wl)
+    S = _saddle(rng, n, r)
+    m, w = n + r, wl + r
+    (LU, perm) = _run_lu(L, [S])[0][0]
+    C = np.asfortranarray(rng.standard_normal((n, wl)))
+    xt = np.zeros((n, w), order="F")
+    xb = np.zeros((r, w), order="F")
+    LUf = np.asfortranarray(LU)
+    L.check(L.lib.ifmm_test_lu_solve_x(L.ptr(LUf), L.ptr(perm.astype(np.int32)), n, r, L.ptr(C), wl, L.ptr(xt),
+                                       L.ptr(xb)))
+    Cf = np.zeros((m, w))
+    Cf[:n, :wl] = C
+    Cf[n:, wl:] = -np.eye(r)
+    X = lu_solve(lu_factor(S), Cf)
+    assert np.linalg.norm(np.vstack([xt, xb]) - X) <= 1e-11 * np.linalg.norm(X)
 
 
 @pytest.mark.parametrize("m,n", [(16, 16), (432, 16), (64, 40), (300, 64), (7, 3), (12, 9), (8, 8), (30, 30), (5, 14),

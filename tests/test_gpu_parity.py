@@ -4,9 +4,13 @@ the reference goldens (tests/golden, made by oracle/gen_golden.py).
 Gates:
   G1 tree / lists / colouring bit-exact;
   G2 exact mode (tol = 0): solution vs dense LU <= 1e-11;
-  G3 residual vs the FMM operator <= max(10 eps, 2 x the reference's residual);
-  G4 solution difference vs the oracle in the same (colour9) order;
-  G5 initial ranks equal, r_m within 25 %.
+  G3 residual vs the FMM operator <= max(10 eps, 2 x the reference's own
+     (Morton-order) residual);
+  G4 solution difference vs the reference run in the same (colour9) order:
+     <= 10 eps for the log kernel, <= 2 x the reference's own Morton-vs-colour
+     difference for 1/r (SURVEY.md finding 5: eps x cond apart);
+  G5 initial ranks equal, top-level dimension within 10 %, r_m within 25 %,
+     per-level statistics against the reference's.
 """
 import numpy as np
 import pytest
@@ -94,14 +98,17 @@ def test_factor_solve_residual_and_solution(ifmm, name):
     x = ifmm.solve(fact, g["b"])
     b = g["b"]
     res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
-    ref_res = max(float(g["resid_morton"]), float(g["resid_colour9"]))
-    # G3: residual against the compressed operator
+    ref_res = float(g["resid_morton"])
+    # G3: residual against the compressed operator, vs the reference's own
     assert res <= max(10 * tol, 2 * ref_res), (res, ref_res)
     # G4: solution vs the reference run in the same colour order
     xc = g["x_colour9"]
     diff = np.linalg.norm(x - xc) / np.linalg.norm(xc)
-    morton_vs_colour = np.linalg.norm(g["x_morton"] - xc) / np.linalg.norm(xc)
-    assert diff <= max(10 * tol, 2 * morton_vs_colour), (diff, morton_vs_colour)
+    if str(g["kernel"]).startswith("log"):
+        assert diff <= 10 * tol, diff
+    else:
+        morton_vs_colour = np.linalg.norm(g["x_morton"] - xc) / np.linalg.norm(xc)
+        assert diff <= max(10 * tol, 2 * morton_vs_colour), (diff, morton_vs_colour)
     # G5: ranks.  r_m (max ACA rank) is noise-driven near the cutoff: the CPU
     # oracle itself drops from 28 to 16 on reglog_1k when its LU solves are
     # replaced by an explicit inverse, so gate
@@ -109,6 +116,51 @@ def test_factor_solve_residual_and_solution(ifmm, name):
     ref_top = int(g["top_colour9"])
     assert abs(fact.top_dim - ref_top) <= 0.1 * ref_top, (fact.top_dim, ref_top)
     assert fact.r_m <= 1.25 * int(g["rm_colour9"]) + 1
+    _check_level_stats(fact, g["stats_colour9"])
+
+
+def _check_level_stats(fact, ref):
+    """Per-level LevelStats vs the reference in the same order (ifmm/solver.py:77-82,138-147):
+    cluster counts exact, no dense-kept fill where the reference kept none, compressed-fill
+    counts within 2 % (the batch's fills are the same pairs; a rank decision at the cutoff
+    can make one fill vanish), max ACA rank within 25 %."""
+    for k, clusters, max_rank, compressed, dense in ref:
+        s = fact.level_stats[int(k)]
+        assert s.clusters == clusters, (k, s.clusters, clusters)
+        assert (s.fillins_dense_kept == 0) == (dense == 0), (k, s.fillins_dense_kept, dense)
+        assert abs(s.fillins_compressed - compressed) <= 0.02 * compressed + 1, (k, s.fillins_compressed, compressed)
+        assert s.max_rank <= 1.25 * max_rank + 1, (k, s.max_rank, max_rank)
+
+
+@pytest.mark.slow
+def test_c3_itself_against_the_reference(ifmm):
+    """BASELINE C3 (N = 1,048,576, 1/r, depth 7, eps 1e-6) against the reference algorithm run
+    at C3 on the GPU box's host (tests/golden/c3_1m.npz, oracle/run_c3.py; 20 min / 68 GB on one
+    core).  The reference itself meets pivots above its 1e12 condition limit here (level 6 in
+    Morton order, level 5 in colour order: it would raise SingularPivotError), so both runs use
+    the relaxed limit the bench uses and record those pivots instead."""
+    from oracle import ifmm_oracle as O
+    g = load_golden("c3_1m")
+    N, depth, tol = int(g["N"]), int(g["depth"]), float(g["tol"])
+    assert len(g["singular_morton"]) > 0 and len(g["singular_colour9"]) > 0
+    pts = O.baseline_points(N, seed=0)
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    # G1 at C3: the stable Morton permutation and leaf offsets
+    assert np.array_equal(tree.point_permutation, g["perm"])
+    assert np.array_equal(tree.leaf_offsets, g["leaf_off"])
+    store = ifmm.init_operators(tree, ifmm.baseline_kernel("inv_r", N), p=int(g["p"]), tol=tol)
+    fact = ifmm.factorize(store, tree, pivot_condition_limit=1e15)
+    b = O.baseline_rhs(N, "normal")
+    x = ifmm.solve(fact, b)
+    res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
+    ref = float(g["resid_morton"])
+    assert res <= 2 * ref, (res, ref)  # G3 against the reference's Morton residual
+    xc, xm = g["x_colour9"], g["x_morton"]
+    diff = np.linalg.norm(x - xc) / np.linalg.norm(xc)
+    mvc = np.linalg.norm(xm - xc) / np.linalg.norm(xc)
+    assert diff <= 2 * mvc, (diff, mvc)  # G4
+    assert abs(fact.top_dim - int(g["top_colour9"])) <= 0.1 * int(g["top_colour9"])
+    _check_level_stats(fact, g["stats_colour9"])
 
 
 def test_exact_mode_vs_dense_lu(ifmm):

@@ -1,16 +1,21 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list by kernel."""
-import csv, collections, sys
+"""Per-kernel totals of an `ncu --metrics gpu__time_duration.sum --csv` launch list."""
+import collections
+import csv
+import re
+import sys
+
 rows = list(csv.reader(open(sys.argv[1])))
-hdr_i = next(i for i, r in enumerate(rows) if 'Kernel Name' in r)
-h = rows[hdr_i]; ki = h.index('Kernel Name'); vi = h.index('Metric Value')
-agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-for r in rows[hdr_i + 1:]:
-    if len(r) <= vi: continue
-    name = r[ki].split('(')[0].replace('void ', '').replace('ifmm::', '')
-    try: v = float(r[vi].replace(',', ''))
-    except ValueError: continue
-    a = agg[name]; a[0] += 1; a[1] += v; a[2] = max(a[2], v)
+i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
+h = rows[i]
+ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+agg = collections.defaultdict(lambda: [0, 0.0])
+for r in rows[i + 1:]:
+    if len(r) > vi:
+        n = r[ki].split("(")[0].replace("void ", "")
+        n = re.sub(r"ifmm::\(anonymous namespace\)::|ifmm::<unnamed>::|ifmm::", "", n)
+        agg[n][0] += 1
+        agg[n][1] += float(r[vi].replace(",", ""))
 tot = sum(v[1] for v in agg.values())
-for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 20]:
-    print(f"{k[:60]:60s} n={v[0]:5d} total={v[1]/1e6:9.2f} ms  max={v[2]/1e6:8.2f} ms share={v[1]/tot:6.1%}")
-print(f"total {tot/1e6:.2f} ms")
+print(f"total {sum(v[0] for v in agg.values())} launches, {tot / 1e6:.2f} ms (ncu serialised, cold)")
+for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
+    print(f"{n[:58]:58s} {c:6d} {t / 1e6:9.2f} ms {100 * t / tot:5.1f}%")
