@@ -39,7 +39,10 @@ enum {
 };
 
 enum { IFMM_PTR_HOST = 0, IFMM_PTR_DEVICE = 1 };
-enum { IFMM_FLAG_TIMING = 1 };
+/* IFMM_FLAG_RECORD_SINGULAR: pivots whose condition estimate exceeds the limit
+ * are recorded (ifmm_factor_singular) and the factorization goes on; without it
+ * the first one raises IFMM_SINGULAR_PIVOT, as the reference does */
+enum { IFMM_FLAG_TIMING = 1, IFMM_FLAG_RECORD_SINGULAR = 2 };
 
 /* kernel ids: the reference registry ifmm/kernels.py:160-170 plus the two
  * BASELINE kernels inv_r = scale/r and log_r = scale*(ln r + shift) */
@@ -104,6 +107,13 @@ int ifmm_factorize(ifmm_store* s, double tol, int flags, double cond_limit, ifmm
 int ifmm_factor_info(const ifmm_factor* f, int* r_m, int* top_dim, int64_t* n_records, double* ms);
 /* LevelStats of `level`: clusters, max_rank, fillins_compressed, fillins_dense_kept */
 int ifmm_factor_level_stats(const ifmm_factor* f, int level, int32_t* out4);
+/* largest pivot condition estimate ||S||_1 * est(||S^-1||_1) of `level` (the
+ * quantity the reference compares with PIVOT_CONDITION_LIMIT, ifmm/solver.py:214-218) */
+int ifmm_factor_level_cond(const ifmm_factor* f, int level, double* max_cond);
+/* IFMM_FLAG_RECORD_SINGULAR: *count pivots exceeded the limit; the first `cap`
+ * are written as (level, index, cond) in elimination order (arrays may be null) */
+int ifmm_factor_singular(const ifmm_factor* f, int64_t cap, int32_t* level, int32_t* index, double* cond,
+                         int64_t* count);
 /* per elimination (in order): level, index, n, r, w */
 int ifmm_factor_records(const ifmm_factor* f, int32_t* out5);
 /* work accounting: out[0] executed FP64 flops (GJ inverses, X = S^-1 C,

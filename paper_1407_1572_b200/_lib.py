@@ -59,6 +59,8 @@ SIGNATURES = {
     "ifmm_factorize": (_i32, [_p, _d, _i32, _d, ctypes.POINTER(_p)]),
     "ifmm_factor_info": (_i32, [_p, _pi32, _pi32, _pi64, _pd]),
     "ifmm_factor_level_stats": (_i32, [_p, _i32, _p]),
+    "ifmm_factor_level_cond": (_i32, [_p, _i32, _pd]),
+    "ifmm_factor_singular": (_i32, [_p, _i64, _p, _p, _p, _pi64]),
     "ifmm_factor_records": (_i32, [_p, _p]),
     "ifmm_factor_work": (_i32, [_p, _p]),
     "ifmm_factor_timing": (_i32, [_p, _p, _p]),
@@ -136,6 +138,12 @@ def as_input(x, rows: int):
         t = t.to(torch.float64).contiguous()
         nr = 1 if t.dim() == 1 else int(t.shape[1])
         kind = PTR_DEVICE if t.is_cuda else PTR_HOST
+        if kind == PTR_DEVICE:
+            # the library reads device buffers on its own stream: wait for torch's
+            # stream to finish producing this tensor (and the copy made above)
+            if t.device.index != torch.cuda.current_device():
+                raise ValueError(f"tensor on {t.device}, but the library runs on cuda:{torch.cuda.current_device()}")
+            torch.cuda.current_stream(t.device).synchronize()
         if kind == PTR_HOST:
             a = t.numpy()
             return ptr(a), PTR_HOST, nr, a, True, t.dim() == 1

@@ -261,6 +261,26 @@ int ifmm_factor_level_stats(const ifmm_factor* f, int level, int32_t* out4) {
   });
 }
 
+int ifmm_factor_level_cond(const ifmm_factor* f, int level, double* max_cond) {
+  return guard([&] {
+    if (level < 2 || level >= int(f->h->stats.size())) invalid("level out of range");
+    *max_cond = f->h->stats[level].max_cond;
+  });
+}
+
+int ifmm_factor_singular(const ifmm_factor* f, int64_t cap, int32_t* level, int32_t* index, double* cond,
+                         int64_t* count) {
+  return guard([&] {
+    const auto& v = f->h->singular;
+    if (count) *count = int64_t(v.size());
+    for (int64_t q = 0; q < std::min<int64_t>(cap, int64_t(v.size())); q++) {
+      if (level) level[q] = v[q].level;
+      if (index) index[q] = v[q].index;
+      if (cond) cond[q] = v[q].cond;
+    }
+  });
+}
+
 int ifmm_factor_records(const ifmm_factor* f, int32_t* out5) {
   return guard([&] {
     size_t u = 0;

@@ -133,6 +133,12 @@ struct StoreH {
 
 struct LevelStatsH {
   int clusters = 0, max_rank = 0, compressed = 0, dense_kept = 0;
+  double max_cond = 0;  // largest pivot condition estimate ||S||_1 est||S^-1||_1 (this rank's pivots)
+};
+// A pivot whose condition estimate exceeded the limit (IFMM_FLAG_RECORD_SINGULAR)
+struct SingularH {
+  int level, index;
+  double cond;
 };
 
 // Solve record of one elimination (the reference's _Record, ifmm/solver.py:63-74):
@@ -187,6 +193,7 @@ struct FactorH {
   double phase_ms[8] = {0};
   long long phase_launches[8] = {0};
   int deferred_batches = 0;  // colour batches split by the independence guard
+  std::vector<SingularH> singular;  // IFMM_FLAG_RECORD_SINGULAR: pivots over the limit, in elimination order
   std::vector<std::array<double, 8>> phase_lvl_ms;  // [level][phase]
   std::vector<std::array<double, 2>> host_lvl_ms;   // [level]: host busy until the final sync, time blocked in it
   // sharded factorization (null / 1 rank otherwise): the communicator the
@@ -213,6 +220,9 @@ enum PhaseId : int {
   PH_COMM = 7,       // sharded runs: metadata all-gathers + halo pack/exchange/unpack
 };
 constexpr int IFMM_FLAG_TIMING = 1;
+// Record pivots whose condition estimate exceeds the limit and go on, instead
+// of raising SingularPivotError at the first one (the reference raises).
+constexpr int IFMM_FLAG_RECORD_SINGULAR = 2;
 
 // ------------------------------------------------------------ entry points
 TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_ptr);

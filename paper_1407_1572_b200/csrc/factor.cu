@@ -883,15 +883,23 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   // first numerically singular own pivot (batch position), if any
   int err_pos = INT_MAX, err_index = -1;
   double err_cond = 0;
+  const bool record_only = (flags_ & IFMM_FLAG_RECORD_SINGULAR) != 0;
   for (int u = 0; u < no; u++) {
     const PivInfo& I = P[own[u]];
     if (I.m == 0) continue;  // an empty cluster (clustered inputs): nothing to eliminate
     double rc = (info[u] != 0) ? 0.0 : 1.0 / (nS[u] * nSi[u]);
+    const double cond = 1.0 / std::max(rc, 1e-300);
+    F_->stats[k].max_cond = std::max(F_->stats[k].max_cond, std::isfinite(cond) ? cond : INFINITY);
     if (!std::isfinite(rc) || rc <= 1.0 / cond_limit_) {
-      err_pos = own[u];
-      err_index = I.i;
-      err_cond = 1.0 / std::max(rc, 1e-300);
-      break;
+      if (record_only) {
+        F_->singular.push_back(SingularH{k, I.i, cond});
+        continue;
+      }
+      if (err_pos == INT_MAX) {
+        err_pos = own[u];
+        err_index = I.i;
+        err_cond = cond;
+      }
     }
   }
   // fill outcomes in global fill order (-1: another rank's fill)

@@ -257,21 +257,23 @@ __global__ void __launch_bounds__(GTHREADS, 3) lu_update_kernel(const MatDesc* _
 }
 
 // ------------------------------------------------------------------ condition estimate
-// y = S^-1 x (x, y distinct shared vectors; t scratch)
+// dgecon estimates ||A^-1||_1 as ||U^-1 L^-1||_1 (the row permutation only
+// permutes columns of A^-1, which leaves the 1-norm unchanged) and runs the
+// estimator on the triangular factors alone; so do these, so that the
+// estimator's iterates -- hence the estimate -- follow LAPACK's.
+// y = U^-1 L^-1 x (x, y distinct shared vectors)
 __device__ inline void lu_apply(const MatDesc& D, const double* x, double* y) {
-  for (int l = threadIdx.x; l < D.m; l += blockDim.x) y[l] = x[D.ipiv[l]];
+  for (int l = threadIdx.x; l < D.m; l += blockDim.x) y[l] = x[l];
   __syncthreads();
   cta_trsv_lower_unit(D.A, D.lda, D.m, y);
   cta_trsv_upper(D.A, D.lda, D.m, y);
 }
-// y = S^-T x  (S^-T = P^T L^-T U^-T)
-__device__ inline void lu_apply_t(const MatDesc& D, const double* x, double* y, double* t) {
-  for (int l = threadIdx.x; l < D.m; l += blockDim.x) t[l] = x[l];
+// y = L^-T U^-T x
+__device__ inline void lu_apply_t(const MatDesc& D, const double* x, double* y) {
+  for (int l = threadIdx.x; l < D.m; l += blockDim.x) y[l] = x[l];
   __syncthreads();
-  cta_trsv_upper_t(D.A, D.lda, D.m, t);
-  cta_trsv_lower_unit_t(D.A, D.lda, D.m, t);
-  for (int l = threadIdx.x; l < D.m; l += blockDim.x) y[D.ipiv[l]] = t[l];
-  __syncthreads();
+  cta_trsv_upper_t(D.A, D.lda, D.m, y);
+  cta_trsv_lower_unit_t(D.A, D.lda, D.m, y);
 }
 __device__ inline double vasum(const double* v, int n, double* red) {
   double s = 0.0;
@@ -299,7 +301,6 @@ __global__ void __launch_bounds__(256, 3) lu_inv_norm1_kernel(const MatDesc* __r
   double* x = sm;
   double* y = x + n;
   double* sgn = y + n;
-  double* t = sgn + n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = 1.0 / n;
   __syncthreads();
   lu_apply(D, x, y);
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(256, 3) lu_inv_norm1_kernel(const MatDesc* __r
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) sgn[i] = y[i] >= 0.0 ? 1.0 : -1.0;
   __syncthreads();
-  lu_apply_t(D, sgn, x, t);
+  lu_apply_t(D, sgn, x);
   int jj = viamax(x, n, ared);
   for (int iter = 2;; iter++) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = (i == jj) ? 1.0 : 0.0;
@@ -326,10 +327,13 @@ __global__ void __launch_bounds__(256, 3) lu_inv_norm1_kernel(const MatDesc* __r
     if (!s_flag || est <= old) break;
     for (int i = threadIdx.x; i < n; i += blockDim.x) sgn[i] = y[i] >= 0.0 ? 1.0 : -1.0;
     __syncthreads();
-    lu_apply_t(D, sgn, x, t);
+    lu_apply_t(D, sgn, x);
     const int jlast = jj;
     jj = viamax(x, n, ared);
-    if (!(x[jlast] != fabs(x[jj]) && iter < 5)) break;
+    // every thread reads x before any thread overwrites it for the next iterate
+    const bool again = x[jlast] != fabs(x[jj]) && iter < 5;
+    __syncthreads();
+    if (!again) break;
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     x[i] = ((i & 1) ? -1.0 : 1.0) * (1.0 + double(i) / double(n - 1));
@@ -435,7 +439,7 @@ void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_inf
 
 void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s) {
   if (n <= 0) return;
-  const size_t smem = sizeof(double) * 4 * size_t(std::max(1, maxm));
+  const size_t smem = sizeof(double) * 3 * size_t(std::max(1, maxm));
   if (smem > 224 * 1024) invalid("pivot block too large for the condition estimate");
   static bool attr = false;
   if (!attr) {

@@ -54,6 +54,10 @@ class IfmmFactorization:
     n_records: int = 0
     factor_ms: float = 0.0
     last_refinement: list = field(default_factory=list)
+    # extension: largest pivot condition estimate per level, and (with
+    # on_singular="record") every pivot over the limit as (level, index, cond)
+    max_cond: dict = field(default_factory=dict)
+    singular_pivots: list = field(default_factory=list)
 
     @property
     def n(self) -> int:
@@ -114,7 +118,8 @@ PHASES = ("gather", "gauss_jordan", "x_gemm", "schur_gemm", "compress", "transit
 
 def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None, diagnostics: bool = False,
               release_m2l: bool = True, timing: bool = False,
-              pivot_condition_limit: float = PIVOT_CONDITION_LIMIT, comm=None) -> IfmmFactorization:
+              pivot_condition_limit: float = PIVOT_CONDITION_LIMIT, comm=None,
+              on_singular: str = "raise") -> IfmmFactorization:
     """Eliminate the extended system on the GPU (ifmm/solver.py:106-153).
 
     Unlike the reference the store's initial operators stay intact (the
@@ -124,11 +129,19 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
 
     comm (extension): a `distributed.Communicator`; the call is then
     collective over its ranks, each eliminating its own level-2 subtrees
-    (every rank passes the same store contents)."""
+    (every rank passes the same store contents).
+
+    on_singular (extension): "raise" (the reference's behaviour,
+    ifmm/solver.py:214-218) raises SingularPivotError at the first pivot whose
+    condition estimate exceeds `pivot_condition_limit`; "record" lists such
+    pivots in `fact.singular_pivots` and carries on (sharded runs: each rank
+    lists its own pivots)."""
+    if on_singular not in ("raise", "record"):
+        raise ValueError(f"on_singular must be 'raise' or 'record', got {on_singular!r}")
     if tol is None:
         tol = store.tol
     h = ctypes.c_void_p()
-    flags = 1 if timing else 0
+    flags = (1 if timing else 0) | (2 if on_singular == "record" else 0)
     if comm is not None and comm.size > 1:
         _lib.check(_lib.lib.ifmm_factorize_sharded(store.handle, comm.handle, float(tol), flags,
                                                    float(pivot_condition_limit), ctypes.byref(h)))
@@ -155,6 +168,18 @@ def _wrap_factor(store: OperatorStore, tree: ClusterTree, tol: float, h) -> Ifmm
         st = np.zeros(4, dtype=np.int32)
         _lib.check(_lib.lib.ifmm_factor_level_stats(h, k, _lib.ptr(st)))
         fact.level_stats[k] = LevelStats(*map(int, st))
+        c = ctypes.c_double()
+        _lib.check(_lib.lib.ifmm_factor_level_cond(h, k, ctypes.byref(c)))
+        fact.max_cond[k] = c.value
+    cnt = ctypes.c_int64()
+    _lib.check(_lib.lib.ifmm_factor_singular(h, 0, None, None, None, ctypes.byref(cnt)))
+    if cnt.value:
+        lv = np.zeros(cnt.value, dtype=np.int32)
+        ix = np.zeros(cnt.value, dtype=np.int32)
+        cd = np.zeros(cnt.value)
+        _lib.check(_lib.lib.ifmm_factor_singular(h, cnt.value, _lib.ptr(lv), _lib.ptr(ix), _lib.ptr(cd),
+                                                 ctypes.byref(cnt)))
+        fact.singular_pivots = [(int(a), int(b), float(c)) for a, b, c in zip(lv, ix, cd)]
     return fact
 
 
