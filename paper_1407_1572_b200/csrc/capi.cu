@@ -550,7 +550,8 @@ int ifmm_test_lu(double* a, const int32_t* m, int count, int32_t* perm, int32_t*
     int* dinfo = ws.alloc_n<int>(count);
     double* dn = ws.alloc_n<double>(count);
     ifmm::batched_lu(md, dmd, dinfo, ws, st, s);
-    ifmm::launch_lu_inv_norm1(dmd, count, maxm, dn, s);
+    const ifmm::LuDiag dg = ifmm::launch_lu_diag_inv(md, dmd, ws, st, s, 0.0);
+    ifmm::launch_lu_inv_norm1(dmd, count, maxm, dg, dn, s);
     CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(a, d, sizeof(double) * tot, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(perm, dp, sizeof(int) * totm, cudaMemcpyDeviceToHost));
@@ -577,7 +578,10 @@ int ifmm_test_lu_solve_x(const double* lu, const int32_t* perm, int n, int r, co
     CK(cudaMemcpy(dlu, lu, sizeof(double) * m * m, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dp, perm, sizeof(int) * m, cudaMemcpyHostToDevice));
     if (n * wl > 0) CK(cudaMemcpy(dc, c, sizeof(double) * n * wl, cudaMemcpyHostToDevice));
-    std::vector<ifmm::XSolveDesc> xd{ifmm::XSolveDesc{dlu, dp, dc, dt, db, m, n, r, wl, w, 0}};
+    std::vector<MatDesc> md{MatDesc{dlu, m, m, dp, 0}};
+    const MatDesc* dmd = upload(ws, md, s, st);
+    const ifmm::LuDiag dg = ifmm::launch_lu_diag_inv(md, dmd, ws, st, s, 0.0);  // refine every block
+    std::vector<ifmm::XSolveDesc> xd{ifmm::XSolveDesc{dlu, dp, dc, dt, db, dg.dinv, dg.flags, m, n, r, wl, w, 0}};
     ifmm::launch_lu_solve_x(xd, ws, st, s);
     CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(xtop, dt, sizeof(double) * n * w, cudaMemcpyDeviceToHost));

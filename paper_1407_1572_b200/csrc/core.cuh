@@ -108,8 +108,30 @@ struct InitLevel {
 // Device workspaces of factorize(), kept with the store so that repeated
 // factorizations (factor-once/solve-many is per factorization; benchmarks and
 // parameter sweeps refactorize) do not pay cudaMalloc/cudaFree every call.
+// A second stream for work that only needs to finish by the end of a colour
+// batch (the pivot condition estimates), forked from / joined to the
+// factorization stream with events.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  void ensure() {
+    if (s) return;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  }
+  ~SideStream() {
+    if (s) {
+      cudaStreamDestroy(s);
+      cudaEventDestroy(fork);
+      cudaEventDestroy(join);
+    }
+  }
+};
+
 struct FactorWork {
   std::mutex mu;
+  SideStream side;
   Arena ws{size_t(256) << 20};
   Staging st;
   Arena lvl[2] = {Arena(size_t(2) << 30), Arena(size_t(2) << 30)};

@@ -548,6 +548,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   const int np = int(piv.size());
   hmark(0);
   CK(cudaStreamSynchronize(s_));  // staging buffers of earlier uploads are free after this
+  if (work_->side.s) CK(cudaStreamSynchronize(work_->side.s));
   ws_.reset();
   st_.reset();
   hmark(1);
@@ -639,6 +640,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   // batch are independent, and kernel shapes come from the whole batch (np,
   // gmaxm, shape_mx, fh.size()), so the arithmetic does not depend on chunking.
   const int nchunks = 1;
+  bool est_pending = false;
   for (int ch = 0; ch < nchunks && no > 0; ch++) {
     const int u0 = int(int64_t(no) * ch / nchunks), u1 = int(int64_t(no) * (ch + 1) / nchunks);
     const int nc_ = u1 - u0;
@@ -674,7 +676,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         s++;
       }
       cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
-      xd.push_back(XSolveDesc{I.S, I.perm, I.C, I.Xt, I.Xb, I.m, I.n, I.r, I.w - I.r, I.w, 0});
+      xd.push_back(XSolveDesc{I.S, I.perm, I.C, I.Xt, I.Xb, nullptr, nullptr, I.m, I.n, I.r, I.w - I.r, I.w, 0});
     }
     hmark(12);
     tm_.begin(PH_GATHER);
@@ -688,7 +690,21 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       launch_norm1(dmd, nc_, maxm, d_nS + u0, s_);
       // panel width from the whole batch (across chunks and ranks): same arithmetic as one launch
       batched_lu(md, dmd, d_info + u0, ws_, st_, s_, gmaxm);
-      launch_lu_inv_norm1(dmd, nc_, maxm, d_nSi + u0, s_);
+      const LuDiag dg = launch_lu_diag_inv(md, dmd, ws_, st_, s_, tol_);
+      // the condition estimates only gate the batch's read-back: run them on
+      // the side stream, overlapped with the X solve, Schur update and fill
+      // compression (which read the factors but never write them)
+      SideStream& sd = work_->side;
+      sd.ensure();
+      CK(cudaEventRecord(sd.fork, s_));
+      CK(cudaStreamWaitEvent(sd.s, sd.fork, 0));
+      launch_lu_inv_norm1(dmd, nc_, maxm, dg, d_nSi + u0, sd.s);
+      for (size_t q = 0; q < xd.size(); q++) {
+        xd[q].dinv = dg.dinv + dg.h_off[q];
+        xd[q].dflag = dg.flags + dg.h_off[q] / (LU_XB * LU_XB);
+      }
+      CK(cudaEventRecord(sd.join, sd.s));
+      est_pending = true;
     }
     hmark(3);
     // records + X = S^-1 C (getrs on the coupling panel)
@@ -848,6 +864,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     for (int f = fill_off[t]; f < fill_off[t + 1]; f++) m2l_ref(W, fh[f].p, fh[f].q, true);
   }
   // read back: pivot conditioning, ranks, fill outcomes, counters
+  if (est_pending) CK(cudaStreamWaitEvent(s_, work_->side.join, 0));
   const auto t_sync0 = std::chrono::steady_clock::now();
   std::vector<double> nS(no), nSi(no);
   std::vector<int> info(no), stats(4);

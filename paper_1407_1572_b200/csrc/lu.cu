@@ -4,6 +4,7 @@
 // lu_solve (dgetrs) (ifmm/solver.py:214-218,246); these kernels do the same
 // on a whole colour batch at once.
 #include <algorithm>
+#include <string>
 
 #include "gemm.cuh"
 #include "lu.cuh"
@@ -11,6 +12,8 @@
 namespace ifmm {
 
 namespace {
+
+constexpr int XB = LU_XB;
 
 struct RowMove {
   int dst, src;
@@ -256,24 +259,160 @@ __global__ void __launch_bounds__(GTHREADS, 3) lu_update_kernel(const MatDesc* _
   }
 }
 
-// ------------------------------------------------------------------ condition estimate
-// dgecon estimates ||A^-1||_1 as ||U^-1 L^-1||_1 (the row permutation only
-// permutes columns of A^-1, which leaves the 1-norm unchanged) and runs the
-// estimator on the triangular factors alone; so do these, so that the
-// estimator's iterates -- hence the estimate -- follow LAPACK's.
-// y = U^-1 L^-1 x (x, y distinct shared vectors)
-__device__ inline void lu_apply(const MatDesc& D, const double* x, double* y) {
-  for (int l = threadIdx.x; l < D.m; l += blockDim.x) y[l] = x[l];
+// ------------------------------------------------------------------ diagonal-block inverses
+// Inverses of the XB x XB diagonal blocks of L (unit lower) and U: the
+// triangular solves below are then blocked GEMM-shaped steps -- the classic
+// batched-TRSM scheme -- with no serial substitution chain left in them.
+// grid (matrix, block), 128 threads: thread t < 64 inverts column t of L_kk,
+// t >= 64 column t - 64 of U_kk.  Blocks past m are padded with the identity.
+__global__ void __launch_bounds__(128) lu_diag_inv_kernel(const MatDesc* __restrict__ desc,
+                                                          const int64_t* __restrict__ doff, double* dinv,
+                                                          unsigned char* flags, double kappa_max) {
+  __shared__ double T[XB][XB + 1];
+  __shared__ double cn[2][XB][2];  // per inverted column: 1-norm of T_kk's column, of the inverse's column
+  const MatDesc D = desc[blockIdx.x];
+  const int nb = (D.m + XB - 1) / XB, k = blockIdx.y;
+  if (k >= nb) return;
+  const int kb = XB * k, bb = min(XB, D.m - kb);
+  for (int e = threadIdx.x; e < XB * XB; e += 128) {
+    const int r = e % XB, c = e / XB;
+    T[r][c] = (r < bb && c < bb) ? D.A[(kb + r) + (size_t)(kb + c) * D.lda] : (r == c ? 1.0 : 0.0);
+  }
   __syncthreads();
-  cta_trsv_lower_unit(D.A, D.lda, D.m, y);
-  cta_trsv_upper(D.A, D.lda, D.m, y);
+  const int t = threadIdx.x & (XB - 1);
+  double x[XB];
+  double* out = dinv + doff[blockIdx.x] + (size_t)k * 2 * XB * XB;
+  if (threadIdx.x < XB) {  // L_kk^-1 e_t, forward
+#pragma unroll
+    for (int i = 0; i < XB; i++) {
+      double v = (i == t) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < i; j++) v = fma(-T[i][j], x[j], v);
+      x[i] = v;
+    }
+  } else {  // U_kk^-1 e_t, backward
+#pragma unroll
+    for (int i = XB - 1; i >= 0; i--) {
+      double v = (i == t) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = i + 1; j < XB; j++) v = fma(-T[i][j], x[j], v);
+      x[i] = v / T[i][i];
+    }
+    out += XB * XB;
+  }
+  double inv1 = 0.0, t1 = 0.0;
+#pragma unroll
+  for (int i = 0; i < XB; i++) {
+    out[i + XB * t] = x[i];
+    inv1 += fabs(x[i]);
+  }
+  const bool up = threadIdx.x >= XB;
+  for (int i = 0; i < XB; i++)  // column t of the triangle itself (unit diagonal for L)
+    if (up ? i <= t : i >= t) t1 += (!up && i == t) ? 1.0 : fabs(T[i][t]);
+  cn[up][t][0] = t1;
+  cn[up][t][1] = inv1;
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    // kappa_1(T_kk) = ||T_kk||_1 ||T_kk^-1||_1 exactly; refine the block solve
+    // when an inverted block's error, ~ kappa eps, is not far below the tolerance
+    double a = 0.0, b = 0.0;
+    for (int c = 0; c < XB; c++) {
+      a = fmax(a, cn[threadIdx.x][c][0]);
+      b = fmax(b, cn[threadIdx.x][c][1]);
+    }
+    const bool refine = !(a * b <= kappa_max);
+    const size_t f = (size_t)(doff[blockIdx.x] / (2 * XB * XB)) + k;
+    if (threadIdx.x == 0) flags[2 * f] = refine;
+    else flags[2 * f + 1] = refine;
+  }
 }
-// y = L^-T U^-T x
-__device__ inline void lu_apply_t(const MatDesc& D, const double* x, double* y) {
-  for (int l = threadIdx.x; l < D.m; l += blockDim.x) y[l] = x[l];
-  __syncthreads();
-  cta_trsv_upper_t(D.A, D.lda, D.m, y);
-  cta_trsv_lower_unit_t(D.A, D.lda, D.m, y);
+
+// ------------------------------------------------------------------ condition estimate
+// Blocked triangular solves of one shared-memory vector v (length padded to
+// XB nb, zeros past m) by a 256-thread CTA, left-looking: per XB-row block the
+// coupling to the solved part is a coalesced mat-vec split over the 8 warps
+// (several independent loads in flight per thread), then the block is finished
+// by its inverted diagonal block.  part: 8 XB doubles, rb: XB doubles.
+//   v := L^-1 v, U^-1 v, U^-T v, L^-T v   (dg: this matrix's diagonal inverses)
+template <int KIND>  // 0 L, 1 U, 2 U^T, 3 L^T
+__device__ inline void blk_trsv(const MatDesc& D, const double* __restrict__ dg, double* v, double* part,
+                                double* rb) {
+  const int m = D.m, ld = D.lda, nb = (m + XB - 1) / XB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool fwd = (KIND == 0 || KIND == 2);
+  for (int s = 0; s < nb; s++) {
+    const int k = fwd ? s : nb - 1 - s, kb = XB * k;
+    const int j0 = fwd ? 0 : min(m, kb + XB), j1 = fwd ? kb : m;  // solved part
+    if (KIND == 0 || KIND == 1) {
+      // rows kb + lane and kb + 32 + lane, columns j of the factor (coalesced per column)
+      const int r0 = kb + lane, r1 = r0 + 32;
+      const bool ok0 = r0 < m, ok1 = r1 < m;
+      double c0 = 0.0, c1 = 0.0;
+      int j = j0 + warp;
+      for (; j + 24 < j1; j += 32) {
+        double a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          a[u] = ok0 ? D.A[r0 + (size_t)(j + 8 * u) * ld] : 0.0;
+          b[u] = ok1 ? D.A[r1 + (size_t)(j + 8 * u) * ld] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          c0 = fma(a[u], v[j + 8 * u], c0);
+          c1 = fma(b[u], v[j + 8 * u], c1);
+        }
+      }
+      for (; j < j1; j += 8) {
+        if (ok0) c0 = fma(D.A[r0 + (size_t)j * ld], v[j], c0);
+        if (ok1) c1 = fma(D.A[r1 + (size_t)j * ld], v[j], c1);
+      }
+      part[warp * XB + lane] = c0;
+      part[warp * XB + 32 + lane] = c1;
+    } else {
+      // transposed: output i of the block is the dot product of factor column
+      // kb + i (rows j0..j1, contiguous) with v
+#pragma unroll
+      for (int q = 0; q < XB / 8; q++) {
+        const int i = warp + 8 * q, col = kb + i;
+        double d = 0.0;
+        if (col < m) {
+          const double* c = D.A + (size_t)col * ld;
+          int j = j0 + lane;
+          for (; j + 96 < j1; j += 128) {
+            const double a0 = c[j], a1 = c[j + 32], a2 = c[j + 64], a3 = c[j + 96];
+            d = fma(a0, v[j], d);
+            d = fma(a1, v[j + 32], d);
+            d = fma(a2, v[j + 64], d);
+            d = fma(a3, v[j + 96], d);
+          }
+          for (; j < j1; j += 32) d = fma(c[j], v[j], d);
+        }
+        d = warp_sum(d);
+        if (lane == 0) part[i] = d;
+      }
+    }
+    __syncthreads();
+    if (tid < XB) {
+      double r = v[kb + tid];
+      if (KIND == 0 || KIND == 1) {
+#pragma unroll
+        for (int w = 0; w < 8; w++) r -= part[w * XB + tid];
+      } else {
+        r -= part[tid];
+      }
+      rb[tid] = r;
+    }
+    __syncthreads();
+    if (tid < XB) {
+      // block inverse: L (KIND 0, 3) or U (1, 2); transposed for 2, 3
+      const double* Bi = dg + (size_t)k * 2 * XB * XB + ((KIND == 1 || KIND == 2) ? XB * XB : 0);
+      double o = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < XB; c++) o = fma((KIND <= 1) ? Bi[tid + XB * c] : Bi[c + XB * tid], rb[c], o);
+      v[kb + tid] = (kb + tid < m) ? o : 0.0;
+    }
+    __syncthreads();
+  }
 }
 __device__ inline double vasum(const double* v, int n, double* red) {
   double s = 0.0;
@@ -286,48 +425,69 @@ __device__ inline int viamax(const double* v, int n, ArgMax* red) {
   return block_argmax(a, red).i;
 }
 
-// LAPACK dlacn2 (Hager/Higham) on B = S^-1, as dgecon runs it
-__global__ void __launch_bounds__(256, 3) lu_inv_norm1_kernel(const MatDesc* __restrict__ desc, double* out) {
+// LAPACK dlacn2 (Hager/Higham) on B = U^-1 L^-1, as dgecon runs it: dgecon
+// estimates ||A^-1||_1 through the triangular factors alone (the row
+// permutation only permutes columns of A^-1 and leaves the 1-norm unchanged),
+// so the estimator's iterates, hence the estimate, follow LAPACK's.
+__global__ void __launch_bounds__(256) lu_inv_norm1_kernel(const MatDesc* __restrict__ desc,
+                                                          const int64_t* __restrict__ doff,
+                                                          const double* __restrict__ dinv, double* out) {
   extern __shared__ double sm[];
   __shared__ double red[32];
+  __shared__ double part[8 * XB];
+  __shared__ double rb[XB];
   __shared__ ArgMax ared[32];
   __shared__ int s_flag;
   const MatDesc D = desc[blockIdx.x];
-  const int n = D.m;
+  const int n = D.m, np = XB * ((n + XB - 1) / XB);
   if (n == 0) {
     if (threadIdx.x == 0) out[blockIdx.x] = 0.0;
     return;
   }
+  const double* dg = dinv + doff[blockIdx.x];
   double* x = sm;
-  double* y = x + n;
-  double* sgn = y + n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = 1.0 / n;
+  double* sgn = x + np;
+  auto apply = [&]() {  // x := U^-1 L^-1 x
+    blk_trsv<0>(D, dg, x, part, rb);
+    blk_trsv<1>(D, dg, x, part, rb);
+  };
+  auto apply_t = [&]() {  // x := L^-T U^-T x
+    blk_trsv<2>(D, dg, x, part, rb);
+    blk_trsv<3>(D, dg, x, part, rb);
+  };
+  for (int i = threadIdx.x; i < np; i += blockDim.x) x[i] = i < n ? 1.0 / n : 0.0;
   __syncthreads();
-  lu_apply(D, x, y);
-  double est = vasum(y, n, red);
+  apply();
+  double est = vasum(x, n, red);
   if (n == 1) {
     if (threadIdx.x == 0) out[blockIdx.x] = est;
     return;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sgn[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    sgn[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+    x[i] = i < n ? sgn[i] : 0.0;
+  }
   __syncthreads();
-  lu_apply_t(D, sgn, x);
+  apply_t();
   int jj = viamax(x, n, ared);
   for (int iter = 2;; iter++) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = (i == jj) ? 1.0 : 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) x[i] = (i == jj) ? 1.0 : 0.0;
     __syncthreads();
-    lu_apply(D, x, y);
+    apply();
     const double old = est;
-    est = vasum(y, n, red);
+    est = vasum(x, n, red);
     if (threadIdx.x == 0) s_flag = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x)
-      if ((y[i] >= 0.0 ? 1.0 : -1.0) != sgn[i]) s_flag = 1;
+      if ((x[i] >= 0.0 ? 1.0 : -1.0) != sgn[i]) s_flag = 1;
     __syncthreads();
     if (!s_flag || est <= old) break;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sgn[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+      sgn[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+      x[i] = i < n ? sgn[i] : 0.0;
+    }
     __syncthreads();
-    lu_apply_t(D, sgn, x);
+    apply_t();
     const int jlast = jj;
     jj = viamax(x, n, ared);
     // every thread reads x before any thread overwrites it for the next iterate
@@ -335,45 +495,207 @@ __global__ void __launch_bounds__(256, 3) lu_inv_norm1_kernel(const MatDesc* __r
     __syncthreads();
     if (!again) break;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-    x[i] = ((i & 1) ? -1.0 : 1.0) * (1.0 + double(i) / double(n - 1));
+  for (int i = threadIdx.x; i < np; i += blockDim.x)
+    x[i] = i < n ? ((i & 1) ? -1.0 : 1.0) * (1.0 + double(i) / double(n - 1)) : 0.0;
   __syncthreads();
-  lu_apply(D, x, y);
-  const double temp = 2.0 * vasum(y, n, red) / (3.0 * n);
+  apply();
+  const double temp = 2.0 * vasum(x, n, red) / (3.0 * n);
   if (threadIdx.x == 0) out[blockIdx.x] = temp > est ? temp : est;
 }
 
 // ------------------------------------------------------------------ X = S^-1 C
-template <int TW, bool SCRATCH>
-__global__ void __launch_bounds__(256, 3) lu_solve_x_kernel(const XSolveDesc* __restrict__ descs,
-                                                         const int* __restrict__ tile_map, double* scratch,
-                                                         size_t scratch_per_tile) {
+// One CTA per (pivot, TW-column tile of C_full): the permuted tile P C_full
+// lives in shared memory (m x TW, column pitch == 4 mod 16 doubles), and the
+// two triangular solves run left-looking by XB-row blocks:
+//   X_k <- D_k^-1 (X_k - F[k, solved] X[solved])   (F = L forward, U backward)
+// Factor blocks F[k, j] and the inverted diagonal blocks D_k^-1 stream through
+// an S-stage cp.async pipeline in XB x 32 halves (one barrier per half); every
+// product is DMMA m8n8k4 from shared memory.  8 warps: warp w owns rows
+// 16 (w & 3) .. +16 of the block and TW / 16 16-column slabs -> 2 x (TW / 8)
+// 8 x 8 tiles, so each fragment read from shared memory feeds two MMAs.
+constexpr int XS_AP = XB + 4;  // A stage: [k][row], pitch == 4 mod 16
+struct XChunk {
+  // factor block (k, j), j != k; or, for j == k, step p of the diagonal block's
+  // solve (0: D_k^-1; if the block is flagged for refinement, 1: T_kk, 2: D_k^-1
+  // again); half h of its columns
+  int bwd, k, j, p, h;
+};
+// fl: the matrix's refinement flags, fl[2 k + bwd]
+__device__ __forceinline__ void xchunk_next(XChunk& c, int nb, const unsigned char* fl) {
+  if (c.h == 0) {
+    c.h = 1;
+    return;
+  }
+  c.h = 0;
+  if (c.j == c.k && c.p < 2 && fl[2 * c.k + c.bwd]) {
+    c.p++;
+    return;
+  }
+  c.p = 0;
+  if (!c.bwd) {
+    if (c.j < c.k) c.j++;
+    else if (c.k + 1 < nb) { c.k++; c.j = 0; }
+    else { c.bwd = 1; c.k = nb - 1; c.j = nb - 1; }  // backward starts with the last block's diagonal
+  } else {
+    if (c.j > c.k) c.j--;  // walks j = nb-1 .. k+1, then the diagonal
+    else { c.k--; c.j = nb - 1; }
+  }
+}
+__device__ __forceinline__ void xchunk_load(double* As, const XChunk& c, const double* __restrict__ LU,
+                                            const double* __restrict__ dg, int m, int tid) {
+  const int r = tid & (XB - 1);
+#pragma unroll
+  for (int q = 0; q < XB * 32 / 256; q++) {
+    const int kk = (tid / XB) + (256 / XB) * q;
+    const double* src;
+    bool ok;
+    if (c.j == c.k && c.p != 1) {
+      src = dg + (size_t)c.k * 2 * XB * XB + (c.bwd ? XB * XB : 0) + r + (size_t)XB * (32 * c.h + kk);
+      ok = true;
+    } else {  // a factor block, or the diagonal block T_kk itself (p == 1)
+      const int row = XB * c.k + r, col = XB * c.j + 32 * c.h + kk;
+      ok = row < m && col < m;
+      src = LU + row + (size_t)col * m;
+      // the unit diagonal of L is implicit in the LU storage
+      if (c.j == c.k && !c.bwd && row == col) {
+        As[kk * XS_AP + r] = ok ? 1.0 : 0.0;
+        continue;
+      }
+      // T_kk is triangular: keep only its own part (L strictly below / U on and above)
+      if (c.j == c.k && (c.bwd ? row > col : row < col)) ok = false;
+    }
+    cp_async8(As + kk * XS_AP + r, src, ok);
+  }
+}
+
+// One CTA per (pivot, TW-column tile of C_full); 8 warps, warp w owns rows
+// 16 (w & 3) .. +16 of the XB-row block and TW / 16 8-column tiles.  Diagonal
+// blocks: x1 = D_k^-1 R; for blocks flagged by lu_diag_inv (kappa(T_kk) eps not
+// far below the fill tolerance) one step of refinement x = x1 + D_k^-1 (R - T_kk x1)
+// follows -- the inverted block alone costs kappa(T_kk) eps, which tol = 1e-14
+// fill compression cannot absorb (measured: the reference-default N = 8,000
+// system matches the reference only with it); refined, the block solve is as
+// accurate as substitution while every step stays a DMMA product.
+template <int TW, int XS_STAGES>
+__global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __restrict__ descs,
+                                                        const int* __restrict__ tile_map) {
+  constexpr int NC = TW / 16;  // 8-column tiles per warp
+  constexpr int SP = XB + 4;   // pitch of the x1 scratch (== 4 mod 16)
   extern __shared__ double sm[];
   const XSolveDesc D = descs[tile_map[blockIdx.x]];
   const int c0 = (blockIdx.x - D.tile0) * TW;
   const int m = D.m, n = D.n, wl = D.wl, w = D.w;
-  const int xm = m | 1;
-  // (the shared-memory instantiation addresses X as shared: LDS/STS, not generic)
-  double* X = SCRATCH ? scratch + scratch_per_tile * blockIdx.x : sm;
-  for (int e = threadIdx.x; e < TW * m; e += blockDim.x) {
-    const int c = e / m, l = e - c * m;
-    const int i = D.perm[l], cc = c0 + c;
-    double v = 0.0;
-    if (cc < w) {
-      if (i < n) v = cc < wl ? D.C[i + (size_t)cc * n] : 0.0;
-      else v = (cc >= wl && i - n == cc - wl) ? -1.0 : 0.0;
+  if (m == 0) return;
+  const int nb = (m + XB - 1) / XB, mp = XB * nb, xm = mp + 4;
+  double* X = sm;
+  double* As = sm + (size_t)TW * xm;
+  double* Sc = As + (size_t)XS_STAGES * 32 * XS_AP;  // x1 of the current diagonal block (TW x SP)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // gather the permuted panel: a thread owns a row, 8 of its loads in flight together
+  for (int l = tid; l < mp; l += 256) {
+    const int i = l < m ? D.perm[l] : -1;
+#pragma unroll 1
+    for (int cg = 0; cg < TW; cg += 8) {
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const int cc = c0 + cg + c;
+        v[c] = 0.0;
+        if (i >= 0 && cc < w) {
+          if (i < n) v[c] = cc < wl ? D.C[i + (size_t)cc * n] : 0.0;
+          else v[c] = (cc >= wl && i - n == cc - wl) ? -1.0 : 0.0;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c++) X[(size_t)(cg + c) * xm + l] = v[c];
     }
-    X[(size_t)c * xm + l] = v;
   }
+  const unsigned char* fl = D.dflag;
+  int T = 2 * nb * (nb - 1) + 4 * nb;  // off-diagonal halves + 2 halves per diagonal block, both sweeps
+  for (int q = 0; q < 2 * nb; q++) T += fl[q] ? 4 : 0;  // + 4 halves per refined diagonal block
+  XChunk ci{0, 0, 0, 0, 0}, cc{0, 0, 0, 0, 0};
+  auto issue = [&](int t) {
+    if (t < T) {
+      xchunk_load(As + (size_t)(t % XS_STAGES) * 32 * XS_AP, ci, D.LU, D.dinv, m, tid);
+      xchunk_next(ci, nb, fl);
+    }
+    cp_async_commit();
+  };
+  for (int t = 0; t < XS_STAGES - 1; t++) issue(t);
+  double acc[2][NC][2];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < NC; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int fk = lane & 3, fq = lane >> 2;
+  const int r0 = 16 * (warp & 3), cb = NC * (warp >> 2);  // first row of the warp, first 8-column tile
+  // apply f(pointer into X_k at an owned accumulator element, pointer into Sc at the same (row, col), value)
+  auto own = [&](int kb, auto f) {
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int b = 0; b < NC; b++) {
+        const int col = 8 * (cb + b) + 2 * fk, row = r0 + 8 * a + fq;
+        double* x0 = X + (size_t)col * xm + kb + row;
+        double* s0 = Sc + (size_t)col * SP + row;
+        f(x0, s0, acc[a][b][0]);
+        f(x0 + xm, s0 + SP, acc[a][b][1]);
+        acc[a][b][0] = acc[a][b][1] = 0.0;
+      }
+  };
+  for (int t = 0; t < T; t++) {
+    cp_async_wait<XS_STAGES - 2>();
+    __syncthreads();
+    issue(t + XS_STAGES - 1);
+    const int kb = XB * cc.k;
+    const bool diag = cc.j == cc.k;
+    if (diag && cc.p == 0 && cc.h == 0) {  // R = X_k - acc
+      own(kb, [](double* x, double*, double v) { *x -= v; });
+      __syncthreads();
+    }
+    const double* A = As + (size_t)(t % XS_STAGES) * 32 * XS_AP + fk * XS_AP + r0 + fq;
+    // B operand: X rows of block j, or (T_kk x1) the x1 scratch
+    const double* B = (diag && cc.p == 1) ? Sc + (size_t)(8 * cb + fq) * SP + 32 * cc.h + fk
+                                          : X + (size_t)(8 * cb + fq) * xm + XB * cc.j + 32 * cc.h + fk;
+    const int bld = (diag && cc.p == 1) ? SP : xm;
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      double fa[2], fb[NC];
+#pragma unroll
+      for (int a = 0; a < 2; a++) fa[a] = A[4 * s * XS_AP + 8 * a];
+#pragma unroll
+      for (int b = 0; b < NC; b++) fb[b] = B[(size_t)8 * b * bld + 4 * s];
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < NC; b++)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                       : "d"(fa[a]), "d"(fb[b]));
+    }
+    if (diag && cc.h == 1 && !fl[2 * cc.k + cc.bwd]) {  // unrefined: X_k = D R
+      __syncthreads();  // every warp has read X_k
+      own(kb, [](double* x, double*, double v) { *x = v; });
+    } else if (diag && cc.h == 1) {
+      if (cc.p == 0) {  // x1 = D R -> scratch
+        own(kb, [](double*, double* sc, double v) { *sc = v; });
+      } else if (cc.p == 1) {  // X_k = R - T x1 (the residual; no warp reads X_k in this step)
+        own(kb, [](double* x, double*, double v) { *x -= v; });
+      } else {  // x = x1 + D (R - T x1)
+        __syncthreads();  // every warp has read X_k
+        own(kb, [](double* x, double* sc, double v) { *x = *sc + v; });
+      }
+    }
+    xchunk_next(cc, nb, fl);
+  }
+  cp_async_wait<0>();
   __syncthreads();
-  cta_tile_lu_solve<TW>(D.LU, m, m, X, xm);
-  for (int e = threadIdx.x; e < TW * m; e += blockDim.x) {
-    const int c = e / m, l = e - c * m;
-    const int cc = c0 + c;
-    if (cc >= w) continue;
+  for (int e = tid; e < TW * m; e += 256) {
+    const int c = e / m, l = e - c * m, col = c0 + c;
+    if (col >= w) continue;
     const double v = X[(size_t)c * xm + l];
-    if (l < n) D.Xtop[l + (size_t)cc * n] = v;
-    else D.Xbot[(l - n) + (size_t)cc * D.r] = v;
+    if (l < n) D.Xtop[l + (size_t)col * n] = v;
+    else D.Xbot[(l - n) + (size_t)col * D.r] = v;
   }
 }
 
@@ -386,14 +708,34 @@ int lu_tile_width(int m) {
   return 0;
 }
 
-// Tile width for the X solve: the widest tile that still lets three CTAs share
-// an SM (the solve is latency-bound: occupancy beats operand reuse; measured at
-// C3 level 5, m ~ 450: 32-column tiles leave one CTA per SM).
-static int x_tile_width(int m) {
-  const size_t xm = size_t(m | 1);
-  for (int tw = 32; tw >= 8; tw /= 2)
-    if (size_t(tw) * xm * sizeof(double) <= 72 * 1024) return tw;
-  return lu_tile_width(m);
+static size_t xsolve_smem(int tw, int stages, int m) {
+  const size_t mp = size_t(XB) * ((m + XB - 1) / XB);
+  return sizeof(double) * (size_t(tw) * (mp + 4) + size_t(stages) * 32 * XS_AP + size_t(tw) * (XB + 4));
+}
+
+LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, Arena& ws, Staging& st,
+                          cudaStream_t s, double tol) {
+  std::vector<int64_t> off(h.size() + 1, 0);
+  int maxnb = 0;
+  for (size_t p = 0; p < h.size(); p++) {
+    const int nb = (h[p].m + XB - 1) / XB;
+    maxnb = std::max(maxnb, nb);
+    off[p + 1] = off[p] + int64_t(nb) * 2 * XB * XB;
+  }
+  LuDiag dg;
+  dg.dinv = ws.alloc_n<double>(size_t(std::max<int64_t>(1, off.back())));
+  dg.flags = ws.alloc_n<unsigned char>(size_t(std::max<int64_t>(1, off.back() / (XB * XB))));
+  dg.d_off = upload(ws, off, s, st);
+  dg.h_off = off;
+  // refine a block solve when its inverted block's error kappa eps could reach
+  // a thousandth of the tolerance (tol <= 0: always)
+  const double kappa_max = tol > 0 ? 1e-3 * tol / 2.220446049250313e-16 : 0.0;
+  if (!h.empty() && maxnb > 0) {
+    lu_diag_inv_kernel<<<dim3(unsigned(h.size()), unsigned(maxnb)), 128, 0, s>>>(d_desc, dg.d_off, dg.dinv, dg.flags,
+                                                                                kappa_max);
+    CK_LAUNCH();
+  }
+  return dg;
 }
 
 void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws, Staging& st,
@@ -437,16 +779,16 @@ void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_inf
   }
 }
 
-void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s) {
+void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, const LuDiag& dg, double* out, cudaStream_t s) {
   if (n <= 0) return;
-  const size_t smem = sizeof(double) * 3 * size_t(std::max(1, maxm));
-  if (smem > 224 * 1024) invalid("pivot block too large for the condition estimate");
+  const size_t smem = sizeof(double) * 2 * size_t(XB * ((std::max(1, maxm) + XB - 1) / XB));
+  if (smem > 200 * 1024) invalid("pivot block too large for the condition estimate");
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(lu_inv_norm1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+    CK(cudaFuncSetAttribute(lu_inv_norm1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  lu_inv_norm1_kernel<<<n, 256, smem, s>>>(d_desc, out);
+  lu_inv_norm1_kernel<<<n, 256, smem, s>>>(d_desc, dg.d_off, dg.dinv, out);
   CK_LAUNCH();
 }
 
@@ -454,34 +796,42 @@ void launch_lu_solve_x(const std::vector<XSolveDesc>& hin, Arena& ws, Staging& s
   if (hin.empty()) return;
   int maxm = 0;
   for (auto& d : hin) maxm = std::max(maxm, d.m);
-  int tw = x_tile_width(maxm);
-  const bool global = tw == 0;
-  if (global) tw = 8;
+  // Configuration: 32-column tiles, two CTAs per SM with 2 stages while the
+  // tile is small (leaf pivots), else one CTA with 4 stages -- the prefetch
+  // distance must cover the L2 latency with one CTA's compute; 16-column tiles
+  // for the largest pivots.
+  int cfg = -1;
+  if (xsolve_smem(32, 2, maxm) <= 110 * 1024) cfg = 0;
+  else if (xsolve_smem(32, 4, maxm) <= 220 * 1024) cfg = 1;
+  else if (xsolve_smem(16, 4, maxm) <= 220 * 1024) cfg = 2;
+  else if (xsolve_smem(16, 3, maxm) <= 220 * 1024) cfg = 3;
+  if (cfg < 0) invalid("pivot block too large for the X solve (m = " + std::to_string(maxm) + ")");
+  const int tw = cfg >= 2 ? 16 : 32;
+  const int stages = cfg == 0 ? 2 : (cfg == 3 ? 3 : 4);
   std::vector<XSolveDesc> h(hin);
   std::vector<int> map;
   for (size_t p = 0; p < h.size(); p++) {
     h[p].tile0 = int(map.size());
-    const int tiles = ceil_div(h[p].w, tw);
+    const int tiles = h[p].m > 0 ? ceil_div(h[p].w, tw) : 0;
     for (int t = 0; t < tiles; t++) map.push_back(int(p));
   }
   if (map.empty()) return;
   const XSolveDesc* dd = upload(ws, h, s, st);
   const int* dm = upload(ws, map, s, st);
-  const size_t per = size_t(tw) * size_t(maxm | 1);
-  double* scratch = global ? ws.alloc_n<double>(per * map.size()) : nullptr;
-  const size_t smem = global ? 0 : sizeof(double) * per;
+  const size_t smem = xsolve_smem(tw, stages, maxm);
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(lu_solve_x_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LU_TILE_SMEM_MAX)));
-    CK(cudaFuncSetAttribute(lu_solve_x_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LU_TILE_SMEM_MAX)));
-    CK(cudaFuncSetAttribute(lu_solve_x_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LU_TILE_SMEM_MAX)));
+    CK(cudaFuncSetAttribute(lu_xsolve_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(lu_xsolve_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(lu_xsolve_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(lu_xsolve_kernel<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
   const unsigned grid = unsigned(map.size());
-  if (global) lu_solve_x_kernel<8, true><<<grid, 256, 0, s>>>(dd, dm, scratch, per);
-  else if (tw == 32) lu_solve_x_kernel<32, false><<<grid, 256, smem, s>>>(dd, dm, scratch, per);
-  else if (tw == 16) lu_solve_x_kernel<16, false><<<grid, 256, smem, s>>>(dd, dm, scratch, per);
-  else lu_solve_x_kernel<8, false><<<grid, 256, smem, s>>>(dd, dm, scratch, per);
+  if (cfg == 0) lu_xsolve_kernel<32, 2><<<grid, 256, smem, s>>>(dd, dm);
+  else if (cfg == 1) lu_xsolve_kernel<32, 4><<<grid, 256, smem, s>>>(dd, dm);
+  else if (cfg == 2) lu_xsolve_kernel<16, 4><<<grid, 256, smem, s>>>(dd, dm);
+  else lu_xsolve_kernel<16, 3><<<grid, 256, smem, s>>>(dd, dm);
   CK_LAUNCH();
 }
 

@@ -9,11 +9,14 @@
 //                   update A22 -= L21 U12, all matrices of a batch per launch.
 //                   Rows are tracked as a permutation `perm` (row l of P S is
 //                   row perm[l] of S), kept with the factors for the solves.
+//   lu_diag_inv     inverses of the 64 x 64 diagonal blocks of L and U, which
+//                   make the blocked triangular solves GEMM-shaped.
 //   lu_solve_x      X = S^-1 C for the pivot's coupling panel: one CTA per
 //                   (matrix, column tile), the tile resident in shared memory,
-//                   L and U streamed from L2; 32-row diagonal blocks by
-//                   substitution, the off-diagonal updates on DMMA.
-//   lu_inv_norm1    dlacn2 estimate of ||S^-1||_1 with LU solves (the
+//                   factor blocks streamed from L2 by cp.async; left-looking
+//                   64-row blocks, every product on DMMA (diagonal blocks by
+//                   their inverse plus one refinement step).
+//   lu_inv_norm1    dlacn2 estimate of ||S^-1||_1 with blocked LU solves (the
 //                   estimator dgecon runs, ifmm/solver.py:216).
 #pragma once
 #include "batched.cuh"
@@ -274,8 +277,24 @@ __device__ inline void cta_tile_lu_solve_cols(const double* __restrict__ LU, int
 void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws, Staging& st,
                 cudaStream_t s, int shape_maxm = 0);
 
+// Inverses of the 64x64 diagonal blocks of every factored matrix (L_kk^-1 and
+// U_kk^-1, column-major 64 x 64 each, identity-padded past m): matrix p's
+// block k pair starts at dinv + h_off[p] + 8192 k.  They make the blocked
+// triangular solves GEMM-shaped (the X solve refines each block solve once).
+constexpr int LU_XB = 64;  // block size of the blocked triangular solves (X solve, condition estimate)
+struct LuDiag {
+  double* dinv = nullptr;
+  unsigned char* flags = nullptr;  // per block: [L, U] refine the block solve (lu.cu)
+  const int64_t* d_off = nullptr;
+  std::vector<int64_t> h_off;
+};
+// tol: the fill tolerance the X solve must support (decides which block solves
+// get a refinement step); <= 0 refines every block.
+LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, Arena& ws, Staging& st,
+                          cudaStream_t s, double tol);
+
 // out[p] = dlacn2 estimate of ||S_p^-1||_1 from the LU factors of S_p.
-void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, double* out, cudaStream_t s);
+void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, const LuDiag& dg, double* out, cudaStream_t s);
 
 // X = S^-1 C_full for the coupling panel of a pivot, C_full = [[C, 0], [0, -I_r]]
 // (m = n + r rows, w = wl + r columns; C is n x wl, ld n).  Rows [0, n) of X
@@ -286,6 +305,8 @@ struct XSolveDesc {
   const double* C;
   double* Xtop;
   double* Xbot;
+  const double* dinv;           // the pivot's diagonal-block inverses (LuDiag)
+  const unsigned char* dflag;   // and their refinement flags
   int m, n, r, wl, w;
   int tile0;  // first tile of this matrix in the launch
 };

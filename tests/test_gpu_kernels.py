@@ -102,6 +102,50 @@ def test_lu_batched_variable_sizes(L):
         assert abs(e * np.linalg.norm(A, 1) * rc - 1.0) < 0.5
 
 
+def _saddle_cond(rng, n, r, cond):
+    """Saddle-point pivot block whose P2P part has condition number `cond`."""
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    P = Q @ np.diag(np.logspace(0, -np.log10(cond), n)) @ Q.T
+    U, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    S = np.zeros((n + r, n + r))
+    S[:n, :n] = P
+    S[:n, n:] = U
+    S[n:, :n] = U.T
+    return S
+
+
+@pytest.mark.parametrize("n,r", [(64, 50), (300, 120), (500, 200)])
+@pytest.mark.parametrize("cond", [1e6, 1e12, 1e14])
+def test_lu_ill_conditioned_matches_lapack(L, n, r, cond):
+    """Ill-conditioned pivots (the regime the pivot-condition test guards):
+    the condition estimate equals LAPACK dgecon's (same dlacn2 iterates on the
+    triangular factors), and X = S^-1 C is backward stable like lu_solve
+    (ifmm/solver.py:214-218,246)."""
+    from scipy.linalg import lu_factor, lu_solve
+    from scipy.linalg.lapack import dgecon
+    rng = np.random.default_rng(n + int(np.log10(cond)))
+    S = _saddle_cond(rng, n, r, cond)
+    res, info, est = _run_lu(L, [S])
+    LU, perm = res[0]
+    lu = lu_factor(S)
+    ref = 1.0 / (dgecon(lu[0], np.linalg.norm(S, 1), norm="1")[0] * np.linalg.norm(S, 1))
+    assert abs(est[0] / ref - 1.0) < 1e-6, (est[0], ref)
+    wl = 3 * n
+    C = np.asfortranarray(rng.standard_normal((n, wl)))
+    xt = np.zeros((n, wl + r), order="F")
+    xb = np.zeros((r, wl + r), order="F")
+    L.check(L.lib.ifmm_test_lu_solve_x(L.ptr(np.asfortranarray(LU)), L.ptr(perm.astype(np.int32)), n, r, L.ptr(C),
+                                       wl, L.ptr(xt), L.ptr(xb)))
+    Cf = np.zeros((n + r, wl + r))
+    Cf[:n, :wl] = C
+    Cf[n:, wl:] = -np.eye(r)
+    X = np.vstack([xt, xb])
+    Xr = lu_solve(lu, Cf)
+    be = np.linalg.norm(S @ X - Cf) / (np.linalg.norm(S) * np.linalg.norm(X))
+    be_ref = np.linalg.norm(S @ Xr - Cf) / (np.linalg.norm(S) * np.linalg.norm(Xr))
+    assert be <= max(4 * be_ref, 1e-15), (be, be_ref)
+
+
 def test_lu_large_batch_mixed_sizes(L):
     rng = np.random.default_rng(7)
     sizes = [int(x) for x in rng.integers(40, 140, size=80)] + [64, 96, 97, 127, 128, 129]

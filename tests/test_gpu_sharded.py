@@ -52,11 +52,13 @@ def test_sharded_matches_single_gpu(ifmm, case):
     from paper_1407_1572_b200 import distributed as D
     n, depth, kernel, p, tol, ranks = case
     tree, store, b = _system(ifmm, n, depth, kernel, p, tol)
-    f1 = ifmm.factorize(store, tree)
+    # bit-identity of the sharded schedule is the point here, not pivot conditioning
+    # (C3's parameters put some pivots near the reference's 1e12 limit): no limit
+    f1 = ifmm.factorize(store, tree, pivot_condition_limit=np.inf)
     x1 = ifmm.solve(f1, b)
     r1 = _rel(ifmm.fmm_matvec(store, tree, x1), b)
     for V in ranks:
-        fs = D.factorize_emulated(store, tree, V)
+        fs = D.factorize_emulated(store, tree, V, pivot_condition_limit=np.inf)
         assert [f.shard["rank"] for f in fs] == list(range(V))
         assert all(f.shard["nranks"] == V for f in fs)
         assert sum(f.n_records for f in fs) == f1.n_records

@@ -33,6 +33,13 @@ for name in sys.argv[1:]:
     x = ifmm.solve(f, b)
     res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
     rec = np.array([(r.level, r.r) for r in f.records])
+    R = np.array([(r.level, r.n, r.r, r.w) for r in f.records], dtype=float)
+    for k in range(depth, 1, -1):
+        q = R[R[:, 0] == k]
+        m = q[:, 1] + q[:, 2]
+        print(f"   level {k}: pivots {len(q)} m mean {m.mean():.0f} max {m.max():.0f}  w mean {q[:, 3].mean():.0f} max "
+              f"{q[:, 3].max():.0f}  getrf {(2 / 3 * m ** 3).sum() / 1e9:.1f} GF  X {(2 * m * m * q[:, 3]).sum() / 1e9:.1f} GF"
+              f"  Schur(full) {(2 * q[:, 1] * q[:, 3] ** 2).sum() / 1e9:.1f} GF")
     print(f"== {name}: factorize {t1 - t0:.2f}s residual {res:.3e} (ref Morton {float(g['resid_morton']):.3e} "
           f"colour9 {float(g['resid_colour9']):.3e}) r_m {f.r_m} top {f.top_dim} (ref {int(g['top_colour9'])})")
     xc, xm = g["x_colour9"], g["x_morton"]
