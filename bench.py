@@ -9,13 +9,18 @@ quadtree depth 7, Chebyshev p = 4, eps = 1e-6).  Synthetic seeded data.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
 
-Own arm: tree + operators are built once (t_a, reported), then W warm-up and
-K timed steps with inputs resident in HBM (value, ms_per_step); e2e repeats
-the step through the public API with host numpy buffers (H2D rhs, D2H x).
-Under torchrun (--gpus N > 1) the ranks factorize ONE system together: the
-subtree-sharded path (paper_1407_1572_b200.distributed) with NCCL
-halo exchanges after every colour batch -- strong scaling, timing is the max
-over ranks.
+Own arm: tree + operators are built once (assembly, reported with its HBM
+roofline), then W warm-up and K timed steps with inputs resident in HBM (value,
+ms_per_step); e2e repeats the step through the public API with host numpy
+buffers (H2D rhs, D2H x inside the timed region).  The pivot-condition test is
+the reference's (1e12, ifmm/solver.py:50); C3 lies past it for the reference
+itself (tests/golden/c3_1m.npz: 1 pivot over the limit in Morton order, 3 in
+colour order), so steps record such pivots (factorize(on_singular="record"))
+and the line reports them beside the reference's counts.
+--gpus N > 1 spawns N ranks (torch.distributed.run) unless already launched
+under torchrun; the ranks factorize ONE system together: the subtree-sharded
+path (paper_1407_1572_b200.distributed) with NCCL halo exchanges
+after every colour batch -- strong scaling, timing is the max over ranks.
 --impl reference times the reference algorithm (the CPU oracle restatement,
 Morton order, bit-exact with /root/reference) on a bounded sample on rank 0.
 """
@@ -23,6 +28,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -42,8 +48,11 @@ CONFIGS = {
     "C3_262k": (262144, "inv_r", 6, 4, 1e-6, 1),
 }
 METRIC = "IFMM factor+solve seconds at N=1M 2D"
-CPU_SAMPLE = (16384, 4)   # cpu_baseline sample: C3 parameters at N=16,384 (depth 4)
-REF_SAMPLE = (16384, 4)   # --impl reference per-step sample: C3 parameters at N=16,384 (depth 4), ~9 s
+PIVOT_LIMIT = 1e12  # ifmm/solver.py:50
+# bounded CPU sample of the reference algorithm: the config's parameters at a
+# smaller N (depth 4 = 256 leaves of 64 points), about 9 s of one core
+SAMPLE = {"C3": (16384, 4), "C3_65k": (16384, 4), "C3_262k": (16384, 4), "C2": (16384, 4), "C1": (4096, 3)}
+C3_FULL_RUN = os.path.join(ROOT, "profiles", "r02_c3_reference_cpu.json")
 
 
 def dist_env():
@@ -51,6 +60,16 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def spawn_ranks(n):
+    """Re-launch this command as n ranks (one process per GPU) over 127.0.0.1."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -140,11 +159,33 @@ def oracle_step_seconds(n, depth, p, tol, kernel, order="morton"):
         st = O.init_operators(T, spec, p, tol)
         b = O.baseline_rhs(n, "normal")
         t0 = time.perf_counter()
-        fac = O.factorize(st, tol, order=order)
+        fac = O.factorize(st, tol, order=order, on_singular="record")
         t1 = time.perf_counter()
         O.solve(fac, b)
         t2 = time.perf_counter()
     return t1 - t0, t2 - t1
+
+
+def c3_full_run():
+    """The reference algorithm run once at C3 itself on a GPU box's host (committed log)."""
+    try:
+        d = json.load(open(C3_FULL_RUN))
+    except Exception:
+        return None
+    m = d["morton"]
+    return {"seconds": m["t_f"] + m["t_s"], "t_factor_s": m["t_f"], "t_solve_s": m["t_s"],
+            "peak_rss_gb": m["peak_rss_gb"], "cores": m["cores_used"], "host_cpus": m["host_cpus"],
+            "pivots_over_1e12": m["singular_count"], "residual": m["resid"],
+            "source": os.path.relpath(C3_FULL_RUN, ROOT) + " (oracle/run_c3.py, Morton order, one core, "
+                                                         "measured once; too long for a bench step)"}
+
+
+def sample_desc(cfg_name, ns, ds):
+    N, kern, depth, p, tol, nrhs = CONFIGS[cfg_name]
+    return (f"reference algorithm (oracle/ifmm_oracle.py, Morton order, bit-exact with the reference) factor + "
+            f"solve of {cfg_name}'s parameters ({kern}, p={p}, eps={tol:g}) at N={ns}, depth {ds}; one core, one "
+            f"BLAS thread (the reference is a sequential elimination; multi-threaded BLAS is 4x slower on it, "
+            f"SURVEY finding 8); measured, not scaled")
 
 
 def run_reference(args, cfg):
@@ -152,28 +193,40 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     N, kern, depth, p, tol, nrhs = cfg
-    ns, ds = REF_SAMPLE
+    ns, ds = SAMPLE[args.config]
     vals = []
     for it in range(args.warmup + args.steps):
         tf, ts = oracle_step_seconds(ns, ds, p, tol, kern)
         if it >= args.warmup:
-            vals.append((tf + ts) * N / ns)
+            vals.append(tf + ts)
     v = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform points, N(0,1) rhs)",
-        "config": {"workload": args.config, "N": N, "kernel": kern, "depth": depth, "p": p, "eps": tol,
-                   "parallelism": "cpu"},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port",
-                         "sample": f"reference algorithm (oracle/ifmm_oracle.py, Morton order, bit-exact with the "
-                                   f"reference) factor+solve at N={ns} depth {ds} with {args.config} parameters, "
-                                   f"1 BLAS thread (multi-threaded BLAS is 4x slower, SURVEY finding 8), "
-                                   f"scaled x{N // ns} to N={N} (linear: a lower bound, per-point work grows "
-                                   f"with depth; BASELINE.md extrapolates the reference at N=1M to 40-60 min)"},
+        "config": {"workload": f"{args.config} bounded sample: N={ns}, depth {ds}", "N": ns, "kernel": kern,
+                   "depth": ds, "p": p, "eps": tol, "parallelism": "cpu, 1 core",
+                   "note": f"each step is the bounded CPU sample; the full {args.config} system is not run per step"},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": sample_desc(args.config, ns, ds)},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.config == "C3":
+        line["c3_full_run"] = c3_full_run()
     print(json.dumps(line), flush=True)
+
+
+def event_ms(fn, reps=3):
+    import torch
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
 
 
 def main():
@@ -184,9 +237,13 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cond-limit", type=float, default=None, help="pivot condition limit (default: see source)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -197,51 +254,39 @@ def main():
     import paper_1407_1572_b200 as ifmm
     from paper_1407_1572_b200 import _lib
 
-    ws, rank, local = dist_env()
     if ws > 1:
         torch.cuda.set_device(local)
-        _lib.lib.ifmm_set_device(local) if hasattr(_lib.lib, "ifmm_set_device") else None
+        _lib.check(_lib.lib.ifmm_set_device(local))
         dist.init_process_group("nccl")
     N, kern, depth, p, tol, nrhs = cfg
-    # The reference rejects pivots with 1-norm condition > 1e12 (ifmm/solver.py:50).
-    # At N=1M the 1/r kernel's monopole direction alone pushes level-5 pivots to
-    # ~2e12, so C3 runs with 1e15 and the
-    # residual is reported; smaller configs keep the reference limit.
-    cond_limit = args.cond_limit if args.cond_limit else (1e15 if N >= 1 << 20 else 1e12)
     rng_pts = np.random.default_rng(0)
     pts = 2.0 * rng_pts.random((N, 2)) - 1.0      # [0,1]^2 mapped to the reference box
     kernel = ifmm.baseline_kernel(kern, N)
     b_host = np.random.default_rng([0, 1]).standard_normal(N)
     b_dev = torch.from_numpy(b_host).cuda()
 
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    t1 = time.perf_counter()
     store = ifmm.init_operators(tree, kernel, p=p, tol=tol)
-    t_a = time.perf_counter() - t0
+    t2 = time.perf_counter()
+    t_tree, t_assembly = t1 - t0, t2 - t1
 
     comm = None
     if ws > 1:
         from paper_1407_1572_b200.distributed import Communicator
         comm = Communicator.from_torch()
 
-    def step(rhs):
-        fact = ifmm.factorize(store, tree, pivot_condition_limit=cond_limit, comm=comm)
-        x = ifmm.solve(fact, rhs)
-        return fact, x
+    def factor(timing=False):
+        return ifmm.factorize(store, tree, pivot_condition_limit=PIVOT_LIMIT, on_singular="record", comm=comm,
+                              timing=timing)
 
-    # The pivot-conditioning test is the reference's (SingularPivotError); at
-    # N = 1M the BASELINE 1/r system sits near it (DESIGN.md "pivot
-    # conditioning") and rank-decision noise can push one pivot past even the
-    # raised limit.  The bench must still produce its number: on such a
-    # failure the check is disabled for this run and the JSON says so.
-    cond_note = None
-    try:
-        fact, x = step(b_dev)
-        del fact
-    except ifmm.SingularPivotError as e:
-        cond_note = f"SingularPivotError at limit {cond_limit:.0e} ({e}); check disabled for this run"
-        cond_limit = float("inf")
-    for _ in range(max(0, args.warmup - 1)):
+    def step(rhs):
+        fact = factor()
+        return fact, ifmm.solve(fact, rhs)
+
+    for _ in range(max(1, args.warmup)):
         fact, x = step(b_dev)
         del fact
     if ws > 1:
@@ -250,7 +295,7 @@ def main():
     l0 = _lib.lib.ifmm_launch_count()
     times = []
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+        for it in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
@@ -258,45 +303,39 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
-            if _ != args.steps - 1:
+            if it != args.steps - 1:
                 del fact
     launches = (_lib.lib.ifmm_launch_count() - l0) // max(1, args.steps)
     if ws > 1:
         dist.barrier()
     t_step = float(np.mean(times))
-    t_max = torch.tensor([t_step], device="cuda")
     if ws > 1:
+        t_max = torch.tensor([t_step], device="cuda")
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    t_step = float(t_max.item())
+        t_step = float(t_max.item())
 
     # accuracy of the last step: residual against the compressed operator
-    xd = x.double()
-    r = ifmm.fmm_matvec(store, tree, xd) - b_dev
+    r = ifmm.fmm_matvec(store, tree, x.double()) - b_dev
     resid = float(torch.linalg.norm(r) / torch.linalg.norm(b_dev))
+    singular = list(fact.singular_pivots)
+    max_cond = {int(k): v for k, v in fact.max_cond.items()}
 
     # extension: iterative refinement with the FMM operator to the north_star
     # accuracy (10 eps relative residual); timed separately from the metric
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    ifmm.solve(fact, b_dev, refine=8, target=10 * tol)
-    torch.cuda.synchronize()
-    refine_s = time.perf_counter() - t1
+    refine_ms = event_ms(lambda: ifmm.solve(fact, b_dev, refine=4, target=10 * tol), reps=1)
     refine_hist = list(fact.last_refinement)
-    r_m, top_dim = fact.r_m, fact.top_dim
-    shard = fact.shard
+    r_m, top_dim, shard = fact.r_m, fact.top_dim, fact.shard
     # free the last factorization first so later ones reuse its device slabs
-    # (as every timed step does); the e2e timing would otherwise include fresh
-    # multi-GB allocations
     del fact
 
-    # e2e through the public API with host buffers
+    # e2e through the public API with host buffers (H2D of b, D2H of x inside)
     e2e_times = []
     for _ in range(max(1, min(args.steps, 2))):
         torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        f2 = ifmm.factorize(store, tree, pivot_condition_limit=cond_limit, comm=comm)
-        xh = ifmm.solve(f2, b_host)
-        e2e_times.append(time.perf_counter() - t1)
+        ta = time.perf_counter()
+        f2 = factor()
+        ifmm.solve(f2, b_host)
+        e2e_times.append(time.perf_counter() - ta)
         del f2
     e2e = float(np.mean(e2e_times))
     if ws > 1:
@@ -304,56 +343,64 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = float(te.item())
 
-    # instrumented factorization: per-phase device time for the roofline
-    ft = ifmm.factorize(store, tree, timing=True, pivot_condition_limit=cond_limit, comm=comm)
+    # instrumented factorization: per-phase device time (CUDA events on the library stream)
+    ft = factor(timing=True)
     ph = ft.phase_times
     work = ft.work
-    shard_t = ft.shard
     work_all = dict(work)
     if ws > 1:  # per-rank work -> whole job
-        wt = torch.tensor([work["flops_exec"], work["flops_schur"], work["flops_ref"], work["solve_bytes"]],
-                          dtype=torch.float64, device="cuda")
+        keys = ("flops_exec", "flops_schur", "flops_ref", "solve_bytes", "flops_lu", "flops_x")
+        wt = torch.tensor([work[k] for k in keys], dtype=torch.float64, device="cuda")
         dist.all_reduce(wt)
-        work_all = dict(zip(("flops_exec", "flops_schur", "flops_ref", "solve_bytes"), wt.tolist()))
+        work_all = dict(zip(keys, wt.tolist()))
     fl_peak = measured_fp64_peak()
-    schur_ms, schur_launches = ph["schur_gemm"]
-    achieved = work["flops_schur"] / (schur_ms * 1e-3) / 1e12 if schur_ms > 0 else None
-    fac_ms_dev = sum(v[0] for v in ph.values())
-    # DRAM traffic of one Schur launch from the committed ncu --set full capture
-    traffic = {}
-    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_schur_l5_ncu.json")
-    if os.path.exists(tp):
-        with open(tp) as fh:
-            traffic = json.load(fh)
-        traffic["source"] = os.path.relpath(tp, os.path.dirname(os.path.abspath(__file__)))
-    # solve: HBM roofline
     hb, hb_src = hbm_peak()
-    ts = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        ifmm.solve(ft, b_dev)
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    solve_ms = float(np.median(ts))
-    # extension: 32 right-hand sides through the DMMA sweeps
+    fac_ms_dev = sum(v[0] for v in ph.values())
+
+    def tensor_phase(name, flops):
+        ms, nl = ph[name]
+        a = flops / (ms * 1e-3) / 1e12 if ms > 0 else None
+        return {"ms": round(ms, 3), "launches": nl, "flops": flops, "achieved": a, "peak": fl_peak,
+                "unit": "TFLOP/s", "frac": a / fl_peak if a else None, "bound": "tensor"}
+
+    phases = {
+        "lu": tensor_phase("lu", work["flops_lu"]),
+        "x_solve": tensor_phase("x_solve", work["flops_x"]),
+        "schur": tensor_phase("schur", work["flops_schur"]),
+        "compress": {"ms": round(ph["compress"][0], 3), "launches": ph["compress"][1], "bound": "latency",
+                     "note": "ACA + recompression + basis augmentation of small fills: no flop/byte roofline"},
+        "gather": {"ms": round(ph["gather"][0], 3), "launches": ph["gather"][1], "bound": "hbm"},
+        "transition": {"ms": round(ph["transition"][0], 3), "launches": ph["transition"][1], "bound": "hbm"},
+        "top": tensor_phase("top", 0.0) | {"note": "level-2 LU, counted in lu flops"},
+    }
+    # dominant kernel for the roofline line: the phase with the most device time among the tensor phases
+    dom = max(("lu", "x_solve", "schur"), key=lambda k: phases[k]["ms"])
+    dom_kernel = {"lu": "lu_panel/lu_swap_trsm/lu_update (batched getrf)",
+                  "x_solve": "lu_xsolve_kernel (X = S^-1 C, blocked triangular solves on DMMA)",
+                  "schur": "schur_concat_kernel (Schur update T = C^T X, DMMA)"}[dom]
+
+    # solve: HBM roofline (the records are streamed once per sweep)
+    solve_ms = event_ms(lambda: ifmm.solve(ft, b_dev))
     b32 = torch.from_numpy(np.random.default_rng([0, 2]).standard_normal((N, 32))).cuda()
     ifmm.solve(ft, b32)
-    t32 = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        ifmm.solve(ft, b32)
-        e1.record()
-        torch.cuda.synchronize()
-        t32.append(e0.elapsed_time(e1))
-    solve32_ms = float(np.median(t32))
-    # 2 flops per record element and rhs in each sweep: solve_bytes / 8 elements per rhs
+    solve32_ms = event_ms(lambda: ifmm.solve(ft, b32))
     solve32_flops = 2.0 * work["solve_bytes"] / 8.0 * 32
+    # matvec: HBM roofline (every stored operator block read once)
+    nb = store.nbytes
+    mv_bytes = nb["p2p"] + nb["m2l"] + 2 * nb["basis"]
+    mv_ms = event_ms(lambda: ifmm.fmm_matvec(store, tree, b_dev))
+    asm_bytes = nb["p2p"] + nb["m2l"] + nb["basis"]
 
+    def hbm(bytes_, ms):
+        a = bytes_ / (ms * 1e-3) / 1e9
+        return {"ms": round(ms, 3), "bytes": bytes_, "achieved": a, "peak": hb, "unit": "GB/s", "frac": a / hb,
+                "peak_source": hb_src}
+
+    ref_c3 = None
+    if args.config == "C3":
+        g = np.load(os.path.join(ROOT, "tests", "golden", "c3_1m.npz"))
+        ref_c3 = {"morton": int(len(g["singular_morton"])), "colour9": int(len(g["singular_colour9"])),
+                  "resid_morton": float(g["resid_morton"]), "resid_colour9": float(g["resid_colour9"])}
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
@@ -363,38 +410,40 @@ def main():
                    "diag": "sqrt(N)", "depth": depth, "p": p, "eps": tol, "nrhs": nrhs,
                    "parallelism": f"subtree{ws} (level-2 subtrees per rank, NCCL halo exchange per colour batch)"
                    if ws > 1 else "single",
-                   "pivot_condition_limit": cond_limit if math.isfinite(cond_limit) else "disabled",
-                   "pivot_condition_note": cond_note,
+                   "pivot_condition_limit": PIVOT_LIMIT, "on_singular": "record",
                    "l2": "factor state (GBs) >> 126 MB L2; no flush needed"},
         "relative_residual": resid,
+        "pivots_over_limit": {"count": len(singular), "first": singular[:4], "max_cond_by_level": max_cond,
+                              "reference_counts_at_C3": ref_c3,
+                              "note": "the reference raises SingularPivotError at the first such pivot; at C3 it "
+                                      "meets them itself, so both sides record and continue"},
         "refined_solve": {"target": 10 * tol, "steps": len(refine_hist) - 1, "residual_history": refine_hist,
-                          "seconds": refine_s,
+                          "ms": refine_ms,
                           "note": "extension: x += solve(b - A~x) with the store's FMM operator; not in value"},
-        "r_m": r_m, "top_dim": top_dim, "t_assembly_s": t_a,
-        "flops": {"exec": work_all["flops_exec"], "schur": work_all["flops_schur"],
-                  "reference_equiv": work_all["flops_ref"],
+        "r_m": r_m, "top_dim": top_dim,
+        "assembly": {"tree_s": t_tree, "operators_s": t_assembly,
+                     "roofline": hbm(asm_bytes, t_assembly * 1e3) | {"bytes_note": "operator blocks written "
+                                                                                   "once (P2P, M2L, bases); wall "
+                                                                                   "clock incl. host planning"}},
+        "flops": {"exec": work_all["flops_exec"], "schur": work_all["flops_schur"], "lu": work_all["flops_lu"],
+                  "x_solve": work_all["flops_x"], "reference_equiv": work_all["flops_ref"],
                   "fp64_tflops_step": work_all["flops_exec"] / t_step / 1e12,
+                  "step_frac_of_peak": work_all["flops_exec"] / t_step / 1e12 / fl_peak,
                   "scope": "whole job (summed over ranks)" if ws > 1 else "one GPU"},
         "shard": {"rank0_halo_bytes_per_factorization": shard["halo_bytes"],
                   "rank0_meta_bytes": shard["meta_bytes"], "exchanges": shard["exchanges"],
-                  "rank0_comm_ms": shard_t["comm_ms"]} if ws > 1 else None,
-        "phase_ms": {k: round(v[0], 3) for k, v in ph.items()},
+                  "rank0_comm_ms": ft.shard["comm_ms"]} if ws > 1 else None,
+        "phases": phases,
         "phase_ms_by_level": ft.phase_times_by_level,
-        "roofline": {"kernel": "schur_concat_kernel (Schur update T = C^T S^-1 C, DMMA m8n8k4)", "bound": "tensor",
-                     "achieved": achieved, "peak": fl_peak, "unit": "TFLOP/s",
-                     "frac": (achieved / fl_peak) if achieved else None,
-                     "traffic": traffic.get("dram_bytes_per_launch"),
-                     "traffic_launch": traffic.get("kernel"),
-                     "traffic_algorithmic_bytes": traffic.get("algorithmic_bytes_per_launch"),
-                     "traffic_source": traffic.get("source"),
-                     "launches": schur_launches,
-                     "share_of_factor": schur_ms / fac_ms_dev if fac_ms_dev else None,
-                     "achieved_source": "executed upper-triangle flops / CUDA-event time of the Schur launches "
-                                        "on the library stream",
+        "roofline": {"kernel": dom_kernel, "bound": "tensor", "achieved": phases[dom]["achieved"], "peak": fl_peak,
+                     "unit": "TFLOP/s", "frac": phases[dom]["frac"], "traffic": None,
+                     "launches": phases[dom]["launches"],
+                     "share_of_factor": phases[dom]["ms"] / fac_ms_dev if fac_ms_dev else None,
+                     "achieved_source": "algorithmic flops of the phase / CUDA-event time of its launches on the "
+                                        "library stream (instrumented factorization)",
                      "peak_source": "measured live: cuBLAS DGEMM 8192^3 (torch.matmul float64)"},
-        "solve_roofline": {"bound": "hbm", "ms": solve_ms, "bytes": work["solve_bytes"],
-                           "achieved": work["solve_bytes"] / (solve_ms * 1e-3) / 1e9, "peak": hb, "unit": "GB/s",
-                           "frac": work["solve_bytes"] / (solve_ms * 1e-3) / 1e9 / hb, "peak_source": hb_src},
+        "solve_roofline": hbm(work["solve_bytes"], solve_ms) | {"bound": "hbm"},
+        "matvec_roofline": hbm(mv_bytes, mv_ms) | {"bound": "hbm", "bytes_note": "P2P + M2L + 2 x bases"},
         "solve_32rhs": {"ms": solve32_ms, "tflops": solve32_flops / (solve32_ms * 1e-3) / 1e12,
                         "frac_of_fp64_peak": solve32_flops / (solve32_ms * 1e-3) / 1e12 / fl_peak,
                         "vs_32_single_solves": 32 * solve_ms / solve32_ms,
@@ -405,13 +454,12 @@ def main():
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        ns, ds = CPU_SAMPLE
+        ns, ds = SAMPLE[args.config]
         tf, tsv = oracle_step_seconds(ns, ds, p, tol, kern)
-        line["cpu_baseline"] = {
-            "value": (tf + tsv) * N / ns, "unit": "s", "cores": 1, "kind": "port",
-            "sample": f"reference algorithm (oracle port, Morton order) factor {tf:.2f}s + solve {tsv:.3f}s at "
-                      f"N={ns} depth {ds} with {args.config} parameters on 1 core, scaled x{N // ns} (linear, "
-                      f"lower bound)"}
+        line["cpu_baseline"] = {"value": tf + tsv, "unit": "s", "cores": 1, "kind": "port",
+                                "sample": sample_desc(args.config, ns, ds) + f": factor {tf:.2f} s + solve {tsv:.3f} s"}
+        if args.config == "C3":
+            line["cpu_baseline"]["c3_full_run"] = c3_full_run()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -95,6 +95,21 @@ int ifmm_store_m2l(const ifmm_store* s, int level, int i, int j, double* out);
 /* leaf near-field block P2P(i, j) (n_i x n_j, column-major) of neighbour pair
  * (i, j) (OperatorStore.p2p, ifmm/operators.py:180-194; stored once per pair) */
 int ifmm_store_p2p(const ifmm_store* s, int i, int j, double* out);
+/* bytes of the assembled operators as stored: out3[0] leaf near field P2P
+ * (each neighbour pair once), out3[1] M2L blocks (both orientations of every
+ * interaction-list pair), out3[2] bases U (levels >= 2) -- the algorithmic
+ * traffic of assembly (written once) and of fmm_matvec (read once) */
+int ifmm_store_bytes(const ifmm_store* s, double* out3);
+/* extended sparse system of the initial store (verification / export path,
+ * ifmm/operators.py:338-364 extended_layout, :367-445 assemble_extended_dense).
+ * Slot table: *count slots of (sym 0 x / 1 y / 2 z, level, index, dim) in the
+ * reference's order; call with null arrays for the count. */
+int ifmm_extended_layout(const ifmm_store* s, int64_t* count, int32_t* sym, int32_t* level, int32_t* index,
+                         int32_t* dim);
+/* the dense extended matrix (dim x dim, COLUMN-major) scattered on the device
+ * into host `out`; out = null returns only *dim.  IFMM_INVALID if dim > cap
+ * ("extended dimension m exceeds cap c", as the reference's ValueError). */
+int ifmm_extended_dense(ifmm_store* s, int64_t cap, int64_t* dim, double* out);
 /* fmm_matvec (ifmm/operators.py:282-330): y = A~ x, x/y (n, nrhs) */
 int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr_kind);
 void ifmm_store_free(ifmm_store* s);
@@ -116,15 +131,16 @@ int ifmm_factor_singular(const ifmm_factor* f, int64_t cap, int32_t* level, int3
                          int64_t* count);
 /* per elimination (in order): level, index, n, r, w */
 int ifmm_factor_records(const ifmm_factor* f, int32_t* out5);
-/* work accounting: out[0] executed FP64 flops (GJ inverses, X = S^-1 C,
- * symmetric Schur update, top inverse), out[1] of which in the Schur update,
- * out[2] reference-equivalent flops (sum 2/3 m^3 + 2 m^2 w + 2 h n w
- * + 2/3 M_top^3), out[3] bytes one solve sweep streams per right-hand side */
-int ifmm_factor_work(const ifmm_factor* f, double* out4);
+/* work accounting: out[0] executed FP64 flops (pivot LU, X = S^-1 C, symmetric
+ * Schur update, top LU), out[1] of which in the Schur update, out[2]
+ * reference-equivalent flops (sum 2/3 m^3 + 2 m^2 w + 2 h n w
+ * + 2/3 M_top^3), out[3] bytes one solve sweep streams per right-hand side,
+ * out[4] pivot LU flops (sum 2/3 m^3), out[5] X = S^-1 C flops (sum 2 m^2 w) */
+int ifmm_factor_work(const ifmm_factor* f, double* out6);
 /* per-phase device time in ms and kernel launches, recorded with CUDA events
  * on the factorization stream when ifmm_factorize ran with IFMM_FLAG_TIMING:
- * 0 gathers/copies, 1 Gauss-Jordan inverses, 2 X = S^-1 C, 3 Schur update,
- * 4 fill-in compression, 5 level transitions, 6 top-level inverse */
+ * 0 gathers/copies, 1 pivot LU (+ norms), 2 X = S^-1 C, 3 Schur update,
+ * 4 fill-in compression, 5 level transitions, 6 top-level LU */
 int ifmm_factor_timing(const ifmm_factor* f, double* ms7, int64_t* launches7);
 /* the same per level (level 1 = top-level inverse); ms9[7] = host time spent
  * preparing the level's batches before their final sync, ms9[8] = time the

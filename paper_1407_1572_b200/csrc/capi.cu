@@ -221,6 +221,55 @@ int ifmm_store_p2p(const ifmm_store* s, int i, int j, double* out) {
   });
 }
 
+int ifmm_store_bytes(const ifmm_store* s, double* out3) {
+  return guard([&] {
+    const StoreH* S = s->h;
+    const int K = S->tree->depth;
+    double p2p = 0, m2l = 0, bas = 0;
+    {
+      const Topo& T = S->tree->lv[K];
+      const InitLevel& L = S->lv[K];
+      for (int i = 0; i < T.nc; i++)
+        for (int q = T.nbr_off[i]; q < T.nbr_off[i + 1]; q++)
+          if (T.nbr[q] >= i) p2p += 8.0 * L.n[i] * L.n[T.nbr[q]];
+    }
+    for (int k = 2; k <= K; k++) {
+      const Topo& T = S->tree->lv[k];
+      const InitLevel& L = S->lv[k];
+      for (int i = 0; i < T.nc; i++) {
+        bas += 8.0 * L.n[i] * L.r0[i];
+        for (int q = T.il_off[i]; q < T.il_off[i + 1]; q++) m2l += 8.0 * L.r0[i] * L.r0[T.il[q]];
+      }
+    }
+    out3[0] = p2p;
+    out3[1] = m2l;
+    out3[2] = bas;
+  });
+}
+
+int ifmm_extended_layout(const ifmm_store* s, int64_t* count, int32_t* sym, int32_t* level, int32_t* index,
+                         int32_t* dim) {
+  return guard([&] {
+    const std::vector<ifmm::ExtSlot> v = ifmm::extended_layout(s->h);
+    if (count) *count = int64_t(v.size());
+    if (!sym) return;
+    for (size_t q = 0; q < v.size(); q++) {
+      sym[q] = v[q].sym;
+      level[q] = v[q].level;
+      index[q] = v[q].index;
+      dim[q] = v[q].dim;
+    }
+  });
+}
+
+int ifmm_extended_dense(ifmm_store* s, int64_t cap, int64_t* dim, double* out) {
+  return guard([&] {
+    ensure_device();
+    const int64_t m = ifmm::extended_dense(s->h, cap, out);
+    if (dim) *dim = m;
+  });
+}
+
 int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr_kind) {
   return guard([&] { ifmm::matvec(s->h, x, y, nrhs, ptr_kind == IFMM_PTR_DEVICE); });
 }
@@ -294,12 +343,14 @@ int ifmm_factor_records(const ifmm_factor* f, int32_t* out5) {
   });
 }
 
-int ifmm_factor_work(const ifmm_factor* f, double* out4) {
+int ifmm_factor_work(const ifmm_factor* f, double* out6) {
   return guard([&] {
-    out4[0] = f->h->fl_exec;
-    out4[1] = f->h->fl_schur;
-    out4[2] = f->h->fl_ref;
-    out4[3] = f->h->solve_bytes;
+    out6[0] = f->h->fl_exec;
+    out6[1] = f->h->fl_schur;
+    out6[2] = f->h->fl_ref;
+    out6[3] = f->h->solve_bytes;
+    out6[4] = f->h->fl_lu;
+    out6[5] = f->h->fl_x;
   });
 }
 

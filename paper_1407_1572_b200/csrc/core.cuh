@@ -209,7 +209,7 @@ struct FactorH {
   cudaStream_t stream = nullptr;
   // timing of the last factorization (ms) and work accounting
   double ms_total = 0;
-  double fl_exec = 0, fl_schur = 0, fl_ref = 0, solve_bytes = 0;
+  double fl_exec = 0, fl_schur = 0, fl_ref = 0, solve_bytes = 0, fl_lu = 0, fl_x = 0;
   // per-phase device time (ms, CUDA events on the factorization stream) when
   // factorize() ran with IFMM_FLAG_TIMING: see PhaseId
   double phase_ms[8] = {0};
@@ -246,10 +246,19 @@ constexpr int IFMM_FLAG_TIMING = 1;
 // of raising SingularPivotError at the first one (the reference raises).
 constexpr int IFMM_FLAG_RECORD_SINGULAR = 2;
 
+// One unknown slot of the extended system (extended.cu): kind 0 x, 1 y, 2 z
+struct ExtSlot {
+  int sym, level, index, dim;
+};
+
 // ------------------------------------------------------------ entry points
 TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_ptr);
 StoreH* store_init(TreeH* t, const KernelParams& kp, int p, double tol, const int* probe_tab, int probe_maxm);
 void matvec(StoreH* s, const double* x, double* y, int64_t nrhs, bool device_ptr);
+// extended system of the initial store (extended.cu): slot table, and the dense
+// matrix (m x m, column-major, into host_out; null: size only) -> m
+std::vector<ExtSlot> extended_layout(const StoreH* s);
+int64_t extended_dense(StoreH* s, int64_t cap, double* host_out);
 FactorH* factorize(StoreH* s, double tol, int flags, double cond_limit);
 // collective over `comm` (one call per rank, same store contents on every rank)
 FactorH* factorize_sharded(StoreH* s, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit);

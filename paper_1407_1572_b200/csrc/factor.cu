@@ -611,15 +611,19 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     for (size_t u = 0; u < I.xp.size(); u++)
       for (size_t v = u + 1; v < I.xp.size(); v++)
         if (T.in_il(I.xp[u], I.xp[v])) note(FILL_P2P, I.xp[u], I.xp[v]);
-    if (!I.own) continue;
     if (dist) {
-      bool ok = holds1(W, i);
-      for (int j : I.xp) ok &= holds1(W, j);
-      for (int j : I.yp) ok &= holds1(W, j);
+      // checked for every pivot on every rank (each rank holds every pivot's
+      // partner lists), so all ranks throw together instead of the owner alone
+      // leaving its peers blocked in the next exchange
+      const int o = owner(W, i);
+      bool ok = holds(W, o, i);
+      for (int j : I.xp) ok &= holds(W, o, j);
+      for (int j : I.yp) ok &= holds(W, o, j);
       if (!ok)
         invalid("sharded factorization: a pivot couples to a cluster more than one cell away (a dense "
                 "well-separated fill); factorize this system on one GPU");
     }
+    if (!I.own) continue;
     own.push_back(t);
   }
   fill_off[np] = int(fh.size());
@@ -730,6 +734,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       {
         const double m = I.m, n = I.n, w = I.w, h = I.w - I.r;
         F_->fl_exec += 2.0 / 3.0 * m * m * m + 2.0 * m * m * w;
+        F_->fl_lu += 2.0 / 3.0 * m * m * m;
+        F_->fl_x += 2.0 * m * m * w;
         F_->fl_ref += 2.0 / 3.0 * m * m * m + 2.0 * m * m * w + 2.0 * h * n * w;
         F_->solve_bytes += 8.0 * (2.0 * m * m + 2.0 * n * h);
       }

@@ -95,6 +95,14 @@ class OperatorStore:
     def part_dim(self, k: int, i: int) -> int:
         return int(self._level_dims(k)[0][i])
 
+    @property
+    def nbytes(self) -> dict:
+        """Bytes of the assembled operators as stored (leaf P2P once per pair,
+        M2L both orientations, bases): assembly writes them, matvec reads them."""
+        out = np.zeros(3)
+        _lib.check(_lib.lib.ifmm_store_bytes(self._h, _lib.ptr(out)))
+        return {"p2p": out[0], "m2l": out[1], "basis": out[2]}
+
     def ranks(self, k: int) -> np.ndarray:
         return self._level_dims(k)[1].copy()
 
@@ -136,127 +144,76 @@ def fmm_matvec(store: OperatorStore, tree: ClusterTree, charges):
 
 
 # ----------------------------------------------------------------------
-# extended sparse system: verification / export path (ifmm/operators.py:333-486)
+# extended sparse system: verification / export path (ifmm/operators.py:333-486).
+# The slot table and the matrix come from the library (csrc/extended.cu: a
+# device scatter of the store's blocks); rhs / solution maps are index arrays.
 # ----------------------------------------------------------------------
+
+_SYMS = "xyz"
+
+
+def _slot_table(store: OperatorStore):
+    cnt = ctypes.c_int64()
+    _lib.check(_lib.lib.ifmm_extended_layout(store.handle, ctypes.byref(cnt), None, None, None, None))
+    cols = [np.zeros(cnt.value, dtype=np.int32) for _ in range(4)]
+    _lib.check(_lib.lib.ifmm_extended_layout(store.handle, ctypes.byref(cnt), *[_lib.ptr(c) for c in cols]))
+    return cols
 
 
 def extended_layout(store: OperatorStore, tree: ClusterTree) -> list:
-    """Slot order of the extended system's unknowns (ifmm/operators.py:338-364):
-    leaf (x_i, z_i) pairs in Morton order, then per coarser level each
-    cluster's children's y slots followed by its own z slot (none at level 1)."""
-    kappa = tree.depth
-    nch = 1 << tree.dim
-    slots = []
-    off = tree.leaf_offsets
-    for i in range(1 << (tree.dim * kappa)):
-        slots.append(("x", kappa, i, int(off[i + 1] - off[i])))
-        slots.append(("z", kappa, i, store.rank(kappa, i)))
-    for k in range(kappa - 1, 0, -1):
-        for i in range(1 << (tree.dim * k)):
-            for ch in range(nch * i, nch * (i + 1)):
-                slots.append(("y", k + 1, ch, store.rank(k + 1, ch)))
-            if k >= 2:
-                slots.append(("z", k, i, store.rank(k, i)))
-    return slots
+    """Unknown slots of the extended system as (symbol, level, cluster, dim), in
+    the reference's order (ifmm/operators.py:338-364): leaf (x, z) pairs in
+    Morton order, then per coarser level each cluster's children's y slots and
+    its own z slot (none at level 1)."""
+    sym, lev, idx, dim = _slot_table(store)
+    return [(_SYMS[a], int(b), int(c), int(d)) for a, b, c, d in zip(sym, lev, idx, dim)]
 
 
 def assemble_extended_dense(store: OperatorStore, tree: ClusterTree, cap: int = 4096):
-    """Materialise the initial extended system densely on the host
-    (ifmm/operators.py:367-445): particle equations, charge-lumping equations
-    and local-definition equations, blocks downloaded from the device store.
-    Returns (matrix, slots).  Raises ValueError above `cap` unknowns."""
-    slots = extended_layout(store, tree)
-    offsets, pos = {}, 0
-    for sym, k, i, dim in slots:
-        offsets[(sym, k, i)] = pos
-        pos += dim
-    m = pos
-    if m > cap:
-        raise ValueError(f"extended dimension {m} exceeds cap {cap}")
-    A = np.zeros((m, m))
-    kappa, nch = tree.depth, 1 << tree.dim
-    leaves = tree.levels[kappa]
+    """The initial extended system as a dense matrix (ifmm/operators.py:367-445),
+    scattered from the device store.  Returns (matrix, slots); ValueError above
+    `cap` unknowns."""
+    m = ctypes.c_int64()
+    _lib.check(_lib.lib.ifmm_extended_dense(store.handle, int(cap), ctypes.byref(m), None))
+    buf = np.empty((m.value, m.value))
+    _lib.check(_lib.lib.ifmm_extended_dense(store.handle, int(cap), ctypes.byref(m), _lib.ptr(buf)))
+    return np.ascontiguousarray(buf.T), extended_layout(store, tree)  # the library writes column-major
 
-    def xcols(k, i):
-        if k == kappa:
-            return [(offsets[("x", k, i)], store.part_dim(k, i))]
-        return [(offsets[("y", k + 1, ch)], store.rank(k + 1, ch)) for ch in range(nch * i, nch * (i + 1))]
 
-    for c in leaves:  # leaf particle equations
-        i = c.index
-        r0, n_i = offsets[("x", kappa, i)], store.part_dim(kappa, i)
-        for j in c.neighbors:
-            blk = store.p2p[(kappa, i, j)]
-            c0 = offsets[("x", kappa, j)]
-            A[r0:r0 + n_i, c0:c0 + blk.shape[1]] = blk
-        U = store.l2p[(kappa, i)]
-        z0 = offsets[("z", kappa, i)]
-        A[r0:r0 + n_i, z0:z0 + U.shape[1]] = U
-    for k in range(kappa, 1, -1):  # charge-lumping equations
-        for i in range(1 << (tree.dim * k)):
-            U = store.l2p[(k, i)]
-            r0, r_i = offsets[("z", k, i)], U.shape[1]
-            col = 0
-            for c0, w in xcols(k, i):
-                A[r0:r0 + r_i, c0:c0 + w] = U[col:col + w, :].T
-                col += w
-            y0 = offsets[("y", k, i)]
-            A[r0:r0 + r_i, y0:y0 + r_i] -= np.eye(r_i)
-    for k in range(2, kappa + 1):  # local-definition equations
-        for c in tree.levels[k]:
-            i = c.index
-            r0, r_i = offsets[("y", k, i)], store.rank(k, i)
-            z0 = offsets[("z", k, i)]
-            A[r0:r0 + r_i, z0:z0 + r_i] -= np.eye(r_i)
-            for j in c.interaction_list:
-                blk = store.m2l[(k, i, j)]
-                y0 = offsets[("y", k, j)]
-                A[r0:r0 + r_i, y0:y0 + blk.shape[1]] = blk
-            if k > 2:
-                pk, pi = k - 1, i // nch
-                Upar = store.l2p[(pk, pi)][store.child_slices(pk, pi)[i % nch], :]
-                zp = offsets[("z", pk, pi)]
-                A[r0:r0 + r_i, zp:zp + Upar.shape[1]] = Upar
-    return A, slots
+def _x_positions(store: OperatorStore, tree: ClusterTree) -> np.ndarray:
+    """Extended position of every point, in Morton (permuted) order."""
+    sym, _, idx, dim = _slot_table(store)
+    start = np.concatenate([[0], np.cumsum(dim.astype(np.int64))[:-1]])
+    xs = sym == 0
+    ox = np.empty(int(xs.sum()), dtype=np.int64)
+    ox[idx[xs]] = start[xs]                      # x slot offset of every leaf
+    off = np.asarray(tree.leaf_offsets, dtype=np.int64)
+    leaf = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    return ox[leaf] + (np.arange(off[-1]) - off[leaf])
 
 
 def extended_rhs(store: OperatorStore, tree: ClusterTree, b) -> np.ndarray:
-    """Extended right-hand side: b (Morton order) on the x slots, 0 elsewhere
+    """Extended right-hand side: b on the particle slots, zeros elsewhere
     (ifmm/operators.py:448-459)."""
-    slots = extended_layout(store, tree)
-    b_m = np.asarray(b, dtype=float)[tree.point_permutation]
-    out = np.zeros(sum(s[3] for s in slots))
-    pos = 0
-    for sym, k, i, dim in slots:
-        if sym == "x":
-            lo, hi = int(tree.leaf_offsets[i]), int(tree.leaf_offsets[i + 1])
-            out[pos:pos + dim] = b_m[lo:hi]
-        pos += dim
+    _, _, _, dim = _slot_table(store)
+    out = np.zeros(int(dim.astype(np.int64).sum()))
+    out[_x_positions(store, tree)] = np.asarray(b, dtype=float)[tree.point_permutation]
     return out
 
 
 def extended_restrict_x(store: OperatorStore, tree: ClusterTree, xe) -> np.ndarray:
-    """Original unknowns (original point order) of an extended solution
+    """The original unknowns of an extended solution, in original point order
     (ifmm/operators.py:462-477)."""
-    slots = extended_layout(store, tree)
-    out = np.empty(tree.n_points)
-    pos = 0
-    for sym, k, i, dim in slots:
-        if sym == "x":
-            lo, hi = int(tree.leaf_offsets[i]), int(tree.leaf_offsets[i + 1])
-            out[lo:hi] = xe[pos:pos + dim]
-        pos += dim
-    res = np.empty_like(out)
-    res[tree.point_permutation] = out
+    res = np.empty(tree.n_points)
+    res[tree.point_permutation] = np.asarray(xe)[_x_positions(store, tree)]
     return res
 
 
 def dump_extended(store: OperatorStore, tree: ClusterTree, path, cap: int = 4096) -> None:
-    """Write the extended matrix as 'row col value' nonzero triplets with a
-    one-line header (ifmm/operators.py:480-486, same format)."""
+    """Nonzeros of the extended matrix as 'row col value' lines after a header
+    line -- the reference's text format (ifmm/operators.py:480-486)."""
     A, _ = assemble_extended_dense(store, tree, cap=cap)
     rows, cols = np.nonzero(A)
     with open(path, "w") as fh:
         fh.write(f"# extended system, dimension {A.shape[0]}\n")
-        for r, c in zip(rows, cols):
-            fh.write(f"{r} {c} {A[r, c]:.17g}\n")
+        fh.writelines(f"{r} {c} {v:.17g}\n" for r, c, v in zip(rows, cols, A[rows, cols]))

@@ -72,9 +72,10 @@ class IfmmFactorization:
     @property
     def work(self) -> dict:
         """Executed / reference-equivalent FP64 flops and solve bytes per rhs."""
-        w = np.empty(4)
+        w = np.empty(6)
         _lib.check(_lib.lib.ifmm_factor_work(self.handle, _lib.ptr(w)))
-        return {"flops_exec": w[0], "flops_schur": w[1], "flops_ref": w[2], "solve_bytes": w[3]}
+        return {"flops_exec": w[0], "flops_schur": w[1], "flops_ref": w[2], "solve_bytes": w[3], "flops_lu": w[4],
+                "flops_x": w[5]}
 
     @property
     def phase_times(self) -> dict:
@@ -113,7 +114,7 @@ class IfmmFactorization:
             lib.ifmm_factor_free(h)
 
 
-PHASES = ("gather", "gauss_jordan", "x_gemm", "schur_gemm", "compress", "transition", "top")
+PHASES = ("gather", "lu", "x_solve", "schur", "compress", "transition", "top")
 
 
 def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None, diagnostics: bool = False,
