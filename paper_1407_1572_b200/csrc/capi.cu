@@ -632,7 +632,7 @@ int ifmm_test_lu_solve_x(const double* lu, const int32_t* perm, int n, int r, co
     std::vector<MatDesc> md{MatDesc{dlu, m, m, dp, 0}};
     const MatDesc* dmd = upload(ws, md, s, st);
     const ifmm::LuDiag dg = ifmm::launch_lu_diag_inv(md, dmd, ws, st, s, 0.0);  // refine every block
-    std::vector<ifmm::XSolveDesc> xd{ifmm::XSolveDesc{dlu, dp, dc, dt, db, dg.dinv, dg.flags, m, n, r, wl, w, 0}};
+    std::vector<ifmm::XSolveDesc> xd{ifmm::XSolveDesc{dlu, dp, dc, dt, db, dg.dinv, dg.flags, dg.pflag, m, n, r, wl, w, 0}};
     ifmm::launch_lu_solve_x(xd, ws, st, s);
     CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(xtop, dt, sizeof(double) * n * w, cudaMemcpyDeviceToHost));

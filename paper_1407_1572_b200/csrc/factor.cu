@@ -680,7 +680,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         s++;
       }
       cb.zero(I.C + size_t(I.soff[s]) * I.n, I.n, I.n, I.r);
-      xd.push_back(XSolveDesc{I.S, I.perm, I.C, I.Xt, I.Xb, nullptr, nullptr, I.m, I.n, I.r, I.w - I.r, I.w, 0});
+      xd.push_back(XSolveDesc{I.S, I.perm, I.C, I.Xt, I.Xb, nullptr, nullptr, nullptr, I.m, I.n, I.r, I.w - I.r, I.w, 0});
     }
     hmark(12);
     tm_.begin(PH_GATHER);
@@ -706,6 +706,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       for (size_t q = 0; q < xd.size(); q++) {
         xd[q].dinv = dg.dinv + dg.h_off[q];
         xd[q].dflag = dg.flags + dg.h_off[q] / (LU_XB * LU_XB);
+        xd[q].pflag = dg.pflag + q;
       }
       CK(cudaEventRecord(sd.join, sd.s));
       est_pending = true;

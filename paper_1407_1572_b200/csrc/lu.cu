@@ -4,6 +4,8 @@
 // lu_solve (dgetrs) (ifmm/solver.py:214-218,246); these kernels do the same
 // on a whole colour batch at once.
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <string>
 
 #include "gemm.cuh"
@@ -267,7 +269,8 @@ __global__ void __launch_bounds__(GTHREADS, 3) lu_update_kernel(const MatDesc* _
 // t >= 64 column t - 64 of U_kk.  Blocks past m are padded with the identity.
 __global__ void __launch_bounds__(128) lu_diag_inv_kernel(const MatDesc* __restrict__ desc,
                                                           const int64_t* __restrict__ doff, double* dinv,
-                                                          unsigned char* flags, double kappa_max) {
+                                                          unsigned char* flags, unsigned char* pflag,
+                                                          double kappa_max) {
   __shared__ double T[XB][XB + 1];
   __shared__ double cn[2][XB][2];  // per inverted column: 1-norm of T_kk's column, of the inverse's column
   const MatDesc D = desc[blockIdx.x];
@@ -324,6 +327,7 @@ __global__ void __launch_bounds__(128) lu_diag_inv_kernel(const MatDesc* __restr
     const size_t f = (size_t)(doff[blockIdx.x] / (2 * XB * XB)) + k;
     if (threadIdx.x == 0) flags[2 * f] = refine;
     else flags[2 * f + 1] = refine;
+    if (refine) pflag[blockIdx.x] = 1;
   }
 }
 
@@ -527,7 +531,7 @@ __device__ __forceinline__ void xchunk_next(XChunk& c, int nb, const unsigned ch
     return;
   }
   c.h = 0;
-  if (c.j == c.k && c.p < 2 && fl[2 * c.k + c.bwd]) {
+  if (fl && c.j == c.k && c.p < 2 && fl[2 * c.k + c.bwd]) {
     c.p++;
     return;
   }
@@ -576,20 +580,21 @@ __device__ __forceinline__ void xchunk_load(double* As, const XChunk& c, const d
 // fill compression cannot absorb (measured: the reference-default N = 8,000
 // system matches the reference only with it); refined, the block solve is as
 // accurate as substitution while every step stays a DMMA product.
-template <int TW, int XS_STAGES>
+template <int TW, int XS_STAGES, bool REFINE>
 __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __restrict__ descs,
                                                         const int* __restrict__ tile_map) {
   constexpr int NC = TW / 16;  // 8-column tiles per warp
-  constexpr int SP = XB + 4;   // pitch of the x1 scratch (== 4 mod 16)
   extern __shared__ double sm[];
   const XSolveDesc D = descs[tile_map[blockIdx.x]];
   const int c0 = (blockIdx.x - D.tile0) * TW;
   const int m = D.m, n = D.n, wl = D.wl, w = D.w;
-  if (m == 0) return;
+  // each pivot is solved by one of the two instantiations: with refinement
+  // support iff one of its diagonal blocks is flagged (the refinement state
+  // costs registers that slow the common path by half, measured)
+  if (m == 0 || (*D.pflag != 0) != REFINE) return;
   const int nb = (m + XB - 1) / XB, mp = XB * nb, xm = mp + 4;
   double* X = sm;
   double* As = sm + (size_t)TW * xm;
-  double* Sc = As + (size_t)XS_STAGES * 32 * XS_AP;  // x1 of the current diagonal block (TW x SP)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // gather the permuted panel: a thread owns a row, 8 of its loads in flight together
   for (int l = tid; l < mp; l += 256) {
@@ -610,9 +615,10 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
       for (int c = 0; c < 8; c++) X[(size_t)(cg + c) * xm + l] = v[c];
     }
   }
-  const unsigned char* fl = D.dflag;
+  const unsigned char* fl = REFINE ? D.dflag : nullptr;
   int T = 2 * nb * (nb - 1) + 4 * nb;  // off-diagonal halves + 2 halves per diagonal block, both sweeps
-  for (int q = 0; q < 2 * nb; q++) T += fl[q] ? 4 : 0;  // + 4 halves per refined diagonal block
+  if (REFINE)
+    for (int q = 0; q < 2 * nb; q++) T += fl[q] ? 4 : 0;  // + 4 halves per refined diagonal block
   XChunk ci{0, 0, 0, 0, 0}, cc{0, 0, 0, 0, 0};
   auto issue = [&](int t) {
     if (t < T) {
@@ -629,17 +635,17 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
     for (int b = 0; b < NC; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int fk = lane & 3, fq = lane >> 2;
   const int r0 = 16 * (warp & 3), cb = NC * (warp >> 2);  // first row of the warp, first 8-column tile
-  // apply f(pointer into X_k at an owned accumulator element, pointer into Sc at the same (row, col), value)
+  // the refinement keeps R and x1 of the warp's own tiles in registers
+  double rv[REFINE ? 2 : 1][NC][2], xv[REFINE ? 2 : 1][NC][2];
+  // f(pointer into X_k at an owned accumulator element, that element's (a, b, e))
   auto own = [&](int kb, auto f) {
 #pragma unroll
     for (int a = 0; a < 2; a++)
 #pragma unroll
       for (int b = 0; b < NC; b++) {
-        const int col = 8 * (cb + b) + 2 * fk, row = r0 + 8 * a + fq;
-        double* x0 = X + (size_t)col * xm + kb + row;
-        double* s0 = Sc + (size_t)col * SP + row;
-        f(x0, s0, acc[a][b][0]);
-        f(x0 + xm, s0 + SP, acc[a][b][1]);
+        double* x0 = X + (size_t)(8 * (cb + b) + 2 * fk) * xm + kb + r0 + 8 * a + fq;
+        f(x0, a, b, 0);
+        f(x0 + xm, a, b, 1);
         acc[a][b][0] = acc[a][b][1] = 0.0;
       }
   };
@@ -650,14 +656,13 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
     const int kb = XB * cc.k;
     const bool diag = cc.j == cc.k;
     if (diag && cc.p == 0 && cc.h == 0) {  // R = X_k - acc
-      own(kb, [](double* x, double*, double v) { *x -= v; });
+      if constexpr (REFINE) own(kb, [&](double* x, int a, int b, int e) { *x = rv[a][b][e] = *x - acc[a][b][e]; });
+      else own(kb, [&](double* x, int a, int b, int e) { *x -= acc[a][b][e]; });
       __syncthreads();
     }
     const double* A = As + (size_t)(t % XS_STAGES) * 32 * XS_AP + fk * XS_AP + r0 + fq;
-    // B operand: X rows of block j, or (T_kk x1) the x1 scratch
-    const double* B = (diag && cc.p == 1) ? Sc + (size_t)(8 * cb + fq) * SP + 32 * cc.h + fk
-                                          : X + (size_t)(8 * cb + fq) * xm + XB * cc.j + 32 * cc.h + fk;
-    const int bld = (diag && cc.p == 1) ? SP : xm;
+    const double* B = X + (size_t)(8 * cb + fq) * xm + XB * cc.j + 32 * cc.h + fk;
+    const int bld = xm;
 #pragma unroll
     for (int s = 0; s < 8; s++) {
       double fa[2], fb[NC];
@@ -673,17 +678,18 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
                        : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
                        : "d"(fa[a]), "d"(fb[b]));
     }
-    if (diag && cc.h == 1 && !fl[2 * cc.k + cc.bwd]) {  // unrefined: X_k = D R
+    if (diag && cc.h == 1) {
       __syncthreads();  // every warp has read X_k
-      own(kb, [](double* x, double*, double v) { *x = v; });
-    } else if (diag && cc.h == 1) {
-      if (cc.p == 0) {  // x1 = D R -> scratch
-        own(kb, [](double*, double* sc, double v) { *sc = v; });
-      } else if (cc.p == 1) {  // X_k = R - T x1 (the residual; no warp reads X_k in this step)
-        own(kb, [](double* x, double*, double v) { *x -= v; });
-      } else {  // x = x1 + D (R - T x1)
-        __syncthreads();  // every warp has read X_k
-        own(kb, [](double* x, double* sc, double v) { *x = *sc + v; });
+      if (!REFINE || !fl[2 * cc.k + cc.bwd]) {  // unrefined: X_k = D R
+        own(kb, [&](double* x, int a, int b, int e) { *x = acc[a][b][e]; });
+      } else if constexpr (REFINE) {
+        if (cc.p == 0) {  // x1 = D R
+          own(kb, [&](double* x, int a, int b, int e) { *x = xv[a][b][e] = acc[a][b][e]; });
+        } else if (cc.p == 1) {  // the residual R - T x1
+          own(kb, [&](double* x, int a, int b, int e) { *x = rv[a][b][e] - acc[a][b][e]; });
+        } else {  // x = x1 + D (R - T x1)
+          own(kb, [&](double* x, int a, int b, int e) { *x = xv[a][b][e] + acc[a][b][e]; });
+        }
       }
     }
     xchunk_next(cc, nb, fl);
@@ -710,7 +716,7 @@ int lu_tile_width(int m) {
 
 static size_t xsolve_smem(int tw, int stages, int m) {
   const size_t mp = size_t(XB) * ((m + XB - 1) / XB);
-  return sizeof(double) * (size_t(tw) * (mp + 4) + size_t(stages) * 32 * XS_AP + size_t(tw) * (XB + 4));
+  return sizeof(double) * (size_t(tw) * (mp + 4) + size_t(stages) * 32 * XS_AP);
 }
 
 LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, Arena& ws, Staging& st,
@@ -725,14 +731,16 @@ LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, 
   LuDiag dg;
   dg.dinv = ws.alloc_n<double>(size_t(std::max<int64_t>(1, off.back())));
   dg.flags = ws.alloc_n<unsigned char>(size_t(std::max<int64_t>(1, off.back() / (XB * XB))));
+  dg.pflag = ws.alloc_n<unsigned char>(std::max<size_t>(1, h.size()));
+  CK(cudaMemsetAsync(dg.pflag, 0, std::max<size_t>(1, h.size()), s));
   dg.d_off = upload(ws, off, s, st);
   dg.h_off = off;
   // refine a block solve when its inverted block's error kappa eps could reach
-  // a thousandth of the tolerance (tol <= 0: always)
-  const double kappa_max = tol > 0 ? 1e-3 * tol / 2.220446049250313e-16 : 0.0;
+  // a hundredth of the tolerance (tol <= 0: always)
+  const double kappa_max = tol > 0 ? 1e-2 * tol / 2.220446049250313e-16 : 0.0;
   if (!h.empty() && maxnb > 0) {
     lu_diag_inv_kernel<<<dim3(unsigned(h.size()), unsigned(maxnb)), 128, 0, s>>>(d_desc, dg.d_off, dg.dinv, dg.flags,
-                                                                                kappa_max);
+                                                                                dg.pflag, kappa_max);
     CK_LAUNCH();
   }
   return dg;
@@ -801,13 +809,13 @@ void launch_lu_solve_x(const std::vector<XSolveDesc>& hin, Arena& ws, Staging& s
   // distance must cover the L2 latency with one CTA's compute; 16-column tiles
   // for the largest pivots.
   int cfg = -1;
-  if (xsolve_smem(32, 2, maxm) <= 110 * 1024) cfg = 0;
+  if (xsolve_smem(32, 3, maxm) <= 110 * 1024) cfg = 0;
   else if (xsolve_smem(32, 4, maxm) <= 220 * 1024) cfg = 1;
   else if (xsolve_smem(16, 4, maxm) <= 220 * 1024) cfg = 2;
   else if (xsolve_smem(16, 3, maxm) <= 220 * 1024) cfg = 3;
   if (cfg < 0) invalid("pivot block too large for the X solve (m = " + std::to_string(maxm) + ")");
   const int tw = cfg >= 2 ? 16 : 32;
-  const int stages = cfg == 0 ? 2 : (cfg == 3 ? 3 : 4);
+  const int stages = (cfg == 0 || cfg == 3) ? 3 : 4;
   std::vector<XSolveDesc> h(hin);
   std::vector<int> map;
   for (size_t p = 0; p < h.size(); p++) {
@@ -819,20 +827,22 @@ void launch_lu_solve_x(const std::vector<XSolveDesc>& hin, Arena& ws, Staging& s
   const XSolveDesc* dd = upload(ws, h, s, st);
   const int* dm = upload(ws, map, s, st);
   const size_t smem = xsolve_smem(tw, stages, maxm);
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(lu_xsolve_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CK(cudaFuncSetAttribute(lu_xsolve_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CK(cudaFuncSetAttribute(lu_xsolve_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CK(cudaFuncSetAttribute(lu_xsolve_kernel<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
-  }
-  const unsigned grid = unsigned(map.size());
-  if (cfg == 0) lu_xsolve_kernel<32, 2><<<grid, 256, smem, s>>>(dd, dm);
-  else if (cfg == 1) lu_xsolve_kernel<32, 4><<<grid, 256, smem, s>>>(dd, dm);
-  else if (cfg == 2) lu_xsolve_kernel<16, 4><<<grid, 256, smem, s>>>(dd, dm);
-  else lu_xsolve_kernel<16, 3><<<grid, 256, smem, s>>>(dd, dm);
-  CK_LAUNCH();
+  auto go = [&](void (*kern)(const XSolveDesc*, const int*)) {
+    static std::mutex mu;
+    static std::set<const void*> ready;  // kernels whose shared-memory limit is raised
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (ready.insert(reinterpret_cast<const void*>(kern)).second)
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    }
+    kern<<<unsigned(map.size()), 256, smem, s>>>(dd, dm);
+    CK_LAUNCH();
+  };
+  // every pivot is handled by exactly one of the two launches (lu_xsolve_kernel)
+  if (cfg == 0) { go(lu_xsolve_kernel<32, 3, false>); go(lu_xsolve_kernel<32, 3, true>); }
+  else if (cfg == 1) { go(lu_xsolve_kernel<32, 4, false>); go(lu_xsolve_kernel<32, 4, true>); }
+  else if (cfg == 2) { go(lu_xsolve_kernel<16, 4, false>); go(lu_xsolve_kernel<16, 4, true>); }
+  else { go(lu_xsolve_kernel<16, 3, false>); go(lu_xsolve_kernel<16, 3, true>); }
 }
 
 }  // namespace ifmm

@@ -285,6 +285,7 @@ constexpr int LU_XB = 64;  // block size of the blocked triangular solves (X sol
 struct LuDiag {
   double* dinv = nullptr;
   unsigned char* flags = nullptr;  // per block: [L, U] refine the block solve (lu.cu)
+  unsigned char* pflag = nullptr;  // per matrix: any block flagged
   const int64_t* d_off = nullptr;
   std::vector<int64_t> h_off;
 };
@@ -307,6 +308,7 @@ struct XSolveDesc {
   double* Xbot;
   const double* dinv;           // the pivot's diagonal-block inverses (LuDiag)
   const unsigned char* dflag;   // and their refinement flags
+  const unsigned char* pflag;   // any of them set
   int m, n, r, wl, w;
   int tile0;  // first tile of this matrix in the launch
 };
