@@ -531,7 +531,7 @@ static int g_test_warp = 0;
 template <class G>
 __global__ void test_jacobi_kernel(double* a, int m, int n, double* v, double* sig, int* ord) {
   __shared__ CtaShared sh;
-  ifmm::g_jacobi_small(G::make_for_test(sh), a, m, n, m, v, n, sig, ord);
+  ifmm::g_jacobi(G::make_for_test(sh), a, m, n, m, v, n, sig, ord);
 }
 
 template <class G>

@@ -5,10 +5,8 @@
 
 namespace ifmm {
 __device__ int g_prof_on = 0;
-__device__ int g_jac_rt = 1;
 __device__ double g_gram_piv = 1e-14;  // K1 Gram route: scaled pivots^2 >= g_gram_piv / tol
-__device__ int g_gram = 1;    // IFMM_GRAM=0: Householder QRs in the K1 recompression   // IFMM_JACOBI_RT=0: Jacobi on R (columns) in new_dirs
-__device__ int g_jac_reg = 0;  // IFMM_JACOBI_REG=1: register-resident Jacobi for <= 16 columns (measured slower)
+__device__ int g_gram = 1;    // 1: Gram routes (K1 recompression, coarse new directions); 0: Householder QRs
 __device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
 }  // namespace ifmm
 // debug: Jacobi sweep statistics (sweeps, calls, columns) under IFMM_PROF
@@ -295,7 +293,7 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
       g_qr(g, Vc, cols, k, cols, Rr, Qr, cols, vv);
       PROF_ACC(1);
       g_gemm(g, k, k, k, 1.0, Rl, k, false, Rr, k, true, 0.0, core, k);
-      g_jacobi_small(g, core, k, k, k, Jv, k, sig, ord, g_jac_reg != 0);
+      g_jacobi(g, core, k, k, k, Jv, k, sig, ord);
       r = trunc_rank_dev(sig, ord, k, tol);
       PROF_ACC(2);
       for (int e = g.rank(); e < rows * r; e += g.size()) {
@@ -406,37 +404,23 @@ __device__ int new_dirs(const G& g, double* H, int nU, int r, const double* wsig
   }
   g_qr(g, H, nU, r, nU, R, Q, nU, vv);  // H = Q R
   PROF_ACC(5);
-  if (g_jac_rt) {
-    // one-sided Jacobi on R^T with the rotations accumulated: R^T V = X, so V
-    // holds the left singular vectors of R and ||X(:,j)|| its singular values.
-    // The rows of the triangular R are far closer to orthogonal than its
-    // columns (QR-preconditioned Jacobi): fewer sweeps, and W = Q V needs no
-    // division by sigma.
-    for (int e = g.rank(); e < r * r; e += g.size()) E[e] = R[(e / r) + (size_t)(e % r) * r];
-    g.sync();
-    g_jacobi(g, E, r, r, r, R, r, sig, ord);  // V -> R
-    PROF_ACC(6);
-    for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
-    w = min(w, cap);
-    for (int e = g.rank(); e < nU * w; e += g.size()) {
-      const int i = e % nU, c = e / nU;
-      const double* v = R + (size_t)ord[c] * r;
-      double acc = 0.0;
-      for (int t = 0; t < r; t++) acc = fma(Q[i + (size_t)t * nU], v[t], acc);
-      W[i + (size_t)c * nU] = acc;
-    }
-  } else {
-    g_jacobi_small(g, R, r, r, r, nullptr, 0, sig, ord, g_jac_reg != 0);  // R V = U_R S
-    PROF_ACC(6);
-    for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
-    w = min(w, cap);
-    for (int e = g.rank(); e < nU * w; e += g.size()) {
-      const int i = e % nU, c = e / nU;
-      const int col = ord[c];
-      double acc = 0.0;
-      for (int t = 0; t < r; t++) acc = fma(Q[i + (size_t)t * nU], R[t + (size_t)col * r], acc);
-      W[i + (size_t)c * nU] = acc / sig[col];
-    }
+  // one-sided Jacobi on R^T with the rotations accumulated: R^T V = X, so V
+  // holds the left singular vectors of R and ||X(:,j)|| its singular values.
+  // The rows of the triangular R are far closer to orthogonal than its
+  // columns (QR-preconditioned Jacobi): fewer sweeps, and W = Q V needs no
+  // division by sigma.
+  for (int e = g.rank(); e < r * r; e += g.size()) E[e] = R[(e / r) + (size_t)(e % r) * r];
+  g.sync();
+  g_jacobi(g, E, r, r, r, R, r, sig, ord);  // V -> R
+  PROF_ACC(6);
+  for (int t = 0; t < r; t++) w += (sig[ord[t]] > cutoff);
+  w = min(w, cap);
+  for (int e = g.rank(); e < nU * w; e += g.size()) {
+    const int i = e % nU, c = e / nU;
+    const double* v = R + (size_t)ord[c] * r;
+    double acc = 0.0;
+    for (int t = 0; t < r; t++) acc = fma(Q[i + (size_t)t * nU], v[t], acc);
+    W[i + (size_t)c * nU] = acc;
   }
   if (g_prof_on && g.rank() == 0 && w == 0) atomicAdd(&g_cyc[12], 1ull);
   g.sync();
@@ -677,51 +661,36 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
   // warp per fill / chain / pivot, 4 warps per CTA -- no block barriers and
   // many fills in flight per SM.  Coarse levels (few, large fills): one wide
   // CTA per fill shortens each step of the dependent chains.
-  static const bool narrow = getenv("IFMM_BS128") != nullptr;  // debug: force 128-thread CTAs
-  static const int warp_mx = getenv("IFMM_WARP_MX") ? atoi(getenv("IFMM_WARP_MX")) : 0;
-  const bool wmode = !narrow && MX <= warp_mx;
-  // fine levels: small CTAs, many fills in flight per SM (IFMM_BS_SMALL: tuning)
-  static const int bs_small = getenv("IFMM_BS_SMALL") ? atoi(getenv("IFMM_BS_SMALL")) : 128;
+  // (warp workers -- one warp per fill -- exist for the test hooks; measured
+  // slower than small CTAs on the C3 leaf level, so production uses CTAs)
+  const bool wmode = false;
+  // fine levels: small CTAs, many fills in flight per SM
+  constexpr int bs_small = 128;
   const int per_sm = 8 * 128 / bs_small;  // resident CTAs per SM at 64 registers
   // coarse levels: per-step latency of few long chains dominates -> widest CTAs
   // for the largest blocks (measured: 1024 wins for MX >= ~800, loses at 265-570)
-  static const int bs_big_env = getenv("IFMM_BS_BIG") ? atoi(getenv("IFMM_BS_BIG")) : 0;  // tuning override
-  const int bs_big = bs_big_env ? bs_big_env : (MX >= 700 ? 1024 : 512);
-  static const int nf_big = getenv("IFMM_K1_NF_BIG") ? atoi(getenv("IFMM_K1_NF_BIG")) : 2048;  // tuning
-  const int bs_fill = narrow ? 128 : (MX >= 256 && nf_shape < nf_big) ? bs_big : (MX >= 128 ? 256 : bs_small);
+  const int bs_big = MX >= 700 ? 1024 : 512;
+  constexpr int nf_big = 2048;
+  const int bs_fill = (MX >= 256 && nf_shape < nf_big) ? bs_big : (MX >= 128 ? 256 : bs_small);
   // level-6-sized bases (256 <= MX < 400): 256-thread chains measured best (112 -> 102 ms)
-  static const int bs_mid = getenv("IFMM_BS_MID") ? atoi(getenv("IFMM_BS_MID")) : 256;
-  const int bs_dirs = narrow ? 128
-                             : (bs_mid && MX >= 256 && MX < 400) ? bs_mid
-                                                                 : MX >= 256 ? bs_big : (MX >= 128 ? 256 : bs_small);
+  const int bs_dirs = (MX >= 256 && MX < 400) ? 256 : MX >= 256 ? bs_big : (MX >= 128 ? 256 : bs_small);
   constexpr int WPB = 4;  // warps per CTA in warp mode
   static const bool prof = getenv("IFMM_PROF") != nullptr;
-  static const int jac_reg = getenv("IFMM_JACOBI_REG") ? atoi(getenv("IFMM_JACOBI_REG")) : 0;
-  static const int jac_rt = getenv("IFMM_JACOBI_RT") ? atoi(getenv("IFMM_JACOBI_RT")) : 1;
-  static bool jac_set = false;
-  if (!jac_set) {
-    CK(cudaMemcpyToSymbolAsync(g_jac_rt, &jac_rt, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyToSymbolAsync(g_jac_reg, &jac_reg, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-    jac_set = true;
-  }
   {
     // The Gram routes (K1 recompression through the cross Gram matrices, new
     // directions through H^T H) lose accuracy ~ eps * cond^2; that is far below
     // the truncation for tol >= 1e-9, but at tolerances near machine precision
     // (the reference default 1e-14) the duplicated directions make pivots
     // singular, so the Householder routes run there.
-    static const int gram_env = getenv("IFMM_GRAM") ? atoi(getenv("IFMM_GRAM")) : 1;
-    // IFMM_GRAM=0: Householder everywhere; 2: Gram only in the K1 recompression
-    const int gram = (gram_env != 0 && tol >= 1e-9) ? gram_env : 0;
+    const int gram = tol >= 1e-9 ? 1 : 0;
     CK(cudaMemcpyToSymbolAsync(g_gram, &gram, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-    static const double gpiv = getenv("IFMM_GRAM_PIV") ? atof(getenv("IFMM_GRAM_PIV")) : 1e-14;
+    const double gpiv = 1e-14;
     CK(cudaMemcpyToSymbolAsync(g_gram_piv, &gpiv, sizeof(double), 0, cudaMemcpyHostToDevice, s));
     // Jacobi rotation threshold from the truncation tolerance: singular values
     // then carry ~(1e-4 tol)^2 relative error -- far below the truncation decisions
     // (1e-2 tol measured: 15 ms faster at C3 but a C3-parameter pivot crossed the
     // 1e12 condition limit; 1e-4 tol: 10 ms faster, all gates green)
-    static const double jscale = getenv("IFMM_JAC_TOL_SCALE") ? atof(getenv("IFMM_JAC_TOL_SCALE")) : 1e-4;
-    const double jt = tol > 0.0 ? std::max(1e-15, std::min(1e-8, tol * jscale)) : 1e-15;
+    const double jt = tol > 0.0 ? std::max(1e-15, std::min(1e-8, tol * 1e-4)) : 1e-15;
     CK(cudaMemcpyToSymbolAsync(g_jac_tol, &jt, sizeof(double), 0, cudaMemcpyHostToDevice, s));
   }
   if (prof) {
@@ -765,14 +734,12 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
       const int grid = resident_grid(nf, bs_fill == bs_small ? per_sm : 8);
       double* scr = ws.alloc_n<double>(slot * grid);
       // ACA and recompression as two passes over the fills: every CTA on an SM
-      // then runs the same (smaller) code region (IFMM_K1_SPLIT=0: one pass)
-      static const int split_env = getenv("IFMM_K1_SPLIT") ? atoi(getenv("IFMM_K1_SPLIT")) : 1;
-      if (split_env == 2 || (split_env && bs_fill == bs_small)) {  // measured: a gain at the leaf level only
-        // fills of one kind (P2P, then hybrid) run side by side (IFMM_K1_ORDER=0: batch order;
+      // then runs the same (smaller) code region
+      if (bs_fill == bs_small) {  // measured: a gain at the leaf level only
+        // fills of one kind (P2P, then hybrid) run side by side (batch order instead:
         // measured 100 -> 98 ms at the C3 leaf level; largest-first within a kind: 107 ms)
-        static const int order_env = getenv("IFMM_K1_ORDER") ? atoi(getenv("IFMM_K1_ORDER")) : 1;
         const int* dorder = nullptr;
-        if (order_env) {
+        {
           std::vector<int> ord;
           ord.reserve(nf);
           for (int f = 0; f < nf; f++)

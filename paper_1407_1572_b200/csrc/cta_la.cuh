@@ -381,137 +381,6 @@ __device__ inline void g_jacobi(const G& g, double* A, int m, int n, int lda, do
   g.sync();
 }
 
-// Register-resident one-sided Jacobi for m <= M, n <= 32, run by ONE warp:
-// lane j holds column j of A (and of V).  Round r of the circle method pairs
-// player r with nn-1 and p with (2r - p) mod (nn-1) otherwise (nn = n rounded
-// up to even; nn-1 rounds cover every pair once).  Partners exchange columns
-// with shuffles and both compute the pair's rotation from the same values in
-// the same order, so they agree bit for bit -- no reductions, no barriers.
-// Same rotation formula and skip rules as g_jacobi.
-template <int M, bool WANT_V>
-__device__ __noinline__ void warp_jacobi_reg(double* A, int m, int n, int lda, double* V, int ldv, double* sig,
-                                             int* ord, int max_sweeps) {
-  constexpr bool KEEP = M <= 16;  // keep the partner column in registers
-  const int lane = threadIdx.x & 31;
-  const bool own = lane < n;
-  double x[M], v[WANT_V ? M : 1];
-#pragma unroll
-  for (int i = 0; i < M; i++) x[i] = (own && i < m) ? A[i + (size_t)lane * lda] : 0.0;
-  if (WANT_V) {
-#pragma unroll
-    for (int i = 0; i < M; i++) v[i] = (i == lane) ? 1.0 : 0.0;
-  }
-  const int nn = n + (n & 1), np = nn - 1;
-  for (int sweep = 0; sweep < max_sweeps && n > 1; sweep++) {
-    bool rot = false;
-    for (int r = 0; r < np; r++) {
-      int P;
-      if (lane == np) P = r;
-      else if (lane == r) P = np;
-      else {
-        P = 2 * r - lane;  // in (-np, 2 np)
-        if (P < 0) P += np;
-        if (P >= np) P -= np;
-      }
-      const bool act = own && P < n;
-      const int src = act ? P : lane;
-      const bool low = lane < P;
-      double y[KEEP ? M : 1];
-      double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-      for (int i = 0; i < M; i++) {
-        if (i < m) {  // warp-uniform
-          const double o = __shfl_sync(0xffffffffu, x[i], src);
-          if (KEEP) y[i] = o;
-          const double xl = low ? x[i] : o, yh = low ? o : x[i];
-          al = fma(xl, xl, al);
-          be = fma(yh, yh, be);
-          ga = fma(xl, yh, ga);
-        }
-      }
-      double c = 1.0, sn = 0.0;
-      bool doit = act && !(ga == 0.0 || fabs(ga) <= g_jac_tol * sqrt(al * be));
-      if (doit) {
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        if (fabs(t) < 1e-16) doit = false;
-        c = 1.0 / sqrt(1.0 + t * t);
-        sn = c * t;
-      }
-      rot |= doit;
-      if (!__any_sync(0xffffffffu, doit)) continue;
-#pragma unroll
-      for (int i = 0; i < M; i++) {
-        if (i < m) {
-          const double o = KEEP ? y[i] : __shfl_sync(0xffffffffu, x[i], src);
-          if (doit) x[i] = low ? c * x[i] - sn * o : sn * o + c * x[i];
-        }
-      }
-      if (WANT_V) {
-#pragma unroll
-        for (int i = 0; i < M; i++) {
-          if (i < n) {
-            const double o = __shfl_sync(0xffffffffu, v[i], src);
-            if (doit) v[i] = low ? c * v[i] - sn * o : sn * o + c * v[i];
-          }
-        }
-      }
-    }
-    if (!__any_sync(0xffffffffu, rot)) {
-#ifdef IFMM_JACOBI_STATS
-      IFMM_JACOBI_STATS(sweep + 1, n, lane == 0);
-#endif
-      break;
-    }
-  }
-  double nrm = 0.0;
-#pragma unroll
-  for (int i = 0; i < M; i++) nrm = fma(x[i], x[i], nrm);
-  nrm = sqrt(nrm);
-  int rank = 0;
-  for (int o = 0; o < n; o++) {
-    const double so = __shfl_sync(0xffffffffu, nrm, o);
-    rank += (so > nrm) || (so == nrm && o < lane);
-  }
-  if (own) {
-#pragma unroll
-    for (int i = 0; i < M; i++)
-      if (i < m) A[i + (size_t)lane * lda] = x[i];
-    if (WANT_V) {
-#pragma unroll
-      for (int i = 0; i < M; i++)
-        if (i < n) V[i + (size_t)lane * ldv] = v[i];
-    }
-    sig[lane] = nrm;
-    ord[rank] = lane;
-  }
-}
-
-// Jacobi entry used by the compression: register path for small problems
-// (warp 0 of a CTA group does it while the others wait), else g_jacobi.
-template <class G>
-__device__ inline void g_jacobi_small(const G& g, double* A, int m, int n, int lda, double* V, int ldv, double* sig,
-                                      int* ord, bool use_reg = true, int max_sweeps = 40) {
-  // rows held per lane: m (plus n for the V columns)
-  const int mm = V ? max(m, n) : m;
-  // measured: the single-warp register path wins ~2x for <= 16 columns and
-  // loses to the CTA's warp-parallel pair rounds beyond that
-  if (use_reg && n <= 16 && mm <= 16) {
-    if (g.warp() == 0) {
-      if (mm <= 8) {
-        if (V) warp_jacobi_reg<8, true>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
-        else warp_jacobi_reg<8, false>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
-      } else if (mm <= 16) {
-        if (V) warp_jacobi_reg<16, true>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
-        else warp_jacobi_reg<16, false>(A, m, n, lda, V, ldv, sig, ord, max_sweeps);
-      }
-    }
-    g.sync();
-    return;
-  }
-  g_jacobi(g, A, m, n, lda, V, ldv, sig, ord, max_sweeps);
-}
-
 // Smallest r with s[r]/s[0] < tol (s sorted decreasing); ifmm/lowrank.py:137-144
 __device__ inline int trunc_rank_dev(const double* sig, const int* ord, int n, double tol) {
   if (n == 0) return 0;

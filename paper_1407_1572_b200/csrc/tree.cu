@@ -252,7 +252,7 @@ TreeH* tree_build(const double* pts_in, int64_t n, int dim, int depth, bool devi
     invalid("duplicate points at indices " + std::to_string(i) + " and " + std::to_string(j));
   }
   for (int64_t c = 0; c < nleaf; c++)
-    if (cnt[c] == 0 && !getenv("IFMM_EXPERIMENTAL_EMPTY_LEAVES"))  // experiment
+    if (cnt[c] == 0)  // uniform trees only, as the reference (ifmm/geometry.py:191-195)
       invalid("leaf cell " + std::to_string(c) + " is empty at depth " + std::to_string(depth));
   build_lists(t.get());
   return t.release();
