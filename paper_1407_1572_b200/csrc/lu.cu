@@ -137,6 +137,143 @@ __global__ void __launch_bounds__(512) lu_panel_kernel(const MatDesc* __restrict
   if (tid == 0) nmoves[blockIdx.x] = cnt;
 }
 
+// The same panel factorization with the panel in registers: 256 threads,
+// thread t owns panel rows t + 256 q (q < RPT), all 32 of their panel values.
+// One barrier per column: every warp posts its best candidate (|value|,
+// position, row) and, from the candidate's owner, the candidate's whole panel
+// row into a per-warp slot (double-buffered by column parity); after the
+// barrier every thread reduces the <= 8 candidates itself and reads the pivot
+// row from the winning slot.  Positions are tracked per row in registers (the
+// row at position c and the pivot row trade positions).  Same pivot choices
+// (ties to the smallest position) and the same fma sequence as lu_panel_kernel,
+// so both give identical factors.  b == 32 only.
+template <int RPT>
+__global__ void __launch_bounds__(256) lu_panel_reg_kernel(const MatDesc* __restrict__ desc, int j, int* info,
+                                                           RowMove* moves, int* nmoves) {
+  constexpr int B = 32, NT = 256, NW = NT / 32;
+  __shared__ double cv[2][NW], crow[2][NW][B];
+  __shared__ int cp[2][NW], cr[2][NW];
+  __shared__ int s_cnt;
+  __shared__ int mv_dst[2 * B], mv_src[2 * B], mv_perm[2 * B];
+  const MatDesc D = desc[blockIdx.x];
+  const int m = D.m;
+  if (m <= j) return;
+  const int bb = min(B, m - j), nr = m - j;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double v[RPT][B];
+  int pos[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    const int r = tid + NT * q;
+    pos[q] = r < nr ? r : 0x7fffffff;
+#pragma unroll
+    for (int c = 0; c < B; c++) v[q][c] = (r < nr && c < bb) ? D.A[(j + r) + (size_t)(j + c) * D.lda] : 0.0;
+  }
+  if (tid == 0) s_cnt = 0;
+  bool sing_seen = false;
+#pragma unroll
+  for (int c = 0; c < B; c++) {
+    if (c >= bb) break;
+    const int par = c & 1;
+    // local candidate among own rows at positions >= c
+    double bv = -1.0;
+    int bp = 0x7fffffff, bq = -1;
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      const double a = fabs(v[q][c]);
+      if (pos[q] >= c && pos[q] != 0x7fffffff && (a > bv || (a == bv && pos[q] < bp))) {
+        bv = a;
+        bp = pos[q];
+        bq = q;
+      }
+    }
+    int br = bq >= 0 ? tid + NT * bq : -1;
+    double wv = bv;
+    int wp = bp, wr = br;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, wp, o), orr = __shfl_xor_sync(0xffffffffu, wr, o);
+      if (ov > wv || (ov == wv && op < wp)) { wv = ov; wp = op; wr = orr; }
+    }
+    // the warp's winner posts its row
+    if (br >= 0 && br == wr) {
+#pragma unroll
+      for (int q = 0; q < RPT; q++)
+        if (q == bq)
+#pragma unroll
+          for (int cc = 0; cc < B; cc++) crow[par][warp][cc] = v[q][cc];
+    }
+    if (lane == 0) {
+      cv[par][warp] = wv;
+      cp[par][warp] = wp;
+      cr[par][warp] = wr;
+    }
+    __syncthreads();
+    double gv = -1.0;
+    int gp = 0x7fffffff, gw = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+      const double a = cv[par][w];
+      const int p = cp[par][w];
+      if (a > gv || (a == gv && p < gp)) { gv = a; gp = p; gw = w; }
+    }
+    const int grow = cr[par][gw];
+    const double pv = crow[par][gw][c];
+    const bool sing = (pv == 0.0 || pv != pv);
+    if (sing && tid == 0 && !sing_seen && info[blockIdx.x] == 0) info[blockIdx.x] = j + c + 1;
+    sing_seen |= sing;
+    const double inv = sing ? 0.0 : 1.0 / pv;
+    // positions: the pivot row moves to c, the row at c to the pivot's old position
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      const int r = tid + NT * q;
+      if (r == grow) pos[q] = c;
+      else if (pos[q] == c) pos[q] = gp;
+    }
+    // eliminate below the pivot
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      if (pos[q] > c && pos[q] != 0x7fffffff) {
+        const double f = v[q][c] * inv;
+        v[q][c] = f;
+        if (f != 0.0)
+#pragma unroll
+          for (int cc = c + 1; cc < B; cc++) v[q][cc] = fma(-f, crow[par][gw][cc], v[q][cc]);
+      }
+    }
+  }
+  // write back in final order; moves and the permutation update
+  int oldperm[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    const int r = tid + NT * q;
+    oldperm[q] = r < nr ? D.ipiv[j + r] : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    const int r = tid + NT * q;
+    if (r >= nr) continue;
+    const int l = pos[q];
+    double* dst = D.A + j + l;
+#pragma unroll
+    for (int c = 0; c < B; c++)
+      if (c < bb) dst[(size_t)(j + c) * D.lda] = v[q][c];
+    if (l != r) {
+      D.ipiv[j + l] = oldperm[q];
+      const int k = atomicAdd(&s_cnt, 1);
+      mv_dst[k] = j + l;
+      mv_src[k] = j + r;
+    }
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  if (tid < cnt) moves[(size_t)blockIdx.x * 2 * B + tid] = RowMove{mv_dst[tid], mv_src[tid]};
+  if (tid == 0) nmoves[blockIdx.x] = cnt;
+  (void)mv_perm;
+}
+
 // Row moves on every column outside the panel, then U12 = L11^-1 A12 on the
 // columns right of it (forward substitution with the unit lower panel block,
 // lanes own rows).  One warp per column.
@@ -773,7 +910,12 @@ void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_inf
   const int gy = std::max(1, std::min(16, (maxm + 63) / 64));
   for (int j = 0; j < maxm; j += b) {
     const size_t smem = size_t(maxm - j) * (std::min(b, maxm - j) + 1) * 8 + size_t(maxm - j) * 8;
-    lu_panel_kernel<<<n, pthreads, smem, s>>>(d_desc, j, b, d_info, moves, nmoves);
+    // register panel while the tallest panel fits 3 rows per thread (b = 32)
+    const int rows = maxm - j;
+    if (b == 32 && rows <= 256) lu_panel_reg_kernel<1><<<n, 256, 0, s>>>(d_desc, j, d_info, moves, nmoves);
+    else if (b == 32 && rows <= 512) lu_panel_reg_kernel<2><<<n, 256, 0, s>>>(d_desc, j, d_info, moves, nmoves);
+    else if (b == 32 && rows <= 768) lu_panel_reg_kernel<3><<<n, 256, 0, s>>>(d_desc, j, d_info, moves, nmoves);
+    else lu_panel_kernel<<<n, pthreads, smem, s>>>(d_desc, j, b, d_info, moves, nmoves);
     CK_LAUNCH();
     lu_swap_trsm_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, j, b, moves, nmoves);
     CK_LAUNCH();
