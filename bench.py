@@ -46,12 +46,15 @@ CONFIGS = {
     "C3": (1048576, "inv_r", 7, 4, 1e-6, 1),
     "C3_65k": (65536, "inv_r", 5, 4, 1e-6, 1),
     "C3_262k": (262144, "inv_r", 6, 4, 1e-6, 1),
+    # BASELINE C5: 32 simultaneous rhs; sized for 8 GPUs (records alone ~0.85 TB)
+    "C5": (16777216, "log_r", 9, 4, 1e-6, 32),
 }
 METRIC = "IFMM factor+solve seconds at N=1M 2D"
 PIVOT_LIMIT = 1e12  # ifmm/solver.py:50
 # bounded CPU sample of the reference algorithm: the config's parameters at a
 # smaller N (depth 4 = 256 leaves of 64 points), about 9 s of one core
-SAMPLE = {"C3": (16384, 4), "C3_65k": (16384, 4), "C3_262k": (16384, 4), "C2": (16384, 4), "C1": (4096, 3)}
+SAMPLE = {"C3": (16384, 4), "C3_65k": (16384, 4), "C3_262k": (16384, 4), "C2": (16384, 4), "C1": (4096, 3),
+          "C5": (16384, 4)}
 C3_FULL_RUN = os.path.join(ROOT, "profiles", "r02_c3_reference_cpu.json")
 
 
@@ -237,6 +240,9 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="N > 1: NCCL (one GPU per rank), or host-staged over gloo (ranks may share a GPU; "
+                         "validates the multi-process path, not a performance mode)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     ws, rank, local = dist_env()
@@ -255,14 +261,15 @@ def main():
     from paper_1407_1572_b200 import _lib
 
     if ws > 1:
-        torch.cuda.set_device(local)
-        _lib.check(_lib.lib.ifmm_set_device(local))
-        dist.init_process_group("nccl")
+        dev = local % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
+        _lib.check(_lib.lib.ifmm_set_device(dev))
+        dist.init_process_group("nccl" if args.transport == "nccl" else "gloo")
     N, kern, depth, p, tol, nrhs = cfg
     rng_pts = np.random.default_rng(0)
     pts = 2.0 * rng_pts.random((N, 2)) - 1.0      # [0,1]^2 mapped to the reference box
     kernel = ifmm.baseline_kernel(kern, N)
-    b_host = np.random.default_rng([0, 1]).standard_normal(N)
+    b_host = np.random.default_rng([0, 1]).standard_normal((N, nrhs) if nrhs > 1 else N)
     b_dev = torch.from_numpy(b_host).cuda()
 
     torch.cuda.synchronize()
@@ -276,7 +283,7 @@ def main():
     comm = None
     if ws > 1:
         from paper_1407_1572_b200.distributed import Communicator
-        comm = Communicator.from_torch()
+        comm = Communicator.from_torch() if args.transport == "nccl" else Communicator.host()
 
     def factor(timing=False):
         return ifmm.factorize(store, tree, pivot_condition_limit=PIVOT_LIMIT, on_singular="record", comm=comm,
@@ -309,8 +316,9 @@ def main():
     if ws > 1:
         dist.barrier()
     t_step = float(np.mean(times))
+    red_dev = "cuda" if args.transport == "nccl" else "cpu"
     if ws > 1:
-        t_max = torch.tensor([t_step], device="cuda")
+        t_max = torch.tensor([t_step], device=red_dev)
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
         t_step = float(t_max.item())
 
@@ -339,7 +347,7 @@ def main():
         del f2
     e2e = float(np.mean(e2e_times))
     if ws > 1:
-        te = torch.tensor([e2e], device="cuda")
+        te = torch.tensor([e2e], device=red_dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = float(te.item())
 
@@ -350,7 +358,7 @@ def main():
     work_all = dict(work)
     if ws > 1:  # per-rank work -> whole job
         keys = ("flops_exec", "flops_schur", "flops_ref", "solve_bytes", "flops_lu", "flops_x")
-        wt = torch.tensor([work[k] for k in keys], dtype=torch.float64, device="cuda")
+        wt = torch.tensor([work[k] for k in keys], dtype=torch.float64, device=red_dev)
         dist.all_reduce(wt)
         work_all = dict(zip(keys, wt.tolist()))
     fl_peak = measured_fp64_peak()
@@ -408,8 +416,8 @@ def main():
         "dtype": "f64", "data": "synthetic (seeded uniform points in [0,1]^2, N(0,1) rhs)",
         "config": {"workload": args.config, "N": N, "kernel": "1/|x-y|" if kern == "inv_r" else "log|x-y|",
                    "diag": "sqrt(N)", "depth": depth, "p": p, "eps": tol, "nrhs": nrhs,
-                   "parallelism": f"subtree{ws} (level-2 subtrees per rank, NCCL halo exchange per colour batch)"
-                   if ws > 1 else "single",
+                   "parallelism": f"subtree{ws} (level-2 subtrees per rank, {args.transport} halo exchange per "
+                                  f"colour batch)" if ws > 1 else "single",
                    "pivot_condition_limit": PIVOT_LIMIT, "on_singular": "record",
                    "l2": "factor state (GBs) >> 126 MB L2; no flush needed"},
         "relative_residual": resid,

@@ -171,6 +171,19 @@ int ifmm_comm_nccl_unique_id(uint8_t* out128);
 int ifmm_comm_nccl_version(int* version);
 /* collective: communicator over the current CUDA device of every rank */
 int ifmm_comm_nccl_init(const uint8_t* id128, int nranks, int rank, ifmm_comm** out);
+/* host-staged transport: the collectives call back into the caller (e.g.
+ * torch.distributed over gloo) with pinned host buffers; every rank must make
+ * the same sequence of calls.  allgather: recv (nranks * bytes, rank-major)
+ * receives every rank's `bytes` from send.  exchange: nsend sends / nrecv
+ * receives (peer, buffer, bytes); messages between a pair match in list order.
+ * Callbacks return 0 on success.  Runs the real multi-process schedule on
+ * processes that share one GPU. */
+typedef int (*ifmm_host_allgather_fn)(void* ctx, const void* send, void* recv, int64_t bytes);
+typedef int (*ifmm_host_exchange_fn)(void* ctx, int nsend, const int32_t* send_peer, void* const* send_buf,
+                                     const int64_t* send_bytes, int nrecv, const int32_t* recv_peer,
+                                     void* const* recv_buf, const int64_t* recv_bytes);
+int ifmm_comm_host_init(int nranks, int rank, ifmm_host_allgather_fn allgather, ifmm_host_exchange_fn exchange,
+                        void* ctx, ifmm_comm** out);
 void ifmm_comm_free(ifmm_comm* c);
 /* collective transport check: all-gather of n doubles and a ring send/recv
  * (a 1-rank communicator sends to itself); ok = 1 if all data arrived */

@@ -75,6 +75,7 @@ SIGNATURES = {
     "ifmm_comm_nccl_unique_id": (_i32, [_p]),
     "ifmm_comm_nccl_version": (_i32, [_pi32]),
     "ifmm_comm_nccl_init": (_i32, [_p, _i32, _i32, ctypes.POINTER(_p)]),
+    "ifmm_comm_host_init": (_i32, [_i32, _i32, _p, _p, _p, ctypes.POINTER(_p)]),
     "ifmm_comm_free": (None, [_p]),
     "ifmm_comm_selftest": (_i32, [_p, _i64, _pi32]),
     "ifmm_factorize_sharded": (_i32, [_p, _p, _d, _i32, _d, ctypes.POINTER(_p)]),

@@ -396,6 +396,16 @@ int ifmm_comm_nccl_init(const uint8_t* id128, int nranks, int rank, ifmm_comm** 
   });
 }
 
+int ifmm_comm_host_init(int nranks, int rank, ifmm_host_allgather_fn allgather, ifmm_host_exchange_fn exchange,
+                        void* ctx, ifmm_comm** out) {
+  return guard([&] {
+    if (!allgather || !exchange || !out) invalid("null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) invalid("bad rank / nranks");
+    ensure_device();
+    *out = new ifmm_comm{std::make_shared<ifmm::HostComm>(nranks, rank, allgather, exchange, ctx)};
+  });
+}
+
 void ifmm_comm_free(ifmm_comm* c) { delete c; }
 
 int ifmm_comm_selftest(ifmm_comm* c, int64_t n, int32_t* ok) {

@@ -114,6 +114,47 @@ void NcclComm::exchange(const std::vector<Msg>& sends, const std::vector<Msg>& r
   nccl_check(*api_, api_->GroupEnd(), "GroupEnd");
 }
 
+// -------------------------------------------------------------- host-staged
+void HostComm::allgather(const void* dsend, void* drecv, size_t bytes, cudaStream_t s) {
+  calls++;
+  bytes_meta += double(bytes) * (size_ - 1);
+  st_.reset();
+  char* hs = static_cast<char*>(st_.get(std::max<size_t>(1, bytes)));
+  char* hr = static_cast<char*>(st_.get(std::max<size_t>(1, bytes * size_)));
+  if (bytes) CK(cudaMemcpyAsync(hs, dsend, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (ag_(ctx_, hs, hr, int64_t(bytes)) != 0) throw Error(IFMM_CUDA, "host all-gather callback failed");
+  if (bytes) CK(cudaMemcpyAsync(drecv, hr, bytes * size_, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+void HostComm::exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t s) {
+  calls++;
+  st_.reset();
+  std::vector<int32_t> sp, rp;
+  std::vector<void*> sb, rb;
+  std::vector<int64_t> sn, rn;
+  for (const Msg& m : sends) {
+    void* h = st_.get(std::max<size_t>(1, m.bytes));
+    if (m.bytes) CK(cudaMemcpyAsync(h, m.ptr, m.bytes, cudaMemcpyDeviceToHost, s));
+    sp.push_back(m.peer);
+    sb.push_back(h);
+    sn.push_back(int64_t(m.bytes));
+    bytes_sent += double(m.bytes);
+  }
+  for (const Msg& m : recvs) {
+    rp.push_back(m.peer);
+    rb.push_back(st_.get(std::max<size_t>(1, m.bytes)));
+    rn.push_back(int64_t(m.bytes));
+  }
+  CK(cudaStreamSynchronize(s));
+  if (ex_(ctx_, int(sp.size()), sp.data(), sb.data(), sn.data(), int(rp.size()), rp.data(), rb.data(), rn.data()) != 0)
+    throw Error(IFMM_CUDA, "host exchange callback failed");
+  for (size_t q = 0; q < recvs.size(); q++)
+    if (recvs[q].bytes) CK(cudaMemcpyAsync(recvs[q].ptr, rb[q], recvs[q].bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+
 // -------------------------------------------------------------- threads
 void LocalWorld::barrier() {
   std::unique_lock<std::mutex> lk(mu);

@@ -65,6 +65,33 @@ class NcclComm : public Comm {
 void nccl_unique_id(void* out128);
 int nccl_version();
 
+// -------------------------------------------------------------- host-staged
+// Collectives through caller-supplied host callbacks (e.g. torch.distributed
+// over gloo): device buffers are staged through pinned host memory.  Slow, but
+// it runs the real multi-process control flow -- one process per rank, the
+// same schedule and messages as NCCL -- on any number of processes sharing
+// one GPU (the kernels of different ranks never wait on one another).
+typedef int (*HostAllgatherFn)(void* ctx, const void* send, void* recv, int64_t bytes);
+typedef int (*HostExchangeFn)(void* ctx, int nsend, const int32_t* send_peer, void* const* send_buf,
+                              const int64_t* send_bytes, int nrecv, const int32_t* recv_peer, void* const* recv_buf,
+                              const int64_t* recv_bytes);
+class HostComm : public Comm {
+ public:
+  HostComm(int nranks, int rank, HostAllgatherFn ag, HostExchangeFn ex, void* ctx)
+      : ag_(ag), ex_(ex), ctx_(ctx) {
+    rank_ = rank;
+    size_ = nranks;
+  }
+  void allgather(const void* dsend, void* drecv, size_t bytes, cudaStream_t s) override;
+  void exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t s) override;
+
+ private:
+  HostAllgatherFn ag_;
+  HostExchangeFn ex_;
+  void* ctx_;
+  Staging st_;
+};
+
 // -------------------------------------------------------------- threads
 struct LocalWorld {
   explicit LocalWorld(int n) : size(n), posted_ptr(n), posted_sends(n) {}

@@ -53,6 +53,13 @@ def broadcast_unique_id(group=None) -> bytes:
     return obj[0]
 
 
+_P = ctypes.POINTER
+_HOST_AG = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+_HOST_EX = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, _P(ctypes.c_int32), _P(ctypes.c_void_p),
+                            _P(ctypes.c_int64), ctypes.c_int, _P(ctypes.c_int32), _P(ctypes.c_void_p),
+                            _P(ctypes.c_int64))
+
+
 class Communicator:
     """NCCL communicator of the library (one rank per process / GPU)."""
 
@@ -87,6 +94,75 @@ class Communicator:
         import torch.distributed as dist
         rank, size = dist.get_rank(group), dist.get_world_size(group)
         return cls.nccl(broadcast_unique_id(group), size, rank)
+
+    @classmethod
+    def host(cls, group=None) -> "Communicator":
+        """Collective over a torch.distributed group of ANY backend (gloo on
+        CPU tensors): the library's collectives are staged through pinned host
+        memory and handed to torch.distributed (all_gather, isend / irecv).
+        Slow; it runs the real multi-process schedule on processes that share
+        one GPU, where NCCL refuses duplicate devices."""
+        import torch
+        import torch.distributed as dist
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+        glob = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+
+        def view(addr, n):
+            return np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(addr)) if n else np.zeros(0, np.uint8)
+
+        def allgather(ctx, send, recv, nbytes):
+            try:
+                t = torch.from_numpy(view(send, nbytes).copy())
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(size)]
+                dist.all_gather(outs, t, group=group)
+                dst = view(recv, nbytes * size)
+                for q, o in enumerate(outs):
+                    dst[q * nbytes:(q + 1) * nbytes] = o.numpy()
+                return 0
+            except Exception:  # pragma: no cover - reported as a library error
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def exchange(ctx, ns, sp, sb, sn, nr, rp, rb, rn):
+            try:
+                reqs, keep, tags = [], [], {}
+                # zero-byte messages are not sent (as with NCCL); the k-th nonzero
+                # message between a pair carries tag k on both sides
+                for i in range(ns):
+                    if sn[i] == 0:
+                        continue
+                    tag = tags.get(("s", sp[i]), 0)
+                    tags[("s", sp[i])] = tag + 1
+                    t = torch.from_numpy(view(sb[i], sn[i]).copy())
+                    keep.append(t)
+                    reqs.append(dist.isend(t, dst=glob(sp[i]), group=group, tag=tag))
+                outs = []
+                for i in range(nr):
+                    if rn[i] == 0:
+                        continue
+                    tag = tags.get(("r", rp[i]), 0)
+                    tags[("r", rp[i])] = tag + 1
+                    t = torch.empty(rn[i], dtype=torch.uint8)
+                    outs.append((i, t))
+                    reqs.append(dist.irecv(t, src=glob(rp[i]), group=group, tag=tag))
+                for r in reqs:
+                    r.wait()
+                for i, t in outs:
+                    view(rb[i], rn[i])[:] = t.numpy()
+                return 0
+            except Exception:  # pragma: no cover
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        cb_ag, cb_ex = _HOST_AG(allgather), _HOST_EX(exchange)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib.ifmm_comm_host_init(int(size), int(rank), ctypes.cast(cb_ag, ctypes.c_void_p),
+                                                ctypes.cast(cb_ex, ctypes.c_void_p), None, ctypes.byref(h)))
+        c = cls(h, rank, size)
+        c._callbacks = (cb_ag, cb_ex)  # the library holds raw pointers to them
+        return c
 
     def selftest(self, n: int = 4096) -> bool:
         """Collective: all-gather + ring send/recv of n doubles through the library's transport."""

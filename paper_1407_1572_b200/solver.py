@@ -150,6 +150,7 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
         _lib.check(_lib.lib.ifmm_factorize(store.handle, float(tol), flags, float(pivot_condition_limit),
                                            ctypes.byref(h)))
     fact = _wrap_factor(store, tree, float(tol), h)
+    fact._comm = comm  # collective solves call back through the communicator
     if diagnostics:
         for k in range(tree.depth, 1, -1):
             s = fact.level_stats[k]

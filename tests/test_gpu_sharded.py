@@ -10,6 +10,8 @@ and the kernels' blocking / worker shapes are chosen from the whole colour
 batch across ranks, so every pivot and fill sees the same arithmetic.  The
 NCCL transport itself is exercised through a 1-rank communicator.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -113,3 +115,31 @@ def test_nccl_transport_one_rank(ifmm):
     x = ifmm.solve(ifmm.factorize(store, tree, comm=comm), b)
     x1 = ifmm.solve(ifmm.factorize(store, tree), b)
     assert np.array_equal(x, x1)
+
+
+def test_two_processes_host_transport(ifmm, tmp_path):
+    """The real multi-process control flow: two processes (torch.distributed.run,
+    gloo) share this GPU and factorize ONE system through the host-staged
+    communicator (Communicator.host: the library's all-gathers and halo
+    exchanges handed to torch.distributed).  Bit-identical to one GPU."""
+    import socket
+    import subprocess
+    import sys
+    n, depth, kern, p, tol = 16384, 4, "log_r", 5, 1e-6
+    tree, store, b = _system(ifmm, n, depth, kern, p, tol)
+    f1 = ifmm.factorize(store, tree, pivot_condition_limit=np.inf)
+    x1 = ifmm.solve(f1, b)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = str(tmp_path / "x.npz")
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "host_transport_worker.py")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", f"--master-port={port}", worker, out, str(n), str(depth),
+                        kern, str(p), str(tol)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    g = np.load(out)
+    assert int(g["nrec"]) < f1.n_records  # rank 0 eliminated only its own subtrees
+    assert int(g["exchanges"]) > 0 and float(g["halo"]) > 0
+    assert int(g["top"]) == f1.top_dim
+    assert np.array_equal(g["x"], x1)
