@@ -339,3 +339,36 @@ def test_dense_fills_beyond_window(ifmm):
     res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
     assert res <= 1e-8, res
     assert sum(s.fillins_dense_kept for s in f.level_stats.values()) > 0
+
+
+REGISTRY = ["log", "laplace3d", "biharmonic", "bessel_y0", "inverse_quadric", "inverse_multiquadric", "helmholtz3d",
+            "gaussian", "multiquadric", "exact_inverse_quadric"]
+
+
+@pytest.mark.parametrize("name", REGISTRY)
+def test_registry_kernels_against_the_reference(ifmm, name):
+    """Every kernel of the reference registry (ifmm/kernels.py:160-170) through IfmmSolver with the
+    reference's regularisation a = 1e-3 at tol = 1e-10, p = 6, N = 4,000 (and inverse-quadric in exact
+    mode, N = 1,024), against the reference's own run (tests/golden/registry_*.npz,
+    oracle/gen_golden_registry.py): residual within 2x the reference's (or 10 tol), or the same
+    SingularPivotError where the reference raises it (biharmonic: cond 5.9e13 at level 2)."""
+    g = load_golden(f"registry_{name}")
+    n = int(g["n"])
+    X = 2.0 * np.random.default_rng(0).random((n, 2)) - 1.0
+    est = ifmm.IfmmSolver(kernel=str(g["kernel"]), a=1e-3, tol=float(g["tol"]), p=int(g["p"]))
+    if str(g["error"]):
+        assert str(g["error"]).startswith("SingularPivotError")
+        with pytest.raises(ifmm.SingularPivotError):
+            est.fit(X)
+        return
+    est.fit(X)
+    assert est.tree_.depth == int(g["depth"])
+    x = est.solve(g["b"])
+    res = np.linalg.norm(est.matvec(x) - g["b"]) / np.linalg.norm(g["b"])
+    print(f"\n{name}: residual {res:.2e} (reference {float(g['resid']):.2e})")
+    # inverse-multiquadric at a = 1e-3 is a nearly singular system (the reference reaches only
+    # 1.3e-3 at tol 1e-10; in colour order 1.9e-3): its fills sit at ACA's tiny-pivot restarts,
+    # where the GPU takes the lowest unused row instead of the reference's random draw (DESIGN.md
+    # section 2), and 28 of ~1,100 keep/compress decisions differ -> bounded at 20x
+    factor = 20.0 if name == "inverse_multiquadric" else 2.0
+    assert res <= max(10 * float(g["tol"]), factor * float(g["resid"])), (res, float(g["resid"]))
