@@ -81,8 +81,11 @@ int ifmm_tree_colours(const ifmm_tree* t, int level, int32_t* colours);
 void ifmm_tree_free(ifmm_tree* t);
 
 /* ---- operators: init_operators(tree, kernel, p, tol) (ifmm/operators.py:164-274)
- * probe_table: (probe_maxm+1) x 10 ACA probe rows (row m = the seeded draw of
- * ifmm/lowrank.py:196-197 for an m-row fill). */
+ * probe_table: (probe_maxm+1) x 22 int32, row m for an m-row fill: the 10 ACA
+ * probe rows of ifmm/lowrank.py:196-197 (np.random.default_rng(0).choice), then
+ * that generator's PCG64 state after the draw (6 x 64-bit little-endian:
+ * state hi, state lo, increment hi, increment lo, has_uint32, uinteger), which
+ * the random restart rows of ifmm/lowrank.py:224-226 continue. */
 int ifmm_store_init(ifmm_tree* t, int kernel_id, double a, double scale, double shift, int p, double tol,
                     const int32_t* probe_table, int probe_maxm, ifmm_store** out);
 int ifmm_store_max_init_rank(const ifmm_store* s, int* r);
@@ -228,7 +231,8 @@ int ifmm_test_gemm(int transA, int transB, int M, int N, int K, double alpha, co
 int ifmm_test_jacobi(double* a, int m, int n, double* v, double* sig);
 /* Householder QR: A (m x k) -> Q (m x k), R (k x k) */
 int ifmm_test_qr(const double* a, int m, int k, double* q, double* r);
-/* ACA + recompression of F (m x n): returns rank, left (m x rank), right (n x rank) */
+/* ACA of F (m x n): returns rank, left (m x rank), right (n x rank); probes = one
+ * 22-int row of the probe table (see ifmm_store_init) */
 int ifmm_test_aca(const double* f, int m, int n, double tol, const int32_t* probes, int kmax, double* left,
                   double* right, int32_t* rank, int32_t* incompressible);
 /* fill compression K1 on one m x n fill (ACA + recompression, ifmm/lowrank.py:137-263):

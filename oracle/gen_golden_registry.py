@@ -14,6 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(HERE))
 import ifmm  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(HERE), "tests", "golden", "registry_{}.npz")
@@ -30,10 +31,18 @@ def run(name, kernel, n, tol, p):
         est = ifmm.IfmmSolver(kernel=kernel, a=1e-3, tol=tol, p=p).fit(X)
         x = est.solve(b)
         res = np.linalg.norm(est.matvec(x) - b) / np.linalg.norm(b)
+        # the same system eliminated in the GPU's colour order by the CPU oracle (a
+        # restatement pinned bit-exactly to the reference in Morton order)
+        from oracle import ifmm_oracle as O
+        spec = O.KernelSpec(kernel, a=1e-3)
+        T = O.build_tree(X, est.tree_.depth)
+        fo = O.factorize(O.init_operators(T, spec, p, tol), order="colour9", on_singular="record")
+        xo = O.solve(fo, b)
+        res9 = np.linalg.norm(O.fmm_matvec(O.init_operators(T, spec, p, tol), xo) - b) / np.linalg.norm(b)
         np.savez_compressed(OUT.format(name), n=n, kernel=kernel, tol=tol, p=p, depth=est.tree_.depth, b=b, x=x,
-                            resid=res, r_m=est.factorization_.r_m, error="")
-        print(f"{name}: residual {res:.2e} r_m {est.factorization_.r_m} depth {est.tree_.depth} "
-              f"({time.perf_counter() - t0:.1f} s)", flush=True)
+                            resid=res, resid_colour9=res9, x_colour9=xo, r_m=est.factorization_.r_m, error="")
+        print(f"{name}: residual {res:.2e} (colour order {res9:.2e}) r_m {est.factorization_.r_m} depth "
+              f"{est.tree_.depth} ({time.perf_counter() - t0:.1f} s)", flush=True)
     except Exception as e:  # the reference's own failure is the expected behaviour
         np.savez_compressed(OUT.format(name), n=n, kernel=kernel, tol=tol, p=p, b=b, error=f"{type(e).__name__}: {e}")
         print(f"{name}: {type(e).__name__}: {e} ({time.perf_counter() - t0:.1f} s)", flush=True)

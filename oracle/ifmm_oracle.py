@@ -295,9 +295,25 @@ def aca_block(F, tol):
     """Partially pivoted ACA + recompression on a dense block.
     Returns (left, right, incompressible).  ifmm/lowrank.py:174-271."""
     m, n = F.shape
-    full = min(m, n)
     if m == 0 or n == 0:
         return np.zeros((m, 0)), np.zeros((n, 0)), False
+    U, V, done = _aca_raw(F, tol)
+    if U.shape[1] == 0:
+        return np.zeros((m, 0)), np.zeros((n, 0)), False
+    L, R = recompress(U, V, tol)
+    return L, R, (not done and U.shape[1] >= min(m, n) and tol > 0)
+
+
+def aca_crosses(F, tol):
+    """The raw ACA crosses (u_t, v_t as columns) before recompression."""
+    U, V, _ = _aca_raw(F, tol)
+    return U, V
+
+
+def _aca_raw(F, tol):
+    """ifmm/lowrank.py:174-263: (crosses U, V, converged)."""
+    m, n = F.shape
+    full = min(m, n)
     rng, probes = aca_probe_rows(m)
     nxt = max((int(i) for i in probes), key=lambda i: np.abs(F[i]).max(initial=0.0))
     us, vs = [], []
@@ -348,9 +364,8 @@ def aca_block(F, tol):
             done = True
             break
     if not us:
-        return np.zeros((m, 0)), np.zeros((n, 0)), False
-    L, R = recompress(np.stack(us, 1), np.stack(vs, 1), tol)
-    return L, R, (not done and len(us) >= full and tol > 0)
+        return np.zeros((m, 0)), np.zeros((n, 0)), done
+    return np.stack(us, 1), np.stack(vs, 1), done
 
 
 # --------------------------------------------------------------------------

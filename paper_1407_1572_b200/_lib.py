@@ -169,17 +169,36 @@ def alloc_output(like, kind: int, rows: int, nrhs: int, one_d: bool):
     return out, ptr(out)
 
 
+ACA_PROBE_STRIDE = 22
+
+
+def aca_probe_row(m: int) -> np.ndarray:
+    """One row of the ACA probe table for an m-row fill: the reference's probe
+    draw np.random.default_rng(0).choice(m, size=min(10, m), replace=False)
+    (ifmm/lowrank.py:196-197), then the PCG64 state it leaves (state, increment
+    as hi/lo 64-bit words, has_uint32, uinteger) -- the stream the reference's
+    random restart rows continue (ifmm/lowrank.py:224-226)."""
+    row = np.zeros(ACA_PROBE_STRIDE, dtype=np.int32)
+    rng = np.random.default_rng(0)
+    d = rng.choice(m, size=min(10, m), replace=False)
+    row[:len(d)] = d
+    st = rng.bit_generator.state
+    mask = (1 << 64) - 1
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    words = np.array([s >> 64, s & mask, inc >> 64, inc & mask, st["has_uint32"], st["uinteger"]], dtype=np.uint64)
+    row[10:] = words.view(np.int32)
+    return row
+
+
 def aca_probe_table(maxm: int = 4096) -> np.ndarray:
-    """Probe rows of the reference's ACA for every fill height m <= maxm:
-    numpy's default_rng(0).choice(m, size=min(10, m), replace=False), exactly
-    as ifmm/lowrank.py:196-197 draws them."""
+    """Probe rows (+ generator state) of the reference's ACA for every fill
+    height m <= maxm (rows of aca_probe_row)."""
     global _PROBES
     if _PROBES is not None and _PROBES.shape[0] > maxm:
         return _PROBES
-    tab = np.zeros((maxm + 1, 10), dtype=np.int32)
+    tab = np.zeros((maxm + 1, ACA_PROBE_STRIDE), dtype=np.int32)
     for m in range(1, maxm + 1):
-        d = np.random.default_rng(0).choice(m, size=min(10, m), replace=False)
-        tab[m, :len(d)] = d
+        tab[m] = aca_probe_row(m)
     _PROBES = tab
     return tab
 

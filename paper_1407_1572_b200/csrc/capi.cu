@@ -711,10 +711,10 @@ int ifmm_test_aca(const double* f, int m, int n, double tol, const int32_t* prob
     double* df = ws.alloc_n<double>(size_t(m) * n);
     double *du = ws.alloc_n<double>(size_t(m) * kmax), *dv = ws.alloc_n<double>(size_t(n) * kmax);
     double* scr = ws.alloc_n<double>(size_t(2) * (m + n) + kmax + 16);
-    int* dp = ws.alloc_n<int>(10);
+    int* dp = ws.alloc_n<int>(ifmm::ACA_PROBE_STRIDE);
     int* dout = ws.alloc_n<int>(2);
     CK(cudaMemcpy(df, f, sizeof(double) * m * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dp, probes, sizeof(int) * std::min(10, m), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dp, probes, sizeof(int) * ifmm::ACA_PROBE_STRIDE, cudaMemcpyHostToDevice));
     TEST_LAUNCH(test_aca_kernel, df, m, n, tol, dp, kmax, du, dv, scr, dout);
     CK_LAUNCH();
     CK(cudaDeviceSynchronize());
@@ -738,10 +738,11 @@ int ifmm_test_recompress(const double* f, int m, int n, double tol, const int32_
     const int kf = std::max(1, std::min(96, std::min(m, n)));
     double* df = ws.alloc_n<double>(size_t(m) * n);
     double* dout = ws.alloc_n<double>(size_t(m + n + 1) * kf);
-    int* dp = ws.alloc_n<int>(size_t(m + 1) * 10);  // probe table: row m only
+    const size_t PS = ifmm::ACA_PROBE_STRIDE;
+    int* dp = ws.alloc_n<int>(size_t(m + 1) * PS);  // probe table: row m only
     auto* dstate = ws.alloc_n<ifmm::FillState>(1);
-    std::vector<int> tab(size_t(m + 1) * 10, 0);
-    for (int t = 0; t < std::min(10, m); t++) tab[size_t(m) * 10 + t] = probes[t];
+    std::vector<int> tab(size_t(m + 1) * PS, 0);
+    for (size_t t = 0; t < PS; t++) tab[size_t(m) * PS + t] = probes[t];
     CK(cudaMemcpy(df, f, sizeof(double) * m * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dp, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
     ifmm::test_recompress_one(df, m, n, tol, dp, m, gram, dout, dstate, ws, st, s);

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
     const int mrow = rows < probe_maxm ? rows : probe_maxm;
     const int kmax = min(D.Kf, KK);
     if (g_prof_on) _pt = clock64();
-    AcaOut ao = g_aca(g, D.F, D.ldF, D.transF, rows, cols, tol, probes + (size_t)mrow * 10, min(10, rows), Uc, Vc,
+    AcaOut ao = g_aca(g, D.F, D.ldF, D.transF, rows, cols, tol, probes + (size_t)mrow * ACA_PROBE_STRIDE, min(10, rows), Uc, Vc,
                       kmax, rr, cc, usedr, usedc, dots, g_gram ? Rl : nullptr, g_gram ? Rr : nullptr, KK);
     PROF_ACC(0);
     k = ao.k;

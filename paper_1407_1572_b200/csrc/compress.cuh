@@ -18,6 +18,13 @@ namespace ifmm {
 
 enum FillKind : int { FILL_HYBRID = 0, FILL_P2P = 1 };
 
+// One row per fill height m of the ACA probe table: the reference's 10 probe
+// rows (np.random.default_rng(0).choice(m, min(10, m), replace=False),
+// ifmm/lowrank.py:196-197), then that generator's PCG64 state after the draw
+// (6 x 64 bits: state hi/lo, increment hi/lo, has_uint32, uinteger) for the
+// random restart rows (ifmm/lowrank.py:224-226).
+constexpr int ACA_PROBE_STRIDE = 22;
+
 struct FillDesc {
   int kind, p, q;
   double* F;    // fill block; F(a,b) = transF ? F[b + a*ldF] : F[a + b*ldF]

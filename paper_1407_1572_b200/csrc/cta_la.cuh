@@ -408,6 +408,53 @@ __device__ inline double Fat(const double* F, int ld, int trans, int a, int b) {
   return trans ? F[b + (size_t)a * ld] : F[a + (size_t)b * ld];
 }
 
+// numpy's PCG64 (the reference's np.random.default_rng(0) stream, continued
+// after the probe-row draw): 128-bit LCG step, XSL-RR output, 32-bit draws
+// buffered from 64-bit outputs, and Generator.integers(0, k)'s Lemire bounded
+// draw.  Every thread steps its own copy identically.
+struct Pcg64 {
+  unsigned long long shi, slo, ihi, ilo;
+  unsigned long long has, u;
+  __device__ unsigned long long next64() {
+    const unsigned long long mhi = 0x2360ed051fc65da4ull, mlo = 0x4385df649fccf645ull;
+    const unsigned long long lo = slo * mlo;
+    const unsigned long long hi = __umul64hi(slo, mlo) + slo * mhi + shi * mlo;
+    slo = lo + ilo;
+    shi = hi + ihi + (slo < lo ? 1ull : 0ull);
+    const unsigned long long x = shi ^ slo;
+    const unsigned r = unsigned(shi >> 58);
+    return (x >> r) | (x << ((64u - r) & 63u));
+  }
+  __device__ unsigned next32() {
+    if (has) {
+      has = 0;
+      return unsigned(u);
+    }
+    const unsigned long long v = next64();
+    has = 1;
+    u = v >> 32;
+    return unsigned(v & 0xffffffffull);
+  }
+  // Generator.integers(0, k), k <= 2^32 (rng.choice over a list of k rows)
+  __device__ unsigned bounded(unsigned k) {
+    const unsigned rng = k - 1;
+    if (rng == 0) return 0;
+    const unsigned long long ex = (unsigned long long)rng + 1ull;
+    unsigned long long mm = (unsigned long long)next32() * ex;
+    unsigned long long left = mm & 0xffffffffull;
+    if (left < ex) {
+      const unsigned long long thr = (0xffffffffull - rng) % ex;
+      while (left < thr) {
+        mm = (unsigned long long)next32() * ex;
+        left = mm & 0xffffffffull;
+      }
+    }
+    return unsigned(mm >> 32);
+  }
+};
+
+// probes: one row of the ACA probe table (ACA_PROBE_STRIDE ints): the 10
+// probe rows, then the PCG64 state after drawing them (6 x 64 bits)
 template <class G>
 __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, int m, int n, double tol,
                                  const int* probes, int nprobe, double* Uc, double* Vc, int kmax, double* rr,
@@ -452,6 +499,11 @@ __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, i
   int k = 0, strikes = 0, nused = 0;
   double nsq = 0.0;
   bool done = false;
+  Pcg64 rng;
+  {
+    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(probes + 10);
+    rng = Pcg64{w[0], w[1], w[2], w[3], w[4], w[5]};
+  }
   const int kcap = min(full, kmax);
   while (k < kcap) {
     const int i = next;
@@ -476,13 +528,19 @@ __device__ inline AcaOut g_aca(const G& g, const double* F, int ld, int trans, i
         done = true;
         break;
       }
-      // deterministic substitute for the reference's random restart row
-      // (ifmm/lowrank.py:224-226): the lowest-index unused row.  (Restarting
-      // at the unused row holding the largest remaining entry was measured
-      // worse: reference defaults at N = 8,000 went from 9e-14 to 4e-10.)
+      // the reference's random restart row (ifmm/lowrank.py:224-226):
+      // rng.choice over the unused rows in ascending order, drawn from the
+      // same PCG64 stream -> the idx-th unused row
+      const unsigned idx = rng.bounded(unsigned(m - nused));
       ArgMax lo{-1.0, -1};
-      for (int r = g.rank(); r < m; r += g.size())
-        if (!usedr[r]) lo = argmax_merge(lo, ArgMax{1.0, r});
+      if (g.rank() == 0) {
+        unsigned c = 0;
+        for (int r = 0; r < m; r++)
+          if (!usedr[r] && c++ == idx) {
+            lo = ArgMax{1.0, r};
+            break;
+          }
+      }
       lo = g.argmax(lo);
       next = lo.i;
       if (next < 0) {

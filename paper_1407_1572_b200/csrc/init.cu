@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "compress.cuh"
 #include "core.cuh"
 #include "cta_la.cuh"
 
@@ -312,7 +313,7 @@ StoreH* store_init(TreeH* t, const KernelParams& kp, int p, double tol, const in
   Arena ws(size_t(256) << 20);
   Staging st;
   const int dim = t->dim, K = t->depth;
-  S->probe_tab.assign(probe_tab, probe_tab + size_t(probe_maxm + 1) * 10);
+  S->probe_tab.assign(probe_tab, probe_tab + size_t(probe_maxm + 1) * ACA_PROBE_STRIDE);
   S->probe_maxm = probe_maxm;
   S->d_probe = S->arena.alloc_n<int>(S->probe_tab.size());
   CK(cudaMemcpyAsync(S->d_probe, S->probe_tab.data(), sizeof(int) * S->probe_tab.size(), cudaMemcpyHostToDevice, s));

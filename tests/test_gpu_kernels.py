@@ -243,13 +243,13 @@ def test_aca_matches_oracle_crosses(L, group, m, n, rank):
     from oracle import ifmm_oracle as O
     rng = np.random.default_rng(m + n)
     F = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n)) * np.logspace(0, -6, n)
-    _, probes = O.aca_probe_rows(m)
+    probes = L.aca_probe_row(m)
     kmax = min(m, n)
     left = np.empty((m, kmax), order="F")
     right = np.empty((n, kmax), order="F")
     rk = np.zeros(1, dtype=np.int32)
     inc = np.zeros(1, dtype=np.int32)
-    L.check(L.lib.ifmm_test_aca(L.ptr(np.asfortranarray(F)), m, n, 1e-8, L.ptr(probes.astype(np.int32)), kmax,
+    L.check(L.lib.ifmm_test_aca(L.ptr(np.asfortranarray(F)), m, n, 1e-8, L.ptr(probes), kmax,
                                 L.ptr(left), L.ptr(right), L.ptr(rk), L.ptr(inc)))
     k = int(rk[0])
     approx = left[:, :k] @ right[:, :k].T
@@ -257,6 +257,35 @@ def test_aca_matches_oracle_crosses(L, group, m, n, rank):
     Lo, Ro, bad = O.aca_block(F, 1e-8)
     assert not bad and not inc[0]
     assert abs(k - Lo.shape[1]) <= 2
+
+
+@pytest.mark.parametrize("m,n,seed", [(30, 40, 1), (90, 60, 2), (240, 200, 3)])
+def test_aca_random_restarts_match_the_reference(L, group, m, n, seed):
+    """Two uncoupled low-rank blocks separated by zero rows: once the first block is
+    exhausted ACA meets zero pivots and restarts from random unused rows
+    (ifmm/lowrank.py:224-226).  The device draws them from the same PCG64 stream
+    (probe-table state + Generator.integers' bounded draw), so the crosses are the
+    oracle's (= the reference's) row for row -- restarting at the lowest unused row
+    instead finds 3 crosses where the reference finds 7."""
+    from oracle import ifmm_oracle as O
+    rng = np.random.default_rng(seed)
+    q = m // 3
+    F = np.zeros((m, n))
+    F[:q, :n // 2] = rng.standard_normal((q, 3)) @ rng.standard_normal((3, n // 2))
+    F[2 * q:, n // 2:] = rng.standard_normal((m - 2 * q, 4)) @ rng.standard_normal((4, n - n // 2))
+    probes = L.aca_probe_row(m)
+    kmax = min(m, n)
+    left = np.zeros((m, kmax), order="F")
+    right = np.zeros((n, kmax), order="F")
+    rk = np.zeros(1, dtype=np.int32)
+    inc = np.zeros(1, dtype=np.int32)
+    L.check(L.lib.ifmm_test_aca(L.ptr(np.asfortranarray(F)), m, n, 1e-8, L.ptr(probes), kmax, L.ptr(left),
+                                L.ptr(right), L.ptr(rk), L.ptr(inc)))
+    k = int(rk[0])
+    Lo, Ro = O.aca_crosses(F, 1e-8)
+    assert k == Lo.shape[1] > 0, (k, Lo.shape[1])
+    assert np.allclose(left[:, :k], Lo, rtol=1e-12, atol=1e-12 * np.abs(Lo).max())
+    assert np.allclose(right[:, :k], Ro, rtol=1e-12, atol=1e-12 * np.abs(Ro).max())
 
 
 @pytest.mark.parametrize("m,n,rank,decay", [(64, 64, 8, 1e-3), (90, 40, 12, 1e-5), (200, 150, 20, 1e-2),
@@ -269,7 +298,7 @@ def test_fill_recompression_gram_vs_householder(L, m, n, rank, decay):
     rng = np.random.default_rng(m * n + rank)
     s = np.logspace(0, np.log10(decay), rank)
     F = (rng.standard_normal((m, rank)) * s) @ rng.standard_normal((rank, n))
-    _, probes = O.aca_probe_rows(m)
+    probes = L.aca_probe_row(m)
     tol = 1e-6
     out = {}
     for gram in (1, 0):
@@ -280,7 +309,7 @@ def test_fill_recompression_gram_vs_householder(L, m, n, rank, decay):
         rk = np.zeros(1, dtype=np.int32)
         st = np.zeros(1, dtype=np.int32)
         L.check(L.lib.ifmm_test_recompress(L.ptr(np.asfortranarray(F)), m, n, tol,
-                                           L.ptr(probes.astype(np.int32)), gram, L.ptr(left), L.ptr(right),
+                                           L.ptr(probes), gram, L.ptr(left), L.ptr(right),
                                            L.ptr(sv), L.ptr(rk), L.ptr(st)))
         r = int(rk[0])
         assert st[0] == 0

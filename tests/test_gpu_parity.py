@@ -365,10 +365,14 @@ def test_registry_kernels_against_the_reference(ifmm, name):
     assert est.tree_.depth == int(g["depth"])
     x = est.solve(g["b"])
     res = np.linalg.norm(est.matvec(x) - g["b"]) / np.linalg.norm(g["b"])
-    print(f"\n{name}: residual {res:.2e} (reference {float(g['resid']):.2e})")
+    ref = max(float(g["resid"]), float(g["resid_colour9"]))  # the reference's Morton run, the oracle's colour run
+    xd = np.linalg.norm(x - g["x_colour9"]) / np.linalg.norm(g["x_colour9"])
+    print(f"\n{name}: residual {res:.2e} (reference {float(g['resid']):.2e}, colour order "
+          f"{float(g['resid_colour9']):.2e}), solution vs colour order {xd:.1e}")
     # inverse-multiquadric at a = 1e-3 is a nearly singular system (the reference reaches only
-    # 1.3e-3 at tol 1e-10; in colour order 1.9e-3): its fills sit at ACA's tiny-pivot restarts,
-    # where the GPU takes the lowest unused row instead of the reference's random draw (DESIGN.md
-    # section 2), and 28 of ~1,100 keep/compress decisions differ -> bounded at 20x
-    factor = 20.0 if name == "inverse_multiquadric" else 2.0
-    assert res <= max(10 * float(g["tol"]), factor * float(g["resid"])), (res, float(g["resid"]))
+    # 1.3e-3 at tol 1e-10, 1.9e-3 in colour order): 28 of ~1,100 keep/compress decisions of its
+    # near-noise fills differ from the same-order oracle's -> bounded at 15x
+    factor = 15.0 if name == "inverse_multiquadric" else 2.0
+    assert res <= max(10 * float(g["tol"]), factor * ref), (res, ref)
+    if not name.startswith(("inverse", "exact")):  # G4 where the system is well conditioned (measured <= 2e-13)
+        assert xd <= 1e-9, xd

@@ -61,6 +61,24 @@ def test_probe_table_matches_reference_draw():
         assert list(tab[m, :len(probes)]) == [int(v) for v in probes]
 
 
+def test_probe_table_carries_the_generator_state():
+    """Rows of the probe table continue the reference's generator: a Generator rebuilt
+    from the stored PCG64 words draws what np.random.default_rng(0) draws after the probe
+    choice (the random ACA restart rows, ifmm/lowrank.py:224-226)."""
+    from paper_1407_1572_b200 import _lib
+    for m in (1, 7, 10, 64, 513):
+        row = _lib.aca_probe_row(m)
+        w = [int(x) for x in row[10:].view(np.uint64)]
+        g = np.random.Generator(np.random.PCG64())
+        g.bit_generator.state = {"bit_generator": "PCG64", "state": {"state": (w[0] << 64) | w[1],
+                                                                     "inc": (w[2] << 64) | w[3]},
+                                 "has_uint32": w[4], "uinteger": w[5]}
+        ref = np.random.default_rng(0)
+        ref.choice(m, size=min(10, m), replace=False)
+        for k in (1, 2, 5, m, 3 * m + 1):
+            assert g.choice(list(range(k))) == ref.choice(list(range(k)))
+
+
 def test_kernel_host_eval_matches_oracle():
     import paper_1407_1572_b200 as ifmm
     from oracle import ifmm_oracle as O
