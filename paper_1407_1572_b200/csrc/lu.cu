@@ -682,30 +682,59 @@ __device__ __forceinline__ void xchunk_next(XChunk& c, int nb, const unsigned ch
     else { c.k--; c.j = nb - 1; }
   }
 }
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(pred ? gmem : nullptr), "r"(n));
+}
+// Stage half h of block (k, j) -- a 64-row x 32-column slab -- as As[kk * XS_AP + row].
+// Thread t copies rows 2 (t & 31), +1 of columns (t >> 5) + 8 q, q < 4: 16-byte
+// copies when both rows are in range and the pair is 16-byte aligned (always for
+// the diagonal inverses; for the factor when m or the column is even), else two
+// 8-byte copies.  Address arithmetic is incremental in q.
 __device__ __forceinline__ void xchunk_load(double* As, const XChunk& c, const double* __restrict__ LU,
                                             const double* __restrict__ dg, int m, int tid) {
-  const int r = tid & (XB - 1);
+  const int r = 2 * (tid & 31), kk0 = tid >> 5;
+  double* dst = As + kk0 * XS_AP + r;
+  if (c.j == c.k && c.p != 1) {
+    const double* src = dg + (size_t)c.k * 2 * XB * XB + (c.bwd ? XB * XB : 0) + r + (size_t)XB * (32 * c.h + kk0);
 #pragma unroll
-  for (int q = 0; q < XB * 32 / 256; q++) {
-    const int kk = (tid / XB) + (256 / XB) * q;
-    const double* src;
-    bool ok;
-    if (c.j == c.k && c.p != 1) {
-      src = dg + (size_t)c.k * 2 * XB * XB + (c.bwd ? XB * XB : 0) + r + (size_t)XB * (32 * c.h + kk);
-      ok = true;
-    } else {  // a factor block, or the diagonal block T_kk itself (p == 1)
-      const int row = XB * c.k + r, col = XB * c.j + 32 * c.h + kk;
-      ok = row < m && col < m;
-      src = LU + row + (size_t)col * m;
+    for (int q = 0; q < 4; q++) cp_async16(dst + 8 * q * XS_AP, src + 8 * q * XB, true);
+    return;
+  }
+  // a factor block, or the diagonal block T_kk itself (p == 1)
+  const int row = XB * c.k + r, col0 = XB * c.j + 32 * c.h + kk0;
+  const bool r0ok = row < m, r1ok = row + 1 < m;
+  const bool diag = c.j == c.k;
+  const double* src = LU + row + (size_t)col0 * m;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int col = col0 + 8 * q;
+    const double* s_ = src + (size_t)8 * q * m;
+    double* d_ = dst + 8 * q * XS_AP;
+    bool ok0 = r0ok && col < m, ok1 = r1ok && col < m;
+    if (diag) {
+      // T_kk is triangular: keep only its own part (L strictly below / U on and above);
       // the unit diagonal of L is implicit in the LU storage
-      if (c.j == c.k && !c.bwd && row == col) {
-        As[kk * XS_AP + r] = ok ? 1.0 : 0.0;
-        continue;
+      if (c.bwd) {
+        ok0 &= row <= col;
+        ok1 &= row + 1 <= col;
+      } else {
+        ok0 &= row >= col;
+        ok1 &= row + 1 >= col;
       }
-      // T_kk is triangular: keep only its own part (L strictly below / U on and above)
-      if (c.j == c.k && (c.bwd ? row > col : row < col)) ok = false;
     }
-    cp_async8(As + kk * XS_AP + r, src, ok);
+    if (diag && !c.bwd) {  // L_kk: the unit diagonal is stored directly (no copy to that slot)
+      if (row == col) d_[0] = ok0 ? 1.0 : 0.0;
+      else cp_async8(d_, s_, ok0);
+      if (row + 1 == col) d_[1] = ok1 ? 1.0 : 0.0;
+      else cp_async8(d_ + 1, s_ + 1, ok1);
+    } else if (ok0 && ok1 && ((reinterpret_cast<uintptr_t>(s_) & 15) == 0)) {
+      cp_async16(d_, s_, true);
+    } else {
+      cp_async8(d_, s_, ok0);
+      cp_async8(d_ + 1, s_ + 1, ok1);
+    }
   }
 }
 
@@ -833,12 +862,11 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
   }
   cp_async_wait<0>();
   __syncthreads();
-  for (int e = tid; e < TW * m; e += 256) {
-    const int c = e / m, l = e - c * m, col = c0 + c;
-    if (col >= w) continue;
-    const double v = X[(size_t)c * xm + l];
-    if (l < n) D.Xtop[l + (size_t)col * n] = v;
-    else D.Xbot[(l - n) + (size_t)col * D.r] = v;
+  for (int c = 0; c < TW && c0 + c < w; c++) {
+    const int col = c0 + c;
+    const double* x = X + (size_t)c * xm;
+    for (int l = tid; l < n; l += 256) D.Xtop[l + (size_t)col * n] = x[l];
+    for (int l = n + tid; l < m; l += 256) D.Xbot[(l - n) + (size_t)col * D.r] = x[l];
   }
 }
 
