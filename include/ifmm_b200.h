@@ -132,6 +132,17 @@ int ifmm_factor_level_cond(const ifmm_factor* f, int level, double* max_cond);
  * are written as (level, index, cond) in elimination order (arrays may be null) */
 int ifmm_factor_singular(const ifmm_factor* f, int64_t cap, int32_t* level, int32_t* index, double* cond,
                          int64_t* count);
+/* record idx (elimination order) -- the reference's _Record (ifmm/solver.py:63-74):
+ * info7 = level, index, n, r, w, #x partners, #y partners; xp / yp (may be null)
+ * receive the partner cluster indices */
+int ifmm_factor_record(const ifmm_factor* f, int64_t idx, int32_t* info7, int32_t* xp, int32_t* yp);
+/* its pivot factors: lu ((n+r) x (n+r), column-major, L unit lower + U) and perm
+ * (row l of P S is row perm[l] of S) -- the reference keeps scipy lu_factor's (lu, piv) */
+int ifmm_factor_record_lu(const ifmm_factor* f, int64_t idx, double* lu, int32_t* perm);
+/* the level-2 top system's LU (top_dim^2, column-major) + perm, and the offsets
+ * of the level-2 clusters in it (4^2 + 1 in 2-D) -- IfmmFactorization.top_lu /
+ * top_offsets (ifmm/solver.py:85-98, 528-546) */
+int ifmm_factor_top(const ifmm_factor* f, double* lu, int32_t* perm, int64_t* offsets);
 /* per elimination (in order): level, index, n, r, w */
 int ifmm_factor_records(const ifmm_factor* f, int32_t* out5);
 /* work accounting: out[0] executed FP64 flops (pivot LU, X = S^-1 C, symmetric

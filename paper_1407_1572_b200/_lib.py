@@ -64,6 +64,9 @@ SIGNATURES = {
     "ifmm_factor_level_stats": (_i32, [_p, _i32, _p]),
     "ifmm_factor_level_cond": (_i32, [_p, _i32, _pd]),
     "ifmm_factor_singular": (_i32, [_p, _i64, _p, _p, _p, _pi64]),
+    "ifmm_factor_record": (_i32, [_p, _i64, _p, _p, _p]),
+    "ifmm_factor_record_lu": (_i32, [_p, _i64, _p, _p]),
+    "ifmm_factor_top": (_i32, [_p, _p, _p, _p]),
     "ifmm_factor_records": (_i32, [_p, _p]),
     "ifmm_factor_work": (_i32, [_p, _p]),
     "ifmm_factor_timing": (_i32, [_p, _p, _p]),

@@ -330,6 +330,45 @@ int ifmm_factor_singular(const ifmm_factor* f, int64_t cap, int32_t* level, int3
   });
 }
 
+int ifmm_factor_record(const ifmm_factor* f, int64_t idx, int32_t* info7, int32_t* xp, int32_t* yp) {
+  return guard([&] {
+    const FactorH& F = *f->h;
+    if (idx < 0 || idx >= int64_t(F.recs.size())) invalid("record index out of range");
+    const RecordH& R = F.recs[size_t(idx)];
+    const auto& X = F.rec_xp[size_t(idx)];
+    const auto& Y = F.rec_yp[size_t(idx)];
+    if (info7) {
+      const int32_t v[7] = {R.level, R.index, R.n, R.r, R.w, int32_t(X.size()), int32_t(Y.size())};
+      memcpy(info7, v, sizeof v);
+    }
+    if (xp) std::copy(X.begin(), X.end(), xp);
+    if (yp) std::copy(Y.begin(), Y.end(), yp);
+  });
+}
+
+int ifmm_factor_record_lu(const ifmm_factor* f, int64_t idx, double* lu, int32_t* perm) {
+  return guard([&] {
+    const FactorH& F = *f->h;
+    if (idx < 0 || idx >= int64_t(F.recs.size())) invalid("record index out of range");
+    const RecordH& R = F.recs[size_t(idx)];
+    const size_t m = size_t(R.n + R.r);
+    CK(cudaStreamSynchronize(F.stream));
+    if (lu && m) CK(cudaMemcpy(lu, R.lu, sizeof(double) * m * m, cudaMemcpyDeviceToHost));
+    if (perm && m) CK(cudaMemcpy(perm, R.perm, sizeof(int) * m, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifmm_factor_top(const ifmm_factor* f, double* lu, int32_t* perm, int64_t* offsets) {
+  return guard([&] {
+    const FactorH& F = *f->h;
+    const size_t M = size_t(F.top_dim);
+    CK(cudaStreamSynchronize(F.stream));
+    if (lu && M) CK(cudaMemcpy(lu, F.top_lu, sizeof(double) * M * M, cudaMemcpyDeviceToHost));
+    if (perm && M) CK(cudaMemcpy(perm, F.top_perm, sizeof(int) * M, cudaMemcpyDeviceToHost));
+    if (offsets) std::copy(F.top_off.begin(), F.top_off.end(), offsets);
+  });
+}
+
 int ifmm_factor_records(const ifmm_factor* f, int32_t* out5) {
   return guard([&] {
     size_t u = 0;

@@ -216,6 +216,10 @@ struct FactorH {
   long long phase_launches[8] = {0};
   int deferred_batches = 0;  // colour batches split by the independence guard
   std::vector<SingularH> singular;  // IFMM_FLAG_RECORD_SINGULAR: pivots over the limit, in elimination order
+  // per record (host): the x / y partners of the elimination (the reference's
+  // _Record.x_partners / y_partners, ifmm/solver.py:63-74)
+  std::vector<std::vector<int>> rec_xp, rec_yp;
+  std::vector<int64_t> top_off;  // offsets of the level-2 clusters in the top system
   std::vector<std::array<double, 8>> phase_lvl_ms;  // [level][phase]
   std::vector<std::array<double, 2>> host_lvl_ms;   // [level]: host busy until the final sync, time blocked in it
   // sharded factorization (null / 1 rank otherwise): the communicator the

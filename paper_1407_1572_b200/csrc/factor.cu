@@ -732,6 +732,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       for (int j : I.yp) sl.push_back({1, j, W.r[j]});
       sl.push_back({1, I.i, I.r});
       rec_slots_.push_back(sl);
+      F_->rec_xp.push_back(I.xp);
+      F_->rec_yp.push_back(I.yp);
       {
         const double m = I.m, n = I.n, w = I.w, h = I.w - I.r;
         F_->fl_exec += 2.0 / 3.0 * m * m * m + 2.0 * m * m * w;
@@ -1190,6 +1192,7 @@ void Factorizer::factor_top() {
   for (int i = 0; i < W.nc; i++) off[i + 1] = off[i] + W.r[i];
   const int M = int(off[W.nc]);
   F_->top_dim = M;
+  F_->top_off = off;
   ws_.reset();
   st_.reset();
   F_->top_lu = F_->arena.alloc_n<double>(size_t(std::max(1, M)) * std::max(1, M));

@@ -33,13 +33,55 @@ class LevelStats:
     fillins_dense_kept: int = 0
 
 
-@dataclass
+def _perm_to_piv(perm: np.ndarray) -> np.ndarray:
+    """Row permutation (row l of P S = row perm[l] of S) -> LAPACK getrf pivots
+    (row l was interchanged with row piv[l], applied in order), as scipy's
+    lu_factor returns them."""
+    m = len(perm)
+    cur = np.arange(m)
+    where = np.arange(m)
+    piv = np.empty(m, dtype=np.int32)
+    for l in range(m):
+        p = where[perm[l]]
+        piv[l] = p
+        a, b = cur[l], cur[p]
+        cur[l], cur[p] = b, a
+        where[b], where[a] = l, p
+    return piv
+
+
 class Record:
-    level: int
-    index: int
-    n: int
-    r: int
-    w: int
+    """One cluster elimination (the reference's _Record, ifmm/solver.py:63-74).
+    `lu` is scipy lu_factor's (lu, piv) of the pivot block S, downloaded on
+    first access; z_partners equal y_partners (the stored system is symmetric:
+    the local rows referencing x_i belong to the partners it couples through M2P)."""
+
+    __slots__ = ("_fact", "_idx", "level", "index", "n", "r", "w", "x_partners", "y_partners", "_lu")
+
+    def __init__(self, fact, idx, info, xp, yp):
+        self._fact, self._idx = fact, idx
+        self.level, self.index, self.n, self.r, self.w = map(int, info[:5])
+        self.x_partners = [int(v) for v in xp]
+        self.y_partners = [int(v) for v in yp]
+        self._lu = None
+
+    @property
+    def z_partners(self) -> list:
+        return list(self.y_partners)
+
+    @property
+    def lu(self) -> tuple:
+        if self._lu is None:
+            m = self.n + self.r
+            a = np.empty((m, m))  # column-major m x m = a.T
+            perm = np.empty(m, dtype=np.int32)
+            _lib.check(_lib.lib.ifmm_factor_record_lu(self._fact.handle, self._idx, _lib.ptr(a), _lib.ptr(perm)))
+            self._lu = (np.ascontiguousarray(a.T), _perm_to_piv(perm))
+        return self._lu
+
+    def __repr__(self):
+        return (f"Record(level={self.level}, index={self.index}, n={self.n}, r={self.r}, w={self.w}, "
+                f"x_partners={self.x_partners}, y_partners={self.y_partners})")
 
 
 @dataclass
@@ -65,9 +107,33 @@ class IfmmFactorization:
 
     @property
     def records(self) -> list:
-        out = np.empty((self.n_records, 5), dtype=np.int32)
-        _lib.check(_lib.lib.ifmm_factor_records(self.handle, _lib.ptr(out)))
-        return [Record(*map(int, row)) for row in out]
+        """Eliminations in order (ifmm/solver.py:63-74 _Record); a sharded
+        factorization lists this rank's own."""
+        out = []
+        info = np.zeros(7, dtype=np.int32)
+        for idx in range(self.n_records):
+            _lib.check(_lib.lib.ifmm_factor_record(self.handle, idx, _lib.ptr(info), None, None))
+            xp = np.zeros(max(1, int(info[5])), dtype=np.int32)
+            yp = np.zeros(max(1, int(info[6])), dtype=np.int32)
+            _lib.check(_lib.lib.ifmm_factor_record(self.handle, idx, _lib.ptr(info), _lib.ptr(xp), _lib.ptr(yp)))
+            out.append(Record(self, idx, info.copy(), xp[:info[5]], yp[:info[6]]))
+        return out
+
+    @property
+    def top_lu(self) -> tuple:
+        """scipy lu_factor-style (lu, piv) of the level-2 top system (ifmm/solver.py:528-546)."""
+        m = self.top_dim
+        a = np.empty((m, m))
+        perm = np.empty(max(1, m), dtype=np.int32)
+        _lib.check(_lib.lib.ifmm_factor_top(self.handle, _lib.ptr(a), _lib.ptr(perm), None))
+        return np.ascontiguousarray(a.T), _perm_to_piv(perm[:m])
+
+    @property
+    def top_offsets(self) -> np.ndarray:
+        """Offsets of the level-2 clusters in the top system (IfmmFactorization.top_offsets)."""
+        off = np.zeros((1 << (2 * self.tree.dim)) + 1, dtype=np.int64)
+        _lib.check(_lib.lib.ifmm_factor_top(self.handle, None, None, _lib.ptr(off)))
+        return off
 
     @property
     def work(self) -> dict:

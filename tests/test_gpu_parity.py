@@ -376,3 +376,37 @@ def test_registry_kernels_against_the_reference(ifmm, name):
     assert res <= max(10 * float(g["tol"]), factor * ref), (res, ref)
     if not name.startswith(("inverse", "exact")):  # G4 where the system is well conditioned (measured <= 2e-13)
         assert xd <= 1e-9, xd
+
+
+def test_records_and_top_system_match_the_oracle(ifmm):
+    """fact.records mirror the reference's _Record list (ifmm/solver.py:63-74) and
+    top_lu / top_offsets its IfmmFactorization fields (:85-98): same elimination
+    sequence and leaf partner lists as the oracle in the same (colour) order, each
+    record's lu a scipy (lu, piv) pair of the pivot block (symmetric saddle point,
+    zero local-local block), and the top LU inverts the top system."""
+    from scipy.linalg import lu_solve
+    from oracle import ifmm_oracle as O
+    g, pts, tree = _setup(ifmm, "c1_invr")
+    tol = float(g["tol"])
+    store = ifmm.init_operators(tree, _kernel(ifmm, g), p=int(g["p"]), tol=tol)
+    fact = ifmm.factorize(store, tree)
+    recs = fact.records
+    T = O.build_tree(pts, int(g["depth"]))
+    fo = O.factorize(O.init_operators(T, golden_kernel(g), int(g["p"]), tol), order="colour9")
+    assert [(r.level, r.index) for r in recs] == [(r.level, r.index) for r in fo.recs]
+    for r, ro in zip(recs, fo.recs):
+        if r.level == int(g["depth"]):
+            assert r.n == ro.n
+            assert sorted(r.x_partners) == sorted(ro.xp) and sorted(r.y_partners) == sorted(ro.yp)
+    for r in recs[:5] + recs[-3:]:
+        lu, piv = r.lu
+        m = r.n + r.r
+        e = np.eye(m)
+        S = np.linalg.inv(lu_solve((lu, piv), e))  # the pivot block itself
+        assert np.allclose(S, S.T, atol=1e-9 * np.abs(S).max())
+        assert np.abs(S[r.n:, r.n:]).max() <= 1e-9 * np.abs(S).max()
+    lu, piv = fact.top_lu
+    off = fact.top_offsets
+    assert off[0] == 0 and off[-1] == fact.top_dim == lu.shape[0]
+    A = np.linalg.inv(lu_solve((lu, piv), np.eye(fact.top_dim)))
+    assert np.allclose(A, A.T, atol=1e-8 * np.abs(A).max())
