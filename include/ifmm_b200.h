@@ -98,6 +98,14 @@ int ifmm_store_m2l(const ifmm_store* s, int level, int i, int j, double* out);
 /* leaf near-field block P2P(i, j) (n_i x n_j, column-major) of neighbour pair
  * (i, j) (OperatorStore.p2p, ifmm/operators.py:180-194; stored once per pair) */
 int ifmm_store_p2p(const ifmm_store* s, int i, int j, double* out);
+/* test hook: overwrite the store's initial operators with blocks
+ * built elsewhere -- e.g. the reference's own OperatorStore (ifmm/operators.py:42-137)
+ * -- so the elimination can be checked on bit-identical inputs.  Same shapes and
+ * layouts as the getters above (basis n x r, M2L r_i x r_j, leaf P2P n_i x n_j,
+ * column-major); the ranks must equal the store's. */
+int ifmm_store_set_basis(ifmm_store* s, int level, int index, const double* in);
+int ifmm_store_set_m2l(ifmm_store* s, int level, int i, int j, const double* in);
+int ifmm_store_set_p2p(ifmm_store* s, int i, int j, const double* in);
 /* bytes of the assembled operators as stored: out3[0] leaf near field P2P
  * (each neighbour pair once), out3[1] M2L blocks (both orientations of every
  * interaction-list pair), out3[2] bases U (levels >= 2) -- the algorithmic

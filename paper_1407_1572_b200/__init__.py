@@ -9,7 +9,7 @@ from .estimator import IfmmSolver, default_depth
 from .geometry import ClusterTree, Cluster, PointSet, build_tree, compute_lists, morton_decode, morton_encode
 from .kernels import KERNEL_NAMES, Kernel, baseline_kernel, kernel_block, make_kernel
 from .operators import (OperatorStore, assemble_extended_dense, dump_extended, extended_layout, extended_restrict_x,
-                        extended_rhs, fmm_matvec, init_operators)
+                        extended_rhs, fmm_matvec, init_operators, load_operator_blocks)
 from .solver import IfmmFactorization, LevelStats, factorize, solve
 from . import distributed  # noqa: E402  (sharded factorize / solve)
 
@@ -37,6 +37,7 @@ __all__ = [
     "fmm_matvec",
     "init_operators",
     "kernel_block",
+    "load_operator_blocks",
     "make_kernel",
     "morton_decode",
     "morton_encode",

@@ -55,6 +55,9 @@ SIGNATURES = {
     "ifmm_store_m2l": (_i32, [_p, _i32, _i32, _i32, _p]),
     "ifmm_store_p2p": (_i32, [_p, _i32, _i32, _p]),
     "ifmm_store_bytes": (_i32, [_p, _p]),
+    "ifmm_store_set_basis": (_i32, [_p, _i32, _i32, _p]),
+    "ifmm_store_set_m2l": (_i32, [_p, _i32, _i32, _i32, _p]),
+    "ifmm_store_set_p2p": (_i32, [_p, _i32, _i32, _p]),
     "ifmm_extended_layout": (_i32, [_p, _pi64, _p, _p, _p, _p]),
     "ifmm_extended_dense": (_i32, [_p, _i64, _pi64, _p]),
     "ifmm_matvec": (_i32, [_p, _p, _p, _i64, _i32]),

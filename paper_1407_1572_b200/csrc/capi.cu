@@ -270,6 +270,54 @@ int ifmm_extended_dense(ifmm_store* s, int64_t cap, int64_t* dim, double* out) {
   });
 }
 
+int ifmm_store_set_basis(ifmm_store* s, int level, int index, const double* in) {
+  return guard([&] {
+    if (level < 2 || level > s->h->tree->depth) invalid("level out of range");
+    const InitLevel& L = s->h->lv[level];
+    if (index < 0 || index >= L.nc) invalid("index out of range");
+    CK(cudaMemcpy(L.U[index], in, sizeof(double) * L.n[index] * L.r0[index], cudaMemcpyHostToDevice));
+  });
+}
+
+int ifmm_store_set_m2l(ifmm_store* s, int level, int i, int j, const double* in) {
+  return guard([&] {
+    if (level < 2 || level > s->h->tree->depth) invalid("level out of range");
+    const InitLevel& L = s->h->lv[level];
+    const Topo& T = s->h->tree->lv[level];
+    if (i < 0 || i >= L.nc) invalid("index out of range");
+    for (int q = T.il_off[i]; q < T.il_off[i + 1]; q++)
+      if (T.il[q] == j) {
+        CK(cudaMemcpy(L.m2l[q], in, sizeof(double) * L.r0[i] * L.r0[j], cudaMemcpyHostToDevice));
+        return;
+      }
+    invalid("(i, j) is not an interaction-list pair");
+  });
+}
+
+int ifmm_store_set_p2p(ifmm_store* s, int i, int j, const double* in) {
+  return guard([&] {
+    const StoreH* S = s->h;
+    const int K = S->tree->depth;
+    const Topo& T = S->tree->lv[K];
+    const InitLevel& L = S->lv[K];
+    if (i < 0 || j < 0 || i >= T.nc || j >= T.nc) invalid("index out of range");
+    const int a = std::min(i, j), b = std::max(i, j), sl = T.slot(a, b);
+    double* blk = sl >= 0 ? S->leaf_p2p[size_t(a) * T.win() + sl] : nullptr;
+    bool nb = false;
+    for (int q = T.nbr_off[i]; q < T.nbr_off[i + 1]; q++) nb |= T.nbr[q] == j;
+    if (!nb || !blk) invalid("(i, j) is not a leaf neighbour pair");
+    const int na = L.n[a], nbb = L.n[b];
+    if (i == a) {
+      CK(cudaMemcpy(blk, in, sizeof(double) * size_t(na) * nbb, cudaMemcpyHostToDevice));
+    } else {  // stored once as (a, b): in is n_i x n_j = n_b x n_a, store its transpose
+      std::vector<double> h(size_t(na) * nbb);
+      for (int c = 0; c < nbb; c++)
+        for (int r = 0; r < na; r++) h[r + size_t(c) * na] = in[c + size_t(r) * nbb];
+      CK(cudaMemcpy(blk, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    }
+  });
+}
+
 int ifmm_matvec(ifmm_store* s, const double* x, double* y, int64_t nrhs, int ptr_kind) {
   return guard([&] { ifmm::matvec(s->h, x, y, nrhs, ptr_kind == IFMM_PTR_DEVICE); });
 }

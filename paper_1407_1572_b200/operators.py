@@ -130,6 +130,33 @@ def init_operators(tree: ClusterTree, kernel: Kernel, p: int = 8, tol: float = 1
     return OperatorStore(h, tree, kernel, int(p), float(tol))
 
 
+def load_operator_blocks(store: OperatorStore, bases: dict, m2l: dict, p2p: dict) -> OperatorStore:
+    """Test hook: overwrite the GPU store's initial operators with
+    blocks built elsewhere, e.g. a reference OperatorStore's `l2p`, `m2l`, `p2p`
+    dicts (ifmm/operators.py:42-137), so factorize runs on bit-identical inputs.
+    bases[(k, i)] n x r; m2l[(k, i, j)] r_i x r_j on interaction-list pairs;
+    p2p[(k, i, j)] n_i x n_j on leaf neighbour pairs.  Shapes must match the
+    store's (same tree, same initial ranks); ValueError otherwise."""
+    K = store.tree.depth
+
+    def col(a):
+        return np.asfortranarray(np.asarray(a, dtype=float))
+
+    for (k, i), U in bases.items():
+        if U.shape != (store.part_dim(k, i), store.rank(k, i)):
+            raise ValueError(f"basis ({k}, {i}) has shape {U.shape}, the store {store.part_dim(k, i), store.rank(k, i)}")
+        _lib.check(_lib.lib.ifmm_store_set_basis(store.handle, k, i, _lib.ptr(col(U))))
+    for (k, i, j), M in m2l.items():
+        if M.shape != (store.rank(k, i), store.rank(k, j)):
+            raise ValueError(f"M2L ({k}, {i}, {j}) has shape {M.shape}")
+        _lib.check(_lib.lib.ifmm_store_set_m2l(store.handle, k, i, j, _lib.ptr(col(M))))
+    for (k, i, j), P in p2p.items():
+        if k != K:
+            continue  # the initial store holds the leaf near field only
+        _lib.check(_lib.lib.ifmm_store_set_p2p(store.handle, i, j, _lib.ptr(col(P))))
+    return store
+
+
 def fmm_matvec(store: OperatorStore, tree: ClusterTree, charges):
     """Apply the compressed operator (ifmm/operators.py:282-330).  `charges` is
     (N,) or (N, nrhs), numpy or torch (CUDA tensors stay on the device)."""
