@@ -48,13 +48,15 @@ CONFIGS = {
     "C3_262k": (262144, "inv_r", 6, 4, 1e-6, 1),
     # BASELINE C5: 32 simultaneous rhs; sized for 8 GPUs (records alone ~0.85 TB)
     "C5": (16777216, "log_r", 9, 4, 1e-6, 32),
+    # C5's parameters (log r, p 4, eps 1e-6, 32 rhs) at the largest size one B200 holds
+    "C5_1m": (1048576, "log_r", 7, 4, 1e-6, 32),
 }
 METRIC = "IFMM factor+solve seconds at N=1M 2D"
 PIVOT_LIMIT = 1e12  # ifmm/solver.py:50
 # bounded CPU sample of the reference algorithm: the config's parameters at a
 # smaller N (depth 4 = 256 leaves of 64 points), about 9 s of one core
 SAMPLE = {"C3": (16384, 4), "C3_65k": (16384, 4), "C3_262k": (16384, 4), "C2": (16384, 4), "C1": (4096, 3),
-          "C5": (16384, 4)}
+          "C5": (16384, 4), "C5_1m": (16384, 4)}
 C3_FULL_RUN = os.path.join(ROOT, "profiles", "r02_c3_reference_cpu.json")
 
 
