@@ -411,6 +411,14 @@ def main():
         g = np.load(os.path.join(ROOT, "tests", "golden", "c3_1m.npz"))
         ref_c3 = {"morton": int(len(g["singular_morton"])), "colour9": int(len(g["singular_colour9"])),
                   "resid_morton": float(g["resid_morton"]), "resid_colour9": float(g["resid_colour9"])}
+    # DRAM traffic of one launch of the dominant kernel from the committed ncu --set full capture
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", {"x_solve": "r02_xsolve_l5_ncu.json", "schur": "r01_schur_l5_ncu.json"}.get(
+        dom, "none.json"))
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh)
+        traffic["source_file"] = os.path.relpath(tp, ROOT)
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
@@ -446,7 +454,8 @@ def main():
         "phases": phases,
         "phase_ms_by_level": ft.phase_times_by_level,
         "roofline": {"kernel": dom_kernel, "bound": "tensor", "achieved": phases[dom]["achieved"], "peak": fl_peak,
-                     "unit": "TFLOP/s", "frac": phases[dom]["frac"], "traffic": None,
+                     "unit": "TFLOP/s", "frac": phases[dom]["frac"], "traffic": traffic.get("dram_bytes_per_launch"),
+                     "traffic_launch": traffic.get("kernel"), "traffic_source": traffic.get("source_file"),
                      "launches": phases[dom]["launches"],
                      "share_of_factor": phases[dom]["ms"] / fac_ms_dev if fac_ms_dev else None,
                      "achieved_source": "algorithmic flops of the phase / CUDA-event time of its launches on the "
