@@ -131,7 +131,8 @@ struct SideStream {
 
 struct FactorWork {
   std::mutex mu;
-  SideStream side;
+  SideStream side;     // condition estimates
+  SideStream ahead;    // LU panel look-ahead
   Arena ws{size_t(256) << 20};
   Staging st;
   Arena lvl[2] = {Arena(size_t(2) << 30), Arena(size_t(2) << 30)};

@@ -549,6 +549,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   hmark(0);
   CK(cudaStreamSynchronize(s_));  // staging buffers of earlier uploads are free after this
   if (work_->side.s) CK(cudaStreamSynchronize(work_->side.s));
+  if (work_->ahead.s) CK(cudaStreamSynchronize(work_->ahead.s));
   ws_.reset();
   st_.reset();
   hmark(1);
@@ -693,7 +694,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       tm_.begin(PH_GJ);
       launch_norm1(dmd, nc_, maxm, d_nS + u0, s_);
       // panel width from the whole batch (across chunks and ranks): same arithmetic as one launch
-      batched_lu(md, dmd, d_info + u0, ws_, st_, s_, gmaxm);
+      batched_lu(md, dmd, d_info + u0, ws_, st_, s_, gmaxm, &work_->ahead);
       const LuDiag dg = launch_lu_diag_inv(md, dmd, ws_, st_, s_, tol_);
       // the condition estimates only gate the batch's read-back: run them on
       // the side stream, overlapped with the X solve, Schur update and fill
@@ -1220,7 +1221,7 @@ void Factorizer::factor_top() {
     const MatDesc* dmd = upload(ws_, md, s_, st_);
     int* d_info = ws_.alloc_n<int>(1);
     tm_.begin(PH_TOP);
-    batched_lu(md, dmd, d_info, ws_, st_, s_);
+    batched_lu(md, dmd, d_info, ws_, st_, s_, 0, &work_->ahead);
     CK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, s_));
   }
   CK(cudaStreamSynchronize(s_));

@@ -317,7 +317,9 @@ __global__ void __launch_bounds__(256) lu_swap_trsm_kernel(const MatDesc* __rest
 // Trailing update A22 -= L21 U12 (rows and columns [j+bb, m)), grid (matrix,
 // 64x64 tile); operands on the cp.async pipeline of gemm.cuh (L21 i-contiguous,
 // U12 k-contiguous), DMMA m8n8k4.
-__global__ void __launch_bounds__(GTHREADS, 3) lu_update_kernel(const MatDesc* __restrict__ desc, int j, int b) {
+// Column tiles [ct_lo, ct_hi) of the trailing matrix (ct_hi < 0: all), all row tiles.
+__global__ void __launch_bounds__(GTHREADS, 3) lu_update_kernel(const MatDesc* __restrict__ desc, int j, int b,
+                                                                 int ct_lo, int ct_hi) {
   extern __shared__ double gsm[];
   const MatDesc D = desc[blockIdx.x];
   const int m = D.m;
@@ -326,9 +328,10 @@ __global__ void __launch_bounds__(GTHREADS, 3) lu_update_kernel(const MatDesc* _
   const int t0 = j + bb, nt = m - t0;
   if (nt <= 0) return;
   const int tiles = (nt + GBM - 1) / GBM;
+  const int ctn = (ct_hi < 0 ? tiles : min(ct_hi, tiles)) - ct_lo;
   const int tl = blockIdx.y;
-  if (tl >= tiles * tiles) return;
-  const int i0 = (tl % tiles) * GBM, c0 = (tl / tiles) * GBN;
+  if (ctn <= 0 || tl >= tiles * ctn) return;
+  const int i0 = (tl % tiles) * GBM, c0 = (ct_lo + tl / tiles) * GBN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
   auto Asm = [&](int st) { return gsm + (size_t)st * 2 * GTILE_D; };
@@ -912,7 +915,7 @@ LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, 
 }
 
 void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws, Staging& st,
-                cudaStream_t s, int shape_maxm) {
+                cudaStream_t s, int shape_maxm, SideStream* la) {
   (void)st;
   const int n = int(h.size());
   if (n == 0) return;
@@ -936,23 +939,52 @@ void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_inf
   CK_LAUNCH();
   const int pthreads = std::min(512, std::max(64, (maxm + 31) / 32 * 32));
   const int gy = std::max(1, std::min(16, (maxm + 63) / 64));
-  for (int j = 0; j < maxm; j += b) {
+  auto panel = [&](int j, cudaStream_t ps) {
     const size_t smem = size_t(maxm - j) * (std::min(b, maxm - j) + 1) * 8 + size_t(maxm - j) * 8;
     // register panel while the tallest panel fits 3 rows per thread (b = 32)
     const int rows = maxm - j;
-    if (b == 32 && rows <= 256) lu_panel_reg_kernel<1><<<n, 256, 0, s>>>(d_desc, j, d_info, moves, nmoves);
-    else if (b == 32 && rows <= 512) lu_panel_reg_kernel<2><<<n, 256, 0, s>>>(d_desc, j, d_info, moves, nmoves);
-    else if (b == 32 && rows <= 768) lu_panel_reg_kernel<3><<<n, 256, 0, s>>>(d_desc, j, d_info, moves, nmoves);
-    else lu_panel_kernel<<<n, pthreads, smem, s>>>(d_desc, j, b, d_info, moves, nmoves);
+    if (b == 32 && rows <= 256) lu_panel_reg_kernel<1><<<n, 256, 0, ps>>>(d_desc, j, d_info, moves, nmoves);
+    else if (b == 32 && rows <= 512) lu_panel_reg_kernel<2><<<n, 256, 0, ps>>>(d_desc, j, d_info, moves, nmoves);
+    else if (b == 32 && rows <= 768) lu_panel_reg_kernel<3><<<n, 256, 0, ps>>>(d_desc, j, d_info, moves, nmoves);
+    else lu_panel_kernel<<<n, pthreads, smem, ps>>>(d_desc, j, b, d_info, moves, nmoves);
     CK_LAUNCH();
+  };
+  // Look-ahead for batches of few matrices (the coarse levels, where the
+  // single-CTA panel chain is the critical path): after step j's row moves,
+  // the trailing update of the first column tile (it holds panel j+1) runs
+  // first, panel j+1 then factors on the side stream while the rest of the
+  // update proceeds; step j+1's moves wait for both.  Same kernels, same
+  // arithmetic on disjoint columns: identical factors.
+  const bool ahead = la != nullptr && n < 148 && b == 32 && GBN >= 2 * b;
+  if (ahead) la->ensure();
+  panel(0, s);
+  for (int j = 0; j < maxm; j += b) {
     lu_swap_trsm_kernel<<<dim3(n, gy), 256, 0, s>>>(d_desc, j, b, moves, nmoves);
     CK_LAUNCH();
-    int mt = 0;
+    int rt = 0;
     for (auto& d : h)
-      if (d.m > j + b) mt = std::max(mt, ceil_div(d.m - j - b, GBM) * ceil_div(d.m - j - b, GBM));
-    if (mt > 0) {
-      lu_update_kernel<<<dim3(n, mt), GTHREADS, GSMEM, s>>>(d_desc, j, b);
+      if (d.m > j + b) rt = std::max(rt, ceil_div(d.m - j - b, GBM));
+    const bool next = j + b < maxm;
+    if (rt == 0) {
+      if (next) panel(j + b, s);
+      continue;
+    }
+    if (ahead && next) {
+      lu_update_kernel<<<dim3(n, rt), GTHREADS, GSMEM, s>>>(d_desc, j, b, 0, 1);
       CK_LAUNCH();
+      CK(cudaEventRecord(la->fork, s));
+      CK(cudaStreamWaitEvent(la->s, la->fork, 0));
+      panel(j + b, la->s);
+      CK(cudaEventRecord(la->join, la->s));
+      if (rt > 1) {
+        lu_update_kernel<<<dim3(n, rt * (rt - 1)), GTHREADS, GSMEM, s>>>(d_desc, j, b, 1, -1);
+        CK_LAUNCH();
+      }
+      CK(cudaStreamWaitEvent(s, la->join, 0));
+    } else {
+      lu_update_kernel<<<dim3(n, rt * rt), GTHREADS, GSMEM, s>>>(d_desc, j, b, 0, -1);
+      CK_LAUNCH();
+      if (next) panel(j + b, s);
     }
   }
 }

@@ -20,6 +20,7 @@
 //                   estimator dgecon runs, ifmm/solver.py:216).
 #pragma once
 #include "batched.cuh"
+#include "core.cuh"
 
 namespace ifmm {
 
@@ -274,8 +275,9 @@ __device__ inline void cta_tile_lu_solve_cols(const double* __restrict__ LU, int
 // info[p] = 0, or 1 + the first column with an exact zero pivot.
 // shape_maxm: largest matrix of the whole colour batch (across ranks) so the
 // panel width -- hence the arithmetic -- does not depend on the sharding.
+// la: a side stream for the panel look-ahead of batches of few matrices (null: none).
 void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_info, Arena& ws, Staging& st,
-                cudaStream_t s, int shape_maxm = 0);
+                cudaStream_t s, int shape_maxm = 0, SideStream* la = nullptr);
 
 // Inverses of the 64x64 diagonal blocks of every factored matrix (L_kk^-1 and
 // U_kk^-1, column-major 64 x 64 each, identity-padded past m): matrix p's
