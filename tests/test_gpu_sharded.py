@@ -117,8 +117,9 @@ def test_nccl_transport_one_rank(ifmm):
     assert np.array_equal(x, x1)
 
 
-def test_two_processes_host_transport(ifmm, tmp_path):
-    """The real multi-process control flow: two processes (torch.distributed.run,
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_processes_host_transport(ifmm, tmp_path, nproc):
+    """The real multi-process control flow: `nproc` processes (torch.distributed.run,
     gloo) share this GPU and factorize ONE system through the host-staged
     communicator (Communicator.host: the library's all-gathers and halo
     exchanges handed to torch.distributed).  Bit-identical to one GPU."""
@@ -134,7 +135,7 @@ def test_two_processes_host_transport(ifmm, tmp_path):
         port = sk.getsockname()[1]
     out = str(tmp_path / "x.npz")
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "host_transport_worker.py")
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
                         "--master-addr", "127.0.0.1", f"--master-port={port}", worker, out, str(n), str(depth),
                         kern, str(p), str(tol)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
