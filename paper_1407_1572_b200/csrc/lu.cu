@@ -691,18 +691,20 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem, boo
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(pred ? gmem : nullptr), "r"(n));
 }
 // Stage half h of block (k, j) -- a 64-row x 32-column slab -- as As[kk * XS_AP + row].
-// Thread t copies rows 2 (t & 31), +1 of columns (t >> 5) + 8 q, q < 4: 16-byte
+// Thread t copies rows 2 (t & 31), +1 of columns (t >> 5) + NW q, q < 32 / NW: 16-byte
 // copies when both rows are in range and the pair is 16-byte aligned (always for
 // the diagonal inverses; for the factor when m or the column is even), else two
 // 8-byte copies.  Address arithmetic is incremental in q.
+template <int NW>
 __device__ __forceinline__ void xchunk_load(double* As, const XChunk& c, const double* __restrict__ LU,
                                             const double* __restrict__ dg, int m, int tid) {
+  constexpr int NQ = 32 / NW;  // columns per thread
   const int r = 2 * (tid & 31), kk0 = tid >> 5;
   double* dst = As + kk0 * XS_AP + r;
   if (c.j == c.k && c.p != 1) {
     const double* src = dg + (size_t)c.k * 2 * XB * XB + (c.bwd ? XB * XB : 0) + r + (size_t)XB * (32 * c.h + kk0);
 #pragma unroll
-    for (int q = 0; q < 4; q++) cp_async16(dst + 8 * q * XS_AP, src + 8 * q * XB, true);
+    for (int q = 0; q < NQ; q++) cp_async16(dst + NW * q * XS_AP, src + NW * q * XB, true);
     return;
   }
   // a factor block, or the diagonal block T_kk itself (p == 1)
@@ -711,10 +713,10 @@ __device__ __forceinline__ void xchunk_load(double* As, const XChunk& c, const d
   const bool diag = c.j == c.k;
   const double* src = LU + row + (size_t)col0 * m;
 #pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const int col = col0 + 8 * q;
-    const double* s_ = src + (size_t)8 * q * m;
-    double* d_ = dst + 8 * q * XS_AP;
+  for (int q = 0; q < NQ; q++) {
+    const int col = col0 + NW * q;
+    const double* s_ = src + (size_t)NW * q * m;
+    double* d_ = dst + NW * q * XS_AP;
     bool ok0 = r0ok && col < m, ok1 = r1ok && col < m;
     if (diag) {
       // T_kk is triangular: keep only its own part (L strictly below / U on and above);
@@ -749,10 +751,12 @@ __device__ __forceinline__ void xchunk_load(double* As, const XChunk& c, const d
 // fill compression cannot absorb (measured: the reference-default N = 8,000
 // system matches the reference only with it); refined, the block solve is as
 // accurate as substitution while every step stays a DMMA product.
-template <int TW, int XS_STAGES, bool REFINE>
-__global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __restrict__ descs,
-                                                        const int* __restrict__ tile_map) {
-  constexpr int NC = TW / 16;  // 8-column tiles per warp
+template <int TW, int XS_STAGES, bool REFINE, int NW = 8>
+__global__ void __launch_bounds__(32 * NW) lu_xsolve_kernel(const XSolveDesc* __restrict__ descs,
+                                                            const int* __restrict__ tile_map) {
+  constexpr int NT = 32 * NW;
+  constexpr int NC = TW / (2 * NW);  // 8-column tiles per warp (NW / 4 column groups)
+  static_assert(NC >= 1 && NC * 2 * NW == TW, "tile width / warp count");
   extern __shared__ double sm[];
   const XSolveDesc D = descs[tile_map[blockIdx.x]];
   const int c0 = (blockIdx.x - D.tile0) * TW;
@@ -765,25 +769,21 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
   double* X = sm;
   double* As = sm + (size_t)TW * xm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // gather the permuted panel: a thread owns a row, 8 of its loads in flight together
-  for (int l = tid; l < mp; l += 256) {
+  // gather the permuted panel asynchronously (one cp.async per element, all in
+  // flight together; the first pipeline wait covers it): rows of C (top, in
+  // pivot order), the -I block of the local slots (bottom), zeros elsewhere
+  for (int l = tid; l < mp; l += NT) {
     const int i = l < m ? D.perm[l] : -1;
-#pragma unroll 1
-    for (int cg = 0; cg < TW; cg += 8) {
-      double v[8];
-#pragma unroll
-      for (int c = 0; c < 8; c++) {
-        const int cc = c0 + cg + c;
-        v[c] = 0.0;
-        if (i >= 0 && cc < w) {
-          if (i < n) v[c] = cc < wl ? D.C[i + (size_t)cc * n] : 0.0;
-          else v[c] = (cc >= wl && i - n == cc - wl) ? -1.0 : 0.0;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 8; c++) X[(size_t)(cg + c) * xm + l] = v[c];
+    const double* src = D.C + (i >= 0 && i < n ? i : 0);
+#pragma unroll 8
+    for (int c = 0; c < TW; c++) {
+      const int cc = c0 + c;
+      double* dst = X + (size_t)c * xm + l;
+      if (i >= n && cc < w && cc >= wl && i - n == cc - wl) *dst = -1.0;
+      else cp_async8(dst, src + (size_t)cc * n, i >= 0 && i < n && cc < wl);  // zero-fill otherwise
     }
   }
+  cp_async_commit();
   const unsigned char* fl = REFINE ? D.dflag : nullptr;
   int T = 2 * nb * (nb - 1) + 4 * nb;  // off-diagonal halves + 2 halves per diagonal block, both sweeps
   if (REFINE)
@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
   XChunk ci{0, 0, 0, 0, 0}, cc{0, 0, 0, 0, 0};
   auto issue = [&](int t) {
     if (t < T) {
-      xchunk_load(As + (size_t)(t % XS_STAGES) * 32 * XS_AP, ci, D.LU, D.dinv, m, tid);
+      xchunk_load<NW>(As + (size_t)(t % XS_STAGES) * 32 * XS_AP, ci, D.LU, D.dinv, m, tid);
       xchunk_next(ci, nb, fl);
     }
     cp_async_commit();
@@ -865,11 +865,16 @@ __global__ void __launch_bounds__(256) lu_xsolve_kernel(const XSolveDesc* __rest
   }
   cp_async_wait<0>();
   __syncthreads();
-  for (int c = 0; c < TW && c0 + c < w; c++) {
-    const int col = c0 + c;
-    const double* x = X + (size_t)c * xm;
-    for (int l = tid; l < n; l += 256) D.Xtop[l + (size_t)col * n] = x[l];
-    for (int l = n + tid; l < m; l += 256) D.Xbot[(l - n) + (size_t)col * D.r] = x[l];
+  // a thread owns a row: its column stores are coalesced across the CTA and
+  // independent of each other
+  const int nc = min(TW, w - c0);
+  for (int l = tid; l < m; l += NT) {
+    const bool top = l < n;
+    double* dst = (top ? D.Xtop + l : D.Xbot + (l - n)) + (size_t)c0 * (top ? n : D.r);
+    const size_t ld = top ? n : D.r;
+#pragma unroll 8
+    for (int c = 0; c < TW; c++)
+      if (c < nc) dst[(size_t)c * ld] = X[(size_t)c * xm + l];
   }
 }
 
@@ -1004,47 +1009,60 @@ void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, const LuDiag& d
 
 void launch_lu_solve_x(const std::vector<XSolveDesc>& hin, Arena& ws, Staging& st, cudaStream_t s) {
   if (hin.empty()) return;
-  int maxm = 0;
-  for (auto& d : hin) maxm = std::max(maxm, d.m);
-  // Configuration: 32-column tiles, two CTAs per SM with 2 stages while the
-  // tile is small (leaf pivots), else one CTA with 4 stages -- the prefetch
-  // distance must cover the L2 latency with one CTA's compute; 16-column tiles
-  // for the largest pivots.
-  int cfg = -1;
-  if (xsolve_smem(32, 3, maxm) <= 110 * 1024) cfg = 0;
-  else if (xsolve_smem(32, 4, maxm) <= 220 * 1024) cfg = 1;
-  else if (xsolve_smem(16, 4, maxm) <= 220 * 1024) cfg = 2;
-  else if (xsolve_smem(16, 3, maxm) <= 220 * 1024) cfg = 3;
-  if (cfg < 0) invalid("pivot block too large for the X solve (m = " + std::to_string(maxm) + ")");
-  const int tw = cfg >= 2 ? 16 : 32;
-  const int stages = (cfg == 0 || cfg == 3) ? 3 : 4;
-  std::vector<XSolveDesc> h(hin);
-  std::vector<int> map;
-  for (size_t p = 0; p < h.size(); p++) {
-    h[p].tile0 = int(map.size());
-    const int tiles = h[p].m > 0 ? ceil_div(h[p].w, tw) : 0;
-    for (int t = 0; t < tiles; t++) map.push_back(int(p));
-  }
-  if (map.empty()) return;
-  const XSolveDesc* dd = upload(ws, h, s, st);
-  const int* dm = upload(ws, map, s, st);
-  const size_t smem = xsolve_smem(tw, stages, maxm);
-  auto go = [&](void (*kern)(const XSolveDesc*, const int*)) {
-    static std::mutex mu;
-    static std::set<const void*> ready;  // kernels whose shared-memory limit is raised
-    {
-      std::lock_guard<std::mutex> lk(mu);
-      if (ready.insert(reinterpret_cast<const void*>(kern)).second)
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    }
-    kern<<<unsigned(map.size()), 256, smem, s>>>(dd, dm);
-    CK_LAUNCH();
+  // Configuration per pivot, from its own m (the columns of X do not depend on
+  // it: every element accumulates the same DMMA sequence): 32-column tiles at
+  // two CTAs per SM with 3 stages while the tile is small, else one CTA with 4
+  // stages -- the prefetch distance must cover the L2 latency with one CTA's
+  // compute; 16-column tiles for the largest pivots.  Pivots of one
+  // configuration share a launch sized for their largest m (a batch mixes m
+  // from ~100 to ~1,000 at the coarse levels: one shared configuration would
+  // give every pivot the largest pivot's shared memory and tile width).
+  auto cfg_of = [](int m) {
+    if (xsolve_smem(32, 3, m) <= 110 * 1024) return 0;
+    if (xsolve_smem(32, 4, m) <= 220 * 1024) return 1;
+    if (xsolve_smem(16, 4, m) <= 220 * 1024) return 2;
+    if (xsolve_smem(16, 3, m) <= 220 * 1024) return 3;
+    return -1;
   };
-  // every pivot is handled by exactly one of the two launches (lu_xsolve_kernel)
-  if (cfg == 0) { go(lu_xsolve_kernel<32, 3, false>); go(lu_xsolve_kernel<32, 3, true>); }
-  else if (cfg == 1) { go(lu_xsolve_kernel<32, 4, false>); go(lu_xsolve_kernel<32, 4, true>); }
-  else if (cfg == 2) { go(lu_xsolve_kernel<16, 4, false>); go(lu_xsolve_kernel<16, 4, true>); }
-  else { go(lu_xsolve_kernel<16, 3, false>); go(lu_xsolve_kernel<16, 3, true>); }
+  std::vector<XSolveDesc> h(hin);
+  std::vector<int> maps[4];
+  int maxm[4] = {0, 0, 0, 0};
+  for (size_t p = 0; p < h.size(); p++) {
+    if (h[p].m <= 0) continue;
+    const int cfg = cfg_of(h[p].m);
+    if (cfg < 0) invalid("pivot block too large for the X solve (m = " + std::to_string(h[p].m) + ")");
+    const int tw = cfg >= 2 ? 16 : 32;
+    std::vector<int>& map = maps[cfg];
+    h[p].tile0 = int(map.size());
+    maxm[cfg] = std::max(maxm[cfg], h[p].m);
+    for (int t = 0, tiles = ceil_div(h[p].w, tw); t < tiles; t++) map.push_back(int(p));
+  }
+  if (maps[0].empty() && maps[1].empty() && maps[2].empty() && maps[3].empty()) return;
+  const XSolveDesc* dd = upload(ws, h, s, st);
+  for (int cfg = 0; cfg < 4; cfg++) {
+    if (maps[cfg].empty()) continue;
+    const int tw = cfg >= 2 ? 16 : 32;
+    const int stages = (cfg == 0 || cfg == 3) ? 3 : 4;
+    const int* dm = upload(ws, maps[cfg], s, st);
+    const size_t smem = xsolve_smem(tw, stages, maxm[cfg]);
+    const unsigned grid = unsigned(maps[cfg].size());
+    auto go = [&](void (*kern)(const XSolveDesc*, const int*)) {
+      static std::mutex mu;
+      static std::set<const void*> ready;  // kernels whose shared-memory limit is raised
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (ready.insert(reinterpret_cast<const void*>(kern)).second)
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      }
+      kern<<<grid, 256, smem, s>>>(dd, dm);
+      CK_LAUNCH();
+    };
+    // every pivot is handled by exactly one of the two launches (lu_xsolve_kernel)
+    if (cfg == 0) { go(lu_xsolve_kernel<32, 3, false>); go(lu_xsolve_kernel<32, 3, true>); }
+    else if (cfg == 1) { go(lu_xsolve_kernel<32, 4, false>); go(lu_xsolve_kernel<32, 4, true>); }
+    else if (cfg == 2) { go(lu_xsolve_kernel<16, 4, false>); go(lu_xsolve_kernel<16, 4, true>); }
+    else { go(lu_xsolve_kernel<16, 3, false>); go(lu_xsolve_kernel<16, 3, true>); }
+  }
 }
 
 }  // namespace ifmm
