@@ -664,9 +664,11 @@ struct XChunk {
   // again); half h of its columns
   int bwd, k, j, p, h;
 };
-// fl: the matrix's refinement flags, fl[2 k + bwd]
-__device__ __forceinline__ void xchunk_next(XChunk& c, int nb, const unsigned char* fl) {
-  if (c.h == 0) {
+// fl: the matrix's refinement flags, fl[2 k + bwd]; sk: the last column
+// block holds <= 32 valid columns (m - XB (nb - 1) <= 32), its second halves
+// multiply zero padding and are skipped
+__device__ __forceinline__ void xchunk_next(XChunk& c, int nb, const unsigned char* fl, bool sk) {
+  if (c.h == 0 && !(sk && c.j == nb - 1)) {
     c.h = 1;
     return;
   }
@@ -788,11 +790,16 @@ __global__ void __launch_bounds__(32 * NW) lu_xsolve_kernel(const XSolveDesc* __
   int T = 2 * nb * (nb - 1) + 4 * nb;  // off-diagonal halves + 2 halves per diagonal block, both sweeps
   if (REFINE)
     for (int q = 0; q < 2 * nb; q++) T += fl[q] ? 4 : 0;  // + 4 halves per refined diagonal block
+  const bool sk = m - XB * (nb - 1) <= 32;
+  if (sk) {  // skipped second halves of the last column block (backward off-diagonals, both diagonals)
+    T -= nb + 1;
+    if (REFINE) T -= 2 * (fl[2 * (nb - 1)] + fl[2 * (nb - 1) + 1]);
+  }
   XChunk ci{0, 0, 0, 0, 0}, cc{0, 0, 0, 0, 0};
   auto issue = [&](int t) {
     if (t < T) {
       xchunk_load<NW>(As + (size_t)(t % XS_STAGES) * 32 * XS_AP, ci, D.LU, D.dinv, m, tid);
-      xchunk_next(ci, nb, fl);
+      xchunk_next(ci, nb, fl, sk);
     }
     cp_async_commit();
   };
@@ -803,7 +810,10 @@ __global__ void __launch_bounds__(32 * NW) lu_xsolve_kernel(const XSolveDesc* __
 #pragma unroll
     for (int b = 0; b < NC; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int fk = lane & 3, fq = lane >> 2;
-  const int r0 = 16 * (warp & 3), cb = NC * (warp >> 2);  // first row of the warp, first 8-column tile
+  // first row of the warp, first 8-column tile.  Warps w and w + 4 share an SM
+  // sub-partition: they take complementary row groups (0/3, 1/2), so the rows
+  // of a partly padded last block (skipped below) leave no sub-partition idle
+  const int r0 = 16 * (warp & 3), cb = NC * (warp >> 2);
   // the refinement keeps R and x1 of the warp's own tiles in registers
   double rv[REFINE ? 2 : 1][NC][2], xv[REFINE ? 2 : 1][NC][2];
   // f(pointer into X_k at an owned accumulator element, that element's (a, b, e))
@@ -847,7 +857,7 @@ __global__ void __launch_bounds__(32 * NW) lu_xsolve_kernel(const XSolveDesc* __
                        : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
                        : "d"(fa[a]), "d"(fb[b]));
     }
-    if (diag && cc.h == 1) {
+    if (diag && (cc.h == 1 || (sk && cc.j == nb - 1))) {
       __syncthreads();  // every warp has read X_k
       if (!REFINE || !fl[2 * cc.k + cc.bwd]) {  // unrefined: X_k = D R
         own(kb, [&](double* x, int a, int b, int e) { *x = acc[a][b][e]; });
@@ -861,7 +871,7 @@ __global__ void __launch_bounds__(32 * NW) lu_xsolve_kernel(const XSolveDesc* __
         }
       }
     }
-    xchunk_next(cc, nb, fl);
+    xchunk_next(cc, nb, fl, sk);
   }
   cp_async_wait<0>();
   __syncthreads();
