@@ -129,6 +129,17 @@ void ifmm_store_free(ifmm_store* s);
  * cond_limit: PIVOT_CONDITION_LIMIT (ifmm/solver.py:50); <= 0 -> 1e12 (reference).
  * The store's initial operators are left intact (matvec stays valid). */
 int ifmm_factorize(ifmm_store* s, double tol, int flags, double cond_limit, ifmm_factor** out);
+/* Extension (SURVEY 8f item 3, rank-growth control; the reference's unused
+ * _maybe_consolidate, ifmm/solver.py:437-492): right before a cluster is
+ * eliminated, its coupling row (its M2L blocks and its rows of the parent's
+ * basis) is re-truncated jointly at rank_tol (relative to the row's largest
+ * singular value, 0 < rank_tol < 1) and its basis rotated onto the kept
+ * directions.  Smaller pivots and parents; not the reference's arithmetic, so
+ * ifmm_factorize stays the parity path.  One GPU only. */
+int ifmm_factorize_rank_control(ifmm_store* s, double tol, int flags, double cond_limit, double rank_tol,
+                                ifmm_factor** out);
+/* out2 = sum of the pivots' basis ranks before / after their consolidation (0, 0 without rank control) */
+int ifmm_factor_rank_control(const ifmm_factor* f, int64_t* out2);
 /* r_m, top-level dimension, number of eliminations, factorization wall ms */
 int ifmm_factor_info(const ifmm_factor* f, int* r_m, int* top_dim, int64_t* n_records, double* ms);
 /* LevelStats of `level`: clusters, max_rank, fillins_compressed, fillins_dense_kept */

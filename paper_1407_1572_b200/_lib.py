@@ -63,6 +63,8 @@ SIGNATURES = {
     "ifmm_matvec": (_i32, [_p, _p, _p, _i64, _i32]),
     "ifmm_store_free": (None, [_p]),
     "ifmm_factorize": (_i32, [_p, _d, _i32, _d, ctypes.POINTER(_p)]),
+    "ifmm_factorize_rank_control": (_i32, [_p, _d, _i32, _d, _d, ctypes.POINTER(_p)]),
+    "ifmm_factor_rank_control": (_i32, [_p, _p]),
     "ifmm_factor_info": (_i32, [_p, _pi32, _pi32, _pi64, _pd]),
     "ifmm_factor_level_stats": (_i32, [_p, _i32, _p]),
     "ifmm_factor_level_cond": (_i32, [_p, _i32, _pd]),

@@ -338,6 +338,23 @@ int ifmm_factorize(ifmm_store* s, double tol, int flags, double cond_limit, ifmm
   });
 }
 
+int ifmm_factorize_rank_control(ifmm_store* s, double tol, int flags, double cond_limit, double rank_tol,
+                                ifmm_factor** out) {
+  return guard([&] {
+    if (!s || !out) invalid("null handle");
+    if (!(rank_tol > 0.0) || !(rank_tol < 1.0)) invalid("rank_tol must lie in (0, 1)");
+    FactorH* h = ifmm::factorize(s->h, tol, flags, cond_limit, rank_tol);
+    *out = new ifmm_factor{h};
+  });
+}
+
+int ifmm_factor_rank_control(const ifmm_factor* f, int64_t* out2) {
+  return guard([&] {
+    out2[0] = f->h->rc_before;
+    out2[1] = f->h->rc_after;
+  });
+}
+
 int ifmm_factor_info(const ifmm_factor* f, int* r_m, int* top_dim, int64_t* n_records, double* ms) {
   return guard([&] {
     if (r_m) *r_m = f->h->r_m;

@@ -232,6 +232,7 @@ struct FactorH {
   bool own_stream = false;
   double halo_bytes = 0, meta_bytes = 0;
   long long exchanges = 0;
+  long long rc_before = 0, rc_after = 0;  // rank-growth control: sum of pivot ranks before / after
   ~FactorH();
 };
 
@@ -264,7 +265,8 @@ void matvec(StoreH* s, const double* x, double* y, int64_t nrhs, bool device_ptr
 // matrix (m x m, column-major, into host_out; null: size only) -> m
 std::vector<ExtSlot> extended_layout(const StoreH* s);
 int64_t extended_dense(StoreH* s, int64_t cap, double* host_out);
-FactorH* factorize(StoreH* s, double tol, int flags, double cond_limit);
+// rank_tol > 0: rank-growth control (consolidate.cu) -- an extension, off in the reference-parity path
+FactorH* factorize(StoreH* s, double tol, int flags, double cond_limit, double rank_tol = 0.0);
 // collective over `comm` (one call per rank, same store contents on every rank)
 FactorH* factorize_sharded(StoreH* s, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit);
 // `nranks` virtual ranks as threads on the current GPU (LocalComm): out[r] is rank r's factorization

@@ -37,6 +37,7 @@
 #include "comm.cuh"
 #include "lu.cuh"
 #include "compress.cuh"
+#include "consolidate.cuh"
 #include "cta_la.cuh"
 
 namespace ifmm {
@@ -58,6 +59,10 @@ struct WorkLevel {
   std::vector<std::vector<int>> ovf_adj;
   int* d_rank = nullptr;
   Arena* arena = nullptr;  // zero-initialised blocks
+  // rank-growth control: rows of the parent's basis belonging to a consolidated
+  // cluster (r' x r0_parent, ld prow_ld), replacing [R_i ; 0] at the transition
+  std::vector<double*> prow;
+  std::vector<int> prow_ld;
 };
 
 struct BlkRef {
@@ -133,12 +138,13 @@ struct PhaseTimer {
 class Factorizer {
  public:
   Factorizer(StoreH* S, FactorWork* work, cudaStream_t s, std::shared_ptr<Comm> comm, double tol, int flags,
-             double cond_limit)
+             double cond_limit, double rank_tol = 0.0)
       : S_(S),
         t_(S->tree),
         tol_(tol),
         flags_(flags),
         cond_limit_(cond_limit),
+        rank_tol_(rank_tol),
         s_(s),
         ws_(work->ws),
         st_(work->st),
@@ -153,6 +159,7 @@ class Factorizer {
   double tol_;
   int flags_;
   double cond_limit_;  // PIVOT_CONDITION_LIMIT (ifmm/solver.py:50), 1e12 by default
+  double rank_tol_;    // > 0: rank-growth control (consolidate.cu) at this relative tolerance
   cudaStream_t s_ = nullptr;
   std::unique_ptr<FactorH> F_;
   Arena& ws_;
@@ -311,6 +318,8 @@ class Factorizer {
     W.ovf_adj.clear();
     W.dead.assign(W.nc, 0);
     W.U.assign(W.nc, nullptr);
+    W.prow.assign(W.nc, nullptr);
+    W.prow_ld.assign(W.nc, 0);
     W.d_rank = W.arena->alloc_n<int>(W.nc);
     hprof_mark("tables");
   }
@@ -350,6 +359,8 @@ class Factorizer {
   void start_leaf_level();
   void start_parent_level(WorkLevel& C, int k);
   void eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred);
+  void consolidate_pivots(const std::vector<int>& piv);
+  std::vector<int> rn_all_;
   void finish_level(int rec_begin);
   void factor_top();
   // sharded runs: one block (or the new columns of a basis) a batch or a
@@ -437,7 +448,10 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
     for (int c = 0; c < nch; c++) {
       const int ch = (i << dim) + c;
       const int64_t ro = L.child_off[size_t(i) * (nch + 1) + c];
-      cb.add(L.U[i] + ro, std::max(1, n0), W.U[i] + off[i][c], W.n[i], S_->lv[k + 1].r0[ch], W.r0[i]);
+      if (C.prow[ch])  // consolidated child: its rotated rows T^T [R ; 0]
+        cb.add(C.prow[ch], C.prow_ld[ch], W.U[i] + off[i][c], W.n[i], C.r[ch], W.r0[i]);
+      else
+        cb.add(L.U[i] + ro, std::max(1, n0), W.U[i] + off[i][c], W.n[i], S_->lv[k + 1].r0[ch], W.r0[i]);
     }
   }
   // parent near field from the children's M2L blocks (ifmm/solver.py:163-192).
@@ -508,6 +522,125 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
   }
 }
 
+// Rank-growth control for the pivots of one colour batch (consolidate.cu): their
+// bases are final (every neighbour of an earlier colour has been eliminated, the
+// remaining ones cannot touch them before they are gone), so each pivot's
+// coupling row -- its M2L blocks and its rows of the parent's basis -- is
+// re-truncated at rank_tol_ and the basis, the blocks and the parent rows are
+// rotated onto the kept directions before S_i and C_i are gathered.
+void Factorizer::consolidate_pivots(const std::vector<int>& piv) {
+  WorkLevel& W = cur_;
+  const Topo& T = *W.T;
+  const int k = W.k, dim = t_->dim, nch = 1 << dim;
+  if (nranks_ > 1) invalid("rank-growth control (rank_tol) is not available for sharded factorizations");
+  const InitLevel* Lp = k > 2 ? &S_->lv[k - 1] : nullptr;
+  std::vector<ConsDesc> cd;
+  struct Part { int l; BlkRef b; };
+  struct Item { int i, r, W, r0p; double *row, *row2; std::vector<Part> parts; };
+  std::vector<Item> items;
+  for (int i : piv) {
+    const int r = W.r[i];
+    if (r <= 0 || W.n[i] <= 0 || W.prow[i]) continue;
+    Item it{i, r, 0, 0, nullptr, nullptr, {}};
+    bool self = false;
+    auto visit = [&](int l) {
+      if (!pm_present(W, i, l)) return;
+      if (l == i) { self = true; return; }
+      BlkRef b = m2l_ref(W, i, l, false);
+      if (!b.p || W.r[l] <= 0) return;
+      it.parts.push_back({l, b});
+      it.W += W.r[l];
+    };
+    for (int t = T.wc_off[i]; t < T.wc_off[i + 1]; t++) visit(T.wc[t]);
+    if (!W.ovf_adj.empty())
+      for (int l : W.ovf_adj[i])
+        if (W.T->slot(i, l) < 0) {
+          bool seen = false;
+          for (const Part& q : it.parts) seen |= q.l == l;
+          if (!seen) visit(l);
+        }
+    if (self) continue;  // only a cluster without a self block is live
+    const int par = i >> dim;
+    it.r0p = Lp ? Lp->r0[par] : 0;
+    it.W += it.r0p;
+    if (it.W == 0) continue;
+    it.row = ws_.alloc_n<double>(size_t(r) * it.W);
+    it.row2 = ws_.alloc_n<double>(size_t(r) * it.W);
+    cd.push_back(ConsDesc{i, W.n[i], r, it.W, W.U[i], it.row, it.row2, nullptr, nullptr, nullptr, nullptr});
+    items.push_back(std::move(it));
+  }
+  if (cd.empty()) return;
+  rn_all_.assign(items.size(), 0);
+  // Two pivots of the batch can share an M2L block (interaction-list pairs three
+  // cells apart have the same colour); it must be rotated from both sides, one
+  // after the other.  Greedy grouping: pivots of a group share no block; groups
+  // run in sequence (a later group gathers the blocks the earlier ones rewrote,
+  // zero beyond their kept ranks).
+  std::unordered_map<int, int> gid;
+  int ngroups = 0;
+  std::vector<int> grp(items.size(), 0);
+  for (size_t u = 0; u < items.size(); u++) {
+    uint64_t used = 0;
+    for (const Part& q : items[u].parts) {
+      auto f = gid.find(q.l);
+      if (f != gid.end() && f->second < 64) used |= uint64_t(1) << f->second;
+    }
+    int g = 0;
+    while (g < 63 && ((used >> g) & 1)) g++;
+    grp[u] = g;
+    gid[items[u].i] = g;
+    ngroups = std::max(ngroups, g + 1);
+  }
+  tm_.begin(PH_COMPRESS);
+  for (int g = 0; g < ngroups; g++) {
+    CopyBatch gather, scatter;
+    std::vector<ConsDesc> cg;
+    std::vector<int> which;
+    for (size_t u = 0; u < items.size(); u++) {
+      if (grp[u] != g) continue;
+      Item& it = items[u];
+      size_t off = 0;
+      for (const Part& q : it.parts) {
+        gather.add(q.b.p, q.b.ld, it.row + off * it.r, it.r, it.r, W.r[q.l], q.b.trans);
+        // stored (l, i) when i > l: dst (r_l x r) = (row2 block)^T
+        if (q.b.trans) scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, W.r[q.l], it.r, true);
+        else scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, it.r, W.r[q.l]);
+        off += W.r[q.l];
+      }
+      if (it.r0p > 0) {
+        const int par = it.i >> dim, c = it.i - (par << dim);
+        const int64_t ro = Lp->child_off[size_t(par) * (nch + 1) + c];
+        const int n0 = int(Lp->child_off[size_t(par) * (nch + 1) + nch]);
+        const int r0i = W.r0[it.i];
+        gather.add(Lp->U[par] + ro, std::max(1, n0), it.row + off * it.r, it.r, r0i, it.r0p);
+        if (it.r > r0i) gather.zero(it.row + off * it.r + r0i, it.r, it.r - r0i, it.r0p);
+        W.prow[it.i] = zalloc(W, size_t(it.r) * it.r0p);
+        W.prow_ld[it.i] = it.r;
+        scatter.add(it.row2 + off * it.r, it.r, W.prow[it.i], it.r, it.r, it.r0p);
+      }
+      cg.push_back(cd[u]);
+      which.push_back(int(u));
+    }
+    int* d_new_g = ws_.alloc_n<int>(cg.size());
+    launch_copies(gather, ws_, st_, s_);
+    launch_consolidate(cg, rank_tol_, W.d_rank, d_new_g, ws_, st_, s_);
+    for (const ConsDesc& D : cg) scatter.add(D.U2, D.n, W.U[D.cluster], D.n, D.n, D.r);
+    launch_copies(scatter, ws_, st_, s_);
+    // group results into item order
+    std::vector<int> hnew(cg.size());
+    CK(cudaMemcpyAsync(hnew.data(), d_new_g, sizeof(int) * cg.size(), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    for (size_t v = 0; v < which.size(); v++) rn_all_[which[v]] = hnew[v];
+  }
+  tm_.end();
+  const std::vector<int>& rn = rn_all_;
+  for (size_t u = 0; u < items.size(); u++) {
+    F_->rc_before += items[u].r;
+    F_->rc_after += rn[u];
+    W.r[items[u].i] = rn[u];
+  }
+}
+
 void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred) {
   const auto t_batch0 = std::chrono::steady_clock::now();
   hmark_ = t_batch0;
@@ -553,6 +686,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   ws_.reset();
   st_.reset();
   hmark(1);
+  if (rank_tol_ > 0.0) consolidate_pivots(piv);
   struct PivInfo {
     int i, n, r, m, w;
     bool own;
@@ -1342,10 +1476,11 @@ FactorH::~FactorH() {
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
-FactorH* factorize(StoreH* S, double tol, int flags, double cond_limit) {
+FactorH* factorize(StoreH* S, double tol, int flags, double cond_limit, double rank_tol) {
   ensure_device();
   std::lock_guard<std::mutex> lock(S->work->mu);  // one factorization per store at a time
-  Factorizer f(S, S->work.get(), S->stream, nullptr, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12);
+  Factorizer f(S, S->work.get(), S->stream, nullptr, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12,
+               rank_tol > 0 ? rank_tol : 0.0);
   return f.run();
 }
 

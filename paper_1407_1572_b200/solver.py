@@ -100,6 +100,8 @@ class IfmmFactorization:
     # on_singular="record") every pivot over the limit as (level, index, cond)
     max_cond: dict = field(default_factory=dict)
     singular_pivots: list = field(default_factory=list)
+    # extension (rank_tol): sum of the pivots' basis ranks before / after consolidation
+    rank_control: tuple = (0, 0)
 
     @property
     def n(self) -> int:
@@ -186,7 +188,7 @@ PHASES = ("gather", "lu", "x_solve", "schur", "compress", "transition", "top")
 def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None, diagnostics: bool = False,
               release_m2l: bool = True, timing: bool = False,
               pivot_condition_limit: float = PIVOT_CONDITION_LIMIT, comm=None,
-              on_singular: str = "raise") -> IfmmFactorization:
+              on_singular: str = "raise", rank_tol: float | None = None) -> IfmmFactorization:
     """Eliminate the extended system on the GPU (ifmm/solver.py:106-153).
 
     Unlike the reference the store's initial operators stay intact (the
@@ -202,14 +204,31 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
     ifmm/solver.py:214-218) raises SingularPivotError at the first pivot whose
     condition estimate exceeds `pivot_condition_limit`; "record" lists such
     pivots in `fact.singular_pivots` and carries on (sharded runs: each rank
-    lists its own pivots)."""
+    lists its own pivots).
+
+    rank_tol (extension, SURVEY 8f item 3 -- rank-growth control, the
+    reference's unused `_maybe_consolidate`, ifmm/solver.py:437-492): right
+    before a cluster is eliminated its coupling row (its M2L blocks and its
+    rows of the parent's basis) is re-truncated jointly at `rank_tol` relative
+    to the row's largest singular value and the basis rotated onto the kept
+    directions.  Ranks stop creeping toward the particle dimension, pivots and
+    parents shrink.  None (default) keeps the reference's arithmetic;
+    `fact.rank_control` = (rank sum before, after).  One GPU only."""
     if on_singular not in ("raise", "record"):
         raise ValueError(f"on_singular must be 'raise' or 'record', got {on_singular!r}")
     if tol is None:
         tol = store.tol
     h = ctypes.c_void_p()
     flags = (1 if timing else 0) | (2 if on_singular == "record" else 0)
-    if comm is not None and comm.size > 1:
+    if rank_tol is not None:
+        if comm is not None and comm.size > 1:
+            raise ValueError("rank_tol is not available for sharded factorizations")
+        if not 0.0 < rank_tol < 1.0:
+            raise ValueError(f"rank_tol must lie in (0, 1), got {rank_tol!r}")
+        _lib.check(_lib.lib.ifmm_factorize_rank_control(store.handle, float(tol), flags,
+                                                        float(pivot_condition_limit), float(rank_tol),
+                                                        ctypes.byref(h)))
+    elif comm is not None and comm.size > 1:
         _lib.check(_lib.lib.ifmm_factorize_sharded(store.handle, comm.handle, float(tol), flags,
                                                    float(pivot_condition_limit), ctypes.byref(h)))
     else:
@@ -232,6 +251,9 @@ def _wrap_factor(store: OperatorStore, tree: ClusterTree, tol: float, h) -> Ifmm
     _lib.check(_lib.lib.ifmm_factor_info(h, ctypes.byref(rm), ctypes.byref(top), ctypes.byref(nrec),
                                          ctypes.byref(ms)))
     fact.r_m, fact.top_dim, fact.n_records, fact.factor_ms = rm.value, top.value, nrec.value, ms.value
+    rc = np.zeros(2, dtype=np.int64)
+    _lib.check(_lib.lib.ifmm_factor_rank_control(h, _lib.ptr(rc)))
+    fact.rank_control = (int(rc[0]), int(rc[1]))
     for k in range(tree.depth, 1, -1):
         st = np.zeros(4, dtype=np.int32)
         _lib.check(_lib.lib.ifmm_factor_level_stats(h, k, _lib.ptr(st)))
