@@ -406,6 +406,39 @@ def main():
         return {"ms": round(ms, 3), "bytes": bytes_, "achieved": a, "peak": hb, "unit": "GB/s", "frac": a / hb,
                 "peak_source": hb_src}
 
+    # extension: the same step with rank-growth control at eps / 10
+    rank_control = None
+    phase_by_level = ft.phase_times_by_level
+    shard_comm_ms = ft.shard["comm_ms"] if ws > 1 else None
+    if ws == 1:
+        del ft
+        rt = tol / 10.0
+        rc_times, frc, xrc = [], None, None
+        for it in range(1 + max(1, min(args.steps, 3))):  # one warm-up
+            if frc is not None:
+                del frc
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            frc = ifmm.factorize(store, tree, pivot_condition_limit=PIVOT_LIMIT, on_singular="record", rank_tol=rt)
+            xrc = ifmm.solve(frc, b_dev)
+            e1.record()
+            torch.cuda.synchronize()
+            if it > 0:
+                rc_times.append(e0.elapsed_time(e1) / 1e3)
+        rr = ifmm.fmm_matvec(store, tree, xrc.double()) - b_dev
+        ifmm.solve(frc, b_dev, refine=1)
+        rank_control = {
+            "rank_tol": rt, "value": float(np.mean(rc_times)), "unit": "s",
+            "relative_residual": float(torch.linalg.norm(rr) / torch.linalg.norm(b_dev)),
+            "residual_after_one_refinement_step": frc.last_refinement[-1],
+            "rank_sum_before_after": list(frc.rank_control), "top_dim": frc.top_dim, "r_m": frc.r_m,
+            "pivots_over_limit": len(frc.singular_pivots), "flops_exec": frc.work["flops_exec"],
+            "note": "extension, not in value: every pivot's coupling row (its M2L blocks + its rows of the parent's "
+                    "basis) re-truncated at rank_tol right before its elimination (csrc/consolidate.cu); the "
+                    "reference never calls its _maybe_consolidate, so `value` stays the parity path"}
+        del frc
+
     ref_c3 = None
     if args.config == "C3":
         g = np.load(os.path.join(ROOT, "tests", "golden", "c3_1m.npz"))
@@ -450,9 +483,9 @@ def main():
                   "scope": "whole job (summed over ranks)" if ws > 1 else "one GPU"},
         "shard": {"rank0_halo_bytes_per_factorization": shard["halo_bytes"],
                   "rank0_meta_bytes": shard["meta_bytes"], "exchanges": shard["exchanges"],
-                  "rank0_comm_ms": ft.shard["comm_ms"]} if ws > 1 else None,
+                  "rank0_comm_ms": shard_comm_ms} if ws > 1 else None,
         "phases": phases,
-        "phase_ms_by_level": ft.phase_times_by_level,
+        "phase_ms_by_level": phase_by_level,
         "roofline": {"kernel": dom_kernel, "bound": "tensor", "achieved": phases[dom]["achieved"], "peak": fl_peak,
                      "unit": "TFLOP/s", "frac": phases[dom]["frac"], "traffic": traffic.get("dram_bytes_per_launch"),
                      "traffic_launch": traffic.get("kernel"), "traffic_source": traffic.get("source_file"),
@@ -468,6 +501,7 @@ def main():
                         "vs_32_single_solves": 32 * solve_ms / solve32_ms,
                         "note": "extension (SURVEY 8f item 1): one factorization, 32 rhs as DMMA GEMM sweeps; "
                                 "not in value"},
+        "rank_control": rank_control,
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 8 * N * nrhs, "d2h_bytes_per_step": 8 * N * nrhs},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -620,6 +620,7 @@ class Factor:
     on_singular: str = "raise"      # "record": note the violation and continue (C3 study)
     singular: list = field(default_factory=list)
     max_cond: dict = field(default_factory=dict)
+    rank_control: list = field(default_factory=lambda: [0, 0])  # extension: rank sums before / after
 
 
 def _parent_near(st: Blocks, k):
@@ -794,6 +795,89 @@ def _eliminate(st: Blocks, k, i, tol, fac: Factor, stats: Stats, ils, dead):
             _squeeze_near(st, k, p, q, tol, stats)
 
 
+def _consolidate(st: Blocks, k, batch, rank_tol, fac: Factor):
+    """Rank-growth control -- NOT reference behaviour: a working
+    restatement of what the reference's unused `_maybe_consolidate`
+    (ifmm/solver.py:437-492) is after, and the checker of the GPU extension
+    `factorize(..., rank_tol=)` (csrc/consolidate.cu).
+
+    Right before the clusters of `batch` are eliminated, each one's coupling row
+    Rw = [M2L(i, l) for every partner l | its rows of the parent's basis] is
+    truncated by a column-pivoted QR of Rw^T at |R_jj| > rank_tol |R_00|, T_i = an
+    orthonormal basis of the kept left factor, and U_i <- U_i T_i,
+    M2L(i, l) <- T_i^T M2L(i, l) T_l (T_l = I for clusters outside the batch),
+    parent rows <- T_i^T rows.  Every T of a batch is computed from the blocks as
+    they were before the batch's rotations (the GPU runs them concurrently)."""
+    tree, d = st.tree, st.tree.dim
+    part = {}
+    inb = set(int(i) for i in batch)
+    for (kk, i, j) in st.blk["m2l"]:
+        if kk == k and i in inb and j != i:
+            part.setdefault(i, []).append(j)
+    T = {}
+    old_r = {}
+    for i in sorted(inb):
+        r = st.r(k, i)
+        if r == 0 or (k, i, i) in st.blk["m2l"]:
+            continue
+        blocks = [st.get("m2l", k, i, l) for l in sorted(part.get(i, [])) if st.r(k, l) > 0]
+        par = i >> d
+        if k > 2:
+            st.refresh_offsets(k - 1, par)
+            o = st.coff[(k - 1, par)]
+            c = i - (par << d)
+            blocks.append(st.U[(k - 1, par)][o[c]:o[c + 1], :])
+        if not blocks:
+            continue
+        Rw = np.concatenate(blocks, axis=1)
+        if Rw.shape[1] == 0:
+            continue
+        _, R, P = qr(Rw.T, mode="economic", pivoting=True)
+        dg = np.abs(np.diag(R))
+        rc = int(np.sum(dg > rank_tol * dg[0])) if dg[0] > 0 else r
+        rc = max(rc, 1)
+        fac.rank_control[0] += r
+        fac.rank_control[1] += min(rc, r)
+        if rc >= r:
+            continue
+        Lm = np.zeros((r, rc))
+        Lm[P, :] = R[:rc, :].T
+        T[i] = qr(Lm, mode="economic")[0]
+        old_r[i] = r
+    if not T:
+        return
+    # pad helpers: blocks are lazily sized; bring them to the pre-rotation ranks first
+    blocks_new = {}
+    for i, Ti in T.items():
+        for l in part.get(i, []):
+            B = st.get("m2l", k, i, l)
+            Tl = T.get(l)
+            blocks_new[(k, i, l)] = Ti.T @ B @ Tl if Tl is not None else Ti.T @ B
+            if l not in T:
+                blocks_new[(k, l, i)] = st.get("m2l", k, l, i) @ Ti
+    prow = {}
+    if k > 2:
+        for i, Ti in T.items():
+            par = i >> d
+            o = st.coff[(k - 1, par)]
+            c = i - (par << d)
+            prow[i] = Ti.T @ st.U[(k - 1, par)][o[c]:o[c + 1], :]
+    for key, B in blocks_new.items():
+        st.blk["m2l"][key] = B
+    for i, Ti in T.items():
+        st.U[(k, i)] = st.U[(k, i)] @ Ti
+    if k > 2:
+        for par in sorted(set(i >> d for i in T)):
+            o = st.coff[(k - 1, par)]
+            P0 = st.U[(k - 1, par)]
+            rows = []
+            for c in range(1 << d):
+                ch = (par << d) + c
+                rows.append(prow[ch] if ch in prow else P0[o[c]:o[c + 1], :])
+            st.U[(k - 1, par)] = np.concatenate(rows, axis=0)
+            st.refresh_offsets(k - 1, par)
+
+
 def _top(fac: Factor):
     """Dense LU of the level-2 M2L system (ifmm/solver.py:528-546)."""
     st, tree = fac.st, fac.tree
@@ -811,7 +895,7 @@ def _top(fac: Factor):
 
 
 def factorize(st: Blocks, tol=None, order="morton", release_m2l=True, cond_limit=COND_LIMIT,
-              on_singular="raise", progress=None) -> Factor:
+              on_singular="raise", progress=None, rank_tol=None) -> Factor:
     """ifmm/solver.py:106-153 with a selectable intra-level order.  `on_singular="record"`
     keeps going past a pivot the reference would reject (ifmm/solver.py:214-218) and lists it
     in `fac.singular`; `progress(k, fac)` is called after each level."""
@@ -831,7 +915,12 @@ def factorize(st: Blocks, tol=None, order="morton", release_m2l=True, cond_limit
         ils = [set(x) for x in tree.ilist[k]]
         dead = np.zeros(tree.n_clusters(k), dtype=bool)
         for batch in elimination_order(tree, k, order):
+            # rank_tol: extension, see _consolidate (off in the reference algorithm)
+            if rank_tol is not None and order != "morton":
+                _consolidate(st, k, batch, rank_tol, fac)
             for i in batch:
+                if rank_tol is not None and order == "morton":
+                    _consolidate(st, k, [i], rank_tol, fac)
                 _eliminate(st, k, int(i), tol, fac, stats, ils, dead)
         fac.r_m = max(fac.r_m, stats.max_rank)
         if progress is not None:

@@ -572,66 +572,62 @@ void Factorizer::consolidate_pivots(const std::vector<int>& piv) {
   if (cd.empty()) return;
   rn_all_.assign(items.size(), 0);
   // Two pivots of the batch can share an M2L block (interaction-list pairs three
-  // cells apart have the same colour); it must be rotated from both sides, one
-  // after the other.  Greedy grouping: pivots of a group share no block; groups
-  // run in sequence (a later group gathers the blocks the earlier ones rewrote,
-  // zero beyond their kept ranks).
-  std::unordered_map<int, int> gid;
-  int ngroups = 0;
-  std::vector<int> grp(items.size(), 0);
-  for (size_t u = 0; u < items.size(); u++) {
-    uint64_t used = 0;
-    for (const Part& q : items[u].parts) {
-      auto f = gid.find(q.l);
-      if (f != gid.end() && f->second < 64) used |= uint64_t(1) << f->second;
-    }
-    int g = 0;
-    while (g < 63 && ((used >> g) & 1)) g++;
-    grp[u] = g;
-    gid[items[u].i] = g;
-    ngroups = std::max(ngroups, g + 1);
-  }
+  // cells apart have the same colour): every pivot computes its rotation from
+  // the block as it was, and the block becomes T_i^T M T_l -- pivot i's rotated
+  // row segment T_i^T M times T_l, one more grouped GEMM over the shared pairs.
+  std::unordered_map<int, int> item_of;
+  for (size_t u = 0; u < items.size(); u++) item_of[items[u].i] = int(u);
   tm_.begin(PH_COMPRESS);
-  for (int g = 0; g < ngroups; g++) {
-    CopyBatch gather, scatter;
-    std::vector<ConsDesc> cg;
-    std::vector<int> which;
-    for (size_t u = 0; u < items.size(); u++) {
-      if (grp[u] != g) continue;
-      Item& it = items[u];
-      size_t off = 0;
-      for (const Part& q : it.parts) {
-        gather.add(q.b.p, q.b.ld, it.row + off * it.r, it.r, it.r, W.r[q.l], q.b.trans);
+  CopyBatch gather, scatter;
+  struct Shared { int u, v; size_t off; const Part* q; };
+  std::vector<Shared> shared;
+  for (size_t u = 0; u < items.size(); u++) {
+    Item& it = items[u];
+    size_t off = 0;
+    for (const Part& q : it.parts) {
+      gather.add(q.b.p, q.b.ld, it.row + off * it.r, it.r, it.r, W.r[q.l], q.b.trans);
+      auto f = item_of.find(q.l);
+      if (f != item_of.end()) {
+        if (it.i < q.l) shared.push_back({int(u), f->second, off, &q});  // handled once, from the smaller cluster
+      } else if (q.b.trans) {
         // stored (l, i) when i > l: dst (r_l x r) = (row2 block)^T
-        if (q.b.trans) scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, W.r[q.l], it.r, true);
-        else scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, it.r, W.r[q.l]);
-        off += W.r[q.l];
+        scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, W.r[q.l], it.r, true);
+      } else {
+        scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, it.r, W.r[q.l]);
       }
-      if (it.r0p > 0) {
-        const int par = it.i >> dim, c = it.i - (par << dim);
-        const int64_t ro = Lp->child_off[size_t(par) * (nch + 1) + c];
-        const int n0 = int(Lp->child_off[size_t(par) * (nch + 1) + nch]);
-        const int r0i = W.r0[it.i];
-        gather.add(Lp->U[par] + ro, std::max(1, n0), it.row + off * it.r, it.r, r0i, it.r0p);
-        if (it.r > r0i) gather.zero(it.row + off * it.r + r0i, it.r, it.r - r0i, it.r0p);
-        W.prow[it.i] = zalloc(W, size_t(it.r) * it.r0p);
-        W.prow_ld[it.i] = it.r;
-        scatter.add(it.row2 + off * it.r, it.r, W.prow[it.i], it.r, it.r, it.r0p);
-      }
-      cg.push_back(cd[u]);
-      which.push_back(int(u));
+      off += W.r[q.l];
     }
-    int* d_new_g = ws_.alloc_n<int>(cg.size());
-    launch_copies(gather, ws_, st_, s_);
-    launch_consolidate(cg, rank_tol_, W.d_rank, d_new_g, ws_, st_, s_);
-    for (const ConsDesc& D : cg) scatter.add(D.U2, D.n, W.U[D.cluster], D.n, D.n, D.r);
-    launch_copies(scatter, ws_, st_, s_);
-    // group results into item order
-    std::vector<int> hnew(cg.size());
-    CK(cudaMemcpyAsync(hnew.data(), d_new_g, sizeof(int) * cg.size(), cudaMemcpyDeviceToHost, s_));
-    CK(cudaStreamSynchronize(s_));
-    for (size_t v = 0; v < which.size(); v++) rn_all_[which[v]] = hnew[v];
+    if (it.r0p > 0) {
+      const int par = it.i >> dim, c = it.i - (par << dim);
+      const int64_t ro = Lp->child_off[size_t(par) * (nch + 1) + c];
+      const int n0 = int(Lp->child_off[size_t(par) * (nch + 1) + nch]);
+      const int r0i = W.r0[it.i];
+      gather.add(Lp->U[par] + ro, std::max(1, n0), it.row + off * it.r, it.r, r0i, it.r0p);
+      if (it.r > r0i) gather.zero(it.row + off * it.r + r0i, it.r, it.r - r0i, it.r0p);
+      W.prow[it.i] = zalloc(W, size_t(it.r) * it.r0p);
+      W.prow_ld[it.i] = it.r;
+      scatter.add(it.row2 + off * it.r, it.r, W.prow[it.i], it.r, it.r, it.r0p);
+    }
   }
+  int* d_new = ws_.alloc_n<int>(cd.size());
+  launch_copies(gather, ws_, st_, s_);
+  launch_consolidate(cd, rank_tol_, W.d_rank, d_new, ws_, st_, s_);
+  for (const ConsDesc& D : cd) scatter.add(D.U2, D.n, W.U[D.cluster], D.n, D.n, D.r);
+  if (!shared.empty()) {
+    // block (l, i) = T_l^T (T_i^T M)^T, written over the stored (i, l), i < l
+    GemmBatch two;
+    for (const Shared& sh : shared) {
+      const Item& a = items[sh.u];
+      const Item& b2 = items[sh.v];
+      double* tmp = ws_.alloc_n<double>(size_t(b2.r) * a.r);
+      two.add(cd[sh.v].T, b2.r, a.row2 + sh.off * a.r, a.r, tmp, b2.r, b2.r, a.r, b2.r, 1.0, 0.0);
+      scatter.add(tmp, b2.r, sh.q->b.p, sh.q->b.ld, a.r, b2.r, true);
+    }
+    launch_grouped_gemm(two, true, true, ws_, st_, s_);
+  }
+  launch_copies(scatter, ws_, st_, s_);
+  CK(cudaMemcpyAsync(rn_all_.data(), d_new, sizeof(int) * cd.size(), cudaMemcpyDeviceToHost, s_));
+  CK(cudaStreamSynchronize(s_));
   tm_.end();
   const std::vector<int>& rn = rn_all_;
   for (size_t u = 0; u < items.size(); u++) {

@@ -1,0 +1,107 @@
+"""Rank-growth control: factorize(..., rank_tol=) on the
+GPU against the oracle's restatement of the same procedure
+(oracle/ifmm_oracle.py::_consolidate, same colour order) and against the
+reference-parity path.  The reference never calls its `_maybe_consolidate`
+(ifmm/solver.py:437-492), so there is no reference output to pin this to: the
+gates are the ones SURVEY 8f asks for -- the residual against the compressed
+operator, next to the same algorithm run on the CPU.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ifmm():
+    import paper_1407_1572_b200 as m
+    from paper_1407_1572_b200 import _lib
+    if _lib.lib.ifmm_device_count() == 0:
+        pytest.skip("no CUDA device")
+    return m
+
+
+def _rank_sums(fact, depth):
+    rec = np.array([(r.level, r.r) for r in fact.records])
+    return {k: int(rec[rec[:, 0] == k, 1].sum()) for k in range(depth, 1, -1)}
+
+
+@pytest.mark.parametrize("kname,N,depth,p,tol,rank_tol", [
+    ("inv_r", 4096, 3, 4, 1e-6, 1e-7),
+    ("log_r", 4096, 3, 5, 1e-6, 1e-7),
+    ("inv_r", 16384, 4, 4, 1e-6, 1e-7),
+])
+def test_rank_control_against_the_oracle(ifmm, kname, N, depth, p, tol, rank_tol):
+    from oracle import ifmm_oracle as O
+    pts = O.baseline_points(N, seed=0)
+    b = O.baseline_rhs(N, "normal")
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    store = ifmm.init_operators(tree, ifmm.baseline_kernel(kname, N), p=p, tol=tol)
+    fact = ifmm.factorize(store, tree, rank_tol=rank_tol)
+    x = ifmm.solve(fact, b)
+    res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
+    # checker: the same procedure on the CPU, same elimination order
+    spec = O.baseline_kernel(kname, N)
+    T = O.build_tree(pts, depth)
+    fo = O.factorize(O.init_operators(T, spec, p, tol), order="colour9", rank_tol=rank_tol)
+    xo = O.solve(fo, b)
+    so = O.init_operators(T, spec, p, tol)
+    res_o = np.linalg.norm(O.fmm_matvec(so, xo) - b) / np.linalg.norm(b)
+    assert res <= max(10 * tol, 2 * res_o), (res, res_o)
+    # both truncate the same coupling rows at the same threshold: ranks agree
+    rs = _rank_sums(fact, depth)
+    for k in range(depth, 1, -1):
+        ro = sum(r.r for r in fo.recs if r.level == k)
+        assert abs(rs[k] - ro) <= 0.03 * ro, (k, rs[k], ro)
+    assert abs(fact.top_dim - int(fo.top_off[-1])) <= 0.03 * fo.top_off[-1]
+    before, after = fact.rank_control
+    assert abs(before - fo.rank_control[0]) <= 0.03 * fo.rank_control[0]
+    assert abs(after - fo.rank_control[1]) <= 0.03 * fo.rank_control[1]
+    # the two solutions differ by the truncation error of the dropped directions
+    # (amplified by the 1/r conditioning), not more
+    diff = np.linalg.norm(x - xo) / np.linalg.norm(xo)
+    assert diff <= max(100 * tol, 4 * res_o), (diff, res_o)
+
+
+def test_rank_control_shrinks_c2_and_keeps_its_accuracy(ifmm):
+    """BASELINE C2 (N = 65,536, log r, p = 5, eps = 1e-6): ranks stop creeping, the
+    residual stays within 10 eps, one refinement step recovers the parity path's."""
+    from oracle import ifmm_oracle as O
+    N, depth, p, tol = 65536, 5, 5, 1e-6
+    pts = O.baseline_points(N, seed=0)
+    b = O.baseline_rhs(N, "normal")
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    store = ifmm.init_operators(tree, ifmm.baseline_kernel("log_r", N), p=p, tol=tol)
+    f0 = ifmm.factorize(store, tree)
+    f1 = ifmm.factorize(store, tree, rank_tol=1e-7)
+    assert f0.rank_control == (0, 0)
+    before, after = f1.rank_control
+    assert after <= 0.5 * before
+    assert f1.top_dim <= 0.7 * f0.top_dim
+    r0, r1 = _rank_sums(f0, depth), _rank_sums(f1, depth)
+    for k in range(depth, 1, -1):
+        assert r1[k] < r0[k]
+    nb = np.linalg.norm(b)
+    x1 = ifmm.solve(f1, b)
+    assert np.linalg.norm(ifmm.fmm_matvec(store, tree, x1) - b) / nb <= 10 * tol
+    x1r = ifmm.solve(f1, b, refine=1)
+    assert np.linalg.norm(ifmm.fmm_matvec(store, tree, x1r) - b) / nb <= 1e-9
+    # multi-rhs solves replay the same (smaller) records
+    B = np.stack([b, 2.0 * b[::-1]], axis=1)
+    X = ifmm.solve(f1, B)
+    assert np.allclose(X[:, 0], x1, rtol=0, atol=1e-9 * np.abs(x1).max())
+
+
+def test_rank_control_arguments(ifmm):
+    from oracle import ifmm_oracle as O
+    N, depth = 1024, 2
+    pts = O.baseline_points(N, seed=0)
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    store = ifmm.init_operators(tree, ifmm.baseline_kernel("log_r", N), p=4, tol=1e-6)
+    for bad in (0.0, -1e-3, 1.0, 2.0):
+        with pytest.raises(ValueError):
+            ifmm.factorize(store, tree, rank_tol=bad)
+    f = ifmm.factorize(store, tree, rank_tol=1e-7)  # depth 2: only the top-level dimension can shrink
+    b = O.baseline_rhs(N, "normal")
+    x = ifmm.solve(f, b)
+    assert np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b) <= 1e-5

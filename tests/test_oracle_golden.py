@@ -71,3 +71,24 @@ def test_nrhs_solve_equals_columnwise():
     for c, v in enumerate((g["b"], g["xm"])):
         ref = O.solve(fac, v)
         assert np.linalg.norm(X[:, c] - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_oracle_rank_control_extension():
+    """oracle/_consolidate (the checker of the GPU's rank_tol extension, not reference
+    behaviour): ranks shrink, the residual against the compressed operator stays
+    near the truncation tolerance, in both elimination orders; off by default."""
+    from oracle import ifmm_oracle as O
+    N, depth, p, tol = 1024, 2, 4, 1e-6
+    pts = O.baseline_points(N, seed=0)
+    spec = O.baseline_kernel("log_r", N)
+    tree = O.build_tree(pts, depth)
+    b = O.baseline_rhs(N, "normal")
+    f0 = O.factorize(O.init_operators(tree, spec, p, tol), order="colour9")
+    assert f0.rank_control == [0, 0]
+    for order in ("colour9", "morton"):
+        f1 = O.factorize(O.init_operators(tree, spec, p, tol), order=order, rank_tol=1e-7)
+        assert 0 < f1.rank_control[1] < f1.rank_control[0]
+        assert f1.top_off[-1] < f0.top_off[-1]
+        x = O.solve(f1, b)
+        res = np.linalg.norm(O.fmm_matvec(O.init_operators(tree, spec, p, tol), x) - b) / np.linalg.norm(b)
+        assert res <= 10 * tol, (order, res)
