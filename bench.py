@@ -50,13 +50,18 @@ CONFIGS = {
     "C5": (16777216, "log_r", 9, 4, 1e-6, 32),
     # C5's parameters (log r, p 4, eps 1e-6, 32 rhs) at the largest size one B200 holds
     "C5_1m": (1048576, "log_r", 7, 4, 1e-6, 32),
+    # C5's parameters at a quarter of C5 (two of its eight shards) on one B200: fits only with
+    # rank-growth control (RANK_TOL below), which this config's factorizations therefore use
+    "C5_4m": (4194304, "log_r", 8, 4, 1e-6, 32),
 }
+# configs whose timed factorizations run with rank-growth control (extension, csrc/consolidate.cu)
+RANK_TOL = {"C5_4m": 1e-7}
 METRIC = "IFMM factor+solve seconds at N=1M 2D"
 PIVOT_LIMIT = 1e12  # ifmm/solver.py:50
 # bounded CPU sample of the reference algorithm: the config's parameters at a
 # smaller N (depth 4 = 256 leaves of 64 points), about 9 s of one core
 SAMPLE = {"C3": (16384, 4), "C3_65k": (16384, 4), "C3_262k": (16384, 4), "C2": (16384, 4), "C1": (4096, 3),
-          "C5": (16384, 4), "C5_1m": (16384, 4)}
+          "C5": (16384, 4), "C5_1m": (16384, 4), "C5_4m": (16384, 4)}
 C3_FULL_RUN = os.path.join(ROOT, "profiles", "r02_c3_reference_cpu.json")
 
 
@@ -287,9 +292,11 @@ def main():
         from paper_1407_1572_b200.distributed import Communicator
         comm = Communicator.from_torch() if args.transport == "nccl" else Communicator.host()
 
+    rt_main = RANK_TOL.get(args.config)  # None: the reference-parity path
+
     def factor(timing=False):
         return ifmm.factorize(store, tree, pivot_condition_limit=PIVOT_LIMIT, on_singular="record", comm=comm,
-                              timing=timing)
+                              timing=timing, rank_tol=rt_main)
 
     def step(rhs):
         fact = factor()
@@ -410,7 +417,12 @@ def main():
     rank_control = None
     phase_by_level = ft.phase_times_by_level
     shard_comm_ms = ft.shard["comm_ms"] if ws > 1 else None
-    if ws == 1:
+    if rt_main is not None:
+        rank_control = {"rank_tol": rt_main, "rank_sum_before_after": list(ft.rank_control),
+                        "note": "this config only fits one B200 with rank-growth control (extension, "
+                                "csrc/consolidate.cu): `value` and every other number of this line are measured "
+                                "with it"}
+    elif ws == 1:
         del ft
         rt = tol / 10.0
         rc_times, frc, xrc = [], None, None
@@ -461,7 +473,7 @@ def main():
                    "diag": "sqrt(N)", "depth": depth, "p": p, "eps": tol, "nrhs": nrhs,
                    "parallelism": f"subtree{ws} (level-2 subtrees per rank, {args.transport} halo exchange per "
                                   f"colour batch)" if ws > 1 else "single",
-                   "pivot_condition_limit": PIVOT_LIMIT, "on_singular": "record",
+                   "pivot_condition_limit": PIVOT_LIMIT, "on_singular": "record", "rank_tol": rt_main,
                    "l2": "factor state (GBs) >> 126 MB L2; no flush needed"},
         "relative_residual": resid,
         "pivots_over_limit": {"count": len(singular), "first": singular[:4], "max_cond_by_level": max_cond,
