@@ -135,7 +135,7 @@ int ifmm_factorize(ifmm_store* s, double tol, int flags, double cond_limit, ifmm
  * basis) is re-truncated jointly at rank_tol (relative to the row's largest
  * singular value, 0 < rank_tol < 1) and its basis rotated onto the kept
  * directions.  Smaller pivots and parents; not the reference's arithmetic, so
- * ifmm_factorize stays the parity path.  One GPU only. */
+ * ifmm_factorize stays the parity path. */
 int ifmm_factorize_rank_control(ifmm_store* s, double tol, int flags, double cond_limit, double rank_tol,
                                 ifmm_factor** out);
 /* out2 = sum of the pivots' basis ranks before / after their consolidation (0, 0 without rank control) */
@@ -229,6 +229,14 @@ int ifmm_factorize_sharded(ifmm_store* s, ifmm_comm* c, double tol, int flags, d
  * (device-to-device copies instead of NCCL): out[nranks] factor handles */
 int ifmm_factorize_emulated(ifmm_store* s, int nranks, double tol, int flags, double cond_limit,
                             ifmm_factor** out);
+/* the sharded / emulated factorizations with rank-growth control (see
+ * ifmm_factorize_rank_control): the rotated M2L blocks travel with each colour
+ * batch's halo, the rotation of a block shared by pivots of two ranks and the
+ * new ranks in two small extra exchanges per batch */
+int ifmm_factorize_sharded_rank_control(ifmm_store* s, ifmm_comm* c, double tol, int flags, double cond_limit,
+                                        double rank_tol, ifmm_factor** out);
+int ifmm_factorize_emulated_rank_control(ifmm_store* s, int nranks, double tol, int flags, double cond_limit,
+                                         double rank_tol, ifmm_factor** out);
 /* solve on every virtual rank; x: nranks consecutive (n, nrhs) solutions */
 int ifmm_solve_emulated(ifmm_factor** f, int nranks, const double* rhs, double* x, int64_t nrhs, int ptr_kind);
 /* rank_nranks[2]; out4: halo bytes sent, metadata bytes sent, exchanges,

@@ -88,6 +88,8 @@ SIGNATURES = {
     "ifmm_comm_selftest": (_i32, [_p, _i64, _pi32]),
     "ifmm_factorize_sharded": (_i32, [_p, _p, _d, _i32, _d, ctypes.POINTER(_p)]),
     "ifmm_factorize_emulated": (_i32, [_p, _i32, _d, _i32, _d, _p]),
+    "ifmm_factorize_sharded_rank_control": (_i32, [_p, _p, _d, _i32, _d, _d, ctypes.POINTER(_p)]),
+    "ifmm_factorize_emulated_rank_control": (_i32, [_p, _i32, _d, _i32, _d, _d, _p]),
     "ifmm_solve_emulated": (_i32, [_p, _i32, _p, _p, _i64, _i32]),
     "ifmm_factor_shard_info": (_i32, [_p, _p, _p]),
     "ifmm_partition": (_i32, [_i32, _i32, _i32, _i32, _p, _p]),

@@ -549,6 +549,27 @@ int ifmm_factorize_sharded(ifmm_store* s, ifmm_comm* c, double tol, int flags, d
   });
 }
 
+int ifmm_factorize_sharded_rank_control(ifmm_store* s, ifmm_comm* c, double tol, int flags, double cond_limit,
+                                        double rank_tol, ifmm_factor** out) {
+  return guard([&] {
+    if (!s || !c || !out) invalid("null handle");
+    if (!(rank_tol > 0.0) || !(rank_tol < 1.0)) invalid("rank_tol must lie in (0, 1)");
+    FactorH* h = ifmm::factorize_sharded(s->h, c->h, tol, flags, cond_limit, rank_tol);
+    *out = new ifmm_factor{h};
+  });
+}
+
+int ifmm_factorize_emulated_rank_control(ifmm_store* s, int nranks, double tol, int flags, double cond_limit,
+                                         double rank_tol, ifmm_factor** out) {
+  return guard([&] {
+    if (!s || !out) invalid("null handle");
+    if (!(rank_tol > 0.0) || !(rank_tol < 1.0)) invalid("rank_tol must lie in (0, 1)");
+    std::vector<FactorH*> v;
+    ifmm::factorize_emulated(s->h, nranks, tol, flags, cond_limit, v, rank_tol);
+    for (int r = 0; r < nranks; r++) out[r] = new ifmm_factor{v[r]};
+  });
+}
+
 int ifmm_factorize_emulated(ifmm_store* s, int nranks, double tol, int flags, double cond_limit,
                             ifmm_factor** out) {
   return guard([&] {

@@ -97,9 +97,9 @@ __global__ void __launch_bounds__(1024, 1)
 }  // namespace
 
 void launch_consolidate(std::vector<ConsDesc>& h, double rank_tol, int* d_rank, int* d_newrank, Arena& ws,
-                        Staging& st, cudaStream_t s) {
+                        Staging& st, cudaStream_t s, int shape_maxr) {
   if (h.empty()) return;
-  int maxr = 1;
+  int maxr = std::max(1, shape_maxr);
   GemmBatch gram, rot, bas;
   for (ConsDesc& D : h) {
     maxr = std::max(maxr, D.r);

@@ -20,7 +20,9 @@ struct ConsDesc {
 
 // newrank[p] = rank kept for descs[p] (== r when nothing is dropped); d_rank[cluster] is updated.
 // On return every desc's row2 / U2 are queued on the stream: copy them back over the blocks / the basis.
+// shape_maxr: largest rank of the whole colour batch across ranks (the CTA width follows it, so a
+// sharded run uses the same arithmetic as one GPU)
 void launch_consolidate(std::vector<ConsDesc>& h, double rank_tol, int* d_rank, int* d_newrank, Arena& ws,
-                        Staging& st, cudaStream_t s);
+                        Staging& st, cudaStream_t s, int shape_maxr = 0);
 
 }  // namespace ifmm

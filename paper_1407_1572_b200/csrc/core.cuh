@@ -268,9 +268,11 @@ int64_t extended_dense(StoreH* s, int64_t cap, double* host_out);
 // rank_tol > 0: rank-growth control (consolidate.cu) -- an extension, off in the reference-parity path
 FactorH* factorize(StoreH* s, double tol, int flags, double cond_limit, double rank_tol = 0.0);
 // collective over `comm` (one call per rank, same store contents on every rank)
-FactorH* factorize_sharded(StoreH* s, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit);
+FactorH* factorize_sharded(StoreH* s, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit,
+                           double rank_tol = 0.0);
 // `nranks` virtual ranks as threads on the current GPU (LocalComm): out[r] is rank r's factorization
-void factorize_emulated(StoreH* s, int nranks, double tol, int flags, double cond_limit, std::vector<FactorH*>& out);
+void factorize_emulated(StoreH* s, int nranks, double tol, int flags, double cond_limit, std::vector<FactorH*>& out,
+                        double rank_tol = 0.0);
 // solve on every virtual rank of an emulated factorization; x[r] is rank r's solution
 void solve_emulated(const std::vector<FactorH*>& f, const double* rhs, const std::vector<double*>& x, int64_t nrhs,
                     bool device_ptr);

@@ -360,7 +360,9 @@ class Factorizer {
   void start_parent_level(WorkLevel& C, int k);
   void eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred);
   void consolidate_pivots(const std::vector<int>& piv);
-  std::vector<int> rn_all_;
+  // pivots consolidated in the current batch -> their M2L partners (the blocks the
+  // rotation rewrote; sharded runs ship them with the batch's halo)
+  std::unordered_map<int, std::vector<int>> cons_parts_;
   void finish_level(int rec_begin);
   void factor_top();
   // sharded runs: one block (or the new columns of a basis) a batch or a
@@ -441,9 +443,14 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
   W.rcap = W.n;
   CopyBatch cb;
   cb.d.reserve(size_t(W.nc) * (4 + 9 * (1 << (2 * dim))));
+  // rank-growth control, sharded: the rotated parent rows of consolidated
+  // children exist on their owner only -- the other ranks storing a parent's
+  // basis receive it from the parent's owner in the transition's halo exchange
+  const bool u_from_owner = nranks_ > 1 && rank_tol_ > 0.0;
   for (int i = 0; i < W.nc; i++) {
     if (!holds1(W, i)) continue;
     W.U[i] = zalloc(W, size_t(W.n[i]) * W.rcap[i]);
+    if (u_from_owner && !mine(W, i)) continue;
     const int n0 = int(L.child_off[size_t(i) * (nch + 1) + nch]);
     for (int c = 0; c < nch; c++) {
       const int ch = (i << dim) + c;
@@ -512,6 +519,17 @@ void Factorizer::start_parent_level(WorkLevel& C, int k) {
       set_pm(W, i, j, 1);
     }
   }
+  if (u_from_owner)
+    for (int i = 0; i < W.nc; i++) {
+      if (W.n[i] <= 0 || W.r[i] <= 0) continue;
+      const HaloItem it{HALO_U, i, 0, 0};
+      if (mine(W, i)) {
+        for (int s = 0; s < nranks_; s++)
+          if (s != rank_ && holds(W, s, i)) send[s].push_back(it);
+      } else if (holds1(W, i)) {
+        recv[owner(W, i)].push_back(it);
+      }
+    }
   CK(cudaMemcpyAsync(W.d_rank, W.r.data(), sizeof(int) * W.nc, cudaMemcpyHostToDevice, s_));
   hprof_mark("parent descriptors");
   launch_copies(cb, ws_, st_, s_);
@@ -532,72 +550,94 @@ void Factorizer::consolidate_pivots(const std::vector<int>& piv) {
   WorkLevel& W = cur_;
   const Topo& T = *W.T;
   const int k = W.k, dim = t_->dim, nch = 1 << dim;
-  if (nranks_ > 1) invalid("rank-growth control (rank_tol) is not available for sharded factorizations");
+  const bool dist = nranks_ > 1;
   const InitLevel* Lp = k > 2 ? &S_->lv[k - 1] : nullptr;
-  std::vector<ConsDesc> cd;
+  // Every rank lists every pivot's coupling row (replicated metadata: presence
+  // flags and ranks); the device work runs for its own pivots only.
   struct Part { int l; BlkRef b; };
-  struct Item { int i, r, W, r0p; double *row, *row2; std::vector<Part> parts; };
+  struct Item { int i, r, W, r0p, cd; bool own; double *row, *row2; std::vector<Part> parts; };
   std::vector<Item> items;
+  std::vector<ConsDesc> cd;
+  cons_parts_.clear();
+  int shape_maxr = 1;
   for (int i : piv) {
     const int r = W.r[i];
-    if (r <= 0 || W.n[i] <= 0 || W.prow[i]) continue;
-    Item it{i, r, 0, 0, nullptr, nullptr, {}};
+    if (r <= 0 || W.n[i] <= 0) continue;
+    Item it{i, r, 0, 0, -1, mine(W, i), nullptr, nullptr, {}};
     bool self = false;
     auto visit = [&](int l) {
       if (!pm_present(W, i, l)) return;
       if (l == i) { self = true; return; }
-      BlkRef b = m2l_ref(W, i, l, false);
-      if (!b.p || W.r[l] <= 0) return;
+      if (W.r[l] <= 0) return;
+      BlkRef b{nullptr, 0, false};
+      if (it.own) {
+        b = m2l_ref(W, i, l, false);
+        if (!b.p) invalid("rank-growth control: an M2L block of an own pivot is not stored on this rank");
+      }
       it.parts.push_back({l, b});
       it.W += W.r[l];
     };
     for (int t = T.wc_off[i]; t < T.wc_off[i + 1]; t++) visit(T.wc[t]);
-    if (!W.ovf_adj.empty())
-      for (int l : W.ovf_adj[i])
-        if (W.T->slot(i, l) < 0) {
-          bool seen = false;
-          for (const Part& q : it.parts) seen |= q.l == l;
-          if (!seen) visit(l);
-        }
+    if (!W.ovf_adj.empty()) {
+      std::vector<int> o(W.ovf_adj[i]);
+      std::sort(o.begin(), o.end());
+      o.erase(std::unique(o.begin(), o.end()), o.end());
+      for (int l : o)
+        if (W.T->slot(i, l) < 0) visit(l);
+    }
     if (self) continue;  // only a cluster without a self block is live
     const int par = i >> dim;
     it.r0p = Lp ? Lp->r0[par] : 0;
     it.W += it.r0p;
     if (it.W == 0) continue;
-    it.row = ws_.alloc_n<double>(size_t(r) * it.W);
-    it.row2 = ws_.alloc_n<double>(size_t(r) * it.W);
-    cd.push_back(ConsDesc{i, W.n[i], r, it.W, W.U[i], it.row, it.row2, nullptr, nullptr, nullptr, nullptr});
+    shape_maxr = std::max(shape_maxr, r);
+    if (it.own) {
+      it.row = ws_.alloc_n<double>(size_t(r) * it.W);
+      it.row2 = ws_.alloc_n<double>(size_t(r) * it.W);
+      it.cd = int(cd.size());
+      cd.push_back(ConsDesc{i, W.n[i], r, it.W, W.U[i], it.row, it.row2, nullptr, nullptr, nullptr, nullptr});
+    }
+    std::vector<int>& cp = cons_parts_[i];
+    for (const Part& q : it.parts) cp.push_back(q.l);
     items.push_back(std::move(it));
   }
-  if (cd.empty()) return;
-  rn_all_.assign(items.size(), 0);
+  if (items.empty()) return;
   // Two pivots of the batch can share an M2L block (interaction-list pairs three
   // cells apart have the same colour): every pivot computes its rotation from
-  // the block as it was, and the block becomes T_i^T M T_l -- pivot i's rotated
-  // row segment T_i^T M times T_l, one more grouped GEMM over the shared pairs.
+  // the block as it was, and the block becomes T_i^T M T_l -- the smaller
+  // cluster's rotated row segment T_i^T M times T_l, one more grouped GEMM over
+  // the shared pairs.  Sharded: when the two pivots have different owners,
+  // owner(l) sends T_l to owner(i), i < l, which forms the block (it reaches the
+  // other ranks storing it with the batch's halo).
   std::unordered_map<int, int> item_of;
   for (size_t u = 0; u < items.size(); u++) item_of[items[u].i] = int(u);
   tm_.begin(PH_COMPRESS);
   CopyBatch gather, scatter;
-  struct Shared { int u, v; size_t off; const Part* q; };
+  struct Shared { int u, v; size_t off; const Part* q; const double* Tl; };
   std::vector<Shared> shared;
+  struct Cross { int u, v; };  // canonical order on every rank: (smaller pivot's item, partner order)
+  std::vector<Cross> cross;
   for (size_t u = 0; u < items.size(); u++) {
     Item& it = items[u];
     size_t off = 0;
     for (const Part& q : it.parts) {
-      gather.add(q.b.p, q.b.ld, it.row + off * it.r, it.r, it.r, W.r[q.l], q.b.trans);
       auto f = item_of.find(q.l);
-      if (f != item_of.end()) {
-        if (it.i < q.l) shared.push_back({int(u), f->second, off, &q});  // handled once, from the smaller cluster
-      } else if (q.b.trans) {
-        // stored (l, i) when i > l: dst (r_l x r) = (row2 block)^T
-        scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, W.r[q.l], it.r, true);
-      } else {
-        scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, it.r, W.r[q.l]);
+      const bool both = f != item_of.end();
+      if (both && it.i < q.l && dist && owner(W, it.i) != owner(W, q.l)) cross.push_back({int(u), f->second});
+      if (it.own) {
+        gather.add(q.b.p, q.b.ld, it.row + off * it.r, it.r, it.r, W.r[q.l], q.b.trans);
+        if (both) {
+          if (it.i < q.l) shared.push_back({int(u), f->second, off, &q, nullptr});  // formed once, by the smaller cluster's owner
+        } else if (q.b.trans) {
+          // stored (l, i) when i > l: dst (r_l x r) = (row2 block)^T
+          scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, W.r[q.l], it.r, true);
+        } else {
+          scatter.add(it.row2 + off * it.r, it.r, q.b.p, q.b.ld, it.r, W.r[q.l]);
+        }
       }
       off += W.r[q.l];
     }
-    if (it.r0p > 0) {
+    if (it.own && it.r0p > 0) {
       const int par = it.i >> dim, c = it.i - (par << dim);
       const int64_t ro = Lp->child_off[size_t(par) * (nch + 1) + c];
       const int n0 = int(Lp->child_off[size_t(par) * (nch + 1) + nch]);
@@ -609,32 +649,71 @@ void Factorizer::consolidate_pivots(const std::vector<int>& piv) {
       scatter.add(it.row2 + off * it.r, it.r, W.prow[it.i], it.r, it.r, it.r0p);
     }
   }
-  int* d_new = ws_.alloc_n<int>(cd.size());
+  int* d_new = ws_.alloc_n<int>(std::max<size_t>(1, cd.size()));
   launch_copies(gather, ws_, st_, s_);
-  launch_consolidate(cd, rank_tol_, W.d_rank, d_new, ws_, st_, s_);
+  launch_consolidate(cd, rank_tol_, W.d_rank, d_new, ws_, st_, s_, shape_maxr);
   for (const ConsDesc& D : cd) scatter.add(D.U2, D.n, W.U[D.cluster], D.n, D.n, D.r);
+  // rotations of the other side of cross-owner pairs
+  std::unordered_map<int64_t, const double*> t_remote;  // (u, v) -> T_l received
+  if (!cross.empty()) {
+    std::vector<Msg> sm, rm;
+    for (const Cross& c : cross) {
+      const Item& a = items[c.u];   // smaller cluster: forms the block
+      const Item& b2 = items[c.v];  // larger cluster: its owner sends T
+      const size_t bytes = sizeof(double) * size_t(b2.r) * b2.r;
+      if (b2.own) sm.push_back(Msg{owner(W, a.i), cd[b2.cd].T, bytes});
+      if (a.own) {
+        double* buf = ws_.alloc_n<double>(size_t(b2.r) * b2.r);
+        rm.push_back(Msg{owner(W, b2.i), buf, bytes});
+        t_remote[(int64_t(c.u) << 32) | uint32_t(c.v)] = buf;
+      }
+    }
+    comm_->exchange(sm, rm, s_);
+    F_->exchanges++;
+  }
   if (!shared.empty()) {
     // block (l, i) = T_l^T (T_i^T M)^T, written over the stored (i, l), i < l
     GemmBatch two;
-    for (const Shared& sh : shared) {
+    for (Shared& sh : shared) {
       const Item& a = items[sh.u];
       const Item& b2 = items[sh.v];
+      auto f = t_remote.find((int64_t(sh.u) << 32) | uint32_t(sh.v));
+      const double* Tl = f != t_remote.end() ? f->second : (b2.own ? cd[b2.cd].T : nullptr);
+      if (!Tl) invalid("rank-growth control: missing rotation of a shared block");
       double* tmp = ws_.alloc_n<double>(size_t(b2.r) * a.r);
-      two.add(cd[sh.v].T, b2.r, a.row2 + sh.off * a.r, a.r, tmp, b2.r, b2.r, a.r, b2.r, 1.0, 0.0);
+      two.add(Tl, b2.r, a.row2 + sh.off * a.r, a.r, tmp, b2.r, b2.r, a.r, b2.r, 1.0, 0.0);
       scatter.add(tmp, b2.r, sh.q->b.p, sh.q->b.ld, a.r, b2.r, true);
     }
     launch_grouped_gemm(two, true, true, ws_, st_, s_);
   }
   launch_copies(scatter, ws_, st_, s_);
-  CK(cudaMemcpyAsync(rn_all_.data(), d_new, sizeof(int) * cd.size(), cudaMemcpyDeviceToHost, s_));
+  std::vector<int> own_new(std::max<size_t>(1, cd.size()), 0);
+  if (!cd.empty()) CK(cudaMemcpyAsync(own_new.data(), d_new, sizeof(int) * cd.size(), cudaMemcpyDeviceToHost, s_));
   CK(cudaStreamSynchronize(s_));
+  std::vector<int> rn(items.size(), -1);
+  for (size_t u = 0; u < items.size(); u++)
+    if (items[u].own) rn[u] = own_new[items[u].cd];
+  if (dist) {
+    // new ranks of every pivot on every rank (the batch's host schedule needs them)
+    int* d_send = upload(ws_, rn, s_, st_);
+    int* d_recv = ws_.alloc_n<int>(rn.size() * nranks_);
+    comm_->allgather(d_send, d_recv, rn.size() * sizeof(int), s_);
+    std::vector<int> all(rn.size() * nranks_);
+    CK(cudaMemcpyAsync(all.data(), d_recv, sizeof(int) * all.size(), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    for (size_t u = 0; u < items.size(); u++) rn[u] = all[size_t(owner(W, items[u].i)) * rn.size() + u];
+    F_->meta_bytes += double(rn.size() * sizeof(int)) * (nranks_ - 1);
+  }
   tm_.end();
-  const std::vector<int>& rn = rn_all_;
   for (size_t u = 0; u < items.size(); u++) {
-    F_->rc_before += items[u].r;
-    F_->rc_after += rn[u];
+    if (rn[u] <= 0 || rn[u] > items[u].r) invalid("rank-growth control: inconsistent consolidated rank");
+    if (items[u].own) {
+      F_->rc_before += items[u].r;
+      F_->rc_after += rn[u];
+    }
     W.r[items[u].i] = rn[u];
   }
+  if (dist) CK(cudaMemcpyAsync(W.d_rank, W.r.data(), sizeof(int) * W.nc, cudaMemcpyHostToDevice, s_));
 }
 
 void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<int>& deferred) {
@@ -1139,10 +1218,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     std::vector<HaloItem> items;
     for (int t = 0; t < np; t++) {
       const PivInfo& I = P[t];
+      auto cpit = cons_parts_.find(I.i);  // rank-growth control: the M2L blocks the pivot's rotation rewrote
       if (!I.own) {  // every item of a pivot lies among {i} u partners: none stored here -> none received
         bool any = holds1(W, I.i);
         for (int j : I.xp) any = any || holds1(W, j);
         for (int j : I.yp) any = any || holds1(W, j);
+        if (cpit != cons_parts_.end())
+          for (int l : cpit->second) any = any || holds1(W, l);
         if (!any) continue;
       }
       items.clear();
@@ -1165,6 +1247,12 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         items.push_back({HALO_M2L, std::min(fh[f].p, fh[f].q), std::max(fh[f].p, fh[f].q), 0});
       for (int x : I.xp)
         if (W.r[x] > r_before[x]) items.push_back({HALO_U, x, 0, r_before[x]});
+      if (cpit != cons_parts_.end())
+        for (int l : cpit->second) {
+          // a block shared with another consolidated pivot was formed by the smaller cluster's owner
+          if (l < I.i && cons_parts_.count(l)) continue;
+          items.push_back({HALO_M2L, std::min(I.i, l), std::max(I.i, l), 0});
+        }
       const int q = owner(W, I.i);
       for (const HaloItem& it : items)
         if (halo_route(*part_, k, q, rank_, it.a, it.kind == HALO_U ? -1 : it.b,
@@ -1480,18 +1568,20 @@ FactorH* factorize(StoreH* S, double tol, int flags, double cond_limit, double r
   return f.run();
 }
 
-FactorH* factorize_sharded(StoreH* S, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit) {
+FactorH* factorize_sharded(StoreH* S, std::shared_ptr<Comm> comm, double tol, int flags, double cond_limit,
+                           double rank_tol) {
   ensure_device();
   if (!comm) invalid("null communicator");
   std::lock_guard<std::mutex> lock(S->work->mu);
   Factorizer f(S, S->work.get(), S->stream, std::move(comm), tol < 0 ? S->tol : tol, flags,
-               cond_limit > 0 ? cond_limit : 1e12);
+               cond_limit > 0 ? cond_limit : 1e12, rank_tol > 0 ? rank_tol : 0.0);
   return f.run();
 }
 
 // Virtual ranks as threads on one GPU: each has its own workspaces, stream and
 // records; the store (initial operators, read-only here) is shared.
-void factorize_emulated(StoreH* S, int nranks, double tol, int flags, double cond_limit, std::vector<FactorH*>& out) {
+void factorize_emulated(StoreH* S, int nranks, double tol, int flags, double cond_limit, std::vector<FactorH*>& out,
+                        double rank_tol) {
   ensure_device();
   if (nranks < 1) invalid("nranks must be >= 1");
   int dev = 0;
@@ -1511,7 +1601,8 @@ void factorize_emulated(StoreH* S, int nranks, double tol, int flags, double con
         std::shared_ptr<Comm> c = std::make_shared<LocalComm>(world, r);
         std::unique_ptr<FactorH> F;
         try {
-          Factorizer f(S, work.get(), s, c, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12);
+          Factorizer f(S, work.get(), s, c, tol < 0 ? S->tol : tol, flags, cond_limit > 0 ? cond_limit : 1e12,
+                       rank_tol > 0 ? rank_tol : 0.0);
           F.reset(f.run());
         } catch (...) {
           cudaStreamSynchronize(s);

@@ -178,15 +178,20 @@ class Communicator:
 
 
 def factorize_emulated(store, tree, nranks: int, tol: float | None = None, timing: bool = False,
-                       pivot_condition_limit: float = 1e12) -> list:
+                       pivot_condition_limit: float = 1e12, rank_tol: float | None = None) -> list:
     """The sharded schedule with `nranks` virtual ranks on the current GPU;
     returns one IfmmFactorization per rank."""
     from .solver import _wrap_factor
     if tol is None:
         tol = store.tol
     hs = (ctypes.c_void_p * nranks)()
-    _lib.check(_lib.lib.ifmm_factorize_emulated(store.handle, int(nranks), float(tol), 1 if timing else 0,
-                                                float(pivot_condition_limit), ctypes.cast(hs, ctypes.c_void_p)))
+    if rank_tol is not None:
+        _lib.check(_lib.lib.ifmm_factorize_emulated_rank_control(
+            store.handle, int(nranks), float(tol), 1 if timing else 0, float(pivot_condition_limit), float(rank_tol),
+            ctypes.cast(hs, ctypes.c_void_p)))
+    else:
+        _lib.check(_lib.lib.ifmm_factorize_emulated(store.handle, int(nranks), float(tol), 1 if timing else 0,
+                                                    float(pivot_condition_limit), ctypes.cast(hs, ctypes.c_void_p)))
     return [_wrap_factor(store, tree, float(tol), ctypes.c_void_p(h)) for h in hs]
 
 

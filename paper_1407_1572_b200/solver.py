@@ -213,22 +213,26 @@ def factorize(store: OperatorStore, tree: ClusterTree, tol: float | None = None,
     to the row's largest singular value and the basis rotated onto the kept
     directions.  Ranks stop creeping toward the particle dimension, pivots and
     parents shrink.  None (default) keeps the reference's arithmetic;
-    `fact.rank_control` = (rank sum before, after).  One GPU only."""
+    `fact.rank_control` = (rank sum before, after; a sharded run counts this
+    rank's pivots)."""
     if on_singular not in ("raise", "record"):
         raise ValueError(f"on_singular must be 'raise' or 'record', got {on_singular!r}")
     if tol is None:
         tol = store.tol
     h = ctypes.c_void_p()
     flags = (1 if timing else 0) | (2 if on_singular == "record" else 0)
-    if rank_tol is not None:
-        if comm is not None and comm.size > 1:
-            raise ValueError("rank_tol is not available for sharded factorizations")
-        if not 0.0 < rank_tol < 1.0:
-            raise ValueError(f"rank_tol must lie in (0, 1), got {rank_tol!r}")
+    sharded = comm is not None and comm.size > 1
+    if rank_tol is not None and not 0.0 < rank_tol < 1.0:
+        raise ValueError(f"rank_tol must lie in (0, 1), got {rank_tol!r}")
+    if rank_tol is not None and sharded:
+        _lib.check(_lib.lib.ifmm_factorize_sharded_rank_control(store.handle, comm.handle, float(tol), flags,
+                                                                float(pivot_condition_limit), float(rank_tol),
+                                                                ctypes.byref(h)))
+    elif rank_tol is not None:
         _lib.check(_lib.lib.ifmm_factorize_rank_control(store.handle, float(tol), flags,
                                                         float(pivot_condition_limit), float(rank_tol),
                                                         ctypes.byref(h)))
-    elif comm is not None and comm.size > 1:
+    elif sharded:
         _lib.check(_lib.lib.ifmm_factorize_sharded(store.handle, comm.handle, float(tol), flags,
                                                    float(pivot_condition_limit), ctypes.byref(h)))
     else:

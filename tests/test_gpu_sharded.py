@@ -49,6 +49,37 @@ CASES = [
 ]
 
 
+RC_CASES = [
+    (4096, 3, "inv_r", 4, 1e-6, 1e-7, [2, 4, 8, 16]),
+    (16384, 4, "log_r", 5, 1e-6, 1e-7, [2, 3, 4, 8]),
+    (65536, 5, "inv_r", 4, 1e-6, 1e-7, [2, 4, 8]),
+]
+
+
+@pytest.mark.parametrize("case", RC_CASES, ids=lambda c: f"N{c[0]}_{c[2]}")
+def test_sharded_rank_control_matches_single_gpu(ifmm, case):
+    """Rank-growth control (rank_tol) in the sharded schedule: the owner of a pivot
+    consolidates it, the rotation of a block shared with another rank's pivot and the
+    new ranks travel in two small exchanges, the rotated blocks with the batch's halo
+    and the parents' bases with the transition's -- bit-identical to one GPU."""
+    from paper_1407_1572_b200 import distributed as D
+    n, depth, kernel, p, tol, rank_tol, ranks = case
+    tree, store, b = _system(ifmm, n, depth, kernel, p, tol)
+    f1 = ifmm.factorize(store, tree, pivot_condition_limit=np.inf, rank_tol=rank_tol)
+    x1 = ifmm.solve(f1, b)
+    assert f1.rank_control[1] < f1.rank_control[0]
+    for V in ranks:
+        fs = D.factorize_emulated(store, tree, V, pivot_condition_limit=np.inf, rank_tol=rank_tol)
+        assert sum(f.n_records for f in fs) == f1.n_records
+        assert all(f.top_dim == f1.top_dim for f in fs), ([f.top_dim for f in fs], f1.top_dim)
+        assert tuple(map(sum, zip(*[f.rank_control for f in fs]))) == f1.rank_control
+        xs = D.solve_emulated(fs, b)
+        for r in range(1, V):
+            assert np.array_equal(xs[r], xs[0]), "ranks disagree on the replicated solution"
+        assert np.array_equal(xs[0], x1), (V, _rel(xs[0], x1))
+        del fs
+
+
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"N{c[0]}_{c[2]}")
 def test_sharded_matches_single_gpu(ifmm, case):
     from paper_1407_1572_b200 import distributed as D
@@ -117,18 +148,19 @@ def test_nccl_transport_one_rank(ifmm):
     assert np.array_equal(x, x1)
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
-def test_processes_host_transport(ifmm, tmp_path, nproc):
+@pytest.mark.parametrize("nproc,rank_tol", [(2, None), (4, None), (4, 1e-7)])
+def test_processes_host_transport(ifmm, tmp_path, nproc, rank_tol):
     """The real multi-process control flow: `nproc` processes (torch.distributed.run,
     gloo) share this GPU and factorize ONE system through the host-staged
     communicator (Communicator.host: the library's all-gathers and halo
-    exchanges handed to torch.distributed).  Bit-identical to one GPU."""
+    exchanges handed to torch.distributed).  Bit-identical to one GPU, with and
+    without rank-growth control."""
     import socket
     import subprocess
     import sys
     n, depth, kern, p, tol = 16384, 4, "log_r", 5, 1e-6
     tree, store, b = _system(ifmm, n, depth, kern, p, tol)
-    f1 = ifmm.factorize(store, tree, pivot_condition_limit=np.inf)
+    f1 = ifmm.factorize(store, tree, pivot_condition_limit=np.inf, rank_tol=rank_tol)
     x1 = ifmm.solve(f1, b)
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
@@ -137,7 +169,8 @@ def test_processes_host_transport(ifmm, tmp_path, nproc):
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "host_transport_worker.py")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
                         "--master-addr", "127.0.0.1", f"--master-port={port}", worker, out, str(n), str(depth),
-                        kern, str(p), str(tol)], capture_output=True, text=True, timeout=600)
+                        kern, str(p), str(tol)] + ([str(rank_tol)] if rank_tol else []),
+                       capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     g = np.load(out)
     assert int(g["nrec"]) < f1.n_records  # rank 0 eliminated only its own subtrees

@@ -1,13 +1,23 @@
 # Round-2 evidence for profiles/ (run on the GPU box; results in gpurun_out/prof/):
-#   bench line, launch list + per-kernel summary, ncu --set full headline metrics of the main kernels
+#   bench lines, launch lists + per-kernel / per-level summaries (parity path and rank control),
+#   ncu --set full headline metrics + hottest source lines of the main kernels
 set -x
 mkdir -p gpurun_out/prof
 timeout 900 python bench.py > gpurun_out/prof/bench_C3.json 2> gpurun_out/prof/bench_C3.err
+timeout 300 python bench.py --config C2 > gpurun_out/prof/bench_C2.json 2> gpurun_out/prof/bench_C2.err
+timeout 300 python bench.py --config C1 > gpurun_out/prof/bench_C1.json 2> gpurun_out/prof/bench_C1.err
+timeout 600 python bench.py --config C5_1m --no-cpu-baseline > gpurun_out/prof/bench_C5_1m.json 2> gpurun_out/prof/bench_C5_1m.err
+timeout 900 python bench.py --config C5_4m --steps 2 --no-cpu-baseline > gpurun_out/prof/bench_C5_4m.json 2> gpurun_out/prof/bench_C5_4m.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_C3.csv \
     python tools/profile_step.py C3 > /dev/null 2>&1
 python tools/launch_summary.py gpurun_out/prof/launches_C3.csv 40 > gpurun_out/prof/launch_summary_C3.txt
-cap() {  # regex skip tag
-  bash tools/ncu_capture.sh "$1" "$2" "$3" > gpurun_out/prof/ncu_$3.txt 2>&1
+python tools/level_kernels.py gpurun_out/prof/launches_C3.csv 10 >> gpurun_out/prof/launch_summary_C3.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_C3_rank_control.csv \
+    python tools/profile_step.py C3 1e-7 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/prof/launches_C3_rank_control.csv 40 > gpurun_out/prof/launch_summary_C3_rank_control.txt
+python tools/level_kernels.py gpurun_out/prof/launches_C3_rank_control.csv 10 >> gpurun_out/prof/launch_summary_C3_rank_control.txt
+cap() {  # regex skip tag [config [rank_tol]]
+  bash tools/ncu_capture.sh "$1" "$2" "$3" "${4:-C3}" "$5" > gpurun_out/prof/ncu_$3.txt 2>&1
   python tools/ncu_lines.py gpurun_out/ncu_$3.ncu-rep 15 >> gpurun_out/prof/ncu_$3.txt 2>&1
   rm -f gpurun_out/ncu_$3.ncu-rep
 }
@@ -21,3 +31,6 @@ cap "augment_kernel" 0 augment_l7
 cap mv_leaf 0 matvec_leaf
 cap kblock 0 assembly_p2p
 cap rec_solve_vec 0 solve_leaf
+cap consolidate_kernel 4 consolidate_l7 C3 1e-7
+cap consolidate_kernel 22 consolidate_l5 C3 1e-7
+cap "grouped_dgemm_v2_kernel<0, 1>" 4 gram_l7 C3 1e-7

@@ -1,9 +1,9 @@
 # ncu --set full capture of one launch of a kernel in the C3 step (regex $1, skip $2, tag $3);
 # keeps the report in gpurun_out/ and prints the stall breakdown + headline metrics.
-# usage (on the GPU box): bash tools/ncu_capture.sh lu_xsolve 18 xsolve_l5 [CONFIG]
+# usage (on the GPU box): bash tools/ncu_capture.sh lu_xsolve 18 xsolve_l5 [CONFIG [rank_tol]]
 cfg=${4:-C3}
 ncu -f --set full --import-source on --clock-control none -k "regex:$1" -s "${2:-0}" -c 1 \
-    -o gpurun_out/ncu_$3 python tools/profile_step.py $cfg > /dev/null 2>&1
+    -o gpurun_out/ncu_$3 python tools/profile_step.py $cfg $5 > /dev/null 2>&1
 ncu -i gpurun_out/ncu_$3.ncu-rep --page raw --csv > /tmp/k_$3.csv 2>/dev/null
 python - /tmp/k_$3.csv $3 <<'PY'
 import csv, sys

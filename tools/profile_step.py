@@ -1,6 +1,6 @@
 """One assembly + factorize + solve of a bench config (for ncu launch lists / captures).
 
-    python tools/profile_step.py [CONFIG]
+    python tools/profile_step.py [CONFIG] [rank_tol]
 """
 import os
 import sys
@@ -19,7 +19,8 @@ pts = 2.0 * np.random.default_rng(0).random((N, 2)) - 1.0
 b = np.random.default_rng([0, 1]).standard_normal(N)
 tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
 store = ifmm.init_operators(tree, ifmm.baseline_kernel(kern, N), p=p, tol=tol)
-fact = ifmm.factorize(store, tree, pivot_condition_limit=1e300)
+rank_tol = float(sys.argv[2]) if len(sys.argv) > 2 else None
+fact = ifmm.factorize(store, tree, pivot_condition_limit=1e300, rank_tol=rank_tol)
 x = ifmm.solve(fact, b)
 res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
 print(f"{name}: residual {res:.3e} r_m {fact.r_m} top {fact.top_dim}")
