@@ -55,7 +55,8 @@ CONFIGS = {
     "C5_4m": (4194304, "log_r", 8, 4, 1e-6, 32),
 }
 # configs whose timed factorizations run with rank-growth control (extension, csrc/consolidate.cu)
-RANK_TOL = {"C5_4m": 1e-7}
+# (C5 itself: 2.1M points per GPU at 8 GPUs only fit with it, like C5_4m on one)
+RANK_TOL = {"C5_4m": 1e-7, "C5": 1e-7}
 METRIC = "IFMM factor+solve seconds at N=1M 2D"
 PIVOT_LIMIT = 1e12  # ifmm/solver.py:50
 # bounded CPU sample of the reference algorithm: the config's parameters at a
@@ -247,6 +248,9 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rank-tol", type=float, default=None,
+                    help="run the timed factorizations with rank-growth control at this tolerance (extension; "
+                         "default: the reference-parity path, except for the configs in RANK_TOL)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="N > 1: NCCL (one GPU per rank), or host-staged over gloo (ranks may share a GPU; "
                          "validates the multi-process path, not a performance mode)")
@@ -292,7 +296,7 @@ def main():
         from paper_1407_1572_b200.distributed import Communicator
         comm = Communicator.from_torch() if args.transport == "nccl" else Communicator.host()
 
-    rt_main = RANK_TOL.get(args.config)  # None: the reference-parity path
+    rt_main = args.rank_tol if args.rank_tol is not None else RANK_TOL.get(args.config)  # None: the parity path
 
     def factor(timing=False):
         return ifmm.factorize(store, tree, pivot_condition_limit=PIVOT_LIMIT, on_singular="record", comm=comm,
@@ -419,9 +423,8 @@ def main():
     shard_comm_ms = ft.shard["comm_ms"] if ws > 1 else None
     if rt_main is not None:
         rank_control = {"rank_tol": rt_main, "rank_sum_before_after": list(ft.rank_control),
-                        "note": "this config only fits one B200 with rank-growth control (extension, "
-                                "csrc/consolidate.cu): `value` and every other number of this line are measured "
-                                "with it"}
+                        "note": "measured with rank-growth control (extension, csrc/consolidate.cu; C5_4m / C5 only "
+                                "fit in HBM with it): `value` and every other number of this line use it"}
     elif ws == 1:
         del ft
         rt = tol / 10.0
