@@ -53,16 +53,23 @@ CONFIGS = {
     # C5's parameters at a quarter of C5 (two of its eight shards) on one B200: fits only with
     # rank-growth control (RANK_TOL below), which this config's factorizations therefore use
     "C5_4m": (4194304, "log_r", 8, 4, 1e-6, 32),
+    # BASELINE C4's input and parameters (16-component Gaussian mixture, std 0.05, clipped; p 6, eps 1e-10)
+    # on a UNIFORM depth-8 tree whose empty cells are accepted (build_tree(allow_empty_leaves=True)) -- not
+    # the adaptive tree C4 names; runs with rank-growth control (without it the bases of
+    # the sparse clusters run out of memory)
+    "C4": (1048576, "inv_r", 8, 6, 1e-10, 1),
+    "C4_65k": (65536, "inv_r", 6, 6, 1e-10, 1),
 }
+MIXTURE = {"C4", "C4_65k"}  # configs whose points are the C4 mixture (the others: uniform)
 # configs whose timed factorizations run with rank-growth control (extension, csrc/consolidate.cu)
 # (C5 itself: 2.1M points per GPU at 8 GPUs only fit with it, like C5_4m on one)
-RANK_TOL = {"C5_4m": 1e-7, "C5": 1e-7}
+RANK_TOL = {"C5_4m": 1e-7, "C5": 1e-7, "C4": 1e-9, "C4_65k": 1e-9}
 METRIC = "IFMM factor+solve seconds at N=1M 2D"
 PIVOT_LIMIT = 1e12  # ifmm/solver.py:50
 # bounded CPU sample of the reference algorithm: the config's parameters at a
 # smaller N (depth 4 = 256 leaves of 64 points), about 9 s of one core
 SAMPLE = {"C3": (16384, 4), "C3_65k": (16384, 4), "C3_262k": (16384, 4), "C2": (16384, 4), "C1": (4096, 3),
-          "C5": (16384, 4), "C5_1m": (16384, 4), "C5_4m": (16384, 4)}
+          "C5": (16384, 4), "C5_1m": (16384, 4), "C5_4m": (16384, 4), "C4": (16384, 4), "C4_65k": (16384, 4)}
 C3_FULL_RUN = os.path.join(ROOT, "profiles", "r02_c3_reference_cpu.json")
 
 
@@ -71,6 +78,21 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def mixture_points(n, seed=0, comps=16, std=0.05):
+    """BASELINE config 4's input: a seeded 16-component isotropic Gaussian mixture in [0,1]^2 (means uniform,
+    std 0.05, clipped to the box; exact duplicates -- clipping piles points onto corners -- redrawn), mapped
+    to the reference box [-1,1]^2."""
+    rng = np.random.default_rng(seed)
+    means = rng.random((comps, 2))
+    pts = np.empty((0, 2))
+    while len(pts) < n:
+        c = rng.integers(0, comps, n)
+        x = np.clip(means[c] + std * rng.standard_normal((n, 2)), 0.0, 1.0)
+        pts = np.unique(np.concatenate([pts, x]), axis=0)
+    pts = pts[rng.permutation(len(pts))[:n]]
+    return 2.0 * pts - 1.0
 
 
 def spawn_ranks(n):
@@ -277,15 +299,18 @@ def main():
         _lib.check(_lib.lib.ifmm_set_device(dev))
         dist.init_process_group("nccl" if args.transport == "nccl" else "gloo")
     N, kern, depth, p, tol, nrhs = cfg
-    rng_pts = np.random.default_rng(0)
-    pts = 2.0 * rng_pts.random((N, 2)) - 1.0      # [0,1]^2 mapped to the reference box
+    sparse = args.config in MIXTURE
+    if sparse:
+        pts = mixture_points(N)
+    else:
+        pts = 2.0 * np.random.default_rng(0).random((N, 2)) - 1.0      # [0,1]^2 mapped to the reference box
     kernel = ifmm.baseline_kernel(kern, N)
     b_host = np.random.default_rng([0, 1]).standard_normal((N, nrhs) if nrhs > 1 else N)
     b_dev = torch.from_numpy(b_host).cuda()
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth, allow_empty_leaves=sparse)
     t1 = time.perf_counter()
     store = ifmm.init_operators(tree, kernel, p=p, tol=tol)
     t2 = time.perf_counter()
@@ -471,12 +496,17 @@ def main():
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded uniform points in [0,1]^2, N(0,1) rhs)",
+        "dtype": "f64", "data": ("synthetic (seeded 16-component Gaussian mixture in [0,1]^2, std 0.05, clipped; "
+                                 "N(0,1) rhs)" if sparse else
+                                 "synthetic (seeded uniform points in [0,1]^2, N(0,1) rhs)"),
         "config": {"workload": args.config, "N": N, "kernel": "1/|x-y|" if kern == "inv_r" else "log|x-y|",
                    "diag": "sqrt(N)", "depth": depth, "p": p, "eps": tol, "nrhs": nrhs,
                    "parallelism": f"subtree{ws} (level-2 subtrees per rank, {args.transport} halo exchange per "
                                   f"colour batch)" if ws > 1 else "single",
                    "pivot_condition_limit": PIVOT_LIMIT, "on_singular": "record", "rank_tol": rt_main,
+                   "tree": (f"uniform depth {depth} with empty cells accepted ({int((np.diff(tree.leaf_offsets) == 0).sum())} "
+                            f"of {4 ** depth} empty, at most {int(np.diff(tree.leaf_offsets).max())} points in a cell); "
+                            "NOT the adaptive tree of BASELINE config 4") if sparse else f"uniform depth {depth}",
                    "l2": "factor state (GBs) >> 126 MB L2; no flush needed"},
         "relative_residual": resid,
         "pivots_over_limit": {"count": len(singular), "first": singular[:4], "max_cond_by_level": max_cond,

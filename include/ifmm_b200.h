@@ -67,6 +67,11 @@ int ifmm_set_device(int device);
 /* ---- tree: PointSet checks + build_tree + compute_lists
  *      (ifmm/geometry.py:47-61, :174-226, :229-262) */
 int ifmm_tree_build(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out);
+/* Extension for clustered inputs (BASELINE config 4's Gaussian mixture): the same
+ * uniform tree, but leaf cells without points are accepted -- the reference
+ * raises on them (ifmm/geometry.py:191-195).  Empty clusters carry no unknowns
+ * and are skipped by the elimination. */
+int ifmm_tree_build_sparse(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out);
 int ifmm_tree_info(const ifmm_tree* t, int64_t* n, int* dim, int* depth);
 /* permuted position -> original index (ClusterTree.point_permutation) */
 int ifmm_tree_permutation(const ifmm_tree* t, int64_t* perm);

@@ -102,6 +102,14 @@ int ifmm_tree_build(const double* points, int64_t n, int dim, int depth, int ptr
   });
 }
 
+int ifmm_tree_build_sparse(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out) {
+  return guard([&] {
+    if (!out) invalid("null output handle");
+    TreeH* h = ifmm::tree_build(points, n, dim, depth, ptr_kind == IFMM_PTR_DEVICE, true);
+    *out = new ifmm_tree{h};
+  });
+}
+
 int ifmm_tree_info(const ifmm_tree* t, int64_t* n, int* dim, int* depth) {
   return guard([&] {
     if (!t) invalid("null tree");

@@ -6,6 +6,7 @@
 namespace ifmm {
 __device__ int g_prof_on = 0;
 __device__ double g_gram_piv = 1e-14;  // K1 Gram route: scaled pivots^2 >= g_gram_piv / tol
+__device__ int g_full_rank_ok = 0;  // sparse trees: a full-rank ACA is absorbed, not kept dense
 __device__ int g_gram = 1;    // 1: Gram routes (K1 recompression, coarse new directions); 0: Householder QRs
 __device__ unsigned long long g_cyc[16];  // debug stage cycle counters (IFMM_PROF)
 }  // namespace ifmm
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(G::kMaxThreads, G::kMinBlocks) aca_recompress_
       g.sync();
       continue;
     }
-    if (!ao.converged && (k >= min(rows, cols) || k >= D.Kf)) {
+    if (!ao.converged && (k >= min(rows, cols) || k >= D.Kf) && !(g_full_rank_ok && k >= min(rows, cols))) {
       S.status = 1;
       if (g.rank() == 0) state[f] = S;
       g.sync();
@@ -684,6 +685,7 @@ void run_compression(CompressBatch& cb, double tol, const int* d_probes, int pro
     // singular, so the Householder routes run there.
     const int gram = tol >= 1e-9 ? 1 : 0;
     CK(cudaMemcpyToSymbolAsync(g_gram, &gram, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyToSymbolAsync(g_full_rank_ok, &cb.full_rank_ok, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     const double gpiv = 1e-14;
     CK(cudaMemcpyToSymbolAsync(g_gram_piv, &gpiv, sizeof(double), 0, cudaMemcpyHostToDevice, s));
     // Jacobi rotation threshold from the truncation tolerance: singular values

@@ -58,6 +58,12 @@ struct CompressBatch {
   // batch across ranks; worker shapes are chosen from them so every fill is
   // compressed with the same arithmetic as on one GPU
   int shape_mx = 0, shape_nf = 0;
+  // Trees with empty / sparse cells (build_tree(..., allow_empty_leaves=True)): a fill whose ACA
+  // runs to the full rank min(m, n) is an exact factorization and is absorbed into the bases at
+  // that rank instead of being kept dense (the reference keeps it dense, ifmm/solver.py:319-325;
+  // between the few-point clusters of a sparse region that chains dense couplings across the
+  // whole region)
+  int full_rank_ok = 0;
 };
 
 // Runs K1..K4 on stream s.  rank: device ranks of the level (updated);

@@ -82,6 +82,7 @@ struct Topo {
 
 struct TreeH {
   int N = 0, dim = 2, depth = 0;
+  bool sparse = false;                // built with allow_empty: leaf cells may hold no points
   std::vector<Topo> lv;               // index k = 1..depth (0 unused)
   std::vector<int64_t> perm;          // permuted position -> original index
   std::vector<int64_t> leaf_off;      // 4^depth + 1
@@ -258,7 +259,9 @@ struct ExtSlot {
 };
 
 // ------------------------------------------------------------ entry points
-TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_ptr);
+// allow_empty: leaf cells without points are accepted (extension for clustered inputs; the
+// reference raises, ifmm/geometry.py:191-195)
+TreeH* tree_build(const double* pts, int64_t n, int dim, int depth, bool device_ptr, bool allow_empty = false);
 StoreH* store_init(TreeH* t, const KernelParams& kp, int p, double tol, const int* probe_tab, int probe_maxm);
 void matvec(StoreH* s, const double* x, double* y, int64_t nrhs, bool device_ptr);
 // extended system of the initial store (extended.cu): slot table, and the dense

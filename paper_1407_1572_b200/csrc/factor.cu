@@ -1054,6 +1054,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     cbz.rank_host = W.r.data();
     cbz.shape_mx = shape_mx;  // worker shapes from the whole batch (across chunks and ranks)
     cbz.shape_nf = int(fh.size());
+    cbz.full_rank_ok = t_->sparse ? 1 : 0;
     hmark(5);
     tm_.begin(PH_COMPRESS);
     if (!cbz.fills.empty())

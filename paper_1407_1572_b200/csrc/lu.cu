@@ -1032,27 +1032,32 @@ void launch_lu_solve_x(const std::vector<XSolveDesc>& hin, Arena& ws, Staging& s
     if (xsolve_smem(32, 4, m) <= 220 * 1024) return 1;
     if (xsolve_smem(16, 4, m) <= 220 * 1024) return 2;
     if (xsolve_smem(16, 3, m) <= 220 * 1024) return 3;
+    if (xsolve_smem(16, 2, m) <= 220 * 1024) return 4;  // the dense leaves of clustered inputs
+    if (xsolve_smem(8, 2, m) <= 220 * 1024) return 5;   // (m up to 2,944: 8-column tiles, 4 warps)
     return -1;
   };
   std::vector<XSolveDesc> h(hin);
-  std::vector<int> maps[4];
-  int maxm[4] = {0, 0, 0, 0};
+  std::vector<int> maps[6];
+  int maxm[6] = {0, 0, 0, 0, 0, 0};
   for (size_t p = 0; p < h.size(); p++) {
     if (h[p].m <= 0) continue;
     const int cfg = cfg_of(h[p].m);
     if (cfg < 0) invalid("pivot block too large for the X solve (m = " + std::to_string(h[p].m) + ")");
-    const int tw = cfg >= 2 ? 16 : 32;
+    const int tw = cfg == 5 ? 8 : cfg >= 2 ? 16 : 32;
     std::vector<int>& map = maps[cfg];
     h[p].tile0 = int(map.size());
     maxm[cfg] = std::max(maxm[cfg], h[p].m);
     for (int t = 0, tiles = ceil_div(h[p].w, tw); t < tiles; t++) map.push_back(int(p));
   }
-  if (maps[0].empty() && maps[1].empty() && maps[2].empty() && maps[3].empty()) return;
+  bool any = false;
+  for (auto& mp_ : maps) any |= !mp_.empty();
+  if (!any) return;
   const XSolveDesc* dd = upload(ws, h, s, st);
-  for (int cfg = 0; cfg < 4; cfg++) {
+  for (int cfg = 0; cfg < 6; cfg++) {
     if (maps[cfg].empty()) continue;
-    const int tw = cfg >= 2 ? 16 : 32;
-    const int stages = (cfg == 0 || cfg == 3) ? 3 : 4;
+    const int tw = cfg == 5 ? 8 : cfg >= 2 ? 16 : 32;
+    const int stages = cfg >= 4 ? 2 : (cfg == 0 || cfg == 3) ? 3 : 4;
+    const int threads = cfg == 5 ? 128 : 256;
     const int* dm = upload(ws, maps[cfg], s, st);
     const size_t smem = xsolve_smem(tw, stages, maxm[cfg]);
     const unsigned grid = unsigned(maps[cfg].size());
@@ -1064,14 +1069,16 @@ void launch_lu_solve_x(const std::vector<XSolveDesc>& hin, Arena& ws, Staging& s
         if (ready.insert(reinterpret_cast<const void*>(kern)).second)
           CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
       }
-      kern<<<grid, 256, smem, s>>>(dd, dm);
+      kern<<<grid, threads, smem, s>>>(dd, dm);
       CK_LAUNCH();
     };
     // every pivot is handled by exactly one of the two launches (lu_xsolve_kernel)
     if (cfg == 0) { go(lu_xsolve_kernel<32, 3, false>); go(lu_xsolve_kernel<32, 3, true>); }
     else if (cfg == 1) { go(lu_xsolve_kernel<32, 4, false>); go(lu_xsolve_kernel<32, 4, true>); }
     else if (cfg == 2) { go(lu_xsolve_kernel<16, 4, false>); go(lu_xsolve_kernel<16, 4, true>); }
-    else { go(lu_xsolve_kernel<16, 3, false>); go(lu_xsolve_kernel<16, 3, true>); }
+    else if (cfg == 3) { go(lu_xsolve_kernel<16, 3, false>); go(lu_xsolve_kernel<16, 3, true>); }
+    else if (cfg == 4) { go(lu_xsolve_kernel<16, 2, false>); go(lu_xsolve_kernel<16, 2, true>); }
+    else { go(lu_xsolve_kernel<8, 2, false, 4>); go(lu_xsolve_kernel<8, 2, true, 4>); }
   }
 }
 

@@ -181,7 +181,7 @@ static void build_lists(TreeH* t) {
   }
 }
 
-TreeH* tree_build(const double* pts_in, int64_t n, int dim, int depth, bool device_ptr) {
+TreeH* tree_build(const double* pts_in, int64_t n, int dim, int depth, bool device_ptr, bool allow_empty) {
   ensure_device();
   if (dim < 1 || dim > 3) invalid("dim must be 1, 2 or 3, got " + std::to_string(dim));
   if (n <= 0) invalid("points must have shape (n, dim) with n >= 1");
@@ -251,9 +251,10 @@ TreeH* tree_build(const double* pts_in, int64_t n, int dim, int depth, bool devi
     long long i = (long long)(best / (unsigned long long)n), j = (long long)(best % (unsigned long long)n);
     invalid("duplicate points at indices " + std::to_string(i) + " and " + std::to_string(j));
   }
-  for (int64_t c = 0; c < nleaf; c++)
+  for (int64_t c = 0; c < nleaf && !allow_empty; c++)
     if (cnt[c] == 0)  // uniform trees only, as the reference (ifmm/geometry.py:191-195)
       invalid("leaf cell " + std::to_string(c) + " is empty at depth " + std::to_string(depth));
+  t->sparse = allow_empty;
   build_lists(t.get());
   return t.release();
 }

@@ -162,14 +162,18 @@ class ClusterTree:
         return int(self.leaf_offsets[index * step]), int(self.leaf_offsets[(index + 1) * step])
 
 
-def build_tree(ps: PointSet, depth: int) -> ClusterTree:
+def build_tree(ps: PointSet, depth: int, allow_empty_leaves: bool = False) -> ClusterTree:
     """GPU tree build (ifmm/geometry.py:174-226); raises ValueError like the
-    reference for depth < 2, duplicate points and empty leaves."""
+    reference for depth < 2, duplicate points and empty leaves.
+
+    allow_empty_leaves (extension, for clustered inputs such as BASELINE config
+    4's Gaussian mixture): leaf cells without points are accepted; their
+    clusters carry no unknowns."""
     if not isinstance(ps, PointSet):
         raise TypeError("build_tree expects a PointSet")
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib.ifmm_tree_build(_lib.ptr(ps.points), len(ps), ps.dim, int(depth), _lib.PTR_HOST,
-                                        ctypes.byref(h)))
+    fn = _lib.lib.ifmm_tree_build_sparse if allow_empty_leaves else _lib.lib.ifmm_tree_build
+    _lib.check(fn(_lib.ptr(ps.points), len(ps), ps.dim, int(depth), _lib.PTR_HOST, ctypes.byref(h)))
     return ClusterTree(h, ps, int(depth))
 
 
