@@ -837,6 +837,25 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     own.push_back(t);
   }
   fill_off[np] = int(fh.size());
+  // Pivot LU by size class (register panels up to 256 / 768 rows, shared-memory
+  // panels beyond) when a large batch mixes sizes: clustered inputs put
+  // few-point and thousand-point cells in one batch, and one launch chain sized
+  // for the largest matrix would drag thousands of finished small ones through
+  // every step (C4 leaf level: 1.15 s of LU).  Batches of similar sizes, and the
+  // small batches of the coarse levels (where a second chain only adds latency),
+  // stay one class.  Own pivots are taken in class order (stable); the decision
+  // and each class's panel width follow the whole batch (all ranks), so the
+  // factors of a pivot do not depend on the sharding.
+  int class_cnt[3] = {0, 0, 0};
+  auto size_class = [](int m) { return m <= 256 ? 0 : m <= 768 ? 1 : 2; };
+  for (int t = 0; t < np; t++) class_cnt[size_class(P[t].m)]++;
+  const bool lu_split = (class_cnt[0] >= 512 && class_cnt[1] + class_cnt[2] > 0) ||
+                        (class_cnt[0] + class_cnt[1] >= 512 && class_cnt[2] > 0);
+  auto lu_class = [&](int m) { return lu_split ? size_class(m) : 0; };
+  int class_maxm[3] = {0, 0, 0};
+  for (int t = 0; t < np; t++) class_maxm[lu_class(P[t].m)] = std::max(class_maxm[lu_class(P[t].m)], P[t].m);
+  if (lu_split)
+    std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return lu_class(P[a].m) < lu_class(P[b].m); });
   const int no = int(own.size());
   // per-batch device results of this rank's pivots / fills
   double* d_nS = ws_.alloc_n<double>(std::max(1, no));
@@ -903,7 +922,14 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       tm_.begin(PH_GJ);
       launch_norm1(dmd, nc_, maxm, d_nS + u0, s_);
       // panel width from the whole batch (across chunks and ranks): same arithmetic as one launch
-      batched_lu(md, dmd, d_info + u0, ws_, st_, s_, gmaxm, &work_->ahead);
+      for (size_t q0 = 0; q0 < md.size();) {
+        const int c = lu_class(md[q0].m);
+        size_t q1 = q0;
+        while (q1 < md.size() && lu_class(md[q1].m) == c) q1++;
+        std::vector<MatDesc> sub(md.begin() + q0, md.begin() + q1);
+        batched_lu(sub, dmd + q0, d_info + u0 + q0, ws_, st_, s_, class_maxm[c], &work_->ahead);
+        q0 = q1;
+      }
       const LuDiag dg = launch_lu_diag_inv(md, dmd, ws_, st_, s_, tol_);
       // the condition estimates only gate the batch's read-back: run them on
       // the side stream, overlapped with the X solve, Schur update and fill

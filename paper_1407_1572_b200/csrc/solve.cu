@@ -619,7 +619,7 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     launch_rec_solves(b, F, V, G, T, nr, true, ws, s);
     const int nrec = b.rec1 - b.rec0;
     if (mm) {
-      cpl_fwd_mm_kernel<<<dim3(nrec, (b.maxw + GBM - 1) / GBM, nqc), GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0,
+      cpl_fwd_mm_kernel<<<dim3(nrec, std::max(1, (b.maxw + GBM - 1) / GBM), nqc), GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0,
                                                                                              F->d_g_off, V, G, nr);
     } else {
       // column dots split finely: >= 8 CTAs per SM in total (few large records
@@ -666,7 +666,7 @@ void solve(FactorH* F, const double* rhs, double* x, int64_t nrhs, bool device_p
     }
     const int nrec = b.rec1 - b.rec0;
     if (mm) {
-      cpl_bwd_mm_kernel<<<dim3(nrec, (b.maxn + GBM - 1) / GBM, nqc), GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0,
+      cpl_bwd_mm_kernel<<<dim3(nrec, std::max(1, (b.maxn + GBM - 1) / GBM), nqc), GTHREADS, MM_SMEM, s>>>(b.d_recs, b.rec0,
                                                                                              F->d_g_off, V, T, nr);
     } else {
       const dim3 grid(nrec, solve_chunks(b));
