@@ -1482,6 +1482,9 @@ void Factorizer::factor_top() {
 
 FactorH* Factorizer::run() {
   auto t0 = std::chrono::steady_clock::now();
+  // exact mode keeps identity bases and adds fills to the far blocks as they are:
+  // a rotated basis would break that
+  if (rank_tol_ > 0.0 && !(tol_ > 0.0)) invalid("rank_tol needs a compression tolerance tol > 0 (exact mode keeps identity bases)");
   if (getenv("IFMM_HOST_PROF")) fprintf(stderr, "host factorize begin\n");
   tm_.on = (flags_ & IFMM_FLAG_TIMING) != 0;
   tm_.s = s_;

@@ -101,6 +101,9 @@ def test_rank_control_arguments(ifmm):
     for bad in (0.0, -1e-3, 1.0, 2.0):
         with pytest.raises(ValueError):
             ifmm.factorize(store, tree, rank_tol=bad)
+    exact = ifmm.init_operators(tree, ifmm.baseline_kernel("log_r", N), p=4, tol=0.0)
+    with pytest.raises(ValueError, match="exact mode"):
+        ifmm.factorize(exact, tree, rank_tol=1e-7)
     f = ifmm.factorize(store, tree, rank_tol=1e-7)  # depth 2: only the top-level dimension can shrink
     b = O.baseline_rhs(N, "normal")
     x = ifmm.solve(f, b)

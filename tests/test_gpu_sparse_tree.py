@@ -75,3 +75,20 @@ def test_mixture_on_a_tree_with_empty_cells(ifmm, n, depth, p, tol, rank_tol, bo
     x2 = ifmm.solve(f, b, refine=2)
     res2 = np.linalg.norm(ifmm.fmm_matvec(store, tree, x2) - b) / nb
     assert res2 <= max(1e-3 * bound, 100 * tol), (res, res2)
+
+
+def test_sparse_tree_through_the_estimator_and_sharded(ifmm):
+    """IfmmSolver(allow_empty_leaves=True, rank_tol=...) on the mixture, and the same
+    factorization on 4 virtual ranks (bit-identical to one GPU)."""
+    from paper_1407_1572_b200 import distributed as D
+    n = 16384
+    X = _mixture(n)
+    k = ifmm.baseline_kernel("inv_r", n)
+    est = ifmm.IfmmSolver(kernel="inv_r", tol=1e-6, p=4, depth=5, kernel_scale=k.scale, kernel_shift=k.shift,
+                          rank_tol=1e-7, allow_empty_leaves=True).fit(X)
+    b = np.random.default_rng(1).standard_normal(n)
+    x = est.solve(b)
+    assert np.linalg.norm(est.matvec(x) - b) / np.linalg.norm(b) <= 1e-3
+    fs = D.factorize_emulated(est.store_, est.tree_, 4, rank_tol=1e-7)
+    xs = D.solve_emulated(fs, b)
+    assert np.array_equal(xs[0], x) and np.array_equal(xs[3], x)
