@@ -136,6 +136,7 @@ class Tree:
     grid: dict                  # k -> (4^k, dim) int
     nbr: dict                   # k -> list of sorted lists (self included)
     ilist: dict                 # k -> list of sorted lists
+    sparse: bool = False        # built with allow_empty (extension): leaf cells may hold no points
 
     def n_clusters(self, k):
         return 1 << (self.dim * k)
@@ -171,8 +172,10 @@ def check_points(points):
     return pts
 
 
-def build_tree(points, depth) -> Tree:
-    """ifmm/geometry.py:174-226 and compute_lists :229-262."""
+def build_tree(points, depth, allow_empty=False) -> Tree:
+    """ifmm/geometry.py:174-226 and compute_lists :229-262.  allow_empty (extension, NOT
+    reference behaviour -- the reference raises, ifmm/geometry.py:191-195): accept leaf cells
+    without points; the checker of the GPU's build_tree(allow_empty_leaves=True)."""
     pts = check_points(points)
     if depth < 2:
         raise ValueError("depth must be >= 2")
@@ -184,7 +187,7 @@ def build_tree(points, depth) -> Tree:
     codes = morton(cell, depth)
     perm = np.argsort(codes, kind="stable")
     cnt = np.bincount(codes[perm], minlength=1 << (dim * depth))
-    if cnt.min() == 0:
+    if cnt.min() == 0 and not allow_empty:
         raise ValueError(f"leaf cell {int(np.argmin(cnt))} is empty at depth {depth}")
     off = np.concatenate([[0], np.cumsum(cnt)])
     grid, nbr, il = {}, {}, {}
@@ -208,7 +211,9 @@ def build_tree(points, depth) -> Tree:
             cand = [c for pn in nbr[k - 1][i >> dim] for c in range(pn << dim, (pn + 1) << dim)]
             out.append(sorted(c for c in cand if c not in s))
         il[k] = out
-    return Tree(depth, dim, pts[perm], perm, off, grid, nbr, il)
+    t = Tree(depth, dim, pts[perm], perm, off, grid, nbr, il)
+    t.sparse = bool(allow_empty)
+    return t
 
 
 def elimination_order(tree: Tree, k: int, order: str):
@@ -491,11 +496,16 @@ def init_operators(tree: Tree, spec: KernelSpec, p=8, tol=1e-14) -> Blocks:
             for i in range(nc):
                 il = tree.ilist[k][i]
                 if k == K:
-                    B = tinterp(tree.leaf_pts(i), tree.center(k, i), tree.half(k), p)
+                    lp = tree.leaf_pts(i)
+                    B = tinterp(lp, tree.center(k, i), tree.half(k), p) if len(lp) else np.zeros((0, nd))
                 else:
                     B = np.concatenate([raw[(k + 1, c)] @ tr[c - (i << d)]
                                         for c in range((i << d), (i + 1) << d)], axis=0)
                 ni = B.shape[0]
+                if ni == 0:  # an empty cluster (sparse trees): no unknowns
+                    st.U[(k, i)] = np.zeros((0, 0))
+                    raw[(k, i)] = np.zeros((0, nd))
+                    continue
                 row = (np.concatenate([kblock(spec, nodes[i], nodes[j]) for j in il], axis=1)
                        if il else np.zeros((nd, 0)))
                 Uf, s, _ = svd(row, full_matrices=False)
@@ -691,7 +701,7 @@ def _squeeze_hybrid(st, k, p, q, tol, stats):
     if F is None:
         return
     A, B, bad = _compress(F, tol)
-    if bad:
+    if bad and not st.tree.sparse:  # sparse trees (extension): a full-rank ACA is exact and is absorbed
         stats.dense_kept += 1
         return
     stats.compressed += 1
@@ -713,7 +723,7 @@ def _squeeze_near(st, k, p, q, tol, stats):
     if F is None:
         return
     A, B, bad = _compress(F, tol)
-    if bad:
+    if bad and not st.tree.sparse:  # sparse trees (extension): a full-rank ACA is exact and is absorbed
         stats.dense_kept += 1
         return
     stats.compressed += 1
@@ -736,6 +746,9 @@ def _eliminate(st: Blocks, k, i, tol, fac: Factor, stats: Stats, ils, dead):
     """One cluster elimination (ifmm/solver.py:195-311)."""
     U = st.U[(k, i)]
     n, r = U.shape
+    if n + r == 0:  # an empty cluster of a sparse tree (extension): nothing to eliminate, no record
+        dead[i] = True
+        return
     S = np.zeros((n + r, n + r))
     S[:n, :n] = st.get("p2p", k, i, i)
     S[:n, n:] = U
@@ -949,7 +962,8 @@ def solve(fac: Factor, rhs):
         k, i = rec.level, rec.index
         if k != cur:
             for c in range(tree.n_clusters(k)):
-                bx[(k, c)] = np.concatenate([bz[(k + 1, ch)] for ch in range(c << d, (c + 1) << d)])
+                bx[(k, c)] = np.concatenate([bz.get((k + 1, ch), np.zeros((0, nr)))
+                                             for ch in range(c << d, (c + 1) << d)])
             cur = k
         g = lu_solve(rec.lu, np.concatenate([bx[(k, i)], np.zeros((rec.r, nr))]))
         gs.append(g)
@@ -959,7 +973,7 @@ def solve(fac: Factor, rhs):
             bz[(k, j)] -= st.blk["p2l"][(k, j, i)] @ g[:rec.n]
         bz[(k, i)] = g[rec.n:].copy()
     off = fac.top_off
-    yt = lu_solve(fac.top_lu, np.concatenate([bz[(2, c)] for c in range(tree.n_clusters(2))]))
+    yt = lu_solve(fac.top_lu, np.concatenate([bz.get((2, c), np.zeros((0, nr))) for c in range(tree.n_clusters(2))]))
     y = {(2, c): yt[off[c]:off[c + 1]] for c in range(tree.n_clusters(2))}
     xv = {}
     by = {}
@@ -970,7 +984,8 @@ def solve(fac: Factor, rhs):
             i = rec.index
             top = np.zeros((rec.n, nr))
             for j in rec.xp:
-                top += st.blk["p2p"][(k, i, j)] @ xv[(k, j)]
+                if (k, j) in xv:  # (an empty cluster of a sparse tree has no unknowns)
+                    top += st.blk["p2p"][(k, i, j)] @ xv[(k, j)]
             for j in rec.yp:
                 top += st.blk["m2p"][(k, i, j)] @ y[(k, j)]
             sol = g - lu_solve(rec.lu, np.concatenate([top, -y[(k, i)]]))
@@ -981,7 +996,8 @@ def solve(fac: Factor, rhs):
                     y[(k + 1, ch)] = sol[o[c]:o[c + 1]]
     out = np.empty((len(tree.points), nr))
     for i in range(tree.n_clusters(K)):
-        out[tree.leaf_off[i]:tree.leaf_off[i + 1]] = xv[(K, i)]
+        if (K, i) in xv:
+            out[tree.leaf_off[i]:tree.leaf_off[i + 1]] = xv[(K, i)]
     res = np.empty_like(out)
     res[tree.perm] = out
     return res[:, 0] if one else res

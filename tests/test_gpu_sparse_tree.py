@@ -92,3 +92,35 @@ def test_sparse_tree_through_the_estimator_and_sharded(ifmm):
     fs = D.factorize_emulated(est.store_, est.tree_, 4, rank_tol=1e-7)
     xs = D.solve_emulated(fs, b)
     assert np.array_equal(xs[0], x) and np.array_equal(xs[3], x)
+
+
+@pytest.mark.parametrize("rank_tol", [None, 1e-7])
+def test_sparse_tree_against_the_oracle(ifmm, rank_tol):
+    """The oracle's restatement of the same extension (oracle build_tree(allow_empty=True):
+    empty clusters skipped, full-rank fills absorbed), same colour order: tree bit-exact,
+    ranks and top dimension within 5 %, residual within 2x, solutions within the
+    compression error."""
+    from oracle import ifmm_oracle as O
+    n, depth, p, tol = 4096, 4, 4, 1e-6
+    X = _mixture(n)
+    tree = ifmm.build_tree(ifmm.PointSet(2, X), depth, allow_empty_leaves=True)
+    T = O.build_tree(X, depth, allow_empty=True)
+    assert np.array_equal(tree.point_permutation, T.perm)
+    assert np.array_equal(tree.leaf_offsets, T.leaf_off)
+    store = ifmm.init_operators(tree, ifmm.baseline_kernel("inv_r", n), p=p, tol=tol)
+    f = ifmm.factorize(store, tree, rank_tol=rank_tol)
+    b = np.random.default_rng(1).standard_normal(n)
+    x = ifmm.solve(f, b)
+    res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
+    spec = O.baseline_kernel("inv_r", n)
+    fo = O.factorize(O.init_operators(T, spec, p, tol), order="colour9", rank_tol=rank_tol)
+    xo = O.solve(fo, b)
+    res_o = np.linalg.norm(O.fmm_matvec(O.init_operators(T, spec, p, tol), xo) - b) / np.linalg.norm(b)
+    assert res <= max(10 * tol, 2 * res_o), (res, res_o)
+    assert f.n_records == len(fo.recs)  # empty clusters are eliminated by neither
+    assert abs(f.top_dim - int(fo.top_off[-1])) <= 0.05 * fo.top_off[-1], (f.top_dim, fo.top_off[-1])
+    rec = np.array([(r.level, r.r) for r in f.records])
+    for k in range(depth, 1, -1):
+        ro = sum(r.r for r in fo.recs if r.level == k)
+        assert abs(int(rec[rec[:, 0] == k, 1].sum()) - ro) <= 0.05 * ro, (k, ro)
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) <= 100 * tol

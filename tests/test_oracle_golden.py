@@ -92,3 +92,27 @@ def test_oracle_rank_control_extension():
         x = O.solve(f1, b)
         res = np.linalg.norm(O.fmm_matvec(O.init_operators(tree, spec, p, tol), x) - b) / np.linalg.norm(b)
         assert res <= 10 * tol, (order, res)
+
+
+def test_oracle_sparse_tree_extension():
+    """oracle build_tree(allow_empty=True) (the checker of the GPU's allow_empty_leaves
+    extension, not reference behaviour): exact mode equals the dense LU solution on a tree
+    with empty cells; with compression no fill is kept dense; the default still raises."""
+    import bench
+    from oracle import ifmm_oracle as O
+    n, depth = 1024, 3
+    X = bench.mixture_points(n)
+    with pytest.raises(ValueError, match="empty"):
+        O.build_tree(X, depth)
+    T = O.build_tree(X, depth, allow_empty=True)
+    assert (np.diff(T.leaf_off) == 0).any()
+    spec = O.baseline_kernel("inv_r", n)
+    b = np.random.default_rng(1).standard_normal(n)
+    x = O.solve(O.factorize(O.init_operators(T, spec, 4, 0.0)), b)
+    xd = np.linalg.solve(O.dense_matrix(spec, X), b)
+    assert np.linalg.norm(x - xd) / np.linalg.norm(xd) <= 1e-10
+    fac = O.factorize(O.init_operators(T, spec, 4, 1e-6), order="colour9")
+    assert sum(s.dense_kept for s in fac.stats.values()) == 0
+    x = O.solve(fac, b)
+    res = np.linalg.norm(O.fmm_matvec(O.init_operators(T, spec, 4, 1e-6), x) - b) / np.linalg.norm(b)
+    assert res <= 1e-4
