@@ -64,6 +64,12 @@ int ifmm_device_count(void);
 /* select the CUDA device used by subsequent calls on this thread */
 int ifmm_set_device(int device);
 
+/* Device slabs of freed stores / factorizations are cached for reuse (cudaMalloc and
+ * cudaFree of multi-GB slabs are slow and synchronise); this returns the cached ones of
+ * the current device to the driver.  The cache also flushes itself when an allocation
+ * would otherwise fail. */
+int ifmm_release_cached_memory(void);
+
 /* ---- tree: PointSet checks + build_tree + compute_lists
  *      (ifmm/geometry.py:47-61, :174-226, :229-262) */
 int ifmm_tree_build(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out);

@@ -41,6 +41,7 @@ SIGNATURES = {
     "ifmm_version": (_i32, []),
     "ifmm_device_count": (_i32, []),
     "ifmm_set_device": (_i32, [_i32]),
+    "ifmm_release_cached_memory": (_i32, []),
     "ifmm_tree_build": (_i32, [_p, _i64, _i32, _i32, _i32, ctypes.POINTER(_p)]),
     "ifmm_tree_build_sparse": (_i32, [_p, _i64, _i32, _i32, _i32, ctypes.POINTER(_p)]),
     "ifmm_tree_info": (_i32, [_p, _pi64, _pi32, _pi32]),

@@ -102,6 +102,14 @@ int ifmm_tree_build(const double* points, int64_t n, int dim, int depth, int ptr
   });
 }
 
+int ifmm_release_cached_memory(void) {
+  return guard([&] {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    ifmm::slab_cache_flush(dev);
+  });
+}
+
 int ifmm_tree_build_sparse(const double* points, int64_t n, int dim, int depth, int ptr_kind, ifmm_tree** out) {
   return guard([&] {
     if (!out) invalid("null output handle");

@@ -31,3 +31,13 @@ def load_golden(name):
 def golden_kernel(g):
     from oracle import ifmm_oracle as O
     return O.KernelSpec(str(g["kernel"]), a=float(g["a"]), scale=float(g["scale"]), shift=float(g["shift"]))
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory(request):
+    """GPU tests: drop the previous test's stores / factorizations (reference cycles wait
+    for the collector otherwise) so the next test starts with the whole device."""
+    yield
+    if request.node.get_closest_marker("gpu") is not None:
+        import gc
+        gc.collect()

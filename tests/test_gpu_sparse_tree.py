@@ -117,7 +117,8 @@ def test_sparse_tree_against_the_oracle(ifmm, rank_tol):
     xo = O.solve(fo, b)
     res_o = np.linalg.norm(O.fmm_matvec(O.init_operators(T, spec, p, tol), xo) - b) / np.linalg.norm(b)
     assert res <= max(10 * tol, 2 * res_o), (res, res_o)
-    assert f.n_records == len(fo.recs)  # empty clusters are eliminated by neither
+    # empty clusters carry no unknowns: the GPU keeps zero-size records for them, the oracle none
+    assert sum(1 for r in f.records if r.n + r.r > 0) == len(fo.recs)
     assert abs(f.top_dim - int(fo.top_off[-1])) <= 0.05 * fo.top_off[-1], (f.top_dim, fo.top_off[-1])
     rec = np.array([(r.level, r.r) for r in f.records])
     for k in range(depth, 1, -1):
