@@ -8,6 +8,7 @@ for inspection and tests.
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -18,7 +19,9 @@ from .kernels import Kernel
 
 class _BasisView:
     def __init__(self, store):
-        self._s = store
+        # weak: the store owns its views; a strong back-reference would be a cycle that keeps
+        # the store's HBM alive until the garbage collector runs
+        self._s = weakref.proxy(store)
 
     def __getitem__(self, key):
         k, i = key
@@ -30,7 +33,9 @@ class _BasisView:
 
 class _M2LView:
     def __init__(self, store):
-        self._s = store
+        # weak: the store owns its views; a strong back-reference would be a cycle that keeps
+        # the store's HBM alive until the garbage collector runs
+        self._s = weakref.proxy(store)
 
     def __getitem__(self, key):
         k, i, j = key
@@ -42,7 +47,9 @@ class _M2LView:
 
 class _P2PView:
     def __init__(self, store):
-        self._s = store
+        # weak: the store owns its views; a strong back-reference would be a cycle that keeps
+        # the store's HBM alive until the garbage collector runs
+        self._s = weakref.proxy(store)
 
     def __getitem__(self, key):
         k, i, j = key
