@@ -176,6 +176,11 @@ struct RecordH {
   double* c;         // n x w (ld n); columns [w - r, w) are zero
   int* pos;          // w absolute positions in the solve vector
   int64_t xoff;      // absolute position of x_i
+  // larger pivots: inverted 64 x 64 diagonal blocks of L and U (per block: L_kk^-1, U_kk^-1,
+  // column-major), kept with the record so the single-rhs sweeps replace the substitution
+  // chains by block mat-vecs; *pflag != 0: a block is too ill-conditioned for that (lu.cu)
+  const double* dinv;
+  const unsigned char* pflag;
 };
 
 struct BatchH {

@@ -770,6 +770,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
     double *S, *C, *Xt, *Xb;
     int* perm;
     int rec;
+    const double* dinv = nullptr;
+    const unsigned char* pflag = nullptr;
   };
   // Every rank walks all pivots of the batch (metadata); device work is done
   // for its own pivots only (all of them on one GPU).  The batch's fills are
@@ -930,7 +932,23 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         batched_lu(sub, dmd + q0, d_info + u0 + q0, ws_, st_, s_, class_maxm[c], &work_->ahead);
         q0 = q1;
       }
-      const LuDiag dg = launch_lu_diag_inv(md, dmd, ws_, st_, s_, tol_);
+      const LuDiag dg = launch_lu_diag_inv(md, dmd, ws_, st_, s_, tol_, &F_->arena);
+      // larger pivots keep their inverted diagonal blocks for the single-rhs sweeps (solve.cu)
+      {
+        CopyBatch keep;
+        for (int u = u0; u < u1; u++) {
+          PivInfo& I = P[own[u]];
+          I.dinv = nullptr;
+          I.pflag = dg.pflag + (u - u0);
+          if (I.m < SOLVE_BLK_MIN_M) continue;
+          const int nb = (I.m + LU_XB - 1) / LU_XB;
+          const int len = nb * 2 * LU_XB * LU_XB;
+          double* d = F_->arena.alloc_n<double>(size_t(len));
+          keep.add(dg.dinv + dg.h_off[u - u0], len, d, len, len, 1);
+          I.dinv = d;
+        }
+        launch_copies(keep, ws_, st_, s_);
+      }
       // the condition estimates only gate the batch's read-back: run them on
       // the side stream, overlapped with the X solve, Schur update and fill
       // compression (which read the factors but never write them)
@@ -961,6 +979,8 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       R.perm = I.perm;
       R.c = I.C;
       R.pos = nullptr;  // set by finish_level (one block per level)
+      R.dinv = I.dinv;
+      R.pflag = I.pflag;
       I.rec = int(F_->recs.size());
       F_->recs.push_back(R);
       std::vector<SlotRef> sl;

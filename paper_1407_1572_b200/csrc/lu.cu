@@ -903,7 +903,7 @@ static size_t xsolve_smem(int tw, int stages, int m) {
 }
 
 LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, Arena& ws, Staging& st,
-                          cudaStream_t s, double tol) {
+                          cudaStream_t s, double tol, Arena* keep) {
   std::vector<int64_t> off(h.size() + 1, 0);
   int maxnb = 0;
   for (size_t p = 0; p < h.size(); p++) {
@@ -914,7 +914,7 @@ LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, 
   LuDiag dg;
   dg.dinv = ws.alloc_n<double>(size_t(std::max<int64_t>(1, off.back())));
   dg.flags = ws.alloc_n<unsigned char>(size_t(std::max<int64_t>(1, off.back() / (XB * XB))));
-  dg.pflag = ws.alloc_n<unsigned char>(std::max<size_t>(1, h.size()));
+  dg.pflag = (keep ? *keep : ws).alloc_n<unsigned char>(std::max<size_t>(1, h.size()));
   CK(cudaMemsetAsync(dg.pflag, 0, std::max<size_t>(1, h.size()), s));
   dg.d_off = upload(ws, off, s, st);
   dg.h_off = off;

@@ -283,6 +283,7 @@ void batched_lu(const std::vector<MatDesc>& h, const MatDesc* d_desc, int* d_inf
 // U_kk^-1, column-major 64 x 64 each, identity-padded past m): matrix p's
 // block k pair starts at dinv + h_off[p] + 8192 k.  They make the blocked
 // triangular solves GEMM-shaped (the X solve refines each block solve once).
+constexpr int SOLVE_BLK_MIN_M = 192;  // pivots from this size keep inverted diagonal blocks for the solve
 constexpr int LU_XB = 64;  // block size of the blocked triangular solves (X solve, condition estimate)
 struct LuDiag {
   double* dinv = nullptr;
@@ -293,8 +294,9 @@ struct LuDiag {
 };
 // tol: the fill tolerance the X solve must support (decides which block solves
 // get a refinement step); <= 0 refines every block.
+// keep: arena for the per-matrix flags when they must outlive the batch workspace (solve records)
 LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, Arena& ws, Staging& st,
-                          cudaStream_t s, double tol);
+                          cudaStream_t s, double tol, Arena* keep = nullptr);
 
 // out[p] = dlacn2 estimate of ||S_p^-1||_1 from the LU factors of S_p.
 void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, const LuDiag& dg, double* out, cudaStream_t s);

@@ -37,6 +37,63 @@ __device__ __forceinline__ double rec_rhs(const RecordH& R, bool fwd, int i, int
   return i < R.n ? T[(size_t)i * nrhs + q] : -V[(int64_t)R.pos[wl + i - R.n] * nrhs + q];
 }
 
+// Triangular solves of one shared-memory vector with the record's inverted
+// 64 x 64 diagonal blocks (RecordH::dinv): per block a 64 x 64 mat-vec (four
+// threads per row, partial sums combined in shared memory) instead of two
+// 32-step substitution chains on one warp, then the block's column strip
+// updates the remaining rows (thread per row, coalesced column reads).  The
+// coarse levels -- a few records of several hundred rows per batch -- are
+// bound by exactly that chain.  part: SB doubles of shared memory.
+__device__ __forceinline__ double blk_matvec_part(const double* __restrict__ Ti, const double* x, int kb, int bb,
+                                                  int row, int part) {
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < LU_XB / 4; c++) {
+    const int cc = part * (LU_XB / 4) + c;
+    s = fma(Ti[row + LU_XB * cc], cc < bb ? x[kb + cc] : 0.0, s);
+  }
+  return s;
+}
+__device__ __forceinline__ void blk_row_update(const double* __restrict__ LU, int ld, int r, int kb, int bb, double* x) {
+  double s = 0.0;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {  // 32 loads in flight at a time
+    double a[32];
+#pragma unroll
+    for (int c = 0; c < 32; c++) a[c] = 32 * h + c < bb ? LU[r + (size_t)(kb + 32 * h + c) * ld] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 32; c++) s = fma(a[c], 32 * h + c < bb ? x[kb + 32 * h + c] : 0.0, s);
+  }
+  x[r] -= s;
+}
+__device__ inline void cta_trsv_lower_unit_blk(const double* __restrict__ LU, int ld, int m, double* x,
+                                               const double* __restrict__ dinv, double* part) {
+  const int tid = threadIdx.x, row = tid & (LU_XB - 1), q = tid >> 6;
+  for (int kb = 0, k = 0; kb < m; kb += LU_XB, k++) {
+    const int bb = min(LU_XB, m - kb);
+    part[q * LU_XB + row] = blk_matvec_part(dinv + (size_t)k * 2 * LU_XB * LU_XB, x, kb, bb, row, q);
+    __syncthreads();
+    if (tid < bb) x[kb + tid] = (part[tid] + part[LU_XB + tid]) + (part[2 * LU_XB + tid] + part[3 * LU_XB + tid]);
+    __syncthreads();
+    for (int r = kb + bb + tid; r < m; r += blockDim.x) blk_row_update(LU, ld, r, kb, bb, x);
+    __syncthreads();
+  }
+}
+__device__ inline void cta_trsv_upper_blk(const double* __restrict__ LU, int ld, int m, double* x,
+                                          const double* __restrict__ dinv, double* part) {
+  const int tid = threadIdx.x, row = tid & (LU_XB - 1), q = tid >> 6;
+  for (int k = (m - 1) / LU_XB; k >= 0; k--) {
+    const int kb = k * LU_XB, bb = min(LU_XB, m - kb);
+    part[q * LU_XB + row] =
+        blk_matvec_part(dinv + (size_t)k * 2 * LU_XB * LU_XB + LU_XB * LU_XB, x, kb, bb, row, q);
+    __syncthreads();
+    if (tid < bb) x[kb + tid] = (part[tid] + part[LU_XB + tid]) + (part[2 * LU_XB + tid] + part[3 * LU_XB + tid]);
+    __syncthreads();
+    for (int r = tid; r < kb; r += blockDim.x) blk_row_update(LU, ld, r, kb, bb, x);
+    __syncthreads();
+  }
+}
+
 template <bool FWD>
 __global__ void __launch_bounds__(SB, 3) rec_solve_vec_kernel(const RecordH* __restrict__ recs, int rec0,
                                                            const int64_t* __restrict__ g_off, double* V, double* G,
@@ -48,8 +105,14 @@ __global__ void __launch_bounds__(SB, 3) rec_solve_vec_kernel(const RecordH* __r
   const int64_t go = g_off[rec0 + blockIdx.x];
   for (int l = threadIdx.x; l < m; l += blockDim.x) y[l] = rec_rhs(R, FWD, R.perm[l], wl, V, T + go, 1, 0);
   __syncthreads();
-  cta_trsv_lower_unit(R.lu, m, m, y);
-  cta_trsv_upper(R.lu, m, m, y);
+  if (R.dinv != nullptr && *R.pflag == 0) {  // uniform over the CTA
+    __shared__ double part[SB];
+    cta_trsv_lower_unit_blk(R.lu, m, m, y, R.dinv, part);
+    cta_trsv_upper_blk(R.lu, m, m, y, R.dinv, part);
+  } else {
+    cta_trsv_lower_unit(R.lu, m, m, y);
+    cta_trsv_upper(R.lu, m, m, y);
+  }
   if (FWD) {
     for (int t = threadIdx.x; t < n; t += blockDim.x) G[go + t] = y[t];
     for (int t = threadIdx.x; t < r; t += blockDim.x) V[R.pos[wl + t]] += y[n + t];
