@@ -932,22 +932,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
         batched_lu(sub, dmd + q0, d_info + u0 + q0, ws_, st_, s_, class_maxm[c], &work_->ahead);
         q0 = q1;
       }
-      const LuDiag dg = launch_lu_diag_inv(md, dmd, ws_, st_, s_, tol_, &F_->arena);
-      // larger pivots keep their inverted diagonal blocks for the single-rhs sweeps (solve.cu)
-      {
-        CopyBatch keep;
-        for (int u = u0; u < u1; u++) {
-          PivInfo& I = P[own[u]];
-          I.dinv = nullptr;
-          I.pflag = dg.pflag + (u - u0);
-          if (I.m < SOLVE_BLK_MIN_M) continue;
-          const int nb = (I.m + LU_XB - 1) / LU_XB;
-          const int len = nb * 2 * LU_XB * LU_XB;
-          double* d = F_->arena.alloc_n<double>(size_t(len));
-          keep.add(dg.dinv + dg.h_off[u - u0], len, d, len, len, 1);
-          I.dinv = d;
-        }
-        launch_copies(keep, ws_, st_, s_);
+      // larger pivots keep their inverted diagonal blocks (written straight into the records'
+      // arena) for the single-rhs sweeps (solve.cu)
+      const LuDiag dg = launch_lu_diag_inv(md, dmd, ws_, st_, s_, tol_, &F_->arena, SOLVE_BLK_MIN_M);
+      for (int u = u0; u < u1; u++) {
+        PivInfo& I = P[own[u]];
+        I.pflag = dg.pflag + (u - u0);
+        I.dinv = I.m >= SOLVE_BLK_MIN_M ? dg.dinv + dg.h_off[u - u0] : nullptr;
       }
       // the condition estimates only gate the batch's read-back: run them on
       // the side stream, overlapped with the X solve, Schur update and fill
@@ -959,7 +950,7 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
       launch_lu_inv_norm1(dmd, nc_, maxm, dg, d_nSi + u0, sd.s);
       for (size_t q = 0; q < xd.size(); q++) {
         xd[q].dinv = dg.dinv + dg.h_off[q];
-        xd[q].dflag = dg.flags + dg.h_off[q] / (LU_XB * LU_XB);
+        xd[q].dflag = dg.flags + 2 * dg.h_foff[q];
         xd[q].pflag = dg.pflag + q;
       }
       CK(cudaEventRecord(sd.join, sd.s));

@@ -408,7 +408,8 @@ __global__ void __launch_bounds__(GTHREADS, 3) lu_update_kernel(const MatDesc* _
 // grid (matrix, block), 128 threads: thread t < 64 inverts column t of L_kk,
 // t >= 64 column t - 64 of U_kk.  Blocks past m are padded with the identity.
 __global__ void __launch_bounds__(128) lu_diag_inv_kernel(const MatDesc* __restrict__ desc,
-                                                          const int64_t* __restrict__ doff, double* dinv,
+                                                          const int64_t* __restrict__ doff,
+                                                          const int64_t* __restrict__ foff, double* dinv,
                                                           unsigned char* flags, unsigned char* pflag,
                                                           double kappa_max) {
   __shared__ double T[XB][XB + 1];
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(128) lu_diag_inv_kernel(const MatDesc* __restr
       b = fmax(b, cn[threadIdx.x][c][1]);
     }
     const bool refine = !(a * b <= kappa_max);
-    const size_t f = (size_t)(doff[blockIdx.x] / (2 * XB * XB)) + k;
+    const size_t f = (size_t)foff[blockIdx.x] + k;
     if (threadIdx.x == 0) flags[2 * f] = refine;
     else flags[2 * f + 1] = refine;
     if (refine) pflag[blockIdx.x] = 1;
@@ -903,27 +904,40 @@ static size_t xsolve_smem(int tw, int stages, int m) {
 }
 
 LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, Arena& ws, Staging& st,
-                          cudaStream_t s, double tol, Arena* keep) {
-  std::vector<int64_t> off(h.size() + 1, 0);
+                          cudaStream_t s, double tol, Arena* keep, int keep_min_m) {
+  std::vector<int64_t> off(h.size() + 1, 0), foff(h.size() + 1, 0);
   int maxnb = 0;
+  int64_t tot = 0;
   for (size_t p = 0; p < h.size(); p++) {
     const int nb = (h[p].m + XB - 1) / XB;
     maxnb = std::max(maxnb, nb);
-    off[p + 1] = off[p] + int64_t(nb) * 2 * XB * XB;
+    foff[p + 1] = foff[p] + nb;
+    const bool kept = keep != nullptr && h[p].m >= keep_min_m;
+    off[p] = kept ? -1 : tot;
+    if (!kept) tot += int64_t(nb) * 2 * XB * XB;
   }
   LuDiag dg;
-  dg.dinv = ws.alloc_n<double>(size_t(std::max<int64_t>(1, off.back())));
-  dg.flags = ws.alloc_n<unsigned char>(size_t(std::max<int64_t>(1, off.back() / (XB * XB))));
+  dg.dinv = ws.alloc_n<double>(size_t(std::max<int64_t>(1, tot)));
+  for (size_t p = 0; p < h.size(); p++)
+    if (off[p] < 0) {  // kept with the records: its own allocation, addressed relative to dinv
+      const int nb = (h[p].m + XB - 1) / XB;
+      const double* kp = keep->alloc_n<double>(size_t(nb) * 2 * XB * XB);
+      off[p] = (int64_t(reinterpret_cast<intptr_t>(kp)) - int64_t(reinterpret_cast<intptr_t>(dg.dinv))) /
+               int64_t(sizeof(double));
+    }
+  dg.flags = ws.alloc_n<unsigned char>(size_t(std::max<int64_t>(1, 2 * foff.back())));
   dg.pflag = (keep ? *keep : ws).alloc_n<unsigned char>(std::max<size_t>(1, h.size()));
   CK(cudaMemsetAsync(dg.pflag, 0, std::max<size_t>(1, h.size()), s));
   dg.d_off = upload(ws, off, s, st);
   dg.h_off = off;
+  dg.d_foff = upload(ws, foff, s, st);
+  dg.h_foff = foff;
   // refine a block solve when its inverted block's error kappa eps could reach
   // a hundredth of the tolerance (tol <= 0: always)
   const double kappa_max = tol > 0 ? 1e-2 * tol / 2.220446049250313e-16 : 0.0;
   if (!h.empty() && maxnb > 0) {
-    lu_diag_inv_kernel<<<dim3(unsigned(h.size()), unsigned(maxnb)), 128, 0, s>>>(d_desc, dg.d_off, dg.dinv, dg.flags,
-                                                                                dg.pflag, kappa_max);
+    lu_diag_inv_kernel<<<dim3(unsigned(h.size()), unsigned(maxnb)), 128, 0, s>>>(d_desc, dg.d_off, dg.d_foff, dg.dinv,
+                                                                                dg.flags, dg.pflag, kappa_max);
     CK_LAUNCH();
   }
   return dg;

@@ -290,13 +290,17 @@ struct LuDiag {
   unsigned char* flags = nullptr;  // per block: [L, U] refine the block solve (lu.cu)
   unsigned char* pflag = nullptr;  // per matrix: any block flagged
   const int64_t* d_off = nullptr;
-  std::vector<int64_t> h_off;
+  std::vector<int64_t> h_off;   // per matrix: offset of its blocks from dinv, in doubles (matrices kept
+                                // with the solve records live in another arena: the offset may be negative)
+  const int64_t* d_foff = nullptr;
+  std::vector<int64_t> h_foff;  // per matrix: index of its first block (flags: 2 per block)
 };
 // tol: the fill tolerance the X solve must support (decides which block solves
 // get a refinement step); <= 0 refines every block.
-// keep: arena for the per-matrix flags when they must outlive the batch workspace (solve records)
+// keep: arena for what must outlive the batch workspace (solve records): the per-matrix flags, and the
+// inverted blocks of the matrices with m >= keep_min_m
 LuDiag launch_lu_diag_inv(const std::vector<MatDesc>& h, const MatDesc* d_desc, Arena& ws, Staging& st,
-                          cudaStream_t s, double tol, Arena* keep = nullptr);
+                          cudaStream_t s, double tol, Arena* keep = nullptr, int keep_min_m = 1 << 30);
 
 // out[p] = dlacn2 estimate of ||S_p^-1||_1 from the LU factors of S_p.
 void launch_lu_inv_norm1(const MatDesc* d_desc, int n, int maxm, const LuDiag& dg, double* out, cudaStream_t s);

@@ -18,7 +18,8 @@ except Exception:
     print(sys.argv[1], 'FAILED'); print(open('gpurun_out/ab.log').read()[-2000:]); sys.exit()
 ph = {k: round(v['ms'], 1) for k, v in d['phases'].items()}
 lv = {k: round(v['compress'], 1) for k, v in d['phase_ms_by_level'].items() if k != '1'}
-print(f"{sys.argv[1]:32s} step {d['value']*1e3:7.1f} ms resid {d['relative_residual']:.4e} {ph} compress/level {lv}", flush=True)
+rc = (d.get('rank_control') or {}).get('value')
+print(f"{sys.argv[1]:32s} step {d['value']*1e3:7.1f} ms rank control {rc} solve {d['solve_roofline']['ms']} resid {d['relative_residual']:.4e} {ph} compress/level {lv}", flush=True)
 PY
 done; done
 cp /tmp/ab_orig.so $LIB
