@@ -20,6 +20,15 @@ is the order the GPU executes (clusters grouped by (gx mod 3, gy mod 3),
 Morton order inside each colour).  Because same-colour clusters are >= 3 cells
 apart, their neighbourhoods are disjoint and the GPU's batched elimination of
 one colour equals this sequential sweep.
+
+Two code paths here are NOT reference behaviour and therefore PARITY UNPINNED
+(the reference has no output to pin them to): `factorize(..., rank_tol=)` /
+`_consolidate` (rank-growth control; the reference never calls its
+`_maybe_consolidate`, ifmm/solver.py:437-492) and `build_tree(...,
+allow_empty=True)` with the full-rank absorption rule of the squeeze functions
+(the reference raises on an empty leaf, ifmm/geometry.py:191-195).  Both are off
+by default, restate the GPU extensions of the same names on the CPU, and are
+checked against dense LU where that is possible (tests/test_oracle_golden.py).
 """
 from __future__ import annotations
 
