@@ -150,6 +150,7 @@ class Arena {
         if (off + bytes <= s.size) {
           s.used = off + bytes;
           in_use_ += bytes;
+          if (zero_) zero_upto(s, s.used);
           return static_cast<char*>(s.ptr) + off;
         }
         ++cur_;
@@ -157,34 +158,32 @@ class Arena {
       }
       size_t sz = bytes > slab_ ? bytes : slab_;
       void* p = slab_get(sz, &sz);
-      cudaError_t e = cudaSuccess;
       if (p == nullptr) {
         char buf[256];
         snprintf(buf, sizeof buf, "device allocation of %.3f GB failed (arena holds %.3f GB)", sz / 1e9,
                  reserved() / 1e9);
         throw Error(IFMM_OOM, buf);
       }
-      if (zero_stream_) {
-        e = cudaMemsetAsync(p, 0, sz, zero_stream_);
-        if (e != cudaSuccess) throw Error(IFMM_CUDA, "cudaMemsetAsync failed on arena slab");
-      }
-      slabs_.push_back({p, sz, 0});
+      // a slab from the cache holds whatever its last user left: all of it may be non-zero
+      slabs_.push_back({p, sz, 0, zero_ ? sz : 0, 0});
       cur_ = slabs_.size() - 1;
     }
   }
-  // When set, new slabs and the used part of recycled slabs are zeroed on `s`,
-  // so every allocation starts as zeros (stream-ordered).
+  // When set, every allocation starts as zeros: cleared on `s` when it is handed out (lazily, see reset()).
   void set_zero_stream(cudaStream_t s) { zero_stream_ = s; zero_ = true; }
   template <class T>
   T* alloc_n(size_t n) {
     return static_cast<T*>(alloc(n * sizeof(T)));
   }
+  // Zeroing is lazy (zero arenas): a reset only notes how far each slab may hold old data; the
+  // allocations of the next round clear what they take, 256 MB ahead at a time, stream-ordered
+  // before any work that can touch the memory.  A level that needs a quarter of what the level
+  // before it used clears a quarter (C3: ~150 GB of memsets per factorization otherwise).
   void reset() {
     for (auto& s : slabs_) {
-      if (zero_ && s.used) {
-        cudaError_t e = cudaMemsetAsync(s.ptr, 0, s.used, zero_stream_);
-        if (e != cudaSuccess) throw Error(IFMM_CUDA, "cudaMemsetAsync failed on arena reset");
-      }
+      const size_t stale = s.zeroed < s.dirty ? s.dirty : 0;  // old data beyond what this round cleared
+      s.dirty = zero_ ? (s.used > stale ? s.used : stale) : 0;
+      s.zeroed = 0;
       s.used = 0;
     }
     cur_ = 0;
@@ -208,7 +207,19 @@ class Arena {
     void* ptr;
     size_t size;
     size_t used;
+    size_t dirty;   // zero arenas: bytes [0, dirty) may hold old data, the rest of the slab is zero
+    size_t zeroed;  // bytes [0, zeroed) have been cleared since the last reset
   };
+  void zero_upto(Slab& s, size_t end) {
+    const size_t need = end < s.dirty ? end : s.dirty;
+    if (s.zeroed >= need) return;
+    constexpr size_t kAhead = size_t(256) << 20;
+    size_t to = s.zeroed + kAhead > need ? s.zeroed + kAhead : need;
+    if (to > s.dirty) to = s.dirty;
+    if (cudaMemsetAsync(static_cast<char*>(s.ptr) + s.zeroed, 0, to - s.zeroed, zero_stream_) != cudaSuccess)
+      throw Error(IFMM_CUDA, "cudaMemsetAsync failed on an arena slab");
+    s.zeroed = to;
+  }
   std::vector<Slab> slabs_;
   size_t cur_ = 0;
   size_t slab_;
