@@ -108,3 +108,32 @@ def test_rank_control_arguments(ifmm):
     b = O.baseline_rhs(N, "normal")
     x = ifmm.solve(f, b)
     assert np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b) <= 1e-5
+
+
+@pytest.mark.slow
+def test_rank_control_at_c3_against_the_oracle(ifmm):
+    """BASELINE C3 itself with rank_tol = 1e-7 against the oracle's run of the same procedure
+    at C3 (tests/golden/c3_1m_rank_control.json: 576 s of one core on the GPU box's host):
+    rank sums per level within 3 %, top dimension within 5 %, residual within 2x (C3's pivots
+    sit near the condition limit, the residual is rounding noise at the 1e-3 level)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    from oracle import ifmm_oracle as O
+    g = json.load(open(os.path.join(GOLDEN, "c3_1m_rank_control.json")))
+    N, depth, p, tol = 1048576, 7, 4, 1e-6
+    pts = O.baseline_points(N, seed=0)
+    b = O.baseline_rhs(N, "normal")
+    tree = ifmm.build_tree(ifmm.PointSet(2, pts), depth)
+    store = ifmm.init_operators(tree, ifmm.baseline_kernel("inv_r", N), p=p, tol=tol)
+    f = ifmm.factorize(store, tree, on_singular="record", rank_tol=1e-7)
+    rs = _rank_sums(f, depth)
+    for k in range(depth, 1, -1):
+        ro = g["rank_sum"][str(k)]
+        assert abs(rs[k] - ro) <= 0.03 * ro, (k, rs[k], ro)
+    assert abs(f.top_dim - g["top_dim"]) <= 0.05 * g["top_dim"]
+    assert abs(f.rank_control[1] - g["rank_control"][1]) <= 0.01 * g["rank_control"][1]
+    x = ifmm.solve(f, b)
+    res = np.linalg.norm(ifmm.fmm_matvec(store, tree, x) - b) / np.linalg.norm(b)
+    assert res <= 2 * g["residual"], (res, g["residual"])
+    assert len(f.singular_pivots) <= g["pivots_over_limit"] + 3
