@@ -856,8 +856,13 @@ void Factorizer::eliminate_batch(std::vector<int>& piv, int colour, std::vector<
   auto lu_class = [&](int m) { return lu_split ? size_class(m) : 0; };
   int class_maxm[3] = {0, 0, 0};
   for (int t = 0; t < np; t++) class_maxm[lu_class(P[t].m)] = std::max(class_maxm[lu_class(P[t].m)], P[t].m);
-  if (lu_split)
+  if (lu_split) {
     std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return lu_class(P[a].m) < lu_class(P[b].m); });
+    // the device fill states follow the order the own pivots are processed in
+    int dev = 0;
+    for (int t : own)
+      for (int f = fill_off[t]; f < fill_off[t + 1]; f++) fh[f].dev = dev++;
+  }
   const int no = int(own.size());
   // per-batch device results of this rank's pivots / fills
   double* d_nS = ws_.alloc_n<double>(std::max(1, no));
