@@ -157,3 +157,22 @@ def test_mixed_size_batches_against_the_oracle_run(ifmm):
     assert res <= 5e-3, res  # the oracle: 3.0e-4; the clipped mixture is ill-conditioned (pivots near 1e12)
     x2 = ifmm.solve(f, b, refine=2)
     assert np.linalg.norm(ifmm.fmm_matvec(store, tree, x2) - b) / np.linalg.norm(b) <= 1e-5
+
+
+def test_mixed_size_batches_sharded(ifmm):
+    """The same 262,144-point system on 2 and 4 virtual ranks: the size-class order of each
+    rank's own pivots and the per-class panel widths come from the whole batch, so the sharded
+    result is bit-identical to one GPU."""
+    from paper_1407_1572_b200 import distributed as D
+    n, depth = 262144, 7
+    X = _mixture(n)
+    b = np.random.default_rng(1).standard_normal(n)
+    tree = ifmm.build_tree(ifmm.PointSet(2, X), depth, allow_empty_leaves=True)
+    store = ifmm.init_operators(tree, ifmm.baseline_kernel("inv_r", n), p=4, tol=1e-6)
+    f = ifmm.factorize(store, tree, rank_tol=1e-7, pivot_condition_limit=np.inf)
+    x = ifmm.solve(f, b)
+    for V in (2, 4):
+        fs = D.factorize_emulated(store, tree, V, rank_tol=1e-7, pivot_condition_limit=np.inf)
+        xs = D.solve_emulated(fs, b)
+        assert np.array_equal(xs[0], x) and np.array_equal(xs[V - 1], x), V
+        del fs
